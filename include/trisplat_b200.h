@@ -1,0 +1,144 @@
+/*
+ * trisplat_b200.h -- C ABI of the B200-native triangle-splat rasterizer.
+ *
+ * Drop-in boundary for the reference package's Python operator API (the
+ * reference has no FFI; these entry points are what its Python surface
+ * binds):
+ *
+ *   ts_forward    replaces render()                     render.py:364-432
+ *                 (project_scene render.py:253-312, build_tile_lists
+ *                  render.py:349-361, rasterize_forward _kernels.py:59-132,
+ *                  stats reduction render.py:411-418)
+ *   ts_backward   replaces render_backward()            backward.py:93-211
+ *                 (rasterize_backward _kernels.py:181-318, _phis_q_grad
+ *                  backward.py:59-90, chain backward.py:158-210)
+ *   ts_debug_copy exposes project_scene / build_tile_lists internals for
+ *                 parity dumps (render.py:134-156, 349-361)
+ *
+ * Conventions: plain pointers and sizes, no framework types.  All array
+ * arguments are DEVICE pointers (CUDA), outputs are caller-allocated, every
+ * call is ordered on the given stream.  Functions return 0 on success or a
+ * negative TS_ERR_* code; ts_error_string() names it.  A context owns its
+ * scratch memory and the state of its last forward pass; it is safe to use
+ * one context per host thread / stream.  Input validation mirrors the
+ * reference: non-finite parameters are reported per group (vertices,
+ * opacity, sigma, sh) as the first offending triangle index
+ * (soup.py:67-77) through ts_forward_result.err_index.
+ */
+#ifndef TRISPLAT_B200_H
+#define TRISPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_OK 0
+#define TS_ERR_INVALID_ARG -1
+#define TS_ERR_CUDA -2
+#define TS_ERR_OOM -3
+#define TS_ERR_NO_FORWARD -4
+#define TS_ERR_NONFINITE -5
+#define TS_ERR_TILE_SIZE -6
+#define TS_ERR_FRAGMENTS -7
+
+/* geometry.py:32-74: intrinsics + world->camera pose x_cam = R x + t */
+typedef struct ts_camera {
+    double fx, fy, cx, cy, z_near;
+    double R[9]; /* row-major */
+    double t[3];
+    int32_t width, height;
+} ts_camera;
+
+typedef struct ts_options {
+    int32_t mode;       /* 0 = NORMALIZED, 1 = SIGMOID (geometry.py:25-29) */
+    int32_t sh_degree;  /* active SH degree 0..3 (render.py:300) */
+    int32_t tile_size;  /* must be 16 */
+    int32_t solid;      /* soup.solid: opacity treated as 1 (render.py:262) */
+    double tau_cutoff;  /* bbox cutoff, default 1/255 (geometry.py:22) */
+    double tau_contrib; /* pixel-count floor, default 1/255 (render.py:27) */
+    double background[3];
+    int32_t precision;   /* 0 = fast fp32 path with fp64 guard-band fix-up, 1 = exact fp64 */
+    int32_t param_dtype; /* 0 = float32 parameters, 1 = float64 parameters */
+    int32_t validate;    /* 1 = non-finite check (soup.py:67-77), 0 = skip */
+    int32_t reserved;
+} ts_options;
+
+/* Triangle soup parameters (soup.py:17-30), device pointers, SoA blocks:
+ * vertices (N,3,3), opacity (N), sigma (N), sh (N,16,3) band-major. */
+typedef struct ts_soup {
+    const void* vertices;
+    const void* opacity;
+    const void* sigma;
+    const void* sh;
+    int64_t n;
+} ts_soup;
+
+/* RenderOutput (render.py:84-91).  Any pointer may be NULL to skip it. */
+typedef struct ts_forward_out {
+    float* image;        /* (H,W,3) clipped to [0,1] */
+    float* alpha_map;    /* (H,W) */
+    float* max_weight;   /* (N) per_triangle_max_weight */
+    int32_t* pixel_count;/* (N) per_triangle_pixel_count */
+    float* area;         /* (N) per_triangle_area (0 if culled) */
+    int32_t* last_src;   /* (H,W) source id of the last composited fragment, -1 if none */
+    int32_t* n_frag;     /* (H,W) composited fragments per pixel */
+} ts_forward_out;
+
+/* Host-side summary of a forward pass, filled by ts_forward. */
+typedef struct ts_forward_result {
+    int64_t n_visible;    /* M: accepted triangles */
+    int64_t n_entries;    /* E: tile entries */
+    int64_t n_flagged;    /* pixels re-resolved by the fp64 guard-band fix-up */
+    int64_t err_index[4]; /* first non-finite triangle per group, -1 if none */
+} ts_forward_result;
+
+/* GradientSet (backward.py:24-56), device pointers, float32. */
+typedef struct ts_grads {
+    float* d_vertices; /* (N,3,3) */
+    float* d_opacity;  /* (N) */
+    float* d_sigma;    /* (N) */
+    float* d_sh;       /* (N,16,3) */
+} ts_grads;
+
+typedef struct ts_context ts_context;
+
+int ts_context_create(ts_context** out, int device);
+int ts_context_destroy(ts_context* ctx);
+const char* ts_error_string(int code);
+const char* ts_version(void);
+
+/* render(): project, cull, depth-sort, bin, composite.  Synchronizes the
+ * stream once (after projection) to size the tile-entry buffers. */
+int ts_forward(ts_context* ctx, const ts_camera* cam, const ts_options* opt, const ts_soup* soup,
+               const ts_forward_out* out, ts_forward_result* result, void* stream);
+
+/* render_backward(): gradients of sum(d_image * image_unclipped) w.r.t. all
+ * 59 parameters of every triangle, for the scene of the context's last
+ * ts_forward (same soup/camera/options).  d_image is (H,W,3) float32.
+ * accumulate=1 adds into the gradient buffers, 0 overwrites them. */
+int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, int accumulate,
+                void* stream);
+
+/* Debug/parity dumps of the last forward pass (device destination):
+ *  TS_DUMP_SORTED_IDX  int32[M]       depth-sorted source ids (render.py:275-277)
+ *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)
+ *  TS_DUMP_ENTRY_RANK  int32[E]       tile entries as depth ranks (render.py:358-360)
+ *  TS_DUMP_BBOX        int32[N*4]     x0,x1,y0,y1 per source (0s if culled) (render.py:243-250)
+ *  TS_DUMP_DEPTH       float64[N]     camera-space centroid depth per source */
+#define TS_DUMP_SORTED_IDX 1
+#define TS_DUMP_TILE_START 2
+#define TS_DUMP_ENTRY_RANK 3
+#define TS_DUMP_BBOX 4
+#define TS_DUMP_DEPTH 5
+int ts_debug_copy(ts_context* ctx, int what, void* dst, size_t bytes, void* stream);
+
+/* Kernel launches issued by this context since creation (for launch counting). */
+int64_t ts_launch_count(ts_context* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRISPLAT_B200_H */

@@ -1,0 +1,104 @@
+"""ctypes binding of the C ABI declared in include/trisplat_b200.h.
+
+The shared library is built in-tree (``python -m paper_2505_19175_b200.build``
+or ``__graft_entry__.build()``).  There is no CPU fallback: if the library is
+missing or no CUDA device is present, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtrisplat_b200.so")
+
+TS_OK = 0
+TS_ERR_NONFINITE = -5
+TS_DUMP_SORTED_IDX = 1
+TS_DUMP_TILE_START = 2
+TS_DUMP_ENTRY_RANK = 3
+TS_DUMP_BBOX = 4
+TS_DUMP_DEPTH = 5
+
+
+class TsCamera(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double),
+                ("cy", ctypes.c_double), ("z_near", ctypes.c_double),
+                ("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class TsOptions(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("sh_degree", ctypes.c_int32),
+                ("tile_size", ctypes.c_int32), ("solid", ctypes.c_int32),
+                ("tau_cutoff", ctypes.c_double), ("tau_contrib", ctypes.c_double),
+                ("background", ctypes.c_double * 3), ("precision", ctypes.c_int32),
+                ("param_dtype", ctypes.c_int32), ("validate", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class TsSoup(ctypes.Structure):
+    _fields_ = [("vertices", ctypes.c_void_p), ("opacity", ctypes.c_void_p),
+                ("sigma", ctypes.c_void_p), ("sh", ctypes.c_void_p), ("n", ctypes.c_int64)]
+
+
+class TsForwardOut(ctypes.Structure):
+    _fields_ = [("image", ctypes.c_void_p), ("alpha_map", ctypes.c_void_p),
+                ("max_weight", ctypes.c_void_p), ("pixel_count", ctypes.c_void_p),
+                ("area", ctypes.c_void_p), ("last_src", ctypes.c_void_p),
+                ("n_frag", ctypes.c_void_p)]
+
+
+class TsForwardResult(ctypes.Structure):
+    _fields_ = [("n_visible", ctypes.c_int64), ("n_entries", ctypes.c_int64),
+                ("n_flagged", ctypes.c_int64), ("err_index", ctypes.c_int64 * 4)]
+
+
+class TsGrads(ctypes.Structure):
+    _fields_ = [("d_vertices", ctypes.c_void_p), ("d_opacity", ctypes.c_void_p),
+                ("d_sigma", ctypes.c_void_p), ("d_sh", ctypes.c_void_p)]
+
+
+EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_version",
+           "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count"]
+
+_LIB = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the library and declare every exported signature."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is not built; run __graft_entry__.build() "
+                           "(python -m paper_2505_19175_b200.build)")
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    lib.ts_context_create.argtypes = [P(ctypes.c_void_p), ctypes.c_int]
+    lib.ts_context_create.restype = ctypes.c_int
+    lib.ts_context_destroy.argtypes = [ctypes.c_void_p]
+    lib.ts_context_destroy.restype = ctypes.c_int
+    lib.ts_error_string.argtypes = [ctypes.c_int]
+    lib.ts_error_string.restype = ctypes.c_char_p
+    lib.ts_version.argtypes = []
+    lib.ts_version.restype = ctypes.c_char_p
+    lib.ts_forward.argtypes = [ctypes.c_void_p, P(TsCamera), P(TsOptions), P(TsSoup),
+                               P(TsForwardOut), P(TsForwardResult), ctypes.c_void_p]
+    lib.ts_forward.restype = ctypes.c_int
+    lib.ts_backward.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(TsGrads), ctypes.c_int,
+                                ctypes.c_void_p]
+    lib.ts_backward.restype = ctypes.c_int
+    lib.ts_debug_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                  ctypes.c_size_t, ctypes.c_void_p]
+    lib.ts_debug_copy.restype = ctypes.c_int
+    lib.ts_launch_count.argtypes = [ctypes.c_void_p]
+    lib.ts_launch_count.restype = ctypes.c_int64
+    _LIB = lib
+    return lib
+
+
+def check(rc: int, what: str = ""):
+    if rc != TS_OK:
+        msg = load().ts_error_string(rc).decode()
+        raise RuntimeError(f"trisplat_b200 {what} failed: {msg} ({rc})")

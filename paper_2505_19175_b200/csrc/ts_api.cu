@@ -1,0 +1,359 @@
+// ts_api.cu -- C ABI (include/trisplat_b200.h): context, scratch management
+// and the per-view pipeline.
+//
+//   ts_forward  = render()          render.py:364-432
+//   ts_backward = render_backward() backward.py:93-211
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "ts_kernels.cuh"
+
+namespace ts {
+std::atomic<long long> g_launches{0};
+}
+
+using namespace ts;
+
+struct ts_context {
+    int device = 0;
+    // per-triangle scratch
+    long long cap_n = -1;
+    void* tri_buf = nullptr;
+    Rec64* rec = nullptr;
+    unsigned long long* key = nullptr;
+    unsigned* tcount = nullptr;
+    unsigned* flag = nullptr;
+    unsigned long long* keys_c = nullptr;
+    unsigned* vals_c = nullptr;
+    unsigned long long* keys_alt = nullptr;
+    unsigned* vals_alt = nullptr;
+    unsigned* offs = nullptr;
+    int* rank_of = nullptr;
+    double* depth = nullptr;
+    // backward scratch (lazy)
+    long long cap_sg = -1;
+    double* sgrad = nullptr;
+    // per-entry scratch
+    long long cap_e = -1;
+    void* ent_buf = nullptr;
+    unsigned *tkey = nullptr, *tval = nullptr, *tkey_alt = nullptr, *tval_alt = nullptr;
+    // per-pixel scratch
+    long long cap_p = -1, cap_tiles = -1;
+    void* pix_buf = nullptr;
+    double* t_final = nullptr;
+    int* last_pos = nullptr;
+    int* tile_start = nullptr;
+    // sort scratch
+    void* sort_buf = nullptr;
+    SortScratch sort{};
+    // counters
+    Counters* d_ctr = nullptr;
+    Counters* h_ctr = nullptr;
+    // last forward
+    bool have_fwd = false;
+    Cam cam{};
+    Opts opt{};
+    ts_soup soup{};
+    int dtype = 0;
+    long long n = 0, m = 0, e = 0;
+    const unsigned* sorted_src = nullptr;
+    const unsigned* ent_src = nullptr;
+};
+
+static int cuda_err(cudaError_t e) {
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[trisplat_b200] CUDA error: %s\n", cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? TS_ERR_OOM : TS_ERR_CUDA;
+    }
+    return TS_OK;
+}
+#define TS_CHECK(x)                     \
+    do {                                \
+        int _rc = cuda_err((x));        \
+        if (_rc != TS_OK) return _rc;   \
+    } while (0)
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static int ensure_tri(ts_context* c, long long n) {
+    if (n <= c->cap_n) return TS_OK;
+    long long cap = n + n / 4 + 1024;
+    if (c->tri_buf) cudaFree(c->tri_buf);
+    c->tri_buf = nullptr;
+    size_t off = 0, sz;
+    size_t o_rec = off; sz = sizeof(Rec64) * cap; off = align_up(off + sz, 256);
+    size_t o_key = off; sz = 8 * cap; off = align_up(off + sz, 256);
+    size_t o_tc = off; sz = 4 * cap; off = align_up(off + sz, 256);
+    size_t o_fl = off; sz = 4 * cap; off = align_up(off + sz, 256);
+    size_t o_kc = off; sz = 8 * cap; off = align_up(off + sz, 256);
+    size_t o_vc = off; sz = 4 * cap; off = align_up(off + sz, 256);
+    size_t o_ka = off; sz = 8 * cap; off = align_up(off + sz, 256);
+    size_t o_va = off; sz = 4 * cap; off = align_up(off + sz, 256);
+    size_t o_of = off; sz = 4 * (cap + 1); off = align_up(off + sz, 256);
+    size_t o_rk = off; sz = 4 * cap; off = align_up(off + sz, 256);
+    size_t o_dp = off; sz = 8 * cap; off = align_up(off + sz, 256);
+    TS_CHECK(cudaMalloc(&c->tri_buf, off));
+    char* b = (char*)c->tri_buf;
+    c->rec = (Rec64*)(b + o_rec);
+    c->key = (unsigned long long*)(b + o_key);
+    c->tcount = (unsigned*)(b + o_tc);
+    c->flag = (unsigned*)(b + o_fl);
+    c->keys_c = (unsigned long long*)(b + o_kc);
+    c->vals_c = (unsigned*)(b + o_vc);
+    c->keys_alt = (unsigned long long*)(b + o_ka);
+    c->vals_alt = (unsigned*)(b + o_va);
+    c->offs = (unsigned*)(b + o_of);
+    c->rank_of = (int*)(b + o_rk);
+    c->depth = (double*)(b + o_dp);
+    c->cap_n = cap;
+    return TS_OK;
+}
+
+static int ensure_ent(ts_context* c, long long e) {
+    if (e <= c->cap_e) return TS_OK;
+    long long cap = e + e / 4 + 4096;
+    if (c->ent_buf) cudaFree(c->ent_buf);
+    c->ent_buf = nullptr;
+    size_t one = align_up(4 * cap, 256);
+    TS_CHECK(cudaMalloc(&c->ent_buf, 4 * one));
+    char* b = (char*)c->ent_buf;
+    c->tkey = (unsigned*)b;
+    c->tval = (unsigned*)(b + one);
+    c->tkey_alt = (unsigned*)(b + 2 * one);
+    c->tval_alt = (unsigned*)(b + 3 * one);
+    c->cap_e = cap;
+    return TS_OK;
+}
+
+static int ensure_pix(ts_context* c, long long p, long long ntiles) {
+    if (p <= c->cap_p && ntiles <= c->cap_tiles) return TS_OK;
+    if (c->pix_buf) cudaFree(c->pix_buf);
+    c->pix_buf = nullptr;
+    long long cp = p > c->cap_p ? p : c->cap_p;
+    long long ct = ntiles > c->cap_tiles ? ntiles : c->cap_tiles;
+    size_t o_tf = 0, o_lp = align_up(8 * cp, 256), o_ts = o_lp + align_up(4 * cp, 256);
+    size_t tot = o_ts + align_up(4 * (ct + 1), 256);
+    TS_CHECK(cudaMalloc(&c->pix_buf, tot));
+    char* b = (char*)c->pix_buf;
+    c->t_final = (double*)(b + o_tf);
+    c->last_pos = (int*)(b + o_lp);
+    c->tile_start = (int*)(b + o_ts);
+    c->cap_p = cp;
+    c->cap_tiles = ct;
+    return TS_OK;
+}
+
+static int ensure_sg(ts_context* c, long long n) {
+    if (n <= c->cap_sg) return TS_OK;
+    long long cap = n + n / 4 + 1024;
+    if (c->sgrad) cudaFree(c->sgrad);
+    c->sgrad = nullptr;
+    TS_CHECK(cudaMalloc(&c->sgrad, sizeof(double) * SG_STRIDE * cap));
+    c->cap_sg = cap;
+    return TS_OK;
+}
+
+static void build_cam_opts(const ts_camera* cam, const ts_options* opt, Cam& c, Opts& o) {
+    c.fx = cam->fx; c.fy = cam->fy; c.cx = cam->cx; c.cy = cam->cy; c.z_near = cam->z_near;
+    for (int k = 0; k < 9; k++) c.R[k] = cam->R[k];
+    for (int k = 0; k < 3; k++) c.t[k] = cam->t[k];
+    for (int b = 0; b < 3; b++)
+        c.cc[b] = -(cam->R[0 * 3 + b] * cam->t[0] + cam->R[1 * 3 + b] * cam->t[1] + cam->R[2 * 3 + b] * cam->t[2]);
+    c.width = cam->width; c.height = cam->height;
+    c.ntx = (cam->width + TILE - 1) / TILE;
+    c.nty = (cam->height + TILE - 1) / TILE;
+    o.mode = opt->mode;
+    o.sh_degree = opt->sh_degree;
+    o.ncoef = (opt->sh_degree + 1) * (opt->sh_degree + 1);
+    o.solid = opt->solid;
+    o.validate = opt->validate;
+    o.tau_cutoff = opt->tau_cutoff;
+    o.tau_contrib = opt->tau_contrib;
+    for (int k = 0; k < 3; k++) o.bg[k] = opt->background[k];
+}
+
+static int bit_length(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+extern "C" {
+
+const char* ts_version(void) { return "trisplat_b200 0.1.0 (sm_100a)"; }
+
+const char* ts_error_string(int code) {
+    switch (code) {
+        case TS_OK: return "ok";
+        case TS_ERR_INVALID_ARG: return "invalid argument";
+        case TS_ERR_CUDA: return "CUDA error";
+        case TS_ERR_OOM: return "out of device memory";
+        case TS_ERR_NO_FORWARD: return "ts_backward called without a preceding ts_forward";
+        case TS_ERR_NONFINITE: return "non-finite triangle parameters";
+        case TS_ERR_TILE_SIZE: return "only tile_size=16 is supported";
+        case TS_ERR_FRAGMENTS: return "fragment gradients do not match this scene/camera";
+        default: return "unknown error";
+    }
+}
+
+int ts_context_create(ts_context** out, int device) {
+    if (!out) return TS_ERR_INVALID_ARG;
+    TS_CHECK(cudaSetDevice(device));
+    ts_context* c = new ts_context();
+    c->device = device;
+    c->sort.max_blocks = 1184;  // 8 x 148 SMs
+    size_t sb = sort_scratch_bytes(c->sort.max_blocks);
+    int rc = cuda_err(cudaMalloc(&c->sort_buf, sb + 1024));
+    if (rc) { delete c; return rc; }
+    c->sort.hist = (unsigned*)c->sort_buf;
+    c->sort.bsums = c->sort.hist + 256 * (size_t)c->sort.max_blocks + 32;
+    rc = cuda_err(cudaMalloc(&c->d_ctr, sizeof(Counters)));
+    if (!rc) rc = cuda_err(cudaMallocHost(&c->h_ctr, sizeof(Counters)));
+    if (rc) { delete c; return rc; }
+    *out = c;
+    return TS_OK;
+}
+
+int ts_context_destroy(ts_context* c) {
+    if (!c) return TS_OK;
+    cudaFree(c->tri_buf);
+    cudaFree(c->ent_buf);
+    cudaFree(c->pix_buf);
+    cudaFree(c->sgrad);
+    cudaFree(c->sort_buf);
+    cudaFree(c->d_ctr);
+    cudaFreeHost(c->h_ctr);
+    delete c;
+    return TS_OK;
+}
+
+int64_t ts_launch_count(ts_context*) { return g_launches.load(); }
+
+int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const ts_soup* soup,
+               const ts_forward_out* out, ts_forward_result* res, void* stream) {
+    if (!c || !cam || !opt || !soup || !out) return TS_ERR_INVALID_ARG;
+    if (opt->tile_size != TILE) return TS_ERR_TILE_SIZE;
+    if (cam->width < 1 || cam->height < 1 || soup->n < 0 || opt->sh_degree < 0 || opt->sh_degree > 3)
+        return TS_ERR_INVALID_ARG;
+    if (soup->n >= (1ll << 31)) return TS_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    c->have_fwd = false;
+    Cam cm;
+    Opts op;
+    build_cam_opts(cam, opt, cm, op);
+    const long long n = soup->n;
+    const long long P = (long long)cam->width * cam->height;
+    const int ntiles = cm.ntx * cm.nty;
+    int rc = ensure_tri(c, n > 0 ? n : 1);
+    if (rc) return rc;
+    if ((rc = ensure_pix(c, P, ntiles))) return rc;
+    // counters
+    Counters init;
+    memset(&init, 0, sizeof(init));
+    init.key_and = ~0ull;
+    for (int k = 0; k < 4; k++) init.err[k] = 0x7fffffffffffffffLL;
+    *c->h_ctr = init;
+    TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_ctr, sizeof(Counters), cudaMemcpyHostToDevice, st));
+    if (out->max_weight) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
+    if (out->pixel_count) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
+    PreOut po{c->rec, c->key, c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+    launch_preprocess(cm, op, *soup, opt->param_dtype, po, st);
+    g_launches += 1;
+    TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    TS_CHECK(cudaStreamSynchronize(st));
+    TS_CHECK(cudaGetLastError());
+    const Counters h = *c->h_ctr;
+    if (res) {
+        res->n_visible = (int64_t)h.m;
+        res->n_entries = (int64_t)h.e;
+        res->n_flagged = 0;
+        for (int k = 0; k < 4; k++) res->err_index[k] = h.err[k] == 0x7fffffffffffffffLL ? -1 : h.err[k];
+    }
+    if (opt->validate)
+        for (int k = 0; k < 4; k++)
+            if (h.err[k] != 0x7fffffffffffffffLL) return TS_ERR_NONFINITE;
+    const long long m = (long long)h.m, e = (long long)h.e;
+    if (e >= (1ll << 31)) return TS_ERR_INVALID_ARG;
+    if ((rc = ensure_ent(c, e > 0 ? e : 1))) return rc;
+    // depth order: compaction (source order) + stable radix sort on fp64 bits
+    compact_accepted(n, c->flag, c->key, c->keys_c, c->vals_c, c->sort, st);
+    g_launches += 3;
+    unsigned long long diff = h.key_and ^ h.key_or;
+    int lo = diff ? __builtin_ctzll(diff) : 0, hi = bit_length(diff);
+    lo = lo / 8 * 8;
+    int par = radix_sort_u64(m, c->keys_c, c->vals_c, c->keys_alt, c->vals_alt, lo, hi, c->sort, st);
+    if (m > 1 && hi > lo) g_launches += 3 * ((hi - lo + 7) / 8);
+    c->sorted_src = par ? c->vals_alt : c->vals_c;
+    // tile duplication in rank order + stable sort by tile id
+    rank_offsets(m, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
+    duplicate_entries(m, c->sorted_src, c->rec, c->offs, cm.ntx, c->tkey, c->tval, st);
+    g_launches += 4;
+    int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
+    par = radix_sort_u32(e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, 0, tbits, c->sort, st);
+    if (e > 1 && tbits > 0) g_launches += 3 * ((tbits + 7) / 8);
+    const unsigned* skey = par ? c->tkey_alt : c->tkey;
+    c->ent_src = par ? c->tval_alt : c->tval;
+    tile_ranges(e, skey, ntiles, c->tile_start, st);
+    g_launches += 1;
+    BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
+                out->n_frag, c->t_final, c->last_pos};
+    launch_blend_exact(cm, op, c->rec, c->tile_start, (const int*)c->ent_src, bo, st);
+    g_launches += 1;
+    TS_CHECK(cudaGetLastError());
+    c->have_fwd = true;
+    c->cam = cm;
+    c->opt = op;
+    c->soup = *soup;
+    c->dtype = opt->param_dtype;
+    c->n = n;
+    c->m = m;
+    c->e = e;
+    return TS_OK;
+}
+
+int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
+                void* stream) {
+    if (!c || !d_image || !grads) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = ensure_sg(c, c->n > 0 ? c->n : 1);
+    if (rc) return rc;
+    if (c->n > 0) TS_CHECK(cudaMemsetAsync(c->sgrad, 0, sizeof(double) * SG_STRIDE * c->n, st));
+    launch_blend_bwd_exact(c->cam, c->opt, c->rec, c->tile_start, (const int*)c->ent_src, c->t_final,
+                           c->last_pos, d_image, c->sgrad, st);
+    launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, c->sgrad, *grads, accumulate, st);
+    g_launches += 2;
+    TS_CHECK(cudaGetLastError());
+    return TS_OK;
+}
+
+int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream) {
+    if (!c || !dst) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    cudaStream_t st = (cudaStream_t)stream;
+    int ntiles = c->cam.ntx * c->cam.nty;
+    switch (what) {
+        case TS_DUMP_SORTED_IDX:
+            if (bytes < 4 * (size_t)c->m) return TS_ERR_INVALID_ARG;
+            if (c->m) TS_CHECK(cudaMemcpyAsync(dst, c->sorted_src, 4 * c->m, cudaMemcpyDeviceToDevice, st));
+            return TS_OK;
+        case TS_DUMP_TILE_START:
+            if (bytes < 4 * (size_t)(ntiles + 1)) return TS_ERR_INVALID_ARG;
+            TS_CHECK(cudaMemcpyAsync(dst, c->tile_start, 4 * (ntiles + 1), cudaMemcpyDeviceToDevice, st));
+            return TS_OK;
+        case TS_DUMP_ENTRY_RANK:
+            if (bytes < 4 * (size_t)c->e) return TS_ERR_INVALID_ARG;
+            entries_to_rank(c->e, c->ent_src, c->rank_of, (int*)dst, st);
+            return cuda_err(cudaGetLastError());
+        case TS_DUMP_BBOX:
+            if (bytes < 16 * (size_t)c->n) return TS_ERR_INVALID_ARG;
+            bbox_dump(c->n, c->rec, c->flag, (int*)dst, st);
+            return cuda_err(cudaGetLastError());
+        case TS_DUMP_DEPTH:
+            if (bytes < 8 * (size_t)c->n) return TS_ERR_INVALID_ARG;
+            if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->depth, 8 * c->n, cudaMemcpyDeviceToDevice, st));
+            return TS_OK;
+        default:
+            return TS_ERR_INVALID_ARG;
+    }
+}
+
+}  // extern "C"

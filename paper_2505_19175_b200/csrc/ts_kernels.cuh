@@ -1,0 +1,84 @@
+// ts_kernels.cuh -- kernel launch interfaces shared by the translation units.
+#pragma once
+#include "ts_common.cuh"
+
+namespace ts {
+
+struct Counters {
+    unsigned long long m;        // accepted triangles
+    unsigned long long e;        // tile entries
+    unsigned long long key_and;  // AND / OR of accepted depth keys (pass selection)
+    unsigned long long key_or;
+    long long err[4];            // first non-finite index per group
+    unsigned long long n_flagged;
+    unsigned long long pad[7];
+};
+
+struct PreOut {
+    Rec64* rec;                // (N) fp64 records (accepted only)
+    unsigned long long* key;   // (N) depth bits
+    unsigned* tcount;          // (N) tiles touched
+    unsigned* flag;            // (N) accepted
+    float* area;               // (N) per_triangle_area, nullable
+    double* depth;             // (N) centroid depth, nullable
+    Counters* ctr;
+};
+
+struct BlendOut {
+    float* image;
+    float* alpha_map;
+    float* max_weight;
+    int* pixel_count;
+    int* last_src;
+    int* n_frag;
+    double* t_final;
+    int* last_pos;
+};
+
+// ts_exact.cu
+void launch_preprocess(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                       const PreOut& out, cudaStream_t st);
+void launch_blend_exact(const Cam& cam, const Opts& opt, const Rec64* rec, const int* tile_start,
+                        const int* ent_src, const BlendOut& out, cudaStream_t st);
+void launch_blend_bwd_exact(const Cam& cam, const Opts& opt, const Rec64* rec, const int* tile_start,
+                            const int* ent_src, const double* t_final, const int* last_pos,
+                            const float* d_image, double* sgrad, cudaStream_t st);
+void launch_chain_bwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                      const unsigned* flag, const double* sgrad, const ts_grads& g, int accumulate,
+                      cudaStream_t st);
+
+// ts_sort.cu
+struct SortScratch {
+    unsigned* hist;     // RADIX * max_blocks
+    unsigned* bsums;    // max_blocks + 1
+    int max_blocks;
+};
+size_t sort_scratch_bytes(int max_blocks);
+int sort_grid(long long count, int max_blocks);
+
+// compaction of accepted triangles: keys_c[pos] = key[i], vals_c[pos] = i
+void compact_accepted(long long n, const unsigned* flag, const unsigned long long* key,
+                      unsigned long long* keys_c, unsigned* vals_c, const SortScratch& s,
+                      cudaStream_t st);
+// stable LSD radix sort of (key, value) pairs over bits [bit_lo, bit_hi).
+// Returns 0 if the result is in (keys, vals), 1 if in (keys_alt, vals_alt).
+int radix_sort_u64(long long count, unsigned long long* keys, unsigned* vals,
+                   unsigned long long* keys_alt, unsigned* vals_alt, int bit_lo, int bit_hi,
+                   const SortScratch& s, cudaStream_t st);
+int radix_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
+                   unsigned* vals_alt, int bit_lo, int bit_hi, const SortScratch& s,
+                   cudaStream_t st);
+// offs[m] = exclusive scan over m of tcount[sorted_src[m]]; rank_of[sorted_src[m]] = m
+void rank_offsets(long long m, const unsigned* sorted_src, const unsigned* tcount, unsigned* offs,
+                  int* rank_of, const SortScratch& s, cudaStream_t st);
+// tile duplication in depth-rank order: tkey = tile id, tval = source id
+void duplicate_entries(long long m, const unsigned* sorted_src, const Rec64* rec, const unsigned* offs,
+                       int ntx, unsigned* tkey, unsigned* tval, cudaStream_t st);
+// tile_start[t] = first entry of tile t (CSR), tile_start[ntiles] = E
+void tile_ranges(long long e, const unsigned* tkey, int ntiles, int* tile_start, cudaStream_t st);
+// entry_rank[pos] = rank_of[ent_src[pos]]
+void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out,
+                     cudaStream_t st);
+void bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out, cudaStream_t st);
+
+}  // namespace ts

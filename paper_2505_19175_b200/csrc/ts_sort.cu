@@ -1,0 +1,336 @@
+// ts_sort.cu -- device-wide scans, compaction, stable LSD radix sort, tile
+// duplication and tile ranges.
+//
+// Replaces the host side of the reference's binning (render.py:271-283 cull +
+// np.lexsort((idx, z)) and render.py:315-361 _tile_counts/_tile_fill): the
+// accepted triangles are compacted in source order, stably radix-sorted on the
+// fp64 depth bits (a stable sort of idx-ordered items reproduces the index
+// tie-break of np.lexsort), duplicated per touched tile in depth-rank order and
+// stably sorted by tile id, which yields exactly the reference CSR order.
+#include "ts_kernels.cuh"
+
+namespace ts {
+
+constexpr int SB = 256;  // threads per block for scan / sort kernels
+constexpr int RADIX = 256;
+
+size_t sort_scratch_bytes(int max_blocks) {
+    return sizeof(unsigned) * ((size_t)RADIX * max_blocks + max_blocks + 1 + 64);
+}
+
+int sort_grid(long long count, int max_blocks) {
+    long long g = (count + SB * 8 - 1) / (SB * 8);  // >= 8 rounds of 256 per block
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+
+static inline long long chunk_of(long long count, int g) {
+    long long c = (count + g - 1) / g;
+    return (c + SB - 1) / SB * SB;
+}
+
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned& total) {
+    __shared__ unsigned s_warp[SB / 32];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= (unsigned)off) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = lane < SB / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int off = 1; off < SB / 32; off <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= (unsigned)off) w += y;
+        }
+        if (lane < SB / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    unsigned pre = warp ? s_warp[warp - 1] : 0u;
+    total = s_warp[SB / 32 - 1];
+    __syncthreads();
+    return pre + x - v;
+}
+
+// ---------------- generic reduce-then-scan over a functor ----------------
+template <class F>
+__global__ void __launch_bounds__(SB) k_scan_reduce(long long n, long long chunk, F f, unsigned* bsums) {
+    long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
+    unsigned acc = 0;
+    for (long long i = lo + threadIdx.x; i < hi; i += SB) acc += f.load(i);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    __shared__ unsigned s[SB / 32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int w = 0; w < SB / 32; w++) t += s[w];
+        bsums[blockIdx.x] = t;
+    }
+}
+
+// single-block exclusive scan of a[0..len) in place; a[len] = total
+__global__ void __launch_bounds__(1024) k_scan_single(unsigned* a, long long len) {
+    __shared__ unsigned s_warp[32];
+    long long per = (len + 1023) / 1024;
+    long long lo = threadIdx.x * per, hi = min(len, lo + per);
+    unsigned acc = 0;
+    for (long long i = lo; i < hi; i++) acc += a[i];
+    // block exclusive scan of acc (1024 threads)
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = acc;
+    for (int off = 1; off < 32; off <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= (unsigned)off) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = s_warp[lane];
+        for (int off = 1; off < 32; off <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= (unsigned)off) w += y;
+        }
+        s_warp[lane] = w;
+    }
+    __syncthreads();
+    unsigned run = (warp ? s_warp[warp - 1] : 0u) + x - acc;
+    for (long long i = lo; i < hi; i++) {
+        unsigned v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 1023) a[len] = s_warp[31];
+}
+
+template <class F>
+__global__ void __launch_bounds__(SB) k_scan_apply(long long n, long long chunk, F f, const unsigned* bsums) {
+    long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
+    unsigned run = bsums[blockIdx.x];
+    for (long long base = lo; base < hi; base += SB) {
+        long long i = base + threadIdx.x;
+        unsigned v = i < hi ? f.load(i) : 0u;
+        unsigned tot;
+        unsigned ex = block_excl_scan(v, tot);
+        if (i < hi) f.store(i, run + ex, v);
+        run += tot;
+    }
+}
+
+template <class F>
+static void scan_functor(long long n, F f, const SortScratch& s, cudaStream_t st) {
+    if (n <= 0) return;
+    int g = sort_grid(n, s.max_blocks);
+    long long chunk = chunk_of(n, g);
+    g = (int)((n + chunk - 1) / chunk);
+    k_scan_reduce<<<g, SB, 0, st>>>(n, chunk, f, s.bsums);
+    k_scan_single<<<1, 1024, 0, st>>>(s.bsums, g);
+    k_scan_apply<<<g, SB, 0, st>>>(n, chunk, f, s.bsums);
+}
+
+struct CompactF {
+    const unsigned* flag;
+    const unsigned long long* key;
+    unsigned long long* keys_c;
+    unsigned* vals_c;
+    __device__ unsigned load(long long i) const { return flag[i]; }
+    __device__ void store(long long i, unsigned ex, unsigned v) const {
+        if (v) {
+            keys_c[ex] = key[i];
+            vals_c[ex] = (unsigned)i;
+        }
+    }
+};
+
+void compact_accepted(long long n, const unsigned* flag, const unsigned long long* key,
+                      unsigned long long* keys_c, unsigned* vals_c, const SortScratch& s,
+                      cudaStream_t st) {
+    scan_functor(n, CompactF{flag, key, keys_c, vals_c}, s, st);
+}
+
+struct RankF {
+    const unsigned* sorted_src;
+    const unsigned* tcount;
+    unsigned* offs;
+    int* rank_of;
+    __device__ unsigned load(long long m) const { return tcount[sorted_src[m]]; }
+    __device__ void store(long long m, unsigned ex, unsigned) const {
+        offs[m] = ex;
+        rank_of[sorted_src[m]] = (int)m;
+    }
+};
+
+void rank_offsets(long long m, const unsigned* sorted_src, const unsigned* tcount, unsigned* offs,
+                  int* rank_of, const SortScratch& s, cudaStream_t st) {
+    scan_functor(m, RankF{sorted_src, tcount, offs, rank_of}, s, st);
+}
+
+// ---------------- stable LSD radix sort ----------------
+template <typename K>
+__global__ void __launch_bounds__(SB) k_radix_hist(long long count, long long chunk, const K* __restrict__ keys,
+                                                   int shift, unsigned mask, unsigned* hist, int g) {
+    __shared__ unsigned s_h[RADIX];
+    s_h[threadIdx.x] = 0;
+    __syncthreads();
+    long long lo = (long long)blockIdx.x * chunk, hi = min(count, lo + chunk);
+    for (long long i = lo + threadIdx.x; i < hi; i += SB) {
+        unsigned d = (unsigned)(keys[i] >> shift) & mask;
+        atomicAdd(&s_h[d], 1u);
+    }
+    __syncthreads();
+    hist[(size_t)threadIdx.x * g + blockIdx.x] = s_h[threadIdx.x];
+}
+
+template <typename K>
+__global__ void __launch_bounds__(SB) k_radix_scatter(long long count, long long chunk,
+                                                      const K* __restrict__ kin, const unsigned* __restrict__ vin,
+                                                      K* __restrict__ kout, unsigned* __restrict__ vout,
+                                                      int shift, unsigned mask, const unsigned* hist, int g) {
+    __shared__ unsigned s_base[RADIX];
+    __shared__ unsigned s_wcnt[SB / 32][RADIX];
+    const unsigned warp = threadIdx.x >> 5;
+    s_base[threadIdx.x] = hist[(size_t)threadIdx.x * g + blockIdx.x];
+    long long lo = (long long)blockIdx.x * chunk, hi = min(count, lo + chunk);
+    const unsigned lt = lanemask_lt();
+    for (long long base = lo; base < hi; base += SB) {
+        long long i = base + threadIdx.x;
+        bool valid = i < hi;
+        K k = valid ? kin[i] : (K)0;
+        unsigned v = valid ? vin[i] : 0u;
+        unsigned d = valid ? ((unsigned)(k >> shift) & mask) : RADIX;
+#pragma unroll
+        for (int w = 0; w < SB / 32; w++) s_wcnt[w][threadIdx.x] = 0;
+        __syncthreads();
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned rank = __popc(peers & lt);
+        if (valid && rank == 0) s_wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            unsigned pre = s_base[d] + rank;
+            for (unsigned w = 0; w < warp; w++) pre += s_wcnt[w][d];
+            kout[pre] = k;
+            vout[pre] = v;
+        }
+        __syncthreads();
+        unsigned tot = 0;
+#pragma unroll
+        for (int w = 0; w < SB / 32; w++) tot += s_wcnt[w][threadIdx.x];
+        s_base[threadIdx.x] += tot;
+        __syncthreads();
+    }
+}
+
+template <typename K>
+static int radix_sort_impl(long long count, K* keys, unsigned* vals, K* keys_alt, unsigned* vals_alt,
+                           int bit_lo, int bit_hi, const SortScratch& s, cudaStream_t st) {
+    if (count <= 1 || bit_hi <= bit_lo) return 0;
+    int g = sort_grid(count, s.max_blocks);
+    long long chunk = chunk_of(count, g);
+    g = (int)((count + chunk - 1) / chunk);
+    K* kin = keys;
+    unsigned* vin = vals;
+    K* kout = keys_alt;
+    unsigned* vout = vals_alt;
+    int parity = 0;
+    for (int shift = bit_lo; shift < bit_hi; shift += 8) {
+        int nb = bit_hi - shift < 8 ? bit_hi - shift : 8;
+        unsigned mask = (1u << nb) - 1u;
+        k_radix_hist<K><<<g, SB, 0, st>>>(count, chunk, kin, shift, mask, s.hist, g);
+        k_scan_single<<<1, 1024, 0, st>>>(s.hist, (long long)RADIX * g);
+        k_radix_scatter<K><<<g, SB, 0, st>>>(count, chunk, kin, vin, kout, vout, shift, mask, s.hist, g);
+        K* tk = kin; kin = kout; kout = tk;
+        unsigned* tv = vin; vin = vout; vout = tv;
+        parity ^= 1;
+    }
+    return parity;
+}
+
+int radix_sort_u64(long long count, unsigned long long* keys, unsigned* vals,
+                   unsigned long long* keys_alt, unsigned* vals_alt, int bit_lo, int bit_hi,
+                   const SortScratch& s, cudaStream_t st) {
+    return radix_sort_impl<unsigned long long>(count, keys, vals, keys_alt, vals_alt, bit_lo, bit_hi, s, st);
+}
+
+int radix_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
+                   unsigned* vals_alt, int bit_lo, int bit_hi, const SortScratch& s,
+                   cudaStream_t st) {
+    return radix_sort_impl<unsigned>(count, keys, vals, keys_alt, vals_alt, bit_lo, bit_hi, s, st);
+}
+
+// ---------------- duplication / ranges ----------------
+__global__ void __launch_bounds__(256) k_duplicate(long long m, const unsigned* __restrict__ sorted_src,
+                                                   const Rec64* __restrict__ rec, const unsigned* __restrict__ offs,
+                                                   int ntx, unsigned* __restrict__ tkey,
+                                                   unsigned* __restrict__ tval) {
+    long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    unsigned src = sorted_src[k];
+    const Rec64& r = rec[src];
+    int x0 = r.bx0, x1 = r.bx1, y0 = r.by0, y1 = r.by1;
+    if (x1 <= x0 || y1 <= y0) return;
+    int tx0 = x0 / TILE, tx1 = (x1 - 1) / TILE + 1, ty0 = y0 / TILE, ty1 = (y1 - 1) / TILE + 1;
+    unsigned pos = offs[k];
+    for (int ty = ty0; ty < ty1; ty++)
+        for (int tx = tx0; tx < tx1; tx++) {
+            tkey[pos] = (unsigned)(ty * ntx + tx);
+            tval[pos] = src;
+            pos++;
+        }
+}
+
+void duplicate_entries(long long m, const unsigned* sorted_src, const Rec64* rec, const unsigned* offs,
+                       int ntx, unsigned* tkey, unsigned* tval, cudaStream_t st) {
+    if (m <= 0) return;
+    k_duplicate<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, sorted_src, rec, offs, ntx, tkey, tval);
+}
+
+__global__ void k_ranges(long long e, const unsigned* __restrict__ tkey, int ntiles, int* __restrict__ start) {
+    long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= e) return;
+    int k = (int)tkey[pos];
+    int kp = pos > 0 ? (int)tkey[pos - 1] : -1;
+    for (int t = kp + 1; t <= k; t++) start[t] = (int)pos;
+    if (pos == e - 1)
+        for (int t = k + 1; t <= ntiles; t++) start[t] = (int)e;
+}
+
+void tile_ranges(long long e, const unsigned* tkey, int ntiles, int* tile_start, cudaStream_t st) {
+    if (e <= 0) {
+        cudaMemsetAsync(tile_start, 0, sizeof(int) * (ntiles + 1), st);
+        return;
+    }
+    k_ranges<<<(unsigned)((e + 255) / 256), 256, 0, st>>>(e, tkey, ntiles, tile_start);
+}
+
+__global__ void k_entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out) {
+    long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos < e) out[pos] = rank_of[ent_src[pos]];
+}
+
+void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out, cudaStream_t st) {
+    if (e <= 0) return;
+    k_entries_to_rank<<<(unsigned)((e + 255) / 256), 256, 0, st>>>(e, ent_src, rank_of, out);
+}
+
+__global__ void k_bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    bool ok = flag[i] != 0;
+    out[i * 4 + 0] = ok ? rec[i].bx0 : 0;
+    out[i * 4 + 1] = ok ? rec[i].bx1 : 0;
+    out[i * 4 + 2] = ok ? rec[i].by0 : 0;
+    out[i * 4 + 3] = ok ? rec[i].by1 : 0;
+}
+
+void bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out, cudaStream_t st) {
+    if (n <= 0) return;
+    k_bbox_dump<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, rec, flag, out);
+}
+
+}  // namespace ts

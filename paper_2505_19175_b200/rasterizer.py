@@ -1,0 +1,351 @@
+"""B200 rasterizer: device-resident API plus the reference's drop-in functions.
+
+Device-resident API (the hot path; no host copies)::
+
+    rast = Rasterizer()
+    soup = DeviceSoup.from_soup(cpu_soup, dtype=torch.float32)
+    fwd = rast.forward(soup, intr, pose)          # torch tensors on cuda
+    grads = rast.backward(d_image)                # DeviceGrads (fp32)
+
+Drop-in functions with the reference signatures and error behaviour:
+
+    render(triangles, intr, pose, mode, background, collect_fragments,
+           tau_cutoff, tile_size, active_sh_degree) -> RenderOutput     render.py:364-432
+    render_backward(triangles, intr, pose, mode, background, d_image,
+                    frag_grads, tau_cutoff, tile_size, active_sh_degree) -> GradientSet
+                                                                        backward.py:93-211
+
+Both run every stage on the GPU through the C ABI (include/trisplat_b200.h);
+numpy inputs are uploaded (fp64 kept as fp64 so the drop-in sees exactly the
+reference's parameter values) and numpy outputs returned.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .types import (DEFAULT_TAU_CUTOFF, DEFAULT_TILE_SIZE, TAU_CONTRIB, FragmentData,
+                    GradientSet, ImageBuffer, RenderOutput, as_soup, mode_flag)
+
+PRECISION = {"fast": 0, "exact": 1}
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("trisplat_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+@dataclass
+class DeviceSoup:
+    """Triangle parameters resident on the GPU (SoA, soup.py:17-30)."""
+
+    vertices: torch.Tensor  # (N,3,3)
+    opacity: torch.Tensor   # (N,)
+    sigma: torch.Tensor     # (N,)
+    sh: torch.Tensor        # (N,16,3)
+    solid: bool = False
+
+    @classmethod
+    def from_soup(cls, soup, dtype=torch.float32, device="cuda") -> "DeviceSoup":
+        soup = as_soup(soup)
+        n = len(soup.vertices)
+
+        def up(a, shape):
+            return torch.as_tensor(np.ascontiguousarray(np.asarray(a).reshape(shape)),
+                                   dtype=dtype).to(device)
+
+        return cls(up(soup.vertices, (n, 3, 3)), up(soup.opacity, (n,)), up(soup.sigma, (n,)),
+                   up(soup.sh, (n, 16, 3)), bool(getattr(soup, "solid", False)))
+
+    def __len__(self):
+        return self.vertices.shape[0]
+
+    @property
+    def dtype(self):
+        return self.vertices.dtype
+
+    def _ts(self):
+        for t in (self.vertices, self.opacity, self.sigma, self.sh):
+            if not t.is_cuda or not t.is_contiguous() or t.dtype != self.vertices.dtype:
+                raise ValueError("DeviceSoup tensors must be contiguous CUDA tensors of one dtype")
+        return _lib.TsSoup(self.vertices.data_ptr(), self.opacity.data_ptr(),
+                           self.sigma.data_ptr(), self.sh.data_ptr(), len(self))
+
+
+@dataclass
+class DeviceGrads:
+    """GradientSet on the GPU (backward.py:24-56), fp32, one flat buffer
+    [d_vertices (N*9) | d_opacity (N) | d_sigma (N) | d_sh (N*48)] so a
+    single all-reduce covers all 59 parameters."""
+
+    flat: torch.Tensor
+    n: int
+
+    @classmethod
+    def zeros(cls, n: int, device="cuda") -> "DeviceGrads":
+        return cls(torch.zeros(n * 59, dtype=torch.float32, device=device), n)
+
+    @property
+    def d_vertices(self):
+        return self.flat[: self.n * 9].view(self.n, 3, 3)
+
+    @property
+    def d_opacity(self):
+        return self.flat[self.n * 9: self.n * 10]
+
+    @property
+    def d_sigma(self):
+        return self.flat[self.n * 10: self.n * 11]
+
+    @property
+    def d_sh(self):
+        return self.flat[self.n * 11:].view(self.n, 16, 3)
+
+    def _ts(self):
+        return _lib.TsGrads(self.d_vertices.data_ptr(), self.d_opacity.data_ptr(),
+                            self.d_sigma.data_ptr(), self.d_sh.data_ptr())
+
+    def to_gradient_set(self) -> GradientSet:
+        return GradientSet(self.d_vertices.double().cpu().numpy(),
+                           self.d_opacity.double().cpu().numpy(),
+                           self.d_sigma.double().cpu().numpy(),
+                           self.d_sh.double().cpu().numpy())
+
+
+@dataclass
+class ForwardResult:
+    image: torch.Tensor        # (H,W,3) float32, clipped
+    alpha_map: torch.Tensor    # (H,W)
+    max_weight: torch.Tensor   # (N,)
+    pixel_count: torch.Tensor  # (N,) int32
+    area: torch.Tensor         # (N,)
+    last_src: torch.Tensor | None  # (H,W) int32
+    n_frag: torch.Tensor | None    # (H,W) int32
+    n_visible: int
+    n_entries: int
+    n_flagged: int
+
+
+def make_camera(intr, pose) -> _lib.TsCamera:
+    r = np.asarray(pose.rotation, dtype=np.float64).reshape(9)
+    t = np.asarray(pose.translation, dtype=np.float64).reshape(3)
+    return _lib.TsCamera(float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy),
+                         float(getattr(intr, "z_near", 0.01)), (ctypes.c_double * 9)(*r),
+                         (ctypes.c_double * 3)(*t), int(intr.width), int(intr.height))
+
+
+def make_options(mode=0, background=(0.0, 0.0, 0.0), tau_cutoff=DEFAULT_TAU_CUTOFF,
+                 tile_size=DEFAULT_TILE_SIZE, active_sh_degree=3, solid=False, precision="fast",
+                 param_dtype=torch.float32, validate=True) -> _lib.TsOptions:
+    bg = np.asarray(background, dtype=np.float64).reshape(3)
+    if not 0 <= int(active_sh_degree) <= 3:
+        raise ValueError("SH degree must be in [0,3]")
+    if int(tile_size) != 16:
+        raise NotImplementedError("trisplat_b200 supports tile_size=16 only")
+    return _lib.TsOptions(mode_flag(mode), int(active_sh_degree), int(tile_size), int(bool(solid)),
+                          float(tau_cutoff), float(TAU_CONTRIB), (ctypes.c_double * 3)(*bg),
+                          PRECISION[precision] if isinstance(precision, str) else int(precision),
+                          1 if param_dtype == torch.float64 else 0, int(bool(validate)), 0)
+
+
+_NONFINITE_GROUPS = ("vertices", "opacity", "sigma", "sh")
+
+
+class Rasterizer:
+    """One C-ABI context (scratch memory + last forward state) on one device."""
+
+    def __init__(self, device: int | None = None):
+        _require_cuda()
+        self.lib = _lib.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.ts_context_create(ctypes.byref(h), self.device), "context_create")
+        self._ctx = h
+        self._last = None  # (n, H, W)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_ctx", None):
+                self.lib.ts_context_destroy(self._ctx)
+        except Exception:
+            pass
+
+    def launch_count(self) -> int:
+        return int(self.lib.ts_launch_count(self._ctx))
+
+    def forward(self, soup: DeviceSoup, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
+                tau_cutoff=DEFAULT_TAU_CUTOFF, tile_size=DEFAULT_TILE_SIZE, active_sh_degree=3,
+                precision="fast", validate=True, debug=False, out: ForwardResult | None = None,
+                stream=None) -> ForwardResult:
+        n = len(soup)
+        h, w = int(intr.height), int(intr.width)
+        dev = soup.vertices.device
+        if out is None:
+            out = ForwardResult(
+                image=torch.empty((h, w, 3), dtype=torch.float32, device=dev),
+                alpha_map=torch.empty((h, w), dtype=torch.float32, device=dev),
+                max_weight=torch.empty(n, dtype=torch.float32, device=dev),
+                pixel_count=torch.empty(n, dtype=torch.int32, device=dev),
+                area=torch.empty(n, dtype=torch.float32, device=dev),
+                last_src=torch.empty((h, w), dtype=torch.int32, device=dev) if debug else None,
+                n_frag=torch.empty((h, w), dtype=torch.int32, device=dev) if debug else None,
+                n_visible=0, n_entries=0, n_flagged=0)
+        cam = make_camera(intr, pose)
+        opt = make_options(mode, background, tau_cutoff, tile_size, active_sh_degree, soup.solid,
+                           precision, soup.dtype, validate)
+        fo = _lib.TsForwardOut(_ptr(out.image), _ptr(out.alpha_map), _ptr(out.max_weight),
+                               _ptr(out.pixel_count), _ptr(out.area), _ptr(out.last_src),
+                               _ptr(out.n_frag))
+        res = _lib.TsForwardResult()
+        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        ts = soup._ts()
+        rc = self.lib.ts_forward(self._ctx, ctypes.byref(cam), ctypes.byref(opt),
+                                 ctypes.byref(ts), ctypes.byref(fo), ctypes.byref(res),
+                                 ctypes.c_void_p(st))
+        if rc == _lib.TS_ERR_NONFINITE:
+            for g, idx in zip(_NONFINITE_GROUPS, res.err_index):
+                if idx >= 0:
+                    raise ValueError(f"non-finite {g} in triangle {int(idx)}")
+        _lib.check(rc, "forward")
+        out.n_visible, out.n_entries, out.n_flagged = (int(res.n_visible), int(res.n_entries),
+                                                       int(res.n_flagged))
+        self._last = (n, h, w)
+        return out
+
+    def backward(self, d_image: torch.Tensor, grads: DeviceGrads | None = None,
+                 accumulate: bool = False, stream=None) -> DeviceGrads:
+        if self._last is None:
+            raise RuntimeError("backward() needs a preceding forward()")
+        n, h, w = self._last
+        if tuple(d_image.shape) != (h, w, 3):
+            raise ValueError(f"d_image must be {(h, w, 3)}, got {tuple(d_image.shape)}")
+        d_image = d_image.to(dtype=torch.float32).contiguous()
+        if grads is None:
+            grads = DeviceGrads(torch.empty(n * 59, dtype=torch.float32, device=d_image.device), n)
+            accumulate = False
+        st = (stream or torch.cuda.current_stream(d_image.device)).cuda_stream
+        g = grads._ts()
+        _lib.check(self.lib.ts_backward(self._ctx, _ptr(d_image), ctypes.byref(g),
+                                        int(bool(accumulate)), ctypes.c_void_p(st)), "backward")
+        return grads
+
+    # ---- parity dumps (project_scene / build_tile_lists internals) ----
+    def _dump(self, what, numel, dtype):
+        buf = torch.empty(max(numel, 1), dtype=dtype, device="cuda")
+        _lib.check(self.lib.ts_debug_copy(self._ctx, what, _ptr(buf), buf.numel() * buf.element_size(),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                   "debug_copy")
+        return buf[:numel].cpu().numpy()
+
+    def dump_sorted_idx(self, m):
+        return self._dump(_lib.TS_DUMP_SORTED_IDX, m, torch.int32).astype(np.int64)
+
+    def dump_tile_start(self, ntiles):
+        return self._dump(_lib.TS_DUMP_TILE_START, ntiles + 1, torch.int32).astype(np.int64)
+
+    def dump_entry_rank(self, e):
+        return self._dump(_lib.TS_DUMP_ENTRY_RANK, e, torch.int32).astype(np.int64)
+
+    def dump_bbox(self, n):
+        return self._dump(_lib.TS_DUMP_BBOX, n * 4, torch.int32).reshape(n, 4).astype(np.int64)
+
+    def dump_depth(self, n):
+        return self._dump(_lib.TS_DUMP_DEPTH, n, torch.float64)
+
+
+_DEFAULT: Rasterizer | None = None
+
+
+def default_rasterizer() -> Rasterizer:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Rasterizer()
+    return _DEFAULT
+
+
+def _param_dtype(soup):
+    v = np.asarray(soup.vertices)
+    return torch.float32 if v.dtype == np.float32 else torch.float64
+
+
+def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
+           collect_fragments: bool = False, tau_cutoff: float = DEFAULT_TAU_CUTOFF,
+           tile_size: int = DEFAULT_TILE_SIZE, active_sh_degree: int = 3,
+           precision: str = "fast") -> RenderOutput:
+    """Drop-in for trisplat.render.render (render.py:364-432)."""
+    _require_cuda()
+    soup = as_soup(triangles)
+    if collect_fragments:
+        raise NotImplementedError("collect_fragments is not implemented on the B200 path yet")
+    rast = default_rasterizer()
+    ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
+    fwd = rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
+                       precision=precision)
+    return RenderOutput(image=ImageBuffer(fwd.image.double().cpu().numpy()),
+                        alpha_map=fwd.alpha_map.double().cpu().numpy(),
+                        per_triangle_max_weight=fwd.max_weight.double().cpu().numpy(),
+                        per_triangle_pixel_count=fwd.pixel_count.cpu().numpy().astype(np.int64),
+                        per_triangle_area=fwd.area.double().cpu().numpy(),
+                        fragments=None)
+
+
+def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d_image=None,
+                    frag_grads=None, tau_cutoff: float = DEFAULT_TAU_CUTOFF,
+                    tile_size: int = DEFAULT_TILE_SIZE, active_sh_degree: int = 3,
+                    precision: str = "fast") -> GradientSet:
+    """Drop-in for trisplat.backward.render_backward (backward.py:93-211)."""
+    _require_cuda()
+    soup = as_soup(triangles)
+    h, w = intr.height, intr.width
+    d_np = np.ascontiguousarray(d_image, dtype=np.float64)
+    if d_np.shape != (h, w, 3):
+        raise ValueError(f"d_image must be {(h, w, 3)}, got {d_np.shape}")
+    if not np.isfinite(d_np).all():
+        raise ValueError("d_image contains non-finite values")
+    if frag_grads is not None:
+        raise NotImplementedError("frag_grads is not implemented on the B200 path yet")
+    rast = default_rasterizer()
+    ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
+    rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
+                 precision=precision)
+    g = rast.backward(torch.as_tensor(d_np, dtype=torch.float32, device="cuda"))
+    return g.to_gradient_set()
+
+
+def install(trisplat_module=None):
+    """Rebind the reference's render / render_backward to this path.
+
+    The reference imports them by name in several modules (training.py:12,19,
+    synthetic.py:14, cli.py:21, backward.py:17), so each binding is patched.
+    Returns the list of patched attributes."""
+    import importlib
+    import sys
+    patched = []
+    targets = {
+        "trisplat": ("render", "render_backward"),
+        "trisplat.render": ("render",),
+        "trisplat.backward": ("render", "render_backward"),
+        "trisplat.training": ("render", "render_backward"),
+        "trisplat.synthetic": ("render",),
+        "trisplat.cli": ("render",),
+    }
+    repl = {"render": render, "render_backward": render_backward}
+    for mod_name, names in targets.items():
+        try:
+            mod = sys.modules.get(mod_name) or importlib.import_module(mod_name)
+        except Exception:
+            continue
+        for nm in names:
+            if hasattr(mod, nm):
+                setattr(mod, nm, repl[nm])
+                patched.append(f"{mod_name}.{nm}")
+    return patched
