@@ -117,7 +117,9 @@ int ts_forward(ts_context* ctx, const ts_camera* cam, const ts_options* opt, con
 
 /* render_backward(): gradients of sum(d_image * image_unclipped) w.r.t. all
  * 59 parameters of every triangle, for the scene of the context's last
- * ts_forward (same soup/camera/options).  d_image is (H,W,3) float32.
+ * ts_forward (same soup/camera/options).  The soup parameter buffers passed
+ * to that ts_forward are read again here: they must stay allocated and
+ * unmodified until ts_backward returns.  d_image is (H,W,3) float32.
  * accumulate=1 adds into the gradient buffers, 0 overwrites them. */
 int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream);
@@ -127,15 +129,32 @@ int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, in
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)
  *  TS_DUMP_ENTRY_RANK  int32[E]       tile entries as depth ranks (render.py:358-360)
  *  TS_DUMP_BBOX        int32[N*4]     x0,x1,y0,y1 per source (0s if culled) (render.py:243-250)
- *  TS_DUMP_DEPTH       float64[N]     camera-space centroid depth per source */
+ *  TS_DUMP_DEPTH       float64[N]     camera-space centroid depth per source
+ *  TS_DUMP_SGRAD       float64[N*16]  screen-space gradients of the last ts_backward
+ *                                     (gq[6], go, gsig, grgb[3], gphis, gz, pad) per source */
 #define TS_DUMP_SORTED_IDX 1
 #define TS_DUMP_TILE_START 2
 #define TS_DUMP_ENTRY_RANK 3
 #define TS_DUMP_BBOX 4
 #define TS_DUMP_DEPTH 5
+#define TS_DUMP_SGRAD 6
 int ts_debug_copy(ts_context* ctx, int what, void* dst, size_t bytes, void* stream);
 
-/* Kernel launches issued by this context since creation (for launch counting). */
+/* Per-stage device timing with CUDA events recorded on the call's stream.
+ * ts_profile(ctx, 1) enables it; ts_stage_times fills ms[TS_NUM_STAGES] with
+ * the durations of the last ts_forward / ts_backward stages (0 if not run). */
+#define TS_STAGE_PREPROCESS 0
+#define TS_STAGE_DEPTH_SORT 1
+#define TS_STAGE_BINNING 2
+#define TS_STAGE_BLEND 3
+#define TS_STAGE_FIXUP 4
+#define TS_STAGE_BLEND_BWD 5
+#define TS_STAGE_CHAIN_BWD 6
+#define TS_NUM_STAGES 7
+int ts_profile(ts_context* ctx, int enable);
+int ts_stage_times(ts_context* ctx, float* ms, int n);
+
+/* Kernel launches issued by this library since load (for launch counting). */
 int64_t ts_launch_count(ts_context* ctx);
 
 #ifdef __cplusplus

@@ -250,7 +250,7 @@ def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), collect_fr
 
 def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d_image=None,
                     frag_grads=None, tau_cutoff=DEFAULT_TAU_CUTOFF, tile_size=16,
-                    active_sh_degree=3):
+                    active_sh_degree=3, return_screen=False):
     """backward.py:93-211.  Returns a namespace with d_vertices (N,3,3),
     d_opacity (N,), d_sigma (N,), d_sh (N,16,3)."""
     validate_finite(triangles)
@@ -306,6 +306,14 @@ def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d
                               _p(fg_dz), _p(gq_e), _p(go_e), _p(gsig_e), _p(grgb_e), _p(gphis_e),
                               _p(gz_e))
     m = len(proj.sorted_idx)
+    if return_screen:
+        sg = np.zeros((n, 13))
+        src = proj.sorted_idx[entry_tri] if ne else np.zeros(0, np.int64)
+        for j, arr in enumerate((gq_e.reshape(-1, 6)[:ne], go_e[:ne, None], gsig_e[:ne, None],
+                                 grgb_e.reshape(-1, 3)[:ne], gphis_e[:ne, None], gz_e[:ne, None])):
+            off = (0, 6, 7, 8, 11, 12)[j]
+            np.add.at(sg[:, off:off + arr.shape[1]], src, arr)
+        return sg
     grads = SimpleNamespace(d_vertices=np.zeros((n, 3, 3)), d_opacity=np.zeros(n),
                             d_sigma=np.zeros(n), d_sh=np.zeros((n, 16, 3)))
     if m == 0:

@@ -19,6 +19,7 @@ TS_DUMP_TILE_START = 2
 TS_DUMP_ENTRY_RANK = 3
 TS_DUMP_BBOX = 4
 TS_DUMP_DEPTH = 5
+TS_DUMP_SGRAD = 6
 
 
 class TsCamera(ctypes.Structure):
@@ -60,7 +61,9 @@ class TsGrads(ctypes.Structure):
 
 
 EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_version",
-           "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count"]
+           "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
+           "ts_stage_times"]
+STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
 
@@ -94,6 +97,10 @@ def load(path: str = LIB_PATH):
     lib.ts_debug_copy.restype = ctypes.c_int
     lib.ts_launch_count.argtypes = [ctypes.c_void_p]
     lib.ts_launch_count.restype = ctypes.c_int64
+    lib.ts_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.ts_profile.restype = ctypes.c_int
+    lib.ts_stage_times.argtypes = [ctypes.c_void_p, P(ctypes.c_float), ctypes.c_int]
+    lib.ts_stage_times.restype = ctypes.c_int
     _LIB = lib
     return lib
 

@@ -60,7 +60,18 @@ struct ts_context {
     long long n = 0, m = 0, e = 0;
     const unsigned* sorted_src = nullptr;
     const unsigned* ent_src = nullptr;
+    // stage profiling
+    bool profile = false;
+    cudaEvent_t ev[TS_NUM_STAGES][2] = {};
+    bool ev_used[TS_NUM_STAGES] = {};
 };
+
+static void stage_begin(ts_context* c, int s, cudaStream_t st) {
+    if (c->profile) { cudaEventRecord(c->ev[s][0], st); c->ev_used[s] = true; }
+}
+static void stage_end(ts_context* c, int s, cudaStream_t st) {
+    if (c->profile) cudaEventRecord(c->ev[s][1], st);
+}
 
 static int cuda_err(cudaError_t e) {
     if (e != cudaSuccess) {
@@ -221,11 +232,36 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->sort_buf);
     cudaFree(c->d_ctr);
     cudaFreeHost(c->h_ctr);
+    for (int k = 0; k < TS_NUM_STAGES; k++)
+        if (c->ev[k][0]) { cudaEventDestroy(c->ev[k][0]); cudaEventDestroy(c->ev[k][1]); }
     delete c;
     return TS_OK;
 }
 
 int64_t ts_launch_count(ts_context*) { return g_launches.load(); }
+
+int ts_profile(ts_context* c, int enable) {
+    if (!c) return TS_ERR_INVALID_ARG;
+    if (enable && !c->ev[0][0])
+        for (int k = 0; k < TS_NUM_STAGES; k++) {
+            TS_CHECK(cudaEventCreate(&c->ev[k][0]));
+            TS_CHECK(cudaEventCreate(&c->ev[k][1]));
+        }
+    c->profile = enable != 0;
+    return TS_OK;
+}
+
+int ts_stage_times(ts_context* c, float* ms, int n) {
+    if (!c || !ms) return TS_ERR_INVALID_ARG;
+    for (int k = 0; k < n && k < TS_NUM_STAGES; k++) {
+        ms[k] = 0.f;
+        if (c->profile && c->ev_used[k]) {
+            TS_CHECK(cudaEventSynchronize(c->ev[k][1]));
+            TS_CHECK(cudaEventElapsedTime(&ms[k], c->ev[k][0], c->ev[k][1]));
+        }
+    }
+    return TS_OK;
+}
 
 int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const ts_soup* soup,
                const ts_forward_out* out, ts_forward_result* res, void* stream) {
@@ -236,6 +272,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     if (soup->n >= (1ll << 31)) return TS_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     c->have_fwd = false;
+    for (int k = 0; k < TS_NUM_STAGES; k++) c->ev_used[k] = false;
     Cam cm;
     Opts op;
     build_cam_opts(cam, opt, cm, op);
@@ -255,7 +292,9 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     if (out->max_weight) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
     if (out->pixel_count) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
     PreOut po{c->rec, c->key, c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+    stage_begin(c, TS_STAGE_PREPROCESS, st);
     launch_preprocess(cm, op, *soup, opt->param_dtype, po, st);
+    stage_end(c, TS_STAGE_PREPROCESS, st);
     g_launches += 1;
     TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     TS_CHECK(cudaStreamSynchronize(st));
@@ -274,6 +313,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     if (e >= (1ll << 31)) return TS_ERR_INVALID_ARG;
     if ((rc = ensure_ent(c, e > 0 ? e : 1))) return rc;
     // depth order: compaction (source order) + stable radix sort on fp64 bits
+    stage_begin(c, TS_STAGE_DEPTH_SORT, st);
     compact_accepted(n, c->flag, c->key, c->keys_c, c->vals_c, c->sort, st);
     g_launches += 3;
     unsigned long long diff = h.key_and ^ h.key_or;
@@ -282,6 +322,8 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     int par = radix_sort_u64(m, c->keys_c, c->vals_c, c->keys_alt, c->vals_alt, lo, hi, c->sort, st);
     if (m > 1 && hi > lo) g_launches += 3 * ((hi - lo + 7) / 8);
     c->sorted_src = par ? c->vals_alt : c->vals_c;
+    stage_end(c, TS_STAGE_DEPTH_SORT, st);
+    stage_begin(c, TS_STAGE_BINNING, st);
     // tile duplication in rank order + stable sort by tile id
     rank_offsets(m, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
     duplicate_entries(m, c->sorted_src, c->rec, c->offs, cm.ntx, c->tkey, c->tval, st);
@@ -292,10 +334,13 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     const unsigned* skey = par ? c->tkey_alt : c->tkey;
     c->ent_src = par ? c->tval_alt : c->tval;
     tile_ranges(e, skey, ntiles, c->tile_start, st);
+    stage_end(c, TS_STAGE_BINNING, st);
     g_launches += 1;
     BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
                 out->n_frag, c->t_final, c->last_pos};
+    stage_begin(c, TS_STAGE_BLEND, st);
     launch_blend_exact(cm, op, c->rec, c->tile_start, (const int*)c->ent_src, bo, st);
+    stage_end(c, TS_STAGE_BLEND, st);
     g_launches += 1;
     TS_CHECK(cudaGetLastError());
     c->have_fwd = true;
@@ -316,10 +361,15 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
     cudaStream_t st = (cudaStream_t)stream;
     int rc = ensure_sg(c, c->n > 0 ? c->n : 1);
     if (rc) return rc;
+    c->ev_used[TS_STAGE_BLEND_BWD] = c->ev_used[TS_STAGE_CHAIN_BWD] = false;
+    stage_begin(c, TS_STAGE_BLEND_BWD, st);
     if (c->n > 0) TS_CHECK(cudaMemsetAsync(c->sgrad, 0, sizeof(double) * SG_STRIDE * c->n, st));
     launch_blend_bwd_exact(c->cam, c->opt, c->rec, c->tile_start, (const int*)c->ent_src, c->t_final,
                            c->last_pos, d_image, c->sgrad, st);
+    stage_end(c, TS_STAGE_BLEND_BWD, st);
+    stage_begin(c, TS_STAGE_CHAIN_BWD, st);
     launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, c->sgrad, *grads, accumulate, st);
+    stage_end(c, TS_STAGE_CHAIN_BWD, st);
     g_launches += 2;
     TS_CHECK(cudaGetLastError());
     return TS_OK;
@@ -350,6 +400,10 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
         case TS_DUMP_DEPTH:
             if (bytes < 8 * (size_t)c->n) return TS_ERR_INVALID_ARG;
             if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->depth, 8 * c->n, cudaMemcpyDeviceToDevice, st));
+            return TS_OK;
+        case TS_DUMP_SGRAD:
+            if (bytes < 8 * SG_STRIDE * (size_t)c->n || c->cap_sg < c->n) return TS_ERR_INVALID_ARG;
+            if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->sgrad, 8 * SG_STRIDE * c->n, cudaMemcpyDeviceToDevice, st));
             return TS_OK;
         default:
             return TS_ERR_INVALID_ARG;

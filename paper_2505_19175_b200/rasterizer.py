@@ -171,6 +171,7 @@ class Rasterizer:
         _lib.check(self.lib.ts_context_create(ctypes.byref(h), self.device), "context_create")
         self._ctx = h
         self._last = None  # (n, H, W)
+        self._last_soup = None
 
     def __del__(self):
         try:
@@ -181,6 +182,16 @@ class Rasterizer:
 
     def launch_count(self) -> int:
         return int(self.lib.ts_launch_count(self._ctx))
+
+    def profile(self, enable: bool = True):
+        """Record CUDA events around every pipeline stage (on the call's stream)."""
+        _lib.check(self.lib.ts_profile(self._ctx, int(bool(enable))), "profile")
+
+    def stage_times(self) -> dict:
+        """Device milliseconds of each stage of the last forward/backward."""
+        buf = (ctypes.c_float * len(_lib.STAGES))()
+        _lib.check(self.lib.ts_stage_times(self._ctx, buf, len(_lib.STAGES)), "stage_times")
+        return {k: float(v) for k, v in zip(_lib.STAGES, buf)}
 
     def forward(self, soup: DeviceSoup, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
                 tau_cutoff=DEFAULT_TAU_CUTOFF, tile_size=DEFAULT_TILE_SIZE, active_sh_degree=3,
@@ -219,6 +230,7 @@ class Rasterizer:
         out.n_visible, out.n_entries, out.n_flagged = (int(res.n_visible), int(res.n_entries),
                                                        int(res.n_flagged))
         self._last = (n, h, w)
+        self._last_soup = soup  # ts_backward reads these parameters: keep them alive
         return out
 
     def backward(self, d_image: torch.Tensor, grads: DeviceGrads | None = None,
@@ -260,6 +272,9 @@ class Rasterizer:
 
     def dump_depth(self, n):
         return self._dump(_lib.TS_DUMP_DEPTH, n, torch.float64)
+
+    def dump_sgrad(self, n):
+        return self._dump(_lib.TS_DUMP_SGRAD, n * 16, torch.float64).reshape(n, 16)
 
 
 _DEFAULT: Rasterizer | None = None

@@ -61,8 +61,14 @@ def check_forward(rast, fwd, ref, intr, label=""):
 
 def check_grads(g, gref, label=""):
     for k in ("d_vertices", "d_opacity", "d_sigma", "d_sh"):
-        err = rel_err(_np(getattr(g, k)), getattr(gref, k))
-        assert err < GRAD_RTOL, f"{label} {k} rel err {err}"
+        got, want = _np(getattr(g, k)).astype(np.float64), getattr(gref, k)
+        err = rel_err(got, want)
+        if err >= GRAD_RTOL:
+            n = len(want)
+            d = np.abs(got - want).reshape(n, -1).max(1)
+            i = int(np.argmax(d))
+            pytest.fail(f"{label} {k} rel err {err}: tri {i} got {got[i].ravel()[:6]} "
+                        f"want {want[i].ravel()[:6]} scale {np.abs(want).max()}")
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
