@@ -48,6 +48,8 @@ struct ts_context {
     // sort scratch
     void* sort_buf = nullptr;
     SortScratch sort{};
+    void* os_buf = nullptr;
+    long long os_cap = -1;
     // counters
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;
@@ -156,6 +158,16 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     return TS_OK;
 }
 
+static int ensure_os(ts_context* c, long long count) {
+    if (count <= c->os_cap) return TS_OK;
+    long long cap = count + count / 4 + 4096;
+    if (c->os_buf) cudaFree(c->os_buf);
+    c->os_buf = nullptr;
+    TS_CHECK(cudaMalloc(&c->os_buf, onesweep_scratch_bytes(cap, 4)));
+    c->os_cap = cap;
+    return TS_OK;
+}
+
 static int ensure_sg(ts_context* c, long long n) {
     if (n <= c->cap_sg) return TS_OK;
     long long cap = n + n / 4 + 1024;
@@ -230,6 +242,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->pix_buf);
     cudaFree(c->sgrad);
     cudaFree(c->sort_buf);
+    cudaFree(c->os_buf);
     cudaFree(c->d_ctr);
     cudaFreeHost(c->h_ctr);
     for (int k = 0; k < TS_NUM_STAGES; k++)
@@ -286,6 +299,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     Counters init;
     memset(&init, 0, sizeof(init));
     init.key_and = ~0ull;
+    init.key_min = ~0ull;
     for (int k = 0; k < 4; k++) init.err[k] = 0x7fffffffffffffffLL;
     *c->h_ctr = init;
     TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_ctr, sizeof(Counters), cudaMemcpyHostToDevice, st));
@@ -312,16 +326,26 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     const long long m = (long long)h.m, e = (long long)h.e;
     if (e >= (1ll << 31)) return TS_ERR_INVALID_ARG;
     if ((rc = ensure_ent(c, e > 0 ? e : 1))) return rc;
-    // depth order: compaction (source order) + stable radix sort on fp64 bits
+    // depth order: compaction (source order) of range-reduced 32-bit depth
+    // keys, stable onesweep radix sort, then exact (z64, idx) order restored
+    // inside runs of equal reduced keys (np.lexsort((idx, z)), render.py:276)
+    if ((rc = ensure_os(c, (m > e ? m : e) + 1))) return rc;
     stage_begin(c, TS_STAGE_DEPTH_SORT, st);
-    compact_accepted(n, c->flag, c->key, c->keys_c, c->vals_c, c->sort, st);
+    unsigned long long krange = m ? h.key_max - h.key_min : 0ull;
+    int kbits = bit_length(krange);
+    int kshift = kbits > 32 ? kbits - 32 : 0;
+    int knb = kbits > 32 ? 32 : kbits;
+    unsigned* k32 = (unsigned*)c->keys_c;
+    unsigned* k32_alt = (unsigned*)c->keys_alt;
+    compact_accepted32(n, c->flag, c->key, h.key_min, kshift, k32, c->vals_c, c->sort, st);
     g_launches += 3;
-    unsigned long long diff = h.key_and ^ h.key_or;
-    int lo = diff ? __builtin_ctzll(diff) : 0, hi = bit_length(diff);
-    lo = lo / 8 * 8;
-    int par = radix_sort_u64(m, c->keys_c, c->vals_c, c->keys_alt, c->vals_alt, lo, hi, c->sort, st);
-    if (m > 1 && hi > lo) g_launches += 3 * ((hi - lo + 7) / 8);
+    int par = onesweep_sort_u32(m, k32, c->vals_c, k32_alt, c->vals_alt, knb, c->os_buf, st);
+    if (m > 1 && knb > 0) g_launches += 1 + (knb + 7) / 8;
     c->sorted_src = par ? c->vals_alt : c->vals_c;
+    if (kshift > 0) {
+        fix_depth_runs(m, par ? k32_alt : k32, (unsigned*)c->sorted_src, c->key, st);
+        g_launches += 1;
+    }
     stage_end(c, TS_STAGE_DEPTH_SORT, st);
     stage_begin(c, TS_STAGE_BINNING, st);
     // tile duplication in rank order + stable sort by tile id
@@ -329,8 +353,8 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     duplicate_entries(m, c->sorted_src, c->rec, c->offs, cm.ntx, c->tkey, c->tval, st);
     g_launches += 4;
     int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
-    par = radix_sort_u32(e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, 0, tbits, c->sort, st);
-    if (e > 1 && tbits > 0) g_launches += 3 * ((tbits + 7) / 8);
+    par = onesweep_sort_u32(e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits, c->os_buf, st);
+    if (e > 1 && tbits > 0) g_launches += 1 + (tbits + 7) / 8;
     const unsigned* skey = par ? c->tkey_alt : c->tkey;
     c->ent_src = par ? c->tval_alt : c->tval;
     tile_ranges(e, skey, ntiles, c->tile_start, st);

@@ -93,18 +93,20 @@ __global__ void __launch_bounds__(256) k_preprocess(Cam cam, Opts opt, const T* 
         out.key[i] = key;
     }
     // block-aggregated counters
-    unsigned long long kand = ok ? key : ~0ull, kor = ok ? key : 0ull;
+    unsigned long long kmin = ok ? key : ~0ull, kmax = ok ? key : 0ull;
     unsigned cnt = ok ? 1u : 0u;
     unsigned long long tc = tcount;
     for (int off = 16; off > 0; off >>= 1) {
-        kand &= __shfl_xor_sync(0xffffffffu, kand, off);
-        kor |= __shfl_xor_sync(0xffffffffu, kor, off);
+        unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, off);
+        unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, off);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
         cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
         tc += __shfl_xor_sync(0xffffffffu, tc, off);
     }
     if ((threadIdx.x & 31) == 0 && cnt) {
-        atomicAnd(&out.ctr->key_and, kand);
-        atomicOr(&out.ctr->key_or, kor);
+        atomicMin(&out.ctr->key_min, kmin);
+        atomicMax(&out.ctr->key_max, kmax);
         atomicAdd(&out.ctr->m, (unsigned long long)cnt);
         atomicAdd(&out.ctr->e, tc);
     }

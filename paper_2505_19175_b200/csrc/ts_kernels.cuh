@@ -9,9 +9,11 @@ struct Counters {
     unsigned long long e;        // tile entries
     unsigned long long key_and;  // AND / OR of accepted depth keys (pass selection)
     unsigned long long key_or;
+    unsigned long long key_min;
+    unsigned long long key_max;
     long long err[4];            // first non-finite index per group
     unsigned long long n_flagged;
-    unsigned long long pad[7];
+    unsigned long long pad[5];
 };
 
 struct PreOut {
@@ -80,5 +82,15 @@ void tile_ranges(long long e, const unsigned* tkey, int ntiles, int* tile_start,
 void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out,
                      cudaStream_t st);
 void bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out, cudaStream_t st);
+
+// onesweep radix sort (32-bit keys), scratch from onesweep_scratch_bytes
+size_t onesweep_scratch_bytes(long long max_count, int max_passes);
+int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
+                      unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
+void compact_accepted32(long long n, const unsigned* flag, const unsigned long long* key,
+                        unsigned long long kmin, int shift, unsigned* keys_c, unsigned* vals_c,
+                        const SortScratch& s, cudaStream_t st);
+void fix_depth_runs(long long m, const unsigned* k32, unsigned* vals, const unsigned long long* key64,
+                    cudaStream_t st);
 
 }  // namespace ts

@@ -334,3 +334,202 @@ void bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out, cu
 }
 
 }  // namespace ts
+
+// ===========================================================================
+// Onesweep LSD radix sort (single kernel per 8-bit pass, decoupled look-back),
+// 32-bit keys + 32-bit values, stable.  Tile = 4096 items per CTA; each warp
+// owns a contiguous 512-item segment loaded warp-striped so (item, lane)
+// order equals input order, which keeps the sort stable.
+// ===========================================================================
+namespace ts {
+
+constexpr int OS_THREADS = 256;
+constexpr int OS_ITEMS = 16;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096
+constexpr unsigned OS_FLAG_AGG = 1u << 30;
+constexpr unsigned OS_FLAG_INC = 2u << 30;
+constexpr unsigned OS_VAL_MASK = (1u << 30) - 1u;
+
+size_t onesweep_scratch_bytes(long long max_count, int max_passes) {
+    long long tiles = (max_count + OS_TILE - 1) / OS_TILE + 1;
+    return sizeof(unsigned) * ((size_t)max_passes * tiles * RADIX + (size_t)max_passes * RADIX + 64);
+}
+
+__global__ void __launch_bounds__(256) k_os_hist(long long count, const unsigned* __restrict__ keys, int shift0,
+                                                 int npass, unsigned* __restrict__ ghist) {
+    __shared__ unsigned s_h[4][RADIX];
+    for (int k = threadIdx.x; k < 4 * RADIX; k += 256) (&s_h[0][0])[k] = 0;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < count; i += (long long)gridDim.x * 256) {
+        unsigned k = keys[i];
+        for (int p = 0; p < npass; p++) atomicAdd(&s_h[p][(k >> (shift0 + 8 * p)) & 0xffu], 1u);
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; p++) {
+        unsigned v = s_h[p][threadIdx.x];
+        if (v) atomicAdd(&ghist[p * RADIX + threadIdx.x], v);
+    }
+}
+
+__global__ void __launch_bounds__(OS_THREADS) k_onesweep(long long count, const unsigned* __restrict__ kin,
+                                                         const unsigned* __restrict__ vin,
+                                                         unsigned* __restrict__ kout, unsigned* __restrict__ vout,
+                                                         int shift, const unsigned* __restrict__ pass_hist,
+                                                         unsigned* status, unsigned* ticket) {
+    __shared__ unsigned s_wc[OS_THREADS / 32][RADIX];
+    __shared__ unsigned s_gbase[RADIX];
+    __shared__ unsigned s_tile;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int w = 0; w < OS_THREADS / 32; w++) s_wc[w][threadIdx.x] = 0;
+    // exclusive scan of the global digit histogram for this pass
+    unsigned tot;
+    unsigned gofs = block_excl_scan(pass_hist[threadIdx.x], tot);  // contains __syncthreads
+    const unsigned tile = s_tile;
+    const long long base = (long long)tile * OS_TILE + (long long)warp * (OS_TILE / (OS_THREADS / 32));
+    const unsigned lt = lanemask_lt();
+    unsigned key[OS_ITEMS], val[OS_ITEMS], off[OS_ITEMS];
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; i++) {
+        long long idx = base + i * 32 + lane;
+        bool valid = idx < count;
+        key[i] = valid ? kin[idx] : 0u;
+        val[i] = valid ? vin[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; i++) {
+        long long idx = base + i * 32 + lane;
+        bool valid = idx < count;
+        unsigned d = valid ? ((key[i] >> shift) & 0xffu) : 0x100u;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        unsigned rank = __popc(peers & lt);
+        unsigned b = valid ? s_wc[warp][d] : 0u;
+        __syncwarp();
+        if (valid && rank == 0) s_wc[warp][d] = b + __popc(peers);
+        __syncwarp();
+        off[i] = b + rank;
+    }
+    __syncthreads();
+    // per digit: warp-exclusive prefix + block count
+    unsigned run = 0;
+#pragma unroll
+    for (int w = 0; w < OS_THREADS / 32; w++) {
+        unsigned c = s_wc[w][threadIdx.x];
+        s_wc[w][threadIdx.x] = run;
+        run += c;
+    }
+    const unsigned d = threadIdx.x;
+    volatile unsigned* st = status;
+    unsigned excl = 0;
+    if (tile == 0) {
+        st[d] = OS_FLAG_INC | run;
+    } else {
+        st[(size_t)tile * RADIX + d] = OS_FLAG_AGG | run;
+        long long j = (long long)tile - 1;
+        while (true) {
+            unsigned s = st[(size_t)j * RADIX + d];
+            if ((s & ~OS_VAL_MASK) == 0) continue;
+            excl += s & OS_VAL_MASK;
+            if (s & OS_FLAG_INC) break;
+            j--;
+        }
+        st[(size_t)tile * RADIX + d] = OS_FLAG_INC | (excl + run);
+    }
+    s_gbase[d] = gofs + excl;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; i++) {
+        long long idx = base + i * 32 + lane;
+        if (idx < count) {
+            unsigned dd = (key[i] >> shift) & 0xffu;
+            unsigned pos = s_gbase[dd] + s_wc[warp][dd] + off[i];
+            kout[pos] = key[i];
+            vout[pos] = val[i];
+        }
+    }
+}
+
+// Sorts (keys, vals) by bits [0, nbits).  Returns 1 if the result is in the alt buffers.
+int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
+                      unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st) {
+    if (count <= 1 || nbits <= 0) return 0;
+    int npass = (nbits + 7) / 8;
+    long long tiles = (count + OS_TILE - 1) / OS_TILE;
+    unsigned* status = (unsigned*)scratch;
+    unsigned* hist = status + (size_t)npass * tiles * RADIX;
+    unsigned* tickets = hist + npass * RADIX;
+    cudaMemsetAsync(scratch, 0, sizeof(unsigned) * ((size_t)npass * tiles * RADIX + npass * RADIX + 16), st);
+    long long hg = (count + 255) / 256;
+    int hgrid = (int)(hg < 148 * 4 ? hg : 148 * 4);
+    k_os_hist<<<hgrid, 256, 0, st>>>(count, keys, 0, npass, hist);
+    unsigned *kin = keys, *vin = vals, *kout = keys_alt, *vout = vals_alt;
+    int parity = 0;
+    for (int p = 0; p < npass; p++) {
+        k_onesweep<<<(unsigned)tiles, OS_THREADS, 0, st>>>(count, kin, vin, kout, vout, 8 * p, hist + p * RADIX,
+                                                           status + (size_t)p * tiles * RADIX, tickets + p);
+        unsigned* t = kin; kin = kout; kout = t;
+        t = vin; vin = vout; vout = t;
+        parity ^= 1;
+    }
+    return parity;
+}
+
+// ---------------------------------------------------------------------------
+// Depth-key helpers: 32-bit range-reduced keys, then exact (z64, idx) order
+// restored inside runs of equal reduced keys.
+// ---------------------------------------------------------------------------
+struct CompactKey32F {
+    const unsigned* flag;
+    const unsigned long long* key;
+    unsigned long long kmin;
+    int shift;
+    unsigned* keys_c;
+    unsigned* vals_c;
+    __device__ unsigned load(long long i) const { return flag[i]; }
+    __device__ void store(long long i, unsigned ex, unsigned v) const {
+        if (v) {
+            keys_c[ex] = (unsigned)((key[i] - kmin) >> shift);
+            vals_c[ex] = (unsigned)i;
+        }
+    }
+};
+
+void compact_accepted32(long long n, const unsigned* flag, const unsigned long long* key,
+                        unsigned long long kmin, int shift, unsigned* keys_c, unsigned* vals_c,
+                        const SortScratch& s, cudaStream_t st) {
+    scan_functor(n, CompactKey32F{flag, key, kmin, shift, keys_c, vals_c}, s, st);
+}
+
+// Restore exact order inside runs of equal reduced keys: insertion sort on
+// (key64[src], src) -- runs are short in practice and already in src order.
+__global__ void k_fix_runs(long long m, const unsigned* __restrict__ k32, unsigned* __restrict__ vals,
+                           const unsigned long long* __restrict__ key64) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    unsigned k = k32[p];
+    if (p > 0 && k32[p - 1] == k) return;
+    if (p + 1 >= m || k32[p + 1] != k) return;
+    long long end = p + 1;
+    while (end < m && k32[end] == k) end++;
+    for (long long i = p + 1; i < end; i++) {
+        unsigned v = vals[i];
+        unsigned long long kv = key64[v];
+        long long j = i - 1;
+        while (j >= p) {
+            unsigned u = vals[j];
+            unsigned long long ku = key64[u];
+            if (ku < kv || (ku == kv && u < v)) break;
+            vals[j + 1] = u;
+            j--;
+        }
+        vals[j + 1] = v;
+    }
+}
+
+void fix_depth_runs(long long m, const unsigned* k32, unsigned* vals, const unsigned long long* key64,
+                    cudaStream_t st) {
+    if (m <= 1) return;
+    k_fix_runs<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, k32, vals, key64);
+}
+
+}  // namespace ts
