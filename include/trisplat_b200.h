@@ -43,6 +43,7 @@ extern "C" {
 #define TS_ERR_NONFINITE -5
 #define TS_ERR_TILE_SIZE -6
 #define TS_ERR_FRAGMENTS -7
+#define TS_ERR_NO_BWD_STATE -8
 
 /* geometry.py:32-74: intrinsics + world->camera pose x_cam = R x + t */
 typedef struct ts_camera {
@@ -63,7 +64,7 @@ typedef struct ts_options {
     int32_t precision;   /* 0 = fast fp32 path with fp64 guard-band fix-up, 1 = exact fp64 */
     int32_t param_dtype; /* 0 = float32 parameters, 1 = float64 parameters */
     int32_t validate;    /* 1 = non-finite check (soup.py:67-77), 0 = skip */
-    int32_t reserved;
+    int32_t keep_backward; /* 1 = also store the per-triangle state ts_backward needs */
 } ts_options;
 
 /* Triangle soup parameters (soup.py:17-30), device pointers, SoA blocks:
@@ -153,6 +154,10 @@ int ts_debug_copy(ts_context* ctx, int what, void* dst, size_t bytes, void* stre
 #define TS_NUM_STAGES 7
 int ts_profile(ts_context* ctx, int enable);
 int ts_stage_times(ts_context* ctx, float* ms, int n);
+
+/* Pixels of the last fast-path ts_forward whose guard band required the
+ * exact fix-up (valid once the forward's stream has been synchronized). */
+int ts_flagged_pixels(ts_context* ctx, int64_t* n_flagged);
 
 /* Kernel launches issued by this library since load (for launch counting). */
 int64_t ts_launch_count(ts_context* ctx);

@@ -35,7 +35,7 @@ class TsOptions(ctypes.Structure):
                 ("tau_cutoff", ctypes.c_double), ("tau_contrib", ctypes.c_double),
                 ("background", ctypes.c_double * 3), ("precision", ctypes.c_int32),
                 ("param_dtype", ctypes.c_int32), ("validate", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("keep_backward", ctypes.c_int32)]
 
 
 class TsSoup(ctypes.Structure):
@@ -62,7 +62,7 @@ class TsGrads(ctypes.Structure):
 
 EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_version",
            "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
-           "ts_stage_times"]
+           "ts_stage_times", "ts_flagged_pixels"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -101,6 +101,8 @@ def load(path: str = LIB_PATH):
     lib.ts_profile.restype = ctypes.c_int
     lib.ts_stage_times.argtypes = [ctypes.c_void_p, P(ctypes.c_float), ctypes.c_int]
     lib.ts_stage_times.restype = ctypes.c_int
+    lib.ts_flagged_pixels.argtypes = [ctypes.c_void_p, P(ctypes.c_int64)]
+    lib.ts_flagged_pixels.restype = ctypes.c_int
     _LIB = lib
     return lib
 

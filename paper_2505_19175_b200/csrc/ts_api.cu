@@ -3,6 +3,16 @@
 //
 //   ts_forward  = render()          render.py:364-432
 //   ts_backward = render_backward() backward.py:93-211
+//
+// Pipeline per view (one stream):
+//   preprocess (project, cull, edges, bbox, colour, depth key)       1 kernel
+//   -- one host sync: M, E, depth-key range, non-finite indices --
+//   compaction of accepted triangles (range-reduced 32-bit depth key) 3 kernels
+//   onesweep radix sort on depth (+ exact tie-run fix)               <= 6 kernels
+//   rank offsets, tile duplication in depth-rank order               4 kernels
+//   onesweep radix sort on tile id (stable)                          <= 3 kernels
+//   tile ranges                                                      1 kernel
+//   blend (fast: fp32 + guard band, then exact fix-up; or exact fp64) 1-2 kernels
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -16,25 +26,28 @@ std::atomic<long long> g_launches{0};
 
 using namespace ts;
 
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
 struct ts_context {
     int device = 0;
-    // per-triangle scratch
+    // per-triangle scratch (capacity in triangles)
     long long cap_n = -1;
     void* tri_buf = nullptr;
-    Rec64* rec = nullptr;
     unsigned long long* key = nullptr;
     unsigned* tcount = nullptr;
     unsigned* flag = nullptr;
-    unsigned long long* keys_c = nullptr;
+    unsigned long long* keys_c = nullptr;  // also used as 2 x u32 key arrays
     unsigned* vals_c = nullptr;
     unsigned long long* keys_alt = nullptr;
     unsigned* vals_alt = nullptr;
     unsigned* offs = nullptr;
     int* rank_of = nullptr;
     double* depth = nullptr;
-    // backward scratch (lazy)
-    long long cap_sg = -1;
-    double* sgrad = nullptr;
+    short4* bbox = nullptr;
+    DevBuf rec64, recf, recb, sg64, sg32;
     // per-entry scratch
     long long cap_e = -1;
     void* ent_buf = nullptr;
@@ -43,7 +56,9 @@ struct ts_context {
     long long cap_p = -1, cap_tiles = -1;
     void* pix_buf = nullptr;
     double* t_final = nullptr;
+    float* t_final32 = nullptr;
     int* last_pos = nullptr;
+    int2* flags = nullptr;
     int* tile_start = nullptr;
     // sort scratch
     void* sort_buf = nullptr;
@@ -55,6 +70,8 @@ struct ts_context {
     Counters* h_ctr = nullptr;
     // last forward
     bool have_fwd = false;
+    bool have_bwd_state = false;
+    int precision = 0;
     Cam cam{};
     Opts opt{};
     ts_soup soup{};
@@ -62,18 +79,12 @@ struct ts_context {
     long long n = 0, m = 0, e = 0;
     const unsigned* sorted_src = nullptr;
     const unsigned* ent_src = nullptr;
+    int sgrad_kind = 0;  // 0 none, 1 fp64, 2 fp32
     // stage profiling
     bool profile = false;
     cudaEvent_t ev[TS_NUM_STAGES][2] = {};
     bool ev_used[TS_NUM_STAGES] = {};
 };
-
-static void stage_begin(ts_context* c, int s, cudaStream_t st) {
-    if (c->profile) { cudaEventRecord(c->ev[s][0], st); c->ev_used[s] = true; }
-}
-static void stage_end(ts_context* c, int s, cudaStream_t st) {
-    if (c->profile) cudaEventRecord(c->ev[s][1], st);
-}
 
 static int cuda_err(cudaError_t e) {
     if (e != cudaSuccess) {
@@ -82,34 +93,51 @@ static int cuda_err(cudaError_t e) {
     }
     return TS_OK;
 }
-#define TS_CHECK(x)                     \
-    do {                                \
-        int _rc = cuda_err((x));        \
-        if (_rc != TS_OK) return _rc;   \
+#define TS_CHECK(x)                   \
+    do {                              \
+        int _rc = cuda_err((x));      \
+        if (_rc != TS_OK) return _rc; \
     } while (0)
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static void stage_begin(ts_context* c, int s, cudaStream_t st) {
+    if (c->profile) {
+        cudaEventRecord(c->ev[s][0], st);
+        c->ev_used[s] = true;
+    }
+}
+static void stage_end(ts_context* c, int s, cudaStream_t st) {
+    if (c->profile) cudaEventRecord(c->ev[s][1], st);
+}
+
+static int ensure(DevBuf& b, size_t bytes) {
+    if (bytes <= b.bytes) return TS_OK;
+    size_t cap = bytes + bytes / 4 + 4096;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    TS_CHECK(cudaMalloc(&b.p, cap));
+    b.bytes = cap;
+    return TS_OK;
+}
 
 static int ensure_tri(ts_context* c, long long n) {
     if (n <= c->cap_n) return TS_OK;
     long long cap = n + n / 4 + 1024;
     if (c->tri_buf) cudaFree(c->tri_buf);
     c->tri_buf = nullptr;
-    size_t off = 0, sz;
-    size_t o_rec = off; sz = sizeof(Rec64) * cap; off = align_up(off + sz, 256);
-    size_t o_key = off; sz = 8 * cap; off = align_up(off + sz, 256);
-    size_t o_tc = off; sz = 4 * cap; off = align_up(off + sz, 256);
-    size_t o_fl = off; sz = 4 * cap; off = align_up(off + sz, 256);
-    size_t o_kc = off; sz = 8 * cap; off = align_up(off + sz, 256);
-    size_t o_vc = off; sz = 4 * cap; off = align_up(off + sz, 256);
-    size_t o_ka = off; sz = 8 * cap; off = align_up(off + sz, 256);
-    size_t o_va = off; sz = 4 * cap; off = align_up(off + sz, 256);
-    size_t o_of = off; sz = 4 * (cap + 1); off = align_up(off + sz, 256);
-    size_t o_rk = off; sz = 4 * cap; off = align_up(off + sz, 256);
-    size_t o_dp = off; sz = 8 * cap; off = align_up(off + sz, 256);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    size_t o_key = take(8 * cap), o_tc = take(4 * cap), o_fl = take(4 * cap), o_kc = take(8 * cap),
+           o_vc = take(4 * cap), o_ka = take(8 * cap), o_va = take(4 * cap), o_of = take(4 * (cap + 1)),
+           o_rk = take(4 * cap), o_dp = take(8 * cap), o_bb = take(8 * cap);
     TS_CHECK(cudaMalloc(&c->tri_buf, off));
     char* b = (char*)c->tri_buf;
-    c->rec = (Rec64*)(b + o_rec);
     c->key = (unsigned long long*)(b + o_key);
     c->tcount = (unsigned*)(b + o_tc);
     c->flag = (unsigned*)(b + o_fl);
@@ -120,6 +148,7 @@ static int ensure_tri(ts_context* c, long long n) {
     c->offs = (unsigned*)(b + o_of);
     c->rank_of = (int*)(b + o_rk);
     c->depth = (double*)(b + o_dp);
+    c->bbox = (short4*)(b + o_bb);
     c->cap_n = cap;
     return TS_OK;
 }
@@ -146,12 +175,20 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     c->pix_buf = nullptr;
     long long cp = p > c->cap_p ? p : c->cap_p;
     long long ct = ntiles > c->cap_tiles ? ntiles : c->cap_tiles;
-    size_t o_tf = 0, o_lp = align_up(8 * cp, 256), o_ts = o_lp + align_up(4 * cp, 256);
-    size_t tot = o_ts + align_up(4 * (ct + 1), 256);
-    TS_CHECK(cudaMalloc(&c->pix_buf, tot));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    size_t o_tf = take(8 * cp), o_t32 = take(4 * cp), o_lp = take(4 * cp), o_fg = take(8 * cp),
+           o_ts = take(4 * (ct + 1));
+    TS_CHECK(cudaMalloc(&c->pix_buf, off));
     char* b = (char*)c->pix_buf;
     c->t_final = (double*)(b + o_tf);
+    c->t_final32 = (float*)(b + o_t32);
     c->last_pos = (int*)(b + o_lp);
+    c->flags = (int2*)(b + o_fg);
     c->tile_start = (int*)(b + o_ts);
     c->cap_p = cp;
     c->cap_tiles = ct;
@@ -168,23 +205,18 @@ static int ensure_os(ts_context* c, long long count) {
     return TS_OK;
 }
 
-static int ensure_sg(ts_context* c, long long n) {
-    if (n <= c->cap_sg) return TS_OK;
-    long long cap = n + n / 4 + 1024;
-    if (c->sgrad) cudaFree(c->sgrad);
-    c->sgrad = nullptr;
-    TS_CHECK(cudaMalloc(&c->sgrad, sizeof(double) * SG_STRIDE * cap));
-    c->cap_sg = cap;
-    return TS_OK;
-}
-
 static void build_cam_opts(const ts_camera* cam, const ts_options* opt, Cam& c, Opts& o) {
-    c.fx = cam->fx; c.fy = cam->fy; c.cx = cam->cx; c.cy = cam->cy; c.z_near = cam->z_near;
+    c.fx = cam->fx;
+    c.fy = cam->fy;
+    c.cx = cam->cx;
+    c.cy = cam->cy;
+    c.z_near = cam->z_near;
     for (int k = 0; k < 9; k++) c.R[k] = cam->R[k];
     for (int k = 0; k < 3; k++) c.t[k] = cam->t[k];
     for (int b = 0; b < 3; b++)
         c.cc[b] = -(cam->R[0 * 3 + b] * cam->t[0] + cam->R[1 * 3 + b] * cam->t[1] + cam->R[2 * 3 + b] * cam->t[2]);
-    c.width = cam->width; c.height = cam->height;
+    c.width = cam->width;
+    c.height = cam->height;
     c.ntx = (cam->width + TILE - 1) / TILE;
     c.nty = (cam->height + TILE - 1) / TILE;
     o.mode = opt->mode;
@@ -201,7 +233,7 @@ static int bit_length(unsigned long long x) { return x ? 64 - __builtin_clzll(x)
 
 extern "C" {
 
-const char* ts_version(void) { return "trisplat_b200 0.1.0 (sm_100a)"; }
+const char* ts_version(void) { return "trisplat_b200 0.2.0 (sm_100a)"; }
 
 const char* ts_error_string(int code) {
     switch (code) {
@@ -213,6 +245,7 @@ const char* ts_error_string(int code) {
         case TS_ERR_NONFINITE: return "non-finite triangle parameters";
         case TS_ERR_TILE_SIZE: return "only tile_size=16 is supported";
         case TS_ERR_FRAGMENTS: return "fragment gradients do not match this scene/camera";
+        case TS_ERR_NO_BWD_STATE: return "the preceding ts_forward ran with keep_backward=0";
         default: return "unknown error";
     }
 }
@@ -225,12 +258,18 @@ int ts_context_create(ts_context** out, int device) {
     c->sort.max_blocks = 1184;  // 8 x 148 SMs
     size_t sb = sort_scratch_bytes(c->sort.max_blocks);
     int rc = cuda_err(cudaMalloc(&c->sort_buf, sb + 1024));
-    if (rc) { delete c; return rc; }
+    if (rc) {
+        delete c;
+        return rc;
+    }
     c->sort.hist = (unsigned*)c->sort_buf;
     c->sort.bsums = c->sort.hist + 256 * (size_t)c->sort.max_blocks + 32;
     rc = cuda_err(cudaMalloc(&c->d_ctr, sizeof(Counters)));
     if (!rc) rc = cuda_err(cudaMallocHost(&c->h_ctr, sizeof(Counters)));
-    if (rc) { delete c; return rc; }
+    if (rc) {
+        delete c;
+        return rc;
+    }
     *out = c;
     return TS_OK;
 }
@@ -240,13 +279,16 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->tri_buf);
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
-    cudaFree(c->sgrad);
+    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32}) cudaFree(b->p);
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
     cudaFree(c->d_ctr);
     cudaFreeHost(c->h_ctr);
     for (int k = 0; k < TS_NUM_STAGES; k++)
-        if (c->ev[k][0]) { cudaEventDestroy(c->ev[k][0]); cudaEventDestroy(c->ev[k][1]); }
+        if (c->ev[k][0]) {
+            cudaEventDestroy(c->ev[k][0]);
+            cudaEventDestroy(c->ev[k][1]);
+        }
     delete c;
     return TS_OK;
 }
@@ -282,20 +324,28 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     if (opt->tile_size != TILE) return TS_ERR_TILE_SIZE;
     if (cam->width < 1 || cam->height < 1 || soup->n < 0 || opt->sh_degree < 0 || opt->sh_degree > 3)
         return TS_ERR_INVALID_ARG;
-    if (soup->n >= (1ll << 31)) return TS_ERR_INVALID_ARG;
+    if (soup->n >= (1ll << 31) || cam->width > 32000 || cam->height > 32000) return TS_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     c->have_fwd = false;
+    c->have_bwd_state = false;
     for (int k = 0; k < TS_NUM_STAGES; k++) c->ev_used[k] = false;
     Cam cm;
     Opts op;
     build_cam_opts(cam, opt, cm, op);
+    const bool fast = opt->precision == 0;
     const long long n = soup->n;
     const long long P = (long long)cam->width * cam->height;
     const int ntiles = cm.ntx * cm.nty;
-    int rc = ensure_tri(c, n > 0 ? n : 1);
+    const long long n1 = n > 0 ? n : 1;
+    int rc = ensure_tri(c, n1);
     if (rc) return rc;
     if ((rc = ensure_pix(c, P, ntiles))) return rc;
-    // counters
+    if (fast) {
+        if ((rc = ensure(c->recf, sizeof(RecF) * n1))) return rc;
+        if (opt->keep_backward && (rc = ensure(c->recb, sizeof(RecB) * n1))) return rc;
+    } else {
+        if ((rc = ensure(c->rec64, sizeof(Rec64) * n1))) return rc;
+    }
     Counters init;
     memset(&init, 0, sizeof(init));
     init.key_and = ~0ull;
@@ -303,13 +353,19 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     for (int k = 0; k < 4; k++) init.err[k] = 0x7fffffffffffffffLL;
     *c->h_ctr = init;
     TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_ctr, sizeof(Counters), cudaMemcpyHostToDevice, st));
-    if (out->max_weight) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
-    if (out->pixel_count) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
-    PreOut po{c->rec, c->key, c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+    if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
+    if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
     stage_begin(c, TS_STAGE_PREPROCESS, st);
-    launch_preprocess(cm, op, *soup, opt->param_dtype, po, st);
+    if (fast) {
+        FastPreOut po{(RecF*)c->recf.p, opt->keep_backward ? (RecB*)c->recb.p : nullptr, c->bbox, c->key,
+                      c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+        launch_preprocess_fast(cm, op, *soup, opt->param_dtype, po, st);
+    } else {
+        PreOut po{(Rec64*)c->rec64.p, c->bbox, c->key, c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+        launch_preprocess(cm, op, *soup, opt->param_dtype, po, st);
+    }
     stage_end(c, TS_STAGE_PREPROCESS, st);
-    g_launches += 1;
+    g_launches += n > 0 ? 1 : 0;
     TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     TS_CHECK(cudaStreamSynchronize(st));
     TS_CHECK(cudaGetLastError());
@@ -326,10 +382,11 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     const long long m = (long long)h.m, e = (long long)h.e;
     if (e >= (1ll << 31)) return TS_ERR_INVALID_ARG;
     if ((rc = ensure_ent(c, e > 0 ? e : 1))) return rc;
+    if ((rc = ensure_os(c, (m > e ? m : e) + 1))) return rc;
+
     // depth order: compaction (source order) of range-reduced 32-bit depth
     // keys, stable onesweep radix sort, then exact (z64, idx) order restored
     // inside runs of equal reduced keys (np.lexsort((idx, z)), render.py:276)
-    if ((rc = ensure_os(c, (m > e ? m : e) + 1))) return rc;
     stage_begin(c, TS_STAGE_DEPTH_SORT, st);
     unsigned long long krange = m ? h.key_max - h.key_min : 0ull;
     int kbits = bit_length(krange);
@@ -338,7 +395,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     unsigned* k32 = (unsigned*)c->keys_c;
     unsigned* k32_alt = (unsigned*)c->keys_alt;
     compact_accepted32(n, c->flag, c->key, h.key_min, kshift, k32, c->vals_c, c->sort, st);
-    g_launches += 3;
+    g_launches += n > 0 ? 3 : 0;
     int par = onesweep_sort_u32(m, k32, c->vals_c, k32_alt, c->vals_alt, knb, c->os_buf, st);
     if (m > 1 && knb > 0) g_launches += 1 + (knb + 7) / 8;
     c->sorted_src = par ? c->vals_alt : c->vals_c;
@@ -347,27 +404,48 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         g_launches += 1;
     }
     stage_end(c, TS_STAGE_DEPTH_SORT, st);
+
+    // tile duplication in rank order + stable sort by tile id (render.py:315-361)
     stage_begin(c, TS_STAGE_BINNING, st);
-    // tile duplication in rank order + stable sort by tile id
     rank_offsets(m, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
-    duplicate_entries(m, c->sorted_src, c->rec, c->offs, cm.ntx, c->tkey, c->tval, st);
-    g_launches += 4;
+    duplicate_entries(m, c->sorted_src, c->bbox, c->offs, cm.ntx, c->tkey, c->tval, st);
+    g_launches += m > 0 ? 4 : 0;
     int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
     par = onesweep_sort_u32(e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits, c->os_buf, st);
     if (e > 1 && tbits > 0) g_launches += 1 + (tbits + 7) / 8;
     const unsigned* skey = par ? c->tkey_alt : c->tkey;
     c->ent_src = par ? c->tval_alt : c->tval;
     tile_ranges(e, skey, ntiles, c->tile_start, st);
+    g_launches += 1;
     stage_end(c, TS_STAGE_BINNING, st);
-    g_launches += 1;
-    BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
-                out->n_frag, c->t_final, c->last_pos};
-    stage_begin(c, TS_STAGE_BLEND, st);
-    launch_blend_exact(cm, op, c->rec, c->tile_start, (const int*)c->ent_src, bo, st);
-    stage_end(c, TS_STAGE_BLEND, st);
-    g_launches += 1;
+
+    if (fast) {
+        FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
+                        out->n_frag, c->t_final32, c->last_pos, c->flags, c->d_ctr};
+        stage_begin(c, TS_STAGE_BLEND, st);
+        launch_blend_fast(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
+                          bo, st, 0);
+        stage_end(c, TS_STAGE_BLEND, st);
+        stage_begin(c, TS_STAGE_FIXUP, st);
+        launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
+                         bo, st);
+        stage_end(c, TS_STAGE_FIXUP, st);
+        g_launches += 2;
+        // flagged-pixel count (read back asynchronously; valid after the stream syncs)
+        TS_CHECK(cudaMemcpyAsync(&c->h_ctr->n_flagged, &c->d_ctr->n_flagged, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+    } else {
+        BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
+                    out->n_frag, c->t_final, c->last_pos};
+        stage_begin(c, TS_STAGE_BLEND, st);
+        launch_blend_exact(cm, op, (const Rec64*)c->rec64.p, c->tile_start, (const int*)c->ent_src, bo, st);
+        stage_end(c, TS_STAGE_BLEND, st);
+        g_launches += 1;
+    }
     TS_CHECK(cudaGetLastError());
     c->have_fwd = true;
+    c->have_bwd_state = !fast || opt->keep_backward;
+    c->precision = opt->precision;
     c->cam = cm;
     c->opt = op;
     c->soup = *soup;
@@ -382,18 +460,37 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
                 void* stream) {
     if (!c || !d_image || !grads) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
     cudaStream_t st = (cudaStream_t)stream;
-    int rc = ensure_sg(c, c->n > 0 ? c->n : 1);
-    if (rc) return rc;
+    const long long n1 = c->n > 0 ? c->n : 1;
+    int rc;
     c->ev_used[TS_STAGE_BLEND_BWD] = c->ev_used[TS_STAGE_CHAIN_BWD] = false;
-    stage_begin(c, TS_STAGE_BLEND_BWD, st);
-    if (c->n > 0) TS_CHECK(cudaMemsetAsync(c->sgrad, 0, sizeof(double) * SG_STRIDE * c->n, st));
-    launch_blend_bwd_exact(c->cam, c->opt, c->rec, c->tile_start, (const int*)c->ent_src, c->t_final,
-                           c->last_pos, d_image, c->sgrad, st);
-    stage_end(c, TS_STAGE_BLEND_BWD, st);
-    stage_begin(c, TS_STAGE_CHAIN_BWD, st);
-    launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, c->sgrad, *grads, accumulate, st);
-    stage_end(c, TS_STAGE_CHAIN_BWD, st);
+    if (c->precision == 0) {
+        if ((rc = ensure(c->sg32, sizeof(float) * SG_STRIDE * n1))) return rc;
+        float* sg = (float*)c->sg32.p;
+        stage_begin(c, TS_STAGE_BLEND_BWD, st);
+        if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(float) * SG_STRIDE * c->n, st));
+        launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
+                              (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final32, c->last_pos,
+                              d_image, sg, st);
+        stage_end(c, TS_STAGE_BLEND_BWD, st);
+        stage_begin(c, TS_STAGE_CHAIN_BWD, st);
+        launch_chain_bwd32(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+        stage_end(c, TS_STAGE_CHAIN_BWD, st);
+        c->sgrad_kind = 2;
+    } else {
+        if ((rc = ensure(c->sg64, sizeof(double) * SG_STRIDE * n1))) return rc;
+        double* sg = (double*)c->sg64.p;
+        stage_begin(c, TS_STAGE_BLEND_BWD, st);
+        if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
+        launch_blend_bwd_exact(c->cam, c->opt, (const Rec64*)c->rec64.p, c->tile_start, (const int*)c->ent_src,
+                               c->t_final, c->last_pos, d_image, sg, st);
+        stage_end(c, TS_STAGE_BLEND_BWD, st);
+        stage_begin(c, TS_STAGE_CHAIN_BWD, st);
+        launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+        stage_end(c, TS_STAGE_CHAIN_BWD, st);
+        c->sgrad_kind = 1;
+    }
     g_launches += 2;
     TS_CHECK(cudaGetLastError());
     return TS_OK;
@@ -419,19 +516,41 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
             return cuda_err(cudaGetLastError());
         case TS_DUMP_BBOX:
             if (bytes < 16 * (size_t)c->n) return TS_ERR_INVALID_ARG;
-            bbox_dump(c->n, c->rec, c->flag, (int*)dst, st);
+            bbox_dump(c->n, c->bbox, (int*)dst, st);
             return cuda_err(cudaGetLastError());
         case TS_DUMP_DEPTH:
             if (bytes < 8 * (size_t)c->n) return TS_ERR_INVALID_ARG;
             if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->depth, 8 * c->n, cudaMemcpyDeviceToDevice, st));
             return TS_OK;
-        case TS_DUMP_SGRAD:
-            if (bytes < 8 * SG_STRIDE * (size_t)c->n || c->cap_sg < c->n) return TS_ERR_INVALID_ARG;
-            if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->sgrad, 8 * SG_STRIDE * c->n, cudaMemcpyDeviceToDevice, st));
+        case TS_DUMP_SGRAD: {
+            if (bytes < 8 * SG_STRIDE * (size_t)c->n || !c->sgrad_kind) return TS_ERR_INVALID_ARG;
+            if (!c->n) return TS_OK;
+            if (c->sgrad_kind == 1) {
+                TS_CHECK(cudaMemcpyAsync(dst, c->sg64.p, 8 * SG_STRIDE * c->n, cudaMemcpyDeviceToDevice, st));
+            } else {
+                // widen fp32 -> fp64 through a host bounce (debug only)
+                size_t cnt = (size_t)SG_STRIDE * c->n;
+                float* h32 = (float*)malloc(4 * cnt);
+                double* h64 = (double*)malloc(8 * cnt);
+                TS_CHECK(cudaMemcpyAsync(h32, c->sg32.p, 4 * cnt, cudaMemcpyDeviceToHost, st));
+                TS_CHECK(cudaStreamSynchronize(st));
+                for (size_t k = 0; k < cnt; k++) h64[k] = h32[k];
+                TS_CHECK(cudaMemcpyAsync(dst, h64, 8 * cnt, cudaMemcpyHostToDevice, st));
+                TS_CHECK(cudaStreamSynchronize(st));
+                free(h32);
+                free(h64);
+            }
             return TS_OK;
+        }
         default:
             return TS_ERR_INVALID_ARG;
     }
+}
+
+int ts_flagged_pixels(ts_context* c, int64_t* n_flagged) {
+    if (!c || !n_flagged) return TS_ERR_INVALID_ARG;
+    *n_flagged = (int64_t)c->h_ctr->n_flagged;
+    return TS_OK;
 }
 
 }  // extern "C"

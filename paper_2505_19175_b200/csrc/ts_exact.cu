@@ -46,10 +46,12 @@ __global__ void __launch_bounds__(256) k_preprocess(Cam cam, Opts opt, const T* 
         if (out.area) out.area[i] = p.valid_z ? (float)p.area : 0.0f;
         if (out.depth) out.depth[i] = p.z;
         ok = accepted(p);
+        short4 bb = make_short4(0, 0, 0, 0);
         if (ok) {
             double o = opt.solid ? 1.0 : o_raw;
             Edge64 E;
             edge_bbox64(p.q, p.phis, o, sg, opt.mode, opt.tau_cutoff, cam.width, cam.height, E);
+            bb = make_short4((short)E.bb[0], (short)E.bb[1], (short)E.bb[2], (short)E.bb[3]);
             Rec64 r;
 #pragma unroll
             for (int e = 0; e < 3; e++) {
@@ -88,6 +90,7 @@ __global__ void __launch_bounds__(256) k_preprocess(Cam cam, Opts opt, const T* 
             tcount = (unsigned)tiles_touched(r.bx0, r.bx1, r.by0, r.by1);
             key = (unsigned long long)__double_as_longlong(p.z);
         }
+        out.bbox[i] = bb;
         out.flag[i] = ok ? 1u : 0u;
         out.tcount[i] = tcount;
         out.key[i] = key;
@@ -374,11 +377,11 @@ void launch_blend_bwd_exact(const Cam& cam, const Opts& opt, const Rec64* rec, c
 // ---------------------------------------------------------------------------
 // k_chain_bwd: screen-space grads -> 59 parameter grads, one thread per source.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, typename G>
 __global__ void __launch_bounds__(128) k_chain_bwd(Cam cam, Opts opt, const T* __restrict__ verts,
                                                    const T* __restrict__ sh,
                                                    const unsigned* __restrict__ flag,
-                                                   const double* __restrict__ sgrad, long long n,
+                                                   const G* __restrict__ sgrad, long long n,
                                                    ts_grads grads, int accumulate) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(128) k_chain_bwd(Cam cam, Opts opt, const T* _
 #pragma unroll
     for (int k = 0; k < 48; k++) dsh[k] = 0.0;
     if (flag[i]) {
-        const double* sg = sgrad + (size_t)i * SG_STRIDE;
+        const G* sg = sgrad + (size_t)i * SG_STRIDE;
         double gq[6];
 #pragma unroll
         for (int k = 0; k < 6; k++) gq[k] = sg[SG_GQ + k];
@@ -503,20 +506,33 @@ __global__ void __launch_bounds__(128) k_chain_bwd(Cam cam, Opts opt, const T* _
     }
 }
 
-void launch_chain_bwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
-                      const unsigned* flag, const double* sgrad, const ts_grads& g, int accumulate,
-                      cudaStream_t st) {
+template <typename G>
+static void chain_impl(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                       const unsigned* flag, const G* sgrad, const ts_grads& g, int accumulate,
+                       cudaStream_t st) {
     long long n = soup.n;
     if (n <= 0) return;
     unsigned grid = (unsigned)((n + 127) / 128);
     if (dtype == 1)
-        k_chain_bwd<double><<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices,
-                                                  (const double*)soup.sh, flag, sgrad, n, g,
-                                                  accumulate);
+        k_chain_bwd<double, G><<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices,
+                                                     (const double*)soup.sh, flag, sgrad, n, g,
+                                                     accumulate);
     else
-        k_chain_bwd<float><<<grid, 128, 0, st>>>(cam, opt, (const float*)soup.vertices,
-                                                 (const float*)soup.sh, flag, sgrad, n, g,
-                                                 accumulate);
+        k_chain_bwd<float, G><<<grid, 128, 0, st>>>(cam, opt, (const float*)soup.vertices,
+                                                    (const float*)soup.sh, flag, sgrad, n, g,
+                                                    accumulate);
+}
+
+void launch_chain_bwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                      const unsigned* flag, const double* sgrad, const ts_grads& g, int accumulate,
+                      cudaStream_t st) {
+    chain_impl<double>(cam, opt, soup, dtype, flag, sgrad, g, accumulate, st);
+}
+
+void launch_chain_bwd32(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                        const unsigned* flag, const float* sgrad, const ts_grads& g, int accumulate,
+                        cudaStream_t st) {
+    chain_impl<float>(cam, opt, soup, dtype, flag, sgrad, g, accumulate, st);
 }
 
 }  // namespace ts

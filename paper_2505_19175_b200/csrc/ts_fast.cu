@@ -1,0 +1,673 @@
+// ts_fast.cu -- the fast (default) path: fp64 edge functions, fp32 alpha and
+// compositing, with a guard band around every discrete decision of the
+// reference compositor and an exact fp64 fix-up for the rare pixels whose
+// decision falls inside it.
+//
+//   k_preprocess_fast  render.py:159-190, 193-250, 271-273, 292-302 -> RecF/RecB
+//   k_blend_fast       _kernels.py:59-132 (decisions: skip alpha<1/255 :103,
+//                      T<1e-4 stop :121, pixel count w>1/255 :112)
+//   k_fixup_fwd        exact replay (same arithmetic as k_blend_exact) of flagged pixels
+//   k_blend_bwd_fast   _kernels.py:181-318 back to front from the saved last contributor
+//
+// Decision guard band.  r = phi/phi_s is evaluated in fp64 from fp64 edge
+// coefficients (error ~1e-12 vs the reference's fp64 phi/phi_s), so the skip
+// test r >= r* is exact outside the fp32-rounded band [r_lo, r_hi]; inside
+// it the decision is taken with the reference's fp64 arithmetic.  Alpha is
+// then computed in fp32 with a per-fragment relative error bound eps_a, and
+// the transmittance carries its accumulated relative error bound eps_T; a
+// T<1e-4 or w>1/255 test whose operands lie within their error bound of the
+// threshold flags the pixel, which stops here and is recomputed exactly by
+// k_fixup_fwd.
+#include "ts_kernels.cuh"
+
+namespace ts {
+
+constexpr float T_MIN_F = 1e-4f;
+constexpr float ALPHA_CLAMP_F = 0.99f;
+
+__device__ __forceinline__ float fast_lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// exact (oracle-arithmetic) record of one source triangle, recomputed from the
+// parameters -- used only for decisions that fall inside the guard band
+template <typename T>
+__device__ __noinline__ void exact_record(const Cam& cam, const Opts& opt, const T* __restrict__ verts,
+                                          const T* __restrict__ opacity, const T* __restrict__ sigma,
+                                          unsigned src, Rec64& r) {
+    double v[9];
+#pragma unroll
+    for (int k = 0; k < 9; k++) v[k] = (double)verts[(size_t)src * 9 + k];
+    Proj64 p;
+    project64(v, cam, p);
+    double o = opt.solid ? 1.0 : (double)opacity[src];
+    double sg = (double)sigma[src];
+    Edge64 E;
+    edge_bbox64(p.q, p.phis, o, sg, opt.mode, opt.tau_cutoff, cam.width, cam.height, E);
+#pragma unroll
+    for (int e = 0; e < 3; e++) {
+        r.nx[e] = E.nx[e];
+        r.ny[e] = E.ny[e];
+        r.d[e] = E.d[e];
+        r.qx[e] = p.q[e * 2];
+        r.qy[e] = p.q[e * 2 + 1];
+    }
+    r.phis = p.phis;
+    r.sig = sg;
+    r.opa = o;
+    r.esign = E.esign;
+}
+
+// ---------------------------------------------------------------------------
+// preprocess (fast records)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, const T* __restrict__ verts,
+                                                         const T* __restrict__ opacity,
+                                                         const T* __restrict__ sigma,
+                                                         const T* __restrict__ sh, long long n,
+                                                         FastPreOut out) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = false;
+    unsigned long long key = 0;
+    unsigned tcount = 0;
+    if (i < n) {
+        double v[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) v[k] = (double)verts[i * 9 + k];
+        double o_raw = (double)opacity[i];
+        double sg = (double)sigma[i];
+        if (opt.validate) {
+            bool fv = true;
+#pragma unroll
+            for (int k = 0; k < 9; k++) fv &= isfinite(v[k]);
+            if (!fv) atomicMin(&out.ctr->err[0], i);
+            if (!isfinite(o_raw)) atomicMin(&out.ctr->err[1], i);
+            if (!isfinite(sg)) atomicMin(&out.ctr->err[2], i);
+            bool fs = true;
+            const T* shp = sh + i * 48;
+#pragma unroll 8
+            for (int k = 0; k < 48; k++) fs &= isfinite((double)shp[k]);
+            if (!fs) atomicMin(&out.ctr->err[3], i);
+        }
+        Proj64 p;
+        project64(v, cam, p);
+        if (out.area) out.area[i] = p.valid_z ? (float)p.area : 0.0f;
+        if (out.depth) out.depth[i] = p.z;
+        ok = accepted(p);
+        short4 bb = make_short4(0, 0, 0, 0);
+        if (ok) {
+            double o = opt.solid ? 1.0 : o_raw;
+            Edge64 E;
+            edge_bbox64(p.q, p.phis, o, sg, opt.mode, opt.tau_cutoff, cam.width, cam.height, E);
+            int x0 = (int)E.bb[0], x1 = (int)E.bb[1], y0 = (int)E.bb[2], y1 = (int)E.bb[3];
+            bb = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
+            tcount = (unsigned)tiles_touched(x0, x1, y0, y1);
+            if (tcount) {
+                RecF r;
+                int ox = (x0 + x1) >> 1, oy = (y0 + y1) >> 1;
+                double inv = 1.0 / p.phis;
+                double dmax = 0.0;
+#pragma unroll
+                for (int e = 0; e < 3; e++) {
+                    r.a[e * 3 + 0] = E.nx[e] * inv;
+                    r.a[e * 3 + 1] = E.ny[e] * inv;
+                    double de = E.nx[e] * (double)ox + E.ny[e] * (double)oy + E.d[e];
+                    r.a[e * 3 + 2] = de * inv;
+                    dmax = fmax(dmax, fabs(E.d[e]));
+                }
+                // |r_fast - r_ref| bound: both are O(1e-16) x (sum of |terms| / |phi_s|)
+                double mag = (fabs(p.q[0]) + fabs(p.q[1]) + fabs(p.q[2]) + fabs(p.q[3]) + fabs(p.q[4]) +
+                              fabs(p.q[5]) + 4.0 * (cam.width + cam.height) + dmax) / fabs(p.phis);
+                double delta = 1e-13 * mag + 1e-300;
+                double rstar;  // contribution threshold on r (alpha >= 1/255)
+                if (opt.mode == 0) {
+                    rstar = o > ALPHA_MIN ? pow(ALPHA_MIN / o, 1.0 / sg) : 1e30;
+                    if (rstar > 1.0) rstar = 1e30;
+                    r.f0 = (float)sg;
+                    r.f1 = (float)log2(o);
+                } else {
+                    double q = 255.0 * o - 1.0;
+                    rstar = q > 0.0 ? sg * log(q) / p.phis : 1e30;
+                    r.f0 = (float)(p.phis * 1.4426950408889634 / sg);
+                    r.f1 = (float)o;
+                }
+                double rlo = rstar - delta - fabs(rstar) * 1e-12, rhi = rstar + delta + fabs(rstar) * 1e-12;
+                r.r_lo = __double2float_rd(rlo);
+                r.r_hi = __double2float_ru(rhi);
+                // view-dependent colour, render.py:292-302
+                double u[3];
+#pragma unroll
+                for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) / 3.0 - cam.cc[b];
+                double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+                un = un > 1e-12 ? un : 1e-12;
+                double basis[16];
+                sh_basis16(u[0] / un, u[1] / un, u[2] / un, basis);
+                const T* shp = sh + i * 48;
+                double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+                for (int c = 0; c < opt.ncoef; c++) {
+                    acc0 += basis[c] * (double)shp[c * 3 + 0];
+                    acc1 += basis[c] * (double)shp[c * 3 + 1];
+                    acc2 += basis[c] * (double)shp[c * 3 + 2];
+                }
+                r.rgb[0] = (float)fmin(fmax(acc0 + 0.5, 0.0), 1.0);
+                r.rgb[1] = (float)fmin(fmax(acc1 + 0.5, 0.0), 1.0);
+                r.rgb[2] = (float)fmin(fmax(acc2 + 0.5, 0.0), 1.0);
+                r.x0 = (short)x0; r.x1 = (short)x1; r.y0 = (short)y0; r.y1 = (short)y1;
+                r.ox = (short)ox; r.oy = (short)oy;
+                out.rec[i] = r;
+                if (out.recb) {
+                    RecB b;
+#pragma unroll
+                    for (int e = 0; e < 3; e++) {
+                        b.qx[e] = (float)(p.q[e * 2] - ox);
+                        b.qy[e] = (float)(p.q[e * 2 + 1] - oy);
+                    }
+                    b.phis = (float)p.phis;
+                    b.opa = (float)o;
+                    b.sig = (float)sg;
+                    b.esign = E.esign;
+                    b.pad[0] = b.pad[1] = 0.f;
+                    out.recb[i] = b;
+                }
+            }
+            key = (unsigned long long)__double_as_longlong(p.z);
+        }
+        out.bbox[i] = bb;
+        out.flag[i] = ok ? 1u : 0u;
+        out.tcount[i] = tcount;
+        out.key[i] = key;
+    }
+    unsigned long long kmin = ok ? key : ~0ull, kmax = ok ? key : 0ull;
+    unsigned cnt = ok ? 1u : 0u;
+    unsigned long long tc = tcount;
+    for (int off = 16; off > 0; off >>= 1) {
+        unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, off);
+        unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, off);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        tc += __shfl_xor_sync(0xffffffffu, tc, off);
+    }
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicMin(&out.ctr->key_min, kmin);
+        atomicMax(&out.ctr->key_max, kmax);
+        atomicAdd(&out.ctr->m, (unsigned long long)cnt);
+        atomicAdd(&out.ctr->e, tc);
+    }
+}
+
+void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                            const FastPreOut& out, cudaStream_t st) {
+    long long n = soup.n;
+    if (n <= 0) return;
+    unsigned grid = (unsigned)((n + 255) / 256);
+    if (dtype == 1)
+        k_preprocess_fast<double><<<grid, 256, 0, st>>>(cam, opt, (const double*)soup.vertices,
+                                                        (const double*)soup.opacity,
+                                                        (const double*)soup.sigma,
+                                                        (const double*)soup.sh, n, out);
+    else
+        k_preprocess_fast<float><<<grid, 256, 0, st>>>(cam, opt, (const float*)soup.vertices,
+                                                       (const float*)soup.opacity,
+                                                       (const float*)soup.sigma,
+                                                       (const float*)soup.sh, n, out);
+}
+
+// ---------------------------------------------------------------------------
+// shared per-fragment evaluation
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double edge_r(const RecF& r, double dx, double dy, int& arg) {
+    double l0 = fma(r.a[0], dx, fma(r.a[1], dy, r.a[2]));
+    double l1 = fma(r.a[3], dx, fma(r.a[4], dy, r.a[5]));
+    double l2 = fma(r.a[6], dx, fma(r.a[7], dy, r.a[8]));
+    // argmax of phi = argmin of phi/phi_s (phi_s < 0); ties -> lowest edge (strict >, _kernels.py:36-42)
+    double m = l0;
+    arg = 0;
+    if (l1 < m) { m = l1; arg = 1; }
+    if (l2 < m) { m = l2; arg = 2; }
+    return m;
+}
+
+__device__ __forceinline__ double edge_r(const RecF& r, double dx, double dy) {
+    double l0 = fma(r.a[0], dx, fma(r.a[1], dy, r.a[2]));
+    double l1 = fma(r.a[3], dx, fma(r.a[4], dy, r.a[5]));
+    double l2 = fma(r.a[6], dx, fma(r.a[7], dy, r.a[8]));
+    return fmin(l0, fmin(l1, l2));
+}
+
+// fp32 alpha (unclamped) and its relative error bound, given r above the band
+__device__ __forceinline__ float alpha_fast(const RecF& r, double rr, int mode, float& eps) {
+    if (mode == 0) {
+        float rf = (float)fmin(rr, 1.0);
+        float lg = fast_lg2(rf);
+        float arg = fmaf(r.f0, lg, r.f1);
+        float a = fast_ex2(arg);
+        eps = 5e-7f + r.f0 * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
+        return a;
+    } else {
+        float x = (float)rr * r.f0;  // phi/sigma * log2(e)
+        float ex = fast_ex2(fminf(x, 1009.9f));
+        float a = __fdividef(r.f1, 1.0f + ex);
+        eps = 8e-7f + 1.2e-7f * fabsf(x);
+        return a;
+    }
+}
+
+// exact alpha with the reference arithmetic (fragment_alpha64 on a recomputed record)
+template <typename T>
+__device__ double alpha_exact(const Cam& cam, const Opts& opt, const T* verts, const T* opacity,
+                              const T* sigma, unsigned src, int px, int py, double& rr, double& phi,
+                              int& edge) {
+    Rec64 r;
+    exact_record<T>(cam, opt, verts, opacity, sigma, src, r);
+    return fragment_alpha64(px + 0.5, py + 0.5, r, opt.mode, rr, phi, edge);
+}
+
+// ---------------------------------------------------------------------------
+// k_blend_fast: CTA per 16x16 tile, warp = two pixel rows, fp32 compositing.
+// ---------------------------------------------------------------------------
+constexpr int FB = 64;
+
+__global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
+                                                    const int* __restrict__ tile_start,
+                                                    const unsigned* __restrict__ ent_src,
+                                                    FastBlendOut out) {
+    __shared__ RecF s_rec[FB];
+    __shared__ unsigned s_src[FB];
+    __shared__ unsigned s_maxw[FB];
+    __shared__ int s_pix[FB];
+    const int t = blockIdx.x;
+    const int tx = t % cam.ntx, ty = t / cam.ntx;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int px = tx * TILE + (lane & 15);
+    const int py = ty * TILE + 2 * warp + (lane >> 4);
+    const int wy0 = ty * TILE + 2 * warp;
+    const bool inside = px < cam.width && py < cam.height;
+    float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
+    int last = -1, cnt = 0, flag_pos = -1;
+    bool done = !inside;
+    const int s = tile_start[t], e = tile_start[t + 1];
+    const float tau = (float)opt.tau_contrib;
+    if (threadIdx.x < FB) { s_maxw[threadIdx.x] = 0u; s_pix[threadIdx.x] = 0; }
+    for (int b = s; b < e; b += FB) {
+        if (__syncthreads_count(!done) == 0) break;
+        const int nb = min(FB, e - b);
+        for (int c = threadIdx.x; c < nb * 7; c += blockDim.x) {
+            int j = c / 7, q = c - j * 7;
+            unsigned src = __ldg(ent_src + b + j);
+            if (q == 0) s_src[j] = src;
+            reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
+        }
+        __syncthreads();
+        for (int jb = 0; jb < nb; jb += 32) {
+            int jl = jb + (int)lane;
+            bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
+            unsigned mask = __ballot_sync(0xffffffffu, ov);
+            while (mask) {
+                const int j = jb + __ffs(mask) - 1;
+                mask &= mask - 1;
+                const RecF& r = s_rec[j];
+                bool contrib = false;
+                float w = 0.f;
+                if (!done && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
+                    double dx = (double)(px - r.ox) + 0.5, dy = (double)(py - r.oy) + 0.5;
+                    double rr = edge_r(r, dx, dy);
+                    if (rr >= (double)r.r_lo) {
+                        bool flag = rr <= (double)r.r_hi;
+                        if (!flag) {
+                            float ea;
+                            float a = alpha_fast(r, rr, opt.mode, ea);
+                            a = fminf(a, ALPHA_CLAMP_F);
+                            w = T * a;
+                            float tn = T * (1.f - a);
+                            float en = epsT + ea * a / (1.f - a) + 2.4e-7f;
+                            float ew = epsT + ea + 1.2e-7f;
+                            flag = fabsf(tn - T_MIN_F) <= 2.f * en * tn + 1e-11f ||
+                                   fabsf(w - tau) <= 2.f * ew * w + 1e-9f;
+                            if (!flag) {
+                                C0 = fmaf(w, r.rgb[0], C0);
+                                C1 = fmaf(w, r.rgb[1], C1);
+                                C2 = fmaf(w, r.rgb[2], C2);
+                                contrib = true;
+                                last = b + j;
+                                cnt++;
+                                T = tn;
+                                epsT = en;
+                                if (T < T_MIN_F) done = true;
+                            }
+                        }
+                        if (flag) {
+                            flag_pos = b + j;
+                            done = true;
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, contrib)) {
+                    unsigned mx = __reduce_max_sync(0xffffffffu, contrib ? __float_as_uint(w) : 0u);
+                    unsigned pc = __popc(__ballot_sync(0xffffffffu, contrib && w > tau));
+                    if (lane == 0) {
+                        atomicMax(&s_maxw[j], mx);
+                        if (pc) atomicAdd(&s_pix[j], (int)pc);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < nb) {
+            unsigned src = s_src[threadIdx.x];
+            if (s_maxw[threadIdx.x] && out.max_weight)
+                atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
+            if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
+            s_maxw[threadIdx.x] = 0u;
+            s_pix[threadIdx.x] = 0;
+        }
+    }
+    if (inside) {
+        const int p = py * cam.width + px;
+        if (flag_pos >= 0) {
+            unsigned long long k = atomicAdd(&out.ctr->n_flagged, 1ull);
+            out.flags[k] = make_int2(p, flag_pos);
+        } else {
+            if (out.image) {
+                out.image[p * 3 + 0] = fminf(fmaxf(fmaf(T, (float)opt.bg[0], C0), 0.f), 1.f);
+                out.image[p * 3 + 1] = fminf(fmaxf(fmaf(T, (float)opt.bg[1], C1), 0.f), 1.f);
+                out.image[p * 3 + 2] = fminf(fmaxf(fmaf(T, (float)opt.bg[2], C2), 0.f), 1.f);
+            }
+            if (out.alpha_map) out.alpha_map[p] = 1.f - T;
+            out.t_final[p] = T;
+            out.last_pos[p] = last;
+            if (out.n_frag) out.n_frag[p] = cnt;
+            if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_fixup_fwd: exact per-pixel replay of flagged pixels (reference arithmetic).
+// Entries before the flag position already committed their statistics in
+// k_blend_fast (their decisions were certain); from the flag position on the
+// fix-up commits them.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(64) k_fixup_fwd(Cam cam, Opts opt, const T* __restrict__ verts,
+                                                  const T* __restrict__ opacity, const T* __restrict__ sigma,
+                                                  const RecF* __restrict__ rec, const int* __restrict__ tile_start,
+                                                  const unsigned* __restrict__ ent_src, FastBlendOut out) {
+    const unsigned long long nflag = out.ctr->n_flagged;
+    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < nflag;
+         k += (unsigned long long)gridDim.x * blockDim.x) {
+        const int2 f = out.flags[k];
+        const int p = f.x, fpos = f.y;
+        const int px = p % cam.width, py = p / cam.width;
+        const int t = (py / TILE) * cam.ntx + px / TILE;
+        double Tt = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
+        int last = -1, cnt = 0;
+        const int s = tile_start[t], e = tile_start[t + 1];
+        for (int pos = s; pos < e; pos++) {
+            const unsigned src = ent_src[pos];
+            const RecF& r = rec[src];
+            if (px < r.x0 || px >= r.x1 || py < r.y0 || py >= r.y1) continue;
+            double rr, phi;
+            int edge;
+            double alpha = alpha_exact<T>(cam, opt, verts, opacity, sigma, src, px, py, rr, phi, edge);
+            if (alpha > ALPHA_CLAMP) alpha = ALPHA_CLAMP;
+            if (alpha < ALPHA_MIN) continue;
+            double w = Tt * alpha;
+            C0 += w * r.rgb[0];
+            C1 += w * r.rgb[1];
+            C2 += w * r.rgb[2];
+            if (pos >= fpos) {
+                if (out.max_weight) atomicMax((unsigned*)out.max_weight + src, __float_as_uint((float)w));
+                if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + src, 1);
+            }
+            last = pos;
+            cnt++;
+            Tt = TS_M(Tt, TS_S(1.0, alpha));
+            if (Tt < T_MIN) break;
+        }
+        if (out.image) {
+            out.image[p * 3 + 0] = (float)fmin(fmax(C0 + Tt * opt.bg[0], 0.0), 1.0);
+            out.image[p * 3 + 1] = (float)fmin(fmax(C1 + Tt * opt.bg[1], 0.0), 1.0);
+            out.image[p * 3 + 2] = (float)fmin(fmax(C2 + Tt * opt.bg[2], 0.0), 1.0);
+        }
+        if (out.alpha_map) out.alpha_map[p] = (float)(1.0 - Tt);
+        out.t_final[p] = (float)Tt;
+        out.last_pos[p] = last;
+        if (out.n_frag) out.n_frag[p] = cnt;
+        if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
+    }
+}
+
+void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                       cudaStream_t st, int stage_fixup_marker) {
+    (void)stage_fixup_marker;
+    int ntiles = cam.ntx * cam.nty;
+    k_blend_fast<<<ntiles, 256, 0, st>>>(cam, opt, rec, tile_start, ent_src, out);
+}
+
+void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                      const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                      cudaStream_t st) {
+    const int grid = 148 * 2;
+    if (dtype == 1)
+        k_fixup_fwd<double><<<grid, 64, 0, st>>>(cam, opt, (const double*)soup.vertices,
+                                                 (const double*)soup.opacity, (const double*)soup.sigma,
+                                                 rec, tile_start, ent_src, out);
+    else
+        k_fixup_fwd<float><<<grid, 64, 0, st>>>(cam, opt, (const float*)soup.vertices,
+                                                (const float*)soup.opacity, (const float*)soup.sigma,
+                                                rec, tile_start, ent_src, out);
+}
+
+// ---------------------------------------------------------------------------
+// k_blend_bwd_fast: back to front from the saved last contributor, fp32
+// gradients, warp-reduced before fp32 atomics into the per-source buffer.
+// Decisions inside the guard band (skip, clamp) and near-tied argmax edges
+// are resolved with the reference fp64 arithmetic.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const T* __restrict__ verts,
+                                                        const T* __restrict__ opacity,
+                                                        const T* __restrict__ sigma,
+                                                        const RecF* __restrict__ rec,
+                                                        const RecB* __restrict__ recb,
+                                                        const int* __restrict__ tile_start,
+                                                        const unsigned* __restrict__ ent_src,
+                                                        const float* __restrict__ t_final,
+                                                        const int* __restrict__ last_pos,
+                                                        const float* __restrict__ d_image,
+                                                        float* __restrict__ sgrad) {
+    __shared__ RecF s_rec[FB];
+    __shared__ RecB s_rb[FB];
+    __shared__ unsigned s_src[FB];
+    __shared__ int s_hi;
+    const int t = blockIdx.x;
+    const int tx = t % cam.ntx, ty = t / cam.ntx;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int px = tx * TILE + (lane & 15);
+    const int py = ty * TILE + 2 * warp + (lane >> 4);
+    const int wy0 = ty * TILE + 2 * warp;
+    const bool inside = px < cam.width && py < cam.height;
+    const int s = tile_start[t];
+    int my_last = -1;
+    float Tc = 1.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
+    if (inside) {
+        const int p = py * cam.width + px;
+        my_last = last_pos[p];
+        Tc = t_final[p];
+        d0 = d_image[p * 3 + 0];
+        d1 = d_image[p * 3 + 1];
+        d2 = d_image[p * 3 + 2];
+    }
+    float S0 = Tc * (float)opt.bg[0], S1 = Tc * (float)opt.bg[1], S2 = Tc * (float)opt.bg[2];
+    if (threadIdx.x == 0) s_hi = -1;
+    __syncthreads();
+    if (my_last >= 0) atomicMax(&s_hi, my_last);
+    __syncthreads();
+    const int hi = s_hi;
+    const float fpx = (float)(px) + 0.5f, fpy = (float)(py) + 0.5f;
+    for (int bend = hi + 1; bend > s; bend -= FB) {
+        const int bstart = max(s, bend - FB);
+        const int nb = bend - bstart;
+        __syncthreads();
+        for (int c = threadIdx.x; c < nb * 10; c += blockDim.x) {
+            int j = c / 10, q = c - j * 10;
+            unsigned src = __ldg(ent_src + bstart + j);
+            if (q == 0) s_src[j] = src;
+            if (q < 7)
+                reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
+            else
+                reinterpret_cast<float4*>(&s_rb[j])[q - 7] = __ldg(reinterpret_cast<const float4*>(recb + src) + (q - 7));
+        }
+        __syncthreads();
+        for (int jb = ((nb - 1) / 32) * 32; jb >= 0; jb -= 32) {
+            int jl = jb + (int)lane;
+            bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
+            unsigned mask = __ballot_sync(0xffffffffu, ov);
+            while (mask) {
+                const int j = jb + 31 - __clz(mask);
+                mask &= ~(1u << (j - jb));
+                const RecF& r = s_rec[j];
+                const int pos = bstart + j;
+                float g[12];
+#pragma unroll
+                for (int k = 0; k < 12; k++) g[k] = 0.f;
+                bool act = false;
+                if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
+                    const RecB& rb = s_rb[j];
+                    double dx = (double)(px - r.ox) + 0.5, dy = (double)(py - r.oy) + 0.5;
+                    int edge;
+                    double rr = edge_r(r, dx, dy, edge);
+                    bool contributes = rr > (double)r.r_hi;
+                    float alpha = 0.f;
+                    bool clamped = false, exact_done = false;
+                    if (!contributes && rr >= (double)r.r_lo) {
+                        double er, ephi;
+                        int eedge;
+                        double ae = alpha_exact<T>(cam, opt, verts, opacity, sigma, s_src[j], px, py, er, ephi, eedge);
+                        clamped = ae > ALPHA_CLAMP;
+                        if (clamped) ae = ALPHA_CLAMP;
+                        contributes = ae >= ALPHA_MIN;
+                        alpha = (float)ae;
+                        exact_done = true;
+                    }
+                    if (contributes) {
+                        if (!exact_done) {
+                            float ea;
+                            alpha = alpha_fast(r, rr, opt.mode, ea);
+                            if (fabsf(alpha - ALPHA_CLAMP_F) <= 2.f * ea * alpha + 1e-7f) {
+                                double er, ephi;
+                                int eedge;
+                                double ae = alpha_exact<T>(cam, opt, verts, opacity, sigma, s_src[j], px, py, er, ephi, eedge);
+                                clamped = ae > ALPHA_CLAMP;
+                                alpha = clamped ? ALPHA_CLAMP_F : (float)ae;
+                            } else {
+                                clamped = alpha > ALPHA_CLAMP_F;
+                                if (clamped) alpha = ALPHA_CLAMP_F;
+                            }
+                        }
+                        act = true;
+                        const float one_m = 1.f - alpha;
+                        const float tb = Tc / one_m;
+                        const float w = tb * alpha;
+                        const float* c = r.rgb;
+                        g[SG_GRGB + 0] = w * d0;
+                        g[SG_GRGB + 1] = w * d1;
+                        g[SG_GRGB + 2] = w * d2;
+                        const float inv1m = 1.f / one_m;
+                        float ga = d0 * (tb * c[0] - S0 * inv1m) + d1 * (tb * c[1] - S1 * inv1m) +
+                                   d2 * (tb * c[2] - S2 * inv1m);
+                        S0 = fmaf(w, c[0], S0);
+                        S1 = fmaf(w, c[1], S1);
+                        S2 = fmaf(w, c[2], S2);
+                        Tc = tb;
+                        if (!clamped) {
+                            const float o = rb.opa, sg = rb.sig, phis = rb.phis;
+                            g[SG_GO] = ga * (alpha / o);
+                            const float g_win = o * ga;
+                            const float window = alpha / o;
+                            const float rf = (float)rr;
+                            const float phi = rf * phis;
+                            float g_phi;
+                            if (opt.mode == 0) {
+                                const float rc = fminf(rf, 1.f);
+                                g[SG_GSIG] = g_win * window * __logf(rc);
+                                const float g_r = g_win * sg * window / rc;
+                                if (rr >= 1.0) {
+                                    g_phi = 0.f;
+                                } else {
+                                    g_phi = g_r / phis;
+                                    g[SG_GPHIS] = -g_r * rf / phis;
+                                }
+                            } else {
+                                g[SG_GSIG] = g_win * window * (1.f - window) * phi / (sg * sg);
+                                g_phi = -g_win * window * (1.f - window) / sg;
+                            }
+                            // edge line L = s*(n.p)... derivative wrt its endpoints (_kernels.py:296-318)
+                            const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
+                            const float ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
+                            const float pxr = (float)dx, pyr = (float)dy;
+                            const float ex = bx - ax, ey = by - ay;
+                            const float inv_l = rsqrtf(ex * ex + ey * ey);
+                            const float inv_l2 = inv_l * inv_l;
+                            const float sgn = ((rb.esign >> edge) & 1) ? -1.f : 1.f;
+                            const float gax = sgn * (pyr - by) * inv_l - phi * (ax - bx) * inv_l2;
+                            const float gay = sgn * (bx - pxr) * inv_l - phi * (ay - by) * inv_l2;
+                            const float gbx = sgn * (ay - pyr) * inv_l - phi * (bx - ax) * inv_l2;
+                            const float gby = sgn * (pxr - ax) * inv_l - phi * (by - ay) * inv_l2;
+                            g[SG_GQ + ia * 2] = g_phi * gax;
+                            g[SG_GQ + ia * 2 + 1] = g_phi * gay;
+                            g[SG_GQ + ib * 2] = g_phi * gbx;
+                            g[SG_GQ + ib * 2 + 1] = g_phi * gby;
+                        }
+                    }
+                }
+                if (__any_sync(0xffffffffu, act)) {
+#pragma unroll
+                    for (int k = 0; k < 12; k++) {
+                        float v = g[k];
+#pragma unroll
+                        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                        g[k] = v;
+                    }
+                    if (lane < 12) {
+                        float v = g[0];
+#pragma unroll
+                        for (int k = 1; k < 12; k++) v = (lane == (unsigned)k) ? g[k] : v;
+                        if (v != 0.f) atomicAdd(sgrad + (size_t)s_src[j] * SG_STRIDE + lane, v);
+                    }
+                }
+            }
+        }
+    }
+    (void)fpx;
+    (void)fpy;
+}
+
+void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                           const RecB* recb, const int* tile_start, const unsigned* ent_src,
+                           const float* t_final, const int* last_pos, const float* d_image, float* sgrad,
+                           cudaStream_t st) {
+    int ntiles = cam.ntx * cam.nty;
+    if (dtype == 1)
+        k_blend_bwd_fast<double><<<ntiles, 256, 0, st>>>(cam, opt, (const double*)soup.vertices,
+                                                         (const double*)soup.opacity,
+                                                         (const double*)soup.sigma, rec, recb, tile_start,
+                                                         ent_src, t_final, last_pos, d_image, sgrad);
+    else
+        k_blend_bwd_fast<float><<<ntiles, 256, 0, st>>>(cam, opt, (const float*)soup.vertices,
+                                                        (const float*)soup.opacity,
+                                                        (const float*)soup.sigma, rec, recb, tile_start,
+                                                        ent_src, t_final, last_pos, d_image, sgrad);
+}
+
+}  // namespace ts

@@ -18,11 +18,37 @@ struct Counters {
 
 struct PreOut {
     Rec64* rec;                // (N) fp64 records (accepted only)
+    short4* bbox;              // (N) clipped pixel bbox (0s if culled)
     unsigned long long* key;   // (N) depth bits
     unsigned* tcount;          // (N) tiles touched
     unsigned* flag;            // (N) accepted
     float* area;               // (N) per_triangle_area, nullable
     double* depth;             // (N) centroid depth, nullable
+    Counters* ctr;
+};
+
+struct FastPreOut {
+    RecF* rec;                 // (N) fast records (accepted with tiles only)
+    RecB* recb;                // (N) backward records, nullable
+    short4* bbox;              // (N)
+    unsigned long long* key;
+    unsigned* tcount;
+    unsigned* flag;
+    float* area;
+    double* depth;
+    Counters* ctr;
+};
+
+struct FastBlendOut {
+    float* image;
+    float* alpha_map;
+    float* max_weight;
+    int* pixel_count;
+    int* last_src;
+    int* n_frag;
+    float* t_final;
+    int* last_pos;
+    int2* flags;               // (pixel, flag position) of guard-band pixels
     Counters* ctr;
 };
 
@@ -48,6 +74,23 @@ void launch_blend_bwd_exact(const Cam& cam, const Opts& opt, const Rec64* rec, c
 void launch_chain_bwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
                       const unsigned* flag, const double* sgrad, const ts_grads& g, int accumulate,
                       cudaStream_t st);
+void launch_chain_bwd32(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                        const unsigned* flag, const float* sgrad, const ts_grads& g, int accumulate,
+                        cudaStream_t st);
+
+// ts_fast.cu
+void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                            const FastPreOut& out, cudaStream_t st);
+void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                       cudaStream_t st, int stage_fixup_marker);
+void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                      const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                      cudaStream_t st);
+void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                           const RecB* recb, const int* tile_start, const unsigned* ent_src,
+                           const float* t_final, const int* last_pos, const float* d_image, float* sgrad,
+                           cudaStream_t st);
 
 // ts_sort.cu
 struct SortScratch {
@@ -74,14 +117,14 @@ int radix_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* ke
 void rank_offsets(long long m, const unsigned* sorted_src, const unsigned* tcount, unsigned* offs,
                   int* rank_of, const SortScratch& s, cudaStream_t st);
 // tile duplication in depth-rank order: tkey = tile id, tval = source id
-void duplicate_entries(long long m, const unsigned* sorted_src, const Rec64* rec, const unsigned* offs,
+void duplicate_entries(long long m, const unsigned* sorted_src, const short4* bbox, const unsigned* offs,
                        int ntx, unsigned* tkey, unsigned* tval, cudaStream_t st);
 // tile_start[t] = first entry of tile t (CSR), tile_start[ntiles] = E
 void tile_ranges(long long e, const unsigned* tkey, int ntiles, int* tile_start, cudaStream_t st);
 // entry_rank[pos] = rank_of[ent_src[pos]]
 void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out,
                      cudaStream_t st);
-void bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out, cudaStream_t st);
+void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st);
 
 // onesweep radix sort (32-bit keys), scratch from onesweep_scratch_bytes
 size_t onesweep_scratch_bytes(long long max_count, int max_passes);

@@ -265,14 +265,14 @@ int radix_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* ke
 
 // ---------------- duplication / ranges ----------------
 __global__ void __launch_bounds__(256) k_duplicate(long long m, const unsigned* __restrict__ sorted_src,
-                                                   const Rec64* __restrict__ rec, const unsigned* __restrict__ offs,
+                                                   const short4* __restrict__ bbox, const unsigned* __restrict__ offs,
                                                    int ntx, unsigned* __restrict__ tkey,
                                                    unsigned* __restrict__ tval) {
     long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     unsigned src = sorted_src[k];
-    const Rec64& r = rec[src];
-    int x0 = r.bx0, x1 = r.bx1, y0 = r.by0, y1 = r.by1;
+    const short4 bb = bbox[src];
+    int x0 = bb.x, x1 = bb.y, y0 = bb.z, y1 = bb.w;
     if (x1 <= x0 || y1 <= y0) return;
     int tx0 = x0 / TILE, tx1 = (x1 - 1) / TILE + 1, ty0 = y0 / TILE, ty1 = (y1 - 1) / TILE + 1;
     unsigned pos = offs[k];
@@ -284,10 +284,10 @@ __global__ void __launch_bounds__(256) k_duplicate(long long m, const unsigned* 
         }
 }
 
-void duplicate_entries(long long m, const unsigned* sorted_src, const Rec64* rec, const unsigned* offs,
+void duplicate_entries(long long m, const unsigned* sorted_src, const short4* bbox, const unsigned* offs,
                        int ntx, unsigned* tkey, unsigned* tval, cudaStream_t st) {
     if (m <= 0) return;
-    k_duplicate<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, sorted_src, rec, offs, ntx, tkey, tval);
+    k_duplicate<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, sorted_src, bbox, offs, ntx, tkey, tval);
 }
 
 __global__ void k_ranges(long long e, const unsigned* __restrict__ tkey, int ntiles, int* __restrict__ start) {
@@ -318,19 +318,19 @@ void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, i
     k_entries_to_rank<<<(unsigned)((e + 255) / 256), 256, 0, st>>>(e, ent_src, rank_of, out);
 }
 
-__global__ void k_bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out) {
+__global__ void k_bbox_dump(long long n, const short4* bbox, int* out) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    bool ok = flag[i] != 0;
-    out[i * 4 + 0] = ok ? rec[i].bx0 : 0;
-    out[i * 4 + 1] = ok ? rec[i].bx1 : 0;
-    out[i * 4 + 2] = ok ? rec[i].by0 : 0;
-    out[i * 4 + 3] = ok ? rec[i].by1 : 0;
+    const short4 b = bbox[i];
+    out[i * 4 + 0] = b.x;
+    out[i * 4 + 1] = b.y;
+    out[i * 4 + 2] = b.z;
+    out[i * 4 + 3] = b.w;
 }
 
-void bbox_dump(long long n, const Rec64* rec, const unsigned* flag, int* out, cudaStream_t st) {
+void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st) {
     if (n <= 0) return;
-    k_bbox_dump<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, rec, flag, out);
+    k_bbox_dump<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, bbox, out);
 }
 
 }  // namespace ts

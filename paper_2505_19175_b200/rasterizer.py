@@ -145,7 +145,8 @@ def make_camera(intr, pose) -> _lib.TsCamera:
 
 def make_options(mode=0, background=(0.0, 0.0, 0.0), tau_cutoff=DEFAULT_TAU_CUTOFF,
                  tile_size=DEFAULT_TILE_SIZE, active_sh_degree=3, solid=False, precision="fast",
-                 param_dtype=torch.float32, validate=True) -> _lib.TsOptions:
+                 param_dtype=torch.float32, validate=True,
+                 keep_backward=True) -> _lib.TsOptions:
     bg = np.asarray(background, dtype=np.float64).reshape(3)
     if not 0 <= int(active_sh_degree) <= 3:
         raise ValueError("SH degree must be in [0,3]")
@@ -154,7 +155,8 @@ def make_options(mode=0, background=(0.0, 0.0, 0.0), tau_cutoff=DEFAULT_TAU_CUTO
     return _lib.TsOptions(mode_flag(mode), int(active_sh_degree), int(tile_size), int(bool(solid)),
                           float(tau_cutoff), float(TAU_CONTRIB), (ctypes.c_double * 3)(*bg),
                           PRECISION[precision] if isinstance(precision, str) else int(precision),
-                          1 if param_dtype == torch.float64 else 0, int(bool(validate)), 0)
+                          1 if param_dtype == torch.float64 else 0, int(bool(validate)),
+                          int(bool(keep_backward)))
 
 
 _NONFINITE_GROUPS = ("vertices", "opacity", "sigma", "sh")
@@ -187,6 +189,13 @@ class Rasterizer:
         """Record CUDA events around every pipeline stage (on the call's stream)."""
         _lib.check(self.lib.ts_profile(self._ctx, int(bool(enable))), "profile")
 
+    def flagged_pixels(self) -> int:
+        """Pixels of the last fast forward re-resolved by the exact fix-up."""
+        torch.cuda.synchronize()
+        v = ctypes.c_int64()
+        _lib.check(self.lib.ts_flagged_pixels(self._ctx, ctypes.byref(v)), "flagged_pixels")
+        return int(v.value)
+
     def stage_times(self) -> dict:
         """Device milliseconds of each stage of the last forward/backward."""
         buf = (ctypes.c_float * len(_lib.STAGES))()
@@ -196,7 +205,7 @@ class Rasterizer:
     def forward(self, soup: DeviceSoup, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
                 tau_cutoff=DEFAULT_TAU_CUTOFF, tile_size=DEFAULT_TILE_SIZE, active_sh_degree=3,
                 precision="fast", validate=True, debug=False, out: ForwardResult | None = None,
-                stream=None) -> ForwardResult:
+                stream=None, keep_backward=True) -> ForwardResult:
         n = len(soup)
         h, w = int(intr.height), int(intr.width)
         dev = soup.vertices.device
@@ -212,7 +221,7 @@ class Rasterizer:
                 n_visible=0, n_entries=0, n_flagged=0)
         cam = make_camera(intr, pose)
         opt = make_options(mode, background, tau_cutoff, tile_size, active_sh_degree, soup.solid,
-                           precision, soup.dtype, validate)
+                           precision, soup.dtype, validate, keep_backward)
         fo = _lib.TsForwardOut(_ptr(out.image), _ptr(out.alpha_map), _ptr(out.max_weight),
                                _ptr(out.pixel_count), _ptr(out.area), _ptr(out.last_src),
                                _ptr(out.n_frag))
