@@ -49,21 +49,24 @@ struct __align__(16) Rec64 {
 };
 static_assert(sizeof(Rec64) == 208, "Rec64 layout");
 
-// Per-source record of the fast blend (112 B).  Edge functions are stored
-// pre-divided by phi_s and relative to an integer origin (ox, oy) inside the
-// clipped bbox, in fp64, so r = phi/phi_s = min_e(a0*dx + a1*dy + a2) with
-// dx = ix + 0.5 - ox is evaluated with ~1e-12 absolute error.  The
-// contribution decision alpha >= 1/255 (_kernels.py:103) is r >= r*, decided
-// outside the fp32-rounded band [r_lo, r_hi] and resolved exactly inside it.
+// Per-source record of the fast blend (128 B = one cache line).  Edge
+// functions are stored pre-divided by phi_s and relative to an integer origin
+// (ox, oy) inside the clipped bbox, in fp64, so r = phi/phi_s =
+// min_e(a0*dx + a1*dy + a2) with dx = ix + 0.5 - ox is evaluated with ~1e-12
+// absolute error.  The contribution decision alpha >= 1/255
+// (_kernels.py:103) is r >= r*, decided outside the fp32-rounded band
+// [r_lo, r_hi] and resolved in fp64 inside it.
 struct __align__(16) RecF {
     double a[9];      // (a0,a1,a2) per edge
+    double phis;      // phi(s) < 0
     float r_lo, r_hi; // contribution threshold band
     float f0, f1;     // normalized: sigma, log2(opacity); sigmoid: phis*log2(e)/sigma, opacity
     float rgb[3];
     short x0, x1, y0, y1;  // clipped half-open pixel bbox
     short ox, oy;          // origin
+    float opa, sig;        // opacity (1 if solid), sigma
 };
-static_assert(sizeof(RecF) == 112, "RecF layout");
+static_assert(sizeof(RecF) == 128, "RecF layout");
 
 // Backward-only per-source data (48 B): vertices relative to the origin,
 // phi_s, opacity, sigma and the edge-orientation signs.

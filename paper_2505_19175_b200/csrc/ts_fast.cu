@@ -36,35 +36,6 @@ __device__ __forceinline__ float fast_ex2(float x) {
     return y;
 }
 
-// exact (oracle-arithmetic) record of one source triangle, recomputed from the
-// parameters -- used only for decisions that fall inside the guard band
-template <typename T>
-__device__ __noinline__ void exact_record(const Cam& cam, const Opts& opt, const T* __restrict__ verts,
-                                          const T* __restrict__ opacity, const T* __restrict__ sigma,
-                                          unsigned src, Rec64& r) {
-    double v[9];
-#pragma unroll
-    for (int k = 0; k < 9; k++) v[k] = (double)verts[(size_t)src * 9 + k];
-    Proj64 p;
-    project64(v, cam, p);
-    double o = opt.solid ? 1.0 : (double)opacity[src];
-    double sg = (double)sigma[src];
-    Edge64 E;
-    edge_bbox64(p.q, p.phis, o, sg, opt.mode, opt.tau_cutoff, cam.width, cam.height, E);
-#pragma unroll
-    for (int e = 0; e < 3; e++) {
-        r.nx[e] = E.nx[e];
-        r.ny[e] = E.ny[e];
-        r.d[e] = E.d[e];
-        r.qx[e] = p.q[e * 2];
-        r.qy[e] = p.q[e * 2 + 1];
-    }
-    r.phis = p.phis;
-    r.sig = sg;
-    r.opa = o;
-    r.esign = E.esign;
-}
-
 // ---------------------------------------------------------------------------
 // preprocess (fast records)
 // ---------------------------------------------------------------------------
@@ -162,6 +133,9 @@ __global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, cons
                 r.rgb[2] = (float)fmin(fmax(acc2 + 0.5, 0.0), 1.0);
                 r.x0 = (short)x0; r.x1 = (short)x1; r.y0 = (short)y0; r.y1 = (short)y1;
                 r.ox = (short)ox; r.oy = (short)oy;
+                r.phis = p.phis;
+                r.opa = (float)o;
+                r.sig = (float)sg;
                 out.rec[i] = r;
                 if (out.recb) {
                     RecB b;
@@ -261,14 +235,26 @@ __device__ __forceinline__ float alpha_fast(const RecF& r, double rr, int mode, 
     }
 }
 
-// exact alpha with the reference arithmetic (fragment_alpha64 on a recomputed record)
+// fp64 alpha from the fp64 r (the reference's fragment_alpha, _kernels.py:43-56,
+// with phi = r * phi_s); used for decisions inside the guard band.  Opacity and
+// sigma are read from the caller's parameter arrays so they are exact for
+// fp32 and fp64 parameters alike.
 template <typename T>
-__device__ double alpha_exact(const Cam& cam, const Opts& opt, const T* verts, const T* opacity,
-                              const T* sigma, unsigned src, int px, int py, double& rr, double& phi,
-                              int& edge) {
-    Rec64 r;
-    exact_record<T>(cam, opt, verts, opacity, sigma, src, r);
-    return fragment_alpha64(px + 0.5, py + 0.5, r, opt.mode, rr, phi, edge);
+__device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mode, const Opts& opt,
+                                                const T* __restrict__ opacity, const T* __restrict__ sigma,
+                                                unsigned src) {
+    const double o = opt.solid ? 1.0 : (double)opacity[src];
+    const double sg = (double)sigma[src];
+    double window;
+    if (mode == 0) {
+        if (rr <= 0.0) return 0.0;  // phi >= 0
+        window = pow(fmin(rr, 1.0), sg);
+    } else {
+        double x = rr * r.phis / sg;
+        if (x > 700.0) x = 700.0;
+        window = 1.0 / (1.0 + exp(x));
+    }
+    return o * window;
 }
 
 // ---------------------------------------------------------------------------
@@ -300,8 +286,8 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
     for (int b = s; b < e; b += FB) {
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min(FB, e - b);
-        for (int c = threadIdx.x; c < nb * 7; c += blockDim.x) {
-            int j = c / 7, q = c - j * 7;
+        for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
+            int j = c >> 3, q = c & 7;
             unsigned src = __ldg(ent_src + b + j);
             if (q == 0) s_src[j] = src;
             reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
@@ -391,58 +377,80 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
 }
 
 // ---------------------------------------------------------------------------
-// k_fixup_fwd: exact per-pixel replay of flagged pixels (reference arithmetic).
-// Entries before the flag position already committed their statistics in
-// k_blend_fast (their decisions were certain); from the flag position on the
-// fix-up commits them.
+// k_fixup_fwd: exact (fp64) replay of flagged pixels, one warp per pixel:
+// lanes evaluate 32 consecutive tile entries in parallel, then the warp
+// composites the contributing ones in entry order.  Entries before the flag
+// position already committed their statistics in k_blend_fast (their
+// decisions were certain); from the flag position on the fix-up commits them.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(64) k_fixup_fwd(Cam cam, Opts opt, const T* __restrict__ verts,
-                                                  const T* __restrict__ opacity, const T* __restrict__ sigma,
-                                                  const RecF* __restrict__ rec, const int* __restrict__ tile_start,
-                                                  const unsigned* __restrict__ ent_src, FastBlendOut out) {
-    const unsigned long long nflag = out.ctr->n_flagged;
-    for (unsigned long long k = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; k < nflag;
-         k += (unsigned long long)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* __restrict__ opacity,
+                                                   const T* __restrict__ sigma, const RecF* __restrict__ rec,
+                                                   const int* __restrict__ tile_start,
+                                                   const unsigned* __restrict__ ent_src, FastBlendOut out) {
+    const unsigned lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long nflag = (long long)out.ctr->n_flagged;
+    for (long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nflag; k += nw) {
         const int2 f = out.flags[k];
         const int p = f.x, fpos = f.y;
         const int px = p % cam.width, py = p / cam.width;
         const int t = (py / TILE) * cam.ntx + px / TILE;
         double Tt = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
         int last = -1, cnt = 0;
+        bool done = false;
         const int s = tile_start[t], e = tile_start[t + 1];
-        for (int pos = s; pos < e; pos++) {
-            const unsigned src = ent_src[pos];
-            const RecF& r = rec[src];
-            if (px < r.x0 || px >= r.x1 || py < r.y0 || py >= r.y1) continue;
-            double rr, phi;
-            int edge;
-            double alpha = alpha_exact<T>(cam, opt, verts, opacity, sigma, src, px, py, rr, phi, edge);
-            if (alpha > ALPHA_CLAMP) alpha = ALPHA_CLAMP;
-            if (alpha < ALPHA_MIN) continue;
-            double w = Tt * alpha;
-            C0 += w * r.rgb[0];
-            C1 += w * r.rgb[1];
-            C2 += w * r.rgb[2];
-            if (pos >= fpos) {
-                if (out.max_weight) atomicMax((unsigned*)out.max_weight + src, __float_as_uint((float)w));
-                if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + src, 1);
+        for (int base = s; base < e && !done; base += 32) {
+            const int pos = base + (int)lane;
+            double a = 0.0;
+            unsigned src = 0;
+            float cr = 0.f, cg = 0.f, cb = 0.f;
+            if (pos < e) {
+                src = ent_src[pos];
+                const RecF& r = rec[src];
+                if (px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
+                    double dx = (double)(px - r.ox) + 0.5, dy = (double)(py - r.oy) + 0.5;
+                    double rr = edge_r(r, dx, dy);
+                    a = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, src);
+                    if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
+                    if (a < ALPHA_MIN) a = 0.0;
+                    cr = r.rgb[0];
+                    cg = r.rgb[1];
+                    cb = r.rgb[2];
+                }
             }
-            last = pos;
-            cnt++;
-            Tt = TS_M(Tt, TS_S(1.0, alpha));
-            if (Tt < T_MIN) break;
+            unsigned m = __ballot_sync(0xffffffffu, a > 0.0);
+            while (m && !done) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const double aj = __shfl_sync(0xffffffffu, a, j);
+                const double w = Tt * aj;
+                C0 += w * (double)__shfl_sync(0xffffffffu, cr, j);
+                C1 += w * (double)__shfl_sync(0xffffffffu, cg, j);
+                C2 += w * (double)__shfl_sync(0xffffffffu, cb, j);
+                const int posj = base + j;
+                if ((int)lane == j && posj >= fpos) {
+                    if (out.max_weight) atomicMax((unsigned*)out.max_weight + src, __float_as_uint((float)w));
+                    if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + src, 1);
+                }
+                last = posj;
+                cnt++;
+                Tt = TS_M(Tt, TS_S(1.0, aj));
+                if (Tt < T_MIN) done = true;
+            }
         }
-        if (out.image) {
-            out.image[p * 3 + 0] = (float)fmin(fmax(C0 + Tt * opt.bg[0], 0.0), 1.0);
-            out.image[p * 3 + 1] = (float)fmin(fmax(C1 + Tt * opt.bg[1], 0.0), 1.0);
-            out.image[p * 3 + 2] = (float)fmin(fmax(C2 + Tt * opt.bg[2], 0.0), 1.0);
+        if (lane == 0) {
+            if (out.image) {
+                out.image[p * 3 + 0] = (float)fmin(fmax(C0 + Tt * opt.bg[0], 0.0), 1.0);
+                out.image[p * 3 + 1] = (float)fmin(fmax(C1 + Tt * opt.bg[1], 0.0), 1.0);
+                out.image[p * 3 + 2] = (float)fmin(fmax(C2 + Tt * opt.bg[2], 0.0), 1.0);
+            }
+            if (out.alpha_map) out.alpha_map[p] = (float)(1.0 - Tt);
+            out.t_final[p] = (float)Tt;
+            out.last_pos[p] = last;
+            if (out.n_frag) out.n_frag[p] = cnt;
+            if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
         }
-        if (out.alpha_map) out.alpha_map[p] = (float)(1.0 - Tt);
-        out.t_final[p] = (float)Tt;
-        out.last_pos[p] = last;
-        if (out.n_frag) out.n_frag[p] = cnt;
-        if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
     }
 }
 
@@ -457,15 +465,13 @@ void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                       cudaStream_t st) {
-    const int grid = 148 * 2;
+    const int grid = 148 * 4;
     if (dtype == 1)
-        k_fixup_fwd<double><<<grid, 64, 0, st>>>(cam, opt, (const double*)soup.vertices,
-                                                 (const double*)soup.opacity, (const double*)soup.sigma,
-                                                 rec, tile_start, ent_src, out);
+        k_fixup_fwd<double><<<grid, 256, 0, st>>>(cam, opt, (const double*)soup.opacity,
+                                                  (const double*)soup.sigma, rec, tile_start, ent_src, out);
     else
-        k_fixup_fwd<float><<<grid, 64, 0, st>>>(cam, opt, (const float*)soup.vertices,
-                                                (const float*)soup.opacity, (const float*)soup.sigma,
-                                                rec, tile_start, ent_src, out);
+        k_fixup_fwd<float><<<grid, 256, 0, st>>>(cam, opt, (const float*)soup.opacity,
+                                                 (const float*)soup.sigma, rec, tile_start, ent_src, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -519,14 +525,14 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
         const int bstart = max(s, bend - FB);
         const int nb = bend - bstart;
         __syncthreads();
-        for (int c = threadIdx.x; c < nb * 10; c += blockDim.x) {
-            int j = c / 10, q = c - j * 10;
+        for (int c = threadIdx.x; c < nb * 11; c += blockDim.x) {
+            int j = c / 11, q = c - j * 11;
             unsigned src = __ldg(ent_src + bstart + j);
             if (q == 0) s_src[j] = src;
-            if (q < 7)
+            if (q < 8)
                 reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
             else
-                reinterpret_cast<float4*>(&s_rb[j])[q - 7] = __ldg(reinterpret_cast<const float4*>(recb + src) + (q - 7));
+                reinterpret_cast<float4*>(&s_rb[j])[q - 8] = __ldg(reinterpret_cast<const float4*>(recb + src) + (q - 8));
         }
         __syncthreads();
         for (int jb = ((nb - 1) / 32) * 32; jb >= 0; jb -= 32) {
@@ -551,9 +557,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                     float alpha = 0.f;
                     bool clamped = false, exact_done = false;
                     if (!contributes && rr >= (double)r.r_lo) {
-                        double er, ephi;
-                        int eedge;
-                        double ae = alpha_exact<T>(cam, opt, verts, opacity, sigma, s_src[j], px, py, er, ephi, eedge);
+                        double ae = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, s_src[j]);
                         clamped = ae > ALPHA_CLAMP;
                         if (clamped) ae = ALPHA_CLAMP;
                         contributes = ae >= ALPHA_MIN;
@@ -565,9 +569,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                             float ea;
                             alpha = alpha_fast(r, rr, opt.mode, ea);
                             if (fabsf(alpha - ALPHA_CLAMP_F) <= 2.f * ea * alpha + 1e-7f) {
-                                double er, ephi;
-                                int eedge;
-                                double ae = alpha_exact<T>(cam, opt, verts, opacity, sigma, s_src[j], px, py, er, ephi, eedge);
+                                double ae = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, s_src[j]);
                                 clamped = ae > ALPHA_CLAMP;
                                 alpha = clamped ? ALPHA_CLAMP_F : (float)ae;
                             } else {
@@ -609,8 +611,12 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                                     g[SG_GPHIS] = -g_r * rf / phis;
                                 }
                             } else {
-                                g[SG_GSIG] = g_win * window * (1.f - window) * phi / (sg * sg);
-                                g_phi = -g_win * window * (1.f - window) / sg;
+                                // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
+                                const float E = fast_ex2(fminf(rf * r.f0, 126.f));
+                                const float inv = 1.f / (1.f + E);
+                                const float ww = E * inv * inv;
+                                g[SG_GSIG] = g_win * ww * phi / (sg * sg);
+                                g_phi = -g_win * ww / sg;
                             }
                             // edge line L = s*(n.p)... derivative wrt its endpoints (_kernels.py:296-318)
                             const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
