@@ -423,8 +423,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
                         out->n_frag, c->t_final32, c->last_pos, c->flags, c->d_ctr};
         stage_begin(c, TS_STAGE_BLEND, st);
-        launch_blend_fast(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
-                          bo, st, 0);
+        launch_blend_fast(cm, op, (const RecF*)c->recf.p, c->bbox, c->tile_start, c->ent_src, bo, st);
         stage_end(c, TS_STAGE_BLEND, st);
         stage_begin(c, TS_STAGE_FIXUP, st);
         launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,

@@ -50,21 +50,19 @@ struct __align__(16) Rec64 {
 static_assert(sizeof(Rec64) == 208, "Rec64 layout");
 
 // Per-source record of the fast blend (128 B = one cache line).  Edge
-// functions are stored pre-divided by phi_s and relative to an integer origin
-// (ox, oy) inside the clipped bbox, in fp64, so r = phi/phi_s =
-// min_e(a0*dx + a1*dy + a2) with dx = ix + 0.5 - ox is evaluated with ~1e-12
-// absolute error.  The contribution decision alpha >= 1/255
-// (_kernels.py:103) is r >= r*, decided outside the fp32-rounded band
-// [r_lo, r_hi] and resolved in fp64 inside it.
+// functions are stored pre-divided by phi_s, in fp64, as functions of the
+// absolute pixel centre: r = phi/phi_s = min_e(a0*pcx + a1*pcy + a2), which
+// matches the reference's fp64 phi/phi_s to ~1e-13 * (W+H)/|phi_s|.  The
+// contribution decision alpha >= 1/255 (_kernels.py:103) is r >= r*,
+// decided outside the band [r_lo, r_hi] and resolved in fp64 inside it.
 struct __align__(16) RecF {
-    double a[9];      // (a0,a1,a2) per edge
-    double phis;      // phi(s) < 0
-    float r_lo, r_hi; // contribution threshold band
-    float f0, f1;     // normalized: sigma, log2(opacity); sigmoid: phis*log2(e)/sigma, opacity
+    double a[9];           // (a0,a1,a2) per edge
+    double phis;           // phi(s) < 0
+    double r_lo, r_hi;     // contribution threshold band
+    float f0, f1;          // normalized: sigma, log2(opacity); sigmoid: phis*log2(e)/sigma, opacity
     float rgb[3];
     short x0, x1, y0, y1;  // clipped half-open pixel bbox
-    short ox, oy;          // origin
-    float opa, sig;        // opacity (1 if solid), sigma
+    short ox, oy;          // origin of the backward record's relative coordinates
 };
 static_assert(sizeof(RecF) == 128, "RecF layout");
 

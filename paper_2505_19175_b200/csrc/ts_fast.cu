@@ -90,8 +90,7 @@ __global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, cons
                 for (int e = 0; e < 3; e++) {
                     r.a[e * 3 + 0] = E.nx[e] * inv;
                     r.a[e * 3 + 1] = E.ny[e] * inv;
-                    double de = E.nx[e] * (double)ox + E.ny[e] * (double)oy + E.d[e];
-                    r.a[e * 3 + 2] = de * inv;
+                    r.a[e * 3 + 2] = E.d[e] * inv;
                     dmax = fmax(dmax, fabs(E.d[e]));
                 }
                 // |r_fast - r_ref| bound: both are O(1e-16) x (sum of |terms| / |phi_s|)
@@ -110,9 +109,8 @@ __global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, cons
                     r.f0 = (float)(p.phis * 1.4426950408889634 / sg);
                     r.f1 = (float)o;
                 }
-                double rlo = rstar - delta - fabs(rstar) * 1e-12, rhi = rstar + delta + fabs(rstar) * 1e-12;
-                r.r_lo = __double2float_rd(rlo);
-                r.r_hi = __double2float_ru(rhi);
+                r.r_lo = rstar - delta - fabs(rstar) * 1e-12;
+                r.r_hi = rstar + delta + fabs(rstar) * 1e-12;
                 // view-dependent colour, render.py:292-302
                 double u[3];
 #pragma unroll
@@ -134,8 +132,6 @@ __global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, cons
                 r.x0 = (short)x0; r.x1 = (short)x1; r.y0 = (short)y0; r.y1 = (short)y1;
                 r.ox = (short)ox; r.oy = (short)oy;
                 r.phis = p.phis;
-                r.opa = (float)o;
-                r.sig = (float)sg;
                 out.rec[i] = r;
                 if (out.recb) {
                     RecB b;
@@ -198,7 +194,8 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
 // ---------------------------------------------------------------------------
 // shared per-fragment evaluation
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double edge_r(const RecF& r, double dx, double dy, int& arg) {
+__device__ __forceinline__ double edge_r(const RecF& r, double pcx, double pcy, int& arg) {
+    const double dx = pcx, dy = pcy;
     double l0 = fma(r.a[0], dx, fma(r.a[1], dy, r.a[2]));
     double l1 = fma(r.a[3], dx, fma(r.a[4], dy, r.a[5]));
     double l2 = fma(r.a[6], dx, fma(r.a[7], dy, r.a[8]));
@@ -210,7 +207,8 @@ __device__ __forceinline__ double edge_r(const RecF& r, double dx, double dy, in
     return m;
 }
 
-__device__ __forceinline__ double edge_r(const RecF& r, double dx, double dy) {
+__device__ __forceinline__ double edge_r(const RecF& r, double pcx, double pcy) {
+    const double dx = pcx, dy = pcy;
     double l0 = fma(r.a[0], dx, fma(r.a[1], dy, r.a[2]));
     double l1 = fma(r.a[3], dx, fma(r.a[4], dy, r.a[5]));
     double l2 = fma(r.a[6], dx, fma(r.a[7], dy, r.a[8]));
@@ -258,16 +256,34 @@ __device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mo
 }
 
 // ---------------------------------------------------------------------------
-// k_blend_fast: CTA per 16x16 tile, warp = two pixel rows, fp32 compositing.
+// k_blend_fast: CTA per 16x16 tile, warp = two pixel rows (lane = pixel),
+// fp64 edge functions, fp32 alpha and compositing.  Each batch of FB tile
+// entries is staged in shared memory together with, per warp, the 32-bit mask
+// of the warp's pixels inside the entry's bbox (the reference's per-pixel
+// bbox test, _kernels.py:87-95), so a warp only visits entries that overlap
+// it and a lane only evaluates pixels inside the bbox.
 // ---------------------------------------------------------------------------
 constexpr int FB = 64;
 
+__device__ __forceinline__ unsigned strip_mask(short4 bb, int tx0, int y_row0) {
+    // bits: lane l <-> (column l & 15, row l >> 4) of the strip at rows y_row0, y_row0+1
+    int cx0 = max((int)bb.x - tx0, 0), cx1 = min((int)bb.y - tx0, 16);
+    if (cx1 <= cx0) return 0u;
+    unsigned col = (0xffffu >> (16 - (cx1 - cx0))) << cx0;
+    unsigned m = 0u;
+    if (y_row0 >= bb.z && y_row0 < bb.w) m |= col;
+    if (y_row0 + 1 >= bb.z && y_row0 + 1 < bb.w) m |= col << 16;
+    return m;
+}
+
 __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
+                                                    const short4* __restrict__ bbox,
                                                     const int* __restrict__ tile_start,
                                                     const unsigned* __restrict__ ent_src,
                                                     FastBlendOut out) {
     __shared__ RecF s_rec[FB];
     __shared__ unsigned s_src[FB];
+    __shared__ unsigned s_lmask[8][FB];
     __shared__ unsigned s_maxw[FB];
     __shared__ int s_pix[FB];
     const int t = blockIdx.x;
@@ -275,49 +291,64 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int px = tx * TILE + (lane & 15);
     const int py = ty * TILE + 2 * warp + (lane >> 4);
-    const int wy0 = ty * TILE + 2 * warp;
+    const double pcx = px + 0.5, pcy = py + 0.5;
     const bool inside = px < cam.width && py < cam.height;
     float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
     int last = -1, cnt = 0, flag_pos = -1;
     bool done = !inside;
     const int s = tile_start[t], e = tile_start[t + 1];
     const float tau = (float)opt.tau_contrib;
-    if (threadIdx.x < FB) { s_maxw[threadIdx.x] = 0u; s_pix[threadIdx.x] = 0; }
+    if (threadIdx.x < FB) {
+        s_maxw[threadIdx.x] = 0u;
+        s_pix[threadIdx.x] = 0;
+    }
     for (int b = s; b < e; b += FB) {
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min(FB, e - b);
         for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
-            int j = c >> 3, q = c & 7;
-            unsigned src = __ldg(ent_src + b + j);
-            if (q == 0) s_src[j] = src;
+            const int j = c >> 3, q = c & 7;
+            const unsigned src = __ldg(ent_src + b + j);
             reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
+        }
+        {
+            // per (warp, entry) strip masks: thread -> entry j, warps w0, w0+1, ... (4 per thread)
+            const int j = threadIdx.x & (FB - 1);
+            if (j < nb) {
+                const unsigned src = __ldg(ent_src + b + j);
+                if (threadIdx.x < FB) s_src[j] = src;
+                const short4 bb = __ldg(bbox + src);
+                for (int w = threadIdx.x >> 6; w < 8; w += 4)
+                    s_lmask[w][j] = strip_mask(bb, tx * TILE, ty * TILE + 2 * w);
+            }
         }
         __syncthreads();
         for (int jb = 0; jb < nb; jb += 32) {
-            int jl = jb + (int)lane;
-            bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
-            unsigned mask = __ballot_sync(0xffffffffu, ov);
+            if (!__any_sync(0xffffffffu, !done)) break;
+            const int jl = jb + (int)lane;
+            unsigned mask = __ballot_sync(0xffffffffu, jl < nb && s_lmask[warp][jl] != 0u);
             while (mask) {
                 const int j = jb + __ffs(mask) - 1;
                 mask &= mask - 1;
-                const RecF& r = s_rec[j];
+                const unsigned lm = s_lmask[warp][j];
                 bool contrib = false;
                 float w = 0.f;
-                if (!done && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
-                    double dx = (double)(px - r.ox) + 0.5, dy = (double)(py - r.oy) + 0.5;
-                    double rr = edge_r(r, dx, dy);
-                    if (rr >= (double)r.r_lo) {
-                        bool flag = rr <= (double)r.r_hi;
+                if (((lm >> lane) & 1u) && !done) {
+                    const RecF& r = s_rec[j];
+                    const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
+                    const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
+                    const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
+                    if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
+                        const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
+                        bool flag = rr <= r.r_hi;
                         if (!flag) {
                             float ea;
-                            float a = alpha_fast(r, rr, opt.mode, ea);
-                            a = fminf(a, ALPHA_CLAMP_F);
+                            float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
                             w = T * a;
-                            float tn = T * (1.f - a);
-                            float en = epsT + ea * a / (1.f - a) + 2.4e-7f;
-                            float ew = epsT + ea + 1.2e-7f;
-                            flag = fabsf(tn - T_MIN_F) <= 2.f * en * tn + 1e-11f ||
-                                   fabsf(w - tau) <= 2.f * ew * w + 1e-9f;
+                            const float tn = fmaf(-T, a, T);
+                            const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                            const float ew = epsT + ea + 1.2e-7f;
+                            flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                                   fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
                             if (!flag) {
                                 C0 = fmaf(w, r.rgb[0], C0);
                                 C1 = fmaf(w, r.rgb[1], C1);
@@ -327,7 +358,7 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                                 cnt++;
                                 T = tn;
                                 epsT = en;
-                                if (T < T_MIN_F) done = true;
+                                done = T < T_MIN_F;
                             }
                         }
                         if (flag) {
@@ -336,19 +367,15 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                         }
                     }
                 }
-                if (__any_sync(0xffffffffu, contrib)) {
-                    unsigned mx = __reduce_max_sync(0xffffffffu, contrib ? __float_as_uint(w) : 0u);
-                    unsigned pc = __popc(__ballot_sync(0xffffffffu, contrib && w > tau));
-                    if (lane == 0) {
-                        atomicMax(&s_maxw[j], mx);
-                        if (pc) atomicAdd(&s_pix[j], (int)pc);
-                    }
+                if (contrib) {
+                    atomicMax(&s_maxw[j], __float_as_uint(w));
+                    if (w > tau) atomicAdd(&s_pix[j], 1);
                 }
             }
         }
         __syncthreads();
         if (threadIdx.x < nb) {
-            unsigned src = s_src[threadIdx.x];
+            const unsigned src = s_src[threadIdx.x];
             if (s_maxw[threadIdx.x] && out.max_weight)
                 atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
             if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
@@ -409,8 +436,7 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
                 src = ent_src[pos];
                 const RecF& r = rec[src];
                 if (px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
-                    double dx = (double)(px - r.ox) + 0.5, dy = (double)(py - r.oy) + 0.5;
-                    double rr = edge_r(r, dx, dy);
+                    double rr = edge_r(r, px + 0.5, py + 0.5);
                     a = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, src);
                     if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
                     if (a < ALPHA_MIN) a = 0.0;
@@ -454,12 +480,11 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
     }
 }
 
-void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+void launch_blend_fast(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
-                       cudaStream_t st, int stage_fixup_marker) {
-    (void)stage_fixup_marker;
+                       cudaStream_t st) {
     int ntiles = cam.ntx * cam.nty;
-    k_blend_fast<<<ntiles, 256, 0, st>>>(cam, opt, rec, tile_start, ent_src, out);
+    k_blend_fast<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
 }
 
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
@@ -550,9 +575,8 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                 bool act = false;
                 if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
                     const RecB& rb = s_rb[j];
-                    double dx = (double)(px - r.ox) + 0.5, dy = (double)(py - r.oy) + 0.5;
                     int edge;
-                    double rr = edge_r(r, dx, dy, edge);
+                    double rr = edge_r(r, px + 0.5, py + 0.5, edge);
                     bool contributes = rr > (double)r.r_hi;
                     float alpha = 0.f;
                     bool clamped = false, exact_done = false;
@@ -621,7 +645,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                             // edge line L = s*(n.p)... derivative wrt its endpoints (_kernels.py:296-318)
                             const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
                             const float ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
-                            const float pxr = (float)dx, pyr = (float)dy;
+                            const float pxr = (float)(px - r.ox) + 0.5f, pyr = (float)(py - r.oy) + 0.5f;
                             const float ex = bx - ax, ey = by - ay;
                             const float inv_l = rsqrtf(ex * ex + ey * ey);
                             const float inv_l2 = inv_l * inv_l;

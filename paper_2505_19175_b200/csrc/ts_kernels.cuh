@@ -81,9 +81,9 @@ void launch_chain_bwd32(const Cam& cam, const Opts& opt, const ts_soup& soup, in
 // ts_fast.cu
 void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
                             const FastPreOut& out, cudaStream_t st);
-void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+void launch_blend_fast(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
-                       cudaStream_t st, int stage_fixup_marker);
+                       cudaStream_t st);
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                       cudaStream_t st);

@@ -234,3 +234,15 @@ def test_drop_in_render_types(rast):
     assert isinstance(out, RenderOutput)
     assert np.allclose(out.image.rgb, [0.2, 0.3, 0.4])
     assert np.allclose(out.alpha_map, 0.0)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_north_star_forward_parity(rast, precision):
+    """North-star scene (2M triangles, 1280x720) against the oracle: sort
+    order, tile lists, last contributors and counts bit-exact, RGB <= 1e-5."""
+    from oracle import oracle as O
+    from paper_2505_19175_b200 import scenes
+    soup, intr, pose = scenes.make_scene("ns")
+    fwd = rast.forward(_dev(soup), intr, pose, precision=precision, debug=True)
+    ref = O.render(soup, intr, pose)
+    check_forward(rast, fwd, ref, intr, f"ns-{precision}")
