@@ -256,41 +256,39 @@ __device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mo
 }
 
 // ---------------------------------------------------------------------------
-// k_blend_fast: CTA per 16x16 tile, warp = two pixel rows (lane = pixel),
-// fp64 edge functions, fp32 alpha and compositing.  Each batch of FB tile
-// entries is staged in shared memory together with, per warp, the 32-bit mask
-// of the warp's pixels inside the entry's bbox (the reference's per-pixel
-// bbox test, _kernels.py:87-95), so a warp only visits entries that overlap
-// it and a lane only evaluates pixels inside the bbox.
+// k_blend_fast: CTA per 16x16 tile, lane = pixel.  Warp w owns the 2x16
+// column strip x in [2w, 2w+2) of the tile, split into 8 groups of 4 lanes
+// (2x2 pixel quads).  Each group walks its OWN list of the batch's entries
+// whose bbox overlaps its quad (the reference's per-pixel bbox test,
+// _kernels.py:87-95, hoisted to quad level), so lanes stay busy even though
+// the triangles are a few pixels wide.  Edge functions in fp64, alpha and
+// compositing in fp32 with the decision guard band.
 // ---------------------------------------------------------------------------
 constexpr int FB = 64;
 
-__device__ __forceinline__ unsigned strip_mask(short4 bb, int tx0, int y_row0) {
-    // bits: lane l <-> (column l & 15, row l >> 4) of the strip at rows y_row0, y_row0+1
-    int cx0 = max((int)bb.x - tx0, 0), cx1 = min((int)bb.y - tx0, 16);
-    if (cx1 <= cx0) return 0u;
-    unsigned col = (0xffffu >> (16 - (cx1 - cx0))) << cx0;
-    unsigned m = 0u;
-    if (y_row0 >= bb.z && y_row0 < bb.w) m |= col;
-    if (y_row0 + 1 >= bb.z && y_row0 + 1 < bb.w) m |= col << 16;
-    return m;
-}
+struct __align__(16) SRec {
+    RecF r;
+    float4 pad;  // 144-byte stride: groups reading different records hit different banks
+};
 
 __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                     const short4* __restrict__ bbox,
                                                     const int* __restrict__ tile_start,
                                                     const unsigned* __restrict__ ent_src,
                                                     FastBlendOut out) {
-    __shared__ RecF s_rec[FB];
+    __shared__ SRec s_rec[FB];
+    __shared__ short4 s_bb[FB];
     __shared__ unsigned s_src[FB];
-    __shared__ unsigned s_lmask[8][FB];
     __shared__ unsigned s_maxw[FB];
     __shared__ int s_pix[FB];
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int px = tx * TILE + (lane & 15);
-    const int py = ty * TILE + 2 * warp + (lane >> 4);
+    const unsigned grp = lane >> 2;
+    const int X0 = tx * TILE + 2 * (int)warp;  // strip columns [X0, X0+2)
+    const int Y0 = ty * TILE;
+    const int px = X0 + (int)(lane & 1);
+    const int py = Y0 + 2 * (int)grp + (int)((lane >> 1) & 1);
     const double pcx = px + 0.5, pcy = py + 0.5;
     const bool inside = px < cam.width && py < cam.height;
     float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
@@ -308,65 +306,77 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
         for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
             const int j = c >> 3, q = c & 7;
             const unsigned src = __ldg(ent_src + b + j);
-            reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
-        }
-        {
-            // per (warp, entry) strip masks: thread -> entry j, warps w0, w0+1, ... (4 per thread)
-            const int j = threadIdx.x & (FB - 1);
-            if (j < nb) {
-                const unsigned src = __ldg(ent_src + b + j);
-                if (threadIdx.x < FB) s_src[j] = src;
-                const short4 bb = __ldg(bbox + src);
-                for (int w = threadIdx.x >> 6; w < 8; w += 4)
-                    s_lmask[w][j] = strip_mask(bb, tx * TILE, ty * TILE + 2 * w);
+            if (q == 0) {
+                s_src[j] = src;
+                s_bb[j] = __ldg(bbox + src);
             }
+            reinterpret_cast<float4*>(&s_rec[j].r)[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
         }
         __syncthreads();
         for (int jb = 0; jb < nb; jb += 32) {
             if (!__any_sync(0xffffffffu, !done)) break;
+            // lane l tests entry jb+l against the 8 quads of this warp's strip
+            unsigned q8 = 0u;
             const int jl = jb + (int)lane;
-            unsigned mask = __ballot_sync(0xffffffffu, jl < nb && s_lmask[warp][jl] != 0u);
-            while (mask) {
-                const int j = jb + __ffs(mask) - 1;
-                mask &= mask - 1;
-                const unsigned lm = s_lmask[warp][j];
+            if (jl < nb) {
+                const short4 bb = s_bb[jl];
+                if (bb.x < X0 + 2 && bb.y > X0) {
+                    int g0 = max(((int)bb.z - Y0) >> 1, 0), g1 = min(((int)bb.w - 1 - Y0) >> 1, 7);
+                    if (g1 >= g0) q8 = (0xffu >> (7 - (g1 - g0))) << g0;
+                }
+            }
+            unsigned gmask = 0u;
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+                const unsigned bm = __ballot_sync(0xffffffffu, (q8 >> g) & 1u);
+                if ((int)grp == g) gmask = bm;
+            }
+            if (done) gmask = 0u;
+            while (__any_sync(0xffffffffu, gmask != 0u)) {
+                const int jo = __ffs(gmask) - 1;
+                gmask &= gmask - 1;
+                const int j = jb + jo;
                 bool contrib = false;
                 float w = 0.f;
-                if (((lm >> lane) & 1u) && !done) {
-                    const RecF& r = s_rec[j];
-                    const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
-                    const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
-                    const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
-                    if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
-                        const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
-                        bool flag = rr <= r.r_hi;
-                        if (!flag) {
-                            float ea;
-                            float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
-                            w = T * a;
-                            const float tn = fmaf(-T, a, T);
-                            const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
-                            const float ew = epsT + ea + 1.2e-7f;
-                            flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
-                                   fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
+                if (jo >= 0 && !done) {
+                    const short4 bb = s_bb[j];
+                    if (px >= bb.x && px < bb.y && py >= bb.z && py < bb.w) {
+                        const RecF& r = s_rec[j].r;
+                        const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
+                        const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
+                        const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
+                        if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
+                            const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
+                            bool flag = rr <= r.r_hi;
                             if (!flag) {
-                                C0 = fmaf(w, r.rgb[0], C0);
-                                C1 = fmaf(w, r.rgb[1], C1);
-                                C2 = fmaf(w, r.rgb[2], C2);
-                                contrib = true;
-                                last = b + j;
-                                cnt++;
-                                T = tn;
-                                epsT = en;
-                                done = T < T_MIN_F;
+                                float ea;
+                                float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
+                                w = T * a;
+                                const float tn = fmaf(-T, a, T);
+                                const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                                const float ew = epsT + ea + 1.2e-7f;
+                                flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                                       fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
+                                if (!flag) {
+                                    C0 = fmaf(w, r.rgb[0], C0);
+                                    C1 = fmaf(w, r.rgb[1], C1);
+                                    C2 = fmaf(w, r.rgb[2], C2);
+                                    contrib = true;
+                                    last = b + j;
+                                    cnt++;
+                                    T = tn;
+                                    epsT = en;
+                                    done = T < T_MIN_F;
+                                }
                             }
-                        }
-                        if (flag) {
-                            flag_pos = b + j;
-                            done = true;
+                            if (flag) {
+                                flag_pos = b + j;
+                                done = true;
+                            }
                         }
                     }
                 }
+                if (done) gmask = 0u;
                 if (contrib) {
                     atomicMax(&s_maxw[j], __float_as_uint(w));
                     if (w > tau) atomicAdd(&s_pix[j], 1);
