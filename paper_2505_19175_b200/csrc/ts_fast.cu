@@ -256,141 +256,249 @@ __device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mo
 }
 
 // ---------------------------------------------------------------------------
-// k_blend_fast: CTA per 16x16 tile, lane = pixel.  Warp w owns the 2x16
-// column strip x in [2w, 2w+2) of the tile, split into 8 groups of 4 lanes
-// (2x2 pixel quads).  Each group walks its OWN list of the batch's entries
-// whose bbox overlaps its quad (the reference's per-pixel bbox test,
-// _kernels.py:87-95, hoisted to quad level), so lanes stay busy even though
-// the triangles are a few pixels wide.  Edge functions in fp64, alpha and
-// compositing in fp32 with the decision guard band.
+// k_blend_fast: CTA per 16x16 tile, two balanced phases per batch of FB
+// depth-ordered tile entries (render.py:349-361 order):
+//
+//  B. dense evaluation -- the batch's (entry, pixel) pairs with the pixel in
+//     the entry's bbox (the reference's per-pixel bbox test, _kernels.py:87-95)
+//     are enumerated as one flat range; each thread takes a contiguous slice
+//     (merge-path split, record cached in registers while the entry repeats),
+//     evaluates phi/phi_s in fp64 and, for contributing fragments, alpha in
+//     fp32; results go to small per-pixel slot lists in shared memory.
+//  C. compositing -- thread = pixel, walks only its slots in entry order
+//     (front to back, _kernels.py:96-123): weight, colour, transmittance,
+//     early stop, per-entry statistics, and the decision guard band.
+//
+// A pixel whose slot list overflows, or whose decision lands inside the guard
+// band, is flagged and recomputed exactly by k_fixup_fwd.
 // ---------------------------------------------------------------------------
 constexpr int FB = 64;
-
-struct __align__(16) SRec {
-    RecF r;
-    float4 pad;  // 144-byte stride: groups reading different records hit different banks
-};
+constexpr int NSLOT = 12;
 
 __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                     const short4* __restrict__ bbox,
                                                     const int* __restrict__ tile_start,
                                                     const unsigned* __restrict__ ent_src,
                                                     FastBlendOut out) {
-    __shared__ SRec s_rec[FB];
-    __shared__ short4 s_bb[FB];
+    (void)bbox;
+    __shared__ double s_a[9][FB];
+    __shared__ double s_rlo[FB], s_rhi[FB];
+    __shared__ float s_f0[FB], s_f1[FB];
+    __shared__ float s_rgb[3][FB];
     __shared__ unsigned s_src[FB];
+    __shared__ int s_geo[FB];      // cx0 | w << 8 | ry0 << 16  (bbox clipped to the tile)
+    __shared__ int s_pre[FB + 1];  // exclusive prefix of pair counts
     __shared__ unsigned s_maxw[FB];
     __shared__ int s_pix[FB];
+    __shared__ unsigned char s_done[TILE_PIX];
+    __shared__ unsigned char s_ovf[TILE_PIX];
+    __shared__ int s_cnt[TILE_PIX];
+    __shared__ float s_sa[NSLOT][TILE_PIX];          // alpha (or -1: guard band)
+    __shared__ float s_se[NSLOT][TILE_PIX];          // relative error bound of alpha
+    __shared__ unsigned char s_sj[NSLOT][TILE_PIX];  // entry index in the batch
+
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned grp = lane >> 2;
-    const int X0 = tx * TILE + 2 * (int)warp;  // strip columns [X0, X0+2)
-    const int Y0 = ty * TILE;
-    const int px = X0 + (int)(lane & 1);
-    const int py = Y0 + 2 * (int)grp + (int)((lane >> 1) & 1);
-    const double pcx = px + 0.5, pcy = py + 0.5;
+    const int TX0 = tx * TILE, TY0 = ty * TILE;
+    const int tid = threadIdx.x;
+    const int px = TX0 + (tid & 15), py = TY0 + (tid >> 4);
     const bool inside = px < cam.width && py < cam.height;
     float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
     int last = -1, cnt = 0, flag_pos = -1;
     bool done = !inside;
+    s_done[tid] = done ? 1 : 0;
+    s_ovf[tid] = 0;
+    s_cnt[tid] = 0;
     const int s = tile_start[t], e = tile_start[t + 1];
     const float tau = (float)opt.tau_contrib;
-    if (threadIdx.x < FB) {
-        s_maxw[threadIdx.x] = 0u;
-        s_pix[threadIdx.x] = 0;
+    if (tid < FB) {
+        s_maxw[tid] = 0u;
+        s_pix[tid] = 0;
     }
     for (int b = s; b < e; b += FB) {
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min(FB, e - b);
-        for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
+        // ---- stage the batch (SoA) ----
+        for (int c = tid; c < nb * 8; c += 256) {
             const int j = c >> 3, q = c & 7;
             const unsigned src = __ldg(ent_src + b + j);
-            if (q == 0) {
-                s_src[j] = src;
-                s_bb[j] = __ldg(bbox + src);
-            }
-            reinterpret_cast<float4*>(&s_rec[j].r)[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
-        }
-        __syncthreads();
-        for (int jb = 0; jb < nb; jb += 32) {
-            if (!__any_sync(0xffffffffu, !done)) break;
-            // lane l tests entry jb+l against the 8 quads of this warp's strip
-            unsigned q8 = 0u;
-            const int jl = jb + (int)lane;
-            if (jl < nb) {
-                const short4 bb = s_bb[jl];
-                if (bb.x < X0 + 2 && bb.y > X0) {
-                    int g0 = max(((int)bb.z - Y0) >> 1, 0), g1 = min(((int)bb.w - 1 - Y0) >> 1, 7);
-                    if (g1 >= g0) q8 = (0xffu >> (7 - (g1 - g0))) << g0;
+            const float4 v = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
+            const double2 d = *reinterpret_cast<const double2*>(&v);
+            switch (q) {
+                case 0: s_a[0][j] = d.x; s_a[1][j] = d.y; break;
+                case 1: s_a[2][j] = d.x; s_a[3][j] = d.y; break;
+                case 2: s_a[4][j] = d.x; s_a[5][j] = d.y; break;
+                case 3: s_a[6][j] = d.x; s_a[7][j] = d.y; break;
+                case 4: s_a[8][j] = d.x; break;
+                case 5: s_rlo[j] = d.x; s_rhi[j] = d.y; break;
+                case 6: s_f0[j] = v.x; s_f1[j] = v.y; s_rgb[0][j] = v.z; s_rgb[1][j] = v.w; break;
+                default: {
+                    s_rgb[2][j] = v.x;
+                    s_src[j] = src;
+                    const int xx = __float_as_int(v.y), yy = __float_as_int(v.z);
+                    const int x0 = (short)(xx & 0xffff), x1 = (short)(xx >> 16);
+                    const int y0 = (short)(yy & 0xffff), y1 = (short)(yy >> 16);
+                    const int cx0 = max(x0 - TX0, 0), cx1 = min(x1 - TX0, TILE);
+                    const int ry0 = max(y0 - TY0, 0), ry1 = min(y1 - TY0, TILE);
+                    const int w = max(cx1 - cx0, 0), h = max(ry1 - ry0, 0);
+                    s_geo[j] = cx0 | (w << 8) | (ry0 << 16);
+                    s_pre[j + 1] = w * h;  // counts, scanned below
                 }
             }
-            unsigned gmask = 0u;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // exclusive scan of the pair counts (two values per lane)
+            const int c0 = tid * 2 < nb ? s_pre[tid * 2 + 1] : 0;
+            const int c1 = tid * 2 + 1 < nb ? s_pre[tid * 2 + 2] : 0;
+            int x = c0 + c1;
 #pragma unroll
-            for (int g = 0; g < 8; g++) {
-                const unsigned bm = __ballot_sync(0xffffffffu, (q8 >> g) & 1u);
-                if ((int)grp == g) gmask = bm;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
+                if (tid >= off) x += y;
             }
-            if (done) gmask = 0u;
-            while (__any_sync(0xffffffffu, gmask != 0u)) {
-                const int jo = __ffs(gmask) - 1;
-                gmask &= gmask - 1;
-                const int j = jb + jo;
-                bool contrib = false;
-                float w = 0.f;
-                if (jo >= 0 && !done) {
-                    const short4 bb = s_bb[j];
-                    if (px >= bb.x && px < bb.y && py >= bb.z && py < bb.w) {
-                        const RecF& r = s_rec[j].r;
-                        const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
-                        const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
-                        const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
-                        if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
-                            const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
-                            bool flag = rr <= r.r_hi;
-                            if (!flag) {
-                                float ea;
-                                float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
-                                w = T * a;
-                                const float tn = fmaf(-T, a, T);
-                                const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
-                                const float ew = epsT + ea + 1.2e-7f;
-                                flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
-                                       fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
-                                if (!flag) {
-                                    C0 = fmaf(w, r.rgb[0], C0);
-                                    C1 = fmaf(w, r.rgb[1], C1);
-                                    C2 = fmaf(w, r.rgb[2], C2);
-                                    contrib = true;
-                                    last = b + j;
-                                    cnt++;
-                                    T = tn;
-                                    epsT = en;
-                                    done = T < T_MIN_F;
-                                }
-                            }
-                            if (flag) {
-                                flag_pos = b + j;
-                                done = true;
-                            }
+            const int ex = x - c0 - c1;
+            __syncwarp();
+            s_pre[tid * 2] = ex;
+            s_pre[tid * 2 + 1] = ex + c0;
+            if (tid == 31) s_pre[64] = x;
+        }
+        __syncthreads();
+        // ---- B: dense pair evaluation ----
+        {
+            const int P = s_pre[nb];
+            const int per = (P + 255) >> 8;
+            int q = tid * per;
+            const int qend = min(q + per, P);
+            if (q < qend) {
+                int lo = 0, hi = nb - 1;  // largest j with s_pre[j] <= q
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_pre[mid] <= q) lo = mid; else hi = mid - 1;
+                }
+                int j = lo;
+                int jend = s_pre[j + 1];
+                int geo = s_geo[j];
+                int w = (geo >> 8) & 0xff;
+                int tt = q - s_pre[j];
+                int col = tt % w, row = tt / w;
+                double a0 = s_a[0][j], a1 = s_a[1][j], a2 = s_a[2][j], a3 = s_a[3][j], a4 = s_a[4][j],
+                       a5 = s_a[5][j], a6 = s_a[6][j], a7 = s_a[7][j], a8 = s_a[8][j];
+                double rlo = s_rlo[j], rhi = s_rhi[j];
+                for (; q < qend; q++) {
+                    while (q >= jend) {
+                        j++;
+                        jend = s_pre[j + 1];
+                        geo = s_geo[j];
+                        w = (geo >> 8) & 0xff;
+                        col = 0;
+                        row = 0;
+                        a0 = s_a[0][j]; a1 = s_a[1][j]; a2 = s_a[2][j]; a3 = s_a[3][j]; a4 = s_a[4][j];
+                        a5 = s_a[5][j]; a6 = s_a[6][j]; a7 = s_a[7][j]; a8 = s_a[8][j];
+                        rlo = s_rlo[j];
+                        rhi = s_rhi[j];
+                    }
+                    const int lx = (geo & 0xff) + col, ly = (geo >> 16) + row;
+                    const int pidx = ly * TILE + lx;
+                    if (++col == w) { col = 0; row++; }
+                    if (s_done[pidx]) continue;
+                    const double pcx = TX0 + lx + 0.5, pcy = TY0 + ly + 0.5;
+                    const double l0 = fma(a0, pcx, fma(a1, pcy, a2));
+                    const double l1 = fma(a3, pcx, fma(a4, pcy, a5));
+                    const double l2 = fma(a6, pcx, fma(a7, pcy, a8));
+                    if (!(l0 >= rlo && l1 >= rlo && l2 >= rlo)) continue;
+                    const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
+                    float a = -1.f, ea = 0.f;
+                    if (rr > rhi) {
+                        if (opt.mode == 0) {
+                            const float rf = (float)fmin(rr, 1.0);
+                            const float lg = fast_lg2(rf);
+                            const float arg = fmaf(s_f0[j], lg, s_f1[j]);
+                            a = fast_ex2(arg);
+                            ea = 5e-7f + s_f0[j] * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
+                        } else {
+                            const float x = (float)rr * s_f0[j];
+                            a = __fdividef(s_f1[j], 1.0f + fast_ex2(fminf(x, 1009.9f)));
+                            ea = 8e-7f + 1.2e-7f * fabsf(x);
                         }
+                        a = fminf(a, ALPHA_CLAMP_F);
+                    }
+                    const int k = atomicAdd(&s_cnt[pidx], 1);
+                    if (k < NSLOT) {
+                        s_sa[k][pidx] = a;
+                        s_se[k][pidx] = ea;
+                        s_sj[k][pidx] = (unsigned char)j;
+                    } else {
+                        s_ovf[pidx] = 1;
                     }
                 }
-                if (done) gmask = 0u;
-                if (contrib) {
-                    atomicMax(&s_maxw[j], __float_as_uint(w));
-                    if (w > tau) atomicAdd(&s_pix[j], 1);
-                }
             }
         }
         __syncthreads();
-        if (threadIdx.x < nb) {
-            const unsigned src = s_src[threadIdx.x];
-            if (s_maxw[threadIdx.x] && out.max_weight)
-                atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
-            if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
-            s_maxw[threadIdx.x] = 0u;
-            s_pix[threadIdx.x] = 0;
+        // ---- C: per-pixel compositing in entry order ----
+        if (!done) {
+            const int n = s_cnt[tid];
+            if (s_ovf[tid]) {
+                flag_pos = b;  // conservative: nothing of this batch was committed
+                done = true;
+            } else if (n > 0) {
+                // insertion sort of the slots by entry index (n <= NSLOT, usually 1-3)
+                for (int i = 1; i < n; i++) {
+                    const unsigned char jj = s_sj[i][tid];
+                    const float aa = s_sa[i][tid], ee = s_se[i][tid];
+                    int k = i - 1;
+                    while (k >= 0 && s_sj[k][tid] > jj) {
+                        s_sj[k + 1][tid] = s_sj[k][tid];
+                        s_sa[k + 1][tid] = s_sa[k][tid];
+                        s_se[k + 1][tid] = s_se[k][tid];
+                        k--;
+                    }
+                    s_sj[k + 1][tid] = jj;
+                    s_sa[k + 1][tid] = aa;
+                    s_se[k + 1][tid] = ee;
+                }
+                for (int i = 0; i < n && !done; i++) {
+                    const int j = s_sj[i][tid];
+                    const float a = s_sa[i][tid];
+                    if (a < 0.f) {  // r inside the contribution guard band
+                        flag_pos = b + j;
+                        done = true;
+                        break;
+                    }
+                    const float ea = s_se[i][tid];
+                    const float w = T * a;
+                    const float tn = fmaf(-T, a, T);
+                    const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                    const float ew = epsT + ea + 1.2e-7f;
+                    if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                        fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f)) {
+                        flag_pos = b + j;
+                        done = true;
+                        break;
+                    }
+                    C0 = fmaf(w, s_rgb[0][j], C0);
+                    C1 = fmaf(w, s_rgb[1][j], C1);
+                    C2 = fmaf(w, s_rgb[2][j], C2);
+                    last = b + j;
+                    cnt++;
+                    T = tn;
+                    epsT = en;
+                    atomicMax(&s_maxw[j], __float_as_uint(w));
+                    if (w > tau) atomicAdd(&s_pix[j], 1);
+                    if (T < T_MIN_F) done = true;
+                }
+            }
+            s_done[tid] = done ? 1 : 0;
+        }
+        s_cnt[tid] = 0;
+        s_ovf[tid] = 0;
+        __syncthreads();
+        if (tid < nb) {
+            const unsigned src = s_src[tid];
+            if (s_maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, s_maxw[tid]);
+            if (s_pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[tid]);
+            s_maxw[tid] = 0u;
+            s_pix[tid] = 0;
         }
     }
     if (inside) {
