@@ -272,8 +272,10 @@ __device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mo
 // A pixel whose slot list overflows, or whose decision lands inside the guard
 // band, is flagged and recomputed exactly by k_fixup_fwd.
 // ---------------------------------------------------------------------------
-constexpr int FB = 64;
-constexpr int NSLOT = 12;
+constexpr int FB = 64;       // entries staged per batch
+constexpr int PMAX = 4096;   // (entry, pixel) pairs per batch
+constexpr int NSLOT = 12;    // contributing fragments per pixel per batch
+constexpr int SREC_W = 36;   // staged record stride in 32-bit words (144 B: conflict-free broadcasts)
 
 __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                     const short4* __restrict__ bbox,
@@ -281,26 +283,29 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                                                     const unsigned* __restrict__ ent_src,
                                                     FastBlendOut out) {
     (void)bbox;
-    __shared__ double s_a[9][FB];
-    __shared__ double s_rlo[FB], s_rhi[FB];
-    __shared__ float s_f0[FB], s_f1[FB];
-    __shared__ float s_rgb[3][FB];
+    __shared__ __align__(16) unsigned s_rec[FB * SREC_W];
     __shared__ unsigned s_src[FB];
-    __shared__ int s_geo[FB];      // cx0 | w << 8 | ry0 << 16  (bbox clipped to the tile)
-    __shared__ int s_pre[FB + 1];  // exclusive prefix of pair counts
+    __shared__ int s_geo[FB];                 // cx0 | w << 8 | ry0 << 16
+    __shared__ int s_pre[FB + 1];             // exclusive prefix of pair counts
+    __shared__ unsigned char s_pe[PMAX];      // pair -> entry
+    __shared__ unsigned char s_pp[PMAX];      // pair -> pixel
+    __shared__ unsigned short s_wl[PMAX];     // candidate pairs
+    __shared__ float s_wr[PMAX];              // their r (fp32), or -1 for the guard band
+    __shared__ int s_wn, s_nbe;
     __shared__ unsigned s_maxw[FB];
     __shared__ int s_pix[FB];
     __shared__ unsigned char s_done[TILE_PIX];
     __shared__ unsigned char s_ovf[TILE_PIX];
     __shared__ int s_cnt[TILE_PIX];
-    __shared__ float s_sa[NSLOT][TILE_PIX];          // alpha (or -1: guard band)
-    __shared__ float s_se[NSLOT][TILE_PIX];          // relative error bound of alpha
-    __shared__ unsigned char s_sj[NSLOT][TILE_PIX];  // entry index in the batch
+    __shared__ float s_sa[NSLOT][TILE_PIX];
+    __shared__ float s_se[NSLOT][TILE_PIX];
+    __shared__ unsigned char s_sj[NSLOT][TILE_PIX];
 
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
     const int TX0 = tx * TILE, TY0 = ty * TILE;
     const int tid = threadIdx.x;
+    const unsigned lane = tid & 31;
     const int px = TX0 + (tid & 15), py = TY0 + (tid >> 4);
     const bool inside = px < cam.width && py < cam.height;
     float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
@@ -315,76 +320,69 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
         s_maxw[tid] = 0u;
         s_pix[tid] = 0;
     }
-    for (int b = s; b < e; b += FB) {
+    int b = s;
+    while (b < e) {
         if (__syncthreads_count(!done) == 0) break;
-        const int nb = min(FB, e - b);
-        // ---- stage the batch (SoA) ----
-        for (int c = tid; c < nb * 8; c += 256) {
+        const int nb0 = min(FB, e - b);
+        // ---- stage up to FB records (144-byte stride) ----
+        for (int c = tid; c < nb0 * 8; c += 256) {
             const int j = c >> 3, q = c & 7;
             const unsigned src = __ldg(ent_src + b + j);
             const float4 v = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
-            const double2 d = *reinterpret_cast<const double2*>(&v);
-            switch (q) {
-                case 0: s_a[0][j] = d.x; s_a[1][j] = d.y; break;
-                case 1: s_a[2][j] = d.x; s_a[3][j] = d.y; break;
-                case 2: s_a[4][j] = d.x; s_a[5][j] = d.y; break;
-                case 3: s_a[6][j] = d.x; s_a[7][j] = d.y; break;
-                case 4: s_a[8][j] = d.x; break;
-                case 5: s_rlo[j] = d.x; s_rhi[j] = d.y; break;
-                case 6: s_f0[j] = v.x; s_f1[j] = v.y; s_rgb[0][j] = v.z; s_rgb[1][j] = v.w; break;
-                default: {
-                    s_rgb[2][j] = v.x;
-                    s_src[j] = src;
-                    const int xx = __float_as_int(v.y), yy = __float_as_int(v.z);
-                    const int x0 = (short)(xx & 0xffff), x1 = (short)(xx >> 16);
-                    const int y0 = (short)(yy & 0xffff), y1 = (short)(yy >> 16);
-                    const int cx0 = max(x0 - TX0, 0), cx1 = min(x1 - TX0, TILE);
-                    const int ry0 = max(y0 - TY0, 0), ry1 = min(y1 - TY0, TILE);
-                    const int w = max(cx1 - cx0, 0), h = max(ry1 - ry0, 0);
-                    s_geo[j] = cx0 | (w << 8) | (ry0 << 16);
-                    s_pre[j + 1] = w * h;  // counts, scanned below
-                }
+            *reinterpret_cast<float4*>(&s_rec[j * SREC_W + q * 4]) = v;
+            if (q == 7) {
+                s_src[j] = src;
+                const int xx = __float_as_int(v.y), yy = __float_as_int(v.z);
+                const int cx0 = max((int)(short)(xx & 0xffff) - TX0, 0), cx1 = min((int)(short)(xx >> 16) - TX0, TILE);
+                const int ry0 = max((int)(short)(yy & 0xffff) - TY0, 0), ry1 = min((int)(short)(yy >> 16) - TY0, TILE);
+                const int w = max(cx1 - cx0, 0), h = max(ry1 - ry0, 0);
+                s_geo[j] = cx0 | (w << 8) | (ry0 << 16);
+                s_pre[j + 1] = w * h;
             }
         }
+        if (tid == 0) s_wn = 0;
         __syncthreads();
         if (tid < 32) {
-            // exclusive scan of the pair counts (two values per lane)
-            const int c0 = tid * 2 < nb ? s_pre[tid * 2 + 1] : 0;
-            const int c1 = tid * 2 + 1 < nb ? s_pre[tid * 2 + 2] : 0;
+            const int c0 = tid * 2 < nb0 ? s_pre[tid * 2 + 1] : 0;
+            const int c1 = tid * 2 + 1 < nb0 ? s_pre[tid * 2 + 2] : 0;
             int x = c0 + c1;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, x, off);
-                if (tid >= off) x += y;
+                if ((int)lane >= off) x += y;
             }
             const int ex = x - c0 - c1;
             __syncwarp();
             s_pre[tid * 2] = ex;
             s_pre[tid * 2 + 1] = ex + c0;
-            if (tid == 31) s_pre[64] = x;
+            if (tid == 31) s_pre[FB] = x;
+            __syncwarp();
+            // entries of this batch: as many as fit in PMAX pairs (at least one; one entry <= 256)
+            const unsigned fits = __ballot_sync(0xffffffffu, s_pre[tid * 2 + 1] <= PMAX && tid * 2 < nb0);
+            const unsigned fits2 = __ballot_sync(0xffffffffu, s_pre[tid * 2 + 2] <= PMAX && tid * 2 + 1 < nb0);
+            if (tid == 0) {
+                // number of leading entries j with pre[j+1] <= PMAX
+                const int n1 = __popc(fits), n2 = __popc(fits2);
+                s_nbe = max(1, min(nb0, n1 + n2));
+            }
         }
         __syncthreads();
-        // ---- B: dense pair evaluation ----
+        const int nb = s_nbe;
+        const int P = s_pre[nb];
+        // ---- B0: pair -> (entry, pixel) map, contiguous slice per thread ----
         {
-            const int P = s_pre[nb];
             const int per = (P + 255) >> 8;
             int q = tid * per;
             const int qend = min(q + per, P);
             if (q < qend) {
-                int lo = 0, hi = nb - 1;  // largest j with s_pre[j] <= q
+                int lo = 0, hi = nb - 1;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
                     if (s_pre[mid] <= q) lo = mid; else hi = mid - 1;
                 }
-                int j = lo;
-                int jend = s_pre[j + 1];
-                int geo = s_geo[j];
-                int w = (geo >> 8) & 0xff;
+                int j = lo, jend = s_pre[j + 1], geo = s_geo[j], w = (geo >> 8) & 0xff;
                 int tt = q - s_pre[j];
                 int col = tt % w, row = tt / w;
-                double a0 = s_a[0][j], a1 = s_a[1][j], a2 = s_a[2][j], a3 = s_a[3][j], a4 = s_a[4][j],
-                       a5 = s_a[5][j], a6 = s_a[6][j], a7 = s_a[7][j], a8 = s_a[8][j];
-                double rlo = s_rlo[j], rhi = s_rhi[j];
                 for (; q < qend; q++) {
                     while (q >= jend) {
                         j++;
@@ -393,44 +391,79 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                         w = (geo >> 8) & 0xff;
                         col = 0;
                         row = 0;
-                        a0 = s_a[0][j]; a1 = s_a[1][j]; a2 = s_a[2][j]; a3 = s_a[3][j]; a4 = s_a[4][j];
-                        a5 = s_a[5][j]; a6 = s_a[6][j]; a7 = s_a[7][j]; a8 = s_a[8][j];
-                        rlo = s_rlo[j];
-                        rhi = s_rhi[j];
                     }
-                    const int lx = (geo & 0xff) + col, ly = (geo >> 16) + row;
-                    const int pidx = ly * TILE + lx;
+                    s_pe[q] = (unsigned char)j;
+                    s_pp[q] = (unsigned char)((((geo >> 16) + row) << 4) + (geo & 0xff) + col);
                     if (++col == w) { col = 0; row++; }
-                    if (s_done[pidx]) continue;
-                    const double pcx = TX0 + lx + 0.5, pcy = TY0 + ly + 0.5;
-                    const double l0 = fma(a0, pcx, fma(a1, pcy, a2));
-                    const double l1 = fma(a3, pcx, fma(a4, pcy, a5));
-                    const double l2 = fma(a6, pcx, fma(a7, pcy, a8));
-                    if (!(l0 >= rlo && l1 >= rlo && l2 >= rlo)) continue;
-                    const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
-                    float a = -1.f, ea = 0.f;
-                    if (rr > rhi) {
-                        if (opt.mode == 0) {
-                            const float rf = (float)fmin(rr, 1.0);
-                            const float lg = fast_lg2(rf);
-                            const float arg = fmaf(s_f0[j], lg, s_f1[j]);
-                            a = fast_ex2(arg);
-                            ea = 5e-7f + s_f0[j] * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
-                        } else {
-                            const float x = (float)rr * s_f0[j];
-                            a = __fdividef(s_f1[j], 1.0f + fast_ex2(fminf(x, 1009.9f)));
-                            ea = 8e-7f + 1.2e-7f * fabsf(x);
-                        }
-                        a = fminf(a, ALPHA_CLAMP_F);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- B1: dense fp64 evaluation of all pairs; candidates -> work list ----
+        for (int q0 = 0; q0 < P; q0 += 256) {
+            const int q = q0 + tid;
+            bool cand = false;
+            float rf = 0.f;
+            if (q < P) {
+                const int pidx = s_pp[q];
+                if (!s_done[pidx]) {
+                    const double* r = reinterpret_cast<const double*>(&s_rec[s_pe[q] * SREC_W]);
+                    const double pcx = TX0 + (pidx & 15) + 0.5, pcy = TY0 + (pidx >> 4) + 0.5;
+                    const double rlo = r[10];
+                    const double l0 = fma(r[0], pcx, fma(r[1], pcy, r[2]));
+                    const double l1 = fma(r[3], pcx, fma(r[4], pcy, r[5]));
+                    const double l2 = fma(r[6], pcx, fma(r[7], pcy, r[8]));
+                    if (l0 >= rlo && l1 >= rlo && l2 >= rlo) {
+                        const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
+                        cand = true;
+                        // r for alpha, or NaN: inside the guard band, resolved by the fix-up
+                        rf = rr > r[11] ? (float)(opt.mode == 0 ? fmin(rr, 1.0) : rr) : __int_as_float(0x7fc00000);
                     }
-                    const int k = atomicAdd(&s_cnt[pidx], 1);
-                    if (k < NSLOT) {
-                        s_sa[k][pidx] = a;
-                        s_se[k][pidx] = ea;
-                        s_sj[k][pidx] = (unsigned char)j;
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, cand);
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&s_wn, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (cand) {
+                    const int idx = base + __popc(m & lanemask_lt());
+                    s_wl[idx] = (unsigned short)q;
+                    s_wr[idx] = rf;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- B2: alpha for the candidates (dense), append to per-pixel slots ----
+        {
+            const int wn = s_wn;
+            for (int i = tid; i < wn; i += 256) {
+                const int q = s_wl[i];
+                const int j = s_pe[q], pidx = s_pp[q];
+                const float* rf32 = reinterpret_cast<const float*>(&s_rec[j * SREC_W + 24]);  // f0 f1 rgb...
+                float a = -1.f, ea = 0.f;
+                const float rr = s_wr[i];
+                const bool band = isnan(rr);
+                if (!band) {
+                    if (opt.mode == 0) {
+                        const float lg = fast_lg2(rr);
+                        const float arg = fmaf(rf32[0], lg, rf32[1]);
+                        a = fast_ex2(arg);
+                        ea = 5e-7f + rf32[0] * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
                     } else {
-                        s_ovf[pidx] = 1;
+                        const float x = rr * rf32[0];
+                        a = __fdividef(rf32[1], 1.0f + fast_ex2(fminf(x, 1009.9f)));
+                        ea = 8e-7f + 1.2e-7f * fabsf(x);
                     }
+                    a = fminf(a, ALPHA_CLAMP_F);
+                }
+                const int k = atomicAdd(&s_cnt[pidx], 1);
+                if (k < NSLOT) {
+                    s_sa[k][pidx] = a;
+                    s_se[k][pidx] = ea;
+                    s_sj[k][pidx] = (unsigned char)j;
+                } else {
+                    s_ovf[pidx] = 1;
                 }
             }
         }
@@ -439,10 +472,9 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
         if (!done) {
             const int n = s_cnt[tid];
             if (s_ovf[tid]) {
-                flag_pos = b;  // conservative: nothing of this batch was committed
+                flag_pos = b;  // conservative: nothing of this batch was committed for this pixel
                 done = true;
             } else if (n > 0) {
-                // insertion sort of the slots by entry index (n <= NSLOT, usually 1-3)
                 for (int i = 1; i < n; i++) {
                     const unsigned char jj = s_sj[i][tid];
                     const float aa = s_sa[i][tid], ee = s_se[i][tid];
@@ -457,7 +489,7 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                     s_sa[k + 1][tid] = aa;
                     s_se[k + 1][tid] = ee;
                 }
-                for (int i = 0; i < n && !done; i++) {
+                for (int i = 0; i < n; i++) {
                     const int j = s_sj[i][tid];
                     const float a = s_sa[i][tid];
                     if (a < 0.f) {  // r inside the contribution guard band
@@ -476,16 +508,20 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                         done = true;
                         break;
                     }
-                    C0 = fmaf(w, s_rgb[0][j], C0);
-                    C1 = fmaf(w, s_rgb[1][j], C1);
-                    C2 = fmaf(w, s_rgb[2][j], C2);
+                    const float* rgb = reinterpret_cast<const float*>(&s_rec[j * SREC_W + 26]);
+                    C0 = fmaf(w, rgb[0], C0);
+                    C1 = fmaf(w, rgb[1], C1);
+                    C2 = fmaf(w, rgb[2], C2);
                     last = b + j;
                     cnt++;
                     T = tn;
                     epsT = en;
                     atomicMax(&s_maxw[j], __float_as_uint(w));
                     if (w > tau) atomicAdd(&s_pix[j], 1);
-                    if (T < T_MIN_F) done = true;
+                    if (T < T_MIN_F) {
+                        done = true;
+                        break;
+                    }
                 }
             }
             s_done[tid] = done ? 1 : 0;
@@ -497,9 +533,12 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
             const unsigned src = s_src[tid];
             if (s_maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, s_maxw[tid]);
             if (s_pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[tid]);
+        }
+        if (tid < FB) {
             s_maxw[tid] = 0u;
             s_pix[tid] = 0;
         }
+        b += nb;
     }
     if (inside) {
         const int p = py * cam.width + px;
