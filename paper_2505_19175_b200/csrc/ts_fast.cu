@@ -287,19 +287,20 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
     __shared__ unsigned s_src[FB];
     __shared__ int s_geo[FB];                 // cx0 | w << 8 | ry0 << 16
     __shared__ int s_pre[FB + 1];             // exclusive prefix of pair counts
-    __shared__ unsigned char s_pe[PMAX];      // pair -> entry
-    __shared__ unsigned char s_pp[PMAX];      // pair -> pixel
-    __shared__ unsigned short s_wl[PMAX];     // candidate pairs
-    __shared__ float s_wr[PMAX];              // their r (fp32), or -1 for the guard band
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    float* s_wr = reinterpret_cast<float*>(s_dyn);                                  // [PMAX] r, NaN: band
+    float (*s_sa)[TILE_PIX] = reinterpret_cast<float (*)[TILE_PIX]>(s_wr + PMAX);   // [NSLOT][256] alpha
+    float (*s_se)[TILE_PIX] = s_sa + NSLOT;                                         // [NSLOT][256] eps
+    unsigned short* s_wl = reinterpret_cast<unsigned short*>(s_se + NSLOT);        // [PMAX] candidates
+    unsigned char* s_pe = reinterpret_cast<unsigned char*>(s_wl + PMAX);           // [PMAX] pair -> entry
+    unsigned char* s_pp = s_pe + PMAX;                                              // [PMAX] pair -> pixel
+    unsigned char (*s_sj)[TILE_PIX] = reinterpret_cast<unsigned char (*)[TILE_PIX]>(s_pp + PMAX);
     __shared__ int s_wn, s_nbe;
     __shared__ unsigned s_maxw[FB];
     __shared__ int s_pix[FB];
     __shared__ unsigned char s_done[TILE_PIX];
     __shared__ unsigned char s_ovf[TILE_PIX];
     __shared__ int s_cnt[TILE_PIX];
-    __shared__ float s_sa[NSLOT][TILE_PIX];
-    __shared__ float s_se[NSLOT][TILE_PIX];
-    __shared__ unsigned char s_sj[NSLOT][TILE_PIX];
 
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
@@ -637,11 +638,18 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
     }
 }
 
+constexpr size_t BLEND_DYN_SMEM = PMAX * 4 + 2 * NSLOT * TILE_PIX * 4 + PMAX * 2 + 2 * PMAX + NSLOT * TILE_PIX;
+
 void launch_blend_fast(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                        cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_blend_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BLEND_DYN_SMEM);
+        attr = true;
+    }
     int ntiles = cam.ntx * cam.nty;
-    k_blend_fast<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
+    k_blend_fast<<<ntiles, 256, BLEND_DYN_SMEM, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
 }
 
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
