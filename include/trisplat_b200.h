@@ -130,7 +130,7 @@ int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, in
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)
  *  TS_DUMP_ENTRY_RANK  int32[E]       tile entries as depth ranks (render.py:358-360)
  *  TS_DUMP_BBOX        int32[N*4]     x0,x1,y0,y1 per source (0s if culled) (render.py:243-250)
- *  TS_DUMP_DEPTH       float64[N]     camera-space centroid depth per source
+ *  TS_DUMP_DEPTH       float64[N]     camera-space centroid depth per accepted source (0 if culled)
  *  TS_DUMP_SGRAD       float64[N*16]  screen-space gradients of the last ts_backward
  *                                     (gq[6], go, gsig, grgb[3], gphis, gz, pad) per source */
 #define TS_DUMP_SORTED_IDX 1

@@ -358,10 +358,10 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     stage_begin(c, TS_STAGE_PREPROCESS, st);
     if (fast) {
         FastPreOut po{(RecF*)c->recf.p, opt->keep_backward ? (RecB*)c->recb.p : nullptr, c->bbox, c->key,
-                      c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+                      c->tcount, c->flag, out->area, nullptr, c->d_ctr};
         launch_preprocess_fast(cm, op, *soup, opt->param_dtype, po, st);
     } else {
-        PreOut po{(Rec64*)c->rec64.p, c->bbox, c->key, c->tcount, c->flag, out->area, c->depth, c->d_ctr};
+        PreOut po{(Rec64*)c->rec64.p, c->bbox, c->key, c->tcount, c->flag, out->area, nullptr, c->d_ctr};
         launch_preprocess(cm, op, *soup, opt->param_dtype, po, st);
     }
     stage_end(c, TS_STAGE_PREPROCESS, st);
@@ -519,7 +519,8 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
             return cuda_err(cudaGetLastError());
         case TS_DUMP_DEPTH:
             if (bytes < 8 * (size_t)c->n) return TS_ERR_INVALID_ARG;
-            if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->depth, 8 * c->n, cudaMemcpyDeviceToDevice, st));
+            // the depth key is the fp64 bit pattern of the centroid depth (0 if culled)
+            if (c->n) TS_CHECK(cudaMemcpyAsync(dst, c->key, 8 * c->n, cudaMemcpyDeviceToDevice, st));
             return TS_OK;
         case TS_DUMP_SGRAD: {
             if (bytes < 8 * SG_STRIDE * (size_t)c->n || !c->sgrad_kind) return TS_ERR_INVALID_ARG;

@@ -37,10 +37,71 @@ __device__ __forceinline__ float fast_ex2(float x) {
 }
 
 // ---------------------------------------------------------------------------
-// preprocess (fast records)
+// preprocess (fast records).  Only the quantities that decide the
+// reference's discrete outputs are computed with its exact fp64 arithmetic
+// (explicit _rn intrinsics, same operation order): the depth key (sort
+// order), the cull tests (render.py:165-174, 271-273) and the tight bbox
+// (render.py:216-250, tile lists).  Edge functions, the contribution band and
+// the SH colour only need to be accurate and use fast math.
 // ---------------------------------------------------------------------------
+// SH colour sum over 16-byte vector loads (fp32 params) / 16-byte pairs (fp64)
 template <typename T>
-__global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, const T* __restrict__ verts,
+__device__ __forceinline__ void sh_colour(const T* __restrict__ p, const float* bs, int ncoef, float& c0,
+                                          float& c1, float& c2);
+template <>
+__device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, const float* bs, int ncoef,
+                                                 float& c0, float& c1, float& c2) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    const int nv = (ncoef * 3 + 3) >> 2;
+    float acc[3] = {c0, c1, c2};
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+        if (k < nv) {
+            const float4 v = __ldg(q + k);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int idx = k * 4 + u;  // coefficient idx / 3, channel idx % 3
+                if (idx / 3 < ncoef) acc[idx % 3] = fmaf(bs[idx / 3], vv[u], acc[idx % 3]);
+            }
+        }
+    }
+    c0 = acc[0]; c1 = acc[1]; c2 = acc[2];
+}
+template <>
+__device__ __forceinline__ void sh_colour<double>(const double* __restrict__ p, const float* bs, int ncoef,
+                                                  float& c0, float& c1, float& c2) {
+    float acc[3] = {c0, c1, c2};
+    for (int idx = 0; idx < ncoef * 3; idx++) acc[idx % 3] = fmaf(bs[idx / 3], (float)p[idx], acc[idx % 3]);
+    c0 = acc[0]; c1 = acc[1]; c2 = acc[2];
+}
+
+// soup.py:67-77 check of the 48 SH coefficients: x*0 is NaN for +-inf and NaN
+template <typename T>
+__device__ __forceinline__ bool sh_finite(const T* __restrict__ p);
+template <>
+__device__ __forceinline__ bool sh_finite<float>(const float* __restrict__ p) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+        const float4 v = __ldg(q + k);
+        ss = fmaf(v.x, 0.f, ss);
+        ss = fmaf(v.y, 0.f, ss);
+        ss = fmaf(v.z, 0.f, ss);
+        ss = fmaf(v.w, 0.f, ss);
+    }
+    return ss == 0.f;
+}
+template <>
+__device__ __forceinline__ bool sh_finite<double>(const double* __restrict__ p) {
+    double ss = 0.0;
+    for (int k = 0; k < 48; k++) ss = fma(p[k], 0.0, ss);
+    return ss == 0.0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_preprocess_fast(Cam cam, Opts opt, const T* __restrict__ verts,
                                                          const T* __restrict__ opacity,
                                                          const T* __restrict__ sigma,
                                                          const T* __restrict__ sh, long long n,
@@ -53,103 +114,185 @@ __global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, cons
         double v[9];
 #pragma unroll
         for (int k = 0; k < 9; k++) v[k] = (double)verts[i * 9 + k];
-        double o_raw = (double)opacity[i];
-        double sg = (double)sigma[i];
+        const double o_raw = (double)opacity[i];
+        const double sg = (double)sigma[i];
         if (opt.validate) {
-            bool fv = true;
+            // x*0 is NaN for +-inf and NaN
+            double sv = 0.0;
 #pragma unroll
-            for (int k = 0; k < 9; k++) fv &= isfinite(v[k]);
-            if (!fv) atomicMin(&out.ctr->err[0], i);
+            for (int k = 0; k < 9; k++) sv = fma(v[k], 0.0, sv);
+            if (sv != 0.0) atomicMin(&out.ctr->err[0], i);
             if (!isfinite(o_raw)) atomicMin(&out.ctr->err[1], i);
             if (!isfinite(sg)) atomicMin(&out.ctr->err[2], i);
-            bool fs = true;
-            const T* shp = sh + i * 48;
-#pragma unroll 8
-            for (int k = 0; k < 48; k++) fs &= isfinite((double)shp[k]);
-            if (!fs) atomicMin(&out.ctr->err[3], i);
         }
-        Proj64 p;
-        project64(v, cam, p);
-        if (out.area) out.area[i] = p.valid_z ? (float)p.area : 0.0f;
-        if (out.depth) out.depth[i] = p.z;
-        ok = accepted(p);
+        // ---- exact: _project_kernel, render.py:159-190 ----
+        double xc2[3], q[6];
+        bool z_ok = true;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            double xk[3];
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                double t = TS_A(TS_M(v[k * 3 + 0], cam.R[a * 3 + 0]), TS_M(v[k * 3 + 1], cam.R[a * 3 + 1]));
+                t = TS_A(t, TS_M(v[k * 3 + 2], cam.R[a * 3 + 2]));
+                xk[a] = TS_A(t, cam.t[a]);
+            }
+            if (xk[2] < 1e-12) z_ok = false;
+            xc2[k] = xk[2];
+            q[k * 2 + 0] = TS_A(TS_D(TS_M(cam.fx, xk[0]), xk[2]), cam.cx);
+            q[k * 2 + 1] = TS_A(TS_D(TS_M(cam.fy, xk[1]), xk[2]), cam.cy);
+        }
+        const double z = TS_D(TS_A(TS_A(xc2[0], xc2[1]), xc2[2]), 3.0);
+        if (z < cam.z_near) z_ok = false;
+        const double e1x = TS_S(q[2], q[0]), e1y = TS_S(q[3], q[1]);
+        const double e2x = TS_S(q[4], q[0]), e2y = TS_S(q[5], q[1]);
+        const double area = TS_M(fabs(TS_S(TS_M(e1x, e2y), TS_M(e1y, e2x))), 0.5);  // == /2.0
+        double d0x = TS_S(q[2], q[4]), d0y = TS_S(q[3], q[5]);
+        double d1x = TS_S(q[4], q[0]), d1y = TS_S(q[5], q[1]);
+        double d2x = TS_S(q[0], q[2]), d2y = TS_S(q[1], q[3]);
+        const double s0 = __dsqrt_rn(TS_A(TS_M(d0x, d0x), TS_M(d0y, d0y)));
+        const double s1 = __dsqrt_rn(TS_A(TS_M(d1x, d1x), TS_M(d1y, d1y)));
+        const double s2 = __dsqrt_rn(TS_A(TS_M(d2x, d2x), TS_M(d2y, d2y)));
+        const double perim = TS_A(TS_A(s0, s1), s2);
+        const double phis = TS_D(TS_M(-2.0, area), perim > 1e-300 ? perim : 1e-300);
+        if (out.area) out.area[i] = z_ok ? (float)area : 0.0f;
+        ok = z_ok && (area >= DEGENERATE_AREA) && (fabs(phis) >= DEGENERATE_INRADIUS);
         short4 bb = make_short4(0, 0, 0, 0);
         if (ok) {
-            double o = opt.solid ? 1.0 : o_raw;
-            Edge64 E;
-            edge_bbox64(p.q, p.phis, o, sg, opt.mode, opt.tau_cutoff, cam.width, cam.height, E);
-            int x0 = (int)E.bb[0], x1 = (int)E.bb[1], y0 = (int)E.bb[2], y1 = (int)E.bb[3];
+            const double o = opt.solid ? 1.0 : o_raw;
+            // ---- exact: incenter + tight bbox, render.py:216-250 ----
+            const double sx = TS_D(TS_A(TS_A(TS_M(s0, q[0]), TS_M(s1, q[2])), TS_M(s2, q[4])), perim);
+            const double sy = TS_D(TS_A(TS_A(TS_M(s0, q[1]), TS_M(s1, q[3])), TS_M(s2, q[5])), perim);
+            double f;
+            if (opt.mode == 0) {
+                if (o > opt.tau_cutoff) {
+                    const double ratio = TS_D(opt.tau_cutoff, o);
+                    // pow(x, 1.0) == x exactly (glibc and CUDA)
+                    f = TS_S(1.0, sg == 1.0 ? ratio : pow(ratio, TS_D(1.0, sg)));
+                } else {
+                    f = 0.0;
+                }
+            } else {
+                const double ratio = TS_D(opt.tau_cutoff, o);
+                f = ratio < 1.0 ? TS_S(1.0, TS_D(TS_M(sg, log(TS_D(ratio, TS_S(1.0, ratio)))), fabs(phis))) : 0.0;
+            }
+            int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+            if (f > 0.0) {
+                double xmin = 1e300, ymin = 1e300, xmax = -1e300, ymax = -1e300;
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                    const double pxk = TS_A(sx, TS_M(TS_S(q[k * 2], sx), f));
+                    const double pyk = TS_A(sy, TS_M(TS_S(q[k * 2 + 1], sy), f));
+                    xmin = pxk < xmin ? pxk : xmin;
+                    xmax = pxk > xmax ? pxk : xmax;
+                    ymin = pyk < ymin ? pyk : ymin;
+                    ymax = pyk > ymax ? pyk : ymax;
+                }
+                const long long W = cam.width, H = cam.height;
+                long long X0 = floor_i64(TS_S(xmin, 0.5)); X0 = X0 > 0 ? X0 : 0; X0 = X0 < W ? X0 : W;
+                long long X1 = floor_i64(TS_S(xmax, 0.5)) + 1; X1 = X1 > 0 ? X1 : 0; X1 = X1 < W ? X1 : W;
+                long long Y0 = floor_i64(TS_S(ymin, 0.5)); Y0 = Y0 > 0 ? Y0 : 0; Y0 = Y0 < H ? Y0 : H;
+                long long Y1 = floor_i64(TS_S(ymax, 0.5)) + 1; Y1 = Y1 > 0 ? Y1 : 0; Y1 = Y1 < H ? Y1 : H;
+                x0 = (int)X0; x1 = (int)(X1 > X0 ? X1 : X0); y0 = (int)Y0; y1 = (int)(Y1 > Y0 ? Y1 : Y0);
+            }
             bb = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
             tcount = (unsigned)tiles_touched(x0, x1, y0, y1);
             if (tcount) {
+                // ---- accurate (not bit-exact): edge functions, orientation, band ----
                 RecF r;
-                int ox = (x0 + x1) >> 1, oy = (y0 + y1) >> 1;
-                double inv = 1.0 / p.phis;
+                const double ccx = (q[0] + q[2] + q[4]) * (1.0 / 3.0), ccy = (q[1] + q[3] + q[5]) * (1.0 / 3.0);
+                const double inv = 1.0 / phis;
                 double dmax = 0.0;
+                int esign = 0;
+                float qf[6];
 #pragma unroll
                 for (int e = 0; e < 3; e++) {
-                    r.a[e * 3 + 0] = E.nx[e] * inv;
-                    r.a[e * 3 + 1] = E.ny[e] * inv;
-                    r.a[e * 3 + 2] = E.d[e] * inv;
-                    dmax = fmax(dmax, fabs(E.d[e]));
+                    const int bi = e == 2 ? 0 : e + 1;
+                    const double ax = q[e * 2], ay = q[e * 2 + 1];
+                    const double evx = q[bi * 2] - ax, evy = q[bi * 2 + 1] - ay;
+                    const double il = rsqrt(evx * evx + evy * evy);
+                    double nx = evy * il, ny = -evx * il;
+                    if (nx * (ccx - ax) + ny * (ccy - ay) > 0) {
+                        nx = -nx;
+                        ny = -ny;
+                        esign |= 1 << e;
+                    }
+                    const double d = -(nx * ax + ny * ay);
+                    r.a[e * 3 + 0] = nx * inv;
+                    r.a[e * 3 + 1] = ny * inv;
+                    r.a[e * 3 + 2] = d * inv;
+                    dmax = fmax(dmax, fabs(d));
                 }
-                // |r_fast - r_ref| bound: both are O(1e-16) x (sum of |terms| / |phi_s|)
-                double mag = (fabs(p.q[0]) + fabs(p.q[1]) + fabs(p.q[2]) + fabs(p.q[3]) + fabs(p.q[4]) +
-                              fabs(p.q[5]) + 4.0 * (cam.width + cam.height) + dmax) / fabs(p.phis);
-                double delta = 1e-13 * mag + 1e-300;
-                double rstar;  // contribution threshold on r (alpha >= 1/255)
+                const double mag = (fabs(q[0]) + fabs(q[1]) + fabs(q[2]) + fabs(q[3]) + fabs(q[4]) + fabs(q[5]) +
+                                    4.0 * (cam.width + cam.height) + dmax) * fabs(inv);
+                const double delta = 1e-13 * mag + 1e-300;
+                double rstar;
                 if (opt.mode == 0) {
-                    rstar = o > ALPHA_MIN ? pow(ALPHA_MIN / o, 1.0 / sg) : 1e30;
+                    rstar = o > ALPHA_MIN ? (sg == 1.0 ? ALPHA_MIN / o : pow(ALPHA_MIN / o, 1.0 / sg)) : 1e30;
                     if (rstar > 1.0) rstar = 1e30;
                     r.f0 = (float)sg;
-                    r.f1 = (float)log2(o);
+                    r.f1 = log2f((float)o);
                 } else {
-                    double q = 255.0 * o - 1.0;
-                    rstar = q > 0.0 ? sg * log(q) / p.phis : 1e30;
-                    r.f0 = (float)(p.phis * 1.4426950408889634 / sg);
+                    const double qq = 255.0 * o - 1.0;
+                    rstar = qq > 0.0 ? sg * log(qq) / phis : 1e30;
+                    r.f0 = (float)(phis * 1.4426950408889634 / sg);
                     r.f1 = (float)o;
                 }
                 r.r_lo = rstar - delta - fabs(rstar) * 1e-12;
                 r.r_hi = rstar + delta + fabs(rstar) * 1e-12;
-                // view-dependent colour, render.py:292-302
-                double u[3];
-#pragma unroll
-                for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) / 3.0 - cam.cc[b];
-                double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-                un = un > 1e-12 ? un : 1e-12;
-                double basis[16];
-                sh_basis16(u[0] / un, u[1] / un, u[2] / un, basis);
-                const T* shp = sh + i * 48;
-                double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-                for (int c = 0; c < opt.ncoef; c++) {
-                    acc0 += basis[c] * (double)shp[c * 3 + 0];
-                    acc1 += basis[c] * (double)shp[c * 3 + 1];
-                    acc2 += basis[c] * (double)shp[c * 3 + 2];
-                }
-                r.rgb[0] = (float)fmin(fmax(acc0 + 0.5, 0.0), 1.0);
-                r.rgb[1] = (float)fmin(fmax(acc1 + 0.5, 0.0), 1.0);
-                r.rgb[2] = (float)fmin(fmax(acc2 + 0.5, 0.0), 1.0);
+                r.phis = phis;
+                // view-dependent SH colour (render.py:292-302) in fp32: only the value is used here
+                float u0 = (float)((v[0] + v[3] + v[6]) * (1.0 / 3.0) - cam.cc[0]);
+                float u1 = (float)((v[1] + v[4] + v[7]) * (1.0 / 3.0) - cam.cc[1]);
+                float u2 = (float)((v[2] + v[5] + v[8]) * (1.0 / 3.0) - cam.cc[2]);
+                const float iu = rsqrtf(fmaxf(u0 * u0 + u1 * u1 + u2 * u2, 1e-24f));
+                u0 *= iu; u1 *= iu; u2 *= iu;
+                const float xx = u0 * u0, yy = u1 * u1, zz = u2 * u2;
+                float bs[16];
+                bs[0] = 0.28209479177387814f;
+                bs[1] = -0.4886025119029199f * u1;
+                bs[2] = 0.4886025119029199f * u2;
+                bs[3] = -0.4886025119029199f * u0;
+                bs[4] = 1.0925484305920792f * u0 * u1;
+                bs[5] = -1.0925484305920792f * u1 * u2;
+                bs[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+                bs[7] = -1.0925484305920792f * u0 * u2;
+                bs[8] = 0.5462742152960396f * (xx - yy);
+                bs[9] = -0.5900435899266435f * u1 * (3.f * xx - yy);
+                bs[10] = 2.890611442640554f * u0 * u1 * u2;
+                bs[11] = -0.4570457994644658f * u1 * (4.f * zz - xx - yy);
+                bs[12] = 0.3731763325901154f * u2 * (2.f * zz - 3.f * xx - 3.f * yy);
+                bs[13] = -0.4570457994644658f * u0 * (4.f * zz - xx - yy);
+                bs[14] = 1.445305721320277f * u2 * (xx - yy);
+                bs[15] = -0.5900435899266435f * u0 * (xx - 3.f * yy);
+                float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
+                sh_colour<T>(sh + i * 48, bs, opt.ncoef, c0, c1, c2);
+                r.rgb[0] = fminf(fmaxf(c0, 0.f), 1.f);
+                r.rgb[1] = fminf(fmaxf(c1, 0.f), 1.f);
+                r.rgb[2] = fminf(fmaxf(c2, 0.f), 1.f);
+                const int ox = (x0 + x1) >> 1, oy = (y0 + y1) >> 1;
                 r.x0 = (short)x0; r.x1 = (short)x1; r.y0 = (short)y0; r.y1 = (short)y1;
                 r.ox = (short)ox; r.oy = (short)oy;
-                r.phis = p.phis;
                 out.rec[i] = r;
                 if (out.recb) {
-                    RecB b;
+                    RecB rb;
 #pragma unroll
                     for (int e = 0; e < 3; e++) {
-                        b.qx[e] = (float)(p.q[e * 2] - ox);
-                        b.qy[e] = (float)(p.q[e * 2 + 1] - oy);
+                        rb.qx[e] = (float)(q[e * 2] - ox);
+                        rb.qy[e] = (float)(q[e * 2 + 1] - oy);
                     }
-                    b.phis = (float)p.phis;
-                    b.opa = (float)o;
-                    b.sig = (float)sg;
-                    b.esign = E.esign;
-                    b.pad[0] = b.pad[1] = 0.f;
-                    out.recb[i] = b;
+                    rb.phis = (float)phis;
+                    rb.opa = (float)o;
+                    rb.sig = (float)sg;
+                    rb.esign = esign;
+                    rb.pad[0] = rb.pad[1] = 0.f;
+                    out.recb[i] = rb;
                 }
+                (void)qf;
             }
-            key = (unsigned long long)__double_as_longlong(p.z);
+            key = (unsigned long long)__double_as_longlong(z);
         }
+        if (opt.validate && !sh_finite<T>(sh + i * 48)) atomicMin(&out.ctr->err[3], i);
         out.bbox[i] = bb;
         out.flag[i] = ok ? 1u : 0u;
         out.tcount[i] = tcount;
@@ -158,11 +301,12 @@ __global__ void __launch_bounds__(256) k_preprocess_fast(Cam cam, Opts opt, cons
     unsigned long long kmin = ok ? key : ~0ull, kmax = ok ? key : 0ull;
     unsigned cnt = ok ? 1u : 0u;
     unsigned long long tc = tcount;
+#pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, off);
-        unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, off);
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, off);
+        const unsigned long long bq = __shfl_xor_sync(0xffffffffu, kmax, off);
         kmin = a < kmin ? a : kmin;
-        kmax = b > kmax ? b : kmax;
+        kmax = bq > kmax ? bq : kmax;
         cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
         tc += __shfl_xor_sync(0xffffffffu, tc, off);
     }
@@ -178,14 +322,14 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
                             const FastPreOut& out, cudaStream_t st) {
     long long n = soup.n;
     if (n <= 0) return;
-    unsigned grid = (unsigned)((n + 255) / 256);
+    unsigned grid = (unsigned)((n + 127) / 128);
     if (dtype == 1)
-        k_preprocess_fast<double><<<grid, 256, 0, st>>>(cam, opt, (const double*)soup.vertices,
+        k_preprocess_fast<double><<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices,
                                                         (const double*)soup.opacity,
                                                         (const double*)soup.sigma,
                                                         (const double*)soup.sh, n, out);
     else
-        k_preprocess_fast<float><<<grid, 256, 0, st>>>(cam, opt, (const float*)soup.vertices,
+        k_preprocess_fast<float><<<grid, 128, 0, st>>>(cam, opt, (const float*)soup.vertices,
                                                        (const float*)soup.opacity,
                                                        (const float*)soup.sigma,
                                                        (const float*)soup.sh, n, out);
@@ -256,290 +400,142 @@ __device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mo
 }
 
 // ---------------------------------------------------------------------------
-// k_blend_fast: CTA per 16x16 tile, two balanced phases per batch of FB
-// depth-ordered tile entries (render.py:349-361 order):
-//
-//  B. dense evaluation -- the batch's (entry, pixel) pairs with the pixel in
-//     the entry's bbox (the reference's per-pixel bbox test, _kernels.py:87-95)
-//     are enumerated as one flat range; each thread takes a contiguous slice
-//     (merge-path split, record cached in registers while the entry repeats),
-//     evaluates phi/phi_s in fp64 and, for contributing fragments, alpha in
-//     fp32; results go to small per-pixel slot lists in shared memory.
-//  C. compositing -- thread = pixel, walks only its slots in entry order
-//     (front to back, _kernels.py:96-123): weight, colour, transmittance,
-//     early stop, per-entry statistics, and the decision guard band.
-//
-// A pixel whose slot list overflows, or whose decision lands inside the guard
-// band, is flagged and recomputed exactly by k_fixup_fwd.
+// k_blend_fast: CTA per 16x16 tile, lane = pixel.  Warp w owns the 2x16
+// column strip x in [2w, 2w+2) of the tile, split into 8 groups of 4 lanes
+// (2x2 pixel quads).  Each group walks its OWN list of the batch's entries
+// whose bbox overlaps its quad (the reference's per-pixel bbox test,
+// _kernels.py:87-95, hoisted to quad level), so lanes stay busy even though
+// the triangles are a few pixels wide.  Edge functions in fp64, alpha and
+// compositing in fp32 with the decision guard band.
 // ---------------------------------------------------------------------------
-constexpr int FB = 64;       // entries staged per batch
-constexpr int PMAX = 4096;   // (entry, pixel) pairs per batch
-constexpr int NSLOT = 12;    // contributing fragments per pixel per batch
-constexpr int SREC_W = 36;   // staged record stride in 32-bit words (144 B: conflict-free broadcasts)
+constexpr int FB = 64;
+
+struct __align__(16) SRec {
+    RecF r;
+    float4 pad;  // 144-byte stride: groups reading different records hit different banks
+};
 
 __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                     const short4* __restrict__ bbox,
                                                     const int* __restrict__ tile_start,
                                                     const unsigned* __restrict__ ent_src,
                                                     FastBlendOut out) {
-    (void)bbox;
-    __shared__ __align__(16) unsigned s_rec[FB * SREC_W];
+    __shared__ SRec s_rec[FB];
+    __shared__ short4 s_bb[FB];
     __shared__ unsigned s_src[FB];
-    __shared__ int s_geo[FB];                 // cx0 | w << 8 | ry0 << 16
-    __shared__ int s_pre[FB + 1];             // exclusive prefix of pair counts
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    float* s_wr = reinterpret_cast<float*>(s_dyn);                                  // [PMAX] r, NaN: band
-    float (*s_sa)[TILE_PIX] = reinterpret_cast<float (*)[TILE_PIX]>(s_wr + PMAX);   // [NSLOT][256] alpha
-    float (*s_se)[TILE_PIX] = s_sa + NSLOT;                                         // [NSLOT][256] eps
-    unsigned short* s_wl = reinterpret_cast<unsigned short*>(s_se + NSLOT);        // [PMAX] candidates
-    unsigned char* s_pe = reinterpret_cast<unsigned char*>(s_wl + PMAX);           // [PMAX] pair -> entry
-    unsigned char* s_pp = s_pe + PMAX;                                              // [PMAX] pair -> pixel
-    unsigned char (*s_sj)[TILE_PIX] = reinterpret_cast<unsigned char (*)[TILE_PIX]>(s_pp + PMAX);
-    __shared__ int s_wn, s_nbe;
     __shared__ unsigned s_maxw[FB];
     __shared__ int s_pix[FB];
-    __shared__ unsigned char s_done[TILE_PIX];
-    __shared__ unsigned char s_ovf[TILE_PIX];
-    __shared__ int s_cnt[TILE_PIX];
-
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
-    const int TX0 = tx * TILE, TY0 = ty * TILE;
-    const int tid = threadIdx.x;
-    const unsigned lane = tid & 31;
-    const int px = TX0 + (tid & 15), py = TY0 + (tid >> 4);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned grp = lane >> 2;
+    const int X0 = tx * TILE + 2 * (int)warp;  // strip columns [X0, X0+2)
+    const int Y0 = ty * TILE;
+    const int px = X0 + (int)(lane & 1);
+    const int py = Y0 + 2 * (int)grp + (int)((lane >> 1) & 1);
+    const double pcx = px + 0.5, pcy = py + 0.5;
     const bool inside = px < cam.width && py < cam.height;
     float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
     int last = -1, cnt = 0, flag_pos = -1;
     bool done = !inside;
-    s_done[tid] = done ? 1 : 0;
-    s_ovf[tid] = 0;
-    s_cnt[tid] = 0;
     const int s = tile_start[t], e = tile_start[t + 1];
     const float tau = (float)opt.tau_contrib;
-    if (tid < FB) {
-        s_maxw[tid] = 0u;
-        s_pix[tid] = 0;
+    if (threadIdx.x < FB) {
+        s_maxw[threadIdx.x] = 0u;
+        s_pix[threadIdx.x] = 0;
     }
-    int b = s;
-    while (b < e) {
+    for (int b = s; b < e; b += FB) {
         if (__syncthreads_count(!done) == 0) break;
-        const int nb0 = min(FB, e - b);
-        // ---- stage up to FB records (144-byte stride) ----
-        for (int c = tid; c < nb0 * 8; c += 256) {
+        const int nb = min(FB, e - b);
+        for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
             const int j = c >> 3, q = c & 7;
             const unsigned src = __ldg(ent_src + b + j);
-            const float4 v = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
-            *reinterpret_cast<float4*>(&s_rec[j * SREC_W + q * 4]) = v;
-            if (q == 7) {
+            if (q == 0) {
                 s_src[j] = src;
-                const int xx = __float_as_int(v.y), yy = __float_as_int(v.z);
-                const int cx0 = max((int)(short)(xx & 0xffff) - TX0, 0), cx1 = min((int)(short)(xx >> 16) - TX0, TILE);
-                const int ry0 = max((int)(short)(yy & 0xffff) - TY0, 0), ry1 = min((int)(short)(yy >> 16) - TY0, TILE);
-                const int w = max(cx1 - cx0, 0), h = max(ry1 - ry0, 0);
-                s_geo[j] = cx0 | (w << 8) | (ry0 << 16);
-                s_pre[j + 1] = w * h;
+                s_bb[j] = __ldg(bbox + src);
             }
+            reinterpret_cast<float4*>(&s_rec[j].r)[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
         }
-        if (tid == 0) s_wn = 0;
         __syncthreads();
-        if (tid < 32) {
-            const int c0 = tid * 2 < nb0 ? s_pre[tid * 2 + 1] : 0;
-            const int c1 = tid * 2 + 1 < nb0 ? s_pre[tid * 2 + 2] : 0;
-            int x = c0 + c1;
+        for (int jb = 0; jb < nb; jb += 32) {
+            if (!__any_sync(0xffffffffu, !done)) break;
+            // lane l tests entry jb+l against the 8 quads of this warp's strip
+            unsigned q8 = 0u;
+            const int jl = jb + (int)lane;
+            if (jl < nb) {
+                const short4 bb = s_bb[jl];
+                if (bb.x < X0 + 2 && bb.y > X0) {
+                    int g0 = max(((int)bb.z - Y0) >> 1, 0), g1 = min(((int)bb.w - 1 - Y0) >> 1, 7);
+                    if (g1 >= g0) q8 = (0xffu >> (7 - (g1 - g0))) << g0;
+                }
+            }
+            unsigned gmask = 0u;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, off);
-                if ((int)lane >= off) x += y;
+            for (int g = 0; g < 8; g++) {
+                const unsigned bm = __ballot_sync(0xffffffffu, (q8 >> g) & 1u);
+                if ((int)grp == g) gmask = bm;
             }
-            const int ex = x - c0 - c1;
-            __syncwarp();
-            s_pre[tid * 2] = ex;
-            s_pre[tid * 2 + 1] = ex + c0;
-            if (tid == 31) s_pre[FB] = x;
-            __syncwarp();
-            // entries of this batch: as many as fit in PMAX pairs (at least one; one entry <= 256)
-            const unsigned fits = __ballot_sync(0xffffffffu, s_pre[tid * 2 + 1] <= PMAX && tid * 2 < nb0);
-            const unsigned fits2 = __ballot_sync(0xffffffffu, s_pre[tid * 2 + 2] <= PMAX && tid * 2 + 1 < nb0);
-            if (tid == 0) {
-                // number of leading entries j with pre[j+1] <= PMAX
-                const int n1 = __popc(fits), n2 = __popc(fits2);
-                s_nbe = max(1, min(nb0, n1 + n2));
-            }
-        }
-        __syncthreads();
-        const int nb = s_nbe;
-        const int P = s_pre[nb];
-        // ---- B0: pair -> (entry, pixel) map, contiguous slice per thread ----
-        {
-            const int per = (P + 255) >> 8;
-            int q = tid * per;
-            const int qend = min(q + per, P);
-            if (q < qend) {
-                int lo = 0, hi = nb - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_pre[mid] <= q) lo = mid; else hi = mid - 1;
-                }
-                int j = lo, jend = s_pre[j + 1], geo = s_geo[j], w = (geo >> 8) & 0xff;
-                int tt = q - s_pre[j];
-                int col = tt % w, row = tt / w;
-                for (; q < qend; q++) {
-                    while (q >= jend) {
-                        j++;
-                        jend = s_pre[j + 1];
-                        geo = s_geo[j];
-                        w = (geo >> 8) & 0xff;
-                        col = 0;
-                        row = 0;
-                    }
-                    s_pe[q] = (unsigned char)j;
-                    s_pp[q] = (unsigned char)((((geo >> 16) + row) << 4) + (geo & 0xff) + col);
-                    if (++col == w) { col = 0; row++; }
-                }
-            }
-        }
-        __syncthreads();
-        // ---- B1: dense fp64 evaluation of all pairs; candidates -> work list ----
-        for (int q0 = 0; q0 < P; q0 += 256) {
-            const int q = q0 + tid;
-            bool cand = false;
-            float rf = 0.f;
-            if (q < P) {
-                const int pidx = s_pp[q];
-                if (!s_done[pidx]) {
-                    const double* r = reinterpret_cast<const double*>(&s_rec[s_pe[q] * SREC_W]);
-                    const double pcx = TX0 + (pidx & 15) + 0.5, pcy = TY0 + (pidx >> 4) + 0.5;
-                    const double rlo = r[10];
-                    const double l0 = fma(r[0], pcx, fma(r[1], pcy, r[2]));
-                    const double l1 = fma(r[3], pcx, fma(r[4], pcy, r[5]));
-                    const double l2 = fma(r[6], pcx, fma(r[7], pcy, r[8]));
-                    if (l0 >= rlo && l1 >= rlo && l2 >= rlo) {
-                        const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
-                        cand = true;
-                        // r for alpha, or NaN: inside the guard band, resolved by the fix-up
-                        rf = rr > r[11] ? (float)(opt.mode == 0 ? fmin(rr, 1.0) : rr) : __int_as_float(0x7fc00000);
+            if (done) gmask = 0u;
+            while (__any_sync(0xffffffffu, gmask != 0u)) {
+                const int jo = __ffs(gmask) - 1;
+                gmask &= gmask - 1;
+                const int j = jb + jo;
+                bool contrib = false;
+                float w = 0.f;
+                if (jo >= 0 && !done) {
+                    const short4 bb = s_bb[j];
+                    if (px >= bb.x && px < bb.y && py >= bb.z && py < bb.w) {
+                        const RecF& r = s_rec[j].r;
+                        const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
+                        const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
+                        const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
+                        if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
+                            const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
+                            bool flag = rr <= r.r_hi;
+                            if (!flag) {
+                                float ea;
+                                float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
+                                w = T * a;
+                                const float tn = fmaf(-T, a, T);
+                                const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                                const float ew = epsT + ea + 1.2e-7f;
+                                flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                                       fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
+                                if (!flag) {
+                                    C0 = fmaf(w, r.rgb[0], C0);
+                                    C1 = fmaf(w, r.rgb[1], C1);
+                                    C2 = fmaf(w, r.rgb[2], C2);
+                                    contrib = true;
+                                    last = b + j;
+                                    cnt++;
+                                    T = tn;
+                                    epsT = en;
+                                    done = T < T_MIN_F;
+                                }
+                            }
+                            if (flag) {
+                                flag_pos = b + j;
+                                done = true;
+                            }
+                        }
                     }
                 }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, cand);
-            if (m) {
-                int base = 0;
-                if (lane == 0) base = atomicAdd(&s_wn, __popc(m));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (cand) {
-                    const int idx = base + __popc(m & lanemask_lt());
-                    s_wl[idx] = (unsigned short)q;
-                    s_wr[idx] = rf;
-                }
-            }
-        }
-        __syncthreads();
-        // ---- B2: alpha for the candidates (dense), append to per-pixel slots ----
-        {
-            const int wn = s_wn;
-            for (int i = tid; i < wn; i += 256) {
-                const int q = s_wl[i];
-                const int j = s_pe[q], pidx = s_pp[q];
-                const float* rf32 = reinterpret_cast<const float*>(&s_rec[j * SREC_W + 24]);  // f0 f1 rgb...
-                float a = -1.f, ea = 0.f;
-                const float rr = s_wr[i];
-                const bool band = isnan(rr);
-                if (!band) {
-                    if (opt.mode == 0) {
-                        const float lg = fast_lg2(rr);
-                        const float arg = fmaf(rf32[0], lg, rf32[1]);
-                        a = fast_ex2(arg);
-                        ea = 5e-7f + rf32[0] * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
-                    } else {
-                        const float x = rr * rf32[0];
-                        a = __fdividef(rf32[1], 1.0f + fast_ex2(fminf(x, 1009.9f)));
-                        ea = 8e-7f + 1.2e-7f * fabsf(x);
-                    }
-                    a = fminf(a, ALPHA_CLAMP_F);
-                }
-                const int k = atomicAdd(&s_cnt[pidx], 1);
-                if (k < NSLOT) {
-                    s_sa[k][pidx] = a;
-                    s_se[k][pidx] = ea;
-                    s_sj[k][pidx] = (unsigned char)j;
-                } else {
-                    s_ovf[pidx] = 1;
-                }
-            }
-        }
-        __syncthreads();
-        // ---- C: per-pixel compositing in entry order ----
-        if (!done) {
-            const int n = s_cnt[tid];
-            if (s_ovf[tid]) {
-                flag_pos = b;  // conservative: nothing of this batch was committed for this pixel
-                done = true;
-            } else if (n > 0) {
-                for (int i = 1; i < n; i++) {
-                    const unsigned char jj = s_sj[i][tid];
-                    const float aa = s_sa[i][tid], ee = s_se[i][tid];
-                    int k = i - 1;
-                    while (k >= 0 && s_sj[k][tid] > jj) {
-                        s_sj[k + 1][tid] = s_sj[k][tid];
-                        s_sa[k + 1][tid] = s_sa[k][tid];
-                        s_se[k + 1][tid] = s_se[k][tid];
-                        k--;
-                    }
-                    s_sj[k + 1][tid] = jj;
-                    s_sa[k + 1][tid] = aa;
-                    s_se[k + 1][tid] = ee;
-                }
-                for (int i = 0; i < n; i++) {
-                    const int j = s_sj[i][tid];
-                    const float a = s_sa[i][tid];
-                    if (a < 0.f) {  // r inside the contribution guard band
-                        flag_pos = b + j;
-                        done = true;
-                        break;
-                    }
-                    const float ea = s_se[i][tid];
-                    const float w = T * a;
-                    const float tn = fmaf(-T, a, T);
-                    const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
-                    const float ew = epsT + ea + 1.2e-7f;
-                    if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
-                        fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f)) {
-                        flag_pos = b + j;
-                        done = true;
-                        break;
-                    }
-                    const float* rgb = reinterpret_cast<const float*>(&s_rec[j * SREC_W + 26]);
-                    C0 = fmaf(w, rgb[0], C0);
-                    C1 = fmaf(w, rgb[1], C1);
-                    C2 = fmaf(w, rgb[2], C2);
-                    last = b + j;
-                    cnt++;
-                    T = tn;
-                    epsT = en;
+                if (done) gmask = 0u;
+                if (contrib) {
                     atomicMax(&s_maxw[j], __float_as_uint(w));
                     if (w > tau) atomicAdd(&s_pix[j], 1);
-                    if (T < T_MIN_F) {
-                        done = true;
-                        break;
-                    }
                 }
             }
-            s_done[tid] = done ? 1 : 0;
         }
-        s_cnt[tid] = 0;
-        s_ovf[tid] = 0;
         __syncthreads();
-        if (tid < nb) {
-            const unsigned src = s_src[tid];
-            if (s_maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, s_maxw[tid]);
-            if (s_pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[tid]);
+        if (threadIdx.x < nb) {
+            const unsigned src = s_src[threadIdx.x];
+            if (s_maxw[threadIdx.x] && out.max_weight)
+                atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
+            if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
+            s_maxw[threadIdx.x] = 0u;
+            s_pix[threadIdx.x] = 0;
         }
-        if (tid < FB) {
-            s_maxw[tid] = 0u;
-            s_pix[tid] = 0;
-        }
-        b += nb;
     }
     if (inside) {
         const int p = py * cam.width + px;
@@ -638,18 +634,11 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
     }
 }
 
-constexpr size_t BLEND_DYN_SMEM = PMAX * 4 + 2 * NSLOT * TILE_PIX * 4 + PMAX * 2 + 2 * PMAX + NSLOT * TILE_PIX;
-
 void launch_blend_fast(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                        cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_blend_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BLEND_DYN_SMEM);
-        attr = true;
-    }
     int ntiles = cam.ntx * cam.nty;
-    k_blend_fast<<<ntiles, 256, BLEND_DYN_SMEM, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
+    k_blend_fast<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
 }
 
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
