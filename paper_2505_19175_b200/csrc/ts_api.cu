@@ -421,9 +421,11 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
 
     if (fast) {
         FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
-                        out->n_frag, c->t_final32, c->last_pos, c->flags, c->d_ctr};
+                        out->n_frag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
+                        c->flags, c->d_ctr};
         stage_begin(c, TS_STAGE_BLEND, st);
-        launch_blend_fast(cm, op, (const RecF*)c->recf.p, c->bbox, c->tile_start, c->ent_src, bo, st);
+        launch_blend_fast(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p, c->bbox,
+                          c->tile_start, c->ent_src, bo, st);
         stage_end(c, TS_STAGE_BLEND, st);
         stage_begin(c, TS_STAGE_FIXUP, st);
         launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
@@ -470,7 +472,7 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
         if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(float) * SG_STRIDE * c->n, st));
         launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
-                              (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final32, c->last_pos,
+                              (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
                               d_image, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);

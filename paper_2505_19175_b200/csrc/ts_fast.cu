@@ -18,6 +18,8 @@
 // T<1e-4 or w>1/255 test whose operands lie within their error bound of the
 // threshold flags the pixel, which stops here and is recomputed exactly by
 // k_fixup_fwd.
+#include <type_traits>
+
 #include "ts_kernels.cuh"
 
 namespace ts {
@@ -415,12 +417,21 @@ struct __align__(16) SRec {
     float4 pad;  // 144-byte stride: groups reading different records hit different banks
 };
 
+// ACC64 (training forward, keep_backward=1): alpha with the reference formula
+// in fp64 and fp64 transmittance, so the saved T_final and every decision are
+// exact up to the ~1e-13 difference of r; the backward then reconstructs the
+// transmittances the reference uses.
+template <typename PT, bool ACC64>
 __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                     const short4* __restrict__ bbox,
                                                     const int* __restrict__ tile_start,
                                                     const unsigned* __restrict__ ent_src,
+                                                    const PT* __restrict__ opacity,
+                                                    const PT* __restrict__ sigma,
                                                     FastBlendOut out) {
+    using Real = typename std::conditional<ACC64, double, float>::type;
     __shared__ SRec s_rec[FB];
+    __shared__ double2 s_os[ACC64 ? FB : 1];  // exact (opacity, sigma)
     __shared__ short4 s_bb[FB];
     __shared__ unsigned s_src[FB];
     __shared__ unsigned s_maxw[FB];
@@ -435,7 +446,8 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
     const int py = Y0 + 2 * (int)grp + (int)((lane >> 1) & 1);
     const double pcx = px + 0.5, pcy = py + 0.5;
     const bool inside = px < cam.width && py < cam.height;
-    float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
+    Real T = 1, C0 = 0, C1 = 0, C2 = 0;
+    float epsT = 0.f;
     int last = -1, cnt = 0, flag_pos = -1;
     bool done = !inside;
     const int s = tile_start[t], e = tile_start[t + 1];
@@ -453,6 +465,8 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
             if (q == 0) {
                 s_src[j] = src;
                 s_bb[j] = __ldg(bbox + src);
+                if constexpr (ACC64)
+                    s_os[j] = make_double2(opt.solid ? 1.0 : (double)opacity[src], (double)sigma[src]);
             }
             reinterpret_cast<float4*>(&s_rec[j].r)[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
         }
@@ -493,24 +507,56 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                             const double rr = l0 < l1 ? (l0 < l2 ? l0 : l2) : (l1 < l2 ? l1 : l2);
                             bool flag = rr <= r.r_hi;
                             if (!flag) {
-                                float ea;
-                                float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
-                                w = T * a;
-                                const float tn = fmaf(-T, a, T);
-                                const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
-                                const float ew = epsT + ea + 1.2e-7f;
-                                flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
-                                       fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
-                                if (!flag) {
-                                    C0 = fmaf(w, r.rgb[0], C0);
-                                    C1 = fmaf(w, r.rgb[1], C1);
-                                    C2 = fmaf(w, r.rgb[2], C2);
-                                    contrib = true;
-                                    last = b + j;
-                                    cnt++;
-                                    T = tn;
-                                    epsT = en;
-                                    done = T < T_MIN_F;
+                                if constexpr (ACC64) {
+                                    const double2 os = s_os[j];
+                                    double a;
+                                    if (opt.mode == 0) {
+                                        const double rc = fmin(rr, 1.0);
+                                        a = os.x * (os.y == 1.0 ? rc : pow(rc, os.y));
+                                    } else {
+                                        double x = rr * r.phis / os.y;
+                                        if (x > 700.0) x = 700.0;
+                                        a = os.x * (1.0 / (1.0 + exp(x)));
+                                    }
+                                    if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
+                                    const double wd = TS_M(T, a);
+                                    const double tn = TS_M(T, TS_S(1.0, a));
+                                    // r differs from the reference's by ~1e-13 relative
+                                    flag = fabs(tn - T_MIN) <= 1e-9 * tn || fabs(wd - opt.tau_contrib) <= 1e-9 * wd;
+                                    if (!flag) {
+                                        C0 += wd * r.rgb[0];
+                                        C1 += wd * r.rgb[1];
+                                        C2 += wd * r.rgb[2];
+                                        w = (float)wd;
+                                        contrib = true;
+                                        last = b + j;
+                                        cnt++;
+                                        T = tn;
+                                        done = tn < T_MIN;
+                                        // pixel count uses the fp64 weight
+                                        if (wd > opt.tau_contrib) atomicAdd(&s_pix[j], 1);
+                                    }
+                                } else {
+                                    float ea;
+                                    const float a = fminf(alpha_fast(r, rr, opt.mode, ea), ALPHA_CLAMP_F);
+                                    w = (float)T * a;
+                                    const float tn = fmaf(-(float)T, a, (float)T);
+                                    const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                                    const float ew = epsT + ea + 1.2e-7f;
+                                    flag = fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                                           fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f);
+                                    if (!flag) {
+                                        C0 = fmaf(w, r.rgb[0], (float)C0);
+                                        C1 = fmaf(w, r.rgb[1], (float)C1);
+                                        C2 = fmaf(w, r.rgb[2], (float)C2);
+                                        contrib = true;
+                                        last = b + j;
+                                        cnt++;
+                                        T = tn;
+                                        epsT = en;
+                                        done = tn < T_MIN_F;
+                                        if (w > tau) atomicAdd(&s_pix[j], 1);
+                                    }
                                 }
                             }
                             if (flag) {
@@ -521,10 +567,7 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                     }
                 }
                 if (done) gmask = 0u;
-                if (contrib) {
-                    atomicMax(&s_maxw[j], __float_as_uint(w));
-                    if (w > tau) atomicAdd(&s_pix[j], 1);
-                }
+                if (contrib) atomicMax(&s_maxw[j], __float_as_uint(w));
             }
         }
         __syncthreads();
@@ -544,12 +587,13 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
             out.flags[k] = make_int2(p, flag_pos);
         } else {
             if (out.image) {
-                out.image[p * 3 + 0] = fminf(fmaxf(fmaf(T, (float)opt.bg[0], C0), 0.f), 1.f);
-                out.image[p * 3 + 1] = fminf(fmaxf(fmaf(T, (float)opt.bg[1], C1), 0.f), 1.f);
-                out.image[p * 3 + 2] = fminf(fmaxf(fmaf(T, (float)opt.bg[2], C2), 0.f), 1.f);
+                out.image[p * 3 + 0] = (float)fmin(fmax(C0 + T * (Real)opt.bg[0], (Real)0), (Real)1);
+                out.image[p * 3 + 1] = (float)fmin(fmax(C1 + T * (Real)opt.bg[1], (Real)0), (Real)1);
+                out.image[p * 3 + 2] = (float)fmin(fmax(C2 + T * (Real)opt.bg[2], (Real)0), (Real)1);
             }
-            if (out.alpha_map) out.alpha_map[p] = 1.f - T;
-            out.t_final[p] = T;
+            if (out.alpha_map) out.alpha_map[p] = (float)(1 - T);
+            out.t_final[p] = (float)T;
+            if (out.t_final64) out.t_final64[p] = (double)T;
             out.last_pos[p] = last;
             if (out.n_frag) out.n_frag[p] = cnt;
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
@@ -627,6 +671,7 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
             }
             if (out.alpha_map) out.alpha_map[p] = (float)(1.0 - Tt);
             out.t_final[p] = (float)Tt;
+            if (out.t_final64) out.t_final64[p] = Tt;
             out.last_pos[p] = last;
             if (out.n_frag) out.n_frag[p] = cnt;
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
@@ -634,11 +679,21 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
     }
 }
 
-void launch_blend_fast(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
-                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
-                       cudaStream_t st) {
+void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64,
+                       const RecF* rec, const short4* bbox, const int* tile_start, const unsigned* ent_src,
+                       const FastBlendOut& out, cudaStream_t st) {
     int ntiles = cam.ntx * cam.nty;
-    k_blend_fast<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
+    if (dtype == 1) {
+        const double* o = (const double*)soup.opacity;
+        const double* sg = (const double*)soup.sigma;
+        if (acc64) k_blend_fast<double, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
+        else k_blend_fast<double, false><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
+    } else {
+        const float* o = (const float*)soup.opacity;
+        const float* sg = (const float*)soup.sigma;
+        if (acc64) k_blend_fast<float, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
+        else k_blend_fast<float, false><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
+    }
 }
 
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
@@ -654,10 +709,13 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
 }
 
 // ---------------------------------------------------------------------------
-// k_blend_bwd_fast: back to front from the saved last contributor, fp32
-// gradients, warp-reduced before fp32 atomics into the per-source buffer.
-// Decisions inside the guard band (skip, clamp) and near-tied argmax edges
-// are resolved with the reference fp64 arithmetic.
+// k_blend_bwd_fast: back to front from the saved last contributor
+// (_kernels.py:181-318).  Per fragment: r from the fp64 edge functions,
+// alpha with the reference formula in fp64 (exact opacity/sigma staged per
+// entry), transmittance reconstructed in fp64 from the training forward's
+// fp64 T_final, suffix colour and dL/dalpha in fp64 (they cancel); the
+// remaining chain in fp32.  Per-entry sums are warp-reduced before fp32
+// atomics into the per-source screen-gradient buffer.
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const T* __restrict__ verts,
@@ -667,12 +725,14 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                                                         const RecB* __restrict__ recb,
                                                         const int* __restrict__ tile_start,
                                                         const unsigned* __restrict__ ent_src,
-                                                        const float* __restrict__ t_final,
+                                                        const double* __restrict__ t_final,
                                                         const int* __restrict__ last_pos,
                                                         const float* __restrict__ d_image,
                                                         float* __restrict__ sgrad) {
+    (void)verts;
     __shared__ RecF s_rec[FB];
     __shared__ RecB s_rb[FB];
+    __shared__ double2 s_os[FB];
     __shared__ unsigned s_src[FB];
     __shared__ int s_hi;
     const int t = blockIdx.x;
@@ -682,9 +742,11 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
     const int py = ty * TILE + 2 * warp + (lane >> 4);
     const int wy0 = ty * TILE + 2 * warp;
     const bool inside = px < cam.width && py < cam.height;
+    const double pcx = px + 0.5, pcy = py + 0.5;
     const int s = tile_start[t];
     int my_last = -1;
-    float Tc = 1.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
+    double Tc = 1.0;
+    float d0 = 0.f, d1 = 0.f, d2 = 0.f;
     if (inside) {
         const int p = py * cam.width + px;
         my_last = last_pos[p];
@@ -693,21 +755,23 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
         d1 = d_image[p * 3 + 1];
         d2 = d_image[p * 3 + 2];
     }
-    float S0 = Tc * (float)opt.bg[0], S1 = Tc * (float)opt.bg[1], S2 = Tc * (float)opt.bg[2];
+    double S0 = Tc * opt.bg[0], S1 = Tc * opt.bg[1], S2 = Tc * opt.bg[2];
     if (threadIdx.x == 0) s_hi = -1;
     __syncthreads();
     if (my_last >= 0) atomicMax(&s_hi, my_last);
     __syncthreads();
     const int hi = s_hi;
-    const float fpx = (float)(px) + 0.5f, fpy = (float)(py) + 0.5f;
     for (int bend = hi + 1; bend > s; bend -= FB) {
         const int bstart = max(s, bend - FB);
         const int nb = bend - bstart;
         __syncthreads();
         for (int c = threadIdx.x; c < nb * 11; c += blockDim.x) {
-            int j = c / 11, q = c - j * 11;
-            unsigned src = __ldg(ent_src + bstart + j);
-            if (q == 0) s_src[j] = src;
+            const int j = c / 11, q = c - j * 11;
+            const unsigned src = __ldg(ent_src + bstart + j);
+            if (q == 0) {
+                s_src[j] = src;
+                s_os[j] = make_double2(opt.solid ? 1.0 : (double)opacity[src], (double)sigma[src]);
+            }
             if (q < 8)
                 reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
             else
@@ -715,8 +779,8 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
         }
         __syncthreads();
         for (int jb = ((nb - 1) / 32) * 32; jb >= 0; jb -= 32) {
-            int jl = jb + (int)lane;
-            bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
+            const int jl = jb + (int)lane;
+            const bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
             unsigned mask = __ballot_sync(0xffffffffu, ov);
             while (mask) {
                 const int j = jb + 31 - __clz(mask);
@@ -728,90 +792,80 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                 for (int k = 0; k < 12; k++) g[k] = 0.f;
                 bool act = false;
                 if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
-                    const RecB& rb = s_rb[j];
                     int edge;
-                    double rr = edge_r(r, px + 0.5, py + 0.5, edge);
-                    bool contributes = rr > (double)r.r_hi;
-                    float alpha = 0.f;
-                    bool clamped = false, exact_done = false;
-                    if (!contributes && rr >= (double)r.r_lo) {
-                        double ae = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, s_src[j]);
-                        clamped = ae > ALPHA_CLAMP;
-                        if (clamped) ae = ALPHA_CLAMP;
-                        contributes = ae >= ALPHA_MIN;
-                        alpha = (float)ae;
-                        exact_done = true;
-                    }
-                    if (contributes) {
-                        if (!exact_done) {
-                            float ea;
-                            alpha = alpha_fast(r, rr, opt.mode, ea);
-                            if (fabsf(alpha - ALPHA_CLAMP_F) <= 2.f * ea * alpha + 1e-7f) {
-                                double ae = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, s_src[j]);
-                                clamped = ae > ALPHA_CLAMP;
-                                alpha = clamped ? ALPHA_CLAMP_F : (float)ae;
-                            } else {
-                                clamped = alpha > ALPHA_CLAMP_F;
-                                if (clamped) alpha = ALPHA_CLAMP_F;
-                            }
+                    const double rr = edge_r(r, pcx, pcy, edge);
+                    if (rr >= r.r_lo) {
+                        const double2 os = s_os[j];
+                        double a;
+                        if (opt.mode == 0) {
+                            const double rc = fmin(rr, 1.0);
+                            a = rr <= 0.0 ? 0.0 : os.x * (os.y == 1.0 ? rc : pow(rc, os.y));
+                        } else {
+                            double x = rr * r.phis / os.y;
+                            if (x > 700.0) x = 700.0;
+                            a = os.x * (1.0 / (1.0 + exp(x)));
                         }
-                        act = true;
-                        const float one_m = 1.f - alpha;
-                        const float tb = Tc / one_m;
-                        const float w = tb * alpha;
-                        const float* c = r.rgb;
-                        g[SG_GRGB + 0] = w * d0;
-                        g[SG_GRGB + 1] = w * d1;
-                        g[SG_GRGB + 2] = w * d2;
-                        const float inv1m = 1.f / one_m;
-                        float ga = d0 * (tb * c[0] - S0 * inv1m) + d1 * (tb * c[1] - S1 * inv1m) +
-                                   d2 * (tb * c[2] - S2 * inv1m);
-                        S0 = fmaf(w, c[0], S0);
-                        S1 = fmaf(w, c[1], S1);
-                        S2 = fmaf(w, c[2], S2);
-                        Tc = tb;
-                        if (!clamped) {
-                            const float o = rb.opa, sg = rb.sig, phis = rb.phis;
-                            g[SG_GO] = ga * (alpha / o);
-                            const float g_win = o * ga;
-                            const float window = alpha / o;
-                            const float rf = (float)rr;
-                            const float phi = rf * phis;
-                            float g_phi;
-                            if (opt.mode == 0) {
-                                const float rc = fminf(rf, 1.f);
-                                g[SG_GSIG] = g_win * window * __logf(rc);
-                                const float g_r = g_win * sg * window / rc;
-                                if (rr >= 1.0) {
-                                    g_phi = 0.f;
+                        const bool clamped = a > ALPHA_CLAMP;
+                        if (clamped) a = ALPHA_CLAMP;
+                        if (a >= ALPHA_MIN) {
+                            act = true;
+                            const RecB& rb = s_rb[j];
+                            const double one_m = 1.0 - a;
+                            const double tb = Tc / one_m;
+                            const double w = tb * a;
+                            const float* c = r.rgb;
+                            g[SG_GRGB + 0] = (float)(w * d0);
+                            g[SG_GRGB + 1] = (float)(w * d1);
+                            g[SG_GRGB + 2] = (float)(w * d2);
+                            const double ga = d0 * (tb * c[0] - S0 / one_m) + d1 * (tb * c[1] - S1 / one_m) +
+                                              d2 * (tb * c[2] - S2 / one_m);
+                            S0 += w * c[0];
+                            S1 += w * c[1];
+                            S2 += w * c[2];
+                            Tc = tb;
+                            if (!clamped) {
+                                const double o = os.x, sg = os.y;
+                                const float phis = rb.phis;
+                                g[SG_GO] = (float)(ga * (a / o));
+                                const double g_win = o * ga;
+                                const double window = a / o;
+                                const float rf = (float)rr;
+                                const float phi = (float)(rr * r.phis);
+                                float g_phi;
+                                if (opt.mode == 0) {
+                                    const double rc = fmin(rr, 1.0);
+                                    g[SG_GSIG] = (float)(g_win * window) * __logf((float)rc);
+                                    const float g_r = (float)(g_win * sg * window / rc);
+                                    if (rr >= 1.0) {
+                                        g_phi = 0.f;
+                                    } else {
+                                        g_phi = g_r / phis;
+                                        g[SG_GPHIS] = -g_r * rf / phis;
+                                    }
                                 } else {
-                                    g_phi = g_r / phis;
-                                    g[SG_GPHIS] = -g_r * rf / phis;
+                                    // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
+                                    const double E = exp(fmin(rr * r.phis / sg, 700.0));
+                                    const double ww = E / ((1.0 + E) * (1.0 + E));
+                                    g[SG_GSIG] = (float)(g_win * ww * (rr * r.phis) / (sg * sg));
+                                    g_phi = (float)(-g_win * ww / sg);
                                 }
-                            } else {
-                                // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
-                                const float E = fast_ex2(fminf(rf * r.f0, 126.f));
-                                const float inv = 1.f / (1.f + E);
-                                const float ww = E * inv * inv;
-                                g[SG_GSIG] = g_win * ww * phi / (sg * sg);
-                                g_phi = -g_win * ww / sg;
+                                // edge line derivative wrt its endpoints (_kernels.py:296-318)
+                                const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
+                                const float ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
+                                const float pxr = (float)(px - r.ox) + 0.5f, pyr = (float)(py - r.oy) + 0.5f;
+                                const float ex = bx - ax, ey = by - ay;
+                                const float inv_l = rsqrtf(ex * ex + ey * ey);
+                                const float inv_l2 = inv_l * inv_l;
+                                const float sgn = ((rb.esign >> edge) & 1) ? -1.f : 1.f;
+                                const float gax = sgn * (pyr - by) * inv_l - phi * (ax - bx) * inv_l2;
+                                const float gay = sgn * (bx - pxr) * inv_l - phi * (ay - by) * inv_l2;
+                                const float gbx = sgn * (ay - pyr) * inv_l - phi * (bx - ax) * inv_l2;
+                                const float gby = sgn * (pxr - ax) * inv_l - phi * (by - ay) * inv_l2;
+                                g[SG_GQ + ia * 2] = g_phi * gax;
+                                g[SG_GQ + ia * 2 + 1] = g_phi * gay;
+                                g[SG_GQ + ib * 2] = g_phi * gbx;
+                                g[SG_GQ + ib * 2 + 1] = g_phi * gby;
                             }
-                            // edge line L = s*(n.p)... derivative wrt its endpoints (_kernels.py:296-318)
-                            const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
-                            const float ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
-                            const float pxr = (float)(px - r.ox) + 0.5f, pyr = (float)(py - r.oy) + 0.5f;
-                            const float ex = bx - ax, ey = by - ay;
-                            const float inv_l = rsqrtf(ex * ex + ey * ey);
-                            const float inv_l2 = inv_l * inv_l;
-                            const float sgn = ((rb.esign >> edge) & 1) ? -1.f : 1.f;
-                            const float gax = sgn * (pyr - by) * inv_l - phi * (ax - bx) * inv_l2;
-                            const float gay = sgn * (bx - pxr) * inv_l - phi * (ay - by) * inv_l2;
-                            const float gbx = sgn * (ay - pyr) * inv_l - phi * (bx - ax) * inv_l2;
-                            const float gby = sgn * (pxr - ax) * inv_l - phi * (by - ay) * inv_l2;
-                            g[SG_GQ + ia * 2] = g_phi * gax;
-                            g[SG_GQ + ia * 2 + 1] = g_phi * gay;
-                            g[SG_GQ + ib * 2] = g_phi * gbx;
-                            g[SG_GQ + ib * 2 + 1] = g_phi * gby;
                         }
                     }
                 }
@@ -833,13 +887,11 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
             }
         }
     }
-    (void)fpx;
-    (void)fpy;
 }
 
 void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                            const RecB* recb, const int* tile_start, const unsigned* ent_src,
-                           const float* t_final, const int* last_pos, const float* d_image, float* sgrad,
+                           const double* t_final, const int* last_pos, const float* d_image, float* sgrad,
                            cudaStream_t st) {
     int ntiles = cam.ntx * cam.nty;
     if (dtype == 1)

@@ -47,6 +47,7 @@ struct FastBlendOut {
     int* last_src;
     int* n_frag;
     float* t_final;
+    double* t_final64;         // training forward only
     int* last_pos;
     int2* flags;               // (pixel, flag position) of guard-band pixels
     Counters* ctr;
@@ -81,15 +82,15 @@ void launch_chain_bwd32(const Cam& cam, const Opts& opt, const ts_soup& soup, in
 // ts_fast.cu
 void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
                             const FastPreOut& out, cudaStream_t st);
-void launch_blend_fast(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
-                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
-                       cudaStream_t st);
+void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64,
+                       const RecF* rec, const short4* bbox, const int* tile_start, const unsigned* ent_src,
+                       const FastBlendOut& out, cudaStream_t st);
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                       cudaStream_t st);
 void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                            const RecB* recb, const int* tile_start, const unsigned* ent_src,
-                           const float* t_final, const int* last_pos, const float* d_image, float* sgrad,
+                           const double* t_final, const int* last_pos, const float* d_image, float* sgrad,
                            cudaStream_t st);
 
 // ts_sort.cu

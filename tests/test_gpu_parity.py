@@ -20,7 +20,15 @@ pytestmark = pytest.mark.gpu
 RGB_TOL = 1e-5
 GRAD_RTOL = 1e-4
 MAXW_TOL = 1e-6
-PRECISIONS = ("exact", "fast")
+# "fast-render": fp32 compositing with the guard band (render-only forward);
+# "fast": training forward (keep_backward) with fp64 alpha/transmittance
+PRECISIONS = ("exact", "fast", "fast-render")
+
+
+def fwd(rast, soup, intr, pose, precision, **kw):
+    if precision == "fast-render":
+        return rast.forward(soup, intr, pose, precision="fast", keep_backward=False, debug=True, **kw)
+    return rast.forward(soup, intr, pose, precision=precision, debug=True, **kw)
 
 
 @pytest.fixture(scope="module")
@@ -77,12 +85,13 @@ def test_golden_small_scenes(rast, path, precision):
     from oracle import oracle as O
     g = GoldenScene(path)
     ds = _dev(g.soup)
-    fwd = rast.forward(ds, g.intr, g.pose, mode=g.mode, background=g.background,
-                       precision=precision, debug=True)
+    f = fwd(rast, ds, g.intr, g.pose, precision, mode=g.mode, background=g.background)
     ref = O.render(g.soup, g.intr, g.pose, mode=g.mode, background=g.background)
     # the oracle is itself pinned to these fixtures (test_oracle.py); check both
     assert np.array_equal(ref.last_src, g["last_src"])
-    check_forward(rast, fwd, ref, g.intr, g.name)
+    check_forward(rast, f, ref, g.intr, g.name)
+    if precision == "fast-render":
+        return
     gr = rast.backward(torch.as_tensor(g.d_image, dtype=torch.float32, device="cuda"))
     for k in ("d_vertices", "d_opacity", "d_sigma", "d_sh"):
         err = rel_err(_np(getattr(gr, k)), g[k])
@@ -97,14 +106,16 @@ def test_c1_against_golden_and_oracle(rast, precision):
     z = np.load(os.path.join(GOLDEN, "c1.npz"))
     cfg = scenes.CONFIGS["c1"]
     soup, intr, pose = scenes.make_scene(cfg)
-    fwd = rast.forward(_dev(soup), intr, pose, precision=precision, debug=True)
-    assert np.array_equal(rast.dump_sorted_idx(fwd.n_visible), z["sorted_idx"])
-    assert np.array_equal(rast.dump_entry_rank(fwd.n_entries), z["entry_tri"])
-    assert np.array_equal(_np(fwd.last_src), z["last_src"])
-    assert np.array_equal(_np(fwd.n_frag), z["nfrag"])
-    assert np.abs(_np(fwd.image) - z["image"]).max() <= RGB_TOL
+    f = fwd(rast, _dev(soup), intr, pose, precision)
+    assert np.array_equal(rast.dump_sorted_idx(f.n_visible), z["sorted_idx"])
+    assert np.array_equal(rast.dump_entry_rank(f.n_entries), z["entry_tri"])
+    assert np.array_equal(_np(f.last_src), z["last_src"])
+    assert np.array_equal(_np(f.n_frag), z["nfrag"])
+    assert np.abs(_np(f.image) - z["image"]).max() <= RGB_TOL
     ref = O.render(soup, intr, pose)
-    check_forward(rast, fwd, ref, intr, "c1")
+    check_forward(rast, f, ref, intr, "c1")
+    if precision == "fast-render":
+        return
     d_image = scenes.make_d_image(cfg.seed, cfg.height, cfg.width)
     g = rast.backward(torch.as_tensor(d_image, dtype=torch.float32, device="cuda"))
     gref = O.render_backward(soup, intr, pose, d_image=d_image)
@@ -121,10 +132,11 @@ def test_mid_scene_forward_backward(rast, precision, mode):
     from paper_2505_19175_b200 import scenes
     soup = scenes.make_soup(200_000, seed=7, size=0.03, sigma=(0.3, 3.0))
     intr, pose = scenes.frontal_camera(640, 360, 560.0)
-    fwd = rast.forward(_dev(soup), intr, pose, mode=mode, background=(0.2, 0.1, 0.3),
-                       precision=precision, debug=True)
+    f = fwd(rast, _dev(soup), intr, pose, precision, mode=mode, background=(0.2, 0.1, 0.3))
     ref = O.render(soup, intr, pose, mode=mode, background=(0.2, 0.1, 0.3))
-    check_forward(rast, fwd, ref, intr, f"mid-{mode}")
+    check_forward(rast, f, ref, intr, f"mid-{mode}")
+    if precision == "fast-render":
+        return
     d_image = scenes.make_d_image(7, intr.height, intr.width)
     g = rast.backward(torch.as_tensor(d_image, dtype=torch.float32, device="cuda"))
     gref = O.render_backward(soup, intr, pose, mode=mode, background=(0.2, 0.1, 0.3),
@@ -138,9 +150,9 @@ def test_c2_forward_parity(rast, precision):
     from oracle import oracle as O
     from paper_2505_19175_b200 import scenes
     soup, intr, pose = scenes.make_scene("c2")
-    fwd = rast.forward(_dev(soup), intr, pose, precision=precision, debug=True)
+    f = fwd(rast, _dev(soup), intr, pose, precision)
     ref = O.render(soup, intr, pose)
-    check_forward(rast, fwd, ref, intr, "c2")
+    check_forward(rast, f, ref, intr, "c2")
 
 
 def test_fp64_params_match_reference_inputs(rast):
@@ -243,6 +255,6 @@ def test_north_star_forward_parity(rast, precision):
     from oracle import oracle as O
     from paper_2505_19175_b200 import scenes
     soup, intr, pose = scenes.make_scene("ns")
-    fwd = rast.forward(_dev(soup), intr, pose, precision=precision, debug=True)
+    f = fwd(rast, _dev(soup), intr, pose, precision)
     ref = O.render(soup, intr, pose)
-    check_forward(rast, fwd, ref, intr, f"ns-{precision}")
+    check_forward(rast, f, ref, intr, f"ns-{precision}")
