@@ -467,18 +467,18 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
     int rc;
     c->ev_used[TS_STAGE_BLEND_BWD] = c->ev_used[TS_STAGE_CHAIN_BWD] = false;
     if (c->precision == 0) {
-        if ((rc = ensure(c->sg32, sizeof(float) * SG_STRIDE * n1))) return rc;
-        float* sg = (float*)c->sg32.p;
+        if ((rc = ensure(c->sg64, sizeof(double) * SG_STRIDE * n1))) return rc;
+        double* sg = (double*)c->sg64.p;
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
-        if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(float) * SG_STRIDE * c->n, st));
+        if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
         launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
                               (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
                               d_image, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
-        launch_chain_bwd32(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+        launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
         stage_end(c, TS_STAGE_CHAIN_BWD, st);
-        c->sgrad_kind = 2;
+        c->sgrad_kind = 1;
     } else {
         if ((rc = ensure(c->sg64, sizeof(double) * SG_STRIDE * n1))) return rc;
         double* sg = (double*)c->sg64.p;

@@ -714,8 +714,9 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
 // alpha with the reference formula in fp64 (exact opacity/sigma staged per
 // entry), transmittance reconstructed in fp64 from the training forward's
 // fp64 T_final, suffix colour and dL/dalpha in fp64 (they cancel); the
-// remaining chain in fp32.  Per-entry sums are warp-reduced before fp32
-// atomics into the per-source screen-gradient buffer.
+// edge chain in fp64 too (near-degenerate triangles cancel heavily).  Per-entry
+// sums are warp-reduced in fp64 before fp64 atomics (native RED.F64) into the
+// per-source screen-gradient buffer.
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const T* __restrict__ verts,
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                                                         const double* __restrict__ t_final,
                                                         const int* __restrict__ last_pos,
                                                         const float* __restrict__ d_image,
-                                                        float* __restrict__ sgrad) {
+                                                        double* __restrict__ sgrad) {
     (void)verts;
     __shared__ RecF s_rec[FB];
     __shared__ RecB s_rb[FB];
@@ -787,9 +788,9 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                 mask &= ~(1u << (j - jb));
                 const RecF& r = s_rec[j];
                 const int pos = bstart + j;
-                float g[12];
+                double g[12];
 #pragma unroll
-                for (int k = 0; k < 12; k++) g[k] = 0.f;
+                for (int k = 0; k < 12; k++) g[k] = 0.0;
                 bool act = false;
                 if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
                     int edge;
@@ -809,14 +810,13 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                         if (clamped) a = ALPHA_CLAMP;
                         if (a >= ALPHA_MIN) {
                             act = true;
-                            const RecB& rb = s_rb[j];
                             const double one_m = 1.0 - a;
                             const double tb = Tc / one_m;
                             const double w = tb * a;
                             const float* c = r.rgb;
-                            g[SG_GRGB + 0] = (float)(w * d0);
-                            g[SG_GRGB + 1] = (float)(w * d1);
-                            g[SG_GRGB + 2] = (float)(w * d2);
+                            g[SG_GRGB + 0] = w * d0;
+                            g[SG_GRGB + 1] = w * d1;
+                            g[SG_GRGB + 2] = w * d2;
                             const double ga = d0 * (tb * c[0] - S0 / one_m) + d1 * (tb * c[1] - S1 / one_m) +
                                               d2 * (tb * c[2] - S2 / one_m);
                             S0 += w * c[0];
@@ -824,47 +824,43 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                             S2 += w * c[2];
                             Tc = tb;
                             if (!clamped) {
-                                const double o = os.x, sg = os.y;
-                                const float phis = rb.phis;
-                                g[SG_GO] = (float)(ga * (a / o));
+                                const double o = os.x, sg = os.y, phis = r.phis;
+                                g[SG_GO] = ga * (a / o);
                                 const double g_win = o * ga;
                                 const double window = a / o;
-                                const float rf = (float)rr;
-                                const float phi = (float)(rr * r.phis);
-                                float g_phi;
+                                const double phi = rr * phis;
+                                double g_phi;
                                 if (opt.mode == 0) {
                                     const double rc = fmin(rr, 1.0);
-                                    g[SG_GSIG] = (float)(g_win * window) * __logf((float)rc);
-                                    const float g_r = (float)(g_win * sg * window / rc);
+                                    g[SG_GSIG] = g_win * window * (double)__logf((float)rc);
+                                    const double g_r = g_win * sg * window / rc;
                                     if (rr >= 1.0) {
-                                        g_phi = 0.f;
+                                        g_phi = 0.0;
                                     } else {
                                         g_phi = g_r / phis;
-                                        g[SG_GPHIS] = -g_r * rf / phis;
+                                        g[SG_GPHIS] = -g_r * rr / phis;
                                     }
                                 } else {
                                     // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
-                                    const double E = exp(fmin(rr * r.phis / sg, 700.0));
+                                    const double E = exp(fmin(phi / sg, 700.0));
                                     const double ww = E / ((1.0 + E) * (1.0 + E));
-                                    g[SG_GSIG] = (float)(g_win * ww * (rr * r.phis) / (sg * sg));
-                                    g_phi = (float)(-g_win * ww / sg);
+                                    g[SG_GSIG] = g_win * ww * phi / (sg * sg);
+                                    g_phi = -g_win * ww / sg;
                                 }
-                                // edge line derivative wrt its endpoints (_kernels.py:296-318)
+                                // edge line derivative wrt its endpoints (_kernels.py:296-318),
+                                // coordinates relative to the record origin
+                                const RecB& rb = s_rb[j];
                                 const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
-                                const float ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
-                                const float pxr = (float)(px - r.ox) + 0.5f, pyr = (float)(py - r.oy) + 0.5f;
-                                const float ex = bx - ax, ey = by - ay;
-                                const float inv_l = rsqrtf(ex * ex + ey * ey);
-                                const float inv_l2 = inv_l * inv_l;
-                                const float sgn = ((rb.esign >> edge) & 1) ? -1.f : 1.f;
-                                const float gax = sgn * (pyr - by) * inv_l - phi * (ax - bx) * inv_l2;
-                                const float gay = sgn * (bx - pxr) * inv_l - phi * (ay - by) * inv_l2;
-                                const float gbx = sgn * (ay - pyr) * inv_l - phi * (bx - ax) * inv_l2;
-                                const float gby = sgn * (pxr - ax) * inv_l - phi * (by - ay) * inv_l2;
-                                g[SG_GQ + ia * 2] = g_phi * gax;
-                                g[SG_GQ + ia * 2 + 1] = g_phi * gay;
-                                g[SG_GQ + ib * 2] = g_phi * gbx;
-                                g[SG_GQ + ib * 2 + 1] = g_phi * gby;
+                                const double ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
+                                const double pxr = (double)(px - r.ox) + 0.5, pyr = (double)(py - r.oy) + 0.5;
+                                const double ex = bx - ax, ey = by - ay;
+                                const double inv_l = rsqrt(ex * ex + ey * ey);
+                                const double inv_l2 = inv_l * inv_l;
+                                const double sgn = ((rb.esign >> edge) & 1) ? -1.0 : 1.0;
+                                g[SG_GQ + ia * 2] = g_phi * (sgn * (pyr - by) * inv_l - phi * (ax - bx) * inv_l2);
+                                g[SG_GQ + ia * 2 + 1] = g_phi * (sgn * (bx - pxr) * inv_l - phi * (ay - by) * inv_l2);
+                                g[SG_GQ + ib * 2] = g_phi * (sgn * (ay - pyr) * inv_l - phi * (bx - ax) * inv_l2);
+                                g[SG_GQ + ib * 2 + 1] = g_phi * (sgn * (pxr - ax) * inv_l - phi * (by - ay) * inv_l2);
                             }
                         }
                     }
@@ -872,16 +868,16 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
                 if (__any_sync(0xffffffffu, act)) {
 #pragma unroll
                     for (int k = 0; k < 12; k++) {
-                        float v = g[k];
+                        double v = g[k];
 #pragma unroll
                         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
                         g[k] = v;
                     }
                     if (lane < 12) {
-                        float v = g[0];
+                        double v = g[0];
 #pragma unroll
                         for (int k = 1; k < 12; k++) v = (lane == (unsigned)k) ? g[k] : v;
-                        if (v != 0.f) atomicAdd(sgrad + (size_t)s_src[j] * SG_STRIDE + lane, v);
+                        if (v != 0.0) atomicAdd(sgrad + (size_t)s_src[j] * SG_STRIDE + lane, v);
                     }
                 }
             }
@@ -891,7 +887,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
 
 void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                            const RecB* recb, const int* tile_start, const unsigned* ent_src,
-                           const double* t_final, const int* last_pos, const float* d_image, float* sgrad,
+                           const double* t_final, const int* last_pos, const float* d_image, double* sgrad,
                            cudaStream_t st) {
     int ntiles = cam.ntx * cam.nty;
     if (dtype == 1)

@@ -90,7 +90,7 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
                       cudaStream_t st);
 void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                            const RecB* recb, const int* tile_start, const unsigned* ent_src,
-                           const double* t_final, const int* last_pos, const float* d_image, float* sgrad,
+                           const double* t_final, const int* last_pos, const float* d_image, double* sgrad,
                            cudaStream_t st);
 
 // ts_sort.cu
