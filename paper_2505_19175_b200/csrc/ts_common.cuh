@@ -66,15 +66,15 @@ struct __align__(16) RecF {
 };
 static_assert(sizeof(RecF) == 128, "RecF layout");
 
-// Backward-only per-source data (48 B): vertices relative to the origin,
-// phi_s, opacity, sigma and the edge-orientation signs.
+// Backward-only per-source data (64 B): projected vertices relative to the
+// record origin in fp64 (edge lengths of near-degenerate triangles are
+// ill-conditioned) and the edge-orientation signs.
 struct __align__(16) RecB {
-    float qx[3], qy[3];
-    float phis, opa, sig;
+    double qx[3], qy[3];
     int esign;
-    float pad[2];
+    int pad[3];
 };
-static_assert(sizeof(RecB) == 48, "RecB layout");
+static_assert(sizeof(RecB) == 64, "RecB layout");
 
 // Screen-space gradient accumulator per source triangle (backward), fp64.
 // gq[6] (q0x,q0y,q1x,q1y,q2x,q2y), go, gsig, grgb[3], gphis, gz, pad

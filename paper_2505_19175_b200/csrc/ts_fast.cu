@@ -280,14 +280,11 @@ __global__ void __launch_bounds__(128) k_preprocess_fast(Cam cam, Opts opt, cons
                     RecB rb;
 #pragma unroll
                     for (int e = 0; e < 3; e++) {
-                        rb.qx[e] = (float)(q[e * 2] - ox);
-                        rb.qy[e] = (float)(q[e * 2 + 1] - oy);
+                        rb.qx[e] = q[e * 2] - ox;
+                        rb.qy[e] = q[e * 2 + 1] - oy;
                     }
-                    rb.phis = (float)phis;
-                    rb.opa = (float)o;
-                    rb.sig = (float)sg;
                     rb.esign = esign;
-                    rb.pad[0] = rb.pad[1] = 0.f;
+                    rb.pad[0] = rb.pad[1] = rb.pad[2] = 0;
                     out.recb[i] = rb;
                 }
                 (void)qf;
@@ -766,8 +763,8 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
         const int bstart = max(s, bend - FB);
         const int nb = bend - bstart;
         __syncthreads();
-        for (int c = threadIdx.x; c < nb * 11; c += blockDim.x) {
-            const int j = c / 11, q = c - j * 11;
+        for (int c = threadIdx.x; c < nb * 12; c += blockDim.x) {
+            const int j = c / 12, q = c - j * 12;
             const unsigned src = __ldg(ent_src + bstart + j);
             if (q == 0) {
                 s_src[j] = src;
