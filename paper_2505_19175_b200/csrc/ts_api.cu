@@ -407,7 +407,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
 
     // tile duplication in rank order + stable sort by tile id (render.py:315-361)
     stage_begin(c, TS_STAGE_BINNING, st);
-    rank_offsets(m, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
+    rank_offsets(m, c->sorted_src, c->tcount, c->offs, nullptr, c->sort, st);
     duplicate_entries(m, c->sorted_src, c->bbox, c->offs, cm.ntx, c->tkey, c->tval, st);
     g_launches += m > 0 ? 4 : 0;
     int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
@@ -513,6 +513,7 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
             return TS_OK;
         case TS_DUMP_ENTRY_RANK:
             if (bytes < 4 * (size_t)c->e) return TS_ERR_INVALID_ARG;
+            rank_offsets(c->m, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
             entries_to_rank(c->e, c->ent_src, c->rank_of, (int*)dst, st);
             return cuda_err(cudaGetLastError());
         case TS_DUMP_BBOX:

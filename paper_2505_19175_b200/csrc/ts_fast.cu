@@ -389,7 +389,7 @@ __device__ __forceinline__ double alpha_exact_r(const RecF& r, double rr, int mo
     double window;
     if (mode == 0) {
         if (rr <= 0.0) return 0.0;  // phi >= 0
-        window = pow(fmin(rr, 1.0), sg);
+        window = sg == 1.0 ? fmin(rr, 1.0) : pow(fmin(rr, 1.0), sg);  // pow(x, 1) == x
     } else {
         double x = rr * r.phis / sg;
         if (x > 700.0) x = 700.0;
@@ -599,68 +599,87 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
 }
 
 // ---------------------------------------------------------------------------
-// k_fixup_fwd: exact (fp64) replay of flagged pixels, one warp per pixel:
-// lanes evaluate 32 consecutive tile entries in parallel, then the warp
-// composites the contributing ones in entry order.  Entries before the flag
-// position already committed their statistics in k_blend_fast (their
-// decisions were certain); from the flag position on the fix-up commits them.
+// k_fixup_fwd: exact (fp64) replay of flagged pixels, one CTA per pixel.
+// The CTA evaluates alpha for FXC consecutive tile entries in parallel
+// (shared memory), then warp 0 composites the contributing ones in entry
+// order; repeat until the pixel saturates or the tile's list ends.  Entries
+// before the flag position already committed their statistics in
+// k_blend_fast (their decisions were certain); from it on the fix-up does.
 // ---------------------------------------------------------------------------
+constexpr int FXC = 1024;
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* __restrict__ opacity,
                                                    const T* __restrict__ sigma, const RecF* __restrict__ rec,
                                                    const int* __restrict__ tile_start,
                                                    const unsigned* __restrict__ ent_src, FastBlendOut out) {
+    __shared__ double s_a[FXC];
+    __shared__ float s_c[3][FXC];
+    __shared__ unsigned s_s[FXC];
+    __shared__ int s_done;
     const unsigned lane = threadIdx.x & 31;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long nflag = (long long)out.ctr->n_flagged;
-    for (long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nflag; k += nw) {
+    for (long long k = blockIdx.x; k < nflag; k += gridDim.x) {
         const int2 f = out.flags[k];
         const int p = f.x, fpos = f.y;
         const int px = p % cam.width, py = p / cam.width;
         const int t = (py / TILE) * cam.ntx + px / TILE;
         double Tt = 1.0, C0 = 0.0, C1 = 0.0, C2 = 0.0;
         int last = -1, cnt = 0;
-        bool done = false;
         const int s = tile_start[t], e = tile_start[t + 1];
-        for (int base = s; base < e && !done; base += 32) {
-            const int pos = base + (int)lane;
-            double a = 0.0;
-            unsigned src = 0;
-            float cr = 0.f, cg = 0.f, cb = 0.f;
-            if (pos < e) {
-                src = ent_src[pos];
+        if (threadIdx.x == 0) s_done = 0;
+        __syncthreads();
+        for (int base = s; base < e; base += FXC) {
+            const int nb = min(FXC, e - base);
+            for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+                const unsigned src = __ldg(ent_src + base + i);
                 const RecF& r = rec[src];
+                double a = 0.0;
                 if (px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
-                    double rr = edge_r(r, px + 0.5, py + 0.5);
+                    const double rr = edge_r(r, px + 0.5, py + 0.5);
                     a = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, src);
                     if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
                     if (a < ALPHA_MIN) a = 0.0;
-                    cr = r.rgb[0];
-                    cg = r.rgb[1];
-                    cb = r.rgb[2];
+                    s_c[0][i] = r.rgb[0];
+                    s_c[1][i] = r.rgb[1];
+                    s_c[2][i] = r.rgb[2];
+                }
+                s_a[i] = a;
+                s_s[i] = src;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                for (int i0 = 0; i0 < nb && !s_done; i0 += 32) {
+                    const int i = i0 + (int)lane;
+                    unsigned m = __ballot_sync(0xffffffffu, i < nb && s_a[i] > 0.0);
+                    while (m) {
+                        const int j = i0 + __ffs(m) - 1;
+                        m &= m - 1;
+                        const double aj = s_a[j];
+                        const double w = Tt * aj;
+                        C0 += w * (double)s_c[0][j];
+                        C1 += w * (double)s_c[1][j];
+                        C2 += w * (double)s_c[2][j];
+                        const int posj = base + j;
+                        if (lane == 0 && posj >= fpos) {
+                            if (out.max_weight) atomicMax((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
+                            if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + s_s[j], 1);
+                        }
+                        last = posj;
+                        cnt++;
+                        Tt = TS_M(Tt, TS_S(1.0, aj));
+                        if (Tt < T_MIN) {
+                            if (lane == 0) s_done = 1;
+                            break;
+                        }
+                    }
+                    __syncwarp();
                 }
             }
-            unsigned m = __ballot_sync(0xffffffffu, a > 0.0);
-            while (m && !done) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                const double aj = __shfl_sync(0xffffffffu, a, j);
-                const double w = Tt * aj;
-                C0 += w * (double)__shfl_sync(0xffffffffu, cr, j);
-                C1 += w * (double)__shfl_sync(0xffffffffu, cg, j);
-                C2 += w * (double)__shfl_sync(0xffffffffu, cb, j);
-                const int posj = base + j;
-                if ((int)lane == j && posj >= fpos) {
-                    if (out.max_weight) atomicMax((unsigned*)out.max_weight + src, __float_as_uint((float)w));
-                    if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + src, 1);
-                }
-                last = posj;
-                cnt++;
-                Tt = TS_M(Tt, TS_S(1.0, aj));
-                if (Tt < T_MIN) done = true;
-            }
+            __syncthreads();
+            if (s_done) break;
         }
-        if (lane == 0) {
+        if (threadIdx.x == 0) {
             if (out.image) {
                 out.image[p * 3 + 0] = (float)fmin(fmax(C0 + Tt * opt.bg[0], 0.0), 1.0);
                 out.image[p * 3 + 1] = (float)fmin(fmax(C1 + Tt * opt.bg[1], 0.0), 1.0);
@@ -673,6 +692,7 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
             if (out.n_frag) out.n_frag[p] = cnt;
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
         }
+        __syncthreads();
     }
 }
 

@@ -158,11 +158,11 @@ struct RankF {
     const unsigned* sorted_src;
     const unsigned* tcount;
     unsigned* offs;
-    int* rank_of;
+    int* rank_of;  // nullable (debug dumps only)
     __device__ unsigned load(long long m) const { return tcount[sorted_src[m]]; }
     __device__ void store(long long m, unsigned ex, unsigned) const {
         offs[m] = ex;
-        rank_of[sorted_src[m]] = (int)m;
+        if (rank_of) rank_of[sorted_src[m]] = (int)m;
     }
 };
 
@@ -346,9 +346,6 @@ namespace ts {
 constexpr int OS_THREADS = 256;
 constexpr int OS_ITEMS = 16;
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096
-constexpr unsigned OS_FLAG_AGG = 1u << 30;
-constexpr unsigned OS_FLAG_INC = 2u << 30;
-constexpr unsigned OS_VAL_MASK = (1u << 30) - 1u;
 
 size_t onesweep_scratch_bytes(long long max_count, int max_passes) {
     long long tiles = (max_count + OS_TILE - 1) / OS_TILE + 1;
@@ -371,81 +368,116 @@ __global__ void __launch_bounds__(256) k_os_hist(long long count, const unsigned
     }
 }
 
-__global__ void __launch_bounds__(OS_THREADS) k_onesweep(long long count, const unsigned* __restrict__ kin,
-                                                         const unsigned* __restrict__ vin,
-                                                         unsigned* __restrict__ kout, unsigned* __restrict__ vout,
-                                                         int shift, const unsigned* __restrict__ pass_hist,
-                                                         unsigned* status, unsigned* ticket) {
+// per-tile digit counts of one pass: cnt[tile][256]
+__global__ void __launch_bounds__(OS_THREADS) k_os_count(long long count, const unsigned* __restrict__ keys,
+                                                         int shift, unsigned* __restrict__ cnt) {
+    __shared__ unsigned s_h[RADIX];
+    s_h[threadIdx.x] = 0;
+    __syncthreads();
+    const long long base = (long long)blockIdx.x * OS_TILE;
+#pragma unroll 4
+    for (int i = 0; i < OS_ITEMS; i++) {
+        const long long idx = base + i * OS_THREADS + threadIdx.x;
+        if (idx < count) atomicAdd(&s_h[(__ldg(keys + idx) >> shift) & 0xffu], 1u);
+    }
+    __syncthreads();
+    cnt[(size_t)blockIdx.x * RADIX + threadIdx.x] = s_h[threadIdx.x];
+}
+
+// Stable scatter of one 8-bit pass.  Tile b's base offset for digit d is
+// ghist_excl[d] + sum_{j<b} cnt[j][d] (summed here in parallel -- no
+// inter-block waiting); items are ranked with warp match + per-warp counters,
+// staged in shared memory in tile-local sorted order and written out in
+// coalesced runs.
+__global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, const unsigned* __restrict__ kin,
+                                                           const unsigned* __restrict__ vin,
+                                                           unsigned* __restrict__ kout, unsigned* __restrict__ vout,
+                                                           int shift, const unsigned* __restrict__ pass_hist,
+                                                           const unsigned* __restrict__ cnt) {
     __shared__ unsigned s_wc[OS_THREADS / 32][RADIX];
-    __shared__ unsigned s_gbase[RADIX];
-    __shared__ unsigned s_tile;
+    __shared__ unsigned s_lstart[RADIX];  // tile-local start of each digit
+    __shared__ unsigned s_gbase[RADIX];   // global start of this tile's digit run
+    __shared__ unsigned s_k[OS_TILE];  // also holds the predecessor partial sums early on
+    __shared__ unsigned s_v[OS_TILE];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    const unsigned tile = blockIdx.x;
     for (int w = 0; w < OS_THREADS / 32; w++) s_wc[w][threadIdx.x] = 0;
-    // exclusive scan of the global digit histogram for this pass
+    // predecessor sums: warp w sums rows j = w, w+8, ... for all 256 digits (8 per lane)
+    unsigned (*s_part)[RADIX] = reinterpret_cast<unsigned (*)[RADIX]>(s_k);
+    {
+        unsigned acc[RADIX / 32];
+#pragma unroll
+        for (int k = 0; k < RADIX / 32; k++) acc[k] = 0;
+        for (unsigned j = warp; j < tile; j += OS_THREADS / 32) {
+            const unsigned* row = cnt + (size_t)j * RADIX;
+#pragma unroll
+            for (int k = 0; k < RADIX / 32; k++) acc[k] += __ldg(row + k * 32 + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < RADIX / 32; k++) s_part[warp][k * 32 + lane] = acc[k];
+    }
     unsigned tot;
-    unsigned gofs = block_excl_scan(pass_hist[threadIdx.x], tot);  // contains __syncthreads
-    const unsigned tile = s_tile;
+    const unsigned gofs = block_excl_scan(pass_hist[threadIdx.x], tot);  // has __syncthreads
+    {
+        unsigned pre = 0;
+#pragma unroll
+        for (int w = 0; w < OS_THREADS / 32; w++) pre += s_part[w][threadIdx.x];
+        s_gbase[threadIdx.x] = gofs + pre;
+    }
     const long long base = (long long)tile * OS_TILE + (long long)warp * (OS_TILE / (OS_THREADS / 32));
     const unsigned lt = lanemask_lt();
     unsigned key[OS_ITEMS], val[OS_ITEMS], off[OS_ITEMS];
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; i++) {
-        long long idx = base + i * 32 + lane;
-        bool valid = idx < count;
+        const long long idx = base + i * 32 + lane;
+        const bool valid = idx < count;
         key[i] = valid ? kin[idx] : 0u;
         val[i] = valid ? vin[idx] : 0u;
     }
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; i++) {
-        long long idx = base + i * 32 + lane;
-        bool valid = idx < count;
-        unsigned d = valid ? ((key[i] >> shift) & 0xffu) : 0x100u;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        unsigned rank = __popc(peers & lt);
-        unsigned b = valid ? s_wc[warp][d] : 0u;
+        const long long idx = base + i * 32 + lane;
+        const bool valid = idx < count;
+        const unsigned d = valid ? ((key[i] >> shift) & 0xffu) : 0x100u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned rank = __popc(peers & lt);
+        const unsigned b = valid ? s_wc[warp][d] : 0u;
         __syncwarp();
         if (valid && rank == 0) s_wc[warp][d] = b + __popc(peers);
         __syncwarp();
         off[i] = b + rank;
     }
     __syncthreads();
-    // per digit: warp-exclusive prefix + block count
+    // per digit: warp-exclusive prefix and the tile-local digit start
     unsigned run = 0;
 #pragma unroll
     for (int w = 0; w < OS_THREADS / 32; w++) {
-        unsigned c = s_wc[w][threadIdx.x];
+        const unsigned c = s_wc[w][threadIdx.x];
         s_wc[w][threadIdx.x] = run;
         run += c;
     }
-    const unsigned d = threadIdx.x;
-    volatile unsigned* st = status;
-    unsigned excl = 0;
-    if (tile == 0) {
-        st[d] = OS_FLAG_INC | run;
-    } else {
-        st[(size_t)tile * RADIX + d] = OS_FLAG_AGG | run;
-        long long j = (long long)tile - 1;
-        while (true) {
-            unsigned s = st[(size_t)j * RADIX + d];
-            if ((s & ~OS_VAL_MASK) == 0) continue;
-            excl += s & OS_VAL_MASK;
-            if (s & OS_FLAG_INC) break;
-            j--;
-        }
-        st[(size_t)tile * RADIX + d] = OS_FLAG_INC | (excl + run);
-    }
-    s_gbase[d] = gofs + excl;
+    unsigned tot2;
+    const unsigned lstart = block_excl_scan(run, tot2);  // has __syncthreads
+    s_lstart[threadIdx.x] = lstart;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; i++) {
-        long long idx = base + i * 32 + lane;
+        const long long idx = base + i * 32 + lane;
         if (idx < count) {
-            unsigned dd = (key[i] >> shift) & 0xffu;
-            unsigned pos = s_gbase[dd] + s_wc[warp][dd] + off[i];
-            kout[pos] = key[i];
-            vout[pos] = val[i];
+            const unsigned dd = (key[i] >> shift) & 0xffu;
+            const unsigned lp = s_lstart[dd] + s_wc[warp][dd] + off[i];
+            s_k[lp] = key[i];
+            s_v[lp] = val[i];
         }
+    }
+    __syncthreads();
+    const long long n_here = min((long long)OS_TILE, count - (long long)tile * OS_TILE);
+    for (int lp = threadIdx.x; lp < n_here; lp += OS_THREADS) {
+        const unsigned k = s_k[lp];
+        const unsigned dd = (k >> shift) & 0xffu;
+        const unsigned pos = s_gbase[dd] + (lp - s_lstart[dd]);
+        kout[pos] = k;
+        vout[pos] = s_v[lp];
     }
 }
 
@@ -455,18 +487,17 @@ int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned*
     if (count <= 1 || nbits <= 0) return 0;
     int npass = (nbits + 7) / 8;
     long long tiles = (count + OS_TILE - 1) / OS_TILE;
-    unsigned* status = (unsigned*)scratch;
-    unsigned* hist = status + (size_t)npass * tiles * RADIX;
-    unsigned* tickets = hist + npass * RADIX;
-    cudaMemsetAsync(scratch, 0, sizeof(unsigned) * ((size_t)npass * tiles * RADIX + npass * RADIX + 16), st);
+    unsigned* cnt = (unsigned*)scratch;  // [tiles][256]
+    unsigned* hist = cnt + (size_t)4 * tiles * RADIX;
+    cudaMemsetAsync(hist, 0, sizeof(unsigned) * npass * RADIX, st);
     long long hg = (count + 255) / 256;
     int hgrid = (int)(hg < 148 * 4 ? hg : 148 * 4);
     k_os_hist<<<hgrid, 256, 0, st>>>(count, keys, 0, npass, hist);
     unsigned *kin = keys, *vin = vals, *kout = keys_alt, *vout = vals_alt;
     int parity = 0;
     for (int p = 0; p < npass; p++) {
-        k_onesweep<<<(unsigned)tiles, OS_THREADS, 0, st>>>(count, kin, vin, kout, vout, 8 * p, hist + p * RADIX,
-                                                           status + (size_t)p * tiles * RADIX, tickets + p);
+        k_os_count<<<(unsigned)tiles, OS_THREADS, 0, st>>>(count, kin, 8 * p, cnt);
+        k_os_scatter<<<(unsigned)tiles, OS_THREADS, 0, st>>>(count, kin, vin, kout, vout, 8 * p, hist + p * RADIX, cnt);
         unsigned* t = kin; kin = kout; kout = t;
         t = vin; vin = vout; vout = t;
         parity ^= 1;
