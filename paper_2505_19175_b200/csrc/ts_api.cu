@@ -397,7 +397,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     compact_accepted32(n, c->flag, c->key, h.key_min, kshift, k32, c->vals_c, c->sort, st);
     g_launches += n > 0 ? 3 : 0;
     int par = onesweep_sort_u32(m, k32, c->vals_c, k32_alt, c->vals_alt, knb, c->os_buf, st);
-    if (m > 1 && knb > 0) g_launches += 1 + (knb + 7) / 8;
+    if (m > 1 && knb > 0) g_launches += 3 * ((knb + 7) / 8);
     c->sorted_src = par ? c->vals_alt : c->vals_c;
     if (kshift > 0) {
         fix_depth_runs(m, par ? k32_alt : k32, (unsigned*)c->sorted_src, c->key, st);
@@ -412,7 +412,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     g_launches += m > 0 ? 4 : 0;
     int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
     par = onesweep_sort_u32(e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits, c->os_buf, st);
-    if (e > 1 && tbits > 0) g_launches += 1 + (tbits + 7) / 8;
+    if (e > 1 && tbits > 0) g_launches += 3 * ((tbits + 7) / 8);
     const unsigned* skey = par ? c->tkey_alt : c->tkey;
     c->ent_src = par ? c->tval_alt : c->tval;
     tile_ranges(e, skey, ntiles, c->tile_start, st);

@@ -352,78 +352,89 @@ size_t onesweep_scratch_bytes(long long max_count, int max_passes) {
     return sizeof(unsigned) * ((size_t)max_passes * tiles * RADIX + (size_t)max_passes * RADIX + 64);
 }
 
-__global__ void __launch_bounds__(256) k_os_hist(long long count, const unsigned* __restrict__ keys, int shift0,
-                                                 int npass, unsigned* __restrict__ ghist) {
-    __shared__ unsigned s_h[4][RADIX];
-    for (int k = threadIdx.x; k < 4 * RADIX; k += 256) (&s_h[0][0])[k] = 0;
-    __syncthreads();
-    for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < count; i += (long long)gridDim.x * 256) {
-        unsigned k = keys[i];
-        for (int p = 0; p < npass; p++) atomicAdd(&s_h[p][(k >> (shift0 + 8 * p)) & 0xffu], 1u);
-    }
-    __syncthreads();
-    for (int p = 0; p < npass; p++) {
-        unsigned v = s_h[p][threadIdx.x];
-        if (v) atomicAdd(&ghist[p * RADIX + threadIdx.x], v);
-    }
-}
-
-// per-tile digit counts of one pass: cnt[tile][256]
+// per-tile digit counts of one pass, digit-major: cnt[d * tiles + tile]
 __global__ void __launch_bounds__(OS_THREADS) k_os_count(long long count, const unsigned* __restrict__ keys,
-                                                         int shift, unsigned* __restrict__ cnt) {
+                                                         int shift, unsigned* __restrict__ cnt, int tiles) {
     __shared__ unsigned s_h[RADIX];
     s_h[threadIdx.x] = 0;
     __syncthreads();
     const long long base = (long long)blockIdx.x * OS_TILE;
-#pragma unroll 4
-    for (int i = 0; i < OS_ITEMS; i++) {
-        const long long idx = base + i * OS_THREADS + threadIdx.x;
-        if (idx < count) atomicAdd(&s_h[(__ldg(keys + idx) >> shift) & 0xffu], 1u);
+    if (base + OS_TILE <= count && (((size_t)(keys + base)) & 15) == 0) {
+        const uint4* k4 = reinterpret_cast<const uint4*>(keys + base);
+        uint4 v[OS_ITEMS / 4];
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS / 4; i++) v[i] = __ldg(k4 + i * OS_THREADS + threadIdx.x);
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS / 4; i++) {
+            atomicAdd(&s_h[(v[i].x >> shift) & 0xffu], 1u);
+            atomicAdd(&s_h[(v[i].y >> shift) & 0xffu], 1u);
+            atomicAdd(&s_h[(v[i].z >> shift) & 0xffu], 1u);
+            atomicAdd(&s_h[(v[i].w >> shift) & 0xffu], 1u);
+        }
+    } else {
+        for (int i = 0; i < OS_ITEMS; i++) {
+            const long long idx = base + i * OS_THREADS + threadIdx.x;
+            if (idx < count) atomicAdd(&s_h[(__ldg(keys + idx) >> shift) & 0xffu], 1u);
+        }
     }
     __syncthreads();
-    cnt[(size_t)blockIdx.x * RADIX + threadIdx.x] = s_h[threadIdx.x];
+    cnt[(size_t)threadIdx.x * tiles + blockIdx.x] = s_h[threadIdx.x];
 }
 
-// Stable scatter of one 8-bit pass.  Tile b's base offset for digit d is
-// ghist_excl[d] + sum_{j<b} cnt[j][d] (summed here in parallel -- no
-// inter-block waiting); items are ranked with warp match + per-warp counters,
-// staged in shared memory in tile-local sorted order and written out in
-// coalesced runs.
+// per digit (one block each): exclusive scan over tiles in place; tot[d] = column total
+__global__ void __launch_bounds__(1024) k_os_scan(unsigned* __restrict__ cnt, int tiles, unsigned* __restrict__ tot) {
+    __shared__ unsigned s_w[32];
+    unsigned* row = cnt + (size_t)blockIdx.x * tiles;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned carry = 0;
+    for (int b0 = 0; b0 < tiles; b0 += 1024) {
+        const int i = b0 + threadIdx.x;
+        const unsigned v = i < tiles ? row[i] : 0u;
+        unsigned x = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= (unsigned)off) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned w = s_w[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, w, off);
+                if (lane >= (unsigned)off) w += y;
+            }
+            s_w[lane] = w;
+        }
+        __syncthreads();
+        const unsigned ex = carry + (warp ? s_w[warp - 1] : 0u) + x - v;
+        if (i < tiles) row[i] = ex;
+        carry += s_w[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) tot[blockIdx.x] = carry;
+}
+
+// Stable scatter of one 8-bit pass: items are ranked with warp match +
+// per-warp counters, staged in shared memory in tile-local sorted order and
+// written out in coalesced runs at cnt_scanned[d][tile] + global digit start.
 __global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, const unsigned* __restrict__ kin,
                                                            const unsigned* __restrict__ vin,
                                                            unsigned* __restrict__ kout, unsigned* __restrict__ vout,
-                                                           int shift, const unsigned* __restrict__ pass_hist,
-                                                           const unsigned* __restrict__ cnt) {
+                                                           int shift, const unsigned* __restrict__ cnt, int tiles,
+                                                           const unsigned* __restrict__ tot) {
     __shared__ unsigned s_wc[OS_THREADS / 32][RADIX];
-    __shared__ unsigned s_lstart[RADIX];  // tile-local start of each digit
-    __shared__ unsigned s_gbase[RADIX];   // global start of this tile's digit run
-    __shared__ unsigned s_k[OS_TILE];  // also holds the predecessor partial sums early on
+    __shared__ unsigned s_lstart[RADIX];
+    __shared__ unsigned s_gbase[RADIX];
+    __shared__ unsigned s_k[OS_TILE];
     __shared__ unsigned s_v[OS_TILE];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned tile = blockIdx.x;
     for (int w = 0; w < OS_THREADS / 32; w++) s_wc[w][threadIdx.x] = 0;
-    // predecessor sums: warp w sums rows j = w, w+8, ... for all 256 digits (8 per lane)
-    unsigned (*s_part)[RADIX] = reinterpret_cast<unsigned (*)[RADIX]>(s_k);
-    {
-        unsigned acc[RADIX / 32];
-#pragma unroll
-        for (int k = 0; k < RADIX / 32; k++) acc[k] = 0;
-        for (unsigned j = warp; j < tile; j += OS_THREADS / 32) {
-            const unsigned* row = cnt + (size_t)j * RADIX;
-#pragma unroll
-            for (int k = 0; k < RADIX / 32; k++) acc[k] += __ldg(row + k * 32 + lane);
-        }
-#pragma unroll
-        for (int k = 0; k < RADIX / 32; k++) s_part[warp][k * 32 + lane] = acc[k];
-    }
-    unsigned tot;
-    const unsigned gofs = block_excl_scan(pass_hist[threadIdx.x], tot);  // has __syncthreads
-    {
-        unsigned pre = 0;
-#pragma unroll
-        for (int w = 0; w < OS_THREADS / 32; w++) pre += s_part[w][threadIdx.x];
-        s_gbase[threadIdx.x] = gofs + pre;
-    }
+    unsigned tsum;
+    const unsigned gstart = block_excl_scan(tot[threadIdx.x], tsum);  // has __syncthreads
+    s_gbase[threadIdx.x] = gstart + cnt[(size_t)threadIdx.x * tiles + tile];
     const long long base = (long long)tile * OS_TILE + (long long)warp * (OS_TILE / (OS_THREADS / 32));
     const unsigned lt = lanemask_lt();
     unsigned key[OS_ITEMS], val[OS_ITEMS], off[OS_ITEMS];
@@ -431,8 +442,8 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, cons
     for (int i = 0; i < OS_ITEMS; i++) {
         const long long idx = base + i * 32 + lane;
         const bool valid = idx < count;
-        key[i] = valid ? kin[idx] : 0u;
-        val[i] = valid ? vin[idx] : 0u;
+        key[i] = valid ? __ldg(kin + idx) : 0u;
+        val[i] = valid ? __ldg(vin + idx) : 0u;
     }
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; i++) {
@@ -448,7 +459,6 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, cons
         off[i] = b + rank;
     }
     __syncthreads();
-    // per digit: warp-exclusive prefix and the tile-local digit start
     unsigned run = 0;
 #pragma unroll
     for (int w = 0; w < OS_THREADS / 32; w++) {
@@ -486,18 +496,15 @@ int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned*
                       unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st) {
     if (count <= 1 || nbits <= 0) return 0;
     int npass = (nbits + 7) / 8;
-    long long tiles = (count + OS_TILE - 1) / OS_TILE;
-    unsigned* cnt = (unsigned*)scratch;  // [tiles][256]
-    unsigned* hist = cnt + (size_t)4 * tiles * RADIX;
-    cudaMemsetAsync(hist, 0, sizeof(unsigned) * npass * RADIX, st);
-    long long hg = (count + 255) / 256;
-    int hgrid = (int)(hg < 148 * 4 ? hg : 148 * 4);
-    k_os_hist<<<hgrid, 256, 0, st>>>(count, keys, 0, npass, hist);
+    const int tiles = (int)((count + OS_TILE - 1) / OS_TILE);
+    unsigned* cnt = (unsigned*)scratch;  // [256][tiles]
+    unsigned* tot = cnt + (size_t)RADIX * tiles;
     unsigned *kin = keys, *vin = vals, *kout = keys_alt, *vout = vals_alt;
     int parity = 0;
     for (int p = 0; p < npass; p++) {
-        k_os_count<<<(unsigned)tiles, OS_THREADS, 0, st>>>(count, kin, 8 * p, cnt);
-        k_os_scatter<<<(unsigned)tiles, OS_THREADS, 0, st>>>(count, kin, vin, kout, vout, 8 * p, hist + p * RADIX, cnt);
+        k_os_count<<<tiles, OS_THREADS, 0, st>>>(count, kin, 8 * p, cnt, tiles);
+        k_os_scan<<<RADIX, 1024, 0, st>>>(cnt, tiles, tot);
+        k_os_scatter<<<tiles, OS_THREADS, 0, st>>>(count, kin, vin, kout, vout, 8 * p, cnt, tiles, tot);
         unsigned* t = kin; kin = kout; kout = t;
         t = vin; vin = vout; vout = t;
         parity ^= 1;
