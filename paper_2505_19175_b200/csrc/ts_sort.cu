@@ -344,7 +344,7 @@ void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st) {
 namespace ts {
 
 constexpr int OS_THREADS = 256;
-constexpr int OS_ITEMS = 16;
+constexpr int OS_ITEMS = 8;
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096
 
 size_t onesweep_scratch_bytes(long long max_count, int max_passes) {
