@@ -32,6 +32,12 @@ __device__ __forceinline__ float fast_lg2(float x) {
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ void red_max_shared(unsigned* p, unsigned v) {
+    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_shared(int* p, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ float fast_ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -470,32 +476,40 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
         __syncthreads();
         for (int jb = 0; jb < nb; jb += 32) {
             if (!__any_sync(0xffffffffu, !done)) break;
-            // lane l tests entry jb+l against the 8 quads of this warp's strip
-            unsigned q8 = 0u;
+            // lane l builds, for entry jb+l, the 32-bit mask of this warp's pixels inside
+            // its bbox: bits [4g, 4g+4) = quad g (column bit = lane&1, row bit = lane>>1&1)
+            unsigned W = 0u;
             const int jl = jb + (int)lane;
             if (jl < nb) {
                 const short4 bb = s_bb[jl];
-                if (bb.x < X0 + 2 && bb.y > X0) {
-                    int g0 = max(((int)bb.z - Y0) >> 1, 0), g1 = min(((int)bb.w - 1 - Y0) >> 1, 7);
-                    if (g1 >= g0) q8 = (0xffu >> (7 - (g1 - g0))) << g0;
+                const unsigned cb = (unsigned)(X0 >= bb.x && X0 < bb.y) | ((unsigned)(X0 + 1 >= bb.x && X0 + 1 < bb.y) << 1);
+                const int r0 = max((int)bb.z - Y0, 0), r1 = min((int)bb.w - Y0, TILE);
+                if (cb && r1 > r0) {
+                    unsigned x = ((1u << (r1 - r0)) - 1u) << r0;  // rows of the tile, 16 bits
+                    x = (x | (x << 8)) & 0x00FF00FFu;
+                    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+                    x = (x | (x << 2)) & 0x33333333u;
+                    x = (x | (x << 1)) & 0x55555555u;                // row r -> bit 2r
+                    W = x * cb;                                       // row r -> bits 2r, 2r+1 = cb
                 }
             }
             unsigned gmask = 0u;
 #pragma unroll
             for (int g = 0; g < 8; g++) {
-                const unsigned bm = __ballot_sync(0xffffffffu, (q8 >> g) & 1u);
+                const unsigned bm = __ballot_sync(0xffffffffu, ((W >> (4 * g)) & 0xFu) != 0u);
                 if ((int)grp == g) gmask = bm;
             }
             if (done) gmask = 0u;
+            const unsigned mybit = 4u * grp + (lane & 3u);
             while (__any_sync(0xffffffffu, gmask != 0u)) {
                 const int jo = __ffs(gmask) - 1;
                 gmask &= gmask - 1;
                 const int j = jb + jo;
                 bool contrib = false;
                 float w = 0.f;
+                const unsigned Wj = __shfl_sync(0xffffffffu, W, jo & 31);
                 if (jo >= 0 && !done) {
-                    const short4 bb = s_bb[j];
-                    if (px >= bb.x && px < bb.y && py >= bb.z && py < bb.w) {
+                    if ((Wj >> mybit) & 1u) {
                         const RecF& r = s_rec[j].r;
                         const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
                         const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
@@ -531,7 +545,7 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                                         T = tn;
                                         done = tn < T_MIN;
                                         // pixel count uses the fp64 weight
-                                        if (wd > opt.tau_contrib) atomicAdd(&s_pix[j], 1);
+                                        if (wd > opt.tau_contrib) red_add_shared(&s_pix[j], 1);
                                     }
                                 } else {
                                     float ea;
@@ -552,7 +566,7 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                                         T = tn;
                                         epsT = en;
                                         done = tn < T_MIN_F;
-                                        if (w > tau) atomicAdd(&s_pix[j], 1);
+                                        if (w > tau) red_add_shared(&s_pix[j], 1);
                                     }
                                 }
                             }
@@ -564,7 +578,7 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                     }
                 }
                 if (done) gmask = 0u;
-                if (contrib) atomicMax(&s_maxw[j], __float_as_uint(w));
+                if (contrib) red_max_shared(&s_maxw[j], __float_as_uint(w));
             }
         }
         __syncthreads();
