@@ -613,6 +613,236 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
 }
 
 // ---------------------------------------------------------------------------
+// k_blend_render: the render-only forward (fp32 compositing, guard band) with
+// deferred alpha.  Per batch of FB entries, per warp (2x16 strip, 8 groups of
+// 4 lanes = 2x2 quads, as k_blend_fast):
+//   1. evaluation -- each group walks the entries overlapping its quad; a lane
+//      whose pixel is inside the bbox evaluates r in fp64 and, if r >= r_lo,
+//      appends (entry, r) to its slot list (no alpha work here);
+//   2. alpha -- the warp's candidates are processed densely, one per lane;
+//   3. compositing -- lane = pixel walks its slots in entry order.
+// Overflowing a pixel's slots, or any decision inside the guard band, flags
+// the pixel for the exact fix-up (nothing of that batch is committed for it).
+// ---------------------------------------------------------------------------
+constexpr int QCAP = 12;
+
+__global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const RecF* __restrict__ rec,
+                                                      const short4* __restrict__ bbox,
+                                                      const int* __restrict__ tile_start,
+                                                      const unsigned* __restrict__ ent_src,
+                                                      FastBlendOut out) {
+    __shared__ SRec s_rec[FB];
+    __shared__ short4 s_bb[FB];
+    __shared__ unsigned s_src[FB];
+    __shared__ unsigned s_maxw[FB];
+    __shared__ int s_pix[FB];
+    __shared__ float s_qa[8][QCAP][32];          // r (fp32) -> alpha; NaN = guard band
+    __shared__ float s_qe[8][QCAP][32];          // relative error bound of alpha
+    __shared__ unsigned char s_qj[8][QCAP][32];  // entry index in the batch
+    const int t = blockIdx.x;
+    const int tx = t % cam.ntx, ty = t / cam.ntx;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned grp = lane >> 2;
+    const int X0 = tx * TILE + 2 * (int)warp;
+    const int Y0 = ty * TILE;
+    const int px = X0 + (int)(lane & 1);
+    const int py = Y0 + 2 * (int)grp + (int)((lane >> 1) & 1);
+    const double pcx = px + 0.5, pcy = py + 0.5;
+    const bool inside = px < cam.width && py < cam.height;
+    const unsigned mybit = 4u * grp + (lane & 3u);
+    const unsigned lt = lanemask_lt();
+    float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
+    int last = -1, cnt = 0, flag_pos = -1;
+    bool done = !inside;
+    const int s = tile_start[t], e = tile_start[t + 1];
+    const float tau = (float)opt.tau_contrib;
+    if (threadIdx.x < FB) {
+        s_maxw[threadIdx.x] = 0u;
+        s_pix[threadIdx.x] = 0;
+    }
+    float (*qa)[32] = s_qa[warp];
+    float (*qe)[32] = s_qe[warp];
+    unsigned char (*qj)[32] = s_qj[warp];
+    for (int b = s; b < e; b += FB) {
+        if (__syncthreads_count(!done) == 0) break;
+        const int nb = min(FB, e - b);
+        for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
+            const int j = c >> 3, q = c & 7;
+            const unsigned src = __ldg(ent_src + b + j);
+            if (q == 0) {
+                s_src[j] = src;
+                s_bb[j] = __ldg(bbox + src);
+            }
+            reinterpret_cast<float4*>(&s_rec[j].r)[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
+        }
+        __syncthreads();
+        if (__any_sync(0xffffffffu, !done)) {
+            // ---- 1. evaluation ----
+            int qn = 0;
+            for (int jb = 0; jb < nb; jb += 32) {
+                unsigned W = 0u;
+                const int jl = jb + (int)lane;
+                if (jl < nb) {
+                    const short4 bb = s_bb[jl];
+                    const unsigned cb =
+                        (unsigned)(X0 >= bb.x && X0 < bb.y) | ((unsigned)(X0 + 1 >= bb.x && X0 + 1 < bb.y) << 1);
+                    const int r0 = max((int)bb.z - Y0, 0), r1 = min((int)bb.w - Y0, TILE);
+                    if (cb && r1 > r0) {
+                        unsigned x = ((1u << (r1 - r0)) - 1u) << r0;
+                        x = (x | (x << 8)) & 0x00FF00FFu;
+                        x = (x | (x << 4)) & 0x0F0F0F0Fu;
+                        x = (x | (x << 2)) & 0x33333333u;
+                        x = (x | (x << 1)) & 0x55555555u;
+                        W = x * cb;
+                    }
+                }
+                unsigned gmask = 0u;
+#pragma unroll
+                for (int g = 0; g < 8; g++) {
+                    const unsigned bm = __ballot_sync(0xffffffffu, ((W >> (4 * g)) & 0xFu) != 0u);
+                    if ((int)grp == g) gmask = bm;
+                }
+                if (done) gmask = 0u;
+                while (__any_sync(0xffffffffu, gmask != 0u)) {
+                    const int jo = __ffs(gmask) - 1;
+                    gmask &= gmask - 1;
+                    const unsigned Wj = __shfl_sync(0xffffffffu, W, jo & 31);
+                    if (jo >= 0 && ((Wj >> mybit) & 1u)) {
+                        const int j = jb + jo;
+                        const RecF& r = s_rec[j].r;
+                        const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
+                        const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
+                        const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
+                        if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
+                            const double rr = fmin(l0, fmin(l1, l2));
+                            if (qn < QCAP) {
+                                qa[qn][lane] = rr > r.r_hi ? (float)(opt.mode == 0 ? fmin(rr, 1.0) : rr)
+                                                           : __int_as_float(0x7fc00000);
+                                qj[qn][lane] = (unsigned char)j;
+                            }
+                            qn++;
+                        }
+                    }
+                }
+            }
+            // ---- 2. alpha for all candidates of the warp, one per lane ----
+            const int qc = min(qn, QCAP);
+            int o = qc;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, o, off);
+                if ((int)lane >= off) o += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, o, 31);
+            o -= qc;  // exclusive
+            __syncwarp();
+            for (int q0 = 0; q0 < total; q0 += 32) {
+                const int q = q0 + (int)lane;
+                int L = 0;
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = L + step;
+                    const int ov = __shfl_sync(0xffffffffu, o, cand & 31);
+                    if (cand < 32 && ov <= q) L = cand;
+                }
+                const int oL = __shfl_sync(0xffffffffu, o, L);
+                if (q < total) {
+                    const int k = q - oL;
+                    const float rv = qa[k][L];
+                    if (!isnan(rv)) {
+                        const RecF& r = s_rec[qj[k][L]].r;
+                        float a, ea;
+                        if (opt.mode == 0) {
+                            const float lg = fast_lg2(rv);
+                            const float arg = fmaf(r.f0, lg, r.f1);
+                            a = fast_ex2(arg);
+                            ea = 5e-7f + r.f0 * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
+                        } else {
+                            const float x = rv * r.f0;
+                            a = __fdividef(r.f1, 1.0f + fast_ex2(fminf(x, 1009.9f)));
+                            ea = 8e-7f + 1.2e-7f * fabsf(x);
+                        }
+                        qa[k][L] = fminf(a, ALPHA_CLAMP_F);
+                        qe[k][L] = ea;
+                    }
+                }
+            }
+            __syncwarp();
+            // ---- 3. compositing, lane = pixel, slots in entry order ----
+            if (!done) {
+                if (qn > QCAP) {
+                    flag_pos = b;  // nothing of this batch committed for this pixel
+                    done = true;
+                } else {
+                    for (int k = 0; k < qn; k++) {
+                        const int j = qj[k][lane];
+                        const float a = qa[k][lane];
+                        if (isnan(a)) {  // r inside the contribution band
+                            flag_pos = b + j;
+                            done = true;
+                            break;
+                        }
+                        const float ea = qe[k][lane];
+                        const float w = T * a;
+                        const float tn = fmaf(-T, a, T);
+                        const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                        const float ew = epsT + ea + 1.2e-7f;
+                        if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                            fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f)) {
+                            flag_pos = b + j;
+                            done = true;
+                            break;
+                        }
+                        const RecF& r = s_rec[j].r;
+                        C0 = fmaf(w, r.rgb[0], C0);
+                        C1 = fmaf(w, r.rgb[1], C1);
+                        C2 = fmaf(w, r.rgb[2], C2);
+                        last = b + j;
+                        cnt++;
+                        T = tn;
+                        epsT = en;
+                        red_max_shared(&s_maxw[j], __float_as_uint(w));
+                        if (w > tau) red_add_shared(&s_pix[j], 1);
+                        if (T < T_MIN_F) {
+                            done = true;
+                            break;
+                        }
+                    }
+                }
+            }
+            (void)lt;
+        }
+        __syncthreads();
+        if (threadIdx.x < nb) {
+            const unsigned src = s_src[threadIdx.x];
+            if (s_maxw[threadIdx.x] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
+            if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
+            s_maxw[threadIdx.x] = 0u;
+            s_pix[threadIdx.x] = 0;
+        }
+    }
+    if (inside) {
+        const int p = py * cam.width + px;
+        if (flag_pos >= 0) {
+            unsigned long long k = atomicAdd(&out.ctr->n_flagged, 1ull);
+            out.flags[k] = make_int2(p, flag_pos);
+        } else {
+            if (out.image) {
+                out.image[p * 3 + 0] = fminf(fmaxf(fmaf(T, (float)opt.bg[0], C0), 0.f), 1.f);
+                out.image[p * 3 + 1] = fminf(fmaxf(fmaf(T, (float)opt.bg[1], C1), 0.f), 1.f);
+                out.image[p * 3 + 2] = fminf(fmaxf(fmaf(T, (float)opt.bg[2], C2), 0.f), 1.f);
+            }
+            if (out.alpha_map) out.alpha_map[p] = 1.f - T;
+            out.t_final[p] = T;
+            if (out.t_final64) out.t_final64[p] = (double)T;
+            out.last_pos[p] = last;
+            if (out.n_frag) out.n_frag[p] = cnt;
+            if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_fixup_fwd: exact (fp64) replay of flagged pixels, one CTA per pixel.
 // The CTA evaluates alpha for FXC consecutive tile entries in parallel
 // (shared memory), then warp 0 composites the contributing ones in entry
@@ -718,12 +948,12 @@ void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int
         const double* o = (const double*)soup.opacity;
         const double* sg = (const double*)soup.sigma;
         if (acc64) k_blend_fast<double, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
-        else k_blend_fast<double, false><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
+        else k_blend_render<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
     } else {
         const float* o = (const float*)soup.opacity;
         const float* sg = (const float*)soup.sigma;
         if (acc64) k_blend_fast<float, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
-        else k_blend_fast<float, false><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
+        else k_blend_render<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
     }
 }
 
