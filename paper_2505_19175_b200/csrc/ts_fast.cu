@@ -660,9 +660,6 @@ __global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const R
         s_maxw[threadIdx.x] = 0u;
         s_pix[threadIdx.x] = 0;
     }
-    float (*qa)[32] = s_qa[warp];
-    float (*qe)[32] = s_qe[warp];
-    unsigned char (*qj)[32] = s_qj[warp];
     for (int b = s; b < e; b += FB) {
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min(FB, e - b);
@@ -709,16 +706,19 @@ __global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const R
                     const unsigned Wj = __shfl_sync(0xffffffffu, W, jo & 31);
                     if (jo >= 0 && ((Wj >> mybit) & 1u)) {
                         const int j = jb + jo;
-                        const RecF& r = s_rec[j].r;
-                        const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
-                        const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
-                        const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
-                        if (l0 >= r.r_lo && l1 >= r.r_lo && l2 >= r.r_lo) {
-                            const double rr = fmin(l0, fmin(l1, l2));
+                        const double* a = s_rec[j].r.a;
+                        const double rlo = s_rec[j].r.r_lo;
+                        const double l0 = fma(a[0], pcx, fma(a[1], pcy, a[2]));
+                        const double l1 = fma(a[3], pcx, fma(a[4], pcy, a[5]));
+                        const double l2 = fma(a[6], pcx, fma(a[7], pcy, a[8]));
+                        if (l0 >= rlo && l1 >= rlo && l2 >= rlo) {
+                            const double m01 = l0 < l1 ? l0 : l1;
+                            const double rr = m01 < l2 ? m01 : l2;
+                            // NaN marks r inside the contribution band (resolved by the fix-up)
+                            const float rv = rr > s_rec[j].r.r_hi ? (float)rr : __int_as_float(0x7fc00000);
                             if (qn < QCAP) {
-                                qa[qn][lane] = rr > r.r_hi ? (float)(opt.mode == 0 ? fmin(rr, 1.0) : rr)
-                                                           : __int_as_float(0x7fc00000);
-                                qj[qn][lane] = (unsigned char)j;
+                                s_qa[warp][qn][lane] = rv;
+                                s_qj[warp][qn][lane] = (unsigned char)j;
                             }
                             qn++;
                         }
@@ -748,12 +748,12 @@ __global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const R
                 const int oL = __shfl_sync(0xffffffffu, o, L);
                 if (q < total) {
                     const int k = q - oL;
-                    const float rv = qa[k][L];
+                    const float rv = s_qa[warp][k][L];
                     if (!isnan(rv)) {
-                        const RecF& r = s_rec[qj[k][L]].r;
+                        const RecF& r = s_rec[s_qj[warp][k][L]].r;
                         float a, ea;
                         if (opt.mode == 0) {
-                            const float lg = fast_lg2(rv);
+                            const float lg = fast_lg2(fminf(rv, 1.f));
                             const float arg = fmaf(r.f0, lg, r.f1);
                             a = fast_ex2(arg);
                             ea = 5e-7f + r.f0 * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
@@ -762,8 +762,8 @@ __global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const R
                             a = __fdividef(r.f1, 1.0f + fast_ex2(fminf(x, 1009.9f)));
                             ea = 8e-7f + 1.2e-7f * fabsf(x);
                         }
-                        qa[k][L] = fminf(a, ALPHA_CLAMP_F);
-                        qe[k][L] = ea;
+                        s_qa[warp][k][L] = fminf(a, ALPHA_CLAMP_F);
+                        s_qe[warp][k][L] = ea;
                     }
                 }
             }
@@ -775,14 +775,14 @@ __global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const R
                     done = true;
                 } else {
                     for (int k = 0; k < qn; k++) {
-                        const int j = qj[k][lane];
-                        const float a = qa[k][lane];
+                        const int j = s_qj[warp][k][lane];
+                        const float a = s_qa[warp][k][lane];
                         if (isnan(a)) {  // r inside the contribution band
                             flag_pos = b + j;
                             done = true;
                             break;
                         }
-                        const float ea = qe[k][lane];
+                        const float ea = s_qe[warp][k][lane];
                         const float w = T * a;
                         const float tn = fmaf(-T, a, T);
                         const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
