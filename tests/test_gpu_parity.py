@@ -258,3 +258,26 @@ def test_north_star_forward_parity(rast, precision):
     f = fwd(rast, _dev(soup), intr, pose, precision)
     ref = O.render(soup, intr, pose)
     check_forward(rast, f, ref, intr, f"ns-{precision}")
+
+
+def test_view_parallel_step_matches_sum_of_oracle_views(rast):
+    """B200ViewTrainer (world 1): batch gradient == sum of per-view oracle gradients."""
+    from oracle import oracle as O
+    from paper_2505_19175_b200 import scenes
+    from paper_2505_19175_b200.parallel import B200ViewTrainer
+    soup = scenes.make_soup(2000, seed=21, size=0.2, sigma=(0.5, 3.0))
+    intr, _ = scenes.frontal_camera(96, 80, 100.0)
+    poses = scenes.orbit_cameras(4, seed=4)
+    d_np = [np.random.default_rng(100 + v).normal(size=(80, 96, 3)) for v in range(4)]
+    d_dev = [torch.as_tensor(d, dtype=torch.float32, device="cuda") for d in d_np]
+    tr = B200ViewTrainer(_dev(soup), intr, poses, d_dev, rasterizer=rast)
+    g = tr.step().grads.double().cpu().numpy()
+    want = 0
+    for v in range(4):
+        gr = O.render_backward(soup, intr, poses[v], d_image=d_np[v])
+        want = want + np.concatenate([gr.d_vertices.reshape(-1), gr.d_opacity, gr.d_sigma,
+                                      gr.d_sh.reshape(-1)])
+    n = len(soup.vertices)
+    parts = [(0, 9 * n), (9 * n, 10 * n), (10 * n, 11 * n), (11 * n, 59 * n)]
+    for lo, hi in parts:
+        assert rel_err(g[lo:hi], want[lo:hi]) < GRAD_RTOL
