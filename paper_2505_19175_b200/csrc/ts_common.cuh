@@ -66,15 +66,17 @@ struct __align__(16) RecF {
 };
 static_assert(sizeof(RecF) == 128, "RecF layout");
 
-// Backward-only per-source data (64 B): projected vertices relative to the
-// record origin in fp64 (edge lengths of near-degenerate triangles are
-// ill-conditioned) and the edge-orientation signs.
+// Backward-only per-source data (128 B).  Vertices relative to the record
+// origin and, per edge e (q_e -> q_{e+1}), the constants of its endpoint
+// derivative (_kernels.py:296-318) in fp64 -- edge lengths of near-degenerate
+// triangles are ill-conditioned:  sl = s/l,  ul = (b-a)_x/l^2,  vl = (b-a)_y/l^2.
 struct __align__(16) RecB {
     double qx[3], qy[3];
+    double sl[3], ul[3], vl[3];
     int esign;
-    int pad[3];
+    int pad;
 };
-static_assert(sizeof(RecB) == 64, "RecB layout");
+static_assert(sizeof(RecB) == 128, "RecB layout");
 
 // Screen-space gradient accumulator per source triangle (backward), fp64.
 // gq[6] (q0x,q0y,q1x,q1y,q2x,q2y), go, gsig, grgb[3], gphis, gz, pad

@@ -288,9 +288,15 @@ __global__ void __launch_bounds__(128) k_preprocess_fast(Cam cam, Opts opt, cons
                     for (int e = 0; e < 3; e++) {
                         rb.qx[e] = q[e * 2] - ox;
                         rb.qy[e] = q[e * 2 + 1] - oy;
+                        const int bi = e == 2 ? 0 : e + 1;
+                        const double ex = q[bi * 2] - q[e * 2], ey = q[bi * 2 + 1] - q[e * 2 + 1];
+                        const double il = 1.0 / sqrt(ex * ex + ey * ey);
+                        rb.sl[e] = ((esign >> e) & 1) ? -il : il;
+                        rb.ul[e] = ex * il * il;
+                        rb.vl[e] = ey * il * il;
                     }
                     rb.esign = esign;
-                    rb.pad[0] = rb.pad[1] = rb.pad[2] = 0;
+                    rb.pad = 0;
                     out.recb[i] = rb;
                 }
                 (void)qf;
@@ -971,31 +977,39 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
 
 // ---------------------------------------------------------------------------
 // k_blend_bwd_fast: back to front from the saved last contributor
-// (_kernels.py:181-318).  Per fragment: r from the fp64 edge functions,
-// alpha with the reference formula in fp64 (exact opacity/sigma staged per
-// entry), transmittance reconstructed in fp64 from the training forward's
-// fp64 T_final, suffix colour and dL/dalpha in fp64 (they cancel); the
-// edge chain in fp64 too (near-degenerate triangles cancel heavily).  Per-entry
-// sums are warp-reduced in fp64 before fp64 atomics (native RED.F64) into the
-// per-source screen-gradient buffer.
+// (_kernels.py:181-318).  CTA per tile, warp = 16x2 pixel strip, all lanes on
+// the same entry so per-entry sums reduce inside the warp.  Per fragment:
+// r from the fp64 edge functions, alpha with the reference formula in fp64
+// (exact opacity/sigma staged per entry), transmittance reconstructed in
+// fp64 from the training forward's fp64 T_final, suffix colour, dL/dalpha and
+// the edge chain in fp64 (near-degenerate triangles cancel heavily).  The 12
+// per-entry values are butterfly reduce-scattered across the warp (16 double
+// shuffles), stored as per-warp partials in shared memory, summed over the
+// CTA's warps and added with one fp64 RED per (tile entry, component).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double bfly_step(double keep, double send, int off) {
+    return keep + __shfl_xor_sync(0xffffffffu, send, off);
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const T* __restrict__ verts,
-                                                        const T* __restrict__ opacity,
-                                                        const T* __restrict__ sigma,
-                                                        const RecF* __restrict__ rec,
-                                                        const RecB* __restrict__ recb,
-                                                        const int* __restrict__ tile_start,
-                                                        const unsigned* __restrict__ ent_src,
-                                                        const double* __restrict__ t_final,
-                                                        const int* __restrict__ last_pos,
-                                                        const float* __restrict__ d_image,
-                                                        double* __restrict__ sgrad) {
+__global__ void __launch_bounds__(256, 3) k_blend_bwd_fast(Cam cam, Opts opt, const T* __restrict__ verts,
+                                                           const T* __restrict__ opacity,
+                                                           const T* __restrict__ sigma,
+                                                           const RecF* __restrict__ rec,
+                                                           const RecB* __restrict__ recb,
+                                                           const int* __restrict__ tile_start,
+                                                           const unsigned* __restrict__ ent_src,
+                                                           const double* __restrict__ t_final,
+                                                           const int* __restrict__ last_pos,
+                                                           const float* __restrict__ d_image,
+                                                           double* __restrict__ sgrad) {
     (void)verts;
-    __shared__ RecF s_rec[FB];
-    __shared__ RecB s_rb[FB];
-    __shared__ double2 s_os[FB];
-    __shared__ unsigned s_src[FB];
+    constexpr int BB = 32;  // entries per batch
+    __shared__ RecF s_rec[BB];
+    __shared__ RecB s_rb[BB];
+    __shared__ double4 s_os[BB];                 // opacity, sigma, 1/opacity, 1/phis
+    __shared__ unsigned s_src[BB];
+    __shared__ float s_part[8][BB][12];          // per-warp per-entry partial sums
     __shared__ int s_hi;
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
@@ -1008,7 +1022,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
     const int s = tile_start[t];
     int my_last = -1;
     double Tc = 1.0;
-    float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
     if (inside) {
         const int p = py * cam.width + px;
         my_last = last_pos[p];
@@ -1023,125 +1037,154 @@ __global__ void __launch_bounds__(256) k_blend_bwd_fast(Cam cam, Opts opt, const
     if (my_last >= 0) atomicMax(&s_hi, my_last);
     __syncthreads();
     const int hi = s_hi;
-    for (int bend = hi + 1; bend > s; bend -= FB) {
-        const int bstart = max(s, bend - FB);
+    // lane -> reduced component after the butterfly: k = bits(16,8,4,2) of lane
+    const int kred = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    for (int bend = hi + 1; bend > s; bend -= BB) {
+        const int bstart = max(s, bend - BB);
         const int nb = bend - bstart;
         __syncthreads();
-        for (int c = threadIdx.x; c < nb * 12; c += blockDim.x) {
-            const int j = c / 12, q = c - j * 12;
+        for (int c = threadIdx.x; c < nb * 16; c += blockDim.x) {
+            const int j = c >> 4, q = c & 15;
             const unsigned src = __ldg(ent_src + bstart + j);
-            if (q == 0) {
-                s_src[j] = src;
-                s_os[j] = make_double2(opt.solid ? 1.0 : (double)opacity[src], (double)sigma[src]);
-            }
             if (q < 8)
                 reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
             else
                 reinterpret_cast<float4*>(&s_rb[j])[q - 8] = __ldg(reinterpret_cast<const float4*>(recb + src) + (q - 8));
+            if (q == 0) {
+                s_src[j] = src;
+                const double o = opt.solid ? 1.0 : (double)opacity[src];
+                s_os[j] = make_double4(o, (double)sigma[src], 1.0 / o, 0.0);
+            }
         }
+        for (int c = threadIdx.x; c < 8 * BB * 12; c += blockDim.x) (&s_part[0][0][0])[c] = 0.f;
         __syncthreads();
-        for (int jb = ((nb - 1) / 32) * 32; jb >= 0; jb -= 32) {
-            const int jl = jb + (int)lane;
-            const bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
-            unsigned mask = __ballot_sync(0xffffffffu, ov);
-            while (mask) {
-                const int j = jb + 31 - __clz(mask);
-                mask &= ~(1u << (j - jb));
-                const RecF& r = s_rec[j];
-                const int pos = bstart + j;
-                double g[12];
-#pragma unroll
-                for (int k = 0; k < 12; k++) g[k] = 0.0;
-                bool act = false;
-                if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
-                    int edge;
-                    const double rr = edge_r(r, pcx, pcy, edge);
-                    if (rr >= r.r_lo) {
-                        const double2 os = s_os[j];
-                        double a;
-                        if (opt.mode == 0) {
-                            const double rc = fmin(rr, 1.0);
-                            a = rr <= 0.0 ? 0.0 : os.x * (os.y == 1.0 ? rc : pow(rc, os.y));
-                        } else {
-                            double x = rr * r.phis / os.y;
-                            if (x > 700.0) x = 700.0;
-                            a = os.x * (1.0 / (1.0 + exp(x)));
-                        }
-                        const bool clamped = a > ALPHA_CLAMP;
-                        if (clamped) a = ALPHA_CLAMP;
-                        if (a >= ALPHA_MIN) {
-                            act = true;
-                            const double one_m = 1.0 - a;
-                            const double tb = Tc / one_m;
-                            const double w = tb * a;
-                            const float* c = r.rgb;
-                            g[SG_GRGB + 0] = w * d0;
-                            g[SG_GRGB + 1] = w * d1;
-                            g[SG_GRGB + 2] = w * d2;
-                            const double ga = d0 * (tb * c[0] - S0 / one_m) + d1 * (tb * c[1] - S1 / one_m) +
-                                              d2 * (tb * c[2] - S2 / one_m);
-                            S0 += w * c[0];
-                            S1 += w * c[1];
-                            S2 += w * c[2];
-                            Tc = tb;
-                            if (!clamped) {
-                                const double o = os.x, sg = os.y, phis = r.phis;
-                                g[SG_GO] = ga * (a / o);
-                                const double g_win = o * ga;
-                                const double window = a / o;
-                                const double phi = rr * phis;
-                                double g_phi;
-                                if (opt.mode == 0) {
-                                    const double rc = fmin(rr, 1.0);
-                                    g[SG_GSIG] = g_win * window * (double)__logf((float)rc);
-                                    const double g_r = g_win * sg * window / rc;
-                                    if (rr >= 1.0) {
-                                        g_phi = 0.0;
-                                    } else {
-                                        g_phi = g_r / phis;
-                                        g[SG_GPHIS] = -g_r * rr / phis;
-                                    }
+        if (threadIdx.x < nb) s_os[threadIdx.x].w = 1.0 / s_rec[threadIdx.x].phis;
+        __syncthreads();
+        const int jl = (int)lane;
+        const bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
+        unsigned mask = __ballot_sync(0xffffffffu, ov);
+        while (mask) {
+            const int j = 31 - __clz(mask);
+            mask &= ~(1u << j);
+            const RecF& r = s_rec[j];
+            const int pos = bstart + j;
+            double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0, g6 = 0, g7 = 0, g8 = 0, g9 = 0, g10 = 0, g11 = 0;
+            bool act = false;
+            if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
+                const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
+                const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
+                const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
+                // argmax of phi = argmin of phi/phi_s; ties -> lowest edge (strict >, _kernels.py:36-42)
+                int edge = 0;
+                double rr = l0;
+                if (l1 < rr) { rr = l1; edge = 1; }
+                if (l2 < rr) { rr = l2; edge = 2; }
+                if (rr >= r.r_lo) {
+                    const double4 os = s_os[j];
+                    double a;
+                    const double rc = rr < 1.0 ? rr : 1.0;
+                    if (opt.mode == 0) {
+                        a = rr <= 0.0 ? 0.0 : os.x * (os.y == 1.0 ? rc : pow(rc, os.y));
+                    } else {
+                        double x = rr * r.phis / os.y;
+                        if (x > 700.0) x = 700.0;
+                        a = os.x / (1.0 + exp(x));
+                    }
+                    const bool clamped = a > ALPHA_CLAMP;
+                    if (clamped) a = ALPHA_CLAMP;
+                    if (a >= ALPHA_MIN) {
+                        act = true;
+                        const double inv1m = 1.0 / (1.0 - a);
+                        const double tb = Tc * inv1m;
+                        const double w = tb * a;
+                        const float* c = r.rgb;
+                        g8 = w * d0;
+                        g9 = w * d1;
+                        g10 = w * d2;
+                        const double ga = d0 * (tb * c[0] - S0 * inv1m) + d1 * (tb * c[1] - S1 * inv1m) +
+                                          d2 * (tb * c[2] - S2 * inv1m);
+                        S0 = fma(w, (double)c[0], S0);
+                        S1 = fma(w, (double)c[1], S1);
+                        S2 = fma(w, (double)c[2], S2);
+                        Tc = tb;
+                        if (!clamped) {
+                            const double window = a * os.z;
+                            g6 = ga * window;  // d/d opacity = g_alpha * alpha / o
+                            const double g_win = os.x * ga;
+                            const double phi = rr * r.phis;
+                            double g_phi;
+                            if (opt.mode == 0) {
+                                g7 = g_win * window * log(rc);
+                                const double g_r = g_win * os.y * window / rc;
+                                if (rr >= 1.0) {
+                                    g_phi = 0.0;
                                 } else {
-                                    // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
-                                    const double E = exp(fmin(phi / sg, 700.0));
-                                    const double ww = E / ((1.0 + E) * (1.0 + E));
-                                    g[SG_GSIG] = g_win * ww * phi / (sg * sg);
-                                    g_phi = -g_win * ww / sg;
+                                    g_phi = g_r * os.w;
+                                    g11 = -g_r * rr * os.w;
                                 }
-                                // edge line derivative wrt its endpoints (_kernels.py:296-318),
-                                // coordinates relative to the record origin
-                                const RecB& rb = s_rb[j];
-                                const int ia = edge, ib = edge == 2 ? 0 : edge + 1;
-                                const double ax = rb.qx[ia], ay = rb.qy[ia], bx = rb.qx[ib], by = rb.qy[ib];
-                                const double pxr = (double)(px - r.ox) + 0.5, pyr = (double)(py - r.oy) + 0.5;
-                                const double ex = bx - ax, ey = by - ay;
-                                const double inv_l = rsqrt(ex * ex + ey * ey);
-                                const double inv_l2 = inv_l * inv_l;
-                                const double sgn = ((rb.esign >> edge) & 1) ? -1.0 : 1.0;
-                                g[SG_GQ + ia * 2] = g_phi * (sgn * (pyr - by) * inv_l - phi * (ax - bx) * inv_l2);
-                                g[SG_GQ + ia * 2 + 1] = g_phi * (sgn * (bx - pxr) * inv_l - phi * (ay - by) * inv_l2);
-                                g[SG_GQ + ib * 2] = g_phi * (sgn * (ay - pyr) * inv_l - phi * (bx - ax) * inv_l2);
-                                g[SG_GQ + ib * 2 + 1] = g_phi * (sgn * (pxr - ax) * inv_l - phi * (by - ay) * inv_l2);
+                            } else {
+                                // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
+                                const double E = exp(fmin(phi / os.y, 700.0));
+                                const double ww = E / ((1.0 + E) * (1.0 + E));
+                                const double is = 1.0 / os.y;
+                                g7 = g_win * ww * phi * is * is;
+                                g_phi = -g_win * ww * is;
                             }
+                            const RecB& rb = s_rb[j];
+                            const int ib = edge == 2 ? 0 : edge + 1;
+                            const double ax = rb.qx[edge], ay = rb.qy[edge], bx = rb.qx[ib], by = rb.qy[ib];
+                            const double pxr = (double)(px - r.ox) + 0.5, pyr = (double)(py - r.oy) + 0.5;
+                            const double sl = rb.sl[edge], ul = rb.ul[edge], vl = rb.vl[edge];
+                            const double gax = g_phi * (sl * (pyr - by) + phi * ul);
+                            const double gay = g_phi * (sl * (bx - pxr) + phi * vl);
+                            const double gbx = g_phi * (sl * (ay - pyr) - phi * ul);
+                            const double gby = g_phi * (sl * (pxr - ax) - phi * vl);
+                            g0 = edge == 0 ? gax : (ib == 0 ? gbx : 0.0);
+                            g1 = edge == 0 ? gay : (ib == 0 ? gby : 0.0);
+                            g2 = edge == 1 ? gax : (ib == 1 ? gbx : 0.0);
+                            g3 = edge == 1 ? gay : (ib == 1 ? gby : 0.0);
+                            g4 = edge == 2 ? gax : (ib == 2 ? gbx : 0.0);
+                            g5 = edge == 2 ? gay : (ib == 2 ? gby : 0.0);
                         }
-                    }
-                }
-                if (__any_sync(0xffffffffu, act)) {
-#pragma unroll
-                    for (int k = 0; k < 12; k++) {
-                        double v = g[k];
-#pragma unroll
-                        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                        g[k] = v;
-                    }
-                    if (lane < 12) {
-                        double v = g[0];
-#pragma unroll
-                        for (int k = 1; k < 12; k++) v = (lane == (unsigned)k) ? g[k] : v;
-                        if (v != 0.0) atomicAdd(sgrad + (size_t)s_src[j] * SG_STRIDE + lane, v);
                     }
                 }
             }
+            if (__any_sync(0xffffffffu, act)) {
+                // butterfly reduce-scatter of 16 values (12 used) over the warp
+                const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0, h4 = (lane & 4) != 0, h2 = (lane & 2) != 0;
+                double a0 = h16 ? g8 : g0, b0 = h16 ? g0 : g8;
+                double a1 = h16 ? g9 : g1, b1 = h16 ? g1 : g9;
+                double a2 = h16 ? g10 : g2, b2 = h16 ? g2 : g10;
+                double a3 = h16 ? g11 : g3, b3 = h16 ? g3 : g11;
+                double a4 = h16 ? 0.0 : g4, b4 = h16 ? g4 : 0.0;
+                double a5 = h16 ? 0.0 : g5, b5 = h16 ? g5 : 0.0;
+                double a6 = h16 ? 0.0 : g6, b6 = h16 ? g6 : 0.0;
+                double a7 = h16 ? 0.0 : g7, b7 = h16 ? g7 : 0.0;
+                a0 = bfly_step(a0, b0, 16); a1 = bfly_step(a1, b1, 16); a2 = bfly_step(a2, b2, 16);
+                a3 = bfly_step(a3, b3, 16); a4 = bfly_step(a4, b4, 16); a5 = bfly_step(a5, b5, 16);
+                a6 = bfly_step(a6, b6, 16); a7 = bfly_step(a7, b7, 16);
+                // 8 values: local index i holds component (h16 ? 8 : 0) + i
+                double c0 = h8 ? a4 : a0, e0 = h8 ? a0 : a4;
+                double c1 = h8 ? a5 : a1, e1 = h8 ? a1 : a5;
+                double c2 = h8 ? a6 : a2, e2 = h8 ? a2 : a6;
+                double c3 = h8 ? a7 : a3, e3 = h8 ? a3 : a7;
+                c0 = bfly_step(c0, e0, 8); c1 = bfly_step(c1, e1, 8); c2 = bfly_step(c2, e2, 8); c3 = bfly_step(c3, e3, 8);
+                double f0 = h4 ? c2 : c0, h0 = h4 ? c0 : c2;
+                double f1 = h4 ? c3 : c1, h1 = h4 ? c1 : c3;
+                f0 = bfly_step(f0, h0, 4); f1 = bfly_step(f1, h1, 4);
+                double z = h2 ? f1 : f0, zs = h2 ? f0 : f1;
+                z = bfly_step(z, zs, 2);
+                z += __shfl_xor_sync(0xffffffffu, z, 1);
+                if ((lane & 1) == 0 && kred < 12) s_part[warp][j][kred] = (float)z;
+            }
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < nb * 12; c += blockDim.x) {
+            const int j = c / 12, k = c - j * 12;
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) v += (double)s_part[w][j][k];
+            if (v != 0.0) atomicAdd(sgrad + (size_t)s_src[j] * SG_STRIDE + k, v);
         }
     }
 }
