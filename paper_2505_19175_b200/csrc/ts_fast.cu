@@ -27,23 +27,6 @@ namespace ts {
 constexpr float T_MIN_F = 1e-4f;
 constexpr float ALPHA_CLAMP_F = 0.99f;
 
-__device__ __forceinline__ float fast_lg2(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ void red_max_shared(unsigned* p, unsigned v) {
-    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_add_shared(int* p, int v) {
-    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ float fast_ex2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 // ---------------------------------------------------------------------------
 // preprocess (fast records).  Only the quantities that decide the
 // reference's discrete outputs are computed with its exact fp64 arithmetic

@@ -93,6 +93,11 @@ void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup,
                            const double* t_final, const int* last_pos, const float* d_image, double* sgrad,
                            cudaStream_t st);
 
+// ts_blend.cu: render-only forward blend (dense pair evaluation)
+void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
+                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                        cudaStream_t st);
+
 // ts_sort.cu
 struct SortScratch {
     unsigned* hist;     // RADIX * max_blocks
