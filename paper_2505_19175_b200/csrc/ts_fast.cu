@@ -18,6 +18,7 @@
 // T<1e-4 or w>1/255 test whose operands lie within their error bound of the
 // threshold flags the pixel, which stops here and is recomputed exactly by
 // k_fixup_fwd.
+#include <algorithm>
 #include <type_traits>
 
 #include "ts_kernels.cuh"
@@ -48,7 +49,7 @@ __device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, co
 #pragma unroll
     for (int k = 0; k < 12; k++) {
         if (k < nv) {
-            const float4 v = __ldg(q + k);
+            const float4 v = q[k];
             const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int u = 0; u < 4; u++) {
@@ -76,7 +77,7 @@ __device__ __forceinline__ bool sh_finite<float>(const float* __restrict__ p) {
     float ss = 0.f;
 #pragma unroll
     for (int k = 0; k < 12; k++) {
-        const float4 v = __ldg(q + k);
+        const float4 v = q[k];
         ss = fmaf(v.x, 0.f, ss);
         ss = fmaf(v.y, 0.f, ss);
         ss = fmaf(v.z, 0.f, ss);
@@ -91,210 +92,203 @@ __device__ __forceinline__ bool sh_finite<double>(const double* __restrict__ p) 
     return ss == 0.0;
 }
 
+// One triangle of the fast preprocess: v = its 9 vertex coordinates, shp = its
+// 48 SH coefficients (shared-memory copy for fp32 parameters).
 template <typename T>
-__global__ void __launch_bounds__(128) k_preprocess_fast(Cam cam, Opts opt, const T* __restrict__ verts,
-                                                         const T* __restrict__ opacity,
-                                                         const T* __restrict__ sigma,
-                                                         const T* __restrict__ sh, long long n,
-                                                         FastPreOut out) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long long i, const double* v,
+                                        double o_raw, double sg, const T* shp, const FastPreOut& out,
+                                        unsigned long long& key, unsigned& tcount) {
     bool ok = false;
-    unsigned long long key = 0;
-    unsigned tcount = 0;
-    if (i < n) {
-        double v[9];
+    if (opt.validate) {
+        // x*0 is NaN for +-inf and NaN
+        double sv = 0.0;
 #pragma unroll
-        for (int k = 0; k < 9; k++) v[k] = (double)verts[i * 9 + k];
-        const double o_raw = (double)opacity[i];
-        const double sg = (double)sigma[i];
-        if (opt.validate) {
-            // x*0 is NaN for +-inf and NaN
-            double sv = 0.0;
+        for (int k = 0; k < 9; k++) sv = fma(v[k], 0.0, sv);
+        if (sv != 0.0) atomicMin(&out.ctr->err[0], i);
+        if (!isfinite(o_raw)) atomicMin(&out.ctr->err[1], i);
+        if (!isfinite(sg)) atomicMin(&out.ctr->err[2], i);
+    }
+    // ---- exact: _project_kernel, render.py:159-190 ----
+    double xc2[3], q[6];
+    bool z_ok = true;
 #pragma unroll
-            for (int k = 0; k < 9; k++) sv = fma(v[k], 0.0, sv);
-            if (sv != 0.0) atomicMin(&out.ctr->err[0], i);
-            if (!isfinite(o_raw)) atomicMin(&out.ctr->err[1], i);
-            if (!isfinite(sg)) atomicMin(&out.ctr->err[2], i);
+    for (int k = 0; k < 3; k++) {
+        double xk[3];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double t = TS_A(TS_M(v[k * 3 + 0], cam.R[a * 3 + 0]), TS_M(v[k * 3 + 1], cam.R[a * 3 + 1]));
+            t = TS_A(t, TS_M(v[k * 3 + 2], cam.R[a * 3 + 2]));
+            xk[a] = TS_A(t, cam.t[a]);
         }
-        // ---- exact: _project_kernel, render.py:159-190 ----
-        double xc2[3], q[6];
-        bool z_ok = true;
-#pragma unroll
-        for (int k = 0; k < 3; k++) {
-            double xk[3];
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-                double t = TS_A(TS_M(v[k * 3 + 0], cam.R[a * 3 + 0]), TS_M(v[k * 3 + 1], cam.R[a * 3 + 1]));
-                t = TS_A(t, TS_M(v[k * 3 + 2], cam.R[a * 3 + 2]));
-                xk[a] = TS_A(t, cam.t[a]);
-            }
-            if (xk[2] < 1e-12) z_ok = false;
-            xc2[k] = xk[2];
-            q[k * 2 + 0] = TS_A(TS_D(TS_M(cam.fx, xk[0]), xk[2]), cam.cx);
-            q[k * 2 + 1] = TS_A(TS_D(TS_M(cam.fy, xk[1]), xk[2]), cam.cy);
-        }
-        const double z = TS_D(TS_A(TS_A(xc2[0], xc2[1]), xc2[2]), 3.0);
-        if (z < cam.z_near) z_ok = false;
-        const double e1x = TS_S(q[2], q[0]), e1y = TS_S(q[3], q[1]);
-        const double e2x = TS_S(q[4], q[0]), e2y = TS_S(q[5], q[1]);
-        const double area = TS_M(fabs(TS_S(TS_M(e1x, e2y), TS_M(e1y, e2x))), 0.5);  // == /2.0
-        double d0x = TS_S(q[2], q[4]), d0y = TS_S(q[3], q[5]);
-        double d1x = TS_S(q[4], q[0]), d1y = TS_S(q[5], q[1]);
-        double d2x = TS_S(q[0], q[2]), d2y = TS_S(q[1], q[3]);
-        const double s0 = __dsqrt_rn(TS_A(TS_M(d0x, d0x), TS_M(d0y, d0y)));
-        const double s1 = __dsqrt_rn(TS_A(TS_M(d1x, d1x), TS_M(d1y, d1y)));
-        const double s2 = __dsqrt_rn(TS_A(TS_M(d2x, d2x), TS_M(d2y, d2y)));
-        const double perim = TS_A(TS_A(s0, s1), s2);
-        const double phis = TS_D(TS_M(-2.0, area), perim > 1e-300 ? perim : 1e-300);
-        if (out.area) out.area[i] = z_ok ? (float)area : 0.0f;
-        ok = z_ok && (area >= DEGENERATE_AREA) && (fabs(phis) >= DEGENERATE_INRADIUS);
-        short4 bb = make_short4(0, 0, 0, 0);
-        if (ok) {
-            const double o = opt.solid ? 1.0 : o_raw;
-            // ---- exact: incenter + tight bbox, render.py:216-250 ----
-            const double sx = TS_D(TS_A(TS_A(TS_M(s0, q[0]), TS_M(s1, q[2])), TS_M(s2, q[4])), perim);
-            const double sy = TS_D(TS_A(TS_A(TS_M(s0, q[1]), TS_M(s1, q[3])), TS_M(s2, q[5])), perim);
-            double f;
-            if (opt.mode == 0) {
-                if (o > opt.tau_cutoff) {
-                    const double ratio = TS_D(opt.tau_cutoff, o);
-                    // pow(x, 1.0) == x exactly (glibc and CUDA)
-                    f = TS_S(1.0, sg == 1.0 ? ratio : pow(ratio, TS_D(1.0, sg)));
-                } else {
-                    f = 0.0;
-                }
-            } else {
+        if (xk[2] < 1e-12) z_ok = false;
+        xc2[k] = xk[2];
+        q[k * 2 + 0] = TS_A(TS_D(TS_M(cam.fx, xk[0]), xk[2]), cam.cx);
+        q[k * 2 + 1] = TS_A(TS_D(TS_M(cam.fy, xk[1]), xk[2]), cam.cy);
+    }
+    const double z = TS_D(TS_A(TS_A(xc2[0], xc2[1]), xc2[2]), 3.0);
+    if (z < cam.z_near) z_ok = false;
+    const double e1x = TS_S(q[2], q[0]), e1y = TS_S(q[3], q[1]);
+    const double e2x = TS_S(q[4], q[0]), e2y = TS_S(q[5], q[1]);
+    const double area = TS_M(fabs(TS_S(TS_M(e1x, e2y), TS_M(e1y, e2x))), 0.5);  // == /2.0
+    double d0x = TS_S(q[2], q[4]), d0y = TS_S(q[3], q[5]);
+    double d1x = TS_S(q[4], q[0]), d1y = TS_S(q[5], q[1]);
+    double d2x = TS_S(q[0], q[2]), d2y = TS_S(q[1], q[3]);
+    const double s0 = __dsqrt_rn(TS_A(TS_M(d0x, d0x), TS_M(d0y, d0y)));
+    const double s1 = __dsqrt_rn(TS_A(TS_M(d1x, d1x), TS_M(d1y, d1y)));
+    const double s2 = __dsqrt_rn(TS_A(TS_M(d2x, d2x), TS_M(d2y, d2y)));
+    const double perim = TS_A(TS_A(s0, s1), s2);
+    const double phis = TS_D(TS_M(-2.0, area), perim > 1e-300 ? perim : 1e-300);
+    if (out.area) out.area[i] = z_ok ? (float)area : 0.0f;
+    ok = z_ok && (area >= DEGENERATE_AREA) && (fabs(phis) >= DEGENERATE_INRADIUS);
+    short4 bb = make_short4(0, 0, 0, 0);
+    if (ok) {
+        const double o = opt.solid ? 1.0 : o_raw;
+        // ---- exact: incenter + tight bbox, render.py:216-250 ----
+        const double sx = TS_D(TS_A(TS_A(TS_M(s0, q[0]), TS_M(s1, q[2])), TS_M(s2, q[4])), perim);
+        const double sy = TS_D(TS_A(TS_A(TS_M(s0, q[1]), TS_M(s1, q[3])), TS_M(s2, q[5])), perim);
+        double f;
+        if (opt.mode == 0) {
+            if (o > opt.tau_cutoff) {
                 const double ratio = TS_D(opt.tau_cutoff, o);
-                f = ratio < 1.0 ? TS_S(1.0, TS_D(TS_M(sg, log(TS_D(ratio, TS_S(1.0, ratio)))), fabs(phis))) : 0.0;
+                // pow(x, 1.0) == x exactly (glibc and CUDA)
+                f = TS_S(1.0, sg == 1.0 ? ratio : pow(ratio, TS_D(1.0, sg)));
+            } else {
+                f = 0.0;
             }
-            int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-            if (f > 0.0) {
-                double xmin = 1e300, ymin = 1e300, xmax = -1e300, ymax = -1e300;
+        } else {
+            const double ratio = TS_D(opt.tau_cutoff, o);
+            f = ratio < 1.0 ? TS_S(1.0, TS_D(TS_M(sg, log(TS_D(ratio, TS_S(1.0, ratio)))), fabs(phis))) : 0.0;
+        }
+        int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+        if (f > 0.0) {
+            double xmin = 1e300, ymin = 1e300, xmax = -1e300, ymax = -1e300;
 #pragma unroll
-                for (int k = 0; k < 3; k++) {
-                    const double pxk = TS_A(sx, TS_M(TS_S(q[k * 2], sx), f));
-                    const double pyk = TS_A(sy, TS_M(TS_S(q[k * 2 + 1], sy), f));
-                    xmin = pxk < xmin ? pxk : xmin;
-                    xmax = pxk > xmax ? pxk : xmax;
-                    ymin = pyk < ymin ? pyk : ymin;
-                    ymax = pyk > ymax ? pyk : ymax;
-                }
-                const long long W = cam.width, H = cam.height;
-                long long X0 = floor_i64(TS_S(xmin, 0.5)); X0 = X0 > 0 ? X0 : 0; X0 = X0 < W ? X0 : W;
-                long long X1 = floor_i64(TS_S(xmax, 0.5)) + 1; X1 = X1 > 0 ? X1 : 0; X1 = X1 < W ? X1 : W;
-                long long Y0 = floor_i64(TS_S(ymin, 0.5)); Y0 = Y0 > 0 ? Y0 : 0; Y0 = Y0 < H ? Y0 : H;
-                long long Y1 = floor_i64(TS_S(ymax, 0.5)) + 1; Y1 = Y1 > 0 ? Y1 : 0; Y1 = Y1 < H ? Y1 : H;
-                x0 = (int)X0; x1 = (int)(X1 > X0 ? X1 : X0); y0 = (int)Y0; y1 = (int)(Y1 > Y0 ? Y1 : Y0);
+            for (int k = 0; k < 3; k++) {
+                const double pxk = TS_A(sx, TS_M(TS_S(q[k * 2], sx), f));
+                const double pyk = TS_A(sy, TS_M(TS_S(q[k * 2 + 1], sy), f));
+                xmin = pxk < xmin ? pxk : xmin;
+                xmax = pxk > xmax ? pxk : xmax;
+                ymin = pyk < ymin ? pyk : ymin;
+                ymax = pyk > ymax ? pyk : ymax;
             }
-            bb = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
-            tcount = (unsigned)tiles_touched(x0, x1, y0, y1);
-            if (tcount) {
-                // ---- accurate (not bit-exact): edge functions, orientation, band ----
-                RecF r;
-                const double ccx = (q[0] + q[2] + q[4]) * (1.0 / 3.0), ccy = (q[1] + q[3] + q[5]) * (1.0 / 3.0);
-                const double inv = 1.0 / phis;
-                double dmax = 0.0;
-                int esign = 0;
-                float qf[6];
+            const long long W = cam.width, H = cam.height;
+            long long X0 = floor_i64(TS_S(xmin, 0.5)); X0 = X0 > 0 ? X0 : 0; X0 = X0 < W ? X0 : W;
+            long long X1 = floor_i64(TS_S(xmax, 0.5)) + 1; X1 = X1 > 0 ? X1 : 0; X1 = X1 < W ? X1 : W;
+            long long Y0 = floor_i64(TS_S(ymin, 0.5)); Y0 = Y0 > 0 ? Y0 : 0; Y0 = Y0 < H ? Y0 : H;
+            long long Y1 = floor_i64(TS_S(ymax, 0.5)) + 1; Y1 = Y1 > 0 ? Y1 : 0; Y1 = Y1 < H ? Y1 : H;
+            x0 = (int)X0; x1 = (int)(X1 > X0 ? X1 : X0); y0 = (int)Y0; y1 = (int)(Y1 > Y0 ? Y1 : Y0);
+        }
+        bb = make_short4((short)x0, (short)x1, (short)y0, (short)y1);
+        tcount = (unsigned)tiles_touched(x0, x1, y0, y1);
+        if (tcount) {
+            // ---- accurate (not bit-exact): edge functions, orientation, band ----
+            RecF r;
+            const double ccx = (q[0] + q[2] + q[4]) * (1.0 / 3.0), ccy = (q[1] + q[3] + q[5]) * (1.0 / 3.0);
+            const double inv = 1.0 / phis;
+            double dmax = 0.0;
+            int esign = 0;
+            float qf[6];
+#pragma unroll
+            for (int e = 0; e < 3; e++) {
+                const int bi = e == 2 ? 0 : e + 1;
+                const double ax = q[e * 2], ay = q[e * 2 + 1];
+                const double evx = q[bi * 2] - ax, evy = q[bi * 2 + 1] - ay;
+                const double il = rsqrt(evx * evx + evy * evy);
+                double nx = evy * il, ny = -evx * il;
+                if (nx * (ccx - ax) + ny * (ccy - ay) > 0) {
+                    nx = -nx;
+                    ny = -ny;
+                    esign |= 1 << e;
+                }
+                const double d = -(nx * ax + ny * ay);
+                r.a[e * 3 + 0] = nx * inv;
+                r.a[e * 3 + 1] = ny * inv;
+                r.a[e * 3 + 2] = d * inv;
+                dmax = fmax(dmax, fabs(d));
+            }
+            const double mag = (fabs(q[0]) + fabs(q[1]) + fabs(q[2]) + fabs(q[3]) + fabs(q[4]) + fabs(q[5]) +
+                                4.0 * (cam.width + cam.height) + dmax) * fabs(inv);
+            const double delta = 1e-13 * mag + 1e-300;
+            double rstar;
+            if (opt.mode == 0) {
+                rstar = o > ALPHA_MIN ? (sg == 1.0 ? ALPHA_MIN / o : pow(ALPHA_MIN / o, 1.0 / sg)) : 1e30;
+                if (rstar > 1.0) rstar = 1e30;
+                r.f0 = (float)sg;
+                r.f1 = log2f((float)o);
+            } else {
+                const double qq = 255.0 * o - 1.0;
+                rstar = qq > 0.0 ? sg * log(qq) / phis : 1e30;
+                r.f0 = (float)(phis * 1.4426950408889634 / sg);
+                r.f1 = (float)o;
+            }
+            r.r_lo = rstar - delta - fabs(rstar) * 1e-12;
+            r.r_hi = rstar + delta + fabs(rstar) * 1e-12;
+            r.phis = phis;
+            // view-dependent SH colour (render.py:292-302) in fp32: only the value is used here
+            float u0 = (float)((v[0] + v[3] + v[6]) * (1.0 / 3.0) - cam.cc[0]);
+            float u1 = (float)((v[1] + v[4] + v[7]) * (1.0 / 3.0) - cam.cc[1]);
+            float u2 = (float)((v[2] + v[5] + v[8]) * (1.0 / 3.0) - cam.cc[2]);
+            const float iu = rsqrtf(fmaxf(u0 * u0 + u1 * u1 + u2 * u2, 1e-24f));
+            u0 *= iu; u1 *= iu; u2 *= iu;
+            const float xx = u0 * u0, yy = u1 * u1, zz = u2 * u2;
+            float bs[16];
+            bs[0] = 0.28209479177387814f;
+            bs[1] = -0.4886025119029199f * u1;
+            bs[2] = 0.4886025119029199f * u2;
+            bs[3] = -0.4886025119029199f * u0;
+            bs[4] = 1.0925484305920792f * u0 * u1;
+            bs[5] = -1.0925484305920792f * u1 * u2;
+            bs[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+            bs[7] = -1.0925484305920792f * u0 * u2;
+            bs[8] = 0.5462742152960396f * (xx - yy);
+            bs[9] = -0.5900435899266435f * u1 * (3.f * xx - yy);
+            bs[10] = 2.890611442640554f * u0 * u1 * u2;
+            bs[11] = -0.4570457994644658f * u1 * (4.f * zz - xx - yy);
+            bs[12] = 0.3731763325901154f * u2 * (2.f * zz - 3.f * xx - 3.f * yy);
+            bs[13] = -0.4570457994644658f * u0 * (4.f * zz - xx - yy);
+            bs[14] = 1.445305721320277f * u2 * (xx - yy);
+            bs[15] = -0.5900435899266435f * u0 * (xx - 3.f * yy);
+            float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
+            sh_colour<T>(shp, bs, opt.ncoef, c0, c1, c2);
+            r.rgb[0] = fminf(fmaxf(c0, 0.f), 1.f);
+            r.rgb[1] = fminf(fmaxf(c1, 0.f), 1.f);
+            r.rgb[2] = fminf(fmaxf(c2, 0.f), 1.f);
+            const int ox = (x0 + x1) >> 1, oy = (y0 + y1) >> 1;
+            r.x0 = (short)x0; r.x1 = (short)x1; r.y0 = (short)y0; r.y1 = (short)y1;
+            r.ox = (short)ox; r.oy = (short)oy;
+            out.rec[i] = r;
+            if (out.recb) {
+                RecB rb;
 #pragma unroll
                 for (int e = 0; e < 3; e++) {
+                    rb.qx[e] = q[e * 2] - ox;
+                    rb.qy[e] = q[e * 2 + 1] - oy;
                     const int bi = e == 2 ? 0 : e + 1;
-                    const double ax = q[e * 2], ay = q[e * 2 + 1];
-                    const double evx = q[bi * 2] - ax, evy = q[bi * 2 + 1] - ay;
-                    const double il = rsqrt(evx * evx + evy * evy);
-                    double nx = evy * il, ny = -evx * il;
-                    if (nx * (ccx - ax) + ny * (ccy - ay) > 0) {
-                        nx = -nx;
-                        ny = -ny;
-                        esign |= 1 << e;
-                    }
-                    const double d = -(nx * ax + ny * ay);
-                    r.a[e * 3 + 0] = nx * inv;
-                    r.a[e * 3 + 1] = ny * inv;
-                    r.a[e * 3 + 2] = d * inv;
-                    dmax = fmax(dmax, fabs(d));
+                    const double ex = q[bi * 2] - q[e * 2], ey = q[bi * 2 + 1] - q[e * 2 + 1];
+                    const double il = 1.0 / sqrt(ex * ex + ey * ey);
+                    rb.sl[e] = ((esign >> e) & 1) ? -il : il;
+                    rb.ul[e] = ex * il * il;
+                    rb.vl[e] = ey * il * il;
                 }
-                const double mag = (fabs(q[0]) + fabs(q[1]) + fabs(q[2]) + fabs(q[3]) + fabs(q[4]) + fabs(q[5]) +
-                                    4.0 * (cam.width + cam.height) + dmax) * fabs(inv);
-                const double delta = 1e-13 * mag + 1e-300;
-                double rstar;
-                if (opt.mode == 0) {
-                    rstar = o > ALPHA_MIN ? (sg == 1.0 ? ALPHA_MIN / o : pow(ALPHA_MIN / o, 1.0 / sg)) : 1e30;
-                    if (rstar > 1.0) rstar = 1e30;
-                    r.f0 = (float)sg;
-                    r.f1 = log2f((float)o);
-                } else {
-                    const double qq = 255.0 * o - 1.0;
-                    rstar = qq > 0.0 ? sg * log(qq) / phis : 1e30;
-                    r.f0 = (float)(phis * 1.4426950408889634 / sg);
-                    r.f1 = (float)o;
-                }
-                r.r_lo = rstar - delta - fabs(rstar) * 1e-12;
-                r.r_hi = rstar + delta + fabs(rstar) * 1e-12;
-                r.phis = phis;
-                // view-dependent SH colour (render.py:292-302) in fp32: only the value is used here
-                float u0 = (float)((v[0] + v[3] + v[6]) * (1.0 / 3.0) - cam.cc[0]);
-                float u1 = (float)((v[1] + v[4] + v[7]) * (1.0 / 3.0) - cam.cc[1]);
-                float u2 = (float)((v[2] + v[5] + v[8]) * (1.0 / 3.0) - cam.cc[2]);
-                const float iu = rsqrtf(fmaxf(u0 * u0 + u1 * u1 + u2 * u2, 1e-24f));
-                u0 *= iu; u1 *= iu; u2 *= iu;
-                const float xx = u0 * u0, yy = u1 * u1, zz = u2 * u2;
-                float bs[16];
-                bs[0] = 0.28209479177387814f;
-                bs[1] = -0.4886025119029199f * u1;
-                bs[2] = 0.4886025119029199f * u2;
-                bs[3] = -0.4886025119029199f * u0;
-                bs[4] = 1.0925484305920792f * u0 * u1;
-                bs[5] = -1.0925484305920792f * u1 * u2;
-                bs[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
-                bs[7] = -1.0925484305920792f * u0 * u2;
-                bs[8] = 0.5462742152960396f * (xx - yy);
-                bs[9] = -0.5900435899266435f * u1 * (3.f * xx - yy);
-                bs[10] = 2.890611442640554f * u0 * u1 * u2;
-                bs[11] = -0.4570457994644658f * u1 * (4.f * zz - xx - yy);
-                bs[12] = 0.3731763325901154f * u2 * (2.f * zz - 3.f * xx - 3.f * yy);
-                bs[13] = -0.4570457994644658f * u0 * (4.f * zz - xx - yy);
-                bs[14] = 1.445305721320277f * u2 * (xx - yy);
-                bs[15] = -0.5900435899266435f * u0 * (xx - 3.f * yy);
-                float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
-                sh_colour<T>(sh + i * 48, bs, opt.ncoef, c0, c1, c2);
-                r.rgb[0] = fminf(fmaxf(c0, 0.f), 1.f);
-                r.rgb[1] = fminf(fmaxf(c1, 0.f), 1.f);
-                r.rgb[2] = fminf(fmaxf(c2, 0.f), 1.f);
-                const int ox = (x0 + x1) >> 1, oy = (y0 + y1) >> 1;
-                r.x0 = (short)x0; r.x1 = (short)x1; r.y0 = (short)y0; r.y1 = (short)y1;
-                r.ox = (short)ox; r.oy = (short)oy;
-                out.rec[i] = r;
-                if (out.recb) {
-                    RecB rb;
-#pragma unroll
-                    for (int e = 0; e < 3; e++) {
-                        rb.qx[e] = q[e * 2] - ox;
-                        rb.qy[e] = q[e * 2 + 1] - oy;
-                        const int bi = e == 2 ? 0 : e + 1;
-                        const double ex = q[bi * 2] - q[e * 2], ey = q[bi * 2 + 1] - q[e * 2 + 1];
-                        const double il = 1.0 / sqrt(ex * ex + ey * ey);
-                        rb.sl[e] = ((esign >> e) & 1) ? -il : il;
-                        rb.ul[e] = ex * il * il;
-                        rb.vl[e] = ey * il * il;
-                    }
-                    rb.esign = esign;
-                    rb.pad = 0;
-                    out.recb[i] = rb;
-                }
-                (void)qf;
+                rb.esign = esign;
+                rb.pad = 0;
+                out.recb[i] = rb;
             }
-            key = (unsigned long long)__double_as_longlong(z);
+            (void)qf;
         }
-        if (opt.validate && !sh_finite<T>(sh + i * 48)) atomicMin(&out.ctr->err[3], i);
-        out.bbox[i] = bb;
-        out.flag[i] = ok ? 1u : 0u;
-        out.tcount[i] = tcount;
-        out.key[i] = key;
+        key = (unsigned long long)__double_as_longlong(z);
     }
-    unsigned long long kmin = ok ? key : ~0ull, kmax = ok ? key : 0ull;
-    unsigned cnt = ok ? 1u : 0u;
-    unsigned long long tc = tcount;
+    if (opt.validate && !sh_finite<T>(shp)) atomicMin(&out.ctr->err[3], i);
+    out.bbox[i] = bb;
+    out.flag[i] = ok ? 1u : 0u;
+    out.tcount[i] = tcount;
+    out.key[i] = key;
+    return ok;
+}
+
+// Warp-reduce the per-triangle counters and publish them (one atomic set per warp).
+__device__ __forceinline__ void pre_publish(Counters* ctr, unsigned long long kmin, unsigned long long kmax,
+                                            unsigned cnt, unsigned long long tc) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, off);
@@ -305,28 +299,134 @@ __global__ void __launch_bounds__(128) k_preprocess_fast(Cam cam, Opts opt, cons
         tc += __shfl_xor_sync(0xffffffffu, tc, off);
     }
     if ((threadIdx.x & 31) == 0 && cnt) {
-        atomicMin(&out.ctr->key_min, kmin);
-        atomicMax(&out.ctr->key_max, kmax);
-        atomicAdd(&out.ctr->m, (unsigned long long)cnt);
-        atomicAdd(&out.ctr->e, tc);
+        atomicMin(&ctr->key_min, kmin);
+        atomicMax(&ctr->key_max, kmax);
+        atomicAdd(&ctr->m, (unsigned long long)cnt);
+        atomicAdd(&ctr->e, tc);
     }
+}
+
+// fp64 parameters (drop-in parity path): one thread per triangle, direct loads.
+__global__ void __launch_bounds__(128) k_preprocess_fast64(Cam cam, Opts opt, const double* __restrict__ verts,
+                                                           const double* __restrict__ opacity,
+                                                           const double* __restrict__ sigma,
+                                                           const double* __restrict__ sh, long long n,
+                                                           FastPreOut out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long key = 0;
+    unsigned tcount = 0;
+    bool ok = false;
+    if (i < n) {
+        double v[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) v[k] = verts[i * 9 + k];
+        ok = pre_tri<double>(cam, opt, i, v, opacity[i], sigma[i], sh + i * 48, out, key, tcount);
+    }
+    pre_publish(out.ctr, ok ? key : ~0ull, ok ? key : 0ull, ok ? 1u : 0u, tcount);
+}
+
+// fp32 parameters: persistent CTAs walk blocks of 128 triangles; the next
+// block's vertices, opacity, sigma and SH rows are copied to shared memory
+// (cp.async, double-buffered, SH rows padded to 13 float4 so per-thread row
+// reads are bank-conflict free) while the current block is computed.
+constexpr int PRE_BLK = 128;
+struct PreStage {
+    float4 sh[PRE_BLK * 13];
+    float v[PRE_BLK * 9];
+    float o[PRE_BLK], sg[PRE_BLK];
+};
+
+__global__ void __launch_bounds__(PRE_BLK, 3) k_preprocess_fast32(Cam cam, Opts opt, const float* __restrict__ verts,
+                                                               const float* __restrict__ opacity,
+                                                               const float* __restrict__ sigma,
+                                                               const float* __restrict__ sh, long long n,
+                                                               FastPreOut out) {
+    extern __shared__ __align__(16) unsigned char s_pre[];
+    PreStage* stage = reinterpret_cast<PreStage*>(s_pre);  // [2]
+    const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
+    const int tid = threadIdx.x;
+    auto issue = [&](long long blk, int buf) {
+        const long long i0 = blk * PRE_BLK;
+        const int nt = (int)min((long long)PRE_BLK, n - i0);
+        PreStage& S = stage[buf];
+        const float4* g = reinterpret_cast<const float4*>(sh + i0 * 48);
+        for (int c = tid; c < nt * 12; c += PRE_BLK) {
+            const int tri = c / 12;
+            cp_async16(&S.sh[tri * 13 + (c - tri * 12)], g + c);
+        }
+        const float* gv = verts + i0 * 9;
+        if (nt == PRE_BLK) {
+            for (int c = tid; c < PRE_BLK * 9 / 4; c += PRE_BLK)
+                cp_async16(reinterpret_cast<float4*>(S.v) + c, reinterpret_cast<const float4*>(gv) + c);
+            if (tid < PRE_BLK / 4) {
+                cp_async16(reinterpret_cast<float4*>(S.o) + tid, reinterpret_cast<const float4*>(opacity + i0) + tid);
+                cp_async16(reinterpret_cast<float4*>(S.sg) + tid, reinterpret_cast<const float4*>(sigma + i0) + tid);
+            }
+        } else {
+            for (int c = tid; c < nt * 9; c += PRE_BLK) cp_async4(S.v + c, gv + c);
+            if (tid < nt) {
+                cp_async4(S.o + tid, opacity + i0 + tid);
+                cp_async4(S.sg + tid, sigma + i0 + tid);
+            }
+        }
+    };
+    unsigned long long kmin = ~0ull, kmax = 0ull, tc = 0;
+    unsigned cnt = 0;
+    long long blk = blockIdx.x;
+    if (blk < nblk) issue(blk, 0);
+    cp_async_commit();
+    for (int it = 0; blk < nblk; blk += gridDim.x, it++) {
+        const int buf = it & 1;
+        if (blk + gridDim.x < nblk) issue(blk + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait_group1();
+        __syncthreads();
+        const long long i = blk * PRE_BLK + tid;
+        if (i < n) {
+            const PreStage& S = stage[buf];
+            double v[9];
+#pragma unroll
+            for (int k = 0; k < 9; k++) v[k] = (double)S.v[tid * 9 + k];
+            unsigned long long key = 0;
+            unsigned tcount = 0;
+            const bool ok = pre_tri<float>(cam, opt, i, v, (double)S.o[tid], (double)S.sg[tid],
+                                           reinterpret_cast<const float*>(&S.sh[tid * 13]), out, key, tcount);
+            if (ok) {
+                kmin = key < kmin ? key : kmin;
+                kmax = key > kmax ? key : kmax;
+                cnt++;
+            }
+            tc += tcount;
+        }
+        __syncthreads();
+    }
+    cp_async_wait_all();
+    pre_publish(out.ctr, kmin, kmax, cnt, tc);
 }
 
 void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
                             const FastPreOut& out, cudaStream_t st) {
     long long n = soup.n;
     if (n <= 0) return;
-    unsigned grid = (unsigned)((n + 127) / 128);
-    if (dtype == 1)
-        k_preprocess_fast<double><<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices,
-                                                        (const double*)soup.opacity,
-                                                        (const double*)soup.sigma,
-                                                        (const double*)soup.sh, n, out);
-    else
-        k_preprocess_fast<float><<<grid, 128, 0, st>>>(cam, opt, (const float*)soup.vertices,
-                                                       (const float*)soup.opacity,
-                                                       (const float*)soup.sigma,
-                                                       (const float*)soup.sh, n, out);
+    if (dtype == 1) {
+        unsigned grid = (unsigned)((n + 127) / 128);
+        k_preprocess_fast64<<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices, (const double*)soup.opacity,
+                                                  (const double*)soup.sigma, (const double*)soup.sh, n, out);
+    } else {
+        static int sms = 0;
+        static const int smem = 2 * (int)sizeof(PreStage);
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(k_preprocess_fast32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        }
+        const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
+        const long long grid = std::min<long long>(nblk, (long long)sms * 3);
+        k_preprocess_fast32<<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, (const float*)soup.vertices,
+                                                                  (const float*)soup.opacity, (const float*)soup.sigma,
+                                                                  (const float*)soup.sh, n, out);
+    }
 }
 
 // ---------------------------------------------------------------------------
