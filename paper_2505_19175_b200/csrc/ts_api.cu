@@ -425,6 +425,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
                         c->flags, c->d_ctr};
         stage_begin(c, TS_STAGE_BLEND, st);
         static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
+        // training forwards composite in fp64 (exact T_final for the backward recursion)
         if (opt->keep_backward || legacy)
             launch_blend_fast(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
                               c->bbox, c->tile_start, c->ent_src, bo, st);
@@ -475,9 +476,14 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
         double* sg = (double*)c->sg64.p;
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
         if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
-        launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
-                              (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
-                              d_image, sg, st);
+        static const bool bwd_legacy = getenv("TS_BWD_LEGACY") != nullptr;
+        if (bwd_legacy)
+            launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
+                                  (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
+                                  d_image, sg, st);
+        else
+            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, c->tile_start,
+                                   c->ent_src, c->t_final, c->last_pos, d_image, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
         launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);

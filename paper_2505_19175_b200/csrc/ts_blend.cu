@@ -36,16 +36,6 @@ constexpr float ALPHA_CLAMP_F = 0.99f;
 // f0, f1, rgb, bbox); source ids in a ring of 4*DB.  While batch [b, b+nb) is
 // processed, the records of [b+nb, b+nb+DB) and the ids up to b+3*DB are in
 // flight (cp.async).
-struct __align__(16) EvalRec {
-    double a[9];
-    double phis, r_lo, r_hi;
-};
-static_assert(sizeof(EvalRec) == 96, "EvalRec layout");
-struct __align__(16) TailRec {
-    float f0, f1, rgb[3];
-    short x0, x1, y0, y1, ox, oy;
-};
-static_assert(sizeof(TailRec) == 32, "TailRec layout");
 
 template <int DB, int PCAP>
 struct DenseSmem {
@@ -58,6 +48,8 @@ struct DenseSmem {
     float4 col[DB];                // rgb, f0
     float f1[DB];
     int S[DB + 1];                 // first pair of entry j
+    int H[DB + 1];                 // first row unit of entry j (row-interval evaluation)
+    double inva[DB][3];            // 1 / a_e0 per edge (0 if a_e0 == 0)
     unsigned geo[DB];              // cx0 | cy0<<4 | w<<8 | magic<<16
     int2 kb[DB];                   // pair of pixel (lx, ly) = x + ly * y + lx
     unsigned maxw[DB];
@@ -71,7 +63,7 @@ struct DenseSmem {
     int nb;
 };
 
-template <int DB, int PCAP, bool SORT>
+template <int DB, int PCAP, bool SORT, bool ROWS>
 __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                      const int* __restrict__ tile_start,
                                                      const unsigned* __restrict__ ent_src,
@@ -164,6 +156,30 @@ __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const Re
                 incl[hf] = a + carry;
                 carry = __shfl_sync(0xffffffffu, incl[hf], 31);
             }
+            if constexpr (ROWS) {
+                int hcarry = 0;
+#pragma unroll
+                for (int hf = 0; hf < NW; hf++) {
+                    const int j = (int)lane + 32 * hf;
+                    int a = h[hf];
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, a, off);
+                        if ((int)lane >= off) a += y;
+                    }
+                    sm.H[j + 1] = a + hcarry;
+                    hcarry += __shfl_sync(0xffffffffu, a, 31);
+                    if (valid[hf]) {
+                        const EvalRec& r = sm.ev[(b + j) & (RR - 1)];
+#pragma unroll
+                        for (int q = 0; q < 3; q++) {
+                            const double ae = r.a[3 * q];
+                            sm.inva[j][q] = ae != 0.0 ? 1.0 / ae : 0.0;
+                        }
+                    }
+                }
+                if (lane == 0) sm.H[0] = 0;
+            }
             // batch = longest prefix of entries whose pairs fit in PCAP (>= 1 entry)
             int n = 0;
             bool full = true;
@@ -196,6 +212,69 @@ __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const Re
             rhi = max(rhi, nrhi);
             cp_async_commit();
         }
+        if constexpr (ROWS) {
+            // ---- 2. evaluate by row units (entry j, row ly): the pixels of the row with
+            //         r >= r_lo form an interval (intersection of three half-planes),
+            //         solved in fp64 and widened by a margin far above its rounding
+            //         error; only the pixels inside are evaluated, with the exact
+            //         per-pixel formula, so every decision matches the pair evaluation ----
+            const int U = sm.H[nb];
+            for (int u = tid; u < U; u += 256) {
+                int j = 0;
+#pragma unroll
+                for (int step = DB / 2; step > 0; step >>= 1)
+                    if (j + step < nb && sm.H[j + step] <= u) j += step;
+                const unsigned g = sm.geo[j];
+                const int w = (g >> 8) & 31, cx0 = g & 15, cy0 = (g >> 4) & 15;
+                const int ly = cy0 + (u - sm.H[j]);
+                const EvalRec& r = sm.ev[(b + j) & (RR - 1)];
+                const double pcy = sm.yc[ly];
+                const double rlo = r.r_lo;
+                const double D0 = fma(r.a[1], pcy, r.a[2]);
+                const double D1 = fma(r.a[4], pcy, r.a[5]);
+                const double D2 = fma(r.a[7], pcy, r.a[8]);
+                const double a0 = r.a[0], a3 = r.a[3], a6 = r.a[6];
+                int xl = cx0, xr = cx0 + w - 1;
+                const double xoff = (double)X0 + 0.5;
+                auto clip = [&](double ae, double De, double inv) {
+                    if (ae == 0.0) {
+                        if (De < rlo) xr = -1;  // l_e == D_e exactly
+                        return;
+                    }
+                    const double t = (rlo - De) * inv - xoff;  // l_e >= r_lo  <=>  x >= t (ae > 0)
+                    const double eps = 1e-9 + 1e-12 * fabs(t + xoff);
+                    if (ae > 0.0) {
+                        const double tc = fmin(fmax(t - eps, -2.0), 18.0);  // NaN -> no bound
+                        xl = max(xl, (int)ceil(tc));
+                    } else {
+                        const double tc = fmax(fmin(t + eps, 18.0), -2.0);
+                        xr = min(xr, (int)floor(tc));
+                    }
+                };
+                clip(a0, D0, sm.inva[j][0]);
+                clip(a3, D1, sm.inva[j][1]);
+                clip(a6, D2, sm.inva[j][2]);
+                if (xl <= xr) {
+                    const int2 kbj = sm.kb[j];
+                    const double rhi = r.r_hi;
+                    const unsigned bit = 1u << (j & 31);
+                    unsigned* mrow = &sm.mask[j >> 5][ly * TILE];
+                    float* rrow = &sm.r[kbj.x + ly * kbj.y];
+                    for (int x = xl; x <= xr; x++) {
+                        const double pcx = sm.xc[x];
+                        const double l0 = fma(a0, pcx, D0);
+                        const double l1 = fma(a3, pcx, D1);
+                        const double l2 = fma(a6, pcx, D2);
+                        const double m01 = l0 < l1 ? l0 : l1;
+                        const double rr = m01 < l2 ? m01 : l2;
+                        if (rr >= rlo) {
+                            rrow[x] = rr > rhi ? (float)rr : __int_as_float(0x7fc00000);
+                            atomicOr(&mrow[x], bit);
+                        }
+                    }
+                }
+            }
+        } else {
         // ---- 2. evaluate: warp w takes a contiguous range of pairs, 32 consecutive
         //         pairs per step (lane-uniform control flow, broadcast record loads) ----
         {
@@ -232,6 +311,7 @@ __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const Re
                     }
                 }
             }
+        }
         }
         __syncthreads();
         // ---- 3. order live pixels by pass count (descending) so the lanes of a warp
@@ -375,17 +455,17 @@ __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const Re
     }
 }
 
-template <int DB, int PCAP, bool SORT>
+template <int DB, int PCAP, bool SORT, bool ROWS>
 static void launch_dense(const Cam& cam, const Opts& opt, const RecF* rec, const int* tile_start,
                          const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st) {
     const int dyn = (int)sizeof(DenseSmem<DB, PCAP>);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_blend_dense<DB, PCAP, SORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(k_blend_dense<DB, PCAP, SORT, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         attr = true;
     }
     const int ntiles = cam.ntx * cam.nty;
-    k_blend_dense<DB, PCAP, SORT><<<ntiles, 256, dyn, st>>>(cam, opt, rec, tile_start, ent_src, out);
+    k_blend_dense<DB, PCAP, SORT, ROWS><<<ntiles, 256, dyn, st>>>(cam, opt, rec, tile_start, ent_src, out);
 }
 
 void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
@@ -397,9 +477,9 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const 
         return v ? atoi(v) : 0;
     }();
     if (variant == 1)
-        launch_dense<64, 4096, true>(cam, opt, rec, tile_start, ent_src, out, st);
+        launch_dense<64, 4096, false, true>(cam, opt, rec, tile_start, ent_src, out, st);
     else
-        launch_dense<64, 4096, false>(cam, opt, rec, tile_start, ent_src, out, st);
+        launch_dense<64, 4096, false, false>(cam, opt, rec, tile_start, ent_src, out, st);
 }
 
 }  // namespace ts

@@ -73,10 +73,22 @@ static_assert(sizeof(RecF) == 128, "RecF layout");
 struct __align__(16) RecB {
     double qx[3], qy[3];
     double sl[3], ul[3], vl[3];
-    int esign;
-    int pad;
+    float opa, sig;  // opacity (1 for solid soups) and sigma, as float
 };
 static_assert(sizeof(RecB) == 128, "RecB layout");
+
+// Shared-memory images of a RecF for the dense blend kernels: the evaluation
+// part (first 96 B) and the tail (last 32 B), copied with 16-byte cp.async.
+struct __align__(16) EvalRec {
+    double a[9];
+    double phis, r_lo, r_hi;
+};
+static_assert(sizeof(EvalRec) == 96, "EvalRec layout");
+struct __align__(16) TailRec {
+    float f0, f1, rgb[3];
+    short x0, x1, y0, y1, ox, oy;
+};
+static_assert(sizeof(TailRec) == 32, "TailRec layout");
 
 // Screen-space gradient accumulator per source triangle (backward), fp64.
 // gq[6] (q0x,q0y,q1x,q1y,q2x,q2y), go, gsig, grgb[3], gphis, gz, pad

@@ -270,8 +270,8 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
                     rb.ul[e] = ex * il * il;
                     rb.vl[e] = ey * il * il;
                 }
-                rb.esign = esign;
-                rb.pad = 0;
+                rb.opa = (float)o;
+                rb.sig = (float)sg;
                 out.recb[i] = rb;
             }
             (void)qf;

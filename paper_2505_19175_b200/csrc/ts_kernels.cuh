@@ -98,6 +98,11 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const 
                         const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                         cudaStream_t st);
 
+// ts_bwd.cu: dense backward blend
+void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
+                            const int* tile_start, const unsigned* ent_src, const double* t_final,
+                            const int* last_pos, const float* d_image, double* sgrad, cudaStream_t st);
+
 // ts_sort.cu
 struct SortScratch {
     unsigned* hist;     // RADIX * max_blocks
