@@ -486,7 +486,8 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
                                    c->ent_src, c->t_final, c->last_pos, d_image, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
-        launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+        if (!launch_chain_bwd_fast(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st))
+            launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
         stage_end(c, TS_STAGE_CHAIN_BWD, st);
         c->sgrad_kind = 1;
     } else {

@@ -1,0 +1,270 @@
+// ts_chain.cu -- screen-space gradients -> the 59 parameter gradients of every
+// triangle (backward.py:59-90 _phis_q_grad, backward.py:158-210 projection
+// Jacobian and SH colour path, sh.py:55-100 basis gradient), fp32 parameters.
+//
+// CTA = 128 triangles, thread = triangle.  The CTA's SH block, vertices and
+// screen-space gradient rows are copied to shared memory with coalesced
+// cp.async (rows padded against bank conflicts); d_sh is written in place over
+// the thread's own SH row and every output block leaves with coalesced 16-byte
+// stores (read-add-write when accumulating).  Geometry and the view-direction
+// chain are fp64; the 48 SH gradients are basis * dL/draw (fp64, stored fp32).
+#include "ts_kernels.cuh"
+
+namespace ts {
+
+namespace {
+constexpr int CB = 128;     // triangles per CTA
+constexpr int SGW = 18;     // doubles per staged gradient row (16 used; 144 B keeps 16-B chunks aligned)
+
+struct ChainStage {
+    float4 sh[CB * 13];     // SH rows (12 float4, padded to 13); overwritten with d_sh
+    float v[CB * 9];        // vertices; overwritten with d_vertices
+    double sg[CB * SGW];    // screen-space gradient rows
+    float os[2][CB];        // d_opacity, d_sigma
+};
+
+// sum_c s_c * grad(Y_c)(x, y, z) for the 16 real SH basis functions (sh.py:55-100)
+__device__ __forceinline__ void sh_weighted_grad(double x, double y, double z, const double* s, double* g) {
+    const double C1 = 0.4886025119029199;
+    const double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
+                 C23 = -1.0925484305920792, C24 = 0.5462742152960396;
+    const double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
+                 C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
+                 C36 = -0.5900435899266435;
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    gy += s[1] * -C1;
+    gz += s[2] * C1;
+    gx += s[3] * -C1;
+    gx += s[4] * (C20 * y);
+    gy += s[4] * (C20 * x);
+    gy += s[5] * (C21 * z);
+    gz += s[5] * (C21 * y);
+    gx += s[6] * (C22 * (-2.0 * x));
+    gy += s[6] * (C22 * (-2.0 * y));
+    gz += s[6] * (C22 * 4.0 * z);
+    gx += s[7] * (C23 * z);
+    gz += s[7] * (C23 * x);
+    gx += s[8] * (C24 * 2.0 * x);
+    gy += s[8] * (C24 * (-2.0 * y));
+    gx += s[9] * (C30 * 6.0 * x * y);
+    gy += s[9] * (C30 * (3.0 * x * x - 3.0 * y * y));
+    gx += s[10] * (C31 * y * z);
+    gy += s[10] * (C31 * x * z);
+    gz += s[10] * (C31 * x * y);
+    gx += s[11] * (C32 * (-2.0 * x * y));
+    gy += s[11] * (C32 * (4.0 * z * z - x * x - 3.0 * y * y));
+    gz += s[11] * (C32 * 8.0 * y * z);
+    gx += s[12] * (C33 * (-6.0 * x * z));
+    gy += s[12] * (C33 * (-6.0 * y * z));
+    gz += s[12] * (C33 * (6.0 * z * z - 3.0 * x * x - 3.0 * y * y));
+    gx += s[13] * (C34 * (4.0 * z * z - 3.0 * x * x - y * y));
+    gy += s[13] * (C34 * (-2.0 * x * y));
+    gz += s[13] * (C34 * 8.0 * x * z);
+    gx += s[14] * (C35 * 2.0 * x * z);
+    gy += s[14] * (C35 * (-2.0 * y * z));
+    gz += s[14] * (C35 * (x * x - y * y));
+    gx += s[15] * (C36 * (3.0 * x * x - 3.0 * y * y));
+    gy += s[15] * (C36 * (-6.0 * x * y));
+    g[0] = gx;
+    g[1] = gy;
+    g[2] = gz;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(CB, 4) k_chain_bwd32(Cam cam, Opts opt, const float* __restrict__ verts,
+                                                       const float* __restrict__ sh,
+                                                       const unsigned* __restrict__ flag,
+                                                       const double* __restrict__ sgrad, long long n,
+                                                       ts_grads grads, int accumulate) {
+    extern __shared__ __align__(16) unsigned char s_chain[];
+    ChainStage& S = *reinterpret_cast<ChainStage*>(s_chain);
+    const int tid = threadIdx.x;
+    const long long i0 = (long long)blockIdx.x * CB;
+    const int nt = (int)min((long long)CB, n - i0);
+    // ---- stage (coalesced cp.async) ----
+    {
+        const float4* g = reinterpret_cast<const float4*>(sh + i0 * 48);
+        for (int c = tid; c < nt * 12; c += CB) {
+            const int tri = c / 12;
+            cp_async16(&S.sh[tri * 13 + (c - tri * 12)], g + c);
+        }
+        const float* gv = verts + i0 * 9;
+        if (nt == CB) {
+            for (int c = tid; c < CB * 9 / 4; c += CB)
+                cp_async16(reinterpret_cast<float4*>(S.v) + c, reinterpret_cast<const float4*>(gv) + c);
+        } else {
+            for (int c = tid; c < nt * 9; c += CB) cp_async4(S.v + c, gv + c);
+        }
+        const double2* gs = reinterpret_cast<const double2*>(sgrad + i0 * SG_STRIDE);
+        for (int c = tid; c < nt * (SG_STRIDE / 2); c += CB) {
+            const int tri = c / (SG_STRIDE / 2), q = c - tri * (SG_STRIDE / 2);
+            cp_async16(reinterpret_cast<double2*>(&S.sg[tri * SGW]) + q, gs + c);
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    const long long i = i0 + tid;
+    if (tid < nt) {
+        float* vrow = &S.v[tid * 9];
+        float4* shrow = &S.sh[tid * 13];
+        double dv[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) dv[k] = 0.0;
+        double dop = 0.0, dsig = 0.0;
+        if (!flag[i]) {
+#pragma unroll
+            for (int q = 0; q < 12; q++) shrow[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            const double* sg = &S.sg[tid * SGW];
+            double gq[6];
+#pragma unroll
+            for (int k = 0; k < 6; k++) gq[k] = sg[SG_GQ + k];
+            dop = sg[SG_GO];
+            dsig = sg[SG_GSIG];
+            const double grgb[3] = {sg[SG_GRGB], sg[SG_GRGB + 1], sg[SG_GRGB + 2]};
+            const double gphis = sg[SG_GPHIS], gzz = sg[SG_GZ];
+            double v[9];
+#pragma unroll
+            for (int k = 0; k < 9; k++) v[k] = (double)vrow[k];
+            Proj64 p;
+            project64(v, cam, p);
+            const double* q = p.q;
+            if (opt.mode == 0) {
+                // _phis_q_grad, backward.py:59-90: phi_s = -2 area / perimeter
+                const double e1x = q[2] - q[0], e1y = q[3] - q[1];
+                const double e2x = q[4] - q[0], e2y = q[5] - q[1];
+                const double cross = e1x * e2y - e1y * e2x;
+                const double sgn = (cross > 0) - (cross < 0);
+                double dperim[6] = {0, 0, 0, 0, 0, 0};
+                double perim = 0.0;
+#pragma unroll
+                for (int a = 0; a < 3; a++) {
+                    const int b = a == 2 ? 0 : a + 1;
+                    const double dx = q[a * 2] - q[b * 2], dy = q[a * 2 + 1] - q[b * 2 + 1];
+                    const double nd = sqrt(dx * dx + dy * dy);
+                    perim += nd;
+                    const double ux = dx / nd, uy = dy / nd;
+                    dperim[a * 2] += ux;
+                    dperim[a * 2 + 1] += uy;
+                    dperim[b * 2] -= ux;
+                    dperim[b * 2 + 1] -= uy;
+                }
+                const double area = fabs(cross) * 0.5;
+                const double dcross[6] = {q[3] - q[5], q[4] - q[2], q[5] - q[1], q[0] - q[4], q[1] - q[3], q[2] - q[0]};
+                const double coef_a = -2.0 / perim;
+                const double coef_p = 2.0 * area / (perim * perim);
+#pragma unroll
+                for (int k = 0; k < 6; k++) gq[k] += gphis * (coef_a * (0.5 * sgn * dcross[k]) + coef_p * dperim[k]);
+            }
+            // projection Jacobian, backward.py:181-190
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                const double zc = p.xc[k * 3 + 2];
+                const double iz = 1.0 / zc;
+                const double dx = cam.fx * gq[k * 2] * iz;
+                const double dy = cam.fy * gq[k * 2 + 1] * iz;
+                const double dz = (-cam.fx * p.xc[k * 3] * gq[k * 2] - cam.fy * p.xc[k * 3 + 1] * gq[k * 2 + 1]) * (iz * iz) +
+                                  gzz / 3.0;
+#pragma unroll
+                for (int b = 0; b < 3; b++) dv[k * 3 + b] = dx * cam.R[b] + dy * cam.R[3 + b] + dz * cam.R[6 + b];
+            }
+            // colour path, backward.py:192-205 (sh.py:30-52 basis, 55-100 gradient)
+            double u[3];
+#pragma unroll
+            for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) / 3.0 - cam.cc[b];
+            double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+            un = un > 1e-12 ? un : 1e-12;
+            const double vx = u[0] / un, vy = u[1] / un, vz = u[2] / un;
+            double basis[16];
+            sh_basis16(vx, vy, vz, basis);
+            const int ncoef = opt.ncoef;
+            double raw[3] = {0.5, 0.5, 0.5};
+#pragma unroll
+            for (int qd = 0; qd < 12; qd++) {
+                const float4 c4 = shrow[qd];
+                const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                for (int uu = 0; uu < 4; uu++) {
+                    const int idx = qd * 4 + uu;
+                    if (idx / 3 < ncoef) raw[idx % 3] += basis[idx / 3] * (double)cv[uu];
+                }
+            }
+            double d_raw[3];
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) d_raw[ch] = (raw[ch] > 0.0 && raw[ch] < 1.0) ? grgb[ch] : 0.0;
+            // s_c = sum_ch d_raw[ch] * coef[c][ch]; d_sh[c][ch] = basis[c] * d_raw[ch] (in place)
+            double s[16];
+#pragma unroll
+            for (int c = 0; c < 16; c++) s[c] = 0.0;
+#pragma unroll
+            for (int qd = 0; qd < 12; qd++) {
+                const float4 c4 = shrow[qd];
+                const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+                float o4[4];
+#pragma unroll
+                for (int uu = 0; uu < 4; uu++) {
+                    const int idx = qd * 4 + uu, c = idx / 3, ch = idx % 3;
+                    const bool on = c < ncoef;
+                    if (on) s[c] += d_raw[ch] * (double)cv[uu];
+                    o4[uu] = on ? (float)(basis[c] * d_raw[ch]) : 0.f;
+                }
+                shrow[qd] = make_float4(o4[0], o4[1], o4[2], o4[3]);
+            }
+            double ddir[3];
+            sh_weighted_grad(vx, vy, vz, s, ddir);
+            const double dot = vx * ddir[0] + vy * ddir[1] + vz * ddir[2];
+#pragma unroll
+            for (int b = 0; b < 3; b++) {
+                const double du = (ddir[b] - (b == 0 ? vx : b == 1 ? vy : vz) * dot) / un / 3.0;
+#pragma unroll
+                for (int k = 0; k < 3; k++) dv[k * 3 + b] += du;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 9; k++) vrow[k] = (float)dv[k];
+        S.os[0][tid] = (float)dop;
+        S.os[1][tid] = (float)dsig;
+    }
+    __syncthreads();
+    // ---- coalesced write-out ----
+    {
+        float4* g = reinterpret_cast<float4*>(grads.d_sh + i0 * 48);
+        for (int c = tid; c < nt * 12; c += CB) {
+            const int tri = c / 12;
+            float4 v = S.sh[tri * 13 + (c - tri * 12)];
+            if (accumulate) {
+                const float4 o = g[c];
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            }
+            g[c] = v;
+        }
+        float* gv = grads.d_vertices + i0 * 9;
+        for (int c = tid; c < nt * 9; c += CB) gv[c] = accumulate ? gv[c] + S.v[c] : S.v[c];
+        if (tid < nt) {
+            grads.d_opacity[i0 + tid] = accumulate ? grads.d_opacity[i0 + tid] + S.os[0][tid] : S.os[0][tid];
+            grads.d_sigma[i0 + tid] = accumulate ? grads.d_sigma[i0 + tid] + S.os[1][tid] : S.os[1][tid];
+        }
+    }
+}
+
+bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,
+                           const double* sgrad, const ts_grads& g, int accumulate, cudaStream_t st) {
+    const long long n = soup.n;
+    if (dtype != 0) return false;
+    // 16-byte vector access of the SH / gradient blocks
+    if (((uintptr_t)soup.sh | (uintptr_t)g.d_sh | (uintptr_t)soup.vertices) & 15) return false;
+    if (n <= 0) return true;
+    static bool attr = false;
+    const int smem = (int)sizeof(ChainStage);
+    if (!attr) {
+        cudaFuncSetAttribute(k_chain_bwd32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const unsigned grid = (unsigned)((n + CB - 1) / CB);
+    k_chain_bwd32<<<grid, CB, smem, st>>>(cam, opt, (const float*)soup.vertices, (const float*)soup.sh, flag, sgrad, n,
+                                          g, accumulate);
+    return true;
+}
+
+}  // namespace ts

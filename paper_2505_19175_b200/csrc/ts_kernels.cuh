@@ -103,6 +103,10 @@ void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, co
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
                             const int* last_pos, const float* d_image, double* sgrad, cudaStream_t st);
 
+// ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
+bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,
+                           const double* sgrad, const ts_grads& g, int accumulate, cudaStream_t st);
+
 // ts_sort.cu
 struct SortScratch {
     unsigned* hist;     // RADIX * max_blocks
