@@ -282,19 +282,20 @@ __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const Re
             const int chunk = ((total + 255) >> 8) << 5;
             const int k0 = (int)warp * chunk;
             const int kE = min(k0 + chunk, total);
-            int j = 0;
+            int jb = 0;
             if (k0 < kE) {
 #pragma unroll
                 for (int step = DB / 2; step > 0; step >>= 1)
-                    if (j + step < nb && sm.S[j + step] <= k0) j += step;
+                    if (jb + step < nb && sm.S[jb + step] <= k0) jb += step;
             }
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
+                int sj;
+                const int j = pair_step_entry(sm.S, nb, kb, jb, sj);
                 if (k < kE) {
-                    while (sm.S[j + 1] <= k) j++;
                     const unsigned g = sm.geo[j];
                     const int w = (g >> 8) & 31;
-                    const int local = k - sm.S[j];
+                    const int local = k - sj;
                     const int dy = (int)(((unsigned)local * (g >> 16)) >> 15);
                     const int qx = (int)(g & 15) + local - dy * w;
                     const int qy = (int)((g >> 4) & 15) + dy;
@@ -477,6 +478,10 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const 
         return v ? atoi(v) : 0;
     }();
     if (variant == 1)
+        launch_dense<64, 2048, false, false>(cam, opt, rec, tile_start, ent_src, out, st);
+    else if (variant == 2)
+        launch_dense<32, 2048, false, false>(cam, opt, rec, tile_start, ent_src, out, st);
+    else if (variant == 3)
         launch_dense<64, 4096, false, true>(cam, opt, rec, tile_start, ent_src, out, st);
     else
         launch_dense<64, 4096, false, false>(cam, opt, rec, tile_start, ent_src, out, st);

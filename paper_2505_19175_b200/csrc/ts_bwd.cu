@@ -200,20 +200,21 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
             const int chunk = ((total + 255) >> 8) << 5;
             const int k0 = (int)warp * chunk;
             const int kE = min(k0 + chunk, total);
-            int jj = 0;
+            int jb = 0;
             if (k0 < kE) {
 #pragma unroll
                 for (int step = DB / 2; step > 0; step >>= 1)
-                    if (jj + step < nb && sm.S[jj + step] <= k0) jj += step;
+                    if (jb + step < nb && sm.S[jb + step] <= k0) jb += step;
             }
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
                 bool pass = false;
+                int sj;
+                const int jj = pair_step_entry(sm.S, nb, kb, jb, sj);
                 if (k < kE) {
-                    while (sm.S[jj + 1] <= k) jj++;
                     const unsigned g = sm.geo[jj];
                     const int w = (g >> 8) & 31;
-                    const int local = k - sm.S[jj];
+                    const int local = k - sj;
                     const int dy = (int)(((unsigned)local * (g >> 16)) >> 15);
                     const int qx = (int)(g & 15) + local - dy * w;
                     const int qy = (int)((g >> 4) & 15) + dy;
