@@ -125,6 +125,32 @@ int ts_forward(ts_context* ctx, const ts_camera* cam, const ts_options* opt, con
 int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream);
 
+/* Fragment lists of the last ts_forward: render(collect_fragments=True)
+ * (render.py:383-399, 420-425; count_fragments _kernels.py:135-178,
+ * collect branch _kernels.py:107-116).
+ *  ts_fragment_offsets   CSR offsets (int64, H*W+1; pixel p owns
+ *                        offsets[p]:offsets[p+1]) into `offsets` (device,
+ *                        may be NULL) and the fragment total F into
+ *                        *n_fragments (host).  Synchronizes the stream.
+ *  ts_collect_fragments  fills triangle (int32 source ids), weight (float64
+ *                        T*alpha) and depth (float64 camera-space z) of the F
+ *                        fragments in compositing order (device arrays of F
+ *                        elements, offsets as returned above).  Fast path
+ *                        (precision 0) only. */
+int ts_fragment_offsets(ts_context* ctx, int64_t* offsets, int64_t* n_fragments, void* stream);
+int ts_collect_fragments(ts_context* ctx, const int64_t* offsets, int32_t* triangle, double* weight,
+                         double* depth, void* stream);
+
+/* render_backward(frag_grads=(offsets, d_weight, d_depth)) (backward.py:122-142,
+ * _kernels.py:262-272): ts_backward plus upstream gradients on the blend
+ * weight and depth of every fragment of the last forward, in the CSR layout
+ * of ts_fragment_offsets (device arrays).  A layout that differs from this
+ * scene/camera returns TS_ERR_FRAGMENTS.  Needs a keep_backward forward on
+ * the fast path. */
+int ts_backward_fragments(ts_context* ctx, const float* d_image, const int64_t* offsets,
+                          const double* d_weight, const double* d_depth, const ts_grads* grads,
+                          int accumulate, void* stream);
+
 /* Debug/parity dumps of the last forward pass (device destination):
  *  TS_DUMP_SORTED_IDX  int32[M]       depth-sorted source ids (render.py:275-277)
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)

@@ -48,6 +48,7 @@ struct ts_context {
     double* depth = nullptr;
     short4* bbox = nullptr;
     DevBuf rec64, recf, recb, sg64, sg32;
+    DevBuf frag_off, cs_scratch;  // expected fragment CSR offsets + scan scratch
     // per-entry scratch
     long long cap_e = -1;
     void* ent_buf = nullptr;
@@ -58,6 +59,7 @@ struct ts_context {
     double* t_final = nullptr;
     float* t_final32 = nullptr;
     int* last_pos = nullptr;
+    int* nfrag = nullptr;       // composited fragments per pixel of the last forward
     int2* flags = nullptr;
     int* tile_start = nullptr;
     // sort scratch
@@ -182,7 +184,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
         return o;
     };
     size_t o_tf = take(8 * cp), o_t32 = take(4 * cp), o_lp = take(4 * cp), o_fg = take(8 * cp),
-           o_ts = take(4 * (ct + 1));
+           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp);
     TS_CHECK(cudaMalloc(&c->pix_buf, off));
     char* b = (char*)c->pix_buf;
     c->t_final = (double*)(b + o_tf);
@@ -190,6 +192,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     c->last_pos = (int*)(b + o_lp);
     c->flags = (int2*)(b + o_fg);
     c->tile_start = (int*)(b + o_ts);
+    c->nfrag = (int*)(b + o_nf);
     c->cap_p = cp;
     c->cap_tiles = ct;
     return TS_OK;
@@ -279,7 +282,8 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->tri_buf);
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
-    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32}) cudaFree(b->p);
+    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch})
+        cudaFree(b->p);
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
     cudaFree(c->d_ctr);
@@ -421,7 +425,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
 
     if (fast) {
         FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
-                        out->n_frag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
+                        c->nfrag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
                         c->flags, c->d_ctr};
         stage_begin(c, TS_STAGE_BLEND, st);
         static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
@@ -442,12 +446,13 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
                                  cudaMemcpyDeviceToHost, st));
     } else {
         BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
-                    out->n_frag, c->t_final, c->last_pos};
+                    c->nfrag, c->t_final, c->last_pos};
         stage_begin(c, TS_STAGE_BLEND, st);
         launch_blend_exact(cm, op, (const Rec64*)c->rec64.p, c->tile_start, (const int*)c->ent_src, bo, st);
         stage_end(c, TS_STAGE_BLEND, st);
         g_launches += 1;
     }
+    if (out->n_frag && P) TS_CHECK(cudaMemcpyAsync(out->n_frag, c->nfrag, 4 * P, cudaMemcpyDeviceToDevice, st));
     TS_CHECK(cudaGetLastError());
     c->have_fwd = true;
     c->have_bwd_state = !fast || opt->keep_backward;
@@ -462,8 +467,97 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     return TS_OK;
 }
 
+static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
+                         const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream);
+
 int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream) {
+    return backward_impl(c, d_image, grads, accumulate, nullptr, nullptr, nullptr, stream);
+}
+
+// expected fragment CSR offsets of the last forward into c->frag_off; returns F
+static int fragment_offsets(ts_context* c, cudaStream_t st, long long* total) {
+    const long long P = (long long)c->cam.width * c->cam.height;
+    int rc;
+    if ((rc = ensure(c->frag_off, sizeof(long long) * (P + 1)))) return rc;
+    if ((rc = ensure(c->cs_scratch, count_scan_scratch_bytes(P)))) return rc;
+    count_scan_i64(P, c->nfrag, (long long*)c->frag_off.p, c->cs_scratch.p, st);
+    g_launches += 3;
+    long long f = 0;
+    TS_CHECK(cudaMemcpyAsync(&f, (long long*)c->frag_off.p + P, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    TS_CHECK(cudaStreamSynchronize(st));
+    *total = f;
+    return TS_OK;
+}
+
+int ts_fragment_offsets(ts_context* c, int64_t* offsets, int64_t* n_fragments, void* stream) {
+    if (!c || !n_fragments) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    cudaStream_t st = (cudaStream_t)stream;
+    long long f = 0;
+    int rc = fragment_offsets(c, st, &f);
+    if (rc) return rc;
+    const long long P = (long long)c->cam.width * c->cam.height;
+    if (offsets)
+        TS_CHECK(cudaMemcpyAsync(offsets, c->frag_off.p, sizeof(long long) * (P + 1), cudaMemcpyDeviceToDevice, st));
+    *n_fragments = (int64_t)f;
+    return TS_OK;
+}
+
+int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangle, double* weight, double* depth,
+                         void* stream) {
+    if (!c || !offsets || !triangle || !weight || !depth) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    if (c->precision != 0) return TS_ERR_INVALID_ARG;  // fragment lists come from the fast path's fp64 replay
+    cudaStream_t st = (cudaStream_t)stream;
+    // re-composite with fp64 weights and emit every composited fragment
+    // (rasterize_forward collect branch, _kernels.py:107-116); statistics and
+    // images are not touched, flagged pixels are re-emitted by the fix-up
+    TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, sizeof(unsigned long long), st));
+    FastBlendOut bo{};
+    bo.t_final = c->t_final32;
+    bo.t_final64 = nullptr;
+    bo.last_pos = c->last_pos;
+    bo.n_frag = c->nfrag;
+    bo.flags = c->flags;
+    bo.ctr = c->d_ctr;
+    bo.frag_off = (const long long*)offsets;
+    bo.frag_tri = triangle;
+    bo.frag_w = weight;
+    bo.frag_z = depth;
+    bo.zkey = c->key;
+    launch_blend_fast(c->cam, c->opt, c->soup, c->dtype, true, (const RecF*)c->recf.p, c->bbox, c->tile_start,
+                      c->ent_src, bo, st);
+    launch_fixup_fwd(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src, bo, st);
+    g_launches += 2;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* offsets, const double* d_weight,
+                          const double* d_depth, const ts_grads* grads, int accumulate, void* stream) {
+    if (!c || !d_image || !grads || !offsets || !d_weight || !d_depth) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
+    if (c->precision != 0) return TS_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    long long f = 0;
+    int rc = fragment_offsets(c, st, &f);
+    if (rc) return rc;
+    const long long P = (long long)c->cam.width * c->cam.height;
+    // the layout must be the CSR of this scene/camera (backward.py:130-136)
+    TS_CHECK(cudaMemsetAsync(&c->d_ctr->pad[0], 0, sizeof(unsigned long long), st));
+    offsets_mismatch(P, (const long long*)offsets, (const long long*)c->frag_off.p, &c->d_ctr->pad[0], st);
+    g_launches += 1;
+    unsigned long long bad = 0;
+    TS_CHECK(cudaMemcpyAsync(&bad, &c->d_ctr->pad[0], sizeof(bad), cudaMemcpyDeviceToHost, st));
+    TS_CHECK(cudaStreamSynchronize(st));
+    if (bad) return TS_ERR_FRAGMENTS;
+    (void)f;
+    return backward_impl(c, d_image, grads, accumulate, (const long long*)offsets, d_weight, d_depth, stream);
+}
+
+static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
+                         const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream) {
     if (!c || !d_image || !grads) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
@@ -477,13 +571,14 @@ int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int 
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
         if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
         static const bool bwd_legacy = getenv("TS_BWD_LEGACY") != nullptr;
-        if (bwd_legacy)
+        if (bwd_legacy && !frag_off)
             launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
                                   (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
                                   d_image, sg, st);
         else
             launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, c->tile_start,
-                                   c->ent_src, c->t_final, c->last_pos, d_image, sg, st);
+                                   c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
+                                   sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
         if (!launch_chain_bwd_fast(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st))

@@ -54,6 +54,10 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                                                          const double* __restrict__ t_final,
                                                          const int* __restrict__ last_pos,
                                                          const float* __restrict__ d_image,
+                                                         const int* __restrict__ n_frag,
+                                                         const long long* __restrict__ frag_off,
+                                                         const double* __restrict__ fg_dw,
+                                                         const double* __restrict__ fg_dz,
                                                          double* __restrict__ sgrad) {
     using SM = BwdSmem<DB, PCAP, GCAP>;
     constexpr int RR = SM::RR, SR = SM::SR, NW = SM::NW;
@@ -74,8 +78,19 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
     int my_last = -1;
     double T = 1.0, S0 = 0.0, S1 = 0.0, S2 = 0.0;
     double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    // upstream fragment gradients (backward.py:122-142): fragment k of the pixel
+    // is fg_*[fbase + k], visited back to front
+    const bool has_fg = fg_dw != nullptr;
+    const int NC = has_fg ? 13 : 12;
+    long long fbase = 0;
+    int fk = -1;
+    double sw = 0.0;
     if (inside) {
         const int p = py * cam.width + px;
+        if (has_fg) {
+            fbase = frag_off[p];
+            fk = n_frag[p] - 1;
+        }
         my_last = last_pos[p];
         T = t_final[p];
         d0 = d_image[p * 3 + 0];
@@ -326,7 +341,7 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                     if (ae < ALPHA_MIN) {  // (band pairs only) not composited: the slot adds nothing
                         const int sz = sm.wpre[kk >> 5] + __popc(sm.pbits[kk >> 5] & ((1u << (kk & 31)) - 1u));
 #pragma unroll
-                        for (int c = 0; c < 12; c++) sm.g[sz][c] = 0.0;
+                        for (int c = 0; c < 13; c++) sm.g[sz][c] = 0.0;
                         continue;
                     }
                     const bool clamped = ae > ALPHA_CLAMP;
@@ -336,12 +351,20 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                     const double inv1m = 1.0 / (1.0 - a);
                     const double tb = T * inv1m;
                     const double w = tb * a;
-                    double g[12];
+                    double g[13];
                     g[8] = w * d0;
                     g[9] = w * d1;
                     g[10] = w * d2;
-                    const double ga = d0 * (tb * col.x - S0 * inv1m) + d1 * (tb * col.y - S1 * inv1m) +
-                                      d2 * (tb * col.z - S2 * inv1m);
+                    double ga = d0 * (tb * col.x - S0 * inv1m) + d1 * (tb * col.y - S1 * inv1m) +
+                                d2 * (tb * col.z - S2 * inv1m);
+                    g[12] = 0.0;
+                    if (has_fg) {
+                        const double u = fg_dw[fbase + fk];
+                        ga += u * tb - sw * inv1m;
+                        sw += u * w;
+                        g[12] = fg_dz[fbase + fk];
+                        fk--;
+                    }
                     S0 = fma(w, (double)col.x, S0);
                     S1 = fma(w, (double)col.y, S1);
                     S2 = fma(w, (double)col.z, S2);
@@ -390,15 +413,15 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                     }
                     const int slot_g = sm.wpre[kk >> 5] + __popc(sm.pbits[kk >> 5] & ((1u << (kk & 31)) - 1u));
 #pragma unroll
-                    for (int c = 0; c < 12; c++) sm.g[slot_g][c] = g[c];
+                    for (int c = 0; c < 13; c++) sm.g[slot_g][c] = g[c];
                 }
             }
         }
         __syncthreads();
         // ---- 4. flush: per (entry, component) an fp64 sum over the entry's
         //         contributing pairs in a fixed order, one global atomic ----
-        for (int c = tid; c < np * 12; c += 256) {
-            const int jj = c / 12, comp = c - jj * 12;
+        for (int c = tid; c < np * NC; c += 256) {
+            const int jj = c / NC, comp = c - jj * NC;
             auto rank = [&](int k) {
                 const int wi = k >> 5;
                 return sm.wpre[wi] + ((k & 31) ? __popc(sm.pbits[wi] & ((1u << (k & 31)) - 1u)) : 0);
@@ -416,7 +439,9 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
 template <int DB, int PCAP, int GCAP>
 static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                              const int* tile_start, const unsigned* ent_src, const double* t_final,
-                             const int* last_pos, const float* d_image, double* sgrad, cudaStream_t st) {
+                             const int* last_pos, const float* d_image, const int* n_frag,
+                             const long long* frag_off, const double* fg_dw, const double* fg_dz, double* sgrad,
+                             cudaStream_t st) {
     const int dyn = (int)sizeof(BwdSmem<DB, PCAP, GCAP>);
     static bool attr = false;
     if (!attr) {
@@ -425,13 +450,15 @@ static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, c
     }
     const int ntiles = cam.ntx * cam.nty;
     k_blend_bwd_dense<DB, PCAP, GCAP><<<ntiles, 256, dyn, st>>>(cam, opt, rec, recb, tile_start, ent_src, t_final,
-                                                           last_pos, d_image, sgrad);
+                                                           last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz, sgrad);
 }
 
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
-                            const int* last_pos, const float* d_image, double* sgrad, cudaStream_t st) {
-    launch_bwd_dense<64, 2048, 512>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, sgrad, st);
+                            const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
+                            const double* fg_dw, const double* fg_dz, double* sgrad, cudaStream_t st) {
+    launch_bwd_dense<64, 2048, 512>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
+                                    frag_off, fg_dw, fg_dz, sgrad, st);
 }
 
 }  // namespace ts

@@ -630,6 +630,13 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
                                         w = (float)wd;
                                         contrib = true;
                                         last = b + j;
+                                        if (out.frag_tri) {
+                                            const long long fi = out.frag_off[py * cam.width + px] + cnt;
+                                            const unsigned src = s_src[j];
+                                            out.frag_tri[fi] = (int)src;
+                                            out.frag_w[fi] = wd;
+                                            out.frag_z[fi] = __longlong_as_double((long long)out.zkey[src]);
+                                        }
                                         cnt++;
                                         T = tn;
                                         done = tn < T_MIN;
@@ -994,6 +1001,12 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
                         C1 += w * (double)s_c[1][j];
                         C2 += w * (double)s_c[2][j];
                         const int posj = base + j;
+                        if (lane == 0 && out.frag_tri) {
+                            const long long fi = out.frag_off[p] + cnt;
+                            out.frag_tri[fi] = (int)s_s[j];
+                            out.frag_w[fi] = w;
+                            out.frag_z[fi] = __longlong_as_double((long long)out.zkey[s_s[j]]);
+                        }
                         if (lane == 0 && posj >= fpos) {
                             if (out.max_weight) atomicMax((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
                             if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + s_s[j], 1);

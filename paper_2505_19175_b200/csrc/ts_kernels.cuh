@@ -51,6 +51,13 @@ struct FastBlendOut {
     int* last_pos;
     int2* flags;               // (pixel, flag position) of guard-band pixels
     Counters* ctr;
+    // fragment emission (render(collect_fragments=True), render.py:383-399):
+    // fragment i of pixel p goes to frag_off[p] + i; null = no emission
+    const long long* frag_off;
+    int* frag_tri;             // source id
+    double* frag_w;            // blend weight T * alpha
+    double* frag_z;            // camera-space depth of the triangle
+    const unsigned long long* zkey;  // (N) fp64 bit pattern of the centroid depth
 };
 
 struct BlendOut {
@@ -101,7 +108,8 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const 
 // ts_bwd.cu: dense backward blend
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
-                            const int* last_pos, const float* d_image, double* sgrad, cudaStream_t st);
+                            const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
+                            const double* fg_dw, const double* fg_dz, double* sgrad, cudaStream_t st);
 
 // ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
 bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,
@@ -150,5 +158,11 @@ void compact_accepted32(long long n, const unsigned* flag, const unsigned long l
                         const SortScratch& s, cudaStream_t st);
 void fix_depth_runs(long long m, const unsigned* k32, unsigned* vals, const unsigned long long* key64,
                     cudaStream_t st);
+
+// CSR offsets (n+1, int64) from int32 counts; scratch from count_scan_scratch_bytes
+size_t count_scan_scratch_bytes(long long n);
+void count_scan_i64(long long n, const int* cnt, long long* off, void* scratch, cudaStream_t st);
+// *bad += number of i in [0, n] with a[i] != b[i]
+void offsets_mismatch(long long n, const long long* a, const long long* b, unsigned long long* bad, cudaStream_t st);
 
 }  // namespace ts

@@ -570,4 +570,106 @@ void fix_depth_runs(long long m, const unsigned* k32, unsigned* vals, const unsi
     k_fix_runs<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, k32, vals, key64);
 }
 
+
+// ---------------------------------------------------------------------------
+// exclusive scan of per-pixel int32 counts into int64 CSR offsets (P+1):
+// per-block totals, one-block scan of the totals, block scan + offset.
+// ---------------------------------------------------------------------------
+constexpr int CS_T = 512, CS_PER = 8, CS_CHUNK = CS_T * CS_PER;
+
+__device__ __forceinline__ long long cs_block_excl(long long v, long long* s_w, long long& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        long long w = lane < CS_T / 32 ? s_w[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < CS_T / 32) s_w[lane] = w;
+    }
+    __syncthreads();
+    total = s_w[CS_T / 32 - 1];
+    const long long before = warp ? s_w[warp - 1] : 0;
+    __syncthreads();
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(CS_T) k_cs_totals(long long n, const int* __restrict__ cnt, long long* __restrict__ bt) {
+    __shared__ long long s_w[CS_T / 32];
+    const long long base = (long long)blockIdx.x * CS_CHUNK + (long long)threadIdx.x * CS_PER;
+    long long v = 0;
+#pragma unroll
+    for (int k = 0; k < CS_PER; k++)
+        if (base + k < n) v += cnt[base + k];
+    long long tot;
+    cs_block_excl(v, s_w, tot);
+    if (threadIdx.x == 0) bt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(CS_T) k_cs_scan_totals(long long nb, long long* __restrict__ bt) {
+    __shared__ long long s_w[CS_T / 32];
+    long long carry = 0;
+    for (long long b0 = 0; b0 < nb; b0 += CS_T) {
+        const long long i = b0 + threadIdx.x;
+        const long long v = i < nb ? bt[i] : 0;
+        long long tot;
+        const long long ex = cs_block_excl(v, s_w, tot);
+        if (i < nb) bt[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+__global__ void __launch_bounds__(CS_T) k_cs_apply(long long n, const int* __restrict__ cnt, const long long* __restrict__ bt,
+                                                   long long* __restrict__ off) {
+    __shared__ long long s_w[CS_T / 32];
+    const long long base = (long long)blockIdx.x * CS_CHUNK + (long long)threadIdx.x * CS_PER;
+    int c[CS_PER];
+    long long v = 0;
+#pragma unroll
+    for (int k = 0; k < CS_PER; k++) {
+        c[k] = base + k < n ? cnt[base + k] : 0;
+        v += c[k];
+    }
+    long long tot;
+    long long run = bt[blockIdx.x] + cs_block_excl(v, s_w, tot);
+#pragma unroll
+    for (int k = 0; k < CS_PER; k++) {
+        if (base + k < n) off[base + k] = run;
+        run += c[k];
+    }
+    if (base < n && base + CS_PER >= n) off[n] = run;
+}
+
+size_t count_scan_scratch_bytes(long long n) { return sizeof(long long) * (size_t)((n + CS_CHUNK - 1) / CS_CHUNK + 1); }
+
+void count_scan_i64(long long n, const int* cnt, long long* off, void* scratch, cudaStream_t st) {
+    if (n <= 0) {
+        cudaMemsetAsync(off, 0, sizeof(long long), st);
+        return;
+    }
+    const long long nb = (n + CS_CHUNK - 1) / CS_CHUNK;
+    long long* bt = (long long*)scratch;
+    k_cs_totals<<<(unsigned)nb, CS_T, 0, st>>>(n, cnt, bt);
+    k_cs_scan_totals<<<1, CS_T, 0, st>>>(nb, bt);
+    k_cs_apply<<<(unsigned)nb, CS_T, 0, st>>>(n, cnt, bt, off);
+}
+
+__global__ void k_offsets_mismatch(long long n, const long long* __restrict__ a, const long long* __restrict__ b,
+                                   unsigned long long* bad) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x)
+        if (a[i] != b[i]) atomicAdd(bad, 1ull);
+}
+
+void offsets_mismatch(long long n, const long long* a, const long long* b, unsigned long long* bad, cudaStream_t st) {
+    k_offsets_mismatch<<<592, 256, 0, st>>>(n, a, b, bad);
+}
 }  // namespace ts

@@ -122,6 +122,21 @@ class DeviceGrads:
 
 
 @dataclass
+class DeviceFragments:
+    """FragmentData (render.py:68-81) on the GPU."""
+
+    offsets: torch.Tensor   # (H*W+1,) int64
+    triangle: torch.Tensor  # (F,) int32 source ids
+    weight: torch.Tensor    # (F,) float64 T*alpha
+    depth: torch.Tensor     # (F,) float64 camera-space z
+
+    def to_fragment_data(self) -> FragmentData:
+        return FragmentData(offsets=self.offsets.cpu().numpy(),
+                            triangle=self.triangle.cpu().numpy().astype(np.int64),
+                            weight=self.weight.cpu().numpy(), depth=self.depth.cpu().numpy())
+
+
+@dataclass
 class ForwardResult:
     image: torch.Tensor        # (H,W,3) float32, clipped
     alpha_map: torch.Tensor    # (H,W)
@@ -259,6 +274,55 @@ class Rasterizer:
                                         int(bool(accumulate)), ctypes.c_void_p(st)), "backward")
         return grads
 
+    def fragments(self, stream=None) -> "DeviceFragments":
+        """Fragment lists of the last forward (render(collect_fragments=True),
+        render.py:383-399, 420-425): CSR offsets (int64, H*W+1), source ids,
+        blend weights T*alpha (fp64) and depths (fp64), in compositing order."""
+        if self._last is None:
+            raise RuntimeError("fragments() needs a preceding forward()")
+        _, h, w = self._last
+        dev = torch.device("cuda", self.device)
+        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        off = torch.empty(h * w + 1, dtype=torch.int64, device=dev)
+        nf = ctypes.c_int64()
+        _lib.check(self.lib.ts_fragment_offsets(self._ctx, _ptr(off), ctypes.byref(nf), ctypes.c_void_p(st)),
+                   "fragment_offsets")
+        f = int(nf.value)
+        tri = torch.empty(max(f, 1), dtype=torch.int32, device=dev)
+        wgt = torch.empty(max(f, 1), dtype=torch.float64, device=dev)
+        dep = torch.empty(max(f, 1), dtype=torch.float64, device=dev)
+        _lib.check(self.lib.ts_collect_fragments(self._ctx, _ptr(off), _ptr(tri), _ptr(wgt), _ptr(dep),
+                                                 ctypes.c_void_p(st)), "collect_fragments")
+        return DeviceFragments(off, tri[:f], wgt[:f], dep[:f])
+
+    def backward_fragments(self, d_image: torch.Tensor, offsets: torch.Tensor, d_weight: torch.Tensor,
+                           d_depth: torch.Tensor, grads: DeviceGrads | None = None, accumulate: bool = False,
+                           stream=None) -> DeviceGrads:
+        """backward() plus upstream gradients on the blend weight and depth of
+        every fragment (render_backward(frag_grads=...), backward.py:122-142)."""
+        if self._last is None:
+            raise RuntimeError("backward_fragments() needs a preceding forward()")
+        n, h, w = self._last
+        if tuple(d_image.shape) != (h, w, 3):
+            raise ValueError(f"d_image must be {(h, w, 3)}, got {tuple(d_image.shape)}")
+        dev = torch.device("cuda", self.device)
+        d_image = d_image.to(device=dev, dtype=torch.float32).contiguous()
+        offsets = offsets.to(device=dev, dtype=torch.int64).contiguous()
+        d_weight = d_weight.to(device=dev, dtype=torch.float64).contiguous()
+        d_depth = d_depth.to(device=dev, dtype=torch.float64).contiguous()
+        if grads is None:
+            grads = DeviceGrads(torch.empty(n * 59, dtype=torch.float32, device=dev), n)
+            accumulate = False
+        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        g = grads._ts()
+        rc = self.lib.ts_backward_fragments(self._ctx, _ptr(d_image), _ptr(offsets), _ptr(d_weight),
+                                            _ptr(d_depth), ctypes.byref(g), int(bool(accumulate)),
+                                            ctypes.c_void_p(st))
+        if rc == _lib.TS_ERR_FRAGMENTS:
+            raise ValueError("fragment gradients do not match this scene/camera")
+        _lib.check(rc, "backward_fragments")
+        return grads
+
     # ---- parity dumps (project_scene / build_tile_lists internals) ----
     def _dump(self, what, numel, dtype):
         buf = torch.empty(max(numel, 1), dtype=dtype, device="cuda")
@@ -308,18 +372,19 @@ def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
     """Drop-in for trisplat.render.render (render.py:364-432)."""
     _require_cuda()
     soup = as_soup(triangles)
-    if collect_fragments:
-        raise NotImplementedError("collect_fragments is not implemented on the B200 path yet")
+    if collect_fragments and precision != "fast":
+        raise ValueError("collect_fragments needs precision='fast'")
     rast = default_rasterizer()
     ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
     fwd = rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
                        precision=precision)
+    frags = rast.fragments().to_fragment_data() if collect_fragments else None
     return RenderOutput(image=ImageBuffer(fwd.image.double().cpu().numpy()),
                         alpha_map=fwd.alpha_map.double().cpu().numpy(),
                         per_triangle_max_weight=fwd.max_weight.double().cpu().numpy(),
                         per_triangle_pixel_count=fwd.pixel_count.cpu().numpy().astype(np.int64),
                         per_triangle_area=fwd.area.double().cpu().numpy(),
-                        fragments=None)
+                        fragments=frags)
 
 
 def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d_image=None,
@@ -335,13 +400,28 @@ def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d
         raise ValueError(f"d_image must be {(h, w, 3)}, got {d_np.shape}")
     if not np.isfinite(d_np).all():
         raise ValueError("d_image contains non-finite values")
-    if frag_grads is not None:
-        raise NotImplementedError("frag_grads is not implemented on the B200 path yet")
     rast = default_rasterizer()
     ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
     rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
                  precision=precision)
-    g = rast.backward(torch.as_tensor(d_np, dtype=torch.float32, device="cuda"))
+    d_dev = torch.as_tensor(d_np, dtype=torch.float32, device="cuda")
+    if frag_grads is None:
+        return rast.backward(d_dev).to_gradient_set()
+    if precision != "fast":
+        raise ValueError("frag_grads needs precision='fast'")
+    # backward.py:122-136: the layout must be this scene's fragment CSR
+    frag_off, fg_dw, fg_dz = frag_grads
+    frag_off = np.ascontiguousarray(frag_off, dtype=np.int64)
+    fg_dw = np.ascontiguousarray(fg_dw, dtype=np.float64)
+    fg_dz = np.ascontiguousarray(fg_dz, dtype=np.float64)
+    nf = ctypes.c_int64()
+    _lib.check(rast.lib.ts_fragment_offsets(rast._ctx, None, ctypes.byref(nf),
+                                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "fragment_offsets")
+    if frag_off.shape != (h * w + 1,) or len(fg_dw) != nf.value or len(fg_dz) != nf.value:
+        raise ValueError("fragment gradients do not match this scene/camera")
+    g = rast.backward_fragments(d_dev, torch.from_numpy(frag_off), torch.from_numpy(fg_dw),
+                                torch.from_numpy(fg_dz))
     return g.to_gradient_set()
 
 
