@@ -429,12 +429,12 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
                         c->flags, c->d_ctr};
         stage_begin(c, TS_STAGE_BLEND, st);
         static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
-        // training forwards composite in fp64 (exact T_final for the backward recursion)
-        if (opt->keep_backward || legacy)
+        if (legacy)
             launch_blend_fast(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
                               c->bbox, c->tile_start, c->ent_src, bo, st);
         else
-            launch_blend_dense(cm, op, (const RecF*)c->recf.p, c->bbox, c->tile_start, c->ent_src, bo, st);
+            launch_blend_dense(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
+                               c->tile_start, c->ent_src, bo, st);
         stage_end(c, TS_STAGE_BLEND, st);
         stage_begin(c, TS_STAGE_FIXUP, st);
         launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,

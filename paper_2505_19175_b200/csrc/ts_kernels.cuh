@@ -101,9 +101,8 @@ void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup,
                            cudaStream_t st);
 
 // ts_blend.cu: render-only forward blend (dense pair evaluation)
-void launch_blend_dense(const Cam& cam, const Opts& opt, const RecF* rec, const short4* bbox,
-                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
-                        cudaStream_t st);
+void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64, const RecF* rec,
+                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st);
 
 // ts_bwd.cu: dense backward blend
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
