@@ -1,27 +1,46 @@
 // ts_bwd.cu -- dense backward blend (rasterize_backward, _kernels.py:181-318).
 //
-// CTA per 16x16 tile, 256 threads, thread = pixel for the per-pixel pass.
-// The tile's entry list is walked BACK TO FRONT from the largest saved last
-// contributor of the tile, in batches of at most DB entries / PCAP pairs:
+// CTA per 16x16 tile, 256 threads.  The tile's entry list is walked BACK TO
+// FRONT from the largest saved last contributor of the tile, in batches of at
+// most DB entries / PCAP pairs; entry jj of a batch is list position bend-1-jj,
+// so ascending bits = back to front.  Per batch:
 //   1. stage    -- records (evaluation part, tail, backward record) arrive in a
 //                  cp.async ring one batch ahead; warp 0 builds the rectangles
-//                  bbox ∩ tile and their pair scan, entry jj of the batch being
-//                  list position bend-1-jj (so ascending bits = back to front);
-//   2. evaluate -- the batch's (entry, pixel) pairs are split over the warps,
-//                  32 consecutive pairs per step; a pair at or before the
-//                  pixel's last contributor (_kernels.py:226-243) with
-//                  r >= r_lo sets the pixel's bit and stores r (fp32, argmax
-//                  edge in the two low mantissa bits; NaN = contribution band);
-//   3. per pixel -- the pixel walks its bits back to front with the
-//                  reference's recursion (_kernels.py:245-318): T_k from the
-//                  saved T_final, suffix colour S, dL/dalpha, the window and
-//                  edge-chain derivatives (fp64 where they cancel), and adds
-//                  the 12 screen-space gradients of the fragment to per-entry
-//                  shared accumulators;
-//   4. flush    -- one fp64 global atomic per (entry, component) and tile.
+//                  bbox ∩ tile and their pair scan;
+//   2. evaluate -- dense over the batch's (entry, pixel) pairs, 32 consecutive
+//                  pairs per warp step: a pair at or before the pixel's last
+//                  contributor (_kernels.py:226-243) is composited iff
+//                  alpha >= 1/255 with the reference's alpha in fp64
+//                  (_kernels.py:43-56); it stores r (fp32, argmax edge in the
+//                  two low mantissa bits) and alpha (fp64), and sets the pixel's
+//                  bit and the pair's bit;
+//   3. slots    -- composited pairs get entry-major slots (prefix popcounts);
+//                  the batch keeps the longest prefix of entries whose slots
+//                  fit in GCAP (the rest is re-evaluated with the next batch);
+//   4. recursion -- thread = pixel walks its bits back to front with the only
+//                  sequential part of the reference (_kernels.py:255-275):
+//                  T_k = T_{k+1} / (1 - alpha_k) from the saved T_final, the
+//                  suffix colour S and (frag_grads) the suffix weight sum; it
+//                  stores T_k, S behind fragment k and the fragment's upstream
+//                  terms in the fragment's slot;
+//   5. gradients -- dense over slots, 32 per warp step: dL/dalpha, window and
+//                  edge-chain derivatives (fp64 where they cancel,
+//                  _kernels.py:276-318) per slot in fp64, a segmented warp
+//                  reduction (fp32 partials) over the slots of one entry, and
+//                  one fp64 global atomic per (entry, component) and warp step.
 #include "ts_kernels.cuh"
 
 namespace ts {
+
+namespace {
+struct __align__(16) BwdSlot {
+    double tb;             // transmittance in front of the fragment
+    double s0, s1, s2;     // suffix colour behind the fragment
+    int k;                 // pair index
+    int jp;                // entry | pixel << 8
+    double u, sw, dz;      // frag_grads: d_weight, suffix weight sum, d_depth
+};
+}  // namespace
 
 template <int DB, int PCAP, int GCAP>
 struct BwdSmem {
@@ -29,36 +48,37 @@ struct BwdSmem {
     EvalRec ev[RR];
     TailRec tail[RR];
     RecB rb[RR];
-    float r[PCAP];               // per pair: r (edge in the low 2 bits); NaN = inside the band
-    unsigned mask[NW][256];      // per pixel: bit jj = entry jj contributes
+    double al[PCAP];             // per pair: unclamped alpha (fp64)
+    float r[PCAP];               // per pair: r (edge in the low 2 bits)
+    BwdSlot slot[GCAP];
+    unsigned mask[NW][256];      // per pixel: bit jj = entry jj composited
     unsigned srcq[SR];
     float4 col[DB];              // rgb, f0
     float4 par[DB];              // opacity, sigma, 1/opacity, 1/phi_s
-    float f1[DB];
     int S[DB + 1];
     unsigned geo[DB];
     int2 kb[DB];
-    double g[GCAP][13];          // per contributing pair (entry-major rank): 12 screen-space gradients
-    unsigned pbits[PCAP / 32];   // pair k contributes
-    int wpre[PCAP / 32 + 1];     // contributing pairs before word w
+    unsigned pbits[PCAP / 32];   // pair k composited
+    int wpre[PCAP / 32 + 1];     // composited pairs before word w
+    float d[3][256];             // upstream image gradient per pixel
     double xc[TILE], yc[TILE];
     int last[256];
     int nb, np, hi;
 };
 
-template <int DB, int PCAP, int GCAP>
-__global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
-                                                         const RecB* __restrict__ recb,
-                                                         const int* __restrict__ tile_start,
-                                                         const unsigned* __restrict__ ent_src,
-                                                         const double* __restrict__ t_final,
-                                                         const int* __restrict__ last_pos,
-                                                         const float* __restrict__ d_image,
-                                                         const int* __restrict__ n_frag,
-                                                         const long long* __restrict__ frag_off,
-                                                         const double* __restrict__ fg_dw,
-                                                         const double* __restrict__ fg_dz,
-                                                         double* __restrict__ sgrad) {
+template <int DB, int PCAP, int GCAP, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
+                                                            const RecB* __restrict__ recb,
+                                                            const int* __restrict__ tile_start,
+                                                            const unsigned* __restrict__ ent_src,
+                                                            const double* __restrict__ t_final,
+                                                            const int* __restrict__ last_pos,
+                                                            const float* __restrict__ d_image,
+                                                            const int* __restrict__ n_frag,
+                                                            const long long* __restrict__ frag_off,
+                                                            const double* __restrict__ fg_dw,
+                                                            const double* __restrict__ fg_dz,
+                                                            double* __restrict__ sgrad) {
     using SM = BwdSmem<DB, PCAP, GCAP>;
     constexpr int RR = SM::RR, SR = SM::SR, NW = SM::NW;
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -69,22 +89,20 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
     const int t = blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
     const int X0 = tx * TILE, Y0 = ty * TILE;
-    const int lx = tid & 15, ly = tid >> 4;
-    const int px = X0 + lx, py = Y0 + ly;
+    const int px = X0 + (tid & 15), py = Y0 + (tid >> 4);
     const bool inside = px < cam.width && py < cam.height;
     const int s = tile_start[t];
     const int mode = opt.mode;
-    // per-pixel state (the pixel stays with its thread)
+    // per-pixel recursion state (thread = pixel)
     int my_last = -1;
-    double T = 1.0, S0 = 0.0, S1 = 0.0, S2 = 0.0;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-    // upstream fragment gradients (backward.py:122-142): fragment k of the pixel
-    // is fg_*[fbase + k], visited back to front
+    double T = 1.0;
+    // upstream fragment gradients (backward.py:122-142): fragment k of the
+    // pixel is fg_*[fbase + k], visited back to front
     const bool has_fg = fg_dw != nullptr;
-    const int NC = has_fg ? 13 : 12;
     long long fbase = 0;
     int fk = -1;
     double sw = 0.0;
+    float d0 = 0.f, d1 = 0.f, d2 = 0.f;
     if (inside) {
         const int p = py * cam.width + px;
         if (has_fg) {
@@ -97,9 +115,10 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
         d1 = d_image[p * 3 + 1];
         d2 = d_image[p * 3 + 2];
     }
-    S0 = T * opt.bg[0];
-    S1 = T * opt.bg[1];
-    S2 = T * opt.bg[2];
+    double S0 = T * opt.bg[0], S1 = T * opt.bg[1], S2 = T * opt.bg[2];
+    sm.d[0][tid] = d0;
+    sm.d[1][tid] = d1;
+    sm.d[2][tid] = d2;
     sm.last[tid] = my_last;
     if (tid < TILE) sm.xc[tid] = (double)(X0 + tid) + 0.5;
     else if (tid < 2 * TILE) sm.yc[tid - TILE] = (double)(Y0 + tid - TILE) + 0.5;
@@ -121,6 +140,10 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
         else
             cp_async16(reinterpret_cast<float4*>(&sm.rb[slot]) + (q - 8),
                        reinterpret_cast<const float4*>(recb + src) + (q - 8));
+    };
+    auto rank = [&](int k) {  // composited pairs before pair k
+        const int wi = k >> 5;
+        return sm.wpre[wi] + ((k & 31) ? __popc(sm.pbits[wi] & ((1u << (k & 31)) - 1u)) : 0);
     };
     // prologue: ids of [hi+1-3DB, hi], then records of [hi+1-DB, hi]
     int slo = max(s, hi + 1 - 3 * DB), rlo = max(s, hi + 1 - DB);
@@ -164,7 +187,6 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                     w[hf] = max(min(bx1 - X0, TILE) - cx0[hf], 0);
                     h[hf] = max(min(by1 - Y0, TILE) - cy0[hf], 0);
                     sm.col[jj] = make_float4(t0.z, t0.w, __int_as_float(t1.x), t0.x);
-                    sm.f1[jj] = t0.y;
                     const RecB& rb = sm.rb[slot];
                     const float o = rb.opa;
                     sm.par[jj] = make_float4(o, rb.sig, 1.f / o, (float)(1.0 / sm.ev[slot].phis));
@@ -209,7 +231,7 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
             rlo = min(rlo, nrlo);
             cp_async_commit();
         }
-        // ---- 2. evaluate ----
+        // ---- 2. evaluate (dense pairs): r, argmax edge, fp64 alpha, composited? ----
         {
             const int total = sm.S[nb];
             const int chunk = ((total + 255) >> 8) << 5;
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
             }
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
-                bool pass = false;
+                bool comp = false;
                 int sj;
                 const int jj = pair_step_entry(sm.S, nb, kb, jb, sj);
                 if (k < kE) {
@@ -246,21 +268,32 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                         if (l1 < rr) { rr = l1; edge = 1; }
                         if (l2 < rr) { rr = l2; edge = 2; }
                         if (rr >= r.r_lo) {
-                            sm.r[k] = rr > r.r_hi ? __uint_as_float((__float_as_uint((float)rr) & ~3u) | edge)
-                                                  : __int_as_float(0x7fc00000);
-                            atomicOr(&sm.mask[jj >> 5][p], 1u << (jj & 31));
-                            pass = true;
+                            const float4 par = sm.par[jj];
+                            const double o64 = (double)par.x, sg64 = (double)par.y;
+                            double ae;
+                            if (mode == 0) {
+                                const double rc = fmin(rr, 1.0);
+                                ae = rr <= 0.0 ? 0.0 : o64 * (sg64 == 1.0 ? rc : pow(rc, sg64));
+                            } else {
+                                ae = o64 / (1.0 + exp(fmin(rr * r.phis / sg64, 700.0)));
+                            }
+                            // outside the band alpha >= 1/255 holds by construction
+                            if (rr > r.r_hi || ae >= ALPHA_MIN) {
+                                comp = true;
+                                sm.r[k] = __uint_as_float((__float_as_uint((float)rr) & ~3u) | edge);
+                                sm.al[k] = ae;
+                                atomicOr(&sm.mask[jj >> 5][p], 1u << (jj & 31));
+                            }
                         }
                     }
                 }
-                const unsigned pb = __ballot_sync(0xffffffffu, pass);
+                const unsigned pb = __ballot_sync(0xffffffffu, comp);
                 if (lane == 0) sm.pbits[kb >> 5] = pb;
             }
         }
         __syncthreads();
-        // ---- 2b. ranks of contributing pairs; the batch keeps the longest prefix of
-        //          entries whose contributing pairs fit in GCAP (the rest is
-        //          re-evaluated with the next batch) ----
+        // ---- 3. slots: prefix popcounts; the batch keeps the longest prefix of
+        //         entries whose composited pairs fit in GCAP ----
         if (warp == 0) {
             constexpr int NWD = PCAP / 32;
             const int total = sm.S[nb];
@@ -269,7 +302,7 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
 #pragma unroll
             for (int q = 0; q < NWD / 32; q++) {
                 const int wi = (int)lane + 32 * q;
-                int c = wi < nwd ? __popc(sm.pbits[wi]) : 0;
+                const int c = wi < nwd ? __popc(sm.pbits[wi]) : 0;
                 int incl = c;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
@@ -281,7 +314,6 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
             }
             if (lane == 0) sm.wpre[NWD] = carry;
             __syncwarp();
-            // contributing pairs before the end of entry jj
             int n = 0;
             bool full = true;
 #pragma unroll
@@ -301,7 +333,7 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
         }
         __syncthreads();
         const int np = sm.np;
-        // ---- 3. per pixel, back to front ----
+        // ---- 4. recursion (thread = pixel), back to front over entries < np ----
         if (my_last >= 0) {
 #pragma unroll
             for (int wd = 0; wd < NW; wd++) {
@@ -310,76 +342,86 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                 while (m) {
                     const int jj = wd * 32 + __ffs(m) - 1;
                     m &= m - 1;
-                    const int slot = (bend - 1 - jj) & (RR - 1);
                     const int2 kbj = sm.kb[jj];
-                    const int kk = kbj.x + ly * kbj.y + lx;
-                    const float rv = sm.r[kk];
-                    const EvalRec& er = sm.ev[slot];
-                    const float4 par = sm.par[jj];  // o, sigma, 1/o, 1/phi_s
-                    const double pcx = sm.xc[lx], pcy = sm.yc[ly];
-                    // alpha with the reference formula in fp64 (_kernels.py:43-56): the
-                    // transmittance recursion divides by 1 - alpha
-                    int edge;
-                    double r64;
-                    if (!isnan(rv)) {
-                        edge = (int)(__float_as_uint(rv) & 3u);
-                        r64 = fma(er.a[3 * edge], pcx, fma(er.a[3 * edge + 1], pcy, er.a[3 * edge + 2]));
-                    } else {  // r inside the contribution band: argmax edge and r in fp64
-                        const double l0 = fma(er.a[0], pcx, fma(er.a[1], pcy, er.a[2]));
-                        const double l1 = fma(er.a[3], pcx, fma(er.a[4], pcy, er.a[5]));
-                        const double l2 = fma(er.a[6], pcx, fma(er.a[7], pcy, er.a[8]));
-                        r64 = l0;
-                        edge = 0;
-                        if (l1 < r64) { r64 = l1; edge = 1; }
-                        if (l2 < r64) { r64 = l2; edge = 2; }
-                    }
-                    const double o64 = (double)par.x, sg64 = (double)par.y;
-                    const double rc = fmin(r64, 1.0);
-                    double ae;
-                    if (mode == 0) ae = r64 <= 0.0 ? 0.0 : o64 * (sg64 == 1.0 ? rc : pow(rc, sg64));
-                    else ae = o64 / (1.0 + exp(fmin(r64 * er.phis / sg64, 700.0)));
-                    if (ae < ALPHA_MIN) {  // (band pairs only) not composited: the slot adds nothing
-                        const int sz = sm.wpre[kk >> 5] + __popc(sm.pbits[kk >> 5] & ((1u << (kk & 31)) - 1u));
-#pragma unroll
-                        for (int c = 0; c < 13; c++) sm.g[sz][c] = 0.0;
-                        continue;
-                    }
-                    const bool clamped = ae > ALPHA_CLAMP;
-                    const double a = clamped ? ALPHA_CLAMP : ae;
-                    const float lgr = mode == 0 ? fast_lg2((float)rc) : 0.f;
-                    const float4 col = sm.col[jj];
-                    const double inv1m = 1.0 / (1.0 - a);
-                    const double tb = T * inv1m;
+                    const int k = kbj.x + (tid >> 4) * kbj.y + (tid & 15);
+                    double a = sm.al[k];
+                    if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
+                    const double tb = T / (1.0 - a);
                     const double w = tb * a;
-                    double g[13];
-                    g[8] = w * d0;
-                    g[9] = w * d1;
-                    g[10] = w * d2;
-                    double ga = d0 * (tb * col.x - S0 * inv1m) + d1 * (tb * col.y - S1 * inv1m) +
-                                d2 * (tb * col.z - S2 * inv1m);
-                    g[12] = 0.0;
+                    BwdSlot& sl = sm.slot[rank(k)];
+                    sl.tb = tb;
+                    sl.s0 = S0;
+                    sl.s1 = S1;
+                    sl.s2 = S2;
+                    sl.k = k;
+                    sl.jp = jj | (tid << 8);
                     if (has_fg) {
                         const double u = fg_dw[fbase + fk];
-                        ga += u * tb - sw * inv1m;
+                        sl.u = u;
+                        sl.sw = sw;
+                        sl.dz = fg_dz[fbase + fk];
                         sw += u * w;
-                        g[12] = fg_dz[fbase + fk];
                         fk--;
                     }
+                    const float4 col = sm.col[jj];
                     S0 = fma(w, (double)col.x, S0);
                     S1 = fma(w, (double)col.y, S1);
                     S2 = fma(w, (double)col.z, S2);
                     T = tb;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- 5. gradients, dense over the np entries' slots ----
+        {
+            const int nslot = rank(sm.S[np]);
+            for (int q0 = (int)warp * 32; q0 < nslot; q0 += 256) {
+                const int q = q0 + (int)lane;
+                const bool act = q < nslot;
+                double g[13];
 #pragma unroll
-                    for (int c = 0; c < 8; c++) g[c] = 0.0;
-                    g[11] = 0.0;
+                for (int c = 0; c < 13; c++) g[c] = 0.0;
+                int jj = -1 - (int)lane;  // unique keys for idle lanes
+                if (act) {
+                    const BwdSlot& sl = sm.slot[q];
+                    jj = sl.jp & 255;
+                    const int pix = sl.jp >> 8;
+                    const int k = sl.k;
+                    const int slot = (bend - 1 - jj) & (RR - 1);
+                    const float4 par = sm.par[jj];  // o, sigma, 1/o, 1/phi_s
+                    const float4 col = sm.col[jj];
+                    const double ae = sm.al[k];
+                    const bool clamped = ae > ALPHA_CLAMP;
+                    const double a = clamped ? ALPHA_CLAMP : ae;
+                    const double inv1m = 1.0 / (1.0 - a);
+                    const double tb = sl.tb;
+                    const double w = tb * a;
+                    const double dd0 = sm.d[0][pix], dd1 = sm.d[1][pix], dd2 = sm.d[2][pix];
+                    g[8] = w * dd0;
+                    g[9] = w * dd1;
+                    g[10] = w * dd2;
+                    double ga = dd0 * (tb * col.x - sl.s0 * inv1m) + dd1 * (tb * col.y - sl.s1 * inv1m) +
+                                dd2 * (tb * col.z - sl.s2 * inv1m);
+                    if (has_fg) {
+                        ga += sl.u * tb - sl.sw * inv1m;
+                        g[12] = sl.dz;
+                    }
                     if (!clamped) {
+                        const float rv = sm.r[k];
+                        const int edge = (int)(__float_as_uint(rv) & 3u);
+                        const EvalRec& er = sm.ev[slot];
+                        const int lx = pix & 15, ly = pix >> 4;
+                        const double pcx = sm.xc[lx], pcy = sm.yc[ly];
+                        // fp64 r of the argmax edge for the chain (phi = r * phi_s)
+                        const double r64 = fma(er.a[3 * edge], pcx, fma(er.a[3 * edge + 1], pcy, er.a[3 * edge + 2]));
                         const double window = a * (double)par.z;
                         g[6] = ga * window;  // d/d opacity = g_alpha * alpha / o
                         const double g_win = (double)par.x * ga;
                         const double phi = r64 * er.phis;
                         double g_phi;
                         if (mode == 0) {
-                            g[7] = g_win * window * ((double)lgr * 0.6931471805599453);
+                            const double rc = fmin(r64, 1.0);
+                            g[7] = g_win * window * ((double)fast_lg2((float)rc) * 0.6931471805599453);
                             const double g_r = g_win * (double)par.y * window / rc;
                             if (r64 >= 1.0) {
                                 g_phi = 0.0;
@@ -398,12 +440,12 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                         const TailRec& tr = sm.tail[slot];
                         const int ib = edge == 2 ? 0 : edge + 1;
                         const double ax = rb.qx[edge], ay = rb.qy[edge], bx = rb.qx[ib], by = rb.qy[ib];
-                        const double pxr = (double)(px - tr.ox) + 0.5, pyr = (double)(py - tr.oy) + 0.5;
-                        const double sl = rb.sl[edge], ul = rb.ul[edge], vl = rb.vl[edge];
-                        const double gax = (g_phi * (sl * (pyr - by) + phi * ul));
-                        const double gay = (g_phi * (sl * (bx - pxr) + phi * vl));
-                        const double gbx = (g_phi * (sl * (ay - pyr) - phi * ul));
-                        const double gby = (g_phi * (sl * (pxr - ax) - phi * vl));
+                        const double pxr = (double)(X0 + lx - tr.ox) + 0.5, pyr = (double)(Y0 + ly - tr.oy) + 0.5;
+                        const double sl_ = rb.sl[edge], ul = rb.ul[edge], vl = rb.vl[edge];
+                        const double gax = g_phi * (sl_ * (pyr - by) + phi * ul);
+                        const double gay = g_phi * (sl_ * (bx - pxr) + phi * vl);
+                        const double gbx = g_phi * (sl_ * (ay - pyr) - phi * ul);
+                        const double gby = g_phi * (sl_ * (pxr - ax) - phi * vl);
                         g[0] = edge == 0 ? gax : (ib == 0 ? gbx : 0.0);
                         g[1] = edge == 0 ? gay : (ib == 0 ? gby : 0.0);
                         g[2] = edge == 1 ? gax : (ib == 1 ? gbx : 0.0);
@@ -411,32 +453,45 @@ __global__ void __launch_bounds__(256, 2) k_blend_bwd_dense(Cam cam, Opts opt, c
                         g[4] = edge == 2 ? gax : (ib == 2 ? gbx : 0.0);
                         g[5] = edge == 2 ? gay : (ib == 2 ? gby : 0.0);
                     }
-                    const int slot_g = sm.wpre[kk >> 5] + __popc(sm.pbits[kk >> 5] & ((1u << (kk & 31)) - 1u));
+                }
+                // segmented reduction (fp32 partials of fp64 terms): slots of one
+                // entry are consecutive, so a lane adds the lanes below it with the
+                // same entry; the first lane of each run ends with the run's sum.
+                // Only as many levels as the longest run needs.
+                float gf[13];
 #pragma unroll
-                    for (int c = 0; c < 13; c++) sm.g[slot_g][c] = g[c];
+                for (int c = 0; c < 13; c++) gf[c] = (float)g[c];
+                const int jprev = __shfl_up_sync(0xffffffffu, jj, 1);
+                const bool head = lane == 0 || jprev != jj;
+                const unsigned heads = __ballot_sync(0xffffffffu, head);
+                const unsigned later = heads & ~((2u << lane) - 1u);
+                const int runlen = head ? (later ? __ffs(later) - 1 : 32) - (int)lane : 0;
+                const int maxrun = __reduce_max_sync(0xffffffffu, runlen);
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    if (off >= maxrun) break;
+                    const int jo = __shfl_down_sync(0xffffffffu, jj, off);
+                    const bool same = (int)lane + off < 32 && jo == jj;
+#pragma unroll
+                    for (int c = 0; c < 13; c++) {
+                        const float v = __shfl_down_sync(0xffffffffu, gf[c], off);
+                        if (same) gf[c] += v;
+                    }
+                }
+                if (act && head) {
+                    double* dst = sgrad + (size_t)sm.srcq[(bend - 1 - jj) & (SR - 1)] * SG_STRIDE;
+#pragma unroll
+                    for (int c = 0; c < 13; c++)
+                        if (gf[c] != 0.f) atomicAdd(dst + c, (double)gf[c]);
                 }
             }
-        }
-        __syncthreads();
-        // ---- 4. flush: per (entry, component) an fp64 sum over the entry's
-        //         contributing pairs in a fixed order, one global atomic ----
-        for (int c = tid; c < np * NC; c += 256) {
-            const int jj = c / NC, comp = c - jj * NC;
-            auto rank = [&](int k) {
-                const int wi = k >> 5;
-                return sm.wpre[wi] + ((k & 31) ? __popc(sm.pbits[wi] & ((1u << (k & 31)) - 1u)) : 0);
-            };
-            const int r0 = rank(sm.S[jj]), r1 = rank(sm.S[jj + 1]);
-            double v = 0.0;
-            for (int q = r0; q < r1; q++) v += sm.g[q][comp];
-            if (v != 0.0) atomicAdd(sgrad + (size_t)sm.srcq[(bend - 1 - jj) & (SR - 1)] * SG_STRIDE + comp, v);
         }
         nb = np;
     }
     cp_async_wait_all();
 }
 
-template <int DB, int PCAP, int GCAP>
+template <int DB, int PCAP, int GCAP, int MINB>
 static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                              const int* tile_start, const unsigned* ent_src, const double* t_final,
                              const int* last_pos, const float* d_image, const int* n_frag,
@@ -445,20 +500,29 @@ static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, c
     const int dyn = (int)sizeof(BwdSmem<DB, PCAP, GCAP>);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_blend_bwd_dense<DB, PCAP, GCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(k_blend_bwd_dense<DB, PCAP, GCAP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         attr = true;
     }
     const int ntiles = cam.ntx * cam.nty;
-    k_blend_bwd_dense<DB, PCAP, GCAP><<<ntiles, 256, dyn, st>>>(cam, opt, rec, recb, tile_start, ent_src, t_final,
-                                                           last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz, sgrad);
+    k_blend_bwd_dense<DB, PCAP, GCAP, MINB><<<ntiles, 256, dyn, st>>>(cam, opt, rec, recb, tile_start, ent_src, t_final,
+                                                                 last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz,
+                                                                 sgrad);
 }
 
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
                             const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
                             const double* fg_dw, const double* fg_dz, double* sgrad, cudaStream_t st) {
-    launch_bwd_dense<64, 2048, 512>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
-                                    frag_off, fg_dw, fg_dz, sgrad, st);
+    static const int variant = [] {
+        const char* v = getenv("TS_BWD_VARIANT");
+        return v ? atoi(v) : 0;
+    }();
+    if (variant == 1)
+        launch_bwd_dense<64, 2048, 512, 2>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
+                                           frag_off, fg_dw, fg_dz, sgrad, st);
+    else  // 3 CTAs per SM
+        launch_bwd_dense<32, 1024, 384, 3>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
+                                           frag_off, fg_dw, fg_dz, sgrad, st);
 }
 
 }  // namespace ts
