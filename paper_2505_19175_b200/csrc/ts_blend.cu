@@ -55,8 +55,8 @@ struct DenseSmem {
     int nb;
 };
 
-template <int DB, int PCAP, bool ACC64, typename PT>
-__global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
+template <int DB, int PCAP, bool ACC64, typename PT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                      const int* __restrict__ tile_start,
                                                      const unsigned* __restrict__ ent_src,
                                                      const PT* __restrict__ opacity,
@@ -352,18 +352,18 @@ __global__ void __launch_bounds__(256) k_blend_dense(Cam cam, Opts opt, const Re
     }
 }
 
-template <int DB, int PCAP, bool ACC64, typename PT>
+template <int DB, int PCAP, bool ACC64, typename PT, int MINB = 1>
 static void launch_dense(const Cam& cam, const Opts& opt, const RecF* rec, const int* tile_start,
                          const unsigned* ent_src, const PT* opacity, const PT* sigma, const FastBlendOut& out,
                          cudaStream_t st) {
     const int dyn = (int)sizeof(DenseSmem<DB, PCAP, ACC64, PT>);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_blend_dense<DB, PCAP, ACC64, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        cudaFuncSetAttribute(k_blend_dense<DB, PCAP, ACC64, PT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         attr = true;
     }
     const int ntiles = cam.ntx * cam.nty;
-    k_blend_dense<DB, PCAP, ACC64, PT><<<ntiles, 256, dyn, st>>>(cam, opt, rec, tile_start, ent_src, opacity, sigma,
+    k_blend_dense<DB, PCAP, ACC64, PT, MINB><<<ntiles, 256, dyn, st>>>(cam, opt, rec, tile_start, ent_src, opacity, sigma,
                                                                   out);
 }
 
@@ -377,8 +377,14 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
     } else {
         const float* o = (const float*)soup.opacity;
         const float* sg = (const float*)soup.sigma;
+        static const int variant = [] {
+            const char* v = getenv("TS_DENSE_VARIANT");
+            return v ? atoi(v) : 0;
+        }();
+        // render: 5 CTAs per SM (48 registers); the training mode keeps 4
         if (acc64) launch_dense<64, 2048, true, float>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 4096, false, float>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else if (variant == 1) launch_dense<64, 2048, false, float, 6>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else launch_dense<64, 4096, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     }
 }
 
