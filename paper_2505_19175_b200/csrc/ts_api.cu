@@ -394,8 +394,11 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     stage_begin(c, TS_STAGE_DEPTH_SORT, st);
     unsigned long long krange = m ? h.key_max - h.key_min : 0ull;
     int kbits = bit_length(krange);
-    int kshift = kbits > 32 ? kbits - 32 : 0;
-    int knb = kbits > 32 ? 32 : kbits;
+    // 24 key bits (3 radix passes) while ties of the reduced key stay rare
+    // (m / 2^24 < 1/4); the exact order inside ties is restored by fix_depth_runs
+    const int kcap = m < (1ll << 22) ? 24 : 32;
+    int kshift = kbits > kcap ? kbits - kcap : 0;
+    int knb = kbits > kcap ? kcap : kbits;
     unsigned* k32 = (unsigned*)c->keys_c;
     unsigned* k32_alt = (unsigned*)c->keys_alt;
     compact_accepted32(n, c->flag, c->key, h.key_min, kshift, k32, c->vals_c, c->sort, st);
