@@ -44,6 +44,7 @@ extern "C" {
 #define TS_ERR_TILE_SIZE -6
 #define TS_ERR_FRAGMENTS -7
 #define TS_ERR_NO_BWD_STATE -8
+#define TS_ERR_CAPACITY -9
 
 /* geometry.py:32-74: intrinsics + world->camera pose x_cam = R x + t */
 typedef struct ts_camera {
@@ -111,10 +112,22 @@ int ts_context_destroy(ts_context* ctx);
 const char* ts_error_string(int code);
 const char* ts_version(void);
 
-/* render(): project, cull, depth-sort, bin, composite.  Synchronizes the
- * stream once (after projection) to size the tile-entry buffers. */
+/* render(): project, cull, depth-sort, bin, composite.  Every stage is sized
+ * from host capacities and the device counters of the projection, so the
+ * whole frame is enqueued without a host round trip; the call then
+ * synchronizes the stream once to fill *result and report non-finite input
+ * (and, if the tile entries outgrew their buffer, redoes binning + blend). */
 int ts_forward(ts_context* ctx, const ts_camera* cam, const ts_options* opt, const ts_soup* soup,
                const ts_forward_out* out, ts_forward_result* result, void* stream);
+
+/* Asynchronous forwards: with ts_set_async(ctx, 1), ts_forward returns after
+ * enqueueing the frame (result fields set to -1, no error report).
+ * ts_forward_status synchronizes the stream, fills *result for the last
+ * forward and returns its status: TS_ERR_NONFINITE (validate=1),
+ * TS_ERR_CAPACITY if its tile entries outgrew the context's buffer (the frame
+ * must be repeated; the next forward allocates enough), else TS_OK. */
+int ts_set_async(ts_context* ctx, int enable);
+int ts_forward_status(ts_context* ctx, ts_forward_result* result, void* stream);
 
 /* render_backward(): gradients of sum(d_image * image_unclipped) w.r.t. all
  * 59 parameters of every triangle, for the scene of the context's last

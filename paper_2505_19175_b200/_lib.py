@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(HERE, "libtrisplat_b200.so")
 TS_OK = 0
 TS_ERR_NONFINITE = -5
 TS_ERR_FRAGMENTS = -7
+TS_ERR_CAPACITY = -9
 TS_DUMP_SORTED_IDX = 1
 TS_DUMP_TILE_START = 2
 TS_DUMP_ENTRY_RANK = 3
@@ -64,7 +65,7 @@ class TsGrads(ctypes.Structure):
 EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_version",
            "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
            "ts_stage_times", "ts_flagged_pixels", "ts_fragment_offsets", "ts_collect_fragments",
-           "ts_backward_fragments"]
+           "ts_backward_fragments", "ts_set_async", "ts_forward_status"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -102,6 +103,10 @@ def load(path: str = LIB_PATH):
     lib.ts_backward_fragments.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, P(TsGrads), ctypes.c_int, ctypes.c_void_p]
     lib.ts_backward_fragments.restype = ctypes.c_int
+    lib.ts_set_async.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.ts_set_async.restype = ctypes.c_int
+    lib.ts_forward_status.argtypes = [ctypes.c_void_p, P(TsForwardResult), ctypes.c_void_p]
+    lib.ts_forward_status.restype = ctypes.c_int
     lib.ts_debug_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                   ctypes.c_size_t, ctypes.c_void_p]
     lib.ts_debug_copy.restype = ctypes.c_int

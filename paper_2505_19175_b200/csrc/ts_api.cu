@@ -13,6 +13,7 @@
 //   onesweep radix sort on tile id (stable)                          <= 3 kernels
 //   tile ranges                                                      1 kernel
 //   blend (fast: fp32 + guard band, then exact fix-up; or exact fp64) 1-2 kernels
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -69,7 +70,9 @@ struct ts_context {
     long long os_cap = -1;
     // counters
     Counters* d_ctr = nullptr;
-    Counters* h_ctr = nullptr;
+    Counters* h_ctr = nullptr;   // readback of the last frame's counters
+    Counters* h_init = nullptr;  // initial counters (never a copy destination: async frames overlap)
+    unsigned* d_sticky = nullptr;  // entry-capacity overflow since the last ts_forward_status
     // last forward
     bool have_fwd = false;
     bool have_bwd_state = false;
@@ -79,9 +82,15 @@ struct ts_context {
     ts_soup soup{};
     int dtype = 0;
     long long n = 0, m = 0, e = 0;
+    long long e_hint = 0;  // largest entry count seen (entry-buffer sizing)
+    long long wcap = 0;    // working entry capacity of the last forward
     const unsigned* sorted_src = nullptr;
     const unsigned* ent_src = nullptr;
     int sgrad_kind = 0;  // 0 none, 1 fp64, 2 fp32
+    // asynchronous forwards (ts_set_async): no host synchronization per frame
+    bool async_mode = false;
+    bool pending = false;
+    bool last_validate = true;
     // stage profiling
     bool profile = false;
     cudaEvent_t ev[TS_NUM_STAGES][2] = {};
@@ -249,6 +258,7 @@ const char* ts_error_string(int code) {
         case TS_ERR_TILE_SIZE: return "only tile_size=16 is supported";
         case TS_ERR_FRAGMENTS: return "fragment gradients do not match this scene/camera";
         case TS_ERR_NO_BWD_STATE: return "the preceding ts_forward ran with keep_backward=0";
+        case TS_ERR_CAPACITY: return "tile-entry capacity exceeded by an asynchronous forward (repeat the frame)";
         default: return "unknown error";
     }
 }
@@ -269,6 +279,15 @@ int ts_context_create(ts_context** out, int device) {
     c->sort.bsums = c->sort.hist + 256 * (size_t)c->sort.max_blocks + 32;
     rc = cuda_err(cudaMalloc(&c->d_ctr, sizeof(Counters)));
     if (!rc) rc = cuda_err(cudaMallocHost(&c->h_ctr, sizeof(Counters)));
+    if (!rc) rc = cuda_err(cudaMallocHost(&c->h_init, sizeof(Counters)));
+    if (!rc) {
+        memset(c->h_init, 0, sizeof(Counters));
+        c->h_init->key_and = ~0ull;
+        c->h_init->key_min = ~0ull;
+        for (int k = 0; k < 4; k++) c->h_init->err[k] = 0x7fffffffffffffffLL;
+    }
+    if (!rc) rc = cuda_err(cudaMalloc(&c->d_sticky, sizeof(unsigned)));
+    if (!rc) rc = cuda_err(cudaMemset(c->d_sticky, 0, sizeof(unsigned)));
     if (rc) {
         delete c;
         return rc;
@@ -287,7 +306,9 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
     cudaFree(c->d_ctr);
+    cudaFree(c->d_sticky);
     cudaFreeHost(c->h_ctr);
+    cudaFreeHost(c->h_init);
     for (int k = 0; k < TS_NUM_STAGES; k++)
         if (c->ev[k][0]) {
             cudaEventDestroy(c->ev[k][0]);
@@ -322,6 +343,105 @@ int ts_stage_times(ts_context* c, float* ms, int n) {
     return TS_OK;
 }
 
+// Binning + blend of the current forward, sized from host capacities and the
+// device counters of the preprocess (no host round trip): depth keys of all n
+// triangles (culled ones sort last), stable radix sort, exact tie order, rank
+// offsets, tile duplication (bounded by cap_e), stable tile sort over the
+// device entry count, tile ranges, blend, fix-up.
+static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_options* opt, const ts_soup* soup,
+                        const ts_forward_out* out, cudaStream_t st) {
+    const bool fast = opt->precision == 0;
+    const long long n = soup->n;
+    const int ntiles = cm.ntx * cm.nty;
+    if (n > 0) {
+        // depth order (np.lexsort((idx, z)), render.py:276): 24-bit range-reduced
+        // keys while ties stay rare (n < 2^22), else 32-bit; exact (z64, idx)
+        // order restored inside runs of equal reduced keys
+        stage_begin(c, TS_STAGE_DEPTH_SORT, st);
+        const int kcap = n < (1ll << 22) ? 24 : 31;
+        unsigned* k32 = (unsigned*)c->keys_c;
+        unsigned* k32_alt = (unsigned*)c->keys_alt;
+        depth_keys(n, c->flag, c->key, c->d_ctr, kcap, k32, c->vals_c, st);
+        int par = onesweep_sort_u32(n, k32, c->vals_c, k32_alt, c->vals_alt, kcap, c->os_buf, st);
+        c->sorted_src = par ? c->vals_alt : c->vals_c;
+        fix_depth_runs(n, par ? k32_alt : k32, (unsigned*)c->sorted_src, c->key, st, (1u << kcap) - 1u);
+        g_launches += 2 + 3 * ((kcap + 7) / 8);
+        stage_end(c, TS_STAGE_DEPTH_SORT, st);
+
+        // tile duplication in rank order + stable sort by tile id (render.py:315-361)
+        stage_begin(c, TS_STAGE_BINNING, st);
+        rank_offsets(n, c->sorted_src, c->tcount, c->offs, nullptr, c->sort, st);
+        // working capacity: the largest entry count seen so far with headroom
+        // (the sort grids follow it); more entries raise the sticky overflow flag
+        const long long wcap = c->e_hint > 0 ? std::min<long long>(c->cap_e, c->e_hint + c->e_hint / 4 + 4096)
+                                             : c->cap_e;
+        duplicate_entries(n, c->sorted_src, c->bbox, c->offs, cm.ntx, c->tkey, c->tval, wcap, c->d_sticky, st);
+        const int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
+        par = onesweep_sort_u32_dev(wcap, &c->d_ctr->e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits,
+                                    c->os_buf, st);
+        const unsigned* skey = par ? c->tkey_alt : c->tkey;
+        c->ent_src = par ? c->tval_alt : c->tval;
+        tile_ranges_dev(wcap, &c->d_ctr->e, skey, ntiles, c->tile_start, st);
+        c->wcap = wcap;
+        g_launches += 5 + 3 * ((tbits + 7) / 8);
+        stage_end(c, TS_STAGE_BINNING, st);
+    } else {
+        c->sorted_src = c->vals_c;
+        c->ent_src = c->tval;
+        TS_CHECK(cudaMemsetAsync(c->tile_start, 0, sizeof(int) * (ntiles + 1), st));
+    }
+
+    if (fast) {
+        FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
+                        c->nfrag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
+                        c->flags, c->d_ctr};
+        stage_begin(c, TS_STAGE_BLEND, st);
+        static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
+        if (legacy)
+            launch_blend_fast(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
+                              c->bbox, c->tile_start, c->ent_src, bo, st);
+        else
+            launch_blend_dense(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
+                               c->tile_start, c->ent_src, bo, st);
+        stage_end(c, TS_STAGE_BLEND, st);
+        stage_begin(c, TS_STAGE_FIXUP, st);
+        launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
+                         bo, st);
+        stage_end(c, TS_STAGE_FIXUP, st);
+        g_launches += 2;
+    } else {
+        BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
+                    c->nfrag, c->t_final, c->last_pos};
+        stage_begin(c, TS_STAGE_BLEND, st);
+        launch_blend_exact(cm, op, (const Rec64*)c->rec64.p, c->tile_start, (const int*)c->ent_src, bo, st);
+        stage_end(c, TS_STAGE_BLEND, st);
+        g_launches += 1;
+    }
+    const long long P = (long long)cm.width * cm.height;
+    if (out->n_frag && P) TS_CHECK(cudaMemcpyAsync(out->n_frag, c->nfrag, 4 * P, cudaMemcpyDeviceToDevice, st));
+    return cuda_err(cudaGetLastError());
+}
+
+// Host view of the counters of the last forward (after the stream has run it):
+// result fields, non-finite report, entry-capacity check.
+static int finish_forward(ts_context* c, ts_forward_result* res, bool validate) {
+    const Counters& h = *c->h_ctr;
+    c->m = (long long)h.m;
+    c->e = (long long)h.e;
+    c->e_hint = std::max(c->e_hint, c->e);
+    if (res) {
+        res->n_visible = (int64_t)h.m;
+        res->n_entries = (int64_t)h.e;
+        res->n_flagged = (int64_t)h.n_flagged;
+        for (int k = 0; k < 4; k++) res->err_index[k] = h.err[k] == 0x7fffffffffffffffLL ? -1 : h.err[k];
+    }
+    if (validate)
+        for (int k = 0; k < 4; k++)
+            if (h.err[k] != 0x7fffffffffffffffLL) return TS_ERR_NONFINITE;
+    if (c->e >= (1ll << 31)) return TS_ERR_INVALID_ARG;
+    return TS_OK;
+}
+
 int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const ts_soup* soup,
                const ts_forward_out* out, ts_forward_result* res, void* stream) {
     if (!c || !cam || !opt || !soup || !out) return TS_ERR_INVALID_ARG;
@@ -350,13 +470,10 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     } else {
         if ((rc = ensure(c->rec64, sizeof(Rec64) * n1))) return rc;
     }
-    Counters init;
-    memset(&init, 0, sizeof(init));
-    init.key_and = ~0ull;
-    init.key_min = ~0ull;
-    for (int k = 0; k < 4; k++) init.err[k] = 0x7fffffffffffffffLL;
-    *c->h_ctr = init;
-    TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_ctr, sizeof(Counters), cudaMemcpyHostToDevice, st));
+    // tile-entry capacity: the last frame's count with headroom, at least 4 per triangle
+    if ((rc = ensure_ent(c, std::max<long long>(4 * n1 + 4096, c->e_hint + c->e_hint / 2)))) return rc;
+    if ((rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1))) return rc;
+    TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_init, sizeof(Counters), cudaMemcpyHostToDevice, st));
     if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
     if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
     stage_begin(c, TS_STAGE_PREPROCESS, st);
@@ -370,93 +487,8 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     }
     stage_end(c, TS_STAGE_PREPROCESS, st);
     g_launches += n > 0 ? 1 : 0;
+    if ((rc = enqueue_tail(c, cm, op, opt, soup, out, st))) return rc;
     TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    TS_CHECK(cudaStreamSynchronize(st));
-    TS_CHECK(cudaGetLastError());
-    const Counters h = *c->h_ctr;
-    if (res) {
-        res->n_visible = (int64_t)h.m;
-        res->n_entries = (int64_t)h.e;
-        res->n_flagged = 0;
-        for (int k = 0; k < 4; k++) res->err_index[k] = h.err[k] == 0x7fffffffffffffffLL ? -1 : h.err[k];
-    }
-    if (opt->validate)
-        for (int k = 0; k < 4; k++)
-            if (h.err[k] != 0x7fffffffffffffffLL) return TS_ERR_NONFINITE;
-    const long long m = (long long)h.m, e = (long long)h.e;
-    if (e >= (1ll << 31)) return TS_ERR_INVALID_ARG;
-    if ((rc = ensure_ent(c, e > 0 ? e : 1))) return rc;
-    if ((rc = ensure_os(c, (m > e ? m : e) + 1))) return rc;
-
-    // depth order: compaction (source order) of range-reduced 32-bit depth
-    // keys, stable onesweep radix sort, then exact (z64, idx) order restored
-    // inside runs of equal reduced keys (np.lexsort((idx, z)), render.py:276)
-    stage_begin(c, TS_STAGE_DEPTH_SORT, st);
-    unsigned long long krange = m ? h.key_max - h.key_min : 0ull;
-    int kbits = bit_length(krange);
-    // 24 key bits (3 radix passes) while ties of the reduced key stay rare
-    // (m / 2^24 < 1/4); the exact order inside ties is restored by fix_depth_runs
-    const int kcap = m < (1ll << 22) ? 24 : 32;
-    int kshift = kbits > kcap ? kbits - kcap : 0;
-    int knb = kbits > kcap ? kcap : kbits;
-    unsigned* k32 = (unsigned*)c->keys_c;
-    unsigned* k32_alt = (unsigned*)c->keys_alt;
-    compact_accepted32(n, c->flag, c->key, h.key_min, kshift, k32, c->vals_c, c->sort, st);
-    g_launches += n > 0 ? 3 : 0;
-    int par = onesweep_sort_u32(m, k32, c->vals_c, k32_alt, c->vals_alt, knb, c->os_buf, st);
-    if (m > 1 && knb > 0) g_launches += 3 * ((knb + 7) / 8);
-    c->sorted_src = par ? c->vals_alt : c->vals_c;
-    if (kshift > 0) {
-        fix_depth_runs(m, par ? k32_alt : k32, (unsigned*)c->sorted_src, c->key, st);
-        g_launches += 1;
-    }
-    stage_end(c, TS_STAGE_DEPTH_SORT, st);
-
-    // tile duplication in rank order + stable sort by tile id (render.py:315-361)
-    stage_begin(c, TS_STAGE_BINNING, st);
-    rank_offsets(m, c->sorted_src, c->tcount, c->offs, nullptr, c->sort, st);
-    duplicate_entries(m, c->sorted_src, c->bbox, c->offs, cm.ntx, c->tkey, c->tval, st);
-    g_launches += m > 0 ? 4 : 0;
-    int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
-    par = onesweep_sort_u32(e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits, c->os_buf, st);
-    if (e > 1 && tbits > 0) g_launches += 3 * ((tbits + 7) / 8);
-    const unsigned* skey = par ? c->tkey_alt : c->tkey;
-    c->ent_src = par ? c->tval_alt : c->tval;
-    tile_ranges(e, skey, ntiles, c->tile_start, st);
-    g_launches += 1;
-    stage_end(c, TS_STAGE_BINNING, st);
-
-    if (fast) {
-        FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
-                        c->nfrag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
-                        c->flags, c->d_ctr};
-        stage_begin(c, TS_STAGE_BLEND, st);
-        static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
-        if (legacy)
-            launch_blend_fast(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
-                              c->bbox, c->tile_start, c->ent_src, bo, st);
-        else
-            launch_blend_dense(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
-                               c->tile_start, c->ent_src, bo, st);
-        stage_end(c, TS_STAGE_BLEND, st);
-        stage_begin(c, TS_STAGE_FIXUP, st);
-        launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
-                         bo, st);
-        stage_end(c, TS_STAGE_FIXUP, st);
-        g_launches += 2;
-        // flagged-pixel count (read back asynchronously; valid after the stream syncs)
-        TS_CHECK(cudaMemcpyAsync(&c->h_ctr->n_flagged, &c->d_ctr->n_flagged, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
-    } else {
-        BlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
-                    c->nfrag, c->t_final, c->last_pos};
-        stage_begin(c, TS_STAGE_BLEND, st);
-        launch_blend_exact(cm, op, (const Rec64*)c->rec64.p, c->tile_start, (const int*)c->ent_src, bo, st);
-        stage_end(c, TS_STAGE_BLEND, st);
-        g_launches += 1;
-    }
-    if (out->n_frag && P) TS_CHECK(cudaMemcpyAsync(out->n_frag, c->nfrag, 4 * P, cudaMemcpyDeviceToDevice, st));
-    TS_CHECK(cudaGetLastError());
     c->have_fwd = true;
     c->have_bwd_state = !fast || opt->keep_backward;
     c->precision = opt->precision;
@@ -465,9 +497,53 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     c->soup = *soup;
     c->dtype = opt->param_dtype;
     c->n = n;
-    c->m = m;
-    c->e = e;
+    c->last_validate = opt->validate != 0;
+    if (c->async_mode) {
+        // the caller checks the frame later with ts_forward_status()
+        c->pending = true;
+        if (res) memset(res, 0xff, sizeof(*res));
+        return TS_OK;
+    }
+    TS_CHECK(cudaStreamSynchronize(st));
+    if (c->h_ctr->e > (unsigned long long)c->wcap) {
+        TS_CHECK(cudaMemsetAsync(c->d_sticky, 0, sizeof(unsigned), st));
+        // more tile entries than the capacity: grow and redo binning + blend
+        const long long e = (long long)c->h_ctr->e;
+        c->e_hint = std::max(c->e_hint, e);
+        if ((rc = ensure_ent(c, e + e / 4 + 4096))) return rc;
+        if ((rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1))) return rc;
+        TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, sizeof(unsigned long long), st));
+        if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
+        if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
+        if ((rc = enqueue_tail(c, cm, op, opt, soup, out, st))) return rc;
+        TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        TS_CHECK(cudaStreamSynchronize(st));
+    }
+    return finish_forward(c, res, opt->validate != 0);
+}
+
+int ts_set_async(ts_context* c, int enable) {
+    if (!c) return TS_ERR_INVALID_ARG;
+    c->async_mode = enable != 0;
     return TS_OK;
+}
+
+int ts_forward_status(ts_context* c, ts_forward_result* res, void* stream) {
+    if (!c) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned sticky = 0;
+    TS_CHECK(cudaMemcpyAsync(&sticky, c->d_sticky, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    TS_CHECK(cudaStreamSynchronize(st));
+    c->pending = false;
+    if (sticky) {
+        TS_CHECK(cudaMemsetAsync(c->d_sticky, 0, sizeof(unsigned), st));
+        finish_forward(c, res, false);
+        // the next forward sizes its entry buffer from the largest count seen
+        c->e_hint = std::max<long long>(c->e_hint, c->e) * 2;
+        return TS_ERR_CAPACITY;
+    }
+    return finish_forward(c, res, c->last_validate);
 }
 
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
@@ -622,7 +698,7 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
             return TS_OK;
         case TS_DUMP_ENTRY_RANK:
             if (bytes < 4 * (size_t)c->e) return TS_ERR_INVALID_ARG;
-            rank_offsets(c->m, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
+            rank_offsets(c->n, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
             entries_to_rank(c->e, c->ent_src, c->rank_of, (int*)dst, st);
             return cuda_err(cudaGetLastError());
         case TS_DUMP_BBOX:

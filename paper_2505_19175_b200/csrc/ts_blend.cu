@@ -372,8 +372,8 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
     if (dtype == 1) {
         const double* o = (const double*)soup.opacity;
         const double* sg = (const double*)soup.sigma;
-        if (acc64) launch_dense<64, 2048, true, double>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 4096, false, double>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        if (acc64) launch_dense<64, 2048, true, double, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else launch_dense<64, 4096, false, double, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     } else {
         const float* o = (const float*)soup.opacity;
         const float* sg = (const float*)soup.sigma;
@@ -381,8 +381,8 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
             const char* v = getenv("TS_DENSE_VARIANT");
             return v ? atoi(v) : 0;
         }();
-        // render: 5 CTAs per SM (48 registers); the training mode keeps 4
-        if (acc64) launch_dense<64, 2048, true, float>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        // render: 5 CTAs per SM (48 registers); training (fp64 compositing): 4 (64 registers)
+        if (acc64) launch_dense<64, 2048, true, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
         else if (variant == 1) launch_dense<64, 2048, false, float, 6>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
         else launch_dense<64, 4096, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     }

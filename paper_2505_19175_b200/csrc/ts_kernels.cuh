@@ -140,9 +140,13 @@ void rank_offsets(long long m, const unsigned* sorted_src, const unsigned* tcoun
                   int* rank_of, const SortScratch& s, cudaStream_t st);
 // tile duplication in depth-rank order: tkey = tile id, tval = source id
 void duplicate_entries(long long m, const unsigned* sorted_src, const short4* bbox, const unsigned* offs,
-                       int ntx, unsigned* tkey, unsigned* tval, cudaStream_t st);
+                       int ntx, unsigned* tkey, unsigned* tval, long long cap, unsigned* overflow,
+                       cudaStream_t st);
 // tile_start[t] = first entry of tile t (CSR), tile_start[ntiles] = E
 void tile_ranges(long long e, const unsigned* tkey, int ntiles, int* tile_start, cudaStream_t st);
+// same with the entry count read on the device (min(cap, *de))
+void tile_ranges_dev(long long cap, const unsigned long long* de, const unsigned* tkey, int ntiles, int* tile_start,
+                     cudaStream_t st);
 // entry_rank[pos] = rank_of[ent_src[pos]]
 void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out,
                      cudaStream_t st);
@@ -152,11 +156,17 @@ void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st);
 size_t onesweep_scratch_bytes(long long max_count, int max_passes);
 int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
                       unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
+// count = min(cap, *dcount), read on the device
+int onesweep_sort_u32_dev(long long cap, const unsigned long long* dcount, unsigned* keys, unsigned* vals,
+                          unsigned* keys_alt, unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
+// depth keys of all n triangles (culled -> 2^kbits_cap - 1), reduction from the counters
+void depth_keys(long long n, const unsigned* flag, const unsigned long long* key, const Counters* ctr, int kbits_cap,
+                unsigned* k32, unsigned* vals, cudaStream_t st);
 void compact_accepted32(long long n, const unsigned* flag, const unsigned long long* key,
                         unsigned long long kmin, int shift, unsigned* keys_c, unsigned* vals_c,
                         const SortScratch& s, cudaStream_t st);
 void fix_depth_runs(long long m, const unsigned* k32, unsigned* vals, const unsigned long long* key64,
-                    cudaStream_t st);
+                    cudaStream_t st, unsigned skip_key = 0xffffffffu);
 
 // CSR offsets (n+1, int64) from int32 counts; scratch from count_scan_scratch_bytes
 size_t count_scan_scratch_bytes(long long n);

@@ -267,7 +267,7 @@ int radix_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* ke
 __global__ void __launch_bounds__(256) k_duplicate(long long m, const unsigned* __restrict__ sorted_src,
                                                    const short4* __restrict__ bbox, const unsigned* __restrict__ offs,
                                                    int ntx, unsigned* __restrict__ tkey,
-                                                   unsigned* __restrict__ tval) {
+                                                   unsigned* __restrict__ tval, long long cap, unsigned* overflow) {
     long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     unsigned src = sorted_src[k];
@@ -278,20 +278,32 @@ __global__ void __launch_bounds__(256) k_duplicate(long long m, const unsigned* 
     unsigned pos = offs[k];
     for (int ty = ty0; ty < ty1; ty++)
         for (int tx = tx0; tx < tx1; tx++) {
-            tkey[pos] = (unsigned)(ty * ntx + tx);
-            tval[pos] = src;
+            if (pos < cap) {
+                tkey[pos] = (unsigned)(ty * ntx + tx);
+                tval[pos] = src;
+            } else if (overflow) {
+                *overflow = 1u;  // sticky until ts_forward_status
+            }
             pos++;
         }
 }
 
 void duplicate_entries(long long m, const unsigned* sorted_src, const short4* bbox, const unsigned* offs,
-                       int ntx, unsigned* tkey, unsigned* tval, cudaStream_t st) {
+                       int ntx, unsigned* tkey, unsigned* tval, long long cap, unsigned* overflow,
+                       cudaStream_t st) {
     if (m <= 0) return;
-    k_duplicate<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, sorted_src, bbox, offs, ntx, tkey, tval);
+    k_duplicate<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, sorted_src, bbox, offs, ntx, tkey, tval, cap,
+                                                              overflow);
 }
 
-__global__ void k_ranges(long long e, const unsigned* __restrict__ tkey, int ntiles, int* __restrict__ start) {
+__global__ void k_ranges(long long e, const unsigned long long* de, const unsigned* __restrict__ tkey, int ntiles,
+                         int* __restrict__ start) {
+    if (de) e = min(e, (long long)*de);
     long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e <= 0) {
+        if (pos <= ntiles) start[pos] = 0;
+        return;
+    }
     if (pos >= e) return;
     int k = (int)tkey[pos];
     int kp = pos > 0 ? (int)tkey[pos - 1] : -1;
@@ -301,11 +313,13 @@ __global__ void k_ranges(long long e, const unsigned* __restrict__ tkey, int nti
 }
 
 void tile_ranges(long long e, const unsigned* tkey, int ntiles, int* tile_start, cudaStream_t st) {
-    if (e <= 0) {
-        cudaMemsetAsync(tile_start, 0, sizeof(int) * (ntiles + 1), st);
-        return;
-    }
-    k_ranges<<<(unsigned)((e + 255) / 256), 256, 0, st>>>(e, tkey, ntiles, tile_start);
+    tile_ranges_dev(e, nullptr, tkey, ntiles, tile_start, st);
+}
+
+void tile_ranges_dev(long long cap, const unsigned long long* de, const unsigned* tkey, int ntiles, int* tile_start,
+                     cudaStream_t st) {
+    const long long g = (cap > ntiles + 1 ? cap : ntiles + 1);
+    k_ranges<<<(unsigned)((g + 255) / 256), 256, 0, st>>>(cap, de, tkey, ntiles, tile_start);
 }
 
 __global__ void k_entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, int* out) {
@@ -353,8 +367,11 @@ size_t onesweep_scratch_bytes(long long max_count, int max_passes) {
 }
 
 // per-tile digit counts of one pass, digit-major: cnt[d * tiles + tile]
-__global__ void __launch_bounds__(OS_THREADS) k_os_count(long long count, const unsigned* __restrict__ keys,
+__global__ void __launch_bounds__(OS_THREADS) k_os_count(long long count, const unsigned long long* dcount,
+                                                         const unsigned* __restrict__ keys,
                                                          int shift, unsigned* __restrict__ cnt, int tiles) {
+    if (dcount) count = min(count, (long long)*dcount);
+    if ((long long)blockIdx.x * OS_TILE >= count) return;
     __shared__ unsigned s_h[RADIX];
     s_h[threadIdx.x] = 0;
     __syncthreads();
@@ -382,9 +399,12 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_count(long long count, const 
 }
 
 // per digit (one block each): exclusive scan over tiles in place; tot[d] = column total
-__global__ void __launch_bounds__(1024) k_os_scan(unsigned* __restrict__ cnt, int tiles, unsigned* __restrict__ tot) {
+__global__ void __launch_bounds__(1024) k_os_scan(unsigned* __restrict__ cnt, int stride, long long count,
+                                                  const unsigned long long* dcount, unsigned* __restrict__ tot) {
     __shared__ unsigned s_w[32];
-    unsigned* row = cnt + (size_t)blockIdx.x * tiles;
+    if (dcount) count = min(count, (long long)*dcount);
+    const int tiles = (int)((count + OS_TILE - 1) / OS_TILE);
+    unsigned* row = cnt + (size_t)blockIdx.x * stride;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned carry = 0;
     for (int b0 = 0; b0 < tiles; b0 += 1024) {
@@ -419,7 +439,8 @@ __global__ void __launch_bounds__(1024) k_os_scan(unsigned* __restrict__ cnt, in
 // Stable scatter of one 8-bit pass: items are ranked with warp match +
 // per-warp counters, staged in shared memory in tile-local sorted order and
 // written out in coalesced runs at cnt_scanned[d][tile] + global digit start.
-__global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, const unsigned* __restrict__ kin,
+__global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, const unsigned long long* dcount,
+                                                           const unsigned* __restrict__ kin,
                                                            const unsigned* __restrict__ vin,
                                                            unsigned* __restrict__ kout, unsigned* __restrict__ vout,
                                                            int shift, const unsigned* __restrict__ cnt, int tiles,
@@ -429,6 +450,8 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, cons
     __shared__ unsigned s_gbase[RADIX];
     __shared__ unsigned s_k[OS_TILE];
     __shared__ unsigned s_v[OS_TILE];
+    if (dcount) count = min(count, (long long)*dcount);
+    if ((long long)blockIdx.x * OS_TILE >= count) return;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned tile = blockIdx.x;
     for (int w = 0; w < OS_THREADS / 32; w++) s_wc[w][threadIdx.x] = 0;
@@ -494,6 +517,13 @@ __global__ void __launch_bounds__(OS_THREADS) k_os_scatter(long long count, cons
 // Sorts (keys, vals) by bits [0, nbits).  Returns 1 if the result is in the alt buffers.
 int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
                       unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st) {
+    return onesweep_sort_u32_dev(count, nullptr, keys, vals, keys_alt, vals_alt, nbits, scratch, st);
+}
+
+// count = min(cap, *dcount) when dcount is given (read on the device: no host sync)
+int onesweep_sort_u32_dev(long long cap, const unsigned long long* dcount, unsigned* keys, unsigned* vals,
+                          unsigned* keys_alt, unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st) {
+    const long long count = cap;
     if (count <= 1 || nbits <= 0) return 0;
     int npass = (nbits + 7) / 8;
     const int tiles = (int)((count + OS_TILE - 1) / OS_TILE);
@@ -502,9 +532,9 @@ int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned*
     unsigned *kin = keys, *vin = vals, *kout = keys_alt, *vout = vals_alt;
     int parity = 0;
     for (int p = 0; p < npass; p++) {
-        k_os_count<<<tiles, OS_THREADS, 0, st>>>(count, kin, 8 * p, cnt, tiles);
-        k_os_scan<<<RADIX, 1024, 0, st>>>(cnt, tiles, tot);
-        k_os_scatter<<<tiles, OS_THREADS, 0, st>>>(count, kin, vin, kout, vout, 8 * p, cnt, tiles, tot);
+        k_os_count<<<tiles, OS_THREADS, 0, st>>>(count, dcount, kin, 8 * p, cnt, tiles);
+        k_os_scan<<<RADIX, 1024, 0, st>>>(cnt, tiles, count, dcount, tot);
+        k_os_scatter<<<tiles, OS_THREADS, 0, st>>>(count, dcount, kin, vin, kout, vout, 8 * p, cnt, tiles, tot);
         unsigned* t = kin; kin = kout; kout = t;
         t = vin; vin = vout; vout = t;
         parity ^= 1;
@@ -538,13 +568,45 @@ void compact_accepted32(long long n, const unsigned* flag, const unsigned long l
     scan_functor(n, CompactKey32F{flag, key, kmin, shift, keys_c, vals_c}, s, st);
 }
 
+// Depth keys of all n triangles without compaction: accepted triangles get
+// their range-reduced key, clamped below kmax_key; culled ones get kmax_key and
+// therefore sort after every accepted triangle (stable: source order within).
+// The reduction (key_min, shift) comes from the preprocess counters on the
+// device, so the sort is enqueued without a host round trip.
+__global__ void k_depth_keys(long long n, const unsigned* __restrict__ flag, const unsigned long long* __restrict__ key,
+                             const Counters* __restrict__ ctr, int kbits_cap, unsigned* __restrict__ k32,
+                             unsigned* __restrict__ vals) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned kmax_key = (1u << kbits_cap) - 1u;
+    const unsigned long long kmin = ctr->key_min;
+    const unsigned long long range = ctr->m ? ctr->key_max - kmin : 0ull;
+    const int kb = range ? 64 - __clzll((long long)range) : 0;
+    const int shift = kb > kbits_cap ? kb - kbits_cap : 0;
+    unsigned v = kmax_key;
+    if (flag[i]) {
+        const unsigned long long r = (key[i] - kmin) >> shift;
+        v = r < kmax_key ? (unsigned)r : kmax_key - 1u;
+    }
+    k32[i] = v;
+    vals[i] = (unsigned)i;
+}
+
+void depth_keys(long long n, const unsigned* flag, const unsigned long long* key, const Counters* ctr, int kbits_cap,
+                unsigned* k32, unsigned* vals, cudaStream_t st) {
+    if (n <= 0) return;
+    k_depth_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, flag, key, ctr, kbits_cap, k32, vals);
+}
+
 // Restore exact order inside runs of equal reduced keys: insertion sort on
 // (key64[src], src) -- runs are short in practice and already in src order.
+// Keys >= skip_key (culled triangles) are left alone.
 __global__ void k_fix_runs(long long m, const unsigned* __restrict__ k32, unsigned* __restrict__ vals,
-                           const unsigned long long* __restrict__ key64) {
+                           const unsigned long long* __restrict__ key64, unsigned skip_key) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= m) return;
     unsigned k = k32[p];
+    if (k >= skip_key) return;
     if (p > 0 && k32[p - 1] == k) return;
     if (p + 1 >= m || k32[p + 1] != k) return;
     long long end = p + 1;
@@ -565,9 +627,9 @@ __global__ void k_fix_runs(long long m, const unsigned* __restrict__ k32, unsign
 }
 
 void fix_depth_runs(long long m, const unsigned* k32, unsigned* vals, const unsigned long long* key64,
-                    cudaStream_t st) {
+                    cudaStream_t st, unsigned skip_key) {
     if (m <= 1) return;
-    k_fix_runs<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, k32, vals, key64);
+    k_fix_runs<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, k32, vals, key64, skip_key);
 }
 
 

@@ -204,6 +204,27 @@ class Rasterizer:
         """Record CUDA events around every pipeline stage (on the call's stream)."""
         _lib.check(self.lib.ts_profile(self._ctx, int(bool(enable))), "profile")
 
+    def set_async(self, enable: bool = True):
+        """Asynchronous forwards: forward() enqueues the frame and returns without
+        waiting for the GPU (ForwardResult counts are then -1); status() waits and
+        reports the last frame."""
+        _lib.check(self.lib.ts_set_async(self._ctx, int(bool(enable))), "set_async")
+
+    def status(self, stream=None) -> dict:
+        """Wait for the last forward and return its counts; raises on non-finite
+        input or if an asynchronous frame outgrew the tile-entry buffer (repeat it)."""
+        res = _lib.TsForwardResult()
+        dev = torch.device("cuda", self.device)
+        st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+        rc = self.lib.ts_forward_status(self._ctx, ctypes.byref(res), ctypes.c_void_p(st))
+        if rc == _lib.TS_ERR_NONFINITE:
+            for g, idx in zip(_NONFINITE_GROUPS, res.err_index):
+                if idx >= 0:
+                    raise ValueError(f"non-finite {g} in triangle {int(idx)}")
+        _lib.check(rc, "forward_status")
+        return {"n_visible": int(res.n_visible), "n_entries": int(res.n_entries),
+                "n_flagged": int(res.n_flagged)}
+
     def flagged_pixels(self) -> int:
         """Pixels of the last fast forward re-resolved by the exact fix-up."""
         torch.cuda.synchronize()
