@@ -281,3 +281,34 @@ def test_view_parallel_step_matches_sum_of_oracle_views(rast):
     parts = [(0, 9 * n), (9 * n, 10 * n), (10 * n, 11 * n), (11 * n, 59 * n)]
     for lo, hi in parts:
         assert rel_err(g[lo:hi], want[lo:hi]) < GRAD_RTOL
+
+
+def test_entry_capacity_redo_and_async_status(rast):
+    """Tile entries beyond the context's working capacity: a synchronous
+    forward redoes binning + blend with a larger buffer (results still match
+    the oracle); an asynchronous forward raises the sticky overflow flag, which
+    status() reports so the frame can be repeated."""
+    from oracle import oracle as O
+    from paper_2505_19175_b200 import scenes
+    from paper_2505_19175_b200.rasterizer import Rasterizer
+    small = scenes.make_soup(200, seed=21, size=0.02, sigma=(1.0, 1.0))
+    big = scenes.make_soup(200, seed=22, size=1.5, sigma=(1.0, 1.0))
+    intr, pose = scenes.frontal_camera(256, 256, 300.0)
+    r = Rasterizer()
+    r.forward(_dev(small), intr, pose)          # sizes the working capacity on a tiny frame
+    f = r.forward(_dev(big), intr, pose, debug=True)
+    ref = O.render(big, intr, pose)
+    assert f.n_entries > 4 * 200 + 4096
+    assert np.array_equal(_np(f.last_src), ref.last_src)
+    assert np.abs(_np(f.image) - ref.image).max() <= RGB_TOL
+    r2 = Rasterizer()
+    r2.forward(_dev(small), intr, pose)
+    r2.set_async(True)
+    r2.forward(_dev(big), intr, pose)
+    with pytest.raises(RuntimeError, match="capacity"):
+        r2.status()
+    f2 = r2.forward(_dev(big), intr, pose, debug=True)  # repeated frame: buffers now large enough
+    st = r2.status()
+    r2.set_async(False)
+    assert st["n_entries"] == f.n_entries
+    assert np.array_equal(_np(f2.last_src), ref.last_src)
