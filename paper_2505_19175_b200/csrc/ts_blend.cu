@@ -46,6 +46,8 @@ struct DenseSmem {
     float4 col[DB];                // rgb, f0
     float f1[DB];
     int S[DB + 1];                 // first pair of entry j
+    unsigned starts[PCAP / 32];    // bit (k & 31) of word k >> 5: an entry starts at pair k
+    int jfirst[PCAP / 32];         // entry holding pair 32 w
     unsigned geo[DB];              // cx0 | cy0<<4 | w<<8 | magic<<16
     int2 kb[DB];                   // pair of pixel (lx, ly) = x + ly * y + lx
     double2 osj[ACC64 ? DB : 1];   // (opacity, sigma) of batch entry j
@@ -180,6 +182,19 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 sm.geo[j] = (unsigned)cx0[hf] | ((unsigned)cy0[hf] << 4) | ((unsigned)w[hf] << 8) | (magic << 16);
                 sm.kb[j] = make_int2(excl - cy0[hf] * w[hf] - cx0[hf], w[hf]);
             }
+            // pair-word tables of the batch (entries < n): entry starts and the
+            // entry holding the first pair of every 32-pair word
+            for (int w = (int)lane; w < PCAP / 32; w += 32) sm.starts[w] = 0u;
+            __syncwarp();
+#pragma unroll
+            for (int hf = 0; hf < NW; hf++) {
+                const int jq = (int)lane + 32 * hf;
+                if (jq < n) {
+                    const int excl = incl[hf] - w[hf] * h[hf];
+                    atomicOr(&sm.starts[excl >> 5], 1u << (excl & 31));
+                    for (int wq = (excl + 31) >> 5; wq <= ((incl[hf] - 1) >> 5); wq++) sm.jfirst[wq] = jq;
+                }
+            }
             if (lane == 0) {
                 sm.S[0] = 0;
                 sm.nb = n;
@@ -200,16 +215,11 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             const int chunk = ((total + 255) >> 8) << 5;
             const int k0 = (int)warp * chunk;
             const int kE = min(k0 + chunk, total);
-            int jb = 0;
-            if (k0 < kE) {
-#pragma unroll
-                for (int step = DB / 2; step > 0; step >>= 1)
-                    if (jb + step < nb && sm.S[jb + step] <= k0) jb += step;
-            }
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
-                int sj;
-                const int j = pair_step_entry(sm.S, nb, kb, jb, sj);
+                // entry of pair k: the word's first entry plus the entry starts in (kb, k]
+                const int j = sm.jfirst[kb >> 5] + __popc(sm.starts[kb >> 5] & ((2u << lane) - 2u));
+                const int sj = sm.S[j];
                 if (k < kE) {
                     const unsigned g = sm.geo[j];
                     const int w = (g >> 8) & 31;

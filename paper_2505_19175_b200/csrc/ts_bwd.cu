@@ -56,6 +56,8 @@ struct BwdSmem {
     float4 col[DB];              // rgb, f0
     float4 par[DB];              // opacity, sigma, 1/opacity, 1/phi_s
     int S[DB + 1];
+    unsigned starts[PCAP / 32];  // bit (k & 31) of word k >> 5: an entry starts at pair k
+    int jfirst[PCAP / 32];       // entry holding pair 32 w
     unsigned geo[DB];
     int2 kb[DB];
     unsigned pbits[PCAP / 32];   // pair k composited
@@ -218,6 +220,19 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                 sm.geo[jj] = (unsigned)cx0[hf] | ((unsigned)cy0[hf] << 4) | ((unsigned)w[hf] << 8) | (magic << 16);
                 sm.kb[jj] = make_int2(excl - cy0[hf] * w[hf] - cx0[hf], w[hf]);
             }
+            // pair-word tables of the batch (entries < n): entry starts and the
+            // entry holding the first pair of every 32-pair word
+            for (int w = (int)lane; w < PCAP / 32; w += 32) sm.starts[w] = 0u;
+            __syncwarp();
+#pragma unroll
+            for (int hf = 0; hf < NW; hf++) {
+                const int jq = (int)lane + 32 * hf;
+                if (jq < n) {
+                    const int excl = incl[hf] - w[hf] * h[hf];
+                    atomicOr(&sm.starts[excl >> 5], 1u << (excl & 31));
+                    for (int wq = (excl + 31) >> 5; wq <= ((incl[hf] - 1) >> 5); wq++) sm.jfirst[wq] = jq;
+                }
+            }
             if (lane == 0) {
                 sm.S[0] = 0;
                 sm.nb = n;
@@ -237,17 +252,12 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
             const int chunk = ((total + 255) >> 8) << 5;
             const int k0 = (int)warp * chunk;
             const int kE = min(k0 + chunk, total);
-            int jb = 0;
-            if (k0 < kE) {
-#pragma unroll
-                for (int step = DB / 2; step > 0; step >>= 1)
-                    if (jb + step < nb && sm.S[jb + step] <= k0) jb += step;
-            }
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
                 bool comp = false;
-                int sj;
-                const int jj = pair_step_entry(sm.S, nb, kb, jb, sj);
+                // entry of pair k: the word's first entry plus the entry starts in (kb, k]
+                const int jj = sm.jfirst[kb >> 5] + __popc(sm.starts[kb >> 5] & ((2u << lane) - 2u));
+                const int sj = sm.S[jj];
                 if (k < kE) {
                     const unsigned g = sm.geo[jj];
                     const int w = (g >> 8) & 31;

@@ -377,25 +377,5 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// Dense pair walk of the blend kernels: a warp steps through a batch's pair
-// range 32 pairs at a time (lane l takes pair kb + l).  S[j] is the first
-// pair of entry j (S[nb] = total), jb the entry holding pair kb (warp
-// uniform; advanced to the entry holding kb + 32).  Returns the lane's entry
-// and its first pair, without per-lane search loops.
-__device__ __forceinline__ int pair_step_entry(const int* S, int nb, int kb, int& jb, int& sj_out) {
-    const unsigned lane = threadIdx.x & 31;
-    const int jn = min(jb + 1 + (int)lane, nb);
-    const int st = S[jn];
-    const int off = st - kb;
-    const bool real = jn < nb;
-    const unsigned bits = __reduce_or_sync(0xffffffffu, (real && off >= 1 && off <= 31) ? (1u << off) : 0u);
-    const int d = __popc(bits & ((2u << lane) - 1u));
-    const int sjb = S[jb];
-    const int sshf = __shfl_sync(0xffffffffu, st, (d + 31) & 31);
-    sj_out = d == 0 ? sjb : sshf;
-    const int j = jb + d;
-    jb += __popc(__ballot_sync(0xffffffffu, real && off >= 1 && off <= 32));
-    return j;
-}
 
 }  // namespace ts
