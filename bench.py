@@ -364,8 +364,9 @@ def main():
                    "guard_band_pixels": flagged},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "roofline": {"bound": "hbm", "kernel": "k_blend", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_for("k_blend"),
+        "roofline": {"bound": "hbm", "kernel": "k_blend_dense (+ k_fixup_fwd)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic_for("k_blend_dense"),
                      "bytes_per_launch": bbytes, "avg_ms": blend_avg, "peak_source": peak_src},
         "cpu_baseline": cpu,
         "stages_ms": stages,
