@@ -178,6 +178,9 @@ int ts_backward_fragments(ts_context* ctx, const float* d_image, const int64_t* 
 #define TS_DUMP_BBOX 4
 #define TS_DUMP_DEPTH 5
 #define TS_DUMP_SGRAD 6
+/*  TS_DUMP_FRAGREC uint64 count, then count x 48-byte fragment records of the
+ *                  last training forward (T, C[3] fp64; pixel, source, ordinal u32) */
+#define TS_DUMP_FRAGREC 7
 int ts_debug_copy(ts_context* ctx, int what, void* dst, size_t bytes, void* stream);
 
 /* Per-stage device timing with CUDA events recorded on the call's stream.

@@ -22,6 +22,7 @@ TS_DUMP_ENTRY_RANK = 3
 TS_DUMP_BBOX = 4
 TS_DUMP_DEPTH = 5
 TS_DUMP_SGRAD = 6
+TS_DUMP_FRAGREC = 7
 
 
 class TsCamera(ctypes.Structure):

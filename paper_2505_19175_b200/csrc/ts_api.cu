@@ -50,6 +50,9 @@ struct ts_context {
     short4* bbox = nullptr;
     DevBuf rec64, recf, recb, sg64, sg32;
     DevBuf frag_off, cs_scratch;  // expected fragment CSR offsets + scan scratch
+    DevBuf frec, ctot;            // training forward: fragment records + final unclipped colour
+    unsigned long long frec_cap = 0;
+    bool frec_ready = false;      // the last forward wrote fragment records
     // per-entry scratch
     long long cap_e = -1;
     void* ent_buf = nullptr;
@@ -301,7 +304,8 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->tri_buf);
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
-    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch})
+    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
+                      &c->ctot})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
@@ -395,6 +399,12 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
         FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
                         c->nfrag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
                         c->flags, c->d_ctr};
+        static const bool no_stream = getenv("TS_BWD_TILES") != nullptr;
+        if (opt->keep_backward && !no_stream && c->frec.p) {
+            bo.frec = (FragRec*)c->frec.p;
+            bo.frec_cap = c->frec_cap;
+            bo.c_total64 = (double*)c->ctot.p;
+        }
         stage_begin(c, TS_STAGE_BLEND, st);
         static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
         if (legacy)
@@ -473,6 +483,14 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     // tile-entry capacity: the last frame's count with headroom, at least 4 per triangle
     if ((rc = ensure_ent(c, std::max<long long>(4 * n1 + 4096, c->e_hint + c->e_hint / 2)))) return rc;
     if ((rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1))) return rc;
+    c->frec_ready = false;
+    if (fast && opt->keep_backward) {
+        // fragment records of the training forward (~6.5 per tile entry here)
+        const long long want = std::max<long long>(8 * std::max<long long>(c->e_hint, n1), 1ll << 20);
+        if ((rc = ensure(c->frec, sizeof(FragRec) * (size_t)want))) return rc;
+        c->frec_cap = c->frec.bytes / sizeof(FragRec);
+        if ((rc = ensure(c->ctot, sizeof(double) * 3 * (size_t)P))) return rc;
+    }
     TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_init, sizeof(Counters), cudaMemcpyHostToDevice, st));
     if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
     if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
@@ -491,6 +509,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     c->have_fwd = true;
     c->have_bwd_state = !fast || opt->keep_backward;
+    c->frec_ready = fast && opt->keep_backward && getenv("TS_BWD_TILES") == nullptr;
     c->precision = opt->precision;
     c->cam = cm;
     c->opt = op;
@@ -512,7 +531,8 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         c->e_hint = std::max(c->e_hint, e);
         if ((rc = ensure_ent(c, e + e / 4 + 4096))) return rc;
         if ((rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1))) return rc;
-        TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, sizeof(unsigned long long), st));
+        // n_flagged, n_frec, frec_over
+        TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, 3 * sizeof(unsigned long long), st));
         if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
         if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
         if ((rc = enqueue_tail(c, cm, op, opt, soup, out, st))) return rc;
@@ -650,14 +670,23 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
         if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
         static const bool bwd_legacy = getenv("TS_BWD_LEGACY") != nullptr;
-        if (bwd_legacy && !frag_off)
+        if (c->frec_ready && !frag_off && !bwd_legacy) {
+            // streaming backward over the forward's fragment records; the tile
+            // backward runs instead only if the record buffer overflowed
+            launch_bwd_stream(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
+                              (const FragRec*)c->frec.p, c->d_ctr, c->frec_cap, (const double*)c->ctot.p, d_image,
+                              sg, st);
+            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, c->tile_start,
+                                   c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, nullptr, nullptr, nullptr,
+                                   &c->d_ctr->frec_over, sg, st);
+        } else if (bwd_legacy && !frag_off)
             launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
                                   (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
                                   d_image, sg, st);
         else
             launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, c->tile_start,
                                    c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
-                                   sg, st);
+                                   nullptr, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
         if (!launch_chain_bwd_fast(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st))
@@ -728,6 +757,21 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
                 free(h32);
                 free(h64);
             }
+            return TS_OK;
+        }
+        case TS_DUMP_FRAGREC: {
+            // fragment records of the last training forward (48 B each, count first)
+            unsigned long long nrec = 0;
+            TS_CHECK(cudaMemcpyAsync(&nrec, &c->d_ctr->n_frec, sizeof(nrec), cudaMemcpyDeviceToHost, st));
+            TS_CHECK(cudaStreamSynchronize(st));
+            if (!c->frec_ready) nrec = 0;
+            nrec = std::min<unsigned long long>(nrec, c->frec_cap);
+            if (bytes < 8 + sizeof(FragRec) * nrec) return TS_ERR_INVALID_ARG;
+            TS_CHECK(cudaMemcpyAsync(dst, &nrec, 8, cudaMemcpyHostToDevice, st));
+            if (nrec)
+                TS_CHECK(cudaMemcpyAsync((char*)dst + 8, c->frec.p, sizeof(FragRec) * nrec, cudaMemcpyDeviceToDevice,
+                                         st));
+            TS_CHECK(cudaStreamSynchronize(st));
             return TS_OK;
         }
         default:

@@ -51,6 +51,9 @@ struct DenseSmem {
     unsigned geo[DB];              // cx0 | cy0<<4 | w<<8 | magic<<16
     int2 kb[DB];                   // pair of pixel (lx, ly) = x + ly * y + lx
     double2 osj[ACC64 ? DB : 1];   // (opacity, sigma) of batch entry j
+    unsigned pbits[ACC64 ? PCAP / 32 : 1];      // training: pair k passes (record slots)
+    int wpre[ACC64 ? PCAP / 32 + 1 : 1];        // passing pairs before word w
+    unsigned long long rbase;                   // first record of the batch (~0: none)
     unsigned maxw[DB];
     int pix[DB];
     double xc[TILE], yc[TILE];     // pixel centres of the tile (fp64)
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             const int kE = min(k0 + chunk, total);
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
+                bool pass = false;
                 // entry of pair k: the word's first entry plus the entry starts in (kb, k]
                 const int j = sm.jfirst[kb >> 5] + __popc(sm.starts[kb >> 5] & ((2u << lane) - 2u));
                 const int sj = sm.S[j];
@@ -234,15 +238,73 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                     const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
                     const double m01 = l0 < l1 ? l0 : l1;
                     const double rr = m01 < l2 ? m01 : l2;
-                    if (rr >= r.r_lo) {
+                    pass = rr >= r.r_lo;
+                    if (pass) {
                         sm.r[k] = rr > r.r_hi ? (Real)rr : (Real)__int_as_float(0x7fc00000);
                         atomicOr(&sm.mask[j >> 5][qy * TILE + qx], 1u << (j & 31));
                     }
                 }
+                if constexpr (ACC64) {
+                    const unsigned pb = __ballot_sync(0xffffffffu, pass);
+                    if (lane == 0) sm.pbits[kb >> 5] = pb;
+                }
             }
         }
         __syncthreads();
+        if constexpr (ACC64) {
+            // record slots of the batch: passing pairs in entry-major order
+            if (out.frec) {
+                if (warp == 0) {
+                    const int total = sm.S[nb];
+                    const int nwd = (total + 31) >> 5;
+                    int carry = 0;
+                    for (int w0 = 0; w0 < nwd; w0 += 32) {
+                        const int wi = w0 + (int)lane;
+                        const int c = wi < nwd ? __popc(sm.pbits[wi]) : 0;
+                        int incl = c;
+#pragma unroll
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                            if ((int)lane >= off) incl += y;
+                        }
+                        if (wi < nwd) sm.wpre[wi] = incl - c + carry;
+                        carry += __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                    if (lane == 0) {
+                        unsigned long long base = atomicAdd(&out.ctr->n_frec, (unsigned long long)carry);
+                        if (base + carry > out.frec_cap) {
+                            out.ctr->frec_over = 1ull;
+                            base = ~0ull;
+                        }
+                        sm.rbase = base;
+                    }
+                }
+                __syncthreads();
+            }
+        }
         // ---- 3. composite: thread = pixel, passing entries in depth order ----
+        unsigned long long rb = ~0ull;
+        if constexpr (ACC64) {
+            if (out.frec) {
+                rb = sm.rbase;
+                if (rb != ~0ull) {
+                    // every passing pair of the pixel starts as a hole; composited
+                    // fragments overwrite theirs below (same thread, program order)
+#pragma unroll
+                    for (int wd = 0; wd < NW; wd++) {
+                        unsigned m = sm.mask[wd][tid];
+                        while (m) {
+                            const int j = wd * 32 + __ffs(m) - 1;
+                            m &= m - 1;
+                            const int2 kbh = sm.kb[j];
+                            const int kh = kbh.x + ly * kbh.y + lx;
+                            const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
+                            out.frec[rb + slot].pix = ~0u;
+                        }
+                    }
+                }
+            }
+        }
         if (!done) {
 #pragma unroll
             for (int wd = 0; wd < NW; wd++) {
@@ -279,6 +341,14 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                             flag_pos = b + j;
                             done = true;
                             break;
+                        }
+                        if (rb != ~0ull) {
+                            const int kr = kb.x + ly * kb.y + lx;
+                            const int slot = sm.wpre[kr >> 5] + __popc(sm.pbits[kr >> 5] & ((1u << (kr & 31)) - 1u));
+                            double4* fr = reinterpret_cast<double4*>(out.frec + rb + slot);
+                            fr[0] = make_double4((double)T, (double)C0, (double)C1, (double)C2);
+                            reinterpret_cast<uint4*>(fr + 1)[0] =
+                                make_uint4((unsigned)(py * cam.width + px), sm.srcq[(b + j) & (SR - 1)], (unsigned)cnt, 0u);
                         }
                         C0 += wd64 * col.x;
                         C1 += wd64 * col.y;
@@ -355,6 +425,11 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             if (out.alpha_map) out.alpha_map[p] = (float)(1 - T);
             out.t_final[p] = (float)T;
             if (out.t_final64) out.t_final64[p] = (double)T;
+            if (out.c_total64) {
+                out.c_total64[p * 3 + 0] = (double)C0 + (double)T * opt.bg[0];
+                out.c_total64[p * 3 + 1] = (double)C1 + (double)T * opt.bg[1];
+                out.c_total64[p * 3 + 2] = (double)C2 + (double)T * opt.bg[2];
+            }
             out.last_pos[p] = last;
             if (out.n_frag) out.n_frag[p] = cnt;
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;

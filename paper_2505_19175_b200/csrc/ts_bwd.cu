@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                                                             const long long* __restrict__ frag_off,
                                                             const double* __restrict__ fg_dw,
                                                             const double* __restrict__ fg_dz,
+                                                            const unsigned long long* __restrict__ run_if,
                                                             double* __restrict__ sgrad) {
+    if (run_if && *run_if == 0ull) return;  // the streaming backward handled this frame
     using SM = BwdSmem<DB, PCAP, GCAP>;
     constexpr int RR = SM::RR, SR = SM::SR, NW = SM::NW;
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -505,8 +507,8 @@ template <int DB, int PCAP, int GCAP, int MINB>
 static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                              const int* tile_start, const unsigned* ent_src, const double* t_final,
                              const int* last_pos, const float* d_image, const int* n_frag,
-                             const long long* frag_off, const double* fg_dw, const double* fg_dz, double* sgrad,
-                             cudaStream_t st) {
+                             const long long* frag_off, const double* fg_dw, const double* fg_dz,
+                             const unsigned long long* run_if, double* sgrad, cudaStream_t st) {
     const int dyn = (int)sizeof(BwdSmem<DB, PCAP, GCAP>);
     static bool attr = false;
     if (!attr) {
@@ -516,23 +518,24 @@ static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, c
     const int ntiles = cam.ntx * cam.nty;
     k_blend_bwd_dense<DB, PCAP, GCAP, MINB><<<ntiles, 256, dyn, st>>>(cam, opt, rec, recb, tile_start, ent_src, t_final,
                                                                  last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz,
-                                                                 sgrad);
+                                                                 run_if, sgrad);
 }
 
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
                             const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
-                            const double* fg_dw, const double* fg_dz, double* sgrad, cudaStream_t st) {
+                            const double* fg_dw, const double* fg_dz, const unsigned long long* run_if, double* sgrad,
+                            cudaStream_t st) {
     static const int variant = [] {
         const char* v = getenv("TS_BWD_VARIANT");
         return v ? atoi(v) : 0;
     }();
     if (variant == 1)
         launch_bwd_dense<64, 2048, 512, 2>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
-                                           frag_off, fg_dw, fg_dz, sgrad, st);
+                                           frag_off, fg_dw, fg_dz, run_if, sgrad, st);
     else  // 3 CTAs per SM
         launch_bwd_dense<32, 1024, 384, 3>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
-                                           frag_off, fg_dw, fg_dz, sgrad, st);
+                                           frag_off, fg_dw, fg_dz, run_if, sgrad, st);
 }
 
 }  // namespace ts

@@ -1,0 +1,173 @@
+// ts_bwd_stream.cu -- streaming backward blend (rasterize_backward,
+// _kernels.py:181-318) over the fragment records of the training forward.
+//
+// The training forward (k_blend_dense, fp64 compositing, + k_fixup_fwd)
+// writes one FragRec per composited fragment, grouped by (tile, entry): the
+// transmittance T_k and the colour C_k accumulated in front of the fragment,
+// its pixel and source triangle.  With the pixel's final unclipped colour C_N
+// (incl. T_N * background) the reference's back-to-front recursion becomes a
+// closed form per fragment:
+//     w_k = T_k alpha_k,   S_k = C_N - C_k - w_k c_k   (suffix colour),
+//     dL/dalpha_k = sum_c d_c (T_k c_k - S_k / (1 - alpha_k)),
+// so every fragment is independent: one lane per record, r / argmax edge /
+// alpha recomputed in fp64 from the triangle's records, the window and edge
+// chain as in k_blend_bwd_dense, a segmented warp reduction over consecutive
+// records of one triangle and one fp64 atomic per (triangle, component) and
+// warp step.  No tile loop, no CTA barrier.  If the forward's record buffer
+// overflowed, this kernel does nothing and the tile backward runs instead.
+#include "ts_kernels.cuh"
+
+namespace ts {
+
+template <typename PT>
+__global__ void __launch_bounds__(256) k_bwd_stream(Cam cam, Opts opt, const RecF* __restrict__ rec,
+                                                    const RecB* __restrict__ recb,
+                                                    const PT* __restrict__ opacity, const PT* __restrict__ sigma,
+                                                    const FragRec* __restrict__ frec, const Counters* __restrict__ ctr,
+                                                    unsigned long long cap, const double* __restrict__ c_total,
+                                                    const float* __restrict__ d_image, double* __restrict__ sgrad) {
+    if (ctr->frec_over) return;
+    const unsigned long long total = ctr->n_frec;
+    const long long n = (long long)(total < cap ? total : cap);
+    const unsigned lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int mode = opt.mode;
+    for (long long q0 = gw * 32; q0 < n; q0 += nw * 32) {
+        const long long q = q0 + lane;
+        float gf[12];
+#pragma unroll
+        for (int c = 0; c < 12; c++) gf[c] = 0.f;
+        unsigned key = 0xffffffffu - lane;  // unique keys for idle lanes and holes
+        bool act = false;
+        if (q < n) {
+            const double2 ta = __ldg(reinterpret_cast<const double2*>(frec + q));
+            const double2 tb2 = __ldg(reinterpret_cast<const double2*>(frec + q) + 1);
+            const double4 tc = make_double4(ta.x, ta.y, tb2.x, tb2.y);
+            const uint4 ids = __ldg(reinterpret_cast<const uint4*>(frec + q) + 2);
+            if (ids.x != 0xffffffffu) {
+                act = true;
+                const unsigned pix = ids.x, src = ids.y;
+                key = src;
+                const RecF& R = rec[src];
+                const RecB& B = recb[src];
+                const int px = (int)(pix % (unsigned)cam.width), py = (int)(pix / (unsigned)cam.width);
+                const double pcx = px + 0.5, pcy = py + 0.5;
+                const double l0 = fma(__ldg(&R.a[0]), pcx, fma(__ldg(&R.a[1]), pcy, __ldg(&R.a[2])));
+                const double l1 = fma(__ldg(&R.a[3]), pcx, fma(__ldg(&R.a[4]), pcy, __ldg(&R.a[5])));
+                const double l2 = fma(__ldg(&R.a[6]), pcx, fma(__ldg(&R.a[7]), pcy, __ldg(&R.a[8])));
+                // argmax of phi = argmin of phi/phi_s, ties -> lowest edge (_kernels.py:36-42)
+                double r64 = l0;
+                int edge = 0;
+                if (l1 < r64) { r64 = l1; edge = 1; }
+                if (l2 < r64) { r64 = l2; edge = 2; }
+                const double phis = __ldg(&R.phis);
+                const double o = opt.solid ? 1.0 : (double)__ldg(opacity + src);
+                const double sg = (double)__ldg(sigma + src);
+                const double rc = fmin(r64, 1.0);
+                double ae;
+                if (mode == 0) ae = o * (sg == 1.0 ? rc : pow(rc, sg));
+                else ae = o / (1.0 + exp(fmin(r64 * phis / sg, 700.0)));
+                const bool clamped = ae > ALPHA_CLAMP;
+                const double a = clamped ? ALPHA_CLAMP : ae;
+                const double inv1m = 1.0 / (1.0 - a);
+                const double tb = tc.x;
+                const double w = tb * a;
+                const float c0 = __ldg(&R.rgb[0]), c1 = __ldg(&R.rgb[1]), c2 = __ldg(&R.rgb[2]);
+                const double s0 = __ldg(c_total + pix * 3 + 0) - tc.y - w * c0;
+                const double s1 = __ldg(c_total + pix * 3 + 1) - tc.z - w * c1;
+                const double s2 = __ldg(c_total + pix * 3 + 2) - tc.w - w * c2;
+                const double d0 = __ldg(d_image + pix * 3 + 0), d1 = __ldg(d_image + pix * 3 + 1),
+                             d2 = __ldg(d_image + pix * 3 + 2);
+                gf[8] = (float)(w * d0);
+                gf[9] = (float)(w * d1);
+                gf[10] = (float)(w * d2);
+                const double ga = d0 * (tb * c0 - s0 * inv1m) + d1 * (tb * c1 - s1 * inv1m) + d2 * (tb * c2 - s2 * inv1m);
+                if (!clamped) {
+                    const double window = a / o;
+                    gf[6] = (float)(ga * window);  // d/d opacity = g_alpha * alpha / o
+                    const double g_win = o * ga;
+                    const double phi = r64 * phis;
+                    double g_phi;
+                    if (mode == 0) {
+                        gf[7] = (float)(g_win * window * ((double)fast_lg2((float)rc) * 0.6931471805599453));
+                        const double g_r = g_win * sg * window / rc;
+                        if (r64 >= 1.0) {
+                            g_phi = 0.0;
+                        } else {
+                            g_phi = g_r / phis;
+                            gf[11] = (float)(-g_r * r64 / phis);
+                        }
+                    } else {
+                        const double E = exp(fmin(phi / sg, 700.0));
+                        const double ww = E / ((1.0 + E) * (1.0 + E));
+                        const double is = 1.0 / sg;
+                        gf[7] = (float)(g_win * ww * phi * is * is);
+                        g_phi = -g_win * ww * is;
+                    }
+                    const int ib = edge == 2 ? 0 : edge + 1;
+                    const double ax = __ldg(&B.qx[edge]), ay = __ldg(&B.qy[edge]);
+                    const double bx = __ldg(&B.qx[ib]), by = __ldg(&B.qy[ib]);
+                    const double pxr = (double)(px - __ldg(&R.ox)) + 0.5, pyr = (double)(py - __ldg(&R.oy)) + 0.5;
+                    const double sl = __ldg(&B.sl[edge]), ul = __ldg(&B.ul[edge]), vl = __ldg(&B.vl[edge]);
+                    const float gax = (float)(g_phi * (sl * (pyr - by) + phi * ul));
+                    const float gay = (float)(g_phi * (sl * (bx - pxr) + phi * vl));
+                    const float gbx = (float)(g_phi * (sl * (ay - pyr) - phi * ul));
+                    const float gby = (float)(g_phi * (sl * (pxr - ax) - phi * vl));
+                    gf[0] = edge == 0 ? gax : (ib == 0 ? gbx : 0.f);
+                    gf[1] = edge == 0 ? gay : (ib == 0 ? gby : 0.f);
+                    gf[2] = edge == 1 ? gax : (ib == 1 ? gbx : 0.f);
+                    gf[3] = edge == 1 ? gay : (ib == 1 ? gby : 0.f);
+                    gf[4] = edge == 2 ? gax : (ib == 2 ? gbx : 0.f);
+                    gf[5] = edge == 2 ? gay : (ib == 2 ? gby : 0.f);
+                }
+            }
+        }
+        // segmented reduction over consecutive records of one triangle
+        const unsigned kprev = __shfl_up_sync(0xffffffffu, key, 1);
+        const bool head = lane == 0 || kprev != key;
+        const unsigned heads = __ballot_sync(0xffffffffu, head);
+        const unsigned later = heads & ~((2u << lane) - 1u);
+        const int runlen = head ? (later ? __ffs(later) - 1 : 32) - (int)lane : 0;
+        const int maxrun = __reduce_max_sync(0xffffffffu, runlen);
+        // run id (a triangle can reappear after another one within a step)
+        const unsigned rid = __popc(heads & ((2u << lane) - 1u));
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            if (off >= maxrun) break;
+            const unsigned ro = __shfl_down_sync(0xffffffffu, rid, off);
+            const bool same = (int)lane + off < 32 && ro == rid;
+#pragma unroll
+            for (int c = 0; c < 12; c++) {
+                const float v = __shfl_down_sync(0xffffffffu, gf[c], off);
+                if (same) gf[c] += v;
+            }
+        }
+        if (act && head) {
+            double* dst = sgrad + (size_t)key * SG_STRIDE;
+#pragma unroll
+            for (int c = 0; c < 12; c++)
+                if (gf[c] != 0.f) atomicAdd(dst + c, (double)gf[c]);
+        }
+    }
+}
+
+void launch_bwd_stream(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                       const RecB* recb, const FragRec* frec, const Counters* ctr, unsigned long long cap,
+                       const double* c_total, const float* d_image, double* sgrad, cudaStream_t st) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = sms * 8;
+    if (dtype == 1)
+        k_bwd_stream<double><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const double*)soup.opacity,
+                                                   (const double*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
+    else
+        k_bwd_stream<float><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
+                                                  (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
+}
+
+}  // namespace ts

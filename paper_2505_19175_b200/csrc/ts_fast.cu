@@ -997,6 +997,22 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
                         m &= m - 1;
                         const double aj = s_a[j];
                         const double w = Tt * aj;
+                        if (lane == 0 && out.frec && base + j >= fpos) {
+                            // training forward: record of the exactly replayed fragment
+                            const unsigned long long fi = atomicAdd(&out.ctr->n_frec, 1ull);
+                            if (fi < out.frec_cap) {
+                                FragRec& fr = out.frec[fi];
+                                fr.T = Tt;
+                                fr.C[0] = C0;
+                                fr.C[1] = C1;
+                                fr.C[2] = C2;
+                                fr.pix = (unsigned)p;
+                                fr.src = s_s[j];
+                                fr.ord = (unsigned)cnt;
+                            } else {
+                                out.ctr->frec_over = 1ull;
+                            }
+                        }
                         C0 += w * (double)s_c[0][j];
                         C1 += w * (double)s_c[1][j];
                         C2 += w * (double)s_c[2][j];
@@ -1034,6 +1050,11 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
             if (out.alpha_map) out.alpha_map[p] = (float)(1.0 - Tt);
             out.t_final[p] = (float)Tt;
             if (out.t_final64) out.t_final64[p] = Tt;
+            if (out.c_total64) {
+                out.c_total64[p * 3 + 0] = C0 + Tt * opt.bg[0];
+                out.c_total64[p * 3 + 1] = C1 + Tt * opt.bg[1];
+                out.c_total64[p * 3 + 2] = C2 + Tt * opt.bg[2];
+            }
             out.last_pos[p] = last;
             if (out.n_frag) out.n_frag[p] = cnt;
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;

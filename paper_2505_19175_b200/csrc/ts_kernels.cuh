@@ -13,8 +13,21 @@ struct Counters {
     unsigned long long key_max;
     long long err[4];            // first non-finite index per group
     unsigned long long n_flagged;
-    unsigned long long pad[5];
+    unsigned long long n_frec;       // fragment records emitted by the training forward
+    unsigned long long frec_over;    // 1: the record buffer overflowed (backward falls back)
+    unsigned long long pad[3];
 };
+
+// One composited fragment of a training forward, in (tile, batch, entry-major)
+// order, for the streaming backward: the transmittance and the accumulated
+// colour in front of it (fp64), its pixel, source triangle and ordinal in the
+// pixel's list.  pix = ~0u marks a hole (a passing pair that was not composited).
+struct __align__(16) FragRec {
+    double T;
+    double C[3];
+    unsigned pix, src, ord, pad;
+};
+static_assert(sizeof(FragRec) == 48, "FragRec layout");
 
 struct PreOut {
     Rec64* rec;                // (N) fp64 records (accepted only)
@@ -58,6 +71,10 @@ struct FastBlendOut {
     double* frag_w;            // blend weight T * alpha
     double* frag_z;            // camera-space depth of the triangle
     const unsigned long long* zkey;  // (N) fp64 bit pattern of the centroid depth
+    // training forwards: fragment records for the streaming backward (null = none)
+    FragRec* frec;
+    unsigned long long frec_cap;
+    double* c_total64;         // (P,3) unclipped colour incl. T_final * background
 };
 
 struct BlendOut {
@@ -108,7 +125,12 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
                             const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
-                            const double* fg_dw, const double* fg_dz, double* sgrad, cudaStream_t st);
+                            const double* fg_dw, const double* fg_dz, const unsigned long long* run_if, double* sgrad,
+                            cudaStream_t st);
+// ts_bwd_stream.cu: streaming backward over the training forward's fragment records
+void launch_bwd_stream(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                       const RecB* recb, const FragRec* frec, const Counters* ctr, unsigned long long cap,
+                       const double* c_total, const float* d_image, double* sgrad, cudaStream_t st);
 
 // ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
 bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,

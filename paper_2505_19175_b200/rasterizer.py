@@ -367,6 +367,15 @@ class Rasterizer:
     def dump_depth(self, n):
         return self._dump(_lib.TS_DUMP_DEPTH, n, torch.float64)
 
+    def dump_fragment_records(self, max_records):
+        """Fragment records of the last training forward (streaming backward input)."""
+        raw = self._dump(_lib.TS_DUMP_FRAGREC, 8 + 48 * max_records, torch.uint8)
+        cnt = int(raw[:8].view(np.uint64)[0])
+        rec = raw[8:8 + 48 * cnt].reshape(cnt, 48)
+        tc = rec[:, :32].copy().view(np.float64).reshape(cnt, 4)
+        ids = rec[:, 32:].copy().view(np.uint32).reshape(cnt, 4)
+        return tc, ids
+
     def dump_sgrad(self, n):
         return self._dump(_lib.TS_DUMP_SGRAD, n * 16, torch.float64).reshape(n, 16)
 
