@@ -283,40 +283,36 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             }
         }
         // ---- 3. composite: thread = pixel, passing entries in depth order ----
+        static_assert(NW <= 2, "64-bit pixel masks");
+        unsigned long long mm = sm.mask[0][tid];
+        if constexpr (NW == 2) mm |= (unsigned long long)sm.mask[1][tid] << 32;
         unsigned long long rb = ~0ull;
-        if constexpr (ACC64) {
-            if (out.frec) {
-                rb = sm.rbase;
-                if (rb != ~0ull) {
-                    // every passing pair of the pixel starts as a hole; composited
-                    // fragments overwrite theirs below (same thread, program order)
-#pragma unroll
-                    for (int wd = 0; wd < NW; wd++) {
-                        unsigned m = sm.mask[wd][tid];
-                        while (m) {
-                            const int j = wd * 32 + __ffs(m) - 1;
-                            m &= m - 1;
-                            const int2 kbh = sm.kb[j];
-                            const int kh = kbh.x + ly * kbh.y + lx;
-                            const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
-                            out.frec[rb + slot].pix = ~0u;
-                        }
-                    }
-                }
+        if constexpr (ACC64)
+            if (out.frec) rb = sm.rbase;
+        // training records: passing pairs this pixel does not composite are holes
+        auto mark_holes = [&](unsigned long long hm) {
+            while (hm) {
+                const int j = __ffsll((long long)hm) - 1;
+                hm &= hm - 1;
+                const int2 kbh = sm.kb[j];
+                const int kh = kbh.x + ly * kbh.y + lx;
+                const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
+                out.frec[rb + slot].pix = ~0u;
             }
-        }
-        if (!done) {
-#pragma unroll
-            for (int wd = 0; wd < NW; wd++) {
-                unsigned m = sm.mask[wd][tid];
-                while (m) {
-                    const int j = wd * 32 + __ffs(m) - 1;
-                    m &= m - 1;
+        };
+        if (done) {
+            if (rb != ~0ull) mark_holes(mm);
+        } else {
+            {
+                while (mm) {
+                    const int j = __ffsll((long long)mm) - 1;
+                    mm &= mm - 1;
                     const int2 kb = sm.kb[j];
                     const Real rv = sm.r[kb.x + ly * kb.y + lx];
                     if (isnan(rv)) {  // r inside the contribution band
                         flag_pos = b + j;
                         done = true;
+                        mm |= 1ull << j;
                         break;
                     }
                     const float4 col = sm.col[j];
@@ -340,6 +336,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         if (fabs(tn - T_MIN) <= 1e-9 * tn || fabs(wd64 - opt.tau_contrib) <= 1e-9 * wd64) {
                             flag_pos = b + j;
                             done = true;
+                            mm |= 1ull << j;
                             break;
                         }
                         if (rb != ~0ull) {
@@ -398,8 +395,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         break;
                     }
                 }
-                if (done) break;
             }
+            if (done && rb != ~0ull) mark_holes(mm);
         }
         __syncthreads();
         if (tid < nb) {

@@ -19,8 +19,8 @@
 
 namespace ts {
 
-template <typename PT>
-__global__ void __launch_bounds__(256) k_bwd_stream(Cam cam, Opts opt, const RecF* __restrict__ rec,
+template <typename PT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                     const RecB* __restrict__ recb,
                                                     const PT* __restrict__ opacity, const PT* __restrict__ sigma,
                                                     const FragRec* __restrict__ frec, const Counters* __restrict__ ctr,
@@ -162,12 +162,22 @@ void launch_bwd_stream(const Cam& cam, const Opts& opt, const ts_soup& soup, int
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = sms * 8;
+    static const int variant = [] {
+        const char* v = getenv("TS_STREAM_VARIANT");
+        return v ? atoi(v) : 0;
+    }();
     if (dtype == 1)
-        k_bwd_stream<double><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const double*)soup.opacity,
+        k_bwd_stream<double, 4><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const double*)soup.opacity,
                                                    (const double*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
+    else if (variant == 1)
+        k_bwd_stream<float, 3><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
+                                                     (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
+    else if (variant == 2)
+        k_bwd_stream<float, 6><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
+                                                     (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
     else
-        k_bwd_stream<float><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
-                                                  (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
+        k_bwd_stream<float, 4><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
+                                                     (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
 }
 
 }  // namespace ts
