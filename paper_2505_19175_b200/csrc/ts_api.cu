@@ -57,6 +57,11 @@ struct ts_context {
     long long cap_e = -1;
     void* ent_buf = nullptr;
     unsigned *tkey = nullptr, *tval = nullptr, *tkey_alt = nullptr, *tval_alt = nullptr;
+    unsigned *tscr0 = nullptr, *tscr1 = nullptr;  // tile-sort scratch (tiles longer than shared memory)
+    unsigned* tcnt = nullptr;                      // per-tile entry counts
+    ulonglong2* bucket = nullptr;                  // (depth key, source) of every tile entry, unsorted
+    DevBuf binmat;                                 // chunk x tile count matrix of the binning
+    bool sorted_valid = false;                     // sorted_src holds the global depth order
     // per-pixel scratch
     long long cap_p = -1, cap_tiles = -1;
     void* pix_buf = nullptr;
@@ -173,12 +178,15 @@ static int ensure_ent(ts_context* c, long long e) {
     if (c->ent_buf) cudaFree(c->ent_buf);
     c->ent_buf = nullptr;
     size_t one = align_up(4 * cap, 256);
-    TS_CHECK(cudaMalloc(&c->ent_buf, 4 * one));
+    TS_CHECK(cudaMalloc(&c->ent_buf, 10 * one));
     char* b = (char*)c->ent_buf;
     c->tkey = (unsigned*)b;
     c->tval = (unsigned*)(b + one);
     c->tkey_alt = (unsigned*)(b + 2 * one);
     c->tval_alt = (unsigned*)(b + 3 * one);
+    c->tscr0 = (unsigned*)(b + 4 * one);
+    c->tscr1 = (unsigned*)(b + 5 * one);
+    c->bucket = (ulonglong2*)(b + 6 * one);
     c->cap_e = cap;
     return TS_OK;
 }
@@ -196,7 +204,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
         return o;
     };
     size_t o_tf = take(8 * cp), o_t32 = take(4 * cp), o_lp = take(4 * cp), o_fg = take(8 * cp),
-           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp);
+           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp), o_tc = take(4 * (ct + 1));
     TS_CHECK(cudaMalloc(&c->pix_buf, off));
     char* b = (char*)c->pix_buf;
     c->t_final = (double*)(b + o_tf);
@@ -205,6 +213,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     c->flags = (int2*)(b + o_fg);
     c->tile_start = (int*)(b + o_ts);
     c->nfrag = (int*)(b + o_nf);
+    c->tcnt = (unsigned*)(b + o_tc);
     c->cap_p = cp;
     c->cap_tiles = ct;
     return TS_OK;
@@ -305,7 +314,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
     for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
-                      &c->ctot})
+                      &c->ctot, &c->binmat})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
@@ -347,42 +356,63 @@ int ts_stage_times(ts_context* c, float* ms, int n) {
     return TS_OK;
 }
 
+// Global depth order of the current forward (np.lexsort((idx, z)),
+// render.py:276) into sorted_src: 24-bit range-reduced keys while ties stay
+// rare (n < 2^22), else 32-bit; exact (z64, idx) order restored inside runs of
+// equal reduced keys.  Used by the legacy binning and the debug dumps.
+static void global_depth_order(ts_context* c, long long n, cudaStream_t st) {
+    const int kcap = n < (1ll << 22) ? 24 : 31;
+    unsigned* k32 = (unsigned*)c->keys_c;
+    unsigned* k32_alt = (unsigned*)c->keys_alt;
+    depth_keys(n, c->flag, c->key, c->d_ctr, kcap, k32, c->vals_c, st);
+    int par = onesweep_sort_u32(n, k32, c->vals_c, k32_alt, c->vals_alt, kcap, c->os_buf, st);
+    c->sorted_src = par ? c->vals_alt : c->vals_c;
+    fix_depth_runs(n, par ? k32_alt : k32, (unsigned*)c->sorted_src, c->key, st, (1u << kcap) - 1u);
+    g_launches += 2 + 3 * ((kcap + 7) / 8);
+    c->sorted_valid = true;
+}
+
 // Binning + blend of the current forward, sized from host capacities and the
-// device counters of the preprocess (no host round trip): depth keys of all n
-// triangles (culled ones sort last), stable radix sort, exact tie order, rank
-// offsets, tile duplication (bounded by cap_e), stable tile sort over the
-// device entry count, tile ranges, blend, fix-up.
+// device counters of the preprocess (no host round trip).  Default: tile-first
+// binning (ts_bin.cu) -- per-tile counts, scan, bucket fill, then every tile's
+// list sorted by exact (z, idx) in shared memory.  TS_BIN_LEGACY: global depth
+// sort, rank offsets, tile duplication, stable radix sort by tile, ranges.
 static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_options* opt, const ts_soup* soup,
                         const ts_forward_out* out, cudaStream_t st) {
     const bool fast = opt->precision == 0;
     const long long n = soup->n;
     const int ntiles = cm.ntx * cm.nty;
-    if (n > 0) {
-        // depth order (np.lexsort((idx, z)), render.py:276): 24-bit range-reduced
-        // keys while ties stay rare (n < 2^22), else 32-bit; exact (z64, idx)
-        // order restored inside runs of equal reduced keys
+    c->sorted_valid = false;
+    // working capacity: the largest entry count seen so far with headroom
+    // (the sort grids follow it); more entries raise the sticky overflow flag
+    const long long wcap = c->e_hint > 0 ? std::min<long long>(c->cap_e, c->e_hint + c->e_hint / 4 + 4096)
+                                         : c->cap_e;
+    static const bool bin_legacy = getenv("TS_BIN_LEGACY") != nullptr;
+    if (n > 0 && !bin_legacy && ntiles <= bin_max_tiles()) {
+        stage_begin(c, TS_STAGE_BINNING, st);
+        bin_tiles_fill(n, c->bbox, c->key, cm.ntx, ntiles, c->tcnt, (unsigned*)c->binmat.p, c->tile_start,
+                       c->bucket, wcap, c->d_sticky, st);
+        stage_end(c, TS_STAGE_BINNING, st);
         stage_begin(c, TS_STAGE_DEPTH_SORT, st);
-        const int kcap = n < (1ll << 22) ? 24 : 31;
-        unsigned* k32 = (unsigned*)c->keys_c;
-        unsigned* k32_alt = (unsigned*)c->keys_alt;
-        depth_keys(n, c->flag, c->key, c->d_ctr, kcap, k32, c->vals_c, st);
-        int par = onesweep_sort_u32(n, k32, c->vals_c, k32_alt, c->vals_alt, kcap, c->os_buf, st);
-        c->sorted_src = par ? c->vals_alt : c->vals_c;
-        fix_depth_runs(n, par ? k32_alt : k32, (unsigned*)c->sorted_src, c->key, st, (1u << kcap) - 1u);
-        g_launches += 2 + 3 * ((kcap + 7) / 8);
+        unsigned* const scr[4] = {c->tkey_alt, c->tval_alt, c->tscr0, c->tscr1};
+        bin_tiles_sort(n, ntiles, c->tile_start, c->bucket, c->key, c->tval, scr, st);
+        stage_end(c, TS_STAGE_DEPTH_SORT, st);
+        c->ent_src = c->tval;
+        c->sorted_src = c->vals_c;
+        c->wcap = wcap;
+        g_launches += 5;
+    } else if (n > 0) {
+        stage_begin(c, TS_STAGE_DEPTH_SORT, st);
+        global_depth_order(c, n, st);
         stage_end(c, TS_STAGE_DEPTH_SORT, st);
 
         // tile duplication in rank order + stable sort by tile id (render.py:315-361)
         stage_begin(c, TS_STAGE_BINNING, st);
         rank_offsets(n, c->sorted_src, c->tcount, c->offs, nullptr, c->sort, st);
-        // working capacity: the largest entry count seen so far with headroom
-        // (the sort grids follow it); more entries raise the sticky overflow flag
-        const long long wcap = c->e_hint > 0 ? std::min<long long>(c->cap_e, c->e_hint + c->e_hint / 4 + 4096)
-                                             : c->cap_e;
         duplicate_entries(n, c->sorted_src, c->bbox, c->offs, cm.ntx, c->tkey, c->tval, wcap, c->d_sticky, st);
         const int tbits = bit_length((unsigned long long)(ntiles > 1 ? ntiles - 1 : 0));
-        par = onesweep_sort_u32_dev(wcap, &c->d_ctr->e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits,
-                                    c->os_buf, st);
+        int par = onesweep_sort_u32_dev(wcap, &c->d_ctr->e, c->tkey, c->tval, c->tkey_alt, c->tval_alt, tbits,
+                                        c->os_buf, st);
         const unsigned* skey = par ? c->tkey_alt : c->tkey;
         c->ent_src = par ? c->tval_alt : c->tval;
         tile_ranges_dev(wcap, &c->d_ctr->e, skey, ntiles, c->tile_start, st);
@@ -391,6 +421,7 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
         stage_end(c, TS_STAGE_BINNING, st);
     } else {
         c->sorted_src = c->vals_c;
+        c->sorted_valid = true;
         c->ent_src = c->tval;
         TS_CHECK(cudaMemsetAsync(c->tile_start, 0, sizeof(int) * (ntiles + 1), st));
     }
@@ -483,6 +514,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     // tile-entry capacity: the last frame's count with headroom, at least 4 per triangle
     if ((rc = ensure_ent(c, std::max<long long>(4 * n1 + 4096, c->e_hint + c->e_hint / 2)))) return rc;
     if ((rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1))) return rc;
+    if ((rc = ensure(c->binmat, bin_matrix_bytes(n1, cm.ntx * cm.nty)))) return rc;
     c->frec_ready = false;
     if (fast && opt->keep_backward) {
         // fragment records of the training forward (~6.5 per tile entry here)
@@ -719,6 +751,7 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
     switch (what) {
         case TS_DUMP_SORTED_IDX:
             if (bytes < 4 * (size_t)c->m) return TS_ERR_INVALID_ARG;
+            if (!c->sorted_valid) global_depth_order(c, c->n, st);
             if (c->m) TS_CHECK(cudaMemcpyAsync(dst, c->sorted_src, 4 * c->m, cudaMemcpyDeviceToDevice, st));
             return TS_OK;
         case TS_DUMP_TILE_START:
@@ -727,6 +760,7 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
             return TS_OK;
         case TS_DUMP_ENTRY_RANK:
             if (bytes < 4 * (size_t)c->e) return TS_ERR_INVALID_ARG;
+            if (!c->sorted_valid) global_depth_order(c, c->n, st);
             rank_offsets(c->n, c->sorted_src, c->tcount, c->offs, c->rank_of, c->sort, st);
             entries_to_rank(c->e, c->ent_src, c->rank_of, (int*)dst, st);
             return cuda_err(cudaGetLastError());

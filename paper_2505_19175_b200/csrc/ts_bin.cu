@@ -1,0 +1,510 @@
+// ts_bin.cu -- tile-first binning: the per-tile entry lists of the reference
+// (render.py:275-277 depth order np.lexsort((idx, z)), then 315-361
+// duplicate / stable sort by tile / ranges) built without a global sort.
+//
+// The reference sorts all triangles by (z, idx), duplicates each into the
+// tiles its bbox touches and stable-sorts the duplicates by tile id, so a
+// tile's list is its triangles in (z, idx) order.  Here:
+//   k_bin_count  -- CTA per chunk of triangles: per-tile counts in shared
+//                   memory (no global atomics), one row of the chunk x tile
+//                   count matrix;
+//   k_bin_cols   -- per tile: prefix over the chunks (the chunk's first slot
+//                   within the tile) and the tile total;
+//   k_tile_scan  -- one CTA: exclusive scan of the totals -> tile_start (all
+//                   tiles empty and the sticky overflow flag raised if the total
+//                   exceeds the entry capacity);
+//   k_bin_fill   -- CTA per chunk: shared-memory cursors from the matrix, one
+//                   slot per (triangle, tile); the bucket holds the tile's
+//                   triangles (and their depth keys) in arbitrary order;
+//   k_tile_sort  -- CTA per tile: the depth keys (fp64 bit patterns of the
+//                   positive centroid depth, monotone) are range-reduced to 32
+//                   bits, counting-sorted on their top 12 bits in shared memory,
+//                   and every run of equal 12-bit keys is ordered by the exact
+//                   (z, idx) pair.  Tiles longer than the shared-memory
+//                   capacity, or with long runs (equal or clustered depths), take
+//                   a stable LSD radix path (by idx, then by all 64 key bits).
+// The result is bit-identical to the global sort's tile lists.
+#include "ts_kernels.cuh"
+
+namespace ts {
+
+namespace {
+constexpr int BT = 256;       // threads per CTA
+constexpr int BW = BT / 32;   // warps
+constexpr int RUN_SHORT = 48; // runs up to this length are insertion-sorted by one thread
+
+__device__ __forceinline__ unsigned excl_scan_256(unsigned v, unsigned* s_w, unsigned& total) {
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= (unsigned)off) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = lane < BW ? s_w[lane] : 0u;
+#pragma unroll
+        for (int off = 1; off < BW; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= (unsigned)off) w += y;
+        }
+        if (lane < BW) s_w[lane] = w;
+    }
+    __syncthreads();
+    const unsigned pre = warp ? s_w[warp - 1] : 0u;
+    total = s_w[BW - 1];
+    __syncthreads();
+    return pre + x - v;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __restrict__ tcnt, int* __restrict__ tile_start,
+                                                    long long cap, unsigned* overflow) {
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned long long s_total;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long carry = 0;
+    for (int b0 = 0; b0 < ntiles; b0 += 1024) {
+        const int i = b0 + (int)threadIdx.x;
+        const unsigned v = i < ntiles ? tcnt[i] : 0u;
+        unsigned x = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= (unsigned)off) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned w = s_w[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, w, off);
+                if (lane >= (unsigned)off) w += y;
+            }
+            s_w[lane] = w;
+        }
+        __syncthreads();
+        const unsigned long long ex = carry + (warp ? s_w[warp - 1] : 0u) + x - v;
+        if (i < ntiles) {
+            tile_start[i] = (int)ex;
+            tcnt[i] = 0u;  // becomes the fill cursor
+        }
+        carry += s_w[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) s_total = carry;
+    __syncthreads();
+    if (s_total > (unsigned long long)cap) {
+        // over capacity: every tile empty, the forward is redone with larger buffers
+        for (int i = threadIdx.x; i <= ntiles; i += 1024) tile_start[i] = 0;
+        if (threadIdx.x == 0 && overflow) *overflow = 1u;
+    } else if (threadIdx.x == 0) {
+        tile_start[ntiles] = (int)s_total;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two-level counting (chunk x tile matrix): no contended global atomics.
+constexpr int BIN_CT = 1024;               // threads per chunk CTA
+constexpr int BIN_PER = 8;                 // triangles per thread
+constexpr int BIN_CHUNK = BIN_CT * BIN_PER;
+constexpr int BIN_MAX_TILES = 12288;       // shared-memory counters per CTA (48 KB)
+
+__global__ void __launch_bounds__(BIN_CT) k_bin_count(long long n, const short4* __restrict__ bbox, int ntx,
+                                                      int ntiles, unsigned* __restrict__ mat) {
+    extern __shared__ unsigned s_cnt[];
+    for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cnt[t] = 0u;
+    __syncthreads();
+    const long long c0 = (long long)blockIdx.x * BIN_CHUNK;
+#pragma unroll 2
+    for (int k = 0; k < BIN_PER; k++) {
+        const long long i = c0 + k * BIN_CT + threadIdx.x;
+        if (i >= n) break;
+        const short4 bb = __ldg(bbox + i);
+        if (bb.y <= bb.x || bb.w <= bb.z) continue;
+        const int tx0 = bb.x / TILE, tx1 = (bb.y - 1) / TILE + 1, ty0 = bb.z / TILE, ty1 = (bb.w - 1) / TILE + 1;
+        for (int ty = ty0; ty < ty1; ty++)
+            for (int tx = tx0; tx < tx1; tx++) atomicAdd(&s_cnt[ty * ntx + tx], 1u);
+    }
+    __syncthreads();
+    unsigned* row = mat + (size_t)blockIdx.x * ntiles;
+    for (int t = threadIdx.x; t < ntiles; t += BIN_CT) row[t] = s_cnt[t];
+}
+
+// per tile: exclusive prefix over the chunks in place, totals into tcnt.  CTA =
+// 32 consecutive tiles (lane) x 8 chunk ranges (warp): coalesced 128-byte rows.
+__global__ void __launch_bounds__(256) k_bin_cols(int nchunk, int ntiles, unsigned* __restrict__ mat,
+                                                  unsigned* __restrict__ tcnt) {
+    __shared__ unsigned s_part[8][33];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + (int)lane;
+    const int per = (nchunk + 7) / 8;
+    const int b0 = (int)warp * per, b1 = min(nchunk, b0 + per);
+    unsigned sum = 0;
+    if (t < ntiles)
+        for (int b = b0; b < b1; b++) sum += mat[(size_t)b * ntiles + t];
+    s_part[warp][lane] = sum;
+    __syncthreads();
+    unsigned run = 0;
+    for (int w = 0; w < (int)warp; w++) run += s_part[w][lane];
+    if (t < ntiles) {
+        for (int b = b0; b < b1; b++) {
+            const unsigned v = mat[(size_t)b * ntiles + t];
+            mat[(size_t)b * ntiles + t] = run;
+            run += v;
+        }
+        if (warp == 7) tcnt[t] = run;
+    }
+}
+
+__global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* __restrict__ bbox, int ntx,
+                                                     int ntiles, const unsigned* __restrict__ mat,
+                                                     const int* __restrict__ tile_start,
+                                                     const unsigned long long* __restrict__ key64,
+                                                     ulonglong2* __restrict__ bucket) {
+    extern __shared__ unsigned s_cur[];
+    if (tile_start[ntiles] == 0) return;  // empty (or over capacity)
+    const unsigned* row = mat + (size_t)blockIdx.x * ntiles;
+    for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cur[t] = (unsigned)tile_start[t] + row[t];
+    __syncthreads();
+    const long long c0 = (long long)blockIdx.x * BIN_CHUNK;
+#pragma unroll 2
+    for (int k = 0; k < BIN_PER; k++) {
+        const long long i = c0 + k * BIN_CT + threadIdx.x;
+        if (i >= n) break;
+        const short4 bb = __ldg(bbox + i);
+        if (bb.y <= bb.x || bb.w <= bb.z) continue;
+        const unsigned long long key = __ldg(key64 + i);
+        const int tx0 = bb.x / TILE, tx1 = (bb.y - 1) / TILE + 1, ty0 = bb.z / TILE, ty1 = (bb.w - 1) / TILE + 1;
+        for (int ty = ty0; ty < ty1; ty++)
+            for (int tx = tx0; tx < tx1; tx++) {
+                const unsigned pos = atomicAdd(&s_cur[ty * ntx + tx], 1u);
+                bucket[pos] = make_ulonglong2(key, (unsigned long long)i);
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stable LSD pass over items [0, cnt): warp w owns the contiguous segment
+// [w*seg, (w+1)*seg), visited in rounds of 32 (so (round, lane) order is item
+// order); per-warp digit counters, ranked with __match_any_sync.
+template <class Dig>
+__device__ __forceinline__ void radix_pass(int cnt, const unsigned* kin, const unsigned* vin, unsigned* kout,
+                                           unsigned* vout, Dig dig, unsigned (*wc)[256], unsigned* s_w) {
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int seg = (cnt + BW - 1) / BW;
+    const int s0 = (int)warp * seg, s1 = min(cnt, s0 + seg);
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int w = 0; w < BW; w++) wc[w][threadIdx.x] = 0u;
+    __syncthreads();
+    for (int r0 = s0; r0 < s1; r0 += 32) {
+        const int i = r0 + (int)lane;
+        const bool valid = i < s1;
+        const unsigned d = valid ? dig(kin[i], vin[i]) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (valid && (peers & lt) == 0u) wc[warp][d] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    unsigned tot = 0;
+#pragma unroll
+    for (int w = 0; w < BW; w++) tot += wc[w][threadIdx.x];
+    unsigned all;
+    unsigned run = excl_scan_256(tot, s_w, all);
+#pragma unroll
+    for (int w = 0; w < BW; w++) {
+        const unsigned c = wc[w][threadIdx.x];
+        wc[w][threadIdx.x] = run;
+        run += c;
+    }
+    __syncthreads();
+    for (int r0 = s0; r0 < s1; r0 += 32) {
+        const int i = r0 + (int)lane;
+        const bool valid = i < s1;
+        unsigned k = 0u, v = 0u;
+        if (valid) {
+            k = kin[i];
+            v = vin[i];
+        }
+        const unsigned d = valid ? dig(k, v) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned b = valid ? wc[warp][d] : 0u;
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) wc[warp][d] = b + __popc(peers);
+        __syncwarp();
+        if (valid) {
+            const unsigned pos = b + __popc(peers & lt);
+            kout[pos] = k;
+            vout[pos] = v;
+        }
+    }
+    __syncthreads();
+}
+
+// (z, idx) order of two sources (key64 = fp64 bits of the positive depth)
+__device__ __forceinline__ bool zidx_less(const unsigned long long* key64, unsigned a, unsigned b) {
+    const unsigned long long ka = key64[a], kb = key64[b];
+    return ka < kb || (ka == kb && a < b);
+}
+
+// Sorts the tile list [base, base + cnt) of bucket into out (exact (z, idx) order).
+// k0/v0/k1/v1: working arrays of cnt items (shared memory or global scratch).
+__device__ __forceinline__ void sort_tile(int cnt, const ulonglong2* bucket, const unsigned long long* key64,
+                                          unsigned* out, unsigned* k0, unsigned* v0, unsigned* k1, unsigned* v1,
+                                          int srcbits, unsigned (*wc)[256], unsigned* s_w,
+                                          unsigned long long* s_red, int* s_flag) {
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // depth-key range of the tile
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i = threadIdx.x; i < cnt; i += BT) {
+        const unsigned src = (unsigned)bucket[i].y;
+        const unsigned long long k = bucket[i].x;
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+        v0[i] = src;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, off);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if (lane == 0) {
+        s_red[warp] = lo;
+        s_red[BW + warp] = hi;
+    }
+    if (threadIdx.x == 0) *s_flag = 0;
+    __syncthreads();
+    lo = s_red[0];
+    hi = s_red[BW];
+#pragma unroll
+    for (int w = 1; w < BW; w++) {
+        lo = s_red[w] < lo ? s_red[w] : lo;
+        hi = s_red[BW + w] > hi ? s_red[BW + w] : hi;
+    }
+    const unsigned long long range = hi - lo;
+    const int nbits = range ? 64 - __clzll((long long)range) : 0;
+    const int shift = nbits > 16 ? nbits - 16 : 0;
+    const int passes = ((nbits < 16 ? nbits : 16) + 7) / 8;
+    for (int i = threadIdx.x; i < cnt; i += BT) k0[i] = (unsigned)((key64[v0[i]] - lo) >> shift);
+    __syncthreads();
+    for (int p = 0; p < passes; p++) {
+        const int sh = 8 * p;
+        radix_pass(cnt, k0, v0, k1, v1, [sh](unsigned k, unsigned) { return (k >> sh) & 0xffu; }, wc, s_w);
+        unsigned* t = k0; k0 = k1; k1 = t;
+        t = v0; v0 = v1; v1 = t;
+    }
+    // runs of equal reduced keys: exact (z, idx) order
+    for (int i = threadIdx.x; i < cnt; i += BT) {
+        if (i > 0 && k0[i] == k0[i - 1]) continue;
+        int j = i + 1;
+        while (j < cnt && k0[j] == k0[i] && j - i <= RUN_SHORT) j++;
+        if (j - i > RUN_SHORT) {
+            *s_flag = 1;
+            continue;
+        }
+        for (int a = i + 1; a < j; a++) {
+            const unsigned x = v0[a];
+            int b = a - 1;
+            while (b >= i && zidx_less(key64, x, v0[b])) {
+                v0[b + 1] = v0[b];
+                b--;
+            }
+            v0[b + 1] = x;
+        }
+    }
+    __syncthreads();
+    if (*s_flag) {
+        // long runs (clustered or equal depths): stable LSD by idx, then by all 64 key bits
+        for (int p = 0; p < (srcbits + 7) / 8; p++) {
+            const int sh = 8 * p;
+            radix_pass(cnt, k0, v0, k1, v1, [sh](unsigned, unsigned v) { return (v >> sh) & 0xffu; }, wc, s_w);
+            unsigned* t = k0; k0 = k1; k1 = t;
+            t = v0; v0 = v1; v1 = t;
+        }
+        for (int p = 0; p < 8; p++) {
+            const int sh = 8 * p;
+            radix_pass(cnt, k0, v0, k1, v1,
+                       [sh, key64](unsigned, unsigned v) { return (unsigned)(key64[v] >> sh) & 0xffu; }, wc, s_w);
+            unsigned* t = k0; k0 = k1; k1 = t;
+            t = v0; v0 = v1; v1 = t;
+        }
+    }
+    for (int i = threadIdx.x; i < cnt; i += BT) out[i] = v0[i];
+}
+
+// exact (z, idx) order of two packed items (reduced key << 32 | src)
+__device__ __forceinline__ bool item_less(const unsigned long long* key64, unsigned long long a,
+                                          unsigned long long b) {
+    if ((a >> 32) != (b >> 32)) return (a >> 32) < (b >> 32);
+    return zidx_less(key64, (unsigned)a, (unsigned)b);
+}
+
+template <int CAP, int NB>
+__global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restrict__ tile_start,
+                                                  const ulonglong2* __restrict__ bucket,
+                                                  const unsigned long long* __restrict__ key64,
+                                                  unsigned* __restrict__ ent_src, unsigned* gk0, unsigned* gv0,
+                                                  unsigned* gk1, unsigned* gv1, int srcbits) {
+    constexpr int IPT = CAP / BT;
+    __shared__ unsigned long long s_item[CAP];   // reduced key << 32 | src
+    __shared__ unsigned s_hist[NB];
+    __shared__ unsigned s_wc[BW][256];
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned long long s_red[2 * BW];
+    __shared__ int s_flag;
+    const int t = blockIdx.x;
+    const int base = tile_start[t], cnt = tile_start[t + 1] - base;
+    if (cnt <= 0) return;
+    if (cnt > CAP) {
+        sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,
+                  srcbits, s_wc, s_w, s_red, &s_flag);
+        return;
+    }
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long kk[IPT];
+    unsigned src[IPT];
+    unsigned long long lo = ~0ull, hi = 0ull;
+#pragma unroll
+    for (int q = 0; q < IPT; q++) {
+        const int i = q * BT + threadIdx.x;
+        kk[q] = 0ull;
+        src[q] = 0u;
+        if (i < cnt) {
+            const ulonglong2 r = bucket[base + i];
+            kk[q] = r.x;
+            src[q] = (unsigned)r.y;
+            lo = kk[q] < lo ? kk[q] : lo;
+            hi = kk[q] > hi ? kk[q] : hi;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, off);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if (lane == 0) {
+        s_red[warp] = lo;
+        s_red[BW + warp] = hi;
+    }
+    for (int b = threadIdx.x; b < NB; b += BT) s_hist[b] = 0u;
+    if (threadIdx.x == 0) s_flag = 0;
+    __syncthreads();
+    lo = s_red[0];
+    hi = s_red[BW];
+#pragma unroll
+    for (int w = 1; w < BW; w++) {
+        lo = s_red[w] < lo ? s_red[w] : lo;
+        hi = s_red[BW + w] > hi ? s_red[BW + w] : hi;
+    }
+    const unsigned long long range = hi - lo;
+    const int nbits = range ? 64 - __clzll((long long)range) : 0;
+    const int s32 = nbits > 32 ? nbits - 32 : 0;                       // 64 -> 32-bit reduced key
+    const int b32 = nbits < 32 ? nbits : 32;
+    constexpr int LB = NB == 4096 ? 12 : (NB == 2048 ? 11 : 10);
+    const int s12 = b32 > LB ? b32 - LB : 0;                            // 32-bit key -> bucket
+    unsigned kr[IPT];
+#pragma unroll
+    for (int q = 0; q < IPT; q++) {
+        kr[q] = (unsigned)((kk[q] - lo) >> s32);
+        if (q * BT + (int)threadIdx.x < cnt) atomicAdd(&s_hist[kr[q] >> s12], 1u);
+    }
+    __syncthreads();
+    {  // exclusive scan of the NB bucket counts (NB / BT consecutive per thread)
+        constexpr int PT = NB / BT;
+        unsigned v[PT], sum = 0;
+#pragma unroll
+        for (int u = 0; u < PT; u++) {
+            v[u] = s_hist[threadIdx.x * PT + u];
+            sum += v[u];
+        }
+        unsigned all;
+        unsigned run = excl_scan_256(sum, s_w, all);
+#pragma unroll
+        for (int u = 0; u < PT; u++) {
+            s_hist[threadIdx.x * PT + u] = run;
+            run += v[u];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < IPT; q++) {
+        if (q * BT + (int)threadIdx.x < cnt) {
+            const unsigned pos = atomicAdd(&s_hist[kr[q] >> s12], 1u);
+            s_item[pos] = ((unsigned long long)kr[q] << 32) | src[q];
+        }
+    }
+    __syncthreads();
+    // runs of equal buckets: exact (z, idx) order (insertion sort; long runs -> fallback)
+    for (int i = threadIdx.x; i < cnt; i += BT) {
+        const unsigned bi = (unsigned)(s_item[i] >> 32) >> s12;
+        if (i > 0 && ((unsigned)(s_item[i - 1] >> 32) >> s12) == bi) continue;
+        int j = i + 1;
+        while (j < cnt && ((unsigned)(s_item[j] >> 32) >> s12) == bi && j - i <= RUN_SHORT) j++;
+        if (j - i > RUN_SHORT) {
+            s_flag = 1;
+            continue;
+        }
+        for (int a = i + 1; a < j; a++) {
+            const unsigned long long x = s_item[a];
+            int b = a - 1;
+            while (b >= i && item_less(key64, x, s_item[b])) {
+                s_item[b + 1] = s_item[b];
+                b--;
+            }
+            s_item[b + 1] = x;
+        }
+    }
+    __syncthreads();
+    if (s_flag) {
+        sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,
+                  srcbits, s_wc, s_w, s_red, &s_flag);
+        return;
+    }
+    for (int i = threadIdx.x; i < cnt; i += BT) ent_src[base + i] = (unsigned)s_item[i];
+}
+
+void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
+                    unsigned* tcnt, unsigned* mat, int* tile_start, ulonglong2* bucket, long long cap,
+                    unsigned* overflow, cudaStream_t st) {
+    const int nchunk = (int)((n + BIN_CHUNK - 1) / BIN_CHUNK);
+    const int smem = ntiles * (int)sizeof(unsigned);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BIN_MAX_TILES);
+        cudaFuncSetAttribute(k_bin_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BIN_MAX_TILES);
+        attr = true;
+    }
+    if (n > 0) {
+        k_bin_count<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat);
+        k_bin_cols<<<(ntiles + 31) / 32, 256, 0, st>>>(nchunk, ntiles, mat, tcnt);
+    } else {
+        cudaMemsetAsync(tcnt, 0, sizeof(unsigned) * ntiles, st);
+    }
+    k_tile_scan<<<1, 1024, 0, st>>>(ntiles, tcnt, tile_start, cap, overflow);
+    if (n > 0)
+        k_bin_fill<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, bucket);
+}
+
+size_t bin_matrix_bytes(long long n, int ntiles) {
+    const long long nchunk = (n + BIN_CHUNK - 1) / BIN_CHUNK;
+    return sizeof(unsigned) * (size_t)(nchunk > 0 ? nchunk : 1) * (size_t)ntiles;
+}
+
+int bin_max_tiles() { return BIN_MAX_TILES; }
+
+void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const ulonglong2* bucket,
+                    const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4], cudaStream_t st) {
+    const int srcbits = n > 1 ? 64 - __builtin_clzll((unsigned long long)(n - 1)) : 1;
+    k_tile_sort<2048, 4096><<<ntiles, BT, 0, st>>>(ntiles, tile_start, bucket, key64, ent_src, scratch[0],
+                                                  scratch[1], scratch[2], scratch[3], srcbits);
+}
+
+}  // namespace ts
