@@ -32,6 +32,7 @@ namespace {
 constexpr int BT = 256;       // threads per CTA
 constexpr int BW = BT / 32;   // warps
 constexpr int RUN_SHORT = 48; // runs up to this length are insertion-sorted by one thread
+constexpr int RUN_LONG = 64;  // buckets up to this length are ranked item by item
 
 __device__ __forceinline__ unsigned excl_scan_256(unsigned v, unsigned* s_w, unsigned& total) {
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -395,7 +396,6 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
         s_red[BW + warp] = hi;
     }
     for (int b = threadIdx.x; b < NB; b += BT) s_hist[b] = 0u;
-    if (threadIdx.x == 0) s_flag = 0;
     __syncthreads();
     lo = s_red[0];
     hi = s_red[BW];
@@ -442,33 +442,28 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
         }
     }
     __syncthreads();
-    // runs of equal buckets: exact (z, idx) order (insertion sort; long runs -> fallback)
+    // exact (z, idx) order inside every bucket: an item's final position is
+    // its bucket's start plus the number of bucket items ordered before it
+    // (s_hist[b] now holds the end of bucket b); long buckets -> fallback
+    int longb = 0;
     for (int i = threadIdx.x; i < cnt; i += BT) {
-        const unsigned bi = (unsigned)(s_item[i] >> 32) >> s12;
-        if (i > 0 && ((unsigned)(s_item[i - 1] >> 32) >> s12) == bi) continue;
-        int j = i + 1;
-        while (j < cnt && ((unsigned)(s_item[j] >> 32) >> s12) == bi && j - i <= RUN_SHORT) j++;
-        if (j - i > RUN_SHORT) {
-            s_flag = 1;
+        const unsigned long long x = s_item[i];
+        const unsigned b = (unsigned)(x >> 32) >> s12;
+        const int be = (int)s_hist[b], bs = b ? (int)s_hist[b - 1] : 0;
+        if (be - bs > RUN_LONG) {
+            longb = 1;
             continue;
         }
-        for (int a = i + 1; a < j; a++) {
-            const unsigned long long x = s_item[a];
-            int b = a - 1;
-            while (b >= i && item_less(key64, x, s_item[b])) {
-                s_item[b + 1] = s_item[b];
-                b--;
-            }
-            s_item[b + 1] = x;
+        int rank = 0;
+        for (int j = bs; j < be; j++) {
+            const unsigned long long y = s_item[j];
+            if (y != x) rank += item_less(key64, y, x);
         }
+        ent_src[base + bs + rank] = (unsigned)x;
     }
-    __syncthreads();
-    if (s_flag) {
+    if (__syncthreads_or(longb))
         sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,
                   srcbits, s_wc, s_w, s_red, &s_flag);
-        return;
-    }
-    for (int i = threadIdx.x; i < cnt; i += BT) ent_src[base + i] = (unsigned)s_item[i];
 }
 
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
