@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         double g_phi;
                         if (mode == 0) {
                             const double rc = fmin(r64, 1.0);
-                            g[7] = g_win * window * ((double)fast_lg2((float)rc) * 0.6931471805599453);
+                            g[7] = g_win * window * log(rc);
                             const double g_r = g_win * (double)par.y * window / rc;
                             if (r64 >= 1.0) {
                                 g_phi = 0.0;

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                     const double phi = r64 * phis;
                     double g_phi;
                     if (mode == 0) {
-                        gf[7] = (AT)(g_win * window * ((double)fast_lg2((float)rc) * 0.6931471805599453));
+                        gf[7] = (AT)(g_win * window * log(rc));
                         const double g_r = g_win * sg * window / rc;
                         if (r64 >= 1.0) {
                             g_phi = 0.0;

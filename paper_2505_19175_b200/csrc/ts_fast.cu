@@ -36,16 +36,17 @@ constexpr float ALPHA_CLAMP_F = 0.99f;
 // (render.py:216-250, tile lists).  Edge functions, the contribution band and
 // the SH colour only need to be accurate and use fast math.
 // ---------------------------------------------------------------------------
-// SH colour sum over 16-byte vector loads (fp32 params) / 16-byte pairs (fp64)
+// SH colour sum (fp64 basis and accumulation) over 16-byte vector loads
+// (fp32 params) / scalar loads (fp64)
 template <typename T>
-__device__ __forceinline__ void sh_colour(const T* __restrict__ p, const float* bs, int ncoef, float& c0,
-                                          float& c1, float& c2);
+__device__ __forceinline__ void sh_colour(const T* __restrict__ p, const double* bs, int ncoef, double& c0,
+                                          double& c1, double& c2);
 template <>
-__device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, const float* bs, int ncoef,
-                                                 float& c0, float& c1, float& c2) {
+__device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, const double* bs, int ncoef,
+                                                 double& c0, double& c1, double& c2) {
     const float4* q = reinterpret_cast<const float4*>(p);
     const int nv = (ncoef * 3 + 3) >> 2;
-    float acc[3] = {c0, c1, c2};
+    double acc[3] = {c0, c1, c2};
 #pragma unroll
     for (int k = 0; k < 12; k++) {
         if (k < nv) {
@@ -54,17 +55,17 @@ __device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, co
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int idx = k * 4 + u;  // coefficient idx / 3, channel idx % 3
-                if (idx / 3 < ncoef) acc[idx % 3] = fmaf(bs[idx / 3], vv[u], acc[idx % 3]);
+                if (idx / 3 < ncoef) acc[idx % 3] = fma(bs[idx / 3], (double)vv[u], acc[idx % 3]);
             }
         }
     }
     c0 = acc[0]; c1 = acc[1]; c2 = acc[2];
 }
 template <>
-__device__ __forceinline__ void sh_colour<double>(const double* __restrict__ p, const float* bs, int ncoef,
-                                                  float& c0, float& c1, float& c2) {
-    float acc[3] = {c0, c1, c2};
-    for (int idx = 0; idx < ncoef * 3; idx++) acc[idx % 3] = fmaf(bs[idx / 3], (float)p[idx], acc[idx % 3]);
+__device__ __forceinline__ void sh_colour<double>(const double* __restrict__ p, const double* bs, int ncoef,
+                                                  double& c0, double& c1, double& c2) {
+    double acc[3] = {c0, c1, c2};
+    for (int idx = 0; idx < ncoef * 3; idx++) acc[idx % 3] = fma(bs[idx / 3], p[idx], acc[idx % 3]);
     c0 = acc[0]; c1 = acc[1]; c2 = acc[2];
 }
 
@@ -224,32 +225,34 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
             r.r_lo = rstar - delta - fabs(rstar) * 1e-12;
             r.r_hi = rstar + delta + fabs(rstar) * 1e-12;
             r.phis = phis;
-            // view-dependent SH colour (render.py:292-302) in fp32: only the value is used here
-            float u0 = (float)((v[0] + v[3] + v[6]) * (1.0 / 3.0) - cam.cc[0]);
-            float u1 = (float)((v[1] + v[4] + v[7]) * (1.0 / 3.0) - cam.cc[1]);
-            float u2 = (float)((v[2] + v[5] + v[8]) * (1.0 / 3.0) - cam.cc[2]);
-            const float iu = rsqrtf(fmaxf(u0 * u0 + u1 * u1 + u2 * u2, 1e-24f));
+            // view-dependent SH colour (render.py:292-302) in fp64 (rounded once to
+            // fp32: the backward's colour differences cancel, fp32 sums cost ~1e-4)
+            double u0 = (v[0] + v[3] + v[6]) * (1.0 / 3.0) - cam.cc[0];
+            double u1 = (v[1] + v[4] + v[7]) * (1.0 / 3.0) - cam.cc[1];
+            double u2 = (v[2] + v[5] + v[8]) * (1.0 / 3.0) - cam.cc[2];
+            const double iu = rsqrt(fmax(u0 * u0 + u1 * u1 + u2 * u2, 1e-48));
             u0 *= iu; u1 *= iu; u2 *= iu;
-            const float xx = u0 * u0, yy = u1 * u1, zz = u2 * u2;
-            float bs[16];
-            bs[0] = 0.28209479177387814f;
-            bs[1] = -0.4886025119029199f * u1;
-            bs[2] = 0.4886025119029199f * u2;
-            bs[3] = -0.4886025119029199f * u0;
-            bs[4] = 1.0925484305920792f * u0 * u1;
-            bs[5] = -1.0925484305920792f * u1 * u2;
-            bs[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
-            bs[7] = -1.0925484305920792f * u0 * u2;
-            bs[8] = 0.5462742152960396f * (xx - yy);
-            bs[9] = -0.5900435899266435f * u1 * (3.f * xx - yy);
-            bs[10] = 2.890611442640554f * u0 * u1 * u2;
-            bs[11] = -0.4570457994644658f * u1 * (4.f * zz - xx - yy);
-            bs[12] = 0.3731763325901154f * u2 * (2.f * zz - 3.f * xx - 3.f * yy);
-            bs[13] = -0.4570457994644658f * u0 * (4.f * zz - xx - yy);
-            bs[14] = 1.445305721320277f * u2 * (xx - yy);
-            bs[15] = -0.5900435899266435f * u0 * (xx - 3.f * yy);
-            float c0 = 0.5f, c1 = 0.5f, c2 = 0.5f;
-            sh_colour<T>(shp, bs, opt.ncoef, c0, c1, c2);
+            const double xx = u0 * u0, yy = u1 * u1, zz = u2 * u2;
+            double bs[16];
+            bs[0] = 0.28209479177387814;
+            bs[1] = -0.4886025119029199 * u1;
+            bs[2] = 0.4886025119029199 * u2;
+            bs[3] = -0.4886025119029199 * u0;
+            bs[4] = 1.0925484305920792 * u0 * u1;
+            bs[5] = -1.0925484305920792 * u1 * u2;
+            bs[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+            bs[7] = -1.0925484305920792 * u0 * u2;
+            bs[8] = 0.5462742152960396 * (xx - yy);
+            bs[9] = -0.5900435899266435 * u1 * (3.0 * xx - yy);
+            bs[10] = 2.890611442640554 * u0 * u1 * u2;
+            bs[11] = -0.4570457994644658 * u1 * (4.0 * zz - xx - yy);
+            bs[12] = 0.3731763325901154 * u2 * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            bs[13] = -0.4570457994644658 * u0 * (4.0 * zz - xx - yy);
+            bs[14] = 1.445305721320277 * u2 * (xx - yy);
+            bs[15] = -0.5900435899266435 * u0 * (xx - 3.0 * yy);
+            double d0 = 0.5, d1 = 0.5, d2 = 0.5;
+            sh_colour<T>(shp, bs, opt.ncoef, d0, d1, d2);
+            const float c0 = (float)d0, c1 = (float)d1, c2 = (float)d2;
             r.rgb[0] = fminf(fmaxf(c0, 0.f), 1.f);
             r.rgb[1] = fminf(fmaxf(c1, 0.f), 1.f);
             r.rgb[2] = fminf(fmaxf(c2, 0.f), 1.f);
