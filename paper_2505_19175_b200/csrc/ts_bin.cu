@@ -120,13 +120,17 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_count(long long n, const short4*
     for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cnt[t] = 0u;
     __syncthreads();
     const long long c0 = (long long)blockIdx.x * BIN_CHUNK;
-#pragma unroll 2
+    short4 bb[BIN_PER];  // all loads in flight before the first use
+#pragma unroll
     for (int k = 0; k < BIN_PER; k++) {
         const long long i = c0 + k * BIN_CT + threadIdx.x;
-        if (i >= n) break;
-        const short4 bb = __ldg(bbox + i);
-        if (bb.y <= bb.x || bb.w <= bb.z) continue;
-        const int tx0 = bb.x / TILE, tx1 = (bb.y - 1) / TILE + 1, ty0 = bb.z / TILE, ty1 = (bb.w - 1) / TILE + 1;
+        bb[k] = i < n ? __ldg(bbox + i) : make_short4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < BIN_PER; k++) {
+        if (bb[k].y <= bb[k].x || bb[k].w <= bb[k].z) continue;
+        const int tx0 = bb[k].x / TILE, tx1 = (bb[k].y - 1) / TILE + 1;
+        const int ty0 = bb[k].z / TILE, ty1 = (bb[k].w - 1) / TILE + 1;
         for (int ty = ty0; ty < ty1; ty++)
             for (int tx = tx0; tx < tx1; tx++) atomicAdd(&s_cnt[ty * ntx + tx], 1u);
     }
@@ -172,18 +176,24 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* 
     for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cur[t] = (unsigned)tile_start[t] + row[t];
     __syncthreads();
     const long long c0 = (long long)blockIdx.x * BIN_CHUNK;
-#pragma unroll 2
+    short4 bb[BIN_PER];
+    unsigned long long key[BIN_PER];
+#pragma unroll
     for (int k = 0; k < BIN_PER; k++) {
         const long long i = c0 + k * BIN_CT + threadIdx.x;
-        if (i >= n) break;
-        const short4 bb = __ldg(bbox + i);
-        if (bb.y <= bb.x || bb.w <= bb.z) continue;
-        const unsigned long long key = __ldg(key64 + i);
-        const int tx0 = bb.x / TILE, tx1 = (bb.y - 1) / TILE + 1, ty0 = bb.z / TILE, ty1 = (bb.w - 1) / TILE + 1;
+        bb[k] = i < n ? __ldg(bbox + i) : make_short4(0, 0, 0, 0);
+        key[k] = i < n ? __ldg(key64 + i) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < BIN_PER; k++) {
+        if (bb[k].y <= bb[k].x || bb[k].w <= bb[k].z) continue;
+        const unsigned long long i = (unsigned long long)(c0 + k * BIN_CT + threadIdx.x);
+        const int tx0 = bb[k].x / TILE, tx1 = (bb[k].y - 1) / TILE + 1;
+        const int ty0 = bb[k].z / TILE, ty1 = (bb[k].w - 1) / TILE + 1;
         for (int ty = ty0; ty < ty1; ty++)
             for (int tx = tx0; tx < tx1; tx++) {
                 const unsigned pos = atomicAdd(&s_cur[ty * ntx + tx], 1u);
-                bucket[pos] = make_ulonglong2(key, (unsigned long long)i);
+                bucket[pos] = make_ulonglong2(key[k], i);
             }
     }
 }

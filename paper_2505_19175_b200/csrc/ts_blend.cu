@@ -4,13 +4,20 @@
 // CTA per 16x16 tile, 256 threads, thread = pixel for compositing.  The tile's
 // entry list (depth-rank order) is consumed in batches of at most DB entries /
 // PCAP pairs:
-//   1. stage     -- records arrive in a cp.async ring one batch ahead (source
-//                   ids two batches ahead); warp 0 builds the rectangles
-//                   bbox ∩ tile, their pair scan and the batch size;
+//   1. geometry  -- records arrive in a cp.async ring one batch ahead (source
+//                   ids two batches ahead).  Thread (entry j = tid/4, rows
+//                   4q..4q+3) clips every row of the rectangle bbox ∩ tile to
+//                   the span of pixel centres that can pass r >= r_lo (three
+//                   half-planes, fp64, widened by 1e-6 px: a superset of the
+//                   passing pixels); pairs = pixels of the spans, numbered
+//                   entry-major, row by row.  Scans over the 4 threads of an
+//                   entry and over entries give the segment (entry, row) table,
+//                   the batch size (<= PCAP pairs) and the pair-word tables;
 //   2. evaluate  -- the batch's pairs are split over the warps, 32 consecutive
 //                   pairs per step, so every lane evaluates a pixel inside its
 //                   entry's bbox (the reference's per-pixel bbox test,
-//                   _kernels.py:87-95, costs nothing).  A pair whose
+//                   _kernels.py:87-95, costs nothing) and near its pass
+//                   region (~2.5x fewer pairs than the rectangles).  A pair whose
 //                   r = phi/phi_s passes the lower end of the contribution band
 //                   stores r (NaN = inside the band) and sets bit `entry` of the
 //                   pixel's batch mask;
@@ -45,11 +52,13 @@ struct DenseSmem {
     unsigned srcq[SR];
     float4 col[DB];                // rgb, f0
     float f1[DB];
-    int S[DB + 1];                 // first pair of entry j
-    unsigned starts[PCAP / 32];    // bit (k & 31) of word k >> 5: an entry starts at pair k
-    int jfirst[PCAP / 32];         // entry holding pair 32 w
-    unsigned geo[DB];              // cx0 | cy0<<4 | w<<8 | magic<<16
-    int2 kb[DB];                   // pair of pixel (lx, ly) = x + ly * y + lx
+    unsigned seg[DB * TILE];       // segment s (one row of one entry): first pair | j<<13 | row<<19 | xa<<23
+    unsigned rowtab[DB][TILE];     // row ly of entry j: first pair | xa<<16 (rows with a non-empty span)
+    unsigned starts[PCAP / 32];    // bit (k & 31) of word k >> 5: a segment starts at pair k
+    int jfirst[PCAP / 32];         // segment holding pair 32 w
+    unsigned ein[DB];              // per entry: inclusive (pairs<<16 | segments) within its warp
+    unsigned wtot[8];              // per warp: (pairs<<16 | segments) of its 8 entries
+    int total;                     // pairs of the batch
     double2 osj[ACC64 ? DB : 1];   // (opacity, sigma) of batch entry j
     unsigned pbits[ACC64 ? PCAP / 32 : 1];      // training: pair k passes (record slots)
     int wpre[ACC64 ? PCAP / 32 + 1 : 1];        // passing pairs before word w
@@ -57,7 +66,6 @@ struct DenseSmem {
     unsigned maxw[DB];
     int pix[DB];
     double xc[TILE], yc[TILE];     // pixel centres of the tile (fp64)
-    int nb;
 };
 
 template <int DB, int PCAP, bool ACC64, typename PT, int MINB>
@@ -120,6 +128,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
     __syncthreads();
     for (int c = tid; c < (rhi - s) * 8; c += 256) fetch_rec(s + (c >> 3), c & 7);
     cp_async_commit();
+    if (tid < PCAP / 32) sm.starts[tid] = 0u;
     int nb = 0;
     for (int b = s; b < e; b += nb) {
         cp_async_wait_all();
@@ -130,81 +139,144 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             for (int p = shi + tid; p < nshi; p += 256) cp_async4(&sm.srcq[p & (SR - 1)], ent_src + p);
             shi = max(shi, nshi);
         }
-        // ---- 1. rectangles, pair scan, batch size (warp 0); clear the masks ----
+        // ---- 1. geometry: thread (entry j, rows 4q..4q+3); clear the masks ----
+        static_assert(DB == 64 && PCAP <= 8192, "geometry layout: 4 threads per entry, 13-bit pair ids");
 #pragma unroll
         for (int w = 0; w < NW; w++) sm.mask[w][tid] = 0u;
-        if (warp == 0) {
-            int cx0[NW], cy0[NW], w[NW], h[NW], incl[NW];
-            bool valid[NW];
-            int carry = 0;
+        {
+            const int j = tid >> 2, q = tid & 3;
+            const bool vj = j < navail;
+            const int slot = (b + j) & (RR - 1);
+            // rows cy0 + q + 4m of the rectangle (strided: the 4 threads share its rows evenly)
+            int xa[4], len[4], cy0 = 0;
 #pragma unroll
-            for (int hf = 0; hf < NW; hf++) {
-                const int j = (int)lane + 32 * hf;
-                valid[hf] = j < navail;
-                cx0[hf] = cy0[hf] = w[hf] = h[hf] = 0;
-                if (valid[hf]) {
-                    const int slot = (b + j) & (RR - 1);
-                    const float4 t0 = reinterpret_cast<const float4*>(&sm.tail[slot])[0];
-                    const int4 t1 = reinterpret_cast<const int4*>(&sm.tail[slot])[1];
-                    const int bx0 = (short)(t1.y & 0xffff), bx1 = (short)(t1.y >> 16);
-                    const int by0 = (short)(t1.z & 0xffff), by1 = (short)(t1.z >> 16);
-                    cx0[hf] = max(bx0 - X0, 0);
-                    cy0[hf] = max(by0 - Y0, 0);
-                    w[hf] = max(min(bx1 - X0, TILE) - cx0[hf], 0);
-                    h[hf] = max(min(by1 - Y0, TILE) - cy0[hf], 0);
+            for (int m = 0; m < 4; m++) xa[m] = len[m] = 0;
+            if (vj) {
+                const float4 t0 = reinterpret_cast<const float4*>(&sm.tail[slot])[0];
+                const int4 t1 = reinterpret_cast<const int4*>(&sm.tail[slot])[1];
+                const int bx0 = (short)(t1.y & 0xffff), bx1 = (short)(t1.y >> 16);
+                const int by0 = (short)(t1.z & 0xffff), by1 = (short)(t1.z >> 16);
+                const int cx0 = max(bx0 - X0, 0), cx1 = min(bx1 - X0, TILE) - 1;
+                cy0 = max(by0 - Y0, 0);
+                const int cy1 = min(by1 - Y0, TILE) - 1;
+                if (q == 0) {
                     sm.col[j] = make_float4(t0.z, t0.w, __int_as_float(t1.x), t0.x);
                     sm.f1[j] = t0.y;
                     if constexpr (ACC64)
                         sm.osj[j] = make_double2(opt.solid ? 1.0 : (double)sm.os[slot][0], (double)sm.os[slot][1]);
                 }
-                int a = w[hf] * h[hf];
+                if (cy0 + q <= cy1 && cx0 <= cx1) {
+                    const EvalRec& R = sm.ev[slot];
+                    const double rlo = R.r_lo, xl = sm.xc[0], y0 = sm.yc[cy0 + q];
+                    // per edge: r_lo - l(xl, y) at the thread's first row, its step per 4 rows, 1/a0
+                    double n0[3], st[3];
+                    float inv[3];
+                    int sgn[3];
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, a, off);
-                    if ((int)lane >= off) a += y;
+                    for (int ed = 0; ed < 3; ed++) {
+                        const double a0 = R.a[3 * ed], a1 = R.a[3 * ed + 1];
+                        n0[ed] = rlo - fma(a0, xl, fma(a1, y0, R.a[3 * ed + 2]));
+                        st[ed] = -4.0 * a1;
+                        sgn[ed] = a0 > 0.0 ? 1 : (a0 < 0.0 ? -1 : 0);
+                        inv[ed] = __fdividef(1.f, (float)a0);
+                        if (!(fabsf(inv[ed]) < 1e30f)) sgn[ed] = a0 == 0.0 ? 0 : 2;  // |a0| tiny: no bound
+                    }
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        const int row = cy0 + q + 4 * m;
+                        if (row > cy1) break;
+                        int lo = cx0, hi = cx1;
+#pragma unroll
+                        for (int ed = 0; ed < 3; ed++) {
+                            // a0 * (xl + lx) + c >= r_lo: lx >= / <= (r_lo - l(xl)) / a0,
+                            // in fp32 widened by 1e-3 px (a superset of the passing pixels)
+                            const double num = fma((double)m, st[ed], n0[ed]);
+                            const float tb = fminf(fmaxf((float)num * inv[ed], -64.f), 64.f);
+                            if (sgn[ed] == 1) lo = max(lo, __float2int_ru(tb - 1e-3f));
+                            else if (sgn[ed] == -1) hi = min(hi, __float2int_rd(tb + 1e-3f));
+                            else if (sgn[ed] == 0 && num > 1e-9 * (fabs(rlo) + 1.0)) hi = -1;  // a0 == 0
+                        }
+                        xa[m] = lo;
+                        len[m] = max(hi - lo + 1, 0);
+                    }
                 }
-                incl[hf] = a + carry;
-                carry = __shfl_sync(0xffffffffu, incl[hf], 31);
             }
+            // row-major pair / segment numbering within the entry: row cy0 + q + 4m
+            // follows all rows of levels < m and the rows of level m with smaller q
+            unsigned lev[4], exl[4];
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                const unsigned vm = ((unsigned)len[m] << 16) | (unsigned)(len[m] > 0);
+                unsigned x = vm;
+                const unsigned y1 = __shfl_up_sync(0xffffffffu, x, 1);
+                if (q >= 1) x += y1;
+                const unsigned y2 = __shfl_up_sync(0xffffffffu, x, 2);
+                if (q >= 2) x += y2;
+                exl[m] = x - vm;
+                lev[m] = __shfl_sync(0xffffffffu, x, (int)lane | 3);
+            }
+            const unsigned et = lev[0] + lev[1] + lev[2] + lev[3];  // entry total (pairs<<16 | segments)
+            // scans: entries within the warp, warps
+            unsigned ei = et;
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, ei, off);
+                if ((int)lane >= off) ei += y;
+            }
+            if (q == 0) sm.ein[j] = ei;
+            if (lane == 31) sm.wtot[warp] = ei;
+            __syncthreads();
+            unsigned wpre = 0;
+            for (int w2 = 0; w2 < (int)warp; w2++) wpre += sm.wtot[w2];
             // batch = longest prefix of entries whose pairs fit in PCAP (>= 1 entry)
             int n = 0;
-            bool full = true;
+            {
+                unsigned all = 0;
 #pragma unroll
-            for (int hf = 0; hf < NW; hf++) {
-                const unsigned bm = __ballot_sync(0xffffffffu, valid[hf] && incl[hf] <= PCAP);
-                if (full) n += __popc(bm);
-                full = full && bm == 0xffffffffu;
-            }
-            n = max(n, 1);
-#pragma unroll
-            for (int hf = 0; hf < NW; hf++) {
-                const int j = (int)lane + 32 * hf;
-                const int excl = incl[hf] - w[hf] * h[hf];
-                sm.S[j + 1] = incl[hf];
-                const unsigned magic = w[hf] ? (32768u + (unsigned)w[hf] - 1u) / (unsigned)w[hf] : 0u;
-                sm.geo[j] = (unsigned)cx0[hf] | ((unsigned)cy0[hf] << 4) | ((unsigned)w[hf] << 8) | (magic << 16);
-                sm.kb[j] = make_int2(excl - cy0[hf] * w[hf] - cx0[hf], w[hf]);
-            }
-            // pair-word tables of the batch (entries < n): entry starts and the
-            // entry holding the first pair of every 32-pair word
-            for (int w = (int)lane; w < PCAP / 32; w += 32) sm.starts[w] = 0u;
-            __syncwarp();
-#pragma unroll
-            for (int hf = 0; hf < NW; hf++) {
-                const int jq = (int)lane + 32 * hf;
-                if (jq < n) {
-                    const int excl = incl[hf] - w[hf] * h[hf];
-                    atomicOr(&sm.starts[excl >> 5], 1u << (excl & 31));
-                    for (int wq = (excl + 31) >> 5; wq <= ((incl[hf] - 1) >> 5); wq++) sm.jfirst[wq] = jq;
+                for (int w2 = 0; w2 < 8; w2++) all += sm.wtot[w2];
+                if ((all >> 16) <= (unsigned)PCAP) {
+                    n = navail;
+                } else {
+                    unsigned cum = 0;
+                    for (int w2 = 0; w2 < 8; w2++) {
+                        const unsigned wt = sm.wtot[w2];
+                        if (((cum + wt) >> 16) <= (unsigned)PCAP && (w2 + 1) * 8 <= navail) {
+                            cum += wt;
+                            n += 8;
+                            continue;
+                        }
+                        for (int u = 0; u < 8; u++) {
+                            const int jj = w2 * 8 + u;
+                            if (jj >= navail || ((cum + sm.ein[jj]) >> 16) > (unsigned)PCAP) break;
+                            n++;
+                        }
+                        break;
+                    }
+                    n = max(n, 1);
                 }
             }
-            if (lane == 0) {
-                sm.S[0] = 0;
-                sm.nb = n;
+            nb = n;
+            if (j < n) {
+                unsigned base = wpre + ei - et;  // the entry's first (pair, segment)
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    if (len[m] > 0) {
+                        const int ly2 = cy0 + q + 4 * m;
+                        const unsigned pm = base + exl[m];
+                        const unsigned P0 = pm >> 16, S0 = pm & 0xffffu;
+                        sm.rowtab[j][ly2] = P0 | ((unsigned)xa[m] << 16);
+                        sm.seg[S0] = P0 | ((unsigned)j << 13) | ((unsigned)ly2 << 19) | ((unsigned)xa[m] << 23);
+                        atomicOr(&sm.starts[P0 >> 5], 1u << (P0 & 31));
+                        // a segment (<= 16 pairs) holds at most one word start
+                        const unsigned wq = (P0 + 31) >> 5;
+                        if ((wq << 5) <= P0 + (unsigned)len[m] - 1u) sm.jfirst[wq] = (int)S0;
+                    }
+                    base += lev[m];
+                }
+                if (j == n - 1 && q == 0) sm.total = (int)((wpre + ei) >> 16);
             }
         }
         __syncthreads();
-        nb = sm.nb;
         {  // records of the next window [b+nb, b+nb+DB) (their ids arrived in an earlier batch)
             const int nrhi = min(b + nb + DB, e);
             for (int c = tid; c < (nrhi - rhi) * 8; c += 256) fetch_rec(rhi + (c >> 3), c & 7);
@@ -214,23 +286,20 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
         // ---- 2. evaluate: warp w takes a contiguous range of pairs, 32 consecutive
         //         pairs per step (lane-uniform control flow, broadcast record loads) ----
         {
-            const int total = sm.S[nb];
+            const int total = sm.total;
             const int chunk = ((total + 255) >> 8) << 5;
             const int k0 = (int)warp * chunk;
             const int kE = min(k0 + chunk, total);
             for (int kb = k0; kb < kE; kb += 32) {
                 const int k = kb + (int)lane;
                 bool pass = false;
-                // entry of pair k: the word's first entry plus the entry starts in (kb, k]
-                const int j = sm.jfirst[kb >> 5] + __popc(sm.starts[kb >> 5] & ((2u << lane) - 2u));
-                const int sj = sm.S[j];
+                // segment of pair k: the word's first segment plus the segment starts in (kb, k]
+                const int sk = sm.jfirst[kb >> 5] + __popc(sm.starts[kb >> 5] & ((2u << lane) - 2u));
                 if (k < kE) {
-                    const unsigned g = sm.geo[j];
-                    const int w = (g >> 8) & 31;
-                    const int local = k - sj;
-                    const int dy = (int)(((unsigned)local * (g >> 16)) >> 15);
-                    const int qx = (int)(g & 15) + local - dy * w;
-                    const int qy = (int)((g >> 4) & 15) + dy;
+                    const unsigned sg = sm.seg[sk];
+                    const int j = (int)((sg >> 13) & 63u);
+                    const int qx = (int)(sg >> 23) + k - (int)(sg & 0x1fffu);
+                    const int qy = (int)((sg >> 19) & 15u);
                     const double pcx = sm.xc[qx], pcy = sm.yc[qy];
                     const EvalRec& r = sm.ev[(b + j) & (RR - 1)];
                     const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
@@ -251,11 +320,12 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             }
         }
         __syncthreads();
+        if (tid < PCAP / 32) sm.starts[tid] = 0u;  // for the next batch (read by the evaluation only)
         if constexpr (ACC64) {
             // record slots of the batch: passing pairs in entry-major order
             if (out.frec) {
                 if (warp == 0) {
-                    const int total = sm.S[nb];
+                    const int total = sm.total;
                     const int nwd = (total + 31) >> 5;
                     int carry = 0;
                     for (int w0 = 0; w0 < nwd; w0 += 32) {
@@ -294,8 +364,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             while (hm) {
                 const int j = __ffsll((long long)hm) - 1;
                 hm &= hm - 1;
-                const int2 kbh = sm.kb[j];
-                const int kh = kbh.x + ly * kbh.y + lx;
+                const unsigned rth = sm.rowtab[j][ly];
+                const int kh = (int)(rth & 0xffffu) + lx - (int)(rth >> 16);
                 const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
                 out.frec[rb + slot].pix = ~0u;
             }
@@ -307,8 +377,9 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 while (mm) {
                     const int j = __ffsll((long long)mm) - 1;
                     mm &= mm - 1;
-                    const int2 kb = sm.kb[j];
-                    const Real rv = sm.r[kb.x + ly * kb.y + lx];
+                    const unsigned rt = sm.rowtab[j][ly];
+                    const int kp = (int)(rt & 0xffffu) + lx - (int)(rt >> 16);
+                    const Real rv = sm.r[kp];
                     if (isnan(rv)) {  // r inside the contribution band
                         flag_pos = b + j;
                         done = true;
@@ -340,7 +411,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                             break;
                         }
                         if (rb != ~0ull) {
-                            const int kr = kb.x + ly * kb.y + lx;
+                            const int kr = kp;
                             const int slot = sm.wpre[kr >> 5] + __popc(sm.pbits[kr >> 5] & ((1u << (kr & 31)) - 1u));
                             double4* fr = reinterpret_cast<double4*>(out.frec + rb + slot);
                             fr[0] = make_double4((double)T, (double)C0, (double)C1, (double)C2);
@@ -455,7 +526,7 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
         const double* o = (const double*)soup.opacity;
         const double* sg = (const double*)soup.sigma;
         if (acc64) launch_dense<64, 2048, true, double, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 4096, false, double, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else launch_dense<64, 2048, false, double, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     } else {
         const float* o = (const float*)soup.opacity;
         const float* sg = (const float*)soup.sigma;
@@ -465,8 +536,8 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
         }();
         // render: 5 CTAs per SM (48 registers); training (fp64 compositing): 4 (64 registers)
         if (acc64) launch_dense<64, 2048, true, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else if (variant == 1) launch_dense<64, 2048, false, float, 6>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 4096, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else if (variant == 1) launch_dense<64, 4096, false, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else launch_dense<64, 2048, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     }
 }
 
