@@ -171,20 +171,23 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                     // per edge: r_lo - l(xl, y) at the thread's first row, its step per 4 rows, 1/a0
                     double n0[3], st[3];
                     float inv[3];
-                    int sgn[3];
+                    bool up[3], dn[3], zr[3];  // bound below (a0 > 0) / above (a0 < 0) / a0 == 0
 #pragma unroll
                     for (int ed = 0; ed < 3; ed++) {
                         const double a0 = R.a[3 * ed], a1 = R.a[3 * ed + 1];
                         n0[ed] = rlo - fma(a0, xl, fma(a1, y0, R.a[3 * ed + 2]));
                         st[ed] = -4.0 * a1;
-                        sgn[ed] = a0 > 0.0 ? 1 : (a0 < 0.0 ? -1 : 0);
                         inv[ed] = __fdividef(1.f, (float)a0);
-                        if (!(fabsf(inv[ed]) < 1e30f)) sgn[ed] = a0 == 0.0 ? 0 : 2;  // |a0| tiny: no bound
+                        const bool fin = fabsf(inv[ed]) < 1e30f;  // |a0| tiny: no bound
+                        up[ed] = a0 > 0.0 && fin;
+                        dn[ed] = a0 < 0.0 && fin;
+                        zr[ed] = a0 == 0.0;
                     }
+                    const int nrow = (cy1 - cy0 - q) / 4 + 1;
+                    const double zthr = 1e-9 * (fabs(rlo) + 1.0);
 #pragma unroll
                     for (int m = 0; m < 4; m++) {
-                        const int row = cy0 + q + 4 * m;
-                        if (row > cy1) break;
+                        if (m >= nrow) break;
                         int lo = cx0, hi = cx1;
 #pragma unroll
                         for (int ed = 0; ed < 3; ed++) {
@@ -192,9 +195,10 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                             // in fp32 widened by 1e-3 px (a superset of the passing pixels)
                             const double num = fma((double)m, st[ed], n0[ed]);
                             const float tb = fminf(fmaxf((float)num * inv[ed], -64.f), 64.f);
-                            if (sgn[ed] == 1) lo = max(lo, __float2int_ru(tb - 1e-3f));
-                            else if (sgn[ed] == -1) hi = min(hi, __float2int_rd(tb + 1e-3f));
-                            else if (sgn[ed] == 0 && num > 1e-9 * (fabs(rlo) + 1.0)) hi = -1;  // a0 == 0
+                            const int lc = __float2int_ru(tb - 1e-3f), hc = __float2int_rd(tb + 1e-3f);
+                            lo = up[ed] ? max(lo, lc) : lo;
+                            hi = dn[ed] ? min(hi, hc) : hi;
+                            hi = (zr[ed] && num > zthr) ? -1 : hi;
                         }
                         xa[m] = lo;
                         len[m] = max(hi - lo + 1, 0);
@@ -442,7 +446,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         a = fminf(a, ALPHA_CLAMP_F);
                         const float wgt = T * a;
                         const float tn = fmaf(-T, a, T);
-                        const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
+                        // (approximate quotient: the tests below keep a 2x margin on en)
+                        const float en = __fdividef(ea * a, 1.f - a) + (epsT + 2.4e-7f);
                         const float ew = epsT + ea + 1.2e-7f;
                         if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
                             fabsf(wgt - tau) <= fmaf(2.f * ew, wgt, 1e-9f)) {
@@ -526,7 +531,7 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
         const double* o = (const double*)soup.opacity;
         const double* sg = (const double*)soup.sigma;
         if (acc64) launch_dense<64, 2048, true, double, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 2048, false, double, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else launch_dense<64, 2048, false, double, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     } else {
         const float* o = (const float*)soup.opacity;
         const float* sg = (const float*)soup.sigma;
@@ -534,10 +539,11 @@ void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, in
             const char* v = getenv("TS_DENSE_VARIANT");
             return v ? atoi(v) : 0;
         }();
-        // render: 5 CTAs per SM (48 registers); training (fp64 compositing): 4 (64 registers)
+        // render and training: 4 CTAs per SM (64 registers, no spills; 5 at 48 spills)
         if (acc64) launch_dense<64, 2048, true, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
         else if (variant == 1) launch_dense<64, 4096, false, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 2048, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else if (variant == 2) launch_dense<64, 2048, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
+        else launch_dense<64, 2048, false, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
     }
 }
 
