@@ -950,9 +950,10 @@ __global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const R
 // k_blend_fast (their decisions were certain); from it on the fix-up does.
 // ---------------------------------------------------------------------------
 constexpr int FXC = 1024;
+constexpr int FX_T = 512, FX_PER = FXC / FX_T;  // threads per CTA, entries per thread
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* __restrict__ opacity,
+__global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const T* __restrict__ opacity,
                                                    const T* __restrict__ sigma, const RecF* __restrict__ rec,
                                                    const int* __restrict__ tile_start,
                                                    const unsigned* __restrict__ ent_src, FastBlendOut out) {
@@ -974,11 +975,32 @@ __global__ void __launch_bounds__(256) k_fixup_fwd(Cam cam, Opts opt, const T* _
         __syncthreads();
         for (int base = s; base < e; base += FXC) {
             const int nb = min(FXC, e - base);
-            for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-                const unsigned src = __ldg(ent_src + base + i);
+            // FX_PER entries per thread, their source ids and bboxes loaded up front
+            unsigned srcs[FX_PER];
+            short4 bbs[FX_PER];
+#pragma unroll
+            for (int u = 0; u < FX_PER; u++) {
+                const int i = (int)threadIdx.x + u * FX_T;
+                srcs[u] = i < nb ? __ldg(ent_src + base + i) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < FX_PER; u++) {
+                const int i = (int)threadIdx.x + u * FX_T;
+                bbs[u] = make_short4(0, 0, 0, 0);
+                if (i < nb) {  // x0..y1 sit at byte 116 of the record (4-byte aligned)
+                    const int xx = __ldg(reinterpret_cast<const int*>(&rec[srcs[u]].x0));
+                    const int yy = __ldg(reinterpret_cast<const int*>(&rec[srcs[u]].y0));
+                    bbs[u] = make_short4((short)(xx & 0xffff), (short)(xx >> 16), (short)(yy & 0xffff), (short)(yy >> 16));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < FX_PER; u++) {
+                const int i = (int)threadIdx.x + u * FX_T;
+                if (i >= nb) break;
+                const unsigned src = srcs[u];
                 const RecF& r = rec[src];
                 double a = 0.0;
-                if (px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
+                if (px >= bbs[u].x && px < bbs[u].y && py >= bbs[u].z && py < bbs[u].w) {
                     const double rr = edge_r(r, px + 0.5, py + 0.5);
                     a = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, src);
                     if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
@@ -1086,12 +1108,14 @@ void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                       cudaStream_t st) {
-    const int grid = 148 * 4;
+    // 2 entries per thread of a 1024-entry chunk: the dependent record loads of
+    // the whole chunk are in flight at once
+    const int grid = 148 * 2;
     if (dtype == 1)
-        k_fixup_fwd<double><<<grid, 256, 0, st>>>(cam, opt, (const double*)soup.opacity,
+        k_fixup_fwd<double><<<grid, FX_T, 0, st>>>(cam, opt, (const double*)soup.opacity,
                                                   (const double*)soup.sigma, rec, tile_start, ent_src, out);
     else
-        k_fixup_fwd<float><<<grid, 256, 0, st>>>(cam, opt, (const float*)soup.opacity,
+        k_fixup_fwd<float><<<grid, FX_T, 0, st>>>(cam, opt, (const float*)soup.opacity,
                                                  (const float*)soup.sigma, rec, tile_start, ent_src, out);
 }
 
