@@ -961,7 +961,15 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
     __shared__ float s_c[3][FXC];
     __shared__ unsigned s_s[FXC];
     __shared__ int s_done;
-    const unsigned lane = threadIdx.x & 31;
+    __shared__ short s_idx[FXC];        // render path: passing entries of the chunk, in order
+    __shared__ double s_tb[FXC];        // ... and the transmittance in front of each
+    __shared__ int s_np, s_used;
+    __shared__ double s_red[3][FX_T / 32];
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // render forwards (no records / fragments / fp64 colour totals): only the
+    // transmittance chain is sequential (one lane); weights, colour sums and
+    // statistics of the chunk's fragments are computed in parallel
+    const bool fastc = out.frec == nullptr && out.frag_tri == nullptr && out.c_total64 == nullptr;
     const long long nflag = (long long)out.ctr->n_flagged;
     for (long long k = blockIdx.x; k < nflag; k += gridDim.x) {
         const int2 f = out.flags[k];
@@ -1013,6 +1021,75 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                 s_s[i] = src;
             }
             __syncthreads();
+            if (fastc) {
+                if (warp == 0) {  // compaction of the passing entries (entry order)
+                    int np = 0;
+                    for (int i0 = 0; i0 < nb; i0 += 32) {
+                        const int i = i0 + (int)lane;
+                        const bool pz = i < nb && s_a[i] > 0.0;
+                        const unsigned m = __ballot_sync(0xffffffffu, pz);
+                        if (pz) s_idx[np + __popc(m & ((1u << lane) - 1u))] = (short)i;
+                        np += __popc(m);
+                    }
+                    __syncwarp();
+                    if (lane == 0) {  // the reference's sequential fp64 transmittance
+                        int used = np;
+                        double tt = Tt;
+                        for (int q = 0; q < np; q++) {
+                            s_tb[q] = tt;
+                            tt = TS_M(tt, TS_S(1.0, s_a[s_idx[q]]));
+                            if (tt < T_MIN) {
+                                used = q + 1;
+                                s_done = 1;
+                                break;
+                            }
+                        }
+                        s_np = np;
+                        s_used = used;
+                    }
+                }
+                __syncthreads();
+                const int used = s_used;
+                double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+                for (int q = threadIdx.x; q < used; q += FX_T) {
+                    const int j = s_idx[q];
+                    const double w = s_tb[q] * s_a[j];
+                    c0 += w * (double)s_c[0][j];
+                    c1 += w * (double)s_c[1][j];
+                    c2 += w * (double)s_c[2][j];
+                    if (base + j >= fpos) {
+                        if (out.max_weight) atomicMax((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
+                        if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + s_s[j], 1);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    c0 += __shfl_xor_sync(0xffffffffu, c0, off);
+                    c1 += __shfl_xor_sync(0xffffffffu, c1, off);
+                    c2 += __shfl_xor_sync(0xffffffffu, c2, off);
+                }
+                if (lane == 0) {
+                    s_red[0][warp] = c0;
+                    s_red[1][warp] = c1;
+                    s_red[2][warp] = c2;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int w2 = 0; w2 < FX_T / 32; w2++) {
+                    C0 += s_red[0][w2];
+                    C1 += s_red[1][w2];
+                    C2 += s_red[2][w2];
+                }
+                if (used > 0) {
+                    last = base + s_idx[used - 1];
+                    // transmittance after the chunk: continue the chain from the last stored value
+                    Tt = TS_M(s_tb[used - 1], TS_S(1.0, s_a[s_idx[used - 1]]));
+                }
+                cnt += used;
+                __syncthreads();
+                if (s_done) break;
+                continue;
+            }
             if (threadIdx.x < 32) {
                 for (int i0 = 0; i0 < nb && !s_done; i0 += 32) {
                     const int i = i0 + (int)lane;
