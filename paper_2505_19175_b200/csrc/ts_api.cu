@@ -59,7 +59,7 @@ struct ts_context {
     unsigned *tkey = nullptr, *tval = nullptr, *tkey_alt = nullptr, *tval_alt = nullptr;
     unsigned *tscr0 = nullptr, *tscr1 = nullptr;  // tile-sort scratch (tiles longer than shared memory)
     unsigned* tcnt = nullptr;                      // per-tile entry counts
-    ulonglong2* bucket = nullptr;                  // (depth key, source) of every tile entry, unsorted
+    uint2* bucket = nullptr;                       // (reduced depth key, source) of every tile entry, unsorted
     DevBuf binmat;                                 // chunk x tile count matrix of the binning
     bool sorted_valid = false;                     // sorted_src holds the global depth order
     // per-pixel scratch
@@ -178,7 +178,7 @@ static int ensure_ent(ts_context* c, long long e) {
     if (c->ent_buf) cudaFree(c->ent_buf);
     c->ent_buf = nullptr;
     size_t one = align_up(4 * cap, 256);
-    TS_CHECK(cudaMalloc(&c->ent_buf, 10 * one));
+    TS_CHECK(cudaMalloc(&c->ent_buf, 8 * one));
     char* b = (char*)c->ent_buf;
     c->tkey = (unsigned*)b;
     c->tval = (unsigned*)(b + one);
@@ -186,7 +186,7 @@ static int ensure_ent(ts_context* c, long long e) {
     c->tval_alt = (unsigned*)(b + 3 * one);
     c->tscr0 = (unsigned*)(b + 4 * one);
     c->tscr1 = (unsigned*)(b + 5 * one);
-    c->bucket = (ulonglong2*)(b + 6 * one);
+    c->bucket = (uint2*)(b + 6 * one);
     c->cap_e = cap;
     return TS_OK;
 }
@@ -391,7 +391,7 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
     if (n > 0 && !bin_legacy && ntiles <= bin_max_tiles()) {
         stage_begin(c, TS_STAGE_BINNING, st);
         bin_tiles_fill(n, c->bbox, c->key, cm.ntx, ntiles, c->tcnt, (unsigned*)c->binmat.p, c->tile_start,
-                       c->bucket, wcap, c->d_sticky, st);
+                       c->bucket, c->d_ctr, wcap, c->d_sticky, st);
         stage_end(c, TS_STAGE_BINNING, st);
         stage_begin(c, TS_STAGE_DEPTH_SORT, st);
         unsigned* const scr[4] = {c->tkey_alt, c->tval_alt, c->tscr0, c->tscr1};

@@ -169,9 +169,14 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* 
                                                      int ntiles, const unsigned* __restrict__ mat,
                                                      const int* __restrict__ tile_start,
                                                      const unsigned long long* __restrict__ key64,
-                                                     ulonglong2* __restrict__ bucket) {
+                                                     const Counters* __restrict__ ctr, uint2* __restrict__ bucket) {
     extern __shared__ unsigned s_cur[];
     if (tile_start[ntiles] == 0) return;  // empty (or over capacity)
+    // 32-bit depth keys, range-reduced over the accepted triangles (monotone in
+    // the fp64 key; ties of the reduced key are broken exactly by the tile sort)
+    const unsigned long long kmin = ctr->key_min, krange = ctr->key_max - kmin;
+    const int kbits = krange ? 64 - __clzll((long long)krange) : 0;
+    const int gshift = kbits > 32 ? kbits - 32 : 0;
     const unsigned* row = mat + (size_t)blockIdx.x * ntiles;
     for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cur[t] = (unsigned)tile_start[t] + row[t];
     __syncthreads();
@@ -187,13 +192,13 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* 
 #pragma unroll
     for (int k = 0; k < BIN_PER; k++) {
         if (bb[k].y <= bb[k].x || bb[k].w <= bb[k].z) continue;
-        const unsigned long long i = (unsigned long long)(c0 + k * BIN_CT + threadIdx.x);
+        const long long i = c0 + k * BIN_CT + threadIdx.x;
         const int tx0 = bb[k].x / TILE, tx1 = (bb[k].y - 1) / TILE + 1;
         const int ty0 = bb[k].z / TILE, ty1 = (bb[k].w - 1) / TILE + 1;
         for (int ty = ty0; ty < ty1; ty++)
             for (int tx = tx0; tx < tx1; tx++) {
                 const unsigned pos = atomicAdd(&s_cur[ty * ntx + tx], 1u);
-                bucket[pos] = make_ulonglong2(key[k], i);
+                bucket[pos] = make_uint2((unsigned)((key[k] - kmin) >> gshift), (unsigned)i);
             }
     }
 }
@@ -264,7 +269,7 @@ __device__ __forceinline__ bool zidx_less(const unsigned long long* key64, unsig
 
 // Sorts the tile list [base, base + cnt) of bucket into out (exact (z, idx) order).
 // k0/v0/k1/v1: working arrays of cnt items (shared memory or global scratch).
-__device__ __forceinline__ void sort_tile(int cnt, const ulonglong2* bucket, const unsigned long long* key64,
+__device__ __forceinline__ void sort_tile(int cnt, const uint2* bucket, const unsigned long long* key64,
                                           unsigned* out, unsigned* k0, unsigned* v0, unsigned* k1, unsigned* v1,
                                           int srcbits, unsigned (*wc)[256], unsigned* s_w,
                                           unsigned long long* s_red, int* s_flag) {
@@ -272,8 +277,8 @@ __device__ __forceinline__ void sort_tile(int cnt, const ulonglong2* bucket, con
     // depth-key range of the tile
     unsigned long long lo = ~0ull, hi = 0ull;
     for (int i = threadIdx.x; i < cnt; i += BT) {
-        const unsigned src = (unsigned)bucket[i].y;
-        const unsigned long long k = bucket[i].x;
+        const unsigned src = bucket[i].y;
+        const unsigned long long k = key64[src];  // (the bucket's key is the 32-bit reduced one)
         lo = k < lo ? k : lo;
         hi = k > hi ? k : hi;
         v0[i] = src;
@@ -358,7 +363,7 @@ __device__ __forceinline__ bool item_less(const unsigned long long* key64, unsig
 
 template <int CAP, int NB>
 __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restrict__ tile_start,
-                                                  const ulonglong2* __restrict__ bucket,
+                                                  const uint2* __restrict__ bucket,
                                                   const unsigned long long* __restrict__ key64,
                                                   unsigned* __restrict__ ent_src, unsigned* gk0, unsigned* gv0,
                                                   unsigned* gk1, unsigned* gv1, int srcbits) {
@@ -387,9 +392,9 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
         kk[q] = 0ull;
         src[q] = 0u;
         if (i < cnt) {
-            const ulonglong2 r = bucket[base + i];
+            const uint2 r = bucket[base + i];
             kk[q] = r.x;
-            src[q] = (unsigned)r.y;
+            src[q] = r.y;
             lo = kk[q] < lo ? kk[q] : lo;
             hi = kk[q] > hi ? kk[q] : hi;
         }
@@ -477,8 +482,8 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
 }
 
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
-                    unsigned* tcnt, unsigned* mat, int* tile_start, ulonglong2* bucket, long long cap,
-                    unsigned* overflow, cudaStream_t st) {
+                    unsigned* tcnt, unsigned* mat, int* tile_start, uint2* bucket, const Counters* ctr,
+                    long long cap, unsigned* overflow, cudaStream_t st) {
     const int nchunk = (int)((n + BIN_CHUNK - 1) / BIN_CHUNK);
     const int smem = ntiles * (int)sizeof(unsigned);
     static bool attr = false;
@@ -495,7 +500,7 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
     }
     k_tile_scan<<<1, 1024, 0, st>>>(ntiles, tcnt, tile_start, cap, overflow);
     if (n > 0)
-        k_bin_fill<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, bucket);
+        k_bin_fill<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, ctr, bucket);
 }
 
 size_t bin_matrix_bytes(long long n, int ntiles) {
@@ -505,7 +510,7 @@ size_t bin_matrix_bytes(long long n, int ntiles) {
 
 int bin_max_tiles() { return BIN_MAX_TILES; }
 
-void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const ulonglong2* bucket,
+void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
                     const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4], cudaStream_t st) {
     const int srcbits = n > 1 ? 64 - __builtin_clzll((unsigned long long)(n - 1)) : 1;
     k_tile_sort<2048, 4096><<<ntiles, BT, 0, st>>>(ntiles, tile_start, bucket, key64, ent_src, scratch[0],
