@@ -524,12 +524,14 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         if ((rc = ensure(c->ctot, sizeof(double) * 3 * (size_t)P))) return rc;
     }
     TS_CHECK(cudaMemcpyAsync(c->d_ctr, c->h_init, sizeof(Counters), cudaMemcpyHostToDevice, st));
-    if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
-    if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
+    if (!fast) {  // (the fast preprocess zeroes them per triangle)
+        if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
+        if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
+    }
     stage_begin(c, TS_STAGE_PREPROCESS, st);
     if (fast) {
         FastPreOut po{(RecF*)c->recf.p, opt->keep_backward ? (RecB*)c->recb.p : nullptr, c->bbox, c->key,
-                      c->tcount, c->flag, out->area, nullptr, c->d_ctr};
+                      c->tcount, c->flag, out->area, nullptr, c->d_ctr, out->max_weight, out->pixel_count};
         launch_preprocess_fast(cm, op, *soup, opt->param_dtype, po, st);
     } else {
         PreOut po{(Rec64*)c->rec64.p, c->bbox, c->key, c->tcount, c->flag, out->area, nullptr, c->d_ctr};

@@ -285,6 +285,8 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
     out.bbox[i] = bb;
     out.flag[i] = ok ? 1u : 0u;
     out.tcount[i] = tcount;
+    if (out.max_weight) out.max_weight[i] = 0.f;
+    if (out.pixel_count) out.pixel_count[i] = 0;
     out.key[i] = key;
     return ok;
 }

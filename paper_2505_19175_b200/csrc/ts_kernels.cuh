@@ -50,6 +50,8 @@ struct FastPreOut {
     float* area;
     double* depth;
     Counters* ctr;
+    float* max_weight;         // zeroed per triangle (nullable): the blend accumulates into them
+    int* pixel_count;
 };
 
 struct FastBlendOut {
