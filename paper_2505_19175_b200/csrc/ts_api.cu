@@ -59,6 +59,7 @@ struct ts_context {
     unsigned *tkey = nullptr, *tval = nullptr, *tkey_alt = nullptr, *tval_alt = nullptr;
     unsigned *tscr0 = nullptr, *tscr1 = nullptr;  // tile-sort scratch (tiles longer than shared memory)
     unsigned* tcnt = nullptr;                      // per-tile entry counts
+    int* big_list = nullptr;                       // tiles for the long-tile sort, count at [ntiles]
     uint2* bucket = nullptr;                       // (reduced depth key, source) of every tile entry, unsorted
     DevBuf binmat;                                 // chunk x tile count matrix of the binning
     bool sorted_valid = false;                     // sorted_src holds the global depth order
@@ -204,7 +205,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
         return o;
     };
     size_t o_tf = take(8 * cp), o_t32 = take(4 * cp), o_lp = take(4 * cp), o_fg = take(8 * cp),
-           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp), o_tc = take(4 * (ct + 1));
+           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp), o_tc = take(4 * (ct + 1)), o_bl = take(4 * (ct + 1));
     TS_CHECK(cudaMalloc(&c->pix_buf, off));
     char* b = (char*)c->pix_buf;
     c->t_final = (double*)(b + o_tf);
@@ -214,6 +215,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     c->tile_start = (int*)(b + o_ts);
     c->nfrag = (int*)(b + o_nf);
     c->tcnt = (unsigned*)(b + o_tc);
+    c->big_list = (int*)(b + o_bl);
     c->cap_p = cp;
     c->cap_tiles = ct;
     return TS_OK;
@@ -391,16 +393,16 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
     if (n > 0 && !bin_legacy && ntiles <= bin_max_tiles()) {
         stage_begin(c, TS_STAGE_BINNING, st);
         bin_tiles_fill(n, c->bbox, c->key, cm.ntx, ntiles, c->tcnt, (unsigned*)c->binmat.p, c->tile_start,
-                       c->bucket, c->d_ctr, wcap, c->d_sticky, st);
+                       c->bucket, c->d_ctr, wcap, c->d_sticky, c->big_list, st);
         stage_end(c, TS_STAGE_BINNING, st);
         stage_begin(c, TS_STAGE_DEPTH_SORT, st);
         unsigned* const scr[4] = {c->tkey_alt, c->tval_alt, c->tscr0, c->tscr1};
-        bin_tiles_sort(n, ntiles, c->tile_start, c->bucket, c->key, c->tval, scr, st);
+        bin_tiles_sort(n, ntiles, c->tile_start, c->bucket, c->key, c->tval, scr, c->big_list, st);
         stage_end(c, TS_STAGE_DEPTH_SORT, st);
         c->ent_src = c->tval;
         c->sorted_src = c->vals_c;
         c->wcap = wcap;
-        g_launches += 5;
+        g_launches += 6;
     } else if (n > 0) {
         stage_begin(c, TS_STAGE_DEPTH_SORT, st);
         global_depth_order(c, n, st);

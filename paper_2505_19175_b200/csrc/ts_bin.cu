@@ -62,9 +62,12 @@ __device__ __forceinline__ unsigned excl_scan_256(unsigned v, unsigned* s_w, uns
 }  // namespace
 
 __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __restrict__ tcnt, int* __restrict__ tile_start,
-                                                    long long cap, unsigned* overflow) {
+                                                    long long cap, unsigned* overflow, int small_cap,
+                                                    int* __restrict__ big_list, int* __restrict__ n_big) {
     __shared__ unsigned s_w[32];
     __shared__ unsigned long long s_total;
+    __shared__ int s_nbig;
+    if (threadIdx.x == 0) s_nbig = 0;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long carry = 0;
     for (int b0 = 0; b0 < ntiles; b0 += 1024) {
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __rest
         const unsigned long long ex = carry + (warp ? s_w[warp - 1] : 0u) + x - v;
         if (i < ntiles) {
             tile_start[i] = (int)ex;
-            tcnt[i] = 0u;  // becomes the fill cursor
+            if ((int)v > small_cap) big_list[atomicAdd(&s_nbig, 1)] = i;  // long tiles, any order
         }
         carry += s_w[31];
         __syncthreads();
@@ -101,9 +104,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __rest
     if (s_total > (unsigned long long)cap) {
         // over capacity: every tile empty, the forward is redone with larger buffers
         for (int i = threadIdx.x; i <= ntiles; i += 1024) tile_start[i] = 0;
-        if (threadIdx.x == 0 && overflow) *overflow = 1u;
+        if (threadIdx.x == 0) {
+            if (overflow) *overflow = 1u;
+            *n_big = 0;
+        }
     } else if (threadIdx.x == 0) {
         tile_start[ntiles] = (int)s_total;
+        *n_big = s_nbig;
     }
 }
 
@@ -374,14 +381,11 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
     __shared__ unsigned s_w[32];
     __shared__ unsigned long long s_red[2 * BW];
     __shared__ int s_flag;
+    // the long-tile kernel (independent tiles) may launch while this grid drains
+    asm volatile("griddepcontrol.launch_dependents;");
     const int t = blockIdx.x;
     const int base = tile_start[t], cnt = tile_start[t + 1] - base;
-    if (cnt <= 0) return;
-    if (cnt > CAP) {
-        sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,
-                  srcbits, s_wc, s_w, s_red, &s_flag);
-        return;
-    }
+    if (cnt <= 0 || cnt > CAP) return;  // (longer tiles: k_tile_sort_big)
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long kk[IPT];
     unsigned src[IPT];
@@ -481,9 +485,114 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
                   srcbits, s_wc, s_w, s_red, &s_flag);
 }
 
+
+// Tiles of (SMALL, CAP] entries (listed by k_tile_scan): the same bucket sort
+// with the bucket re-read from L2 instead of staged in registers, the sorted
+// items in dynamic shared memory (8 x CAP bytes); longer tiles take the stable
+// LSD path on global scratch.  Persistent CTAs walk the list.
+template <int CAP, int NB>
+__global__ void __launch_bounds__(BT) k_tile_sort_big(const int* __restrict__ big_list, const int* __restrict__ n_big,
+                                                      const int* __restrict__ tile_start,
+                                                      const uint2* __restrict__ bucket,
+                                                      const unsigned long long* __restrict__ key64,
+                                                      unsigned* __restrict__ ent_src, unsigned* gk0, unsigned* gv0,
+                                                      unsigned* gk1, unsigned* gv1, int srcbits) {
+    extern __shared__ __align__(16) unsigned long long s_item[];  // [CAP]
+    __shared__ unsigned s_hist[NB];
+    __shared__ unsigned s_wc[BW][256];
+    __shared__ unsigned s_w[32];
+    __shared__ unsigned long long s_red[2 * BW];
+    __shared__ int s_flag;
+    const int nbig = *n_big;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = blockIdx.x; k < nbig; k += gridDim.x) {
+        const int t = big_list[k];
+        const int base = tile_start[t], cnt = tile_start[t + 1] - base;
+        if (cnt > CAP) {
+            sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,
+                      srcbits, s_wc, s_w, s_red, &s_flag);
+            __syncthreads();
+            continue;
+        }
+        unsigned lo = ~0u, hi = 0u;
+        for (int i = threadIdx.x; i < cnt; i += BT) {
+            const unsigned x = bucket[base + i].x;
+            lo = x < lo ? x : lo;
+            hi = x > hi ? x : hi;
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0) {
+            s_red[warp] = lo;
+            s_red[BW + warp] = hi;
+        }
+        for (int b = threadIdx.x; b < NB; b += BT) s_hist[b] = 0u;
+        __syncthreads();
+        lo = (unsigned)s_red[0];
+        hi = (unsigned)s_red[BW];
+#pragma unroll
+        for (int w = 1; w < BW; w++) {
+            lo = (unsigned)s_red[w] < lo ? (unsigned)s_red[w] : lo;
+            hi = (unsigned)s_red[BW + w] > hi ? (unsigned)s_red[BW + w] : hi;
+        }
+        const unsigned range = hi - lo;
+        const int nbits = range ? 32 - __clz((int)range) : 0;
+        constexpr int LB = NB == 4096 ? 12 : (NB == 2048 ? 11 : 10);
+        const int s12 = nbits > LB ? nbits - LB : 0;
+        for (int i = threadIdx.x; i < cnt; i += BT) atomicAdd(&s_hist[(bucket[base + i].x - lo) >> s12], 1u);
+        __syncthreads();
+        {
+            constexpr int PT = NB / BT;
+            unsigned v[PT], sum = 0;
+#pragma unroll
+            for (int u = 0; u < PT; u++) {
+                v[u] = s_hist[threadIdx.x * PT + u];
+                sum += v[u];
+            }
+            unsigned all;
+            unsigned run = excl_scan_256(sum, s_w, all);
+#pragma unroll
+            for (int u = 0; u < PT; u++) {
+                s_hist[threadIdx.x * PT + u] = run;
+                run += v[u];
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += BT) {
+            const uint2 r = bucket[base + i];
+            const unsigned kr = r.x - lo;
+            const unsigned pos = atomicAdd(&s_hist[kr >> s12], 1u);
+            s_item[pos] = ((unsigned long long)kr << 32) | r.y;
+        }
+        __syncthreads();
+        int longb = 0;
+        for (int i = threadIdx.x; i < cnt; i += BT) {
+            const unsigned long long x = s_item[i];
+            const unsigned b = (unsigned)(x >> 32) >> s12;
+            const int be = (int)s_hist[b], bs = b ? (int)s_hist[b - 1] : 0;
+            if (be - bs > RUN_LONG) {
+                longb = 1;
+                continue;
+            }
+            int rank = 0;
+            for (int j = bs; j < be; j++) {
+                const unsigned long long y = s_item[j];
+                if (y != x) rank += item_less(key64, y, x);
+            }
+            ent_src[base + bs + rank] = (unsigned)x;
+        }
+        if (__syncthreads_or(longb))
+            sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,
+                      srcbits, s_wc, s_w, s_red, &s_flag);
+        __syncthreads();
+    }
+}
+
+constexpr int SORT_SMALL = 2048, SORT_BIG = 8192;
+
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
                     unsigned* tcnt, unsigned* mat, int* tile_start, uint2* bucket, const Counters* ctr,
-                    long long cap, unsigned* overflow, cudaStream_t st) {
+                    long long cap, unsigned* overflow, int* big_list, cudaStream_t st) {
     const int nchunk = (int)((n + BIN_CHUNK - 1) / BIN_CHUNK);
     const int smem = ntiles * (int)sizeof(unsigned);
     static bool attr = false;
@@ -498,7 +607,9 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
     } else {
         cudaMemsetAsync(tcnt, 0, sizeof(unsigned) * ntiles, st);
     }
-    k_tile_scan<<<1, 1024, 0, st>>>(ntiles, tcnt, tile_start, cap, overflow);
+    // big_list[ntiles]: tiles longer than SORT_SMALL; its count at big_list[ntiles]
+    k_tile_scan<<<1, 1024, 0, st>>>(ntiles, tcnt, tile_start, cap, overflow, SORT_SMALL, big_list,
+                                    big_list + ntiles);
     if (n > 0)
         k_bin_fill<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, ctr, bucket);
 }
@@ -511,10 +622,35 @@ size_t bin_matrix_bytes(long long n, int ntiles) {
 int bin_max_tiles() { return BIN_MAX_TILES; }
 
 void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
-                    const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4], cudaStream_t st) {
+                    const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],
+                    const int* big_list, cudaStream_t st) {
     const int srcbits = n > 1 ? 64 - __builtin_clzll((unsigned long long)(n - 1)) : 1;
-    k_tile_sort<2048, 4096><<<ntiles, BT, 0, st>>>(ntiles, tile_start, bucket, key64, ent_src, scratch[0],
-                                                  scratch[1], scratch[2], scratch[3], srcbits);
+    k_tile_sort<SORT_SMALL, 4096><<<ntiles, BT, 0, st>>>(ntiles, tile_start, bucket, key64, ent_src, scratch[0],
+                                                        scratch[1], scratch[2], scratch[3], srcbits);
+    // tiles above SORT_SMALL entries (dense views), listed by k_tile_scan
+    static int sms = 0;
+    const int smem = SORT_BIG * (int)sizeof(unsigned long long);
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_tile_sort_big<SORT_BIG, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
+    // programmatic dependent launch: overlaps the previous kernel's last wave (the
+    // two kernels sort disjoint tiles; everything they read was written before it)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * sms);
+    cfg.blockDim = dim3(BT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int* n_big = big_list + ntiles;
+    cudaLaunchKernelEx(&cfg, k_tile_sort_big<SORT_BIG, 4096>, big_list, n_big, tile_start, bucket, key64, ent_src,
+                       scratch[0], scratch[1], scratch[2], scratch[3], srcbits);
 }
 
 }  // namespace ts

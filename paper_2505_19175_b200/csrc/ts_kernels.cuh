@@ -184,11 +184,12 @@ int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned*
 // bucket: one (32-bit range-reduced depth key, source) record per tile entry.
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
                     unsigned* tcnt, unsigned* mat, int* tile_start, uint2* bucket, const Counters* ctr,
-                    long long cap, unsigned* overflow, cudaStream_t st);
+                    long long cap, unsigned* overflow, int* big_list, cudaStream_t st);
 size_t bin_matrix_bytes(long long n, int ntiles);
 int bin_max_tiles();
 void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
-                    const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4], cudaStream_t st);
+                    const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],
+                    const int* big_list, cudaStream_t st);
 // count = min(cap, *dcount), read on the device
 int onesweep_sort_u32_dev(long long cap, const unsigned long long* dcount, unsigned* keys, unsigned* vals,
                           unsigned* keys_alt, unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);

@@ -1,7 +1,8 @@
 """GPU parity of the tile-first binning (ts_bin.cu) in its corner cases:
 equal depths (one run of equal keys per tile), clustered depths (long runs
 of distinct keys that share a range-reduced key), tiles longer than the
-tile sort's shared-memory capacity (global-scratch path), and the legacy
+tile sort's register / shared-memory staging (2048 / 8192 entries; the
+global-scratch path beyond), and the legacy
 global-sort binning on the same scenes.  Tile lists, last contributors and
 images must equal the oracle's (render.py:275-361 order: np.lexsort((idx, z))
 then stable by tile)."""
@@ -85,6 +86,14 @@ def test_tiles_longer_than_shared_memory(rast):
     intr, pose = _cam(32, 32, 90.0)
     longest = _check(rast, soup, intr, pose, "long tiles")
     assert longest > 2048
+
+
+def test_tiles_longer_than_staging(rast):
+    # > 8192 entries per tile: the stable LSD path on global scratch
+    soup = _soup(24000, 5, lambda rng, n: rng.uniform(-1, 1, n), spread=0.08, size=0.02)
+    intr, pose = _cam(32, 32, 90.0)
+    longest = _check(rast, soup, intr, pose, "very long tiles")
+    assert longest > 8192
 
 
 def test_long_tiles_with_equal_depths(rast):
