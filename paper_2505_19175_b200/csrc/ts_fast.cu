@@ -46,7 +46,9 @@ __device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, co
                                                  double& c0, double& c1, double& c2) {
     const float4* q = reinterpret_cast<const float4*>(p);
     const int nv = (ncoef * 3 + 3) >> 2;
-    double acc[3] = {c0, c1, c2};
+    // two partial sums per channel (even / odd coefficient): halves the
+    // dependent fp64 FMA chain
+    double acc[2][3] = {{c0, c1, c2}, {0.0, 0.0, 0.0}};
 #pragma unroll
     for (int k = 0; k < 12; k++) {
         if (k < nv) {
@@ -55,11 +57,12 @@ __device__ __forceinline__ void sh_colour<float>(const float* __restrict__ p, co
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int idx = k * 4 + u;  // coefficient idx / 3, channel idx % 3
-                if (idx / 3 < ncoef) acc[idx % 3] = fma(bs[idx / 3], (double)vv[u], acc[idx % 3]);
+                const int co = idx / 3;
+                if (co < ncoef) acc[co & 1][idx % 3] = fma(bs[co], (double)vv[u], acc[co & 1][idx % 3]);
             }
         }
     }
-    c0 = acc[0]; c1 = acc[1]; c2 = acc[2];
+    c0 = acc[0][0] + acc[1][0]; c1 = acc[0][1] + acc[1][1]; c2 = acc[0][2] + acc[1][2];
 }
 template <>
 __device__ __forceinline__ void sh_colour<double>(const double* __restrict__ p, const double* bs, int ncoef,
@@ -341,13 +344,14 @@ struct PreStage {
     float o[PRE_BLK], sg[PRE_BLK];
 };
 
-__global__ void __launch_bounds__(PRE_BLK, 3) k_preprocess_fast32(Cam cam, Opts opt, const float* __restrict__ verts,
+template <int NBUF, int MINB>
+__global__ void __launch_bounds__(PRE_BLK, MINB) k_preprocess_fast32(Cam cam, Opts opt, const float* __restrict__ verts,
                                                                const float* __restrict__ opacity,
                                                                const float* __restrict__ sigma,
                                                                const float* __restrict__ sh, long long n,
                                                                FastPreOut out) {
     extern __shared__ __align__(16) unsigned char s_pre[];
-    PreStage* stage = reinterpret_cast<PreStage*>(s_pre);  // [2]
+    PreStage* stage = reinterpret_cast<PreStage*>(s_pre);  // [NBUF]
     const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
     const int tid = threadIdx.x;
     auto issue = [&](long long blk, int buf) {
@@ -378,13 +382,19 @@ __global__ void __launch_bounds__(PRE_BLK, 3) k_preprocess_fast32(Cam cam, Opts 
     unsigned long long kmin = ~0ull, kmax = 0ull, tc = 0;
     unsigned cnt = 0;
     long long blk = blockIdx.x;
-    if (blk < nblk) issue(blk, 0);
+    if (NBUF == 2 && blk < nblk) issue(blk, 0);
     cp_async_commit();
     for (int it = 0; blk < nblk; blk += gridDim.x, it++) {
-        const int buf = it & 1;
-        if (blk + gridDim.x < nblk) issue(blk + gridDim.x, buf ^ 1);
-        cp_async_commit();
-        cp_async_wait_group1();
+        const int buf = NBUF == 2 ? (it & 1) : 0;
+        if constexpr (NBUF == 2) {
+            if (blk + gridDim.x < nblk) issue(blk + gridDim.x, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait_group1();
+        } else {  // single stage: other CTAs of the SM overlap its load
+            issue(blk, 0);
+            cp_async_commit();
+            cp_async_wait_all();
+        }
         __syncthreads();
         const long long i = blk * PRE_BLK + tid;
         if (i < n) {
@@ -419,18 +429,38 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
                                                   (const double*)soup.sigma, (const double*)soup.sh, n, out);
     } else {
         static int sms = 0;
-        static const int smem = 2 * (int)sizeof(PreStage);
+        static const int variant = [] {
+            const char* v = getenv("TS_PRE_VARIANT");
+            return v ? atoi(v) : 0;
+        }();
+        // default: single-buffered stage, 4 CTAs per SM (other CTAs overlap each
+        // one's loads; 126 registers); 1: double-buffered, 3 CTAs; 2: single, 5 CTAs
+        const int nbuf = variant == 1 ? 2 : 1;
+        const int minb = variant == 1 ? 3 : (variant == 2 ? 5 : 4);
+        const int smem = nbuf * (int)sizeof(PreStage);
         if (!sms) {
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(k_preprocess_fast32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k_preprocess_fast32<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * (int)sizeof(PreStage));
+            cudaFuncSetAttribute(k_preprocess_fast32<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PreStage));
+            cudaFuncSetAttribute(k_preprocess_fast32<1, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PreStage));
         }
         const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
-        const long long grid = std::min<long long>(nblk, (long long)sms * 3);
-        k_preprocess_fast32<<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, (const float*)soup.vertices,
-                                                                  (const float*)soup.opacity, (const float*)soup.sigma,
-                                                                  (const float*)soup.sh, n, out);
+        const long long grid = std::min<long long>(nblk, (long long)sms * minb);
+        const float* v = (const float*)soup.vertices;
+        const float* o = (const float*)soup.opacity;
+        const float* sg = (const float*)soup.sigma;
+        const float* sh = (const float*)soup.sh;
+        if (minb == 3)
+            k_preprocess_fast32<2, 3><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
+        else if (minb == 5)
+            k_preprocess_fast32<1, 5><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
+        else
+            k_preprocess_fast32<1, 4><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
     }
 }
 
