@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         double g_phi;
                         if (mode == 0) {
                             const double rc = fmin(r64, 1.0);
-                            g[7] = g_win * window * log(rc);
+                            // log(rc) in fp32 to ~1e-7 relative (log1p of the exact rc - 1 near 1)
+                            g[7] = g_win * window * (double)(rc > 0.5 ? log1pf((float)(rc - 1.0)) : logf((float)rc));
                             const double g_r = g_win * (double)par.y * window / rc;
                             if (r64 >= 1.0) {
                                 g_phi = 0.0;

@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                     const double phi = r64 * phis;
                     double g_phi;
                     if (mode == 0) {
-                        gf[7] = (AT)(g_win * window * log(rc));
+                        // log(rc) in fp32 to ~1e-7 relative: log1p of the exact rc - 1 near 1, log below
+                        const float lrc = rc > 0.5 ? log1pf((float)(rc - 1.0)) : logf((float)rc);
+                        gf[7] = (AT)(g_win * window * (double)lrc);
                         const double g_r = g_win * sg * window / rc;
                         if (r64 >= 1.0) {
                             g_phi = 0.0;
