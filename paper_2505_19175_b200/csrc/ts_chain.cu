@@ -2,7 +2,7 @@
 // triangle (backward.py:59-90 _phis_q_grad, backward.py:158-210 projection
 // Jacobian and SH colour path, sh.py:55-100 basis gradient), fp32 parameters.
 //
-// CTA = 128 triangles, thread = triangle.  The CTA's SH block, vertices and
+// CTA = 64 triangles, thread = triangle.  The CTA's SH block, vertices and
 // screen-space gradient rows are copied to shared memory with coalesced
 // cp.async (rows padded against bank conflicts); d_sh is written in place over
 // the thread's own SH row and every output block leaves with coalesced 16-byte
@@ -13,7 +13,7 @@
 namespace ts {
 
 namespace {
-constexpr int CB = 128;     // triangles per CTA
+constexpr int CB = 64;      // triangles per CTA (8 CTAs per SM: independent load / compute phases overlap)
 constexpr int SGW = 18;     // doubles per staged gradient row (16 used; 144 B keeps 16-B chunks aligned)
 
 struct ChainStage {
@@ -21,6 +21,10 @@ struct ChainStage {
     float v[CB * 9];        // vertices; overwritten with d_vertices
     double sg[CB * SGW];    // screen-space gradient rows
     float os[2][CB];        // d_opacity, d_sigma
+    // accumulating calls: the gradients already in the output, prefetched with the inputs
+    float4 ash[CB * 12];
+    float av[CB * 9];
+    float aos[2][CB];
 };
 
 // sum_c s_c * grad(Y_c)(x, y, z) for the 16 real SH basis functions (sh.py:55-100)
@@ -71,7 +75,7 @@ __device__ __forceinline__ void sh_weighted_grad(double x, double y, double z, c
 }
 }  // namespace
 
-__global__ void __launch_bounds__(CB, 4) k_chain_bwd32(Cam cam, Opts opt, const float* __restrict__ verts,
+__global__ void __launch_bounds__(CB, 8) k_chain_bwd32(Cam cam, Opts opt, const float* __restrict__ verts,
                                                        const float* __restrict__ sh,
                                                        const unsigned* __restrict__ flag,
                                                        const double* __restrict__ sgrad, long long n,
@@ -101,7 +105,20 @@ __global__ void __launch_bounds__(CB, 4) k_chain_bwd32(Cam cam, Opts opt, const 
             cp_async16(reinterpret_cast<double2*>(&S.sg[tri * SGW]) + q, gs + c);
         }
         cp_async_commit();
-        cp_async_wait_all();
+        if (accumulate) {  // the output's current values, consumed only at the write-out
+            const float4* ga = reinterpret_cast<const float4*>(grads.d_sh + i0 * 48);
+            for (int c = tid; c < nt * 12; c += CB) cp_async16(&S.ash[c], ga + c);
+            const float* gva = grads.d_vertices + i0 * 9;
+            for (int c = tid; c < nt * 9; c += CB) cp_async4(&S.av[c], gva + c);
+            if (tid < nt) {
+                cp_async4(&S.aos[0][tid], grads.d_opacity + i0 + tid);
+                cp_async4(&S.aos[1][tid], grads.d_sigma + i0 + tid);
+            }
+            cp_async_commit();
+            cp_async_wait_group1();  // the inputs; the prefetch may still be in flight
+        } else {
+            cp_async_wait_all();
+        }
         __syncthreads();
     }
     const long long i = i0 + tid;
@@ -226,6 +243,7 @@ __global__ void __launch_bounds__(CB, 4) k_chain_bwd32(Cam cam, Opts opt, const 
         S.os[0][tid] = (float)dop;
         S.os[1][tid] = (float)dsig;
     }
+    cp_async_wait_all();
     __syncthreads();
     // ---- coalesced write-out ----
     {
@@ -234,16 +252,16 @@ __global__ void __launch_bounds__(CB, 4) k_chain_bwd32(Cam cam, Opts opt, const 
             const int tri = c / 12;
             float4 v = S.sh[tri * 13 + (c - tri * 12)];
             if (accumulate) {
-                const float4 o = g[c];
+                const float4 o = S.ash[c];
                 v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
             }
             g[c] = v;
         }
         float* gv = grads.d_vertices + i0 * 9;
-        for (int c = tid; c < nt * 9; c += CB) gv[c] = accumulate ? gv[c] + S.v[c] : S.v[c];
+        for (int c = tid; c < nt * 9; c += CB) gv[c] = accumulate ? S.av[c] + S.v[c] : S.v[c];
         if (tid < nt) {
-            grads.d_opacity[i0 + tid] = accumulate ? grads.d_opacity[i0 + tid] + S.os[0][tid] : S.os[0][tid];
-            grads.d_sigma[i0 + tid] = accumulate ? grads.d_sigma[i0 + tid] + S.os[1][tid] : S.os[1][tid];
+            grads.d_opacity[i0 + tid] = accumulate ? S.aos[0][tid] + S.os[0][tid] : S.os[0][tid];
+            grads.d_sigma[i0 + tid] = accumulate ? S.aos[1][tid] + S.os[1][tid] : S.os[1][tid];
         }
     }
 }
