@@ -542,7 +542,9 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     stage_end(c, TS_STAGE_PREPROCESS, st);
     g_launches += n > 0 ? 1 : 0;
     if ((rc = enqueue_tail(c, cm, op, opt, soup, out, st))) return rc;
-    TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    // (asynchronous forwards read the counters back in ts_forward_status only)
+    if (!c->async_mode)
+        TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     c->have_fwd = true;
     c->have_bwd_state = !fast || opt->keep_backward;
     c->frec_ready = fast && opt->keep_backward && getenv("TS_BWD_TILES") == nullptr;
@@ -589,6 +591,7 @@ int ts_forward_status(ts_context* c, ts_forward_result* res, void* stream) {
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     cudaStream_t st = (cudaStream_t)stream;
     unsigned sticky = 0;
+    TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     TS_CHECK(cudaMemcpyAsync(&sticky, c->d_sticky, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     TS_CHECK(cudaStreamSynchronize(st));
     c->pending = false;
