@@ -164,6 +164,17 @@ int ts_backward_fragments(ts_context* ctx, const float* d_image, const int64_t* 
                           const double* d_weight, const double* d_depth, const ts_grads* grads,
                           int accumulate, void* stream);
 
+/* Photometric loss (losses.py:122-142): (1-lambda) L1 + lambda (1-SSIM)/2 of
+ * two H x W x 3 fp32 images on the device (11x11 Gaussian window, sigma 1.5;
+ * the SSIM term is 0 below the window size, skipped for lambda == 0).
+ * out: device double[2] = {loss, mean SSIM}; d_image (nullable): device
+ * float[H*W*3], the gradient of the loss w.r.t. rendered.  Ordered on the
+ * stream; the context supplies the scratch. */
+int ts_photometric_loss(ts_context* ctx, const float* rendered, const float* target, int height, int width,
+                        double lambda_dssim, double* out, float* d_image, void* stream);
+/* Mean SSIM over channels (losses.py:110-119) into out[1] (device double[2]). */
+int ts_ssim(ts_context* ctx, const float* x, const float* y, int height, int width, double* out, void* stream);
+
 /* Debug/parity dumps of the last forward pass (device destination):
  *  TS_DUMP_SORTED_IDX  int32[M]       depth-sorted source ids (render.py:275-277)
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)

@@ -66,7 +66,8 @@ class TsGrads(ctypes.Structure):
 EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_version",
            "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
            "ts_stage_times", "ts_flagged_pixels", "ts_fragment_offsets", "ts_collect_fragments",
-           "ts_backward_fragments", "ts_set_async", "ts_forward_status"]
+           "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_photometric_loss",
+           "ts_ssim"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -111,6 +112,13 @@ def load(path: str = LIB_PATH):
     lib.ts_debug_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                   ctypes.c_size_t, ctypes.c_void_p]
     lib.ts_debug_copy.restype = ctypes.c_int
+    lib.ts_photometric_loss.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p]
+    lib.ts_photometric_loss.restype = ctypes.c_int
+    lib.ts_ssim.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_void_p]
+    lib.ts_ssim.restype = ctypes.c_int
     lib.ts_launch_count.argtypes = [ctypes.c_void_p]
     lib.ts_launch_count.restype = ctypes.c_int64
     lib.ts_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]

@@ -62,6 +62,7 @@ struct ts_context {
     int* big_list = nullptr;                       // tiles for the long-tile sort, count at [ntiles]
     uint2* bucket = nullptr;                       // (reduced depth key, source) of every tile entry, unsorted
     DevBuf binmat;                                 // chunk x tile count matrix of the binning
+    DevBuf lossbuf;                                // photometric loss scratch
     bool sorted_valid = false;                     // sorted_src holds the global depth order
     // per-pixel scratch
     long long cap_p = -1, cap_tiles = -1;
@@ -316,7 +317,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
     for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
-                      &c->ctot, &c->binmat})
+                      &c->ctot, &c->binmat, &c->lossbuf})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
@@ -748,6 +749,26 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
     g_launches += 2;
     TS_CHECK(cudaGetLastError());
     return TS_OK;
+}
+
+int ts_photometric_loss(ts_context* c, const float* rendered, const float* target, int height, int width,
+                        double lambda_dssim, double* out, float* d_image, void* stream) {
+    if (!c || !rendered || !target || !out || height < 1 || width < 1) return TS_ERR_INVALID_ARG;
+    int rc;
+    if ((rc = ensure(c->lossbuf, photometric_scratch_bytes(height, width)))) return rc;
+    launch_photometric_loss(rendered, target, height, width, lambda_dssim, out, d_image, c->lossbuf.p, false,
+                            (cudaStream_t)stream);
+    g_launches += 3;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_ssim(ts_context* c, const float* x, const float* y, int height, int width, double* out, void* stream) {
+    if (!c || !x || !y || !out || height < 1 || width < 1) return TS_ERR_INVALID_ARG;
+    int rc;
+    if ((rc = ensure(c->lossbuf, photometric_scratch_bytes(height, width)))) return rc;
+    launch_photometric_loss(x, y, height, width, 1.0, out, nullptr, c->lossbuf.p, true, (cudaStream_t)stream);
+    g_launches += 2;
+    return cuda_err(cudaGetLastError());
 }
 
 int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream) {

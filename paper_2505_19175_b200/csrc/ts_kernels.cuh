@@ -180,6 +180,11 @@ void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st);
 size_t onesweep_scratch_bytes(long long max_count, int max_passes);
 int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
                       unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
+// ts_loss.cu: photometric loss (L1 + D-SSIM) and gradient
+size_t photometric_scratch_bytes(int H, int W);
+void launch_photometric_loss(const float* x, const float* y, int H, int W, double lam, double* out, float* d_image,
+                             void* scratch, bool ssim_only, cudaStream_t st);
+
 // ts_bin.cu: tile-first binning (chunk x tile counts, scan, fill; per-tile exact depth sort).
 // bucket: one (32-bit range-reduced depth key, source) record per tile entry.
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,

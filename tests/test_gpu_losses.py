@@ -1,0 +1,72 @@
+"""GPU parity of the on-device photometric loss (ts_loss.cu) against the
+oracle (on the same fp32-rounded images) and the live reference's fixtures."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import losses as OL
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "loss.npz")
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def _check(x, y, lam, label):
+    from paper_2505_19175_b200 import losses as DL
+    xr, yr = f32(x), f32(y)
+    want_l, want_g = OL.photometric_loss(xr, yr, lam)
+    got_l, got_g = DL.photometric_loss(xr, yr, lam)
+    assert abs(got_l - want_l) <= 1e-9 + 1e-9 * abs(want_l), f"{label} loss {got_l} vs {want_l}"
+    scale = max(np.abs(want_g).max(), 1e-9)  # (identical images: gradient ~0)
+    err = np.abs(got_g - want_g).max() / scale
+    assert err <= 1e-5, f"{label} grad rel err {err}"
+    if xr.shape[0] >= 11 and xr.shape[1] >= 11:
+        assert abs(DL.ssim(xr, yr) - OL.ssim(xr, yr)) <= 1e-9, label
+
+
+def test_against_reference_fixtures():
+    from paper_2505_19175_b200 import losses as DL
+    z = np.load(GOLD)
+    for k in range(int(z["n"])):
+        x, y, lam = z[f"x{k}"], z[f"y{k}"], float(z[f"lam{k}"])
+        _check(x, y, lam, f"golden{k}")
+        # fp32 inputs vs the reference's fp64 inputs: a few 1e-8
+        got_l, _ = DL.photometric_loss(x, y, lam)
+        assert abs(got_l - float(z[f"loss{k}"])) <= 1e-6, k
+
+
+@pytest.mark.parametrize("shape", [(16, 16), (17, 33), (90, 70), (840, 1297)])
+@pytest.mark.parametrize("lam", [0.0, 0.2, 1.0])
+def test_random_images(shape, lam):
+    rng = np.random.default_rng(shape[0] * 7 + int(lam * 10))
+    x = rng.uniform(0, 1, shape + (3,))
+    y = np.clip(x + rng.normal(0, 0.2, x.shape), 0, 1)
+    _check(x, y, lam, f"{shape} lam {lam}")
+
+
+def test_reference_cases_and_device_tensors():
+    from paper_2505_19175_b200 import losses as DL
+    x = f32(np.random.default_rng(3).uniform(0, 1, (16, 16, 3)))
+    assert DL.photometric_loss(x, x, 0.2)[0] == pytest.approx(0.0, abs=1e-12)
+    assert DL.photometric_loss(np.zeros((16, 16, 3)), np.ones((16, 16, 3)), 0.0)[0] == pytest.approx(1.0)
+    assert DL.photometric_loss(np.full((4, 4, 3), 0.3), np.full((4, 4, 3), 0.7), 0.5)[0] == pytest.approx(0.2,
+                                                                                                          abs=1e-7)
+    assert DL.ssim(x, x) == pytest.approx(1.0)
+    with pytest.raises(ValueError):
+        DL.ssim(np.zeros((16, 16, 3)), np.zeros((17, 16, 3)))
+    with pytest.raises(ValueError):
+        DL.photometric_loss(np.zeros((16, 16, 3)), np.zeros((17, 16, 3)), 0.2)
+    # CUDA tensors in, CUDA gradient out (no host round trip)
+    xt = torch.rand((64, 48, 3), device="cuda")
+    yt = torch.rand((64, 48, 3), device="cuda")
+    loss, g = DL.photometric_loss(xt, yt, 0.2)
+    assert g.is_cuda and g.dtype == torch.float32 and g.shape == xt.shape
+    wl, wg = OL.photometric_loss(xt.double().cpu().numpy(), yt.double().cpu().numpy(), 0.2)
+    assert abs(loss - wl) <= 1e-9
+    assert np.abs(g.double().cpu().numpy() - wg).max() <= 1e-5 * np.abs(wg).max()
