@@ -1,18 +1,21 @@
 // ts_loss.cu -- on-device photometric loss: the
 // reference's (1-lam) L1 + lam (1-SSIM)/2 and its gradient w.r.t. the
-// rendered image (trisplat/losses.py:46-142), fp64 statistics.
+// rendered image (trisplat/losses.py:46-142).  The separable window sums run
+// in fp32 (the SSIM stabilisers c1 = 1e-4, c2 = 9e-4 dominate the fp32
+// cancellation error of E[x^2] - E[x]^2 ~ 1e-8); the per-window SSIM value and
+// its partials are evaluated in fp64.
 //
 //   k_ssim_stats  -- CTA = 16x16 valid 11x11 windows of one channel: the
 //                    26x26 input patch of x and y in shared memory, separable
-//                    Gaussian sums of x, y, x^2, xy, y^2 (horizontal pass over
+//                    Gaussian sums of x, y, x^2, xy, y^2 (fp32; horizontal pass over
 //                    26 rows, vertical pass per window), the SSIM map value and
 //                    its partials w.r.t. the window statistics (losses.py:
 //                    76-100), written as three fp32 gradient maps; the map sum
-//                    per channel by one fp64 atomic per CTA;
+//                    per CTA as an fp64 partial;
 //   k_ssim_grad   -- CTA = 16x16 pixels of one channel: the adjoint (same,
 //                    zero-embedded) correlations of the three maps (:69-73,
 //                    :101-106) combined with x and y, plus the L1 term's sign
-//                    gradient and |diff| sum (:130-132), into d_image;
+//                    gradient and |diff| partial (:130-132), into d_image;
 //   k_loss_final  -- the scalar loss and mean SSIM (:133-142).
 #include "ts_kernels.cuh"
 
@@ -47,33 +50,34 @@ __device__ __forceinline__ double block_sum_256(double v, double* s_red) {
 }  // namespace
 
 __global__ void __launch_bounds__(256) k_ssim_stats(const float* __restrict__ x, const float* __restrict__ y, int H,
-                                                    int W, float* __restrict__ gmap, double* __restrict__ sums) {
-    __shared__ double s_x[LP][LP + 1], s_y[LP][LP + 1];
-    __shared__ double s_h[5][LP][LT];
-    __shared__ double s_w[LW];
+                                                    int W, float* __restrict__ gmap, double* __restrict__ part) {
+    __shared__ float s_x[LP][LP + 1], s_y[LP][LP + 1];
+    __shared__ float s_h[5][LP][LT];
+    __shared__ float s_w[LW];
     __shared__ double s_red[8];
     const int c = blockIdx.z, Hv = H - 2 * LH, Wv = W - 2 * LH;
     const int v0 = blockIdx.y * LT, u0 = blockIdx.x * LT;  // first valid window (row, col)
     const int tid = threadIdx.y * LT + threadIdx.x;
-    if (tid < LW) s_w[tid] = gw(tid);
+    if (tid < LW) s_w[tid] = (float)gw(tid);
     for (int k = tid; k < LP * LP; k += 256) {
         const int r = k / LP, q = k % LP, i = v0 + r, j = u0 + q;
         const bool in = i < H && j < W;
-        s_x[r][q] = in ? (double)x[((size_t)i * W + j) * 3 + c] : 0.0;
-        s_y[r][q] = in ? (double)y[((size_t)i * W + j) * 3 + c] : 0.0;
+        s_x[r][q] = in ? x[((size_t)i * W + j) * 3 + c] : 0.f;
+        s_y[r][q] = in ? y[((size_t)i * W + j) * 3 + c] : 0.f;
     }
     __syncthreads();
     for (int k = tid; k < LP * LT; k += 256) {  // horizontal pass
         const int r = k / LT, q = k % LT;
-        double a = 0, b = 0, aa = 0, ab = 0, bb = 0;
+        float a = 0, b = 0, aa = 0, ab = 0, bb = 0;
 #pragma unroll
         for (int t = 0; t < LW; t++) {
-            const double w = s_w[t], xv = s_x[r][q + t], yv = s_y[r][q + t];
-            a = fma(w, xv, a);
-            b = fma(w, yv, b);
-            aa = fma(w, xv * xv, aa);
-            ab = fma(w, xv * yv, ab);
-            bb = fma(w, yv * yv, bb);
+            const float w = s_w[t], xv = s_x[r][q + t], yv = s_y[r][q + t];
+            const float wx = w * xv, wy = w * yv;
+            a += wx;
+            b += wy;
+            aa = fmaf(wx, xv, aa);
+            ab = fmaf(wx, yv, ab);
+            bb = fmaf(wy, yv, bb);
         }
         s_h[0][r][q] = a; s_h[1][r][q] = b; s_h[2][r][q] = aa; s_h[3][r][q] = ab; s_h[4][r][q] = bb;
     }
@@ -81,21 +85,22 @@ __global__ void __launch_bounds__(256) k_ssim_stats(const float* __restrict__ x,
     const int vi = v0 + threadIdx.y, vj = u0 + threadIdx.x;
     double smap = 0.0;
     if (vi < Hv && vj < Wv) {
-        double st[5] = {0, 0, 0, 0, 0};
+        float sf[5] = {0, 0, 0, 0, 0};
 #pragma unroll
         for (int t = 0; t < LW; t++) {
-            const double w = s_w[t];
+            const float w = s_w[t];
 #pragma unroll
-            for (int m = 0; m < 5; m++) st[m] = fma(w, s_h[m][threadIdx.y + t][threadIdx.x], st[m]);
+            for (int m = 0; m < 5; m++) sf[m] = fmaf(w, s_h[m][threadIdx.y + t][threadIdx.x], sf[m]);
         }
+        const double st[5] = {sf[0], sf[1], sf[2], sf[3], sf[4]};
         const double mx = st[0], my = st[1];
         const double c1 = LK1 * LK1, c2 = LK2 * LK2;
         const double vx = st[2] - mx * mx, vy = st[4] - my * my, cxy = st[3] - mx * my;
         const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * cxy + c2;
         const double b1 = mx * mx + my * my + c1, b2 = vx + vy + c2;
-        const double bb = b1 * b2;
-        smap = (a1 * a2) / bb;
-        const double da1 = a2 / bb, da2 = a1 / bb, db1 = -smap / b1, db2 = -smap / b2;
+        const double ib = 1.0 / (b1 * b2);  // one division: 1/b1 = b2 ib, 1/b2 = b1 ib
+        smap = a1 * a2 * ib;
+        const double da1 = a2 * ib, da2 = a1 * ib, db1 = -smap * b2 * ib, db2 = -smap * b1 * ib;
         const double s = 1.0 / ((double)Hv * (double)Wv);
         const double g_mu = 2.0 * my * da1 + 2.0 * mx * db1 - 2.0 * my * da2 - 2.0 * mx * db2;
         const size_t plane = (size_t)Hv * Wv, o = (size_t)vi * Wv + vj;
@@ -104,16 +109,16 @@ __global__ void __launch_bounds__(256) k_ssim_stats(const float* __restrict__ x,
         g[plane + o] = (float)(db2 * s);
         g[2 * plane + o] = (float)(2.0 * da2 * s);
     }
-    const double t = block_sum_256(smap, s_red);
-    if (tid == 0) atomicAdd(sums + 1 + c, t);
+    const double t = block_sum_256(smap, s_red);  // per-CTA partial (no contended atomics)
+    if (tid == 0) part[((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
 }
 
 __global__ void __launch_bounds__(256) k_ssim_grad(const float* __restrict__ x, const float* __restrict__ y, int H,
                                                    int W, const float* __restrict__ gmap, int with_ssim, double lam,
-                                                   float* __restrict__ d_image, double* __restrict__ sums) {
+                                                   float* __restrict__ d_image, double* __restrict__ part) {
     __shared__ float s_g[3][LP][LP + 1];
-    __shared__ double s_h[3][LP][LT];
-    __shared__ double s_w[LW];
+    __shared__ float s_h[3][LP][LT];
+    __shared__ float s_w[LW];
     __shared__ double s_red[8];
     const int c = blockIdx.z, Hv = H - 2 * LH, Wv = W - 2 * LH;
     const int i0 = blockIdx.y * LT, j0 = blockIdx.x * LT;
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(256) k_ssim_grad(const float* __restrict__ x, 
     const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
     double dssim = 0.0;
     if (with_ssim) {
-        if (tid < LW) s_w[tid] = gw(tid);
+        if (tid < LW) s_w[tid] = (float)gw(tid);
         // zero-embedded maps: pixel (i, j) of the same correlation reads map
         // (i + a - 2 LH, j + b - 2 LH) for taps a, b in [0, LW)
         const size_t plane = (size_t)Hv * Wv;
@@ -137,25 +142,25 @@ __global__ void __launch_bounds__(256) k_ssim_grad(const float* __restrict__ x, 
         __syncthreads();
         for (int k = tid; k < LP * LT; k += 256) {
             const int r = k / LT, q = k % LT;
-            double a = 0, b = 0, d = 0;
+            float a = 0, b = 0, d = 0;
 #pragma unroll
             for (int t = 0; t < LW; t++) {
-                const double w = s_w[t];
-                a = fma(w, (double)s_g[0][r][q + t], a);
-                b = fma(w, (double)s_g[1][r][q + t], b);
-                d = fma(w, (double)s_g[2][r][q + t], d);
+                const float w = s_w[t];
+                a = fmaf(w, s_g[0][r][q + t], a);
+                b = fmaf(w, s_g[1][r][q + t], b);
+                d = fmaf(w, s_g[2][r][q + t], d);
             }
             s_h[0][r][q] = a; s_h[1][r][q] = b; s_h[2][r][q] = d;
         }
         __syncthreads();
         if (i < H && j < W) {
-            double am = 0, ae = 0, ax = 0;
+            float am = 0, ae = 0, ax = 0;
 #pragma unroll
             for (int t = 0; t < LW; t++) {
-                const double w = s_w[t];
-                am = fma(w, s_h[0][threadIdx.y + t][threadIdx.x], am);
-                ae = fma(w, s_h[1][threadIdx.y + t][threadIdx.x], ae);
-                ax = fma(w, s_h[2][threadIdx.y + t][threadIdx.x], ax);
+                const float w = s_w[t];
+                am = fmaf(w, s_h[0][threadIdx.y + t][threadIdx.x], am);
+                ae = fmaf(w, s_h[1][threadIdx.y + t][threadIdx.x], ae);
+                ax = fmaf(w, s_h[2][threadIdx.y + t][threadIdx.x], ax);
             }
             const double xv = x[((size_t)i * W + j) * 3 + c], yv = y[((size_t)i * W + j) * 3 + c];
             dssim = am + 2.0 * xv * ae + yv * ax;
@@ -174,42 +179,72 @@ __global__ void __launch_bounds__(256) k_ssim_grad(const float* __restrict__ x, 
         }
     }
     const double t = block_sum_256(ad, s_red);
-    if (tid == 0) atomicAdd(sums, t);
+    if (tid == 0) part[((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
 }
 
-__global__ void k_loss_final(int H, int W, int with_ssim, double lam, const double* __restrict__ sums,
-                             double* __restrict__ out) {
-    const double l1 = sums[0] / (3.0 * (double)H * (double)W);
-    double sv = 1.0;
-    if (with_ssim) {
-        const double np = (double)(H - 2 * LH) * (double)(W - 2 * LH);
-        sv = (sums[1] + sums[2] + sums[3]) / (3.0 * np);
+// one CTA: sums of the per-CTA partials (|diff| and SSIM map), the loss
+__global__ void __launch_bounds__(256) k_loss_final(int H, int W, int with_ssim, double lam,
+                                                    const double* __restrict__ pl1, int nl1,
+                                                    const double* __restrict__ pss, int nss,
+                                                    double* __restrict__ out) {
+    __shared__ double s_red[8];
+    double a = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < nl1; k += 256) a += pl1[k];
+    for (int k = threadIdx.x; k < nss; k += 256) b += pss[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
     }
-    out[0] = lam == 0.0 ? l1 : (1.0 - lam) * l1 + lam * (1.0 - sv) / 2.0;
-    out[1] = sv;
+    __shared__ double s_b[8];
+    if ((threadIdx.x & 31) == 0) {
+        s_red[threadIdx.x >> 5] = a;
+        s_b[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sa = 0.0, sb = 0.0;
+        for (int w = 0; w < 8; w++) {
+            sa += s_red[w];
+            sb += s_b[w];
+        }
+        const double l1 = sa / (3.0 * (double)H * (double)W);
+        double sv = 1.0;
+        if (with_ssim) sv = sb / (3.0 * (double)(H - 2 * LH) * (double)(W - 2 * LH));
+        out[0] = lam == 0.0 ? l1 : (1.0 - lam) * l1 + lam * (1.0 - sv) / 2.0;
+        out[1] = sv;
+    }
 }
+
+static inline size_t tiles_of(int n) { return (size_t)((n + LT - 1) / LT); }
 
 size_t photometric_scratch_bytes(int H, int W) {
     const size_t hv = H > 2 * LH ? (size_t)(H - 2 * LH) : 0, wv = W > 2 * LH ? (size_t)(W - 2 * LH) : 0;
-    return 64 + sizeof(float) * 9 * hv * wv;
+    const size_t parts = 3 * (tiles_of(H) * tiles_of(W) + tiles_of((int)hv) * tiles_of((int)wv));
+    return sizeof(double) * parts + sizeof(float) * 9 * hv * wv + 256;
 }
 
 // scratch: photometric_scratch_bytes(H, W), 16-byte aligned
 void launch_photometric_loss(const float* x, const float* y, int H, int W, double lam, double* out, float* d_image,
                              void* scratch, bool ssim_only, cudaStream_t st) {
-    double* sums = (double*)scratch;  // |diff| sum, 3 SSIM map sums
-    float* gmap = (float*)((char*)scratch + 64);
-    cudaMemsetAsync(sums, 0, 4 * sizeof(double), st);
     const bool with_ssim = (lam != 0.0 || ssim_only) && H >= LW && W >= LW;
+    const int Hv = H - 2 * LH, Wv = W - 2 * LH;
+    const int nl1 = 3 * (int)(tiles_of(H) * tiles_of(W));
+    const int nss = with_ssim ? 3 * (int)(tiles_of(Hv) * tiles_of(Wv)) : 0;
+    double* pl1 = (double*)scratch;  // per-CTA |diff| partials
+    double* pss = pl1 + nl1;          // per-CTA SSIM map partials
+    float* gmap = (float*)(((uintptr_t)(pss + (with_ssim ? nss : 0)) + 15) & ~(uintptr_t)15);
     if (with_ssim) {
-        const dim3 g((W - 2 * LH + LT - 1) / LT, (H - 2 * LH + LT - 1) / LT, 3);
-        k_ssim_stats<<<g, dim3(LT, LT), 0, st>>>(x, y, H, W, gmap, sums);
+        const dim3 g((unsigned)tiles_of(Wv), (unsigned)tiles_of(Hv), 3);
+        k_ssim_stats<<<g, dim3(LT, LT), 0, st>>>(x, y, H, W, gmap, pss);
     }
+    int nl = 0;
     if (!ssim_only || !with_ssim) {
-        const dim3 g((W + LT - 1) / LT, (H + LT - 1) / LT, 3);
-        k_ssim_grad<<<g, dim3(LT, LT), 0, st>>>(x, y, H, W, gmap, with_ssim && !ssim_only, lam, d_image, sums);
+        const dim3 g((unsigned)tiles_of(W), (unsigned)tiles_of(H), 3);
+        k_ssim_grad<<<g, dim3(LT, LT), 0, st>>>(x, y, H, W, gmap, with_ssim && !ssim_only, lam, d_image, pl1);
+        nl = nl1;
     }
-    k_loss_final<<<1, 1, 0, st>>>(H, W, with_ssim ? 1 : 0, ssim_only ? 1.0 : lam, sums, out);
+    k_loss_final<<<1, 256, 0, st>>>(H, W, with_ssim ? 1 : 0, ssim_only ? 1.0 : lam, pl1, nl, pss, nss, out);
 }
 
 }  // namespace ts

