@@ -5,14 +5,14 @@
 // cancellation error of E[x^2] - E[x]^2 ~ 1e-8); the per-window SSIM value and
 // its partials are evaluated in fp64.
 //
-//   k_ssim_stats  -- CTA = 16x16 valid 11x11 windows of one channel: the
-//                    26x26 input patch of x and y in shared memory, separable
+//   k_ssim_stats  -- CTA = 32x16 valid 11x11 windows of the three channels: the
+//                    42x26 input patch of x and y in shared memory, separable
 //                    Gaussian sums of x, y, x^2, xy, y^2 (fp32; horizontal pass over
 //                    26 rows, vertical pass per window), the SSIM map value and
 //                    its partials w.r.t. the window statistics (losses.py:
 //                    76-100), written as three fp32 gradient maps; the map sum
 //                    per CTA as an fp64 partial;
-//   k_ssim_grad   -- CTA = 16x16 pixels of one channel: the adjoint (same,
+//   k_ssim_grad   -- CTA = 32x16 pixels of the three channels: the adjoint (same,
 //                    zero-embedded) correlations of the three maps (:69-73,
 //                    :101-106) combined with x and y, plus the L1 term's sign
 //                    gradient and |diff| partial (:130-132), into d_image;
@@ -22,7 +22,7 @@
 namespace ts {
 
 namespace {
-constexpr int LW = 11, LH = 5, LT = 16, LP = LT + LW - 1;  // window, half, tile, patch
+constexpr int LW = 11, LH = 5;  // window, half width
 constexpr double LK1 = 0.01, LK2 = 0.03;
 
 __device__ __forceinline__ double gw(int k) {  // normalised Gaussian, sigma 1.5 (losses.py:48-52)
@@ -39,7 +39,7 @@ __device__ __forceinline__ double gw(int k) {  // normalised Gaussian, sigma 1.5
 __device__ __forceinline__ double block_sum_256(double v, double* s_red) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    const int tid = threadIdx.y * LT + threadIdx.x;
+    const int tid = threadIdx.x;
     if ((tid & 31) == 0) s_red[tid >> 5] = v;
     __syncthreads();
     double t = 0.0;
@@ -49,137 +49,165 @@ __device__ __forceinline__ double block_sum_256(double v, double* s_red) {
 }
 }  // namespace
 
+// CTA = TX x TY outputs (windows or pixels) of all three channels; 256
+// threads = TX x (TY / 2), two output rows per thread.  The interleaved RGB
+// patch arrives with coalesced row loads and is split into channel planes in
+// shared memory.
+constexpr int TX = 32, TY = 16, PX = TX + LW - 1, PY = TY + LW - 1;
+
 __global__ void __launch_bounds__(256) k_ssim_stats(const float* __restrict__ x, const float* __restrict__ y, int H,
                                                     int W, float* __restrict__ gmap, double* __restrict__ part) {
-    __shared__ float s_x[LP][LP + 1], s_y[LP][LP + 1];
-    __shared__ float s_h[5][LP][LT];
+    __shared__ float s_x[3][PY][PX + 1], s_y[3][PY][PX + 1];
+    __shared__ float s_h[5][PY][TX];
     __shared__ float s_w[LW];
     __shared__ double s_red[8];
-    const int c = blockIdx.z, Hv = H - 2 * LH, Wv = W - 2 * LH;
-    const int v0 = blockIdx.y * LT, u0 = blockIdx.x * LT;  // first valid window (row, col)
-    const int tid = threadIdx.y * LT + threadIdx.x;
+    const int Hv = H - 2 * LH, Wv = W - 2 * LH;
+    const int v0 = blockIdx.y * TY, u0 = blockIdx.x * TX;  // first valid window (row, col)
+    const int tid = threadIdx.x, tx = tid & (TX - 1), ty = tid / TX;
     if (tid < LW) s_w[tid] = (float)gw(tid);
-    for (int k = tid; k < LP * LP; k += 256) {
-        const int r = k / LP, q = k % LP, i = v0 + r, j = u0 + q;
+    for (int k = tid; k < PY * PX * 3; k += 256) {  // patch rows are 3 PX contiguous floats
+        const int r = k / (3 * PX), rem = k - r * 3 * PX, q = rem / 3, c = rem - q * 3;
+        const int i = v0 + r, j = u0 + q;
         const bool in = i < H && j < W;
-        s_x[r][q] = in ? x[((size_t)i * W + j) * 3 + c] : 0.f;
-        s_y[r][q] = in ? y[((size_t)i * W + j) * 3 + c] : 0.f;
+        const size_t o = ((size_t)i * W + j) * 3 + c;
+        s_x[c][r][q] = in ? x[o] : 0.f;
+        s_y[c][r][q] = in ? y[o] : 0.f;
     }
     __syncthreads();
-    for (int k = tid; k < LP * LT; k += 256) {  // horizontal pass
-        const int r = k / LT, q = k % LT;
-        float a = 0, b = 0, aa = 0, ab = 0, bb = 0;
+    const double s = 1.0 / ((double)Hv * (double)Wv);
+    const size_t plane = (size_t)Hv * Wv;
+    double smap_sum = 0.0;
+    for (int c = 0; c < 3; c++) {
+        for (int k = tid; k < PY * TX; k += 256) {  // horizontal pass
+            const int r = k / TX, q = k % TX;
+            float a = 0, b = 0, aa = 0, ab = 0, bb = 0;
 #pragma unroll
-        for (int t = 0; t < LW; t++) {
-            const float w = s_w[t], xv = s_x[r][q + t], yv = s_y[r][q + t];
-            const float wx = w * xv, wy = w * yv;
-            a += wx;
-            b += wy;
-            aa = fmaf(wx, xv, aa);
-            ab = fmaf(wx, yv, ab);
-            bb = fmaf(wy, yv, bb);
+            for (int t = 0; t < LW; t++) {
+                const float w = s_w[t], xv = s_x[c][r][q + t], yv = s_y[c][r][q + t];
+                const float wx = w * xv, wy = w * yv;
+                a += wx;
+                b += wy;
+                aa = fmaf(wx, xv, aa);
+                ab = fmaf(wx, yv, ab);
+                bb = fmaf(wy, yv, bb);
+            }
+            s_h[0][r][q] = a; s_h[1][r][q] = b; s_h[2][r][q] = aa; s_h[3][r][q] = ab; s_h[4][r][q] = bb;
         }
-        s_h[0][r][q] = a; s_h[1][r][q] = b; s_h[2][r][q] = aa; s_h[3][r][q] = ab; s_h[4][r][q] = bb;
-    }
-    __syncthreads();
-    const int vi = v0 + threadIdx.y, vj = u0 + threadIdx.x;
-    double smap = 0.0;
-    if (vi < Hv && vj < Wv) {
-        float sf[5] = {0, 0, 0, 0, 0};
+        __syncthreads();
 #pragma unroll
-        for (int t = 0; t < LW; t++) {
-            const float w = s_w[t];
+        for (int rr = 0; rr < 2; rr++) {
+            const int oy = ty + rr * (TY / 2);
+            const int vi = v0 + oy, vj = u0 + tx;
+            if (vi < Hv && vj < Wv) {
+                float sf[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-            for (int m = 0; m < 5; m++) sf[m] = fmaf(w, s_h[m][threadIdx.y + t][threadIdx.x], sf[m]);
+                for (int t = 0; t < LW; t++) {
+                    const float w = s_w[t];
+#pragma unroll
+                    for (int m = 0; m < 5; m++) sf[m] = fmaf(w, s_h[m][oy + t][tx], sf[m]);
+                }
+                const double mx = sf[0], my = sf[1];
+                const double c1 = LK1 * LK1, c2 = LK2 * LK2;
+                const double vx = (double)sf[2] - mx * mx, vy = (double)sf[4] - my * my;
+                const double cxy = (double)sf[3] - mx * my;
+                const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * cxy + c2;
+                const double b1 = mx * mx + my * my + c1, b2 = vx + vy + c2;
+                const double ib = 1.0 / (b1 * b2);  // one division: 1/b1 = b2 ib, 1/b2 = b1 ib
+                const double smap = a1 * a2 * ib;
+                const double da1 = a2 * ib, da2 = a1 * ib, db1 = -smap * b2 * ib, db2 = -smap * b1 * ib;
+                const double g_mu = 2.0 * my * da1 + 2.0 * mx * db1 - 2.0 * my * da2 - 2.0 * mx * db2;
+                const size_t o = (size_t)vi * Wv + vj;
+                float* g = gmap + (size_t)c * 3 * plane;
+                g[o] = (float)(g_mu * s);
+                g[plane + o] = (float)(db2 * s);
+                g[2 * plane + o] = (float)(2.0 * da2 * s);
+                smap_sum += smap;
+            }
         }
-        const double st[5] = {sf[0], sf[1], sf[2], sf[3], sf[4]};
-        const double mx = st[0], my = st[1];
-        const double c1 = LK1 * LK1, c2 = LK2 * LK2;
-        const double vx = st[2] - mx * mx, vy = st[4] - my * my, cxy = st[3] - mx * my;
-        const double a1 = 2.0 * mx * my + c1, a2 = 2.0 * cxy + c2;
-        const double b1 = mx * mx + my * my + c1, b2 = vx + vy + c2;
-        const double ib = 1.0 / (b1 * b2);  // one division: 1/b1 = b2 ib, 1/b2 = b1 ib
-        smap = a1 * a2 * ib;
-        const double da1 = a2 * ib, da2 = a1 * ib, db1 = -smap * b2 * ib, db2 = -smap * b1 * ib;
-        const double s = 1.0 / ((double)Hv * (double)Wv);
-        const double g_mu = 2.0 * my * da1 + 2.0 * mx * db1 - 2.0 * my * da2 - 2.0 * mx * db2;
-        const size_t plane = (size_t)Hv * Wv, o = (size_t)vi * Wv + vj;
-        float* g = gmap + (size_t)c * 3 * plane;
-        g[o] = (float)(g_mu * s);
-        g[plane + o] = (float)(db2 * s);
-        g[2 * plane + o] = (float)(2.0 * da2 * s);
+        __syncthreads();
     }
-    const double t = block_sum_256(smap, s_red);  // per-CTA partial (no contended atomics)
-    if (tid == 0) part[((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    const double t = block_sum_256(smap_sum, s_red);  // per-CTA partial (no contended atomics)
+    if (tid == 0) part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
 }
 
 __global__ void __launch_bounds__(256) k_ssim_grad(const float* __restrict__ x, const float* __restrict__ y, int H,
                                                    int W, const float* __restrict__ gmap, int with_ssim, double lam,
                                                    float* __restrict__ d_image, double* __restrict__ part) {
-    __shared__ float s_g[3][LP][LP + 1];
-    __shared__ float s_h[3][LP][LT];
+    __shared__ float s_g[3][PY][PX + 1];
+    __shared__ float s_h[3][PY][TX];
     __shared__ float s_w[LW];
     __shared__ double s_red[8];
-    const int c = blockIdx.z, Hv = H - 2 * LH, Wv = W - 2 * LH;
-    const int i0 = blockIdx.y * LT, j0 = blockIdx.x * LT;
-    const int tid = threadIdx.y * LT + threadIdx.x;
-    const int i = i0 + threadIdx.y, j = j0 + threadIdx.x;
-    double dssim = 0.0;
-    if (with_ssim) {
-        if (tid < LW) s_w[tid] = (float)gw(tid);
-        // zero-embedded maps: pixel (i, j) of the same correlation reads map
-        // (i + a - 2 LH, j + b - 2 LH) for taps a, b in [0, LW)
-        const size_t plane = (size_t)Hv * Wv;
-        const float* g = gmap + (size_t)c * 3 * plane;
-        for (int k = tid; k < LP * LP; k += 256) {
-            const int r = k / LP, q = k % LP, vi = i0 + r - 2 * LH, vj = j0 + q - 2 * LH;
-            const bool in = vi >= 0 && vi < Hv && vj >= 0 && vj < Wv;
-            const size_t o = in ? (size_t)vi * Wv + vj : 0;
-            s_g[0][r][q] = in ? g[o] : 0.f;
-            s_g[1][r][q] = in ? g[plane + o] : 0.f;
-            s_g[2][r][q] = in ? g[2 * plane + o] : 0.f;
-        }
-        __syncthreads();
-        for (int k = tid; k < LP * LT; k += 256) {
-            const int r = k / LT, q = k % LT;
-            float a = 0, b = 0, d = 0;
-#pragma unroll
-            for (int t = 0; t < LW; t++) {
-                const float w = s_w[t];
-                a = fmaf(w, s_g[0][r][q + t], a);
-                b = fmaf(w, s_g[1][r][q + t], b);
-                d = fmaf(w, s_g[2][r][q + t], d);
-            }
-            s_h[0][r][q] = a; s_h[1][r][q] = b; s_h[2][r][q] = d;
-        }
-        __syncthreads();
-        if (i < H && j < W) {
-            float am = 0, ae = 0, ax = 0;
-#pragma unroll
-            for (int t = 0; t < LW; t++) {
-                const float w = s_w[t];
-                am = fmaf(w, s_h[0][threadIdx.y + t][threadIdx.x], am);
-                ae = fmaf(w, s_h[1][threadIdx.y + t][threadIdx.x], ae);
-                ax = fmaf(w, s_h[2][threadIdx.y + t][threadIdx.x], ax);
-            }
-            const double xv = x[((size_t)i * W + j) * 3 + c], yv = y[((size_t)i * W + j) * 3 + c];
-            dssim = am + 2.0 * xv * ae + yv * ax;
-        }
-    }
+    const int Hv = H - 2 * LH, Wv = W - 2 * LH;
+    const int i0 = blockIdx.y * TY, j0 = blockIdx.x * TX;
+    const int tid = threadIdx.x, tx = tid & (TX - 1), ty = tid / TX;
+    const double n = 3.0 * (double)H * (double)W;
+    const size_t plane = (size_t)Hv * Wv;
     double ad = 0.0;
-    if (i < H && j < W) {
-        const size_t o = ((size_t)i * W + j) * 3 + c;
-        const double d = (double)x[o] - (double)y[o];
-        ad = fabs(d);
-        const double sgn = (double)((d > 0.0) - (d < 0.0));
-        const double n = 3.0 * (double)H * (double)W;
-        if (d_image) {
-            const double gl = lam == 0.0 ? sgn / n : (1.0 - lam) * sgn / n - (lam / 2.0) * dssim / 3.0;
-            d_image[o] = (float)gl;
+    if (with_ssim && tid < LW) s_w[tid] = (float)gw(tid);
+    for (int c = 0; c < 3; c++) {
+        double dss[2] = {0.0, 0.0};
+        if (with_ssim) {
+            // zero-embedded maps: pixel (i, j) of the same correlation reads map
+            // (i + a - 2 LH, j + b - 2 LH) for taps a, b in [0, LW)
+            const float* g = gmap + (size_t)c * 3 * plane;
+            for (int k = tid; k < PY * PX; k += 256) {
+                const int r = k / PX, q = k % PX, vi = i0 + r - 2 * LH, vj = j0 + q - 2 * LH;
+                const bool in = vi >= 0 && vi < Hv && vj >= 0 && vj < Wv;
+                const size_t o = in ? (size_t)vi * Wv + vj : 0;
+                s_g[0][r][q] = in ? g[o] : 0.f;
+                s_g[1][r][q] = in ? g[plane + o] : 0.f;
+                s_g[2][r][q] = in ? g[2 * plane + o] : 0.f;
+            }
+            __syncthreads();
+            for (int k = tid; k < PY * TX; k += 256) {
+                const int r = k / TX, q = k % TX;
+                float a = 0, b = 0, d = 0;
+#pragma unroll
+                for (int t = 0; t < LW; t++) {
+                    const float w = s_w[t];
+                    a = fmaf(w, s_g[0][r][q + t], a);
+                    b = fmaf(w, s_g[1][r][q + t], b);
+                    d = fmaf(w, s_g[2][r][q + t], d);
+                }
+                s_h[0][r][q] = a; s_h[1][r][q] = b; s_h[2][r][q] = d;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+                const int oy = ty + rr * (TY / 2), i = i0 + oy, j = j0 + tx;
+                if (i < H && j < W) {
+                    float am = 0, ae = 0, ax = 0;
+#pragma unroll
+                    for (int t = 0; t < LW; t++) {
+                        const float w = s_w[t];
+                        am = fmaf(w, s_h[0][oy + t][tx], am);
+                        ae = fmaf(w, s_h[1][oy + t][tx], ae);
+                        ax = fmaf(w, s_h[2][oy + t][tx], ax);
+                    }
+                    const size_t o = ((size_t)i * W + j) * 3 + c;
+                    dss[rr] = (double)am + 2.0 * (double)x[o] * ae + (double)y[o] * ax;  // (fp64: the terms cancel)
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int i = i0 + ty + rr * (TY / 2), j = j0 + tx;
+            if (i < H && j < W) {
+                const size_t o = ((size_t)i * W + j) * 3 + c;
+                const double d = (double)x[o] - (double)y[o];
+                ad += fabs(d);
+                const double sgn = (double)((d > 0.0) - (d < 0.0));
+                if (d_image) {
+                    const double gl = lam == 0.0 ? sgn / n
+                                                 : (1.0 - lam) * sgn / n - (lam / 2.0) * dss[rr] / 3.0;
+                    d_image[o] = (float)gl;
+                }
+            }
         }
     }
     const double t = block_sum_256(ad, s_red);
-    if (tid == 0) part[((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    if (tid == 0) part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
 }
 
 // one CTA: sums of the per-CTA partials (|diff| and SSIM map), the loss
@@ -216,11 +244,12 @@ __global__ void __launch_bounds__(256) k_loss_final(int H, int W, int with_ssim,
     }
 }
 
-static inline size_t tiles_of(int n) { return (size_t)((n + LT - 1) / LT); }
+static inline size_t tiles_x(int n) { return (size_t)((n + TX - 1) / TX); }
+static inline size_t tiles_y(int n) { return (size_t)((n + TY - 1) / TY); }
 
 size_t photometric_scratch_bytes(int H, int W) {
     const size_t hv = H > 2 * LH ? (size_t)(H - 2 * LH) : 0, wv = W > 2 * LH ? (size_t)(W - 2 * LH) : 0;
-    const size_t parts = 3 * (tiles_of(H) * tiles_of(W) + tiles_of((int)hv) * tiles_of((int)wv));
+    const size_t parts = tiles_x(W) * tiles_y(H) + tiles_x((int)wv) * tiles_y((int)hv);
     return sizeof(double) * parts + sizeof(float) * 9 * hv * wv + 256;
 }
 
@@ -229,19 +258,17 @@ void launch_photometric_loss(const float* x, const float* y, int H, int W, doubl
                              void* scratch, bool ssim_only, cudaStream_t st) {
     const bool with_ssim = (lam != 0.0 || ssim_only) && H >= LW && W >= LW;
     const int Hv = H - 2 * LH, Wv = W - 2 * LH;
-    const int nl1 = 3 * (int)(tiles_of(H) * tiles_of(W));
-    const int nss = with_ssim ? 3 * (int)(tiles_of(Hv) * tiles_of(Wv)) : 0;
+    const int nl1 = (int)(tiles_x(W) * tiles_y(H));
+    const int nss = with_ssim ? (int)(tiles_x(Wv) * tiles_y(Hv)) : 0;
     double* pl1 = (double*)scratch;  // per-CTA |diff| partials
     double* pss = pl1 + nl1;          // per-CTA SSIM map partials
-    float* gmap = (float*)(((uintptr_t)(pss + (with_ssim ? nss : 0)) + 15) & ~(uintptr_t)15);
-    if (with_ssim) {
-        const dim3 g((unsigned)tiles_of(Wv), (unsigned)tiles_of(Hv), 3);
-        k_ssim_stats<<<g, dim3(LT, LT), 0, st>>>(x, y, H, W, gmap, pss);
-    }
+    float* gmap = (float*)(((uintptr_t)(pss + nss) + 15) & ~(uintptr_t)15);
+    if (with_ssim)
+        k_ssim_stats<<<dim3((unsigned)tiles_x(Wv), (unsigned)tiles_y(Hv)), 256, 0, st>>>(x, y, H, W, gmap, pss);
     int nl = 0;
     if (!ssim_only || !with_ssim) {
-        const dim3 g((unsigned)tiles_of(W), (unsigned)tiles_of(H), 3);
-        k_ssim_grad<<<g, dim3(LT, LT), 0, st>>>(x, y, H, W, gmap, with_ssim && !ssim_only, lam, d_image, pl1);
+        k_ssim_grad<<<dim3((unsigned)tiles_x(W), (unsigned)tiles_y(H)), 256, 0, st>>>(
+            x, y, H, W, gmap, with_ssim && !ssim_only, lam, d_image, pl1);
         nl = nl1;
     }
     k_loss_final<<<1, 256, 0, st>>>(H, W, with_ssim ? 1 : 0, ssim_only ? 1.0 : lam, pl1, nl, pss, nss, out);
