@@ -175,6 +175,18 @@ int ts_photometric_loss(ts_context* ctx, const float* rendered, const float* tar
 /* Mean SSIM over channels (losses.py:110-119) into out[1] (device double[2]). */
 int ts_ssim(ts_context* ctx, const float* x, const float* y, int height, int width, double* out, void* stream);
 
+/* Adam step (training.py:81-110) in place on fp32 device parameters
+ * (vertices (N,3,3), opacity (N), sigma (N), sh (N,16,3)) with the gradients
+ * of ts_backward; m, v: device fp32 moments of 59 N elements in the flat
+ * gradient layout [vertices | opacity | sigma | sh], zero-initialised by the
+ * caller; t: the step number after this step (1 for the first); lrs: host
+ * double[4] per-group rates; bad: device int64[4] receiving, per group, the
+ * first triangle with a non-finite gradient (-1 if none) -- if any
+ * group has one, nothing is updated (the reference raises ValueError). */
+int ts_adam_step(ts_context* ctx, float* vertices, float* opacity, float* sigma, float* sh, int64_t n,
+                 const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
+                 void* stream);
+
 /* Debug/parity dumps of the last forward pass (device destination):
  *  TS_DUMP_SORTED_IDX  int32[M]       depth-sorted source ids (render.py:275-277)
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)

@@ -762,6 +762,18 @@ int ts_photometric_loss(ts_context* c, const float* rendered, const float* targe
     return cuda_err(cudaGetLastError());
 }
 
+int ts_adam_step(ts_context* c, float* vertices, float* opacity, float* sigma, float* sh, int64_t n,
+                 const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
+                 void* stream) {
+    if (!c || !grads || !lrs || !bad || n < 0 || t < 1) return TS_ERR_INVALID_ARG;
+    if (n > 0 && (!vertices || !opacity || !sigma || !sh || !m || !v)) return TS_ERR_INVALID_ARG;
+    float* const params[4] = {vertices, opacity, sigma, sh};
+    const float* const g[4] = {grads->d_vertices, grads->d_opacity, grads->d_sigma, grads->d_sh};
+    launch_adam_step(params, g, n, m, v, t, lrs, (long long*)bad, (cudaStream_t)stream);
+    g_launches += n > 0 ? 2 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
 int ts_ssim(ts_context* c, const float* x, const float* y, int height, int width, double* out, void* stream) {
     if (!c || !x || !y || !out || height < 1 || width < 1) return TS_ERR_INVALID_ARG;
     int rc;

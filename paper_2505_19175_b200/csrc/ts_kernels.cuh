@@ -180,6 +180,10 @@ void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st);
 size_t onesweep_scratch_bytes(long long max_count, int max_passes);
 int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
                       unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
+// ts_optim.cu: fused Adam step (bad: device int64[4], first non-finite triangle per group)
+void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
+                      long long t, const double lrs[4], long long* bad, cudaStream_t st);
+
 // ts_loss.cu: photometric loss (L1 + D-SSIM) and gradient
 size_t photometric_scratch_bytes(int H, int W);
 void launch_photometric_loss(const float* x, const float* y, int H, int W, double lam, double* out, float* d_image,

@@ -1,0 +1,84 @@
+// ts_optim.cu -- fused Adam step on the device: the
+// reference's adam_step (trisplat/training.py:81-110) over the 59 fp32
+// parameters of every triangle, with per-group learning rates and the opacity
+// / sigma clamps, moments kept in fp32 on the device.
+//
+//   k_adam_check  -- thread per parameter element: a non-finite gradient
+//                    records the smallest offending triangle of its group
+//                    (the reference raises before touching any state);
+//   k_adam_update -- thread per element, skipped entirely if any group was
+//                    flagged: m, v, bias-corrected step in fp64, clamps.
+// Element e of the flat 59 N space (the DeviceGrads / moment layout
+// [vertices 9N | opacity N | sigma N | sh 48N]) reads the parameter tensors
+// in place, so one grid covers all groups with coalesced accesses.
+#include "ts_kernels.cuh"
+
+namespace ts {
+
+namespace {
+constexpr double ADAM_B1 = 0.9, ADAM_B2 = 0.999, ADAM_EPS = 1e-15;
+
+struct AdamGroups {
+    float* p[4];
+    const float* g[4];
+    long long off[5];  // element offsets of the groups; off[4] = 59 N
+    int width[4];      // elements per triangle
+    double lr[4];
+};
+
+__device__ __forceinline__ int group_of(const AdamGroups& a, long long e) {
+    return e < a.off[1] ? 0 : (e < a.off[2] ? 1 : (e < a.off[3] ? 2 : 3));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_adam_check(AdamGroups a, unsigned long long* __restrict__ bad) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.off[4]) return;
+    const int k = group_of(a, e);
+    const long long local = e - a.off[k];
+    if (!isfinite(a.g[k][local])) atomicMin(bad + k, (unsigned long long)(local / a.width[k]));
+}
+
+__global__ void __launch_bounds__(256) k_adam_update(AdamGroups a, float* __restrict__ m, float* __restrict__ v,
+                                                     double bc1, double bc2,
+                                                     const unsigned long long* __restrict__ bad) {
+    if ((bad[0] & bad[1] & bad[2] & bad[3]) != ~0ull) return;  // some group flagged
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.off[4]) return;
+    const int k = group_of(a, e);
+    const long long local = e - a.off[k];
+    const double g = (double)a.g[k][local];
+    const double mm = ADAM_B1 * (double)m[e] + (1.0 - ADAM_B1) * g;
+    const double vv = ADAM_B2 * (double)v[e] + (1.0 - ADAM_B2) * g * g;
+    m[e] = (float)mm;
+    v[e] = (float)vv;
+    double p = (double)a.p[k][local] - a.lr[k] * (mm / bc1) / (sqrt(vv / bc2) + ADAM_EPS);
+    if (k == 1) p = fmin(fmax(p, 1e-4), 1.0 - 1e-4);  // opacity clamp
+    if (k == 2) p = fmin(fmax(p, 1e-3), 1e3);         // sigma clamp
+    a.p[k][local] = (float)p;
+}
+
+void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
+                      long long t, const double lrs[4], long long* bad, cudaStream_t st) {
+    AdamGroups a;
+    const int width[4] = {9, 1, 1, 48};
+    long long off = 0;
+    for (int k = 0; k < 4; k++) {
+        a.p[k] = params[k];
+        a.g[k] = grads[k];
+        a.width[k] = width[k];
+        a.lr[k] = lrs[k];
+        a.off[k] = off;
+        off += (long long)width[k] * n;
+    }
+    a.off[4] = off;
+    unsigned long long* b = (unsigned long long*)bad;
+    cudaMemsetAsync(b, 0xff, 4 * sizeof(unsigned long long), st);  // "none" = all bits set (-1 as int64)
+    if (off == 0) return;
+    const unsigned grid = (unsigned)((off + 255) / 256);
+    k_adam_check<<<grid, 256, 0, st>>>(a, b);
+    const double bc1 = 1.0 - pow(ADAM_B1, (double)t), bc2 = 1.0 - pow(ADAM_B2, (double)t);
+    k_adam_update<<<grid, 256, 0, st>>>(a, m, v, bc1, bc2, b);
+}
+
+}  // namespace ts

@@ -1,0 +1,63 @@
+"""Fused Adam on the device: drop-in for the reference's
+``adam_step`` / ``AdamState`` (trisplat/training.py:49-110) over a
+``DeviceSoup`` (fp32 parameters, updated in place) and ``DeviceGrads``.
+
+Same semantics as the reference: the first triangle with a non-finite
+gradient (first group in vertices, opacity, sigma, sh order) raises
+``ValueError("non-finite <group> gradient for triangle <i>")`` before any
+state changes; otherwise t += 1, bias-corrected Adam per group with the
+per-group learning rates, then opacity clamped to (1e-4, 1-1e-4) and sigma
+to (1e-3, 1e3).  Moments are fp32 device buffers in the flat gradient layout.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+GROUPS = ("vertices", "opacity", "sigma", "sh")
+
+
+@dataclass
+class DeviceAdamState:
+    m: "object"   # torch fp32 (59 N,)
+    v: "object"
+    n: int
+    t: int = 0
+
+    @classmethod
+    def zeros(cls, n: int, device="cuda") -> "DeviceAdamState":
+        import torch
+        return cls(torch.zeros(59 * n, dtype=torch.float32, device=device),
+                   torch.zeros(59 * n, dtype=torch.float32, device=device), n, 0)
+
+
+def adam_step(soup, grads, state: DeviceAdamState, lrs: dict, rasterizer=None, stream=None, check=True):
+    """One in-place Adam update of ``soup`` (DeviceSoup, fp32) with ``grads``
+    (DeviceGrads).  ``check=False`` skips the host read of the finiteness flags
+    (the device still skips the update if any gradient is non-finite)."""
+    import torch
+    from . import _lib
+    from .rasterizer import default_rasterizer
+    if soup.vertices.dtype != torch.float32:
+        raise TypeError("adam_step needs fp32 device parameters")
+    n = len(soup)
+    if state.n != n or grads.n != n:
+        raise ValueError("state / gradient size differs from the soup")
+    r = rasterizer or default_rasterizer()
+    bad = torch.empty(4, dtype=torch.int64, device="cuda")
+    lr = (ctypes.c_double * 4)(*[float(lrs[k]) for k in GROUPS])
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    g = grads._ts()
+    rc = r.lib.ts_adam_step(r._ctx, ctypes.c_void_p(soup.vertices.data_ptr()),
+                            ctypes.c_void_p(soup.opacity.data_ptr()), ctypes.c_void_p(soup.sigma.data_ptr()),
+                            ctypes.c_void_p(soup.sh.data_ptr()), n, ctypes.byref(g),
+                            ctypes.c_void_p(state.m.data_ptr()), ctypes.c_void_p(state.v.data_ptr()),
+                            state.t + 1, lr, ctypes.c_void_p(bad.data_ptr()), ctypes.c_void_p(st))
+    _lib.check(rc, "adam_step")
+    if check:
+        b = bad.cpu().tolist()
+        for k, i in zip(GROUPS, b):
+            if i >= 0:
+                raise ValueError(f"non-finite {k} gradient for triangle {i}")
+    state.t += 1
+    return state

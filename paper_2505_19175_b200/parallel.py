@@ -75,7 +75,7 @@ class B200ViewTrainer:
     """Forward + backward of each local view on the B200 rasterizer, then one
     NCCL all-reduce.  ``poses`` / ``d_images`` index the batch."""
 
-    def __init__(self, soup, intr, poses, d_images, rasterizer=None, **render_kw):
+    def __init__(self, soup, intr, poses, d_images, rasterizer=None, lrs=None, **render_kw):
         from .rasterizer import DeviceGrads, Rasterizer
         self.rast = rasterizer or Rasterizer()
         self.soup = soup
@@ -84,10 +84,21 @@ class B200ViewTrainer:
         self.d_images = d_images
         self.kw = render_kw
         self.grads = DeviceGrads.zeros(len(soup))
+        # optional fused Adam after the all-reduce (training.py:165-168): every
+        # rank applies the same update to its replica of the parameters
+        self.lrs = lrs
+        self.adam = None
+        if lrs is not None:
+            from .optim import DeviceAdamState
+            self.adam = DeviceAdamState.zeros(len(soup))
 
     def _grad(self, v: int, flat: torch.Tensor, accumulate: bool):
         self.rast.forward(self.soup, self.intr, self.poses[v], keep_backward=True, **self.kw)
         self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate)
 
     def step(self) -> StepResult:
-        return train_step(self._grad, len(self.poses), self.grads.flat)
+        res = train_step(self._grad, len(self.poses), self.grads.flat)
+        if self.adam is not None:
+            from .optim import adam_step
+            adam_step(self.soup, self.grads, self.adam, self.lrs, rasterizer=self.rast)
+        return res
