@@ -175,6 +175,19 @@ int ts_photometric_loss(ts_context* ctx, const float* rendered, const float* tar
 /* Mean SSIM over channels (losses.py:110-119) into out[1] (device double[2]). */
 int ts_ssim(ts_context* ctx, const float* x, const float* y, int height, int width, double* out, void* stream);
 
+/* Distortion loss (losses.py:169-203) over fragment lists in the CSR layout of
+ * ts_fragment_offsets / ts_collect_fragments (device arrays; n_pixels + 1
+ * offsets, fp64 weight / depth): out (device double[1]) = value averaged over
+ * image_size pixels (n_pixels if <= 0); d_weight / d_depth (nullable, device
+ * double[F]).  Sorted runs use the prefix-sum form, unsorted ones the pairwise
+ * form. */
+int ts_distortion_loss(ts_context* ctx, const int64_t* offsets, const double* weight, const double* depth,
+                       int64_t n_pixels, int64_t image_size, double* out, double* d_weight, double* d_depth,
+                       void* stream);
+/* depth_from_fragments (losses.py:206-216): device double[n_pixels]. */
+int ts_fragment_depth(ts_context* ctx, const int64_t* offsets, const double* weight, const double* depth,
+                      int64_t n_pixels, double* out_depth, void* stream);
+
 /* Adam step (training.py:81-110) in place on fp32 device parameters
  * (vertices (N,3,3), opacity (N), sigma (N), sh (N,16,3)) with the gradients
  * of ts_backward; m, v: device fp32 moments of 59 N elements in the flat

@@ -9,6 +9,9 @@ Follows trisplat/losses.py:
   _ssim_channel           :76-107  per-window SSIM map, its partials, d(mean)/dx
   ssim                    :110-119 mean over channels, 1.0 below the window size
   photometric_loss        :122-142 (1-lam) L1 + lam (1-SSIM)/2 and its gradient
+  distortion_loss         :153-203 pairwise w_i w_j |z_i - z_j| per pixel (prefix
+                          sums for depth-sorted runs, pairwise otherwise)
+  depth_from_fragments    :206-216 weight-normalised depth per pixel
 in plain numpy, fp64.  Pinned to the live reference by tests/golden/loss.npz
 (tests/golden/make_loss_golden.py).
 """
@@ -105,3 +108,50 @@ def photometric_loss(rendered, target, lam: float):
             g_s[..., c] = dx / r.shape[2]
         sv = float(np.mean(vals))
     return (1.0 - lam) * l1 + lam * (1.0 - sv) / 2.0, (1.0 - lam) * g_l1 - (lam / 2.0) * g_s
+
+
+def distortion_loss(off, w, z, image_size=None):
+    off = np.asarray(off, dtype=np.int64)
+    w = np.asarray(w, dtype=np.float64)
+    z = np.asarray(z, dtype=np.float64)
+    npix = len(off) - 1
+    scale = 1.0 / max(image_size if image_size is not None else npix, 1)
+    if len(w) == 0:
+        return 0.0, np.zeros(0), np.zeros(0)
+    d_w, d_z = np.zeros_like(w), np.zeros_like(w)
+    total = 0.0
+    counts = np.diff(off)
+    seg = np.repeat(np.arange(npix), counts)
+    same = seg[1:] == seg[:-1]
+    if (z[1:][same] >= z[:-1][same]).all():
+        for p in range(npix):
+            lo, hi = off[p], off[p + 1]
+            ws, zs = w[lo:hi], z[lo:hi]
+            wb = np.concatenate([[0.0], np.cumsum(ws)[:-1]]) if hi > lo else ws
+            sb = np.concatenate([[0.0], np.cumsum(ws * zs)[:-1]]) if hi > lo else ws
+            wa, sa = ws.sum() - wb - ws, (ws * zs).sum() - sb - ws * zs
+            fwd = zs * wb - sb
+            total += 2.0 * float((ws * fwd).sum())
+            d_w[lo:hi] = 2.0 * (fwd + (sa - zs * wa))
+            d_z[lo:hi] = 2.0 * ws * (wb - wa)
+    else:
+        for p in range(npix):
+            lo, hi = off[p], off[p + 1]
+            if hi - lo < 2:
+                continue
+            ws, zs = w[lo:hi], z[lo:hi]
+            dz = np.abs(zs[:, None] - zs[None, :])
+            total += float(ws @ dz @ ws)
+            d_w[lo:hi] = 2.0 * dz @ ws
+            d_z[lo:hi] = 2.0 * (np.sign(zs[:, None] - zs[None, :]) * ws[None, :]).sum(axis=1) * ws
+    return total * scale, d_w * scale, d_z * scale
+
+
+def depth_from_fragments(off, w, z, height, width):
+    off = np.asarray(off, dtype=np.int64)
+    d = np.zeros(height * width)
+    ws = np.zeros(height * width)
+    idx = np.repeat(np.arange(height * width), np.diff(off))
+    np.add.at(d, idx, np.asarray(w) * np.asarray(z))
+    np.add.at(ws, idx, np.asarray(w))
+    return (d / np.maximum(ws, 1e-8)).reshape(height, width)

@@ -67,7 +67,7 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
            "ts_stage_times", "ts_flagged_pixels", "ts_fragment_offsets", "ts_collect_fragments",
            "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_photometric_loss",
-           "ts_ssim", "ts_adam_step"]
+           "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -123,6 +123,11 @@ def load(path: str = LIB_PATH):
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                  P(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p]
     lib.ts_adam_step.restype = ctypes.c_int
+    lib.ts_distortion_loss.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + \
+        [ctypes.c_void_p] * 4
+    lib.ts_distortion_loss.restype = ctypes.c_int
+    lib.ts_fragment_depth.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.ts_fragment_depth.restype = ctypes.c_int
     lib.ts_launch_count.argtypes = [ctypes.c_void_p]
     lib.ts_launch_count.restype = ctypes.c_int64
     lib.ts_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]

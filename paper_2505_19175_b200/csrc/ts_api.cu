@@ -762,6 +762,27 @@ int ts_photometric_loss(ts_context* c, const float* rendered, const float* targe
     return cuda_err(cudaGetLastError());
 }
 
+int ts_distortion_loss(ts_context* c, const int64_t* offsets, const double* weight, const double* depth,
+                       int64_t n_pixels, int64_t image_size, double* out, double* d_weight, double* d_depth,
+                       void* stream) {
+    if (!c || !offsets || !out || n_pixels < 0) return TS_ERR_INVALID_ARG;
+    int rc;
+    if ((rc = ensure(c->lossbuf, distortion_scratch_bytes(n_pixels)))) return rc;
+    launch_distortion_loss(n_pixels, (const long long*)offsets, weight, depth,
+                           image_size > 0 ? image_size : n_pixels, out, d_weight, d_depth, c->lossbuf.p,
+                           (cudaStream_t)stream);
+    g_launches += n_pixels > 0 ? 2 : 1;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_fragment_depth(ts_context* c, const int64_t* offsets, const double* weight, const double* depth,
+                      int64_t n_pixels, double* out_depth, void* stream) {
+    if (!c || !offsets || !out_depth || n_pixels < 0) return TS_ERR_INVALID_ARG;
+    launch_fragment_depth(n_pixels, (const long long*)offsets, weight, depth, out_depth, (cudaStream_t)stream);
+    g_launches += n_pixels > 0 ? 1 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
 int ts_adam_step(ts_context* c, float* vertices, float* opacity, float* sigma, float* sh, int64_t n,
                  const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
                  void* stream) {

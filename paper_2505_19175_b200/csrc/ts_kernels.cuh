@@ -184,6 +184,13 @@ int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned*
 void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
                       long long t, const double lrs[4], long long* bad, cudaStream_t st);
 
+// ts_loss.cu: distortion loss over fragment CSR lists, fragment depth map
+size_t distortion_scratch_bytes(long long npix);
+void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,
+                            long long image_size, double* out, double* d_w, double* d_z, void* scratch,
+                            cudaStream_t st);
+void launch_fragment_depth(long long npix, const long long* off, const double* w, const double* z, double* depth,
+                           cudaStream_t st);
 // ts_loss.cu: photometric loss (L1 + D-SSIM) and gradient
 size_t photometric_scratch_bytes(int H, int W);
 void launch_photometric_loss(const float* x, const float* y, int H, int W, double lam, double* out, float* d_image,

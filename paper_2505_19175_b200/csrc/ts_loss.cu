@@ -274,4 +274,103 @@ void launch_photometric_loss(const float* x, const float* y, int H, int W, doubl
     k_loss_final<<<1, 256, 0, st>>>(H, W, with_ssim ? 1 : 0, ssim_only ? 1.0 : lam, pl1, nl, pss, nss, out);
 }
 
+// ---------------------------------------------------------------------------
+// Distortion loss (losses.py:153-203): per pixel, sum over ordered fragment
+// pairs of w_i w_j |z_i - z_j|, averaged over image_size pixels, with its
+// gradients w.r.t. every fragment's weight and depth.  Thread per pixel over
+// its CSR fragment run: the reference's O(F) prefix-sum form when the run is
+// sorted by depth (the compositing order), the pairwise form otherwise.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_distortion(long long npix, const long long* __restrict__ off,
+                                                    const double* __restrict__ w, const double* __restrict__ z,
+                                                    double scale, double* __restrict__ d_w,
+                                                    double* __restrict__ d_z, double* __restrict__ part) {
+    __shared__ double s_red[8];
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double tot = 0.0;
+    if (p < npix) {
+        const long long lo = off[p], hi = off[p + 1];
+        bool sorted = true;
+        double tw = 0.0, ts = 0.0;
+        for (long long k = lo; k < hi; k++) {
+            tw += w[k];
+            ts += w[k] * z[k];
+            if (k > lo && z[k] < z[k - 1]) sorted = false;
+        }
+        if (hi - lo < 2) {
+            for (long long k = lo; k < hi; k++) {
+                if (d_w) d_w[k] = 0.0;
+                if (d_z) d_z[k] = 0.0;
+            }
+        } else if (sorted) {
+            double wb = 0.0, sb = 0.0;  // weight / weighted depth in front
+            for (long long k = lo; k < hi; k++) {
+                const double wk = w[k], zk = z[k];
+                const double wa = tw - wb - wk, sa = ts - sb - wk * zk;
+                const double fwd = zk * wb - sb;
+                tot += wk * fwd;
+                if (d_w) d_w[k] = 2.0 * (fwd + (sa - zk * wa)) * scale;
+                if (d_z) d_z[k] = 2.0 * wk * (wb - wa) * scale;
+                wb += wk;
+                sb += wk * zk;
+            }
+            tot *= 2.0;
+        } else {  // pairwise (_distortion_pairwise :153-166)
+            for (long long i = lo; i < hi; i++) {
+                double gw_ = 0.0, gz = 0.0;
+                for (long long j = lo; j < hi; j++) {
+                    const double dz = z[i] - z[j];
+                    tot += w[i] * fabs(dz) * w[j];
+                    gw_ += fabs(dz) * w[j];
+                    gz += (double)((dz > 0.0) - (dz < 0.0)) * w[j];
+                }
+                if (d_w) d_w[i] = 2.0 * gw_ * scale;
+                if (d_z) d_z[i] = 2.0 * gz * w[i] * scale;
+            }
+        }
+    }
+    const double t = block_sum_256(tot, s_red);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void __launch_bounds__(256) k_sum_scaled(const double* __restrict__ part, int n, double scale,
+                                                    double* __restrict__ out) {
+    __shared__ double s_red[8];
+    double a = 0.0;
+    for (int k = threadIdx.x; k < n; k += 256) a += part[k];
+    const double t = block_sum_256(a, s_red);
+    if (threadIdx.x == 0) out[0] = t * scale;
+}
+
+// depth_from_fragments (losses.py:206-216): blend-weight-normalised depth per pixel
+__global__ void __launch_bounds__(256) k_fragment_depth(long long npix, const long long* __restrict__ off,
+                                                        const double* __restrict__ w, const double* __restrict__ z,
+                                                        double* __restrict__ depth) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npix) return;
+    double a = 0.0, b = 0.0;
+    for (long long k = off[p]; k < off[p + 1]; k++) {
+        a += w[k] * z[k];
+        b += w[k];
+    }
+    depth[p] = a / fmax(b, 1e-8);
+}
+
+size_t distortion_scratch_bytes(long long npix) { return sizeof(double) * (size_t)((npix + 255) / 256 + 1); }
+
+void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,
+                            long long image_size, double* out, double* d_w, double* d_z, void* scratch,
+                            cudaStream_t st) {
+    const double scale = 1.0 / (double)(image_size > 1 ? image_size : 1);
+    const int nb = (int)((npix + 255) / 256);
+    double* part = (double*)scratch;
+    if (nb > 0) k_distortion<<<nb, 256, 0, st>>>(npix, off, w, z, scale, d_w, d_z, part);
+    k_sum_scaled<<<1, 256, 0, st>>>(part, nb, scale, out);
+}
+
+void launch_fragment_depth(long long npix, const long long* off, const double* w, const double* z, double* depth,
+                           cudaStream_t st) {
+    if (npix > 0) k_fragment_depth<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(npix, off, w, z, depth);
+}
+
 }  // namespace ts

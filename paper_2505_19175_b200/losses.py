@@ -1,5 +1,6 @@
-"""On-device photometric loss: drop-in for the reference's
-``photometric_loss`` / ``ssim`` (trisplat/losses.py:110-142).
+"""On-device losses: drop-ins for the reference's
+``photometric_loss`` / ``ssim`` (trisplat/losses.py:110-142),
+``distortion_loss`` (:169-203) and ``depth_from_fragments`` (:206-216).
 
 Same signatures, return types and errors as the reference:
   photometric_loss(rendered, target, lam) -> (loss: float, grad)
@@ -87,15 +88,77 @@ def ssim(x, y, rasterizer=None, stream=None) -> float:
     return float(out[1].item())
 
 
+def _frag_dev(fragments):
+    """(offsets int64, weight f64, depth f64) CUDA tensors and whether the input was on the device."""
+    import torch
+    off = fragments.offsets
+    if isinstance(off, torch.Tensor):
+        return (off.to(device="cuda", dtype=torch.int64).contiguous(),
+                fragments.weight.to(device="cuda", dtype=torch.float64).contiguous(),
+                fragments.depth.to(device="cuda", dtype=torch.float64).contiguous(), True)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device="cuda")  # noqa: E731
+    return (t(np.asarray(off, dtype=np.int64), torch.int64), t(np.asarray(fragments.weight, np.float64), torch.float64),
+            t(np.asarray(fragments.depth, np.float64), torch.float64), False)
+
+
+def distortion_loss(fragments, image_size: int | None = None, rasterizer=None, stream=None):
+    """Pairwise blend-weighted depth spread averaged over pixels (losses.py:169-203).
+    Returns (value, d_weight, d_depth) aligned with the fragment arrays (CUDA
+    tensors for DeviceFragments input, numpy for FragmentData)."""
+    import torch
+    from . import _lib
+    from .rasterizer import default_rasterizer
+    off, w, z, dev_in = _frag_dev(fragments)
+    npix = off.numel() - 1
+    nf = w.numel()
+    if nf == 0:
+        zero = torch.zeros(0, dtype=torch.float64, device="cuda")
+        return (0.0, zero, zero) if dev_in else (0.0, np.zeros(0), np.zeros(0))
+    r = rasterizer or default_rasterizer()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    d_w = torch.empty_like(w)
+    d_z = torch.empty_like(z)
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    rc = r.lib.ts_distortion_loss(r._ctx, ctypes.c_void_p(off.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                  ctypes.c_void_p(z.data_ptr()), npix,
+                                  int(image_size) if image_size is not None else npix,
+                                  ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(d_w.data_ptr()),
+                                  ctypes.c_void_p(d_z.data_ptr()), ctypes.c_void_p(st))
+    _lib.check(rc, "distortion_loss")
+    if dev_in:
+        return float(out.item()), d_w, d_z
+    return float(out.item()), d_w.cpu().numpy(), d_z.cpu().numpy()
+
+
+def depth_from_fragments(fragments, height: int, width: int, rasterizer=None, stream=None):
+    """Blend-weight-normalised expected depth per pixel, 0 where empty (losses.py:206-216)."""
+    import torch
+    from . import _lib
+    from .rasterizer import default_rasterizer
+    off, w, z, dev_in = _frag_dev(fragments)
+    r = rasterizer or default_rasterizer()
+    d = torch.empty(height * width, dtype=torch.float64, device="cuda")
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    rc = r.lib.ts_fragment_depth(r._ctx, ctypes.c_void_p(off.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                 ctypes.c_void_p(z.data_ptr()), height * width, ctypes.c_void_p(d.data_ptr()),
+                                 ctypes.c_void_p(st))
+    _lib.check(rc, "fragment_depth")
+    d = d.view(height, width)
+    return d if dev_in else d.cpu().numpy()
+
+
 def install(trisplat_module=None):
     """Rebind the reference's photometric_loss / ssim (imported by name in
     training.py:16-17, scene_io.py:23, __init__.py:18-19) to this path."""
     import importlib
     import sys
     patched = []
-    targets = {"trisplat": ("photometric_loss", "ssim"), "trisplat.losses": ("photometric_loss", "ssim"),
-               "trisplat.training": ("photometric_loss",), "trisplat.scene_io": ("_ssim",)}
-    repl = {"photometric_loss": photometric_loss, "ssim": ssim, "_ssim": ssim}
+    targets = {"trisplat": ("photometric_loss", "ssim", "distortion_loss"),
+               "trisplat.losses": ("photometric_loss", "ssim", "distortion_loss", "depth_from_fragments"),
+               "trisplat.training": ("photometric_loss", "distortion_loss", "depth_from_fragments"),
+               "trisplat.scene_io": ("_ssim",)}
+    repl = {"photometric_loss": photometric_loss, "ssim": ssim, "_ssim": ssim, "distortion_loss": distortion_loss,
+            "depth_from_fragments": depth_from_fragments}
     for mod_name, names in targets.items():
         try:
             mod = sys.modules.get(mod_name) or importlib.import_module(mod_name)

@@ -38,6 +38,24 @@ def main():
     loss, grad = L.photometric_loss(x, x, 0.2)
     out[f"loss{k}"], out[f"grad{k}"], out[f"ssim{k}"] = np.float64(loss), grad, np.float64(L.ssim(x, x))
     out["n"] = np.int64(k + 1)
+    # distortion loss / depth map over fragment lists (losses.py:169-216):
+    # a depth-sorted set (prefix-sum path) and a shuffled one (pairwise path)
+    R = importlib.import_module("trisplat.render")
+    h, w = 6, 7
+    counts = rng.integers(0, 9, h * w)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    nf = int(off[-1])
+    wt = rng.uniform(0, 0.5, nf)
+    z = rng.uniform(1, 5, nf)
+    zs = z.copy()
+    for p in range(h * w):
+        zs[off[p]:off[p + 1]] = np.sort(zs[off[p]:off[p + 1]])
+    for tag, zz in (("s", zs), ("u", z)):
+        fr = R.FragmentData(offsets=off, triangle=np.zeros(nf, np.int64), weight=wt, depth=zz)
+        val, dw, dz = L.distortion_loss(fr, image_size=h * w + 5)
+        out[f"dist_{tag}_z"], out[f"dist_{tag}_val"], out[f"dist_{tag}_dw"], out[f"dist_{tag}_dz"] = zz, val, dw, dz
+        out[f"depth_{tag}"] = L.depth_from_fragments(fr, h, w)
+    out["dist_off"], out["dist_w"], out["dist_hw"] = off, wt, np.array([h, w])
     np.savez_compressed(os.path.join(HERE, "loss.npz"), **out)
     print("wrote", k + 1, "cases")
 

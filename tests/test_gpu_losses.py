@@ -70,3 +70,39 @@ def test_reference_cases_and_device_tensors():
     wl, wg = OL.photometric_loss(xt.double().cpu().numpy(), yt.double().cpu().numpy(), 0.2)
     assert abs(loss - wl) <= 1e-6 * abs(wl)
     assert np.abs(g.double().cpu().numpy() - wg).max() <= 1e-5 * np.abs(wg).max()
+
+
+def test_distortion_and_depth_against_fixtures():
+    from paper_2505_19175_b200 import losses as DL
+    from paper_2505_19175_b200.types import FragmentData
+    z = np.load(GOLD)
+    h, w = (int(v) for v in z["dist_hw"])
+    for tag in "su":  # depth-sorted runs (prefix sums) and shuffled ones (pairwise)
+        fr = FragmentData(z["dist_off"], np.zeros(len(z["dist_w"]), np.int64), z["dist_w"], z[f"dist_{tag}_z"])
+        v, dw, dz = DL.distortion_loss(fr, image_size=h * w + 5)
+        assert abs(v - float(z[f"dist_{tag}_val"])) <= 1e-12 * max(1.0, abs(v))
+        assert np.abs(dw - z[f"dist_{tag}_dw"]).max() <= 1e-12
+        assert np.abs(dz - z[f"dist_{tag}_dz"]).max() <= 1e-12
+        d = DL.depth_from_fragments(fr, h, w)
+        assert np.abs(d - z[f"depth_{tag}"]).max() <= 1e-12
+
+
+def test_distortion_on_rendered_fragments():
+    # fragments of a real frame stay on the device: loss and gradients vs the oracle
+    from paper_2505_19175_b200 import losses as DL
+    from paper_2505_19175_b200 import scenes
+    from paper_2505_19175_b200.rasterizer import DeviceSoup, Rasterizer
+    soup, intr, pose = scenes.make_scene("c1")
+    r = Rasterizer()
+    r.forward(DeviceSoup.from_soup(soup, dtype=torch.float32), intr, pose, keep_backward=True)
+    fr = r.fragments()
+    v, dw, dz = DL.distortion_loss(fr, rasterizer=r)
+    assert dw.is_cuda and dw.shape == fr.weight.shape
+    wv, wdw, wdz = OL.distortion_loss(fr.offsets.cpu().numpy(), fr.weight.cpu().numpy(), fr.depth.cpu().numpy())
+    assert abs(v - wv) <= 1e-10 * max(1.0, abs(wv))
+    assert np.abs(dw.cpu().numpy() - wdw).max() <= 1e-10 * max(1.0, np.abs(wdw).max())
+    assert np.abs(dz.cpu().numpy() - wdz).max() <= 1e-10 * max(1.0, np.abs(wdz).max())
+    d = DL.depth_from_fragments(fr, intr.height, intr.width, rasterizer=r)
+    wd = OL.depth_from_fragments(fr.offsets.cpu().numpy(), fr.weight.cpu().numpy(), fr.depth.cpu().numpy(),
+                                 intr.height, intr.width)
+    assert np.abs(d.cpu().numpy() - wd).max() <= 1e-10 * max(1.0, np.abs(wd).max())

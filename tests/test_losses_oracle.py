@@ -47,3 +47,15 @@ def test_gradient_matches_finite_differences():
         xm[i, j, c] -= h
         fd = (OL.photometric_loss(xp, y, 0.2)[0] - OL.photometric_loss(xm, y, 0.2)[0]) / (2 * h)
         assert g[i, j, c] == pytest.approx(fd, rel=1e-4, abs=1e-9)
+
+
+def test_distortion_and_depth_match_reference_fixtures():
+    z = np.load(GOLD)
+    h, w = (int(v) for v in z["dist_hw"])
+    for tag in "su":
+        v, dw, dz = OL.distortion_loss(z["dist_off"], z["dist_w"], z[f"dist_{tag}_z"], image_size=h * w + 5)
+        assert abs(v - float(z[f"dist_{tag}_val"])) <= 1e-12
+        assert np.abs(dw - z[f"dist_{tag}_dw"]).max() <= 1e-12
+        assert np.abs(dz - z[f"dist_{tag}_dz"]).max() <= 1e-12
+        d = OL.depth_from_fragments(z["dist_off"], z["dist_w"], z[f"dist_{tag}_z"], h, w)
+        assert np.abs(d - z[f"depth_{tag}"]).max() <= 1e-12
