@@ -184,6 +184,15 @@ int ts_ssim(ts_context* ctx, const float* x, const float* y, int height, int wid
 int ts_distortion_loss(ts_context* ctx, const int64_t* offsets, const double* weight, const double* depth,
                        int64_t n_pixels, int64_t image_size, double* out, double* d_weight, double* d_depth,
                        void* stream);
+/* Normal loss (losses.py:219-292) of fp32 device vertices (N,3,3) against the
+ * normals of a device fp64 depth map (H x W = cam->height x cam->width) for the
+ * fragment lists (offsets of H*W+1, triangle ids int32, weights fp64, F
+ * fragments): out (device double[1]) = mean over fragments of w (1 - n.N);
+ * d_vertices (nullable, device double[N*9]); d_weight (nullable, device
+ * double[F]).  Depth normals are held fixed (as in the reference). */
+int ts_normal_loss(ts_context* ctx, const float* vertices, int64_t n, const int64_t* offsets,
+                   const int32_t* triangle, const double* weight, int64_t n_fragments, const double* depth,
+                   const ts_camera* cam, double* out, double* d_vertices, double* d_weight, void* stream);
 /* depth_from_fragments (losses.py:206-216): device double[n_pixels]. */
 int ts_fragment_depth(ts_context* ctx, const int64_t* offsets, const double* weight, const double* depth,
                       int64_t n_pixels, double* out_depth, void* stream);

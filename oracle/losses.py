@@ -12,6 +12,7 @@ Follows trisplat/losses.py:
   distortion_loss         :153-203 pairwise w_i w_j |z_i - z_j| per pixel (prefix
                           sums for depth-sorted runs, pairwise otherwise)
   depth_from_fragments    :206-216 weight-normalised depth per pixel
+  depth_normals / normal_loss :219-292 depth-map normals, triangle-normal alignment
 in plain numpy, fp64.  Pinned to the live reference by tests/golden/loss.npz
 (tests/golden/make_loss_golden.py).
 """
@@ -155,3 +156,42 @@ def depth_from_fragments(off, w, z, height, width):
     np.add.at(d, idx, np.asarray(w) * np.asarray(z))
     np.add.at(ws, idx, np.asarray(w))
     return (d / np.maximum(ws, 1e-8)).reshape(height, width)
+
+
+def depth_normals(depth, fx, fy, cx, cy):
+    h, w = depth.shape
+    ys, xs = np.mgrid[0:h, 0:w]
+    p = np.stack([depth * (xs + 0.5 - cx) / fx, depth * (ys + 0.5 - cy) / fy, depth], axis=-1)
+    q = np.pad(p, ((1, 1), (1, 1), (0, 0)), mode="edge")
+    gx = (q[1:-1, 2:] - q[1:-1, :-2]) / 2.0
+    gy = (q[2:, 1:-1] - q[:-2, 1:-1]) / 2.0
+    n = np.cross(gx, gy)
+    n = n / np.maximum(np.linalg.norm(n, axis=-1, keepdims=True), 1e-12)
+    n[n[..., 2] > 0] *= -1.0
+    return n
+
+
+def normal_loss(vertices, off, tri, wgt, depth, fx, fy, cx, cy, rot, trans):
+    v = np.asarray(vertices, dtype=np.float64)
+    n_tri, nf = len(v), len(wgt)
+    if nf == 0:
+        return 0.0, np.zeros((n_tri, 3, 3)), np.zeros(0)
+    h, w = depth.shape
+    mw = depth_normals(depth, fx, fy, cx, cy).reshape(-1, 3)[np.repeat(np.arange(h * w), np.diff(off))] @ rot
+    a, b = v[:, 1] - v[:, 0], v[:, 2] - v[:, 0]
+    c = np.cross(a, b)
+    cn = np.maximum(np.linalg.norm(c, axis=1), 1e-12)
+    ch = c / cn[:, None]
+    facing = ((ch @ rot.T) * (v.mean(axis=1) @ rot.T + trans)).sum(axis=1)
+    fl = np.where(facing > 0, -1.0, 1.0)
+    tri = np.asarray(tri, dtype=np.int64)
+    cm = (ch[tri] * mw).sum(axis=1)
+    dot = cm * fl[tri]
+    value = float((wgt * (1.0 - dot)).sum() / nf)
+    d_w = (1.0 - dot) / nf
+    g = np.zeros((n_tri, 3))
+    np.add.at(g, tri, (-wgt * fl[tri] / nf)[:, None] * (mw - ch[tri] * cm[:, None]) / cn[tri, None])
+    da, db = np.cross(b, g), np.cross(g, a)
+    dv = np.zeros((n_tri, 3, 3))
+    dv[:, 1], dv[:, 2], dv[:, 0] = da, db, -(da + db)
+    return value, dv, d_w

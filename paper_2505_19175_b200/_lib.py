@@ -67,7 +67,8 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
            "ts_stage_times", "ts_flagged_pixels", "ts_fragment_offsets", "ts_collect_fragments",
            "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_photometric_loss",
-           "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth"]
+           "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
+           "ts_normal_loss"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -128,6 +129,10 @@ def load(path: str = LIB_PATH):
     lib.ts_distortion_loss.restype = ctypes.c_int
     lib.ts_fragment_depth.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
     lib.ts_fragment_depth.restype = ctypes.c_int
+    lib.ts_normal_loss.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, P(TsCamera),
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.ts_normal_loss.restype = ctypes.c_int
     lib.ts_launch_count.argtypes = [ctypes.c_void_p]
     lib.ts_launch_count.restype = ctypes.c_int64
     lib.ts_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]

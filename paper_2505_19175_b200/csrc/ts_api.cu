@@ -775,6 +775,23 @@ int ts_distortion_loss(ts_context* c, const int64_t* offsets, const double* weig
     return cuda_err(cudaGetLastError());
 }
 
+int ts_normal_loss(ts_context* c, const float* vertices, int64_t n, const int64_t* offsets,
+                   const int32_t* triangle, const double* weight, int64_t n_fragments, const double* depth,
+                   const ts_camera* cam, double* out, double* d_vertices, double* d_weight, void* stream) {
+    if (!c || !cam || !out || n < 0 || n_fragments < 0 || !offsets || !depth) return TS_ERR_INVALID_ARG;
+    if ((n > 0 && !vertices) || (n_fragments > 0 && (!triangle || !weight))) return TS_ERR_INVALID_ARG;
+    const long long npix = (long long)cam->width * cam->height;
+    int rc;
+    if ((rc = ensure(c->lossbuf, normal_scratch_bytes(n, npix)))) return rc;
+    double cm[16] = {cam->fx, cam->fy, cam->cx, cam->cy};
+    for (int k = 0; k < 9; k++) cm[4 + k] = cam->R[k];
+    for (int k = 0; k < 3; k++) cm[13 + k] = cam->t[k];
+    launch_normal_loss(vertices, n, (const long long*)offsets, triangle, weight, n_fragments, depth, cam->height,
+                       cam->width, cm, out, d_vertices, d_weight, c->lossbuf.p, (cudaStream_t)stream);
+    g_launches += 5;
+    return cuda_err(cudaGetLastError());
+}
+
 int ts_fragment_depth(ts_context* c, const int64_t* offsets, const double* weight, const double* depth,
                       int64_t n_pixels, double* out_depth, void* stream) {
     if (!c || !offsets || !out_depth || n_pixels < 0) return TS_ERR_INVALID_ARG;

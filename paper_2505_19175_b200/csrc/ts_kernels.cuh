@@ -189,6 +189,11 @@ size_t distortion_scratch_bytes(long long npix);
 void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,
                             long long image_size, double* out, double* d_w, double* d_z, void* scratch,
                             cudaStream_t st);
+// normal loss (cam: fx, fy, cx, cy, R[9] row-major, t[3])
+size_t normal_scratch_bytes(long long n, long long npix);
+void launch_normal_loss(const float* v, long long n, const long long* off, const int* ftri, const double* w,
+                        long long nfrag, const double* depth, int H, int W, const double cam[16], double* out,
+                        double* d_vertices, double* d_w, void* scratch, cudaStream_t st);
 void launch_fragment_depth(long long npix, const long long* off, const double* w, const double* z, double* depth,
                            cudaStream_t st);
 // ts_loss.cu: photometric loss (L1 + D-SSIM) and gradient

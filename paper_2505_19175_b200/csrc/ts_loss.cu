@@ -356,6 +356,154 @@ __global__ void __launch_bounds__(256) k_fragment_depth(long long npix, const lo
     depth[p] = a / fmax(b, 1e-8);
 }
 
+// ---------------------------------------------------------------------------
+// Normal loss (losses.py:219-292): blend-weighted misalignment of the
+// camera-facing triangle normals with the normals of the depth map.
+//   k_depth_normals -- per pixel: backprojected points, central differences
+//                      with border replication, unit normal facing the camera,
+//                      rotated into the world frame (n @ R);
+//   k_tri_normals   -- per triangle: c = (v1-v0) x (v2-v0), |c| (floored), the
+//                      unit normal and its camera-facing sign;
+//   k_normal_frag   -- thread per pixel over its fragments: w (1 - n.N), the
+//                      weight gradient, and dL/dc per triangle (fp64 atomics);
+//   k_normal_chain  -- per triangle: the cross-product chain into d_vertices.
+// ---------------------------------------------------------------------------
+struct NCam {
+    double fx, fy, cx, cy, R[9], t[3];
+};
+
+__global__ void __launch_bounds__(256) k_depth_normals(const double* __restrict__ depth, int H, int W, NCam cm,
+                                                       double* __restrict__ nmap) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= H * W) return;
+    const int y = p / W, x = p % W;
+    auto pt = [&](int yy, int xx, double* o) {  // edge-replicated backprojection
+        yy = min(max(yy, 0), H - 1);
+        xx = min(max(xx, 0), W - 1);
+        const double d = depth[(size_t)yy * W + xx];
+        o[0] = d * ((xx + 0.5 - cm.cx) / cm.fx);
+        o[1] = d * ((yy + 0.5 - cm.cy) / cm.fy);
+        o[2] = d;
+    };
+    double xp[3], xm[3], yp[3], ym[3];
+    pt(y, x + 1, xp);
+    pt(y, x - 1, xm);
+    pt(y + 1, x, yp);
+    pt(y - 1, x, ym);
+    double dx[3], dy[3];
+    for (int k = 0; k < 3; k++) {
+        dx[k] = (xp[k] - xm[k]) / 2.0;
+        dy[k] = (yp[k] - ym[k]) / 2.0;
+    }
+    double n[3] = {dx[1] * dy[2] - dx[2] * dy[1], dx[2] * dy[0] - dx[0] * dy[2], dx[0] * dy[1] - dx[1] * dy[0]};
+    const double nn = fmax(sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]), 1e-12);
+    for (int k = 0; k < 3; k++) n[k] /= nn;
+    if (n[2] > 0.0)
+        for (int k = 0; k < 3; k++) n[k] = -n[k];
+    // world frame: m = n @ R  (m_j = sum_i n_i R[i][j])
+    for (int j = 0; j < 3; j++)
+        nmap[(size_t)p * 3 + j] = n[0] * cm.R[0 * 3 + j] + n[1] * cm.R[1 * 3 + j] + n[2] * cm.R[2 * 3 + j];
+}
+
+// tri[8 per triangle]: chat xyz, |c|, flip, pad
+__global__ void __launch_bounds__(256) k_tri_normals(const float* __restrict__ v, long long n, NCam cm,
+                                                     double* __restrict__ tri, double* __restrict__ gc) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[9];
+    for (int k = 0; k < 9; k++) p[k] = (double)v[i * 9 + k];
+    const double a[3] = {p[3] - p[0], p[4] - p[1], p[5] - p[2]};
+    const double b[3] = {p[6] - p[0], p[7] - p[1], p[8] - p[2]};
+    const double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    const double cn = fmax(sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]), 1e-12);
+    const double ch[3] = {c[0] / cn, c[1] / cn, c[2] / cn};
+    // camera-facing orientation: centroid_cam = mean(v) @ R^T + t, n_cam = chat @ R^T
+    double facing = 0.0;
+    for (int r = 0; r < 3; r++) {
+        const double cc = ((p[0] + p[3] + p[6]) / 3.0) * cm.R[r * 3 + 0] + ((p[1] + p[4] + p[7]) / 3.0) * cm.R[r * 3 + 1] +
+                          ((p[2] + p[5] + p[8]) / 3.0) * cm.R[r * 3 + 2] + cm.t[r];
+        const double nc = ch[0] * cm.R[r * 3 + 0] + ch[1] * cm.R[r * 3 + 1] + ch[2] * cm.R[r * 3 + 2];
+        facing += nc * cc;
+    }
+    double* o = tri + i * 8;
+    o[0] = ch[0]; o[1] = ch[1]; o[2] = ch[2]; o[3] = cn; o[4] = facing > 0.0 ? -1.0 : 1.0;
+    gc[i * 3 + 0] = gc[i * 3 + 1] = gc[i * 3 + 2] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_normal_frag(long long npix, const long long* __restrict__ off,
+                                                     const int* __restrict__ ftri, const double* __restrict__ w,
+                                                     const double* __restrict__ nmap, const double* __restrict__ tri,
+                                                     double inv_nf, double* __restrict__ d_w, double* __restrict__ gc,
+                                                     double* __restrict__ part) {
+    __shared__ double s_red[8];
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double sum = 0.0;
+    if (p < npix) {
+        const double m0 = nmap[p * 3 + 0], m1 = nmap[p * 3 + 1], m2 = nmap[p * 3 + 2];
+        for (long long k = off[p]; k < off[p + 1]; k++) {
+            const long long t = ftri[k];
+            const double* o = tri + t * 8;
+            const double c0 = o[0], c1 = o[1], c2 = o[2], cn = o[3], fl = o[4];
+            const double cm = c0 * m0 + c1 * m1 + c2 * m2;
+            const double dot = cm * fl;
+            sum += w[k] * (1.0 - dot);
+            if (d_w) d_w[k] = (1.0 - dot) * inv_nf;
+            const double coef = -w[k] * fl * inv_nf / cn;
+            atomicAdd(gc + t * 3 + 0, coef * (m0 - c0 * cm));
+            atomicAdd(gc + t * 3 + 1, coef * (m1 - c1 * cm));
+            atomicAdd(gc + t * 3 + 2, coef * (m2 - c2 * cm));
+        }
+    }
+    const double s = block_sum_256(sum, s_red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) k_normal_chain(const float* __restrict__ v, long long n,
+                                                      const double* __restrict__ gc, double* __restrict__ dv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double p[9];
+    for (int k = 0; k < 9; k++) p[k] = (double)v[i * 9 + k];
+    const double a[3] = {p[3] - p[0], p[4] - p[1], p[5] - p[2]};
+    const double b[3] = {p[6] - p[0], p[7] - p[1], p[8] - p[2]};
+    const double g[3] = {gc[i * 3], gc[i * 3 + 1], gc[i * 3 + 2]};
+    const double da[3] = {b[1] * g[2] - b[2] * g[1], b[2] * g[0] - b[0] * g[2], b[0] * g[1] - b[1] * g[0]};
+    const double db[3] = {g[1] * a[2] - g[2] * a[1], g[2] * a[0] - g[0] * a[2], g[0] * a[1] - g[1] * a[0]};
+    double* o = dv + i * 9;
+    for (int k = 0; k < 3; k++) {
+        o[3 + k] = da[k];
+        o[6 + k] = db[k];
+        o[k] = -(da[k] + db[k]);
+    }
+}
+
+size_t normal_scratch_bytes(long long n, long long npix) {
+    return sizeof(double) * (size_t)(8 * n + 3 * n + 3 * npix + (npix + 255) / 256 + 8);
+}
+
+void launch_normal_loss(const float* v, long long n, const long long* off, const int* ftri, const double* w,
+                        long long nfrag, const double* depth, int H, int W, const double cam[16], double* out,
+                        double* d_vertices, double* d_w, void* scratch, cudaStream_t st) {
+    NCam cm;
+    cm.fx = cam[0]; cm.fy = cam[1]; cm.cx = cam[2]; cm.cy = cam[3];
+    for (int k = 0; k < 9; k++) cm.R[k] = cam[4 + k];
+    for (int k = 0; k < 3; k++) cm.t[k] = cam[13 + k];
+    const long long npix = (long long)H * W;
+    double* tri = (double*)scratch;
+    double* gc = tri + 8 * n;
+    double* nmap = gc + 3 * n;
+    double* part = nmap + 3 * npix;
+    const int nb = (int)((npix + 255) / 256);
+    if (n > 0) k_tri_normals<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, cm, tri, gc);
+    if (npix > 0) {
+        k_depth_normals<<<nb, 256, 0, st>>>(depth, H, W, cm, nmap);
+        k_normal_frag<<<nb, 256, 0, st>>>(npix, off, ftri, w, nmap, tri, nfrag > 0 ? 1.0 / (double)nfrag : 0.0, d_w,
+                                          gc, part);
+    }
+    k_sum_scaled<<<1, 256, 0, st>>>(part, npix > 0 ? nb : 0, nfrag > 0 ? 1.0 / (double)nfrag : 0.0, out);
+    if (n > 0 && d_vertices) k_normal_chain<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, gc, d_vertices);
+}
+
 size_t distortion_scratch_bytes(long long npix) { return sizeof(double) * (size_t)((npix + 255) / 256 + 1); }
 
 void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,

@@ -1,6 +1,7 @@
 """On-device losses: drop-ins for the reference's
 ``photometric_loss`` / ``ssim`` (trisplat/losses.py:110-142),
-``distortion_loss`` (:169-203) and ``depth_from_fragments`` (:206-216).
+``distortion_loss`` (:169-203), ``depth_from_fragments`` (:206-216) and
+``normal_loss`` (:219-292).
 
 Same signatures, return types and errors as the reference:
   photometric_loss(rendered, target, lam) -> (loss: float, grad)
@@ -147,18 +148,61 @@ def depth_from_fragments(fragments, height: int, width: int, rasterizer=None, st
     return d if dev_in else d.cpu().numpy()
 
 
+def normal_loss(triangles, fragments, depth, intr, pose, rasterizer=None, stream=None):
+    """Blend-weighted misalignment of the camera-facing triangle normals with
+    the depth-map normals (losses.py:219-292, depth normals held fixed).
+    Returns (value, d_vertices (N,3,3) fp64, d_weight (F,) fp64): CUDA tensors
+    for device inputs (DeviceSoup / DeviceFragments), numpy otherwise."""
+    import torch
+    from . import _lib
+    from .rasterizer import default_rasterizer, make_camera
+    from .types import as_soup
+    dev_in = isinstance(getattr(triangles, "vertices", None), torch.Tensor)
+    if dev_in:
+        v = triangles.vertices.to(device="cuda", dtype=torch.float32).contiguous()
+    else:
+        v = torch.as_tensor(np.asarray(as_soup(triangles).vertices, dtype=np.float32), device="cuda").contiguous()
+    n = v.shape[0]
+    off, w, _, _ = _frag_dev(fragments)
+    tri = fragments.triangle
+    tri = (tri if isinstance(tri, torch.Tensor) else torch.as_tensor(np.asarray(tri))).to(
+        device="cuda", dtype=torch.int32).contiguous()
+    d = depth if isinstance(depth, torch.Tensor) else torch.as_tensor(np.asarray(depth, dtype=np.float64))
+    d = d.to(device="cuda", dtype=torch.float64).contiguous()
+    nf = w.numel()
+    if nf == 0:
+        z = torch.zeros((n, 3, 3), dtype=torch.float64, device="cuda")
+        e = torch.zeros(0, dtype=torch.float64, device="cuda")
+        return (0.0, z, e) if dev_in else (0.0, z.cpu().numpy(), e.cpu().numpy())
+    r = rasterizer or default_rasterizer()
+    cam = make_camera(intr, pose)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    dv = torch.empty((n, 3, 3), dtype=torch.float64, device="cuda")
+    dw = torch.empty(nf, dtype=torch.float64, device="cuda")
+    st = (stream or torch.cuda.current_stream()).cuda_stream
+    rc = r.lib.ts_normal_loss(r._ctx, ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(off.data_ptr()),
+                              ctypes.c_void_p(tri.data_ptr()), ctypes.c_void_p(w.data_ptr()), nf,
+                              ctypes.c_void_p(d.data_ptr()), ctypes.byref(cam), ctypes.c_void_p(out.data_ptr()),
+                              ctypes.c_void_p(dv.data_ptr()), ctypes.c_void_p(dw.data_ptr()), ctypes.c_void_p(st))
+    _lib.check(rc, "normal_loss")
+    if dev_in:
+        return float(out.item()), dv, dw
+    return float(out.item()), dv.cpu().numpy(), dw.cpu().numpy()
+
+
 def install(trisplat_module=None):
     """Rebind the reference's photometric_loss / ssim (imported by name in
     training.py:16-17, scene_io.py:23, __init__.py:18-19) to this path."""
     import importlib
     import sys
     patched = []
-    targets = {"trisplat": ("photometric_loss", "ssim", "distortion_loss"),
-               "trisplat.losses": ("photometric_loss", "ssim", "distortion_loss", "depth_from_fragments"),
-               "trisplat.training": ("photometric_loss", "distortion_loss", "depth_from_fragments"),
+    targets = {"trisplat": ("photometric_loss", "ssim", "distortion_loss", "normal_loss"),
+               "trisplat.losses": ("photometric_loss", "ssim", "distortion_loss", "depth_from_fragments",
+                                   "normal_loss"),
+               "trisplat.training": ("photometric_loss", "distortion_loss", "depth_from_fragments", "normal_loss"),
                "trisplat.scene_io": ("_ssim",)}
     repl = {"photometric_loss": photometric_loss, "ssim": ssim, "_ssim": ssim, "distortion_loss": distortion_loss,
-            "depth_from_fragments": depth_from_fragments}
+            "depth_from_fragments": depth_from_fragments, "normal_loss": normal_loss}
     for mod_name, names in targets.items():
         try:
             mod = sys.modules.get(mod_name) or importlib.import_module(mod_name)

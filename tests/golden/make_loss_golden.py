@@ -56,6 +56,25 @@ def main():
         out[f"dist_{tag}_z"], out[f"dist_{tag}_val"], out[f"dist_{tag}_dw"], out[f"dist_{tag}_dz"] = zz, val, dw, dz
         out[f"depth_{tag}"] = L.depth_from_fragments(fr, h, w)
     out["dist_off"], out["dist_w"], out["dist_hw"] = off, wt, np.array([h, w])
+    # normal loss (losses.py:219-292): fp32-representable triangles seen by a
+    # rotated camera, a smooth depth map and random fragment triangle ids
+    G = importlib.import_module("trisplat.geometry")
+    S = importlib.import_module("trisplat.soup")
+    n_tri = 30
+    r32 = lambda a: np.asarray(a, dtype=np.float32).astype(np.float64)  # noqa: E731
+    verts = r32(rng.normal(0, 1, (n_tri, 1, 3)) + 0.3 * rng.normal(0, 1, (n_tri, 3, 3)))
+    soup = S.TriangleSoup(verts, np.full(n_tri, 0.5), np.ones(n_tri), np.zeros((n_tri, 16, 3)))
+    ang = 0.3
+    rot = np.array([[np.cos(ang), 0, np.sin(ang)], [0, 1, 0], [-np.sin(ang), 0, np.cos(ang)]])
+    pose = G.CameraPose(rotation=rot, translation=np.array([0.1, -0.2, 5.0]))
+    intr = G.CameraIntrinsics(fx=9.0, fy=8.0, cx=3.4, cy=3.1, width=w, height=h)
+    ys, xs = np.mgrid[0:h, 0:w]
+    depth = 4.0 + 0.3 * np.sin(0.7 * xs) + 0.2 * np.cos(0.5 * ys) + 0.05 * rng.normal(0, 1, (h, w))
+    ftri = rng.integers(0, n_tri, nf)
+    fr = R.FragmentData(offsets=off, triangle=ftri, weight=wt, depth=z)
+    val, dv, dw = L.normal_loss(soup, fr, depth, intr, pose)
+    out.update(nl_verts=verts, nl_rot=rot, nl_trans=pose.translation, nl_intr=np.array([9.0, 8.0, 3.4, 3.1]),
+               nl_depth=depth, nl_tri=ftri, nl_val=np.float64(val), nl_dv=dv, nl_dw=dw)
     np.savez_compressed(os.path.join(HERE, "loss.npz"), **out)
     print("wrote", k + 1, "cases")
 

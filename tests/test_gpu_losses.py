@@ -106,3 +106,38 @@ def test_distortion_on_rendered_fragments():
     wd = OL.depth_from_fragments(fr.offsets.cpu().numpy(), fr.weight.cpu().numpy(), fr.depth.cpu().numpy(),
                                  intr.height, intr.width)
     assert np.abs(d.cpu().numpy() - wd).max() <= 1e-10 * max(1.0, np.abs(wd).max())
+
+
+def test_normal_loss_against_fixture_and_rendered_fragments():
+    from paper_2505_19175_b200 import losses as DL
+    from paper_2505_19175_b200 import scenes
+    from paper_2505_19175_b200.rasterizer import DeviceSoup, Rasterizer
+    from paper_2505_19175_b200.types import CameraIntrinsics, CameraPose, FragmentData, TriangleSoup
+    z = np.load(GOLD)
+    h, w = (int(v) for v in z["dist_hw"])
+    fx, fy, cx, cy = (float(a) for a in z["nl_intr"])
+    n = len(z["nl_verts"])
+    soup = TriangleSoup(z["nl_verts"], np.full(n, 0.5), np.ones(n), np.zeros((n, 16, 3)))
+    intr = CameraIntrinsics(fx=fx, fy=fy, cx=cx, cy=cy, width=w, height=h)
+    pose = CameraPose(rotation=z["nl_rot"], translation=z["nl_trans"])
+    fr = FragmentData(z["dist_off"], z["nl_tri"], z["dist_w"], z["dist_u_z"])
+    v, dv, dw = DL.normal_loss(soup, fr, z["nl_depth"], intr, pose)
+    assert abs(v - float(z["nl_val"])) <= 1e-12
+    assert np.abs(dv - z["nl_dv"]).max() <= 1e-12 * max(1.0, np.abs(z["nl_dv"]).max()) + 1e-15
+    assert np.abs(dw - z["nl_dw"]).max() <= 1e-12
+    # on a rendered frame, everything on the device
+    s2, intr2, pose2 = scenes.make_scene("c1")
+    r = Rasterizer()
+    ds = DeviceSoup.from_soup(s2, dtype=torch.float32)
+    r.forward(ds, intr2, pose2, keep_backward=True)
+    frs = r.fragments()
+    depth = DL.depth_from_fragments(frs, intr2.height, intr2.width, rasterizer=r)
+    v, dv, dw = DL.normal_loss(ds, frs, depth, intr2, pose2, rasterizer=r)
+    assert dv.is_cuda and dw.shape == frs.weight.shape
+    wv, wdv, wdw = OL.normal_loss(ds.vertices.double().cpu().numpy(), frs.offsets.cpu().numpy(),
+                                  frs.triangle.cpu().numpy(), frs.weight.cpu().numpy(), depth.cpu().numpy(),
+                                  intr2.fx, intr2.fy, intr2.cx, intr2.cy, np.asarray(pose2.rotation),
+                                  np.asarray(pose2.translation))
+    assert abs(v - wv) <= 1e-10 * max(1.0, abs(wv))
+    assert np.abs(dv.cpu().numpy() - wdv).max() <= 1e-9 * max(1e-6, np.abs(wdv).max())
+    assert np.abs(dw.cpu().numpy() - wdw).max() <= 1e-10

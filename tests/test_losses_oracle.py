@@ -59,3 +59,13 @@ def test_distortion_and_depth_match_reference_fixtures():
         assert np.abs(dz - z[f"dist_{tag}_dz"]).max() <= 1e-12
         d = OL.depth_from_fragments(z["dist_off"], z["dist_w"], z[f"dist_{tag}_z"], h, w)
         assert np.abs(d - z[f"depth_{tag}"]).max() <= 1e-12
+
+
+def test_normal_loss_matches_reference_fixture():
+    z = np.load(GOLD)
+    fx, fy, cx, cy = z["nl_intr"]
+    v, dv, dw = OL.normal_loss(z["nl_verts"], z["dist_off"], z["nl_tri"], z["dist_w"], z["nl_depth"],
+                               fx, fy, cx, cy, z["nl_rot"], z["nl_trans"])
+    assert abs(v - float(z["nl_val"])) <= 1e-12
+    assert np.abs(dv - z["nl_dv"]).max() <= 1e-12
+    assert np.abs(dw - z["nl_dw"]).max() <= 1e-12
