@@ -7,7 +7,8 @@
 //                    records the smallest offending triangle of its group
 //                    (the reference raises before touching any state);
 //   k_adam_update -- thread per element, skipped entirely if any group was
-//                    flagged: m, v, bias-corrected step in fp64, clamps.
+//                    flagged: m, v in fp64 arithmetic, the bias-corrected step in
+//                    fp32 (fp64 below the fp32 normal range), clamps.
 // Element e of the flat 59 N space (the DeviceGrads / moment layout
 // [vertices 9N | opacity N | sigma N | sh 48N]) reads the parameter tensors
 // in place, so one grid covers all groups with coalesced accesses.
@@ -29,33 +30,47 @@ struct AdamGroups {
 __device__ __forceinline__ int group_of(const AdamGroups& a, long long e) {
     return e < a.off[1] ? 0 : (e < a.off[2] ? 1 : (e < a.off[3] ? 2 : 3));
 }
+// selects instead of a dynamically indexed parameter array (which would be
+// copied to local memory)
+template <typename T>
+__device__ __forceinline__ T pick(int k, T a0, T a1, T a2, T a3) {
+    return k == 0 ? a0 : (k == 1 ? a1 : (k == 2 ? a2 : a3));
+}
 }  // namespace
 
 __global__ void __launch_bounds__(256) k_adam_check(AdamGroups a, unsigned long long* __restrict__ bad) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= a.off[4]) return;
     const int k = group_of(a, e);
-    const long long local = e - a.off[k];
-    if (!isfinite(a.g[k][local])) atomicMin(bad + k, (unsigned long long)(local / a.width[k]));
+    const long long local = e - pick(k, a.off[0], a.off[1], a.off[2], a.off[3]);
+    const float* g = pick(k, a.g[0], a.g[1], a.g[2], a.g[3]);
+    if (!isfinite(g[local])) atomicMin(bad + k, (unsigned long long)(local / pick(k, 9, 1, 1, 48)));
 }
 
 __global__ void __launch_bounds__(256) k_adam_update(AdamGroups a, float* __restrict__ m, float* __restrict__ v,
-                                                     double bc1, double bc2,
+                                                     double ibc1, double ibc2,
                                                      const unsigned long long* __restrict__ bad) {
     if ((bad[0] & bad[1] & bad[2] & bad[3]) != ~0ull) return;  // some group flagged
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= a.off[4]) return;
     const int k = group_of(a, e);
-    const long long local = e - a.off[k];
-    const double g = (double)a.g[k][local];
+    const long long local = e - pick(k, a.off[0], a.off[1], a.off[2], a.off[3]);
+    const double g = (double)pick(k, a.g[0], a.g[1], a.g[2], a.g[3])[local];
+    float* pp = pick(k, a.p[0], a.p[1], a.p[2], a.p[3]);
+    const double lr = pick(k, a.lr[0], a.lr[1], a.lr[2], a.lr[3]);
     const double mm = ADAM_B1 * (double)m[e] + (1.0 - ADAM_B1) * g;
     const double vv = ADAM_B2 * (double)v[e] + (1.0 - ADAM_B2) * g * g;
     m[e] = (float)mm;
     v[e] = (float)vv;
-    double p = (double)a.p[k][local] - a.lr[k] * (mm / bc1) / (sqrt(vv / bc2) + ADAM_EPS);
-    if (k == 1) p = fmin(fmax(p, 1e-4), 1.0 - 1e-4);  // opacity clamp
-    if (k == 2) p = fmin(fmax(p, 1e-3), 1e3);         // sigma clamp
-    a.p[k][local] = (float)p;
+    // the step in fp32 (the parameter is fp32; ~1e-7 relative) unless the
+    // second moment is below the fp32 normal range (then fp64 as the reference)
+    const double mh = mm * ibc1, vh = vv * ibc2;
+    const float step = vh > 1e-30 ? (float)lr * (float)mh / (sqrtf((float)vh) + 1e-15f)
+                                  : (float)(lr * mh / (sqrt(vh) + ADAM_EPS));
+    float p = pp[local] - step;
+    if (k == 1) p = fminf(fmaxf(p, 1e-4f), 1.0f - 1e-4f);  // opacity clamp
+    if (k == 2) p = fminf(fmaxf(p, 1e-3f), 1e3f);          // sigma clamp
+    pp[local] = p;
 }
 
 void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
@@ -78,7 +93,7 @@ void launch_adam_step(float* const params[4], const float* const grads[4], long 
     const unsigned grid = (unsigned)((off + 255) / 256);
     k_adam_check<<<grid, 256, 0, st>>>(a, b);
     const double bc1 = 1.0 - pow(ADAM_B1, (double)t), bc2 = 1.0 - pow(ADAM_B2, (double)t);
-    k_adam_update<<<grid, 256, 0, st>>>(a, m, v, bc1, bc2, b);
+    k_adam_update<<<grid, 256, 0, st>>>(a, m, v, 1.0 / bc1, 1.0 / bc2, b);
 }
 
 }  // namespace ts
