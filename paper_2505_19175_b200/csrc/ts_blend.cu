@@ -168,37 +168,36 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 if (cy0 + q <= cy1 && cx0 <= cx1) {
                     const EvalRec& R = sm.ev[slot];
                     const double rlo = R.r_lo, xl = sm.xc[0], y0 = sm.yc[cy0 + q];
-                    // per edge: r_lo - l(xl, y) at the thread's first row, its step per 4 rows, 1/a0
-                    double n0[3], st[3];
-                    float inv[3];
-                    bool up[3], dn[3], zr[3];  // bound below (a0 > 0) / above (a0 < 0) / a0 == 0
+                    // per edge, the bound on the tile-local pixel index is linear in the
+                    // row: lx >= / <= tb0 + m * sl (a0 > 0 / < 0) with tb0 = (r_lo -
+                    // l(xl, y0)) / a0 and sl the change per 4 rows, in fp32 with a margin
+                    // covering the fp32 rounding (1e-3 px + 2^-20 of the magnitudes);
+                    // edges with |a0| tiny or a0 == 0 do not narrow the rows
+                    // (a superset of the passing pixels either way)
+                    float tb0[3], sl[3], mg[3];
+                    bool up[3], dn[3];
 #pragma unroll
                     for (int ed = 0; ed < 3; ed++) {
                         const double a0 = R.a[3 * ed], a1 = R.a[3 * ed + 1];
-                        n0[ed] = rlo - fma(a0, xl, fma(a1, y0, R.a[3 * ed + 2]));
-                        st[ed] = -4.0 * a1;
-                        inv[ed] = __fdividef(1.f, (float)a0);
-                        const bool fin = fabsf(inv[ed]) < 1e30f;  // |a0| tiny: no bound
+                        const double n0 = rlo - fma(a0, xl, fma(a1, y0, R.a[3 * ed + 2]));
+                        const float inv = __fdividef(1.f, (float)a0);
+                        tb0[ed] = (float)n0 * inv;
+                        sl[ed] = (float)(-4.0 * a1) * inv;
+                        const bool fin = fabsf(inv) < 1e30f && fabsf(tb0[ed]) < 1e6f && fabsf(sl[ed]) < 1e4f;
+                        mg[ed] = 1e-3f + 9.6e-7f * (fabsf(tb0[ed]) + 4.f * fabsf(sl[ed]));
                         up[ed] = a0 > 0.0 && fin;
                         dn[ed] = a0 < 0.0 && fin;
-                        zr[ed] = a0 == 0.0;
                     }
                     const int nrow = (cy1 - cy0 - q) / 4 + 1;
-                    const double zthr = 1e-9 * (fabs(rlo) + 1.0);
 #pragma unroll
                     for (int m = 0; m < 4; m++) {
                         if (m >= nrow) break;
                         int lo = cx0, hi = cx1;
 #pragma unroll
                         for (int ed = 0; ed < 3; ed++) {
-                            // a0 * (xl + lx) + c >= r_lo: lx >= / <= (r_lo - l(xl)) / a0,
-                            // in fp32 widened by 1e-3 px (a superset of the passing pixels)
-                            const double num = fma((double)m, st[ed], n0[ed]);
-                            const float tb = fminf(fmaxf((float)num * inv[ed], -64.f), 64.f);
-                            const int lc = __float2int_ru(tb - 1e-3f), hc = __float2int_rd(tb + 1e-3f);
-                            lo = up[ed] ? max(lo, lc) : lo;
-                            hi = dn[ed] ? min(hi, hc) : hi;
-                            hi = (zr[ed] && num > zthr) ? -1 : hi;
+                            const float tb = fminf(fmaxf(fmaf((float)m, sl[ed], tb0[ed]), -64.f), 64.f);
+                            lo = up[ed] ? max(lo, __float2int_ru(tb - mg[ed])) : lo;
+                            hi = dn[ed] ? min(hi, __float2int_rd(tb + mg[ed])) : hi;
                         }
                         xa[m] = lo;
                         len[m] = max(hi - lo + 1, 0);
