@@ -119,12 +119,13 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __rest
 constexpr int BIN_CT = 1024;               // threads per chunk CTA
 constexpr int BIN_PER = 8;                 // triangles per thread
 constexpr int BIN_CHUNK = BIN_CT * BIN_PER;
-constexpr int BIN_MAX_TILES = 12288;       // shared-memory counters per CTA (48 KB)
+constexpr int BIN_MAX_TILES = 12288;       // shared-memory counters per CTA (48 KB): tile range per blockIdx.y
 
 __global__ void __launch_bounds__(BIN_CT) k_bin_count(long long n, const short4* __restrict__ bbox, int ntx,
                                                       int ntiles, unsigned* __restrict__ mat) {
     extern __shared__ unsigned s_cnt[];
-    for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cnt[t] = 0u;
+    const int t0 = blockIdx.y * BIN_MAX_TILES, nt = min(BIN_MAX_TILES, ntiles - t0);  // this CTA's tile range
+    for (int t = threadIdx.x; t < nt; t += BIN_CT) s_cnt[t] = 0u;
     __syncthreads();
     const long long c0 = (long long)blockIdx.x * BIN_CHUNK;
     short4 bb[BIN_PER];  // all loads in flight before the first use
@@ -139,11 +140,14 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_count(long long n, const short4*
         const int tx0 = bb[k].x / TILE, tx1 = (bb[k].y - 1) / TILE + 1;
         const int ty0 = bb[k].z / TILE, ty1 = (bb[k].w - 1) / TILE + 1;
         for (int ty = ty0; ty < ty1; ty++)
-            for (int tx = tx0; tx < tx1; tx++) atomicAdd(&s_cnt[ty * ntx + tx], 1u);
+            for (int tx = tx0; tx < tx1; tx++) {
+                const int t = ty * ntx + tx - t0;
+                if ((unsigned)t < (unsigned)nt) atomicAdd(&s_cnt[t], 1u);
+            }
     }
     __syncthreads();
-    unsigned* row = mat + (size_t)blockIdx.x * ntiles;
-    for (int t = threadIdx.x; t < ntiles; t += BIN_CT) row[t] = s_cnt[t];
+    unsigned* row = mat + (size_t)blockIdx.x * ntiles + t0;
+    for (int t = threadIdx.x; t < nt; t += BIN_CT) row[t] = s_cnt[t];
 }
 
 // per tile: exclusive prefix over the chunks in place, totals into tcnt.  CTA =
@@ -179,13 +183,14 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* 
                                                      const Counters* __restrict__ ctr, uint2* __restrict__ bucket) {
     extern __shared__ unsigned s_cur[];
     if (tile_start[ntiles] == 0) return;  // empty (or over capacity)
+    const int t0 = blockIdx.y * BIN_MAX_TILES, nt = min(BIN_MAX_TILES, ntiles - t0);  // this CTA's tile range
     // 32-bit depth keys, range-reduced over the accepted triangles (monotone in
     // the fp64 key; ties of the reduced key are broken exactly by the tile sort)
     const unsigned long long kmin = ctr->key_min, krange = ctr->key_max - kmin;
     const int kbits = krange ? 64 - __clzll((long long)krange) : 0;
     const int gshift = kbits > 32 ? kbits - 32 : 0;
-    const unsigned* row = mat + (size_t)blockIdx.x * ntiles;
-    for (int t = threadIdx.x; t < ntiles; t += BIN_CT) s_cur[t] = (unsigned)tile_start[t] + row[t];
+    const unsigned* row = mat + (size_t)blockIdx.x * ntiles + t0;
+    for (int t = threadIdx.x; t < nt; t += BIN_CT) s_cur[t] = (unsigned)tile_start[t0 + t] + row[t];
     __syncthreads();
     const long long c0 = (long long)blockIdx.x * BIN_CHUNK;
     short4 bb[BIN_PER];
@@ -204,7 +209,9 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* 
         const int ty0 = bb[k].z / TILE, ty1 = (bb[k].w - 1) / TILE + 1;
         for (int ty = ty0; ty < ty1; ty++)
             for (int tx = tx0; tx < tx1; tx++) {
-                const unsigned pos = atomicAdd(&s_cur[ty * ntx + tx], 1u);
+                const int t = ty * ntx + tx - t0;
+                if ((unsigned)t >= (unsigned)nt) continue;
+                const unsigned pos = atomicAdd(&s_cur[t], 1u);
                 bucket[pos] = make_uint2((unsigned)((key[k] - kmin) >> gshift), (unsigned)i);
             }
     }
@@ -594,7 +601,8 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
                     unsigned* tcnt, unsigned* mat, int* tile_start, uint2* bucket, const Counters* ctr,
                     long long cap, unsigned* overflow, int* big_list, cudaStream_t st) {
     const int nchunk = (int)((n + BIN_CHUNK - 1) / BIN_CHUNK);
-    const int smem = ntiles * (int)sizeof(unsigned);
+    const int nrange = (ntiles + BIN_MAX_TILES - 1) / BIN_MAX_TILES;  // tile ranges (grid y)
+    const int smem = (nrange > 1 ? BIN_MAX_TILES : ntiles) * (int)sizeof(unsigned);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BIN_MAX_TILES);
@@ -602,7 +610,7 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
         attr = true;
     }
     if (n > 0) {
-        k_bin_count<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat);
+        k_bin_count<<<dim3(nchunk, nrange), BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat);
         k_bin_cols<<<(ntiles + 31) / 32, 256, 0, st>>>(nchunk, ntiles, mat, tcnt);
     } else {
         cudaMemsetAsync(tcnt, 0, sizeof(unsigned) * ntiles, st);
@@ -611,7 +619,8 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
     k_tile_scan<<<1, 1024, 0, st>>>(ntiles, tcnt, tile_start, cap, overflow, SORT_SMALL, big_list,
                                     big_list + ntiles);
     if (n > 0)
-        k_bin_fill<<<nchunk, BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, ctr, bucket);
+        k_bin_fill<<<dim3(nchunk, nrange), BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, ctr,
+                                                              bucket);
 }
 
 size_t bin_matrix_bytes(long long n, int ntiles) {
@@ -619,7 +628,7 @@ size_t bin_matrix_bytes(long long n, int ntiles) {
     return sizeof(unsigned) * (size_t)(nchunk > 0 ? nchunk : 1) * (size_t)ntiles;
 }
 
-int bin_max_tiles() { return BIN_MAX_TILES; }
+int bin_max_tiles() { return 1 << 22; }  // (any view: larger tile counts use several tile ranges)
 
 void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
                     const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],

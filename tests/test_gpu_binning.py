@@ -119,3 +119,13 @@ def test_legacy_binning_matches():
     env = dict(os.environ, TS_BIN_LEGACY="1")
     p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+def test_many_tiles_uses_tile_ranges(rast):
+    # 3840x2160 = 32400 tiles: the chunk x tile counting runs in several
+    # shared-memory tile ranges (12288 tiles each)
+    from paper_2505_19175_b200 import scenes
+    soup = scenes.make_soup(60_000, seed=9, size=0.03, sigma=(0.5, 2.0))
+    intr, pose = scenes.frontal_camera(3840, 2160, 3300.0)
+    longest = _check(rast, soup, intr, pose, "4k")
+    assert longest > 0
