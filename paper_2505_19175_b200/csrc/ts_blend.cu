@@ -129,11 +129,18 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
     for (int c = tid; c < (rhi - s) * 8; c += 256) fetch_rec(s + (c >> 3), c & 7);
     cp_async_commit();
     if (tid < PCAP / 32) sm.starts[tid] = 0u;
-    int nb = 0;
+    int nb = 0, pb = 0, pnb = 0;  // (pb, pnb): previous batch, statistics not yet flushed
     for (int b = s; b < e; b += nb) {
         cp_async_wait_all();
         if (__syncthreads_count(!done) == 0) break;
         const int navail = min(DB, e - b);
+        if (tid < pnb) {  // per-entry statistics of the previous batch (complete since the barrier)
+            const unsigned src = sm.srcq[(pb + tid) & (SR - 1)];
+            if (sm.maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, sm.maxw[tid]);
+            if (sm.pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, sm.pix[tid]);
+            sm.maxw[tid] = 0u;
+            sm.pix[tid] = 0;
+        }
         {  // ids two batches ahead
             const int nshi = min(b + 3 * DB, e);
             for (int p = shi + tid; p < nshi; p += 256) cp_async4(&sm.srcq[p & (SR - 1)], ent_src + p);
@@ -473,14 +480,14 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             }
             if (done && rb != ~0ull) mark_holes(mm);
         }
-        __syncthreads();
-        if (tid < nb) {
-            const unsigned src = sm.srcq[(b + tid) & (SR - 1)];
-            if (sm.maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, sm.maxw[tid]);
-            if (sm.pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, sm.pix[tid]);
-            sm.maxw[tid] = 0u;
-            sm.pix[tid] = 0;
-        }
+        pb = b;
+        pnb = nb;
+    }
+    __syncthreads();
+    if (tid < pnb) {
+        const unsigned src = sm.srcq[(pb + tid) & (SR - 1)];
+        if (sm.maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, sm.maxw[tid]);
+        if (sm.pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, sm.pix[tid]);
     }
     cp_async_wait_all();
     if (inside) {
