@@ -47,7 +47,8 @@ struct DenseSmem {
     EvalRec ev[RR];
     TailRec tail[RR];
     PT os[ACC64 ? RR : 1][2];      // exact (opacity, sigma) of the ring slots (training forwards)
-    Real r[PCAP];                  // per pair: r; NaN = inside the contribution band
+    Real r[PCAP];                  // per pair: render: alpha (clamped); training: r; NaN = inside the band
+    float ea[ACC64 ? 1 : PCAP];    // render: relative error bound of the fp32 alpha
     unsigned mask[NW][256];        // per pixel: bit j = entry j passes (r >= r_lo)
     unsigned srcq[SR];
     float4 col[DB];                // rgb, f0
@@ -319,7 +320,31 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                     const double rr = m01 < l2 ? m01 : l2;
                     pass = rr >= r.r_lo;
                     if (pass) {
-                        sm.r[k] = rr > r.r_hi ? (Real)rr : (Real)__int_as_float(0x7fc00000);
+                        if constexpr (ACC64) {
+                            sm.r[k] = rr > r.r_hi ? (Real)rr : (Real)__int_as_float(0x7fc00000);
+                        } else {
+                            // render: the fp32 alpha and its error bound here, densely
+                            // (not in the per-pixel compositing loop)
+                            float a = __int_as_float(0x7fc00000), ea = 0.f;
+                            if (rr > r.r_hi) {
+                                const float rv = (float)rr;
+                                const float4 col = sm.col[j];
+                                const float f1 = sm.f1[j];
+                                if (mode == 0) {
+                                    const float lg = fast_lg2(fminf(rv, 1.f));
+                                    const float arg = fmaf(col.w, lg, f1);
+                                    a = fast_ex2(arg);
+                                    ea = 5e-7f + col.w * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
+                                } else {
+                                    const float x = rv * col.w;
+                                    a = __fdividef(f1, 1.0f + fast_ex2(fminf(x, 1009.9f)));
+                                    ea = 8e-7f + 1.2e-7f * fabsf(x);
+                                }
+                                a = fminf(a, ALPHA_CLAMP_F);
+                            }
+                            sm.r[k] = a;
+                            sm.ea[k] = ea;
+                        }
                         atomicOr(&sm.mask[j >> 5][qy * TILE + qx], 1u << (j & 31));
                     }
                 }
@@ -437,19 +462,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         wout = (float)wd64;
                         if (wd64 > opt.tau_contrib) red_add_shared(&sm.pix[j], 1);
                     } else {
-                        const float f1 = sm.f1[j];
-                        float a, ea;
-                        if (mode == 0) {
-                            const float lg = fast_lg2(fminf(rv, 1.f));
-                            const float arg = fmaf(col.w, lg, f1);
-                            a = fast_ex2(arg);
-                            ea = 5e-7f + col.w * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
-                        } else {
-                            const float x = rv * col.w;
-                            a = __fdividef(f1, 1.0f + fast_ex2(fminf(x, 1009.9f)));
-                            ea = 8e-7f + 1.2e-7f * fabsf(x);
-                        }
-                        a = fminf(a, ALPHA_CLAMP_F);
+                        const float a = (float)rv;  // alpha of the evaluation (clamped)
+                        const float ea = sm.ea[kp];
                         const float wgt = T * a;
                         const float tn = fmaf(-T, a, T);
                         // (approximate quotient: the tests below keep a 2x margin on en)
