@@ -350,7 +350,29 @@ def main():
         a1e.record(stream)
         torch.cuda.synchronize()
         adam_ms = a0e.elapsed_time(a1e) / 5
-        del ds_opt, ast
+        del ds_opt
+        # one density-control step (prune + grow, density.py:180-263, default
+        # DensifyConfig) from the statistics of 8 orbit views, plus the Adam
+        # moment remap; host-side wall clock around the synchronized call
+        # (it includes the numpy draws of the caller's Generator)
+        import numpy as _np
+        from paper_2505_19175_b200 import density as _dens
+        dstats = _dens.DeviceViewStats.empty(len(ds3))
+        for vi, pz in enumerate(poses[:8]):
+            fo = rast.forward(ds3, intr3, pz, keep_backward=False, precision=args.precision)
+            dstats.update(vi, fo, 2)
+        torch.cuda.synchronize()
+        dcfg = _dens.DensifyConfig()
+        _dens.densify_step(ds3, dstats, 500, dcfg, _np.random.default_rng(0))  # warm-up
+        torch.cuda.synchronize()
+        tq = time.perf_counter()
+        dsoup, drep = _dens.densify_step(ds3, dstats, 500, dcfg, _np.random.default_rng(1))
+        ast2 = ast.remap(drep["origin"])
+        torch.cuda.synchronize()
+        densify_ms = (time.perf_counter() - tq) * 1e3
+        dinfo = {"n_before": drep["n_before"], "n_after": drep["n_after"], "n_removed": drep["prune"]["n_removed"],
+                 "n_split": drep["n_split"], "n_clone": drep["n_clone"], "views": dstats.n_views}
+        del dsoup, ast2, ast, dstats
         rast.profile(True)
         trainer._grad(0 if len(mine) == 0 else mine[0], trainer.grads.flat, True)
         stt = rast.stage_times()
@@ -363,6 +385,7 @@ def main():
                  "optimizer": "none in the timed step (the metric is fwd+bwd); fused Adam timed "
                               "separately as adam_ms",
                  "adam_ms": adam_ms,
+                 "densify_ms": densify_ms, "densify": dinfo,
                  "workload": f"{c3.n} triangles, {c3.width}x{c3.height}, orbit cameras r=6",
                  "last_view_backward_ms": stt["blend_bwd"] + stt["chain_bwd"],
                  "last_view_stages_ms": {k: round(v, 4) for k, v in stt.items()}}

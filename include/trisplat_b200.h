@@ -209,6 +209,56 @@ int ts_adam_step(ts_context* ctx, float* vertices, float* opacity, float* sigma,
                  const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
                  void* stream);
 
+/* ---------------- adaptive density control (density.py:27-263) ----------------
+ * The array work of ViewStats / prune / sample_candidates / midpoint_subdivide /
+ * clone_with_noise on device-resident triangles; the sequential pick loop of
+ * densify_step (a prefix sum over the picks' costs) and the numpy random draws
+ * stay with the caller.  dtype: 0 = float32 parameters, 1 = float64.  Index
+ * arrays are device int64.  pool / kept may be NULL (identity). */
+#define TS_SAMPLE_INVERSE_SIGMA 0
+#define TS_SAMPLE_OPACITY 1
+/* ViewStats.update + aggregation (density.py:42-71): fold one view's forward
+ * statistics (ts_forward_out max_weight / pixel_count / area) into acc_*
+ * (device double[N] max weight, int32[N] views with pixel_count >= min_pixels,
+ * double[N] area sum); first != 0 initialises them.  Call per view in the
+ * order the views were first recorded. */
+int ts_view_stats_accumulate(ts_context* ctx, int64_t n, const float* max_weight, const int32_t* pixel_count,
+                             const float* area, int min_pixels, int first, double* acc_max_weight,
+                             int32_t* acc_views, double* acc_area, void* stream);
+/* prune (density.py:74-94): flags (device uint8[N]) bit 0 max weight < tau_prune,
+ * bit 1 views < min_views, bit 2 opacity < opacity_dead; kept (device int64[N])
+ * receives the unflagged indices in order, n_kept (device int64[1]) their count. */
+int ts_prune_mark(ts_context* ctx, int64_t n, const double* acc_max_weight, const int32_t* acc_views,
+                  const void* opacity, int dtype, double tau_prune, int min_views, double opacity_dead,
+                  uint8_t* flags, int64_t* kept, int64_t* n_kept, void* stream);
+/* sample_candidates (density.py:103-120): weights of the pool members
+ * (member k is triangle kept[pool[k]]) from param (sigma for
+ * TS_SAMPLE_INVERSE_SIGMA, opacity for TS_SAMPLE_OPACITY), keys =
+ * exponential[k] / max(w, 1e-300) (device double[n_pool], the caller's
+ * rng.exponential(size=n_pool)), picked (device int64[count]) = the first count
+ * positions of the stable ascending order of the keys (pool-local indices). */
+int ts_sample_candidates(ts_context* ctx, int64_t n_pool, const int64_t* pool, const int64_t* kept,
+                         const void* param, int dtype, int criterion, const double* exponential, int64_t count,
+                         int64_t* picked, void* stream);
+/* Per pick (device int64[count] pool-local): source triangle kept[pool[picked]],
+ * its mean area acc_area / max(n_views, 1) and whether |(v1-v0) x (v2-v0)| < 1e-12
+ * (density.py:130-131, 154-157). */
+int ts_pick_info(ts_context* ctx, int64_t count, const int64_t* picked, const int64_t* pool, const int64_t* kept,
+                 const double* acc_area, int64_t n_views, const void* vertices, int dtype, int64_t* source,
+                 double* mean_area, uint8_t* degenerate, void* stream);
+/* dst[r, :] = src[origin[r], :] (zeros where origin[r] < 0) for rows of width
+ * elements of elem_bytes (4 or 8): TriangleSoup.select / AdamState.remap
+ * (soup.py select, training.py:64-78). */
+int ts_gather_rows(ts_context* ctx, int64_t n_out, const int64_t* origin, const void* src, void* dst, int width,
+                   int elem_bytes, void* stream);
+/* Children vertices (density.py:123-171): code[k] in 0..3 -> subdivision corner
+ * of parent[k]; code[k] = 4 + r -> clone jittered in the parent's plane with
+ * uniforms[6r..6r+5] (angle / 2 pi, radius / (max_noise_factor * mean edge) per
+ * vertex, the caller's rng.uniform draws in order); code < 0 -> left as is. */
+int ts_child_vertices(ts_context* ctx, int64_t n_child, const int64_t* parent, const int32_t* code,
+                      const double* uniforms, double max_noise_factor, const void* src_vertices, void* dst_vertices,
+                      int dtype, void* stream);
+
 /* Debug/parity dumps of the last forward pass (device destination):
  *  TS_DUMP_SORTED_IDX  int32[M]       depth-sorted source ids (render.py:275-277)
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)

@@ -68,7 +68,8 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_stage_times", "ts_flagged_pixels", "ts_fragment_offsets", "ts_collect_fragments",
            "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_photometric_loss",
            "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
-           "ts_normal_loss"]
+           "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
+           "ts_pick_info", "ts_gather_rows", "ts_child_vertices"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -133,6 +134,16 @@ def load(path: str = LIB_PATH):
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, P(TsCamera),
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     lib.ts_normal_loss.restype = ctypes.c_int
+    V, I64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    lib.ts_view_stats_accumulate.argtypes = [V, I64, V, V, V, I, I, V, V, V, V]
+    lib.ts_prune_mark.argtypes = [V, I64, V, V, V, I, D, I, D, V, V, V, V]
+    lib.ts_sample_candidates.argtypes = [V, I64, V, V, V, I, I, V, I64, V, V]
+    lib.ts_pick_info.argtypes = [V, I64, V, V, V, V, I64, V, I, V, V, V, V]
+    lib.ts_gather_rows.argtypes = [V, I64, V, V, V, I, I, V]
+    lib.ts_child_vertices.argtypes = [V, I64, V, V, V, D, V, V, I, V]
+    for nm in ("ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",
+               "ts_gather_rows", "ts_child_vertices"):
+        getattr(lib, nm).restype = ctypes.c_int
     lib.ts_launch_count.argtypes = [ctypes.c_void_p]
     lib.ts_launch_count.restype = ctypes.c_int64
     lib.ts_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]

@@ -63,6 +63,7 @@ struct ts_context {
     uint2* bucket = nullptr;                       // (reduced depth key, source) of every tile entry, unsorted
     DevBuf binmat;                                 // chunk x tile count matrix of the binning
     DevBuf lossbuf;                                // photometric loss scratch
+    DevBuf densbuf;                                // density control: sampling keys / sort scratch
     bool sorted_valid = false;                     // sorted_src holds the global depth order
     // per-pixel scratch
     long long cap_p = -1, cap_tiles = -1;
@@ -809,6 +810,80 @@ int ts_adam_step(ts_context* c, float* vertices, float* opacity, float* sigma, f
     const float* const g[4] = {grads->d_vertices, grads->d_opacity, grads->d_sigma, grads->d_sh};
     launch_adam_step(params, g, n, m, v, t, lrs, (long long*)bad, (cudaStream_t)stream);
     g_launches += n > 0 ? 2 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
+// ---------------- density control (density.py:27-263) ----------------
+int ts_view_stats_accumulate(ts_context* c, int64_t n, const float* max_weight, const int32_t* pixel_count,
+                             const float* area, int min_pixels, int first, double* acc_max_weight,
+                             int32_t* acc_views, double* acc_area, void* stream) {
+    if (!c || n < 0) return TS_ERR_INVALID_ARG;
+    if (n > 0 && (!max_weight || !pixel_count || !area || !acc_max_weight || !acc_views || !acc_area))
+        return TS_ERR_INVALID_ARG;
+    launch_stats_accum(n, max_weight, pixel_count, area, min_pixels, first, acc_max_weight, acc_views, acc_area,
+                       (cudaStream_t)stream);
+    g_launches += n > 0 ? 1 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_prune_mark(ts_context* c, int64_t n, const double* acc_max_weight, const int32_t* acc_views,
+                  const void* opacity, int dtype, double tau_prune, int min_views, double opacity_dead,
+                  uint8_t* flags, int64_t* kept, int64_t* n_kept, void* stream) {
+    if (!c || n < 0 || !n_kept || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
+    if (n > 0 && (!acc_max_weight || !acc_views || !opacity || !flags || !kept)) return TS_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_prune_mark(n, acc_max_weight, acc_views, opacity, dtype, tau_prune, min_views, opacity_dead, flags, st);
+    compact_unflagged(n, flags, (long long*)kept, (long long*)n_kept, c->sort, st);
+    g_launches += n > 0 ? 4 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_sample_candidates(ts_context* c, int64_t n_pool, const int64_t* pool, const int64_t* kept,
+                         const void* param, int dtype, int criterion, const double* exponential, int64_t count,
+                         int64_t* picked, void* stream) {
+    if (!c || n_pool < 0 || count < 0 || count > n_pool || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
+    if (criterion != TS_SAMPLE_INVERSE_SIGMA && criterion != TS_SAMPLE_OPACITY) return TS_ERR_INVALID_ARG;
+    if (count == 0) return TS_OK;
+    if (!param || !exponential || !picked) return TS_ERR_INVALID_ARG;
+    if (n_pool > 0xffffffffLL) return TS_ERR_CAPACITY;
+    int rc;
+    if ((rc = ensure(c->densbuf, sample_scratch_bytes(n_pool)))) return rc;
+    launch_sample_candidates(n_pool, (const long long*)pool, (const long long*)kept, param, dtype,
+                             criterion == TS_SAMPLE_INVERSE_SIGMA, exponential, count, (long long*)picked,
+                             c->densbuf.p, c->sort, (cudaStream_t)stream);
+    g_launches += 3 + 3 * 8;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_pick_info(ts_context* c, int64_t count, const int64_t* picked, const int64_t* pool, const int64_t* kept,
+                 const double* acc_area, int64_t n_views, const void* vertices, int dtype, int64_t* source,
+                 double* mean_area, uint8_t* degenerate, void* stream) {
+    if (!c || count < 0 || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
+    if (count > 0 && (!picked || !acc_area || !vertices || !source || !mean_area || !degenerate))
+        return TS_ERR_INVALID_ARG;
+    launch_pick_info(count, (const long long*)picked, (const long long*)pool, (const long long*)kept, acc_area,
+                     n_views, vertices, dtype, (long long*)source, mean_area, degenerate, (cudaStream_t)stream);
+    g_launches += count > 0 ? 1 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_gather_rows(ts_context* c, int64_t n_out, const int64_t* origin, const void* src, void* dst, int width,
+                   int elem_bytes, void* stream) {
+    if (!c || n_out < 0 || width < 0 || (elem_bytes != 4 && elem_bytes != 8)) return TS_ERR_INVALID_ARG;
+    if (n_out > 0 && width > 0 && (!origin || !src || !dst)) return TS_ERR_INVALID_ARG;
+    launch_gather_rows(n_out, (const long long*)origin, src, dst, width, elem_bytes, (cudaStream_t)stream);
+    g_launches += (n_out > 0 && width > 0) ? 1 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_child_vertices(ts_context* c, int64_t n_child, const int64_t* parent, const int32_t* code,
+                      const double* uniforms, double max_noise_factor, const void* src_vertices, void* dst_vertices,
+                      int dtype, void* stream) {
+    if (!c || n_child < 0 || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
+    if (n_child > 0 && (!parent || !code || !src_vertices || !dst_vertices)) return TS_ERR_INVALID_ARG;
+    launch_child_vertices(n_child, (const long long*)parent, code, uniforms, max_noise_factor, src_vertices,
+                          dst_vertices, dtype, (cudaStream_t)stream);
+    g_launches += n_child > 0 ? 1 : 0;
     return cuda_err(cudaGetLastError());
 }
 

@@ -184,6 +184,27 @@ int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned*
 void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
                       long long t, const double lrs[4], long long* bad, cudaStream_t st);
 
+// ts_density.cu: adaptive density control (density.py:27-263)
+void launch_stats_accum(long long n, const float* maxw, const int* pixcnt, const float* area, int min_pixels,
+                        int first, double* acc_maxw, int* acc_views, double* acc_area, cudaStream_t st);
+void launch_prune_mark(long long n, const double* acc_maxw, const int* acc_views, const void* opacity, int is_f64,
+                       double tau_prune, int min_views, double opacity_dead, unsigned char* flags,
+                       cudaStream_t st);
+size_t sample_scratch_bytes(long long n);
+void launch_sample_candidates(long long n, const long long* pool, const long long* kept, const void* param,
+                              int is_f64, int inverse, const double* expo, long long count, long long* picked,
+                              void* scratch, const SortScratch& ss, cudaStream_t st);
+void launch_pick_info(long long count, const long long* picked, const long long* pool, const long long* kept,
+                      const double* acc_area, long long n_views, const void* vertices, int is_f64, long long* src,
+                      double* mean_area, unsigned char* degen, cudaStream_t st);
+void launch_gather_rows(long long n_out, const long long* origin, const void* src, void* dst, int width,
+                        int elem_bytes, cudaStream_t st);
+void launch_child_vertices(long long n_child, const long long* parent, const int* code, const double* uni,
+                           double max_noise_factor, const void* src, void* dst, int is_f64, cudaStream_t st);
+// ts_sort.cu: in-order indices of the zero flags; *n_kept = their count (device)
+void compact_unflagged(long long n, const unsigned char* flags, long long* kept, long long* n_kept,
+                       const SortScratch& s, cudaStream_t st);
+
 // ts_loss.cu: distortion loss over fragment CSR lists, fragment depth map
 size_t distortion_scratch_bytes(long long npix);
 void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,

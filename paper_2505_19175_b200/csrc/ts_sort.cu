@@ -154,6 +154,27 @@ void compact_accepted(long long n, const unsigned* flag, const unsigned long lon
     scan_functor(n, CompactF{flag, key, keys_c, vals_c}, s, st);
 }
 
+struct KeptF {
+    const unsigned char* flags;
+    long long n;
+    long long* kept;
+    long long* n_kept;
+    __device__ unsigned load(long long i) const { return flags[i] == 0 ? 1u : 0u; }
+    __device__ void store(long long i, unsigned ex, unsigned v) const {
+        if (v) kept[ex] = i;
+        if (i == n - 1) *n_kept = (long long)ex + v;
+    }
+};
+
+void compact_unflagged(long long n, const unsigned char* flags, long long* kept, long long* n_kept,
+                       const SortScratch& s, cudaStream_t st) {
+    if (n <= 0) {
+        cudaMemsetAsync(n_kept, 0, sizeof(long long), st);
+        return;
+    }
+    scan_functor(n, KeptF{flags, n, kept, n_kept}, s, st);
+}
+
 struct RankF {
     const unsigned* sorted_src;
     const unsigned* tcount;

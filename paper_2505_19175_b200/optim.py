@@ -30,6 +30,30 @@ class DeviceAdamState:
         return cls(torch.zeros(59 * n, dtype=torch.float32, device=device),
                    torch.zeros(59 * n, dtype=torch.float32, device=device), n, 0)
 
+    def remap(self, origin, rasterizer=None, stream=None) -> "DeviceAdamState":
+        """AdamState.remap (training.py:64-78) after densification: output
+        triangle i takes the moments of origin[i] (zeros where origin[i] < 0);
+        one row gather per parameter group on the device."""
+        import numpy as np
+        import torch
+        from . import _lib
+        from .rasterizer import default_rasterizer
+        r = rasterizer or default_rasterizer()
+        org = torch.as_tensor(np.asarray(origin, dtype=np.int64)).to("cuda")
+        n_new = int(org.numel())
+        new = DeviceAdamState.zeros(n_new)
+        new.t = self.t
+        st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+        o_old = o_new = 0
+        for w in (9, 1, 1, 48):
+            for a, b in ((self.m, new.m), (self.v, new.v)):
+                _lib.check(r.lib.ts_gather_rows(r._ctx, n_new, ctypes.c_void_p(org.data_ptr()),
+                                                ctypes.c_void_p(a.data_ptr() + 4 * o_old),
+                                                ctypes.c_void_p(b.data_ptr() + 4 * o_new), w, 4, st), "gather_rows")
+            o_old += w * self.n
+            o_new += w * n_new
+        return new
+
 
 def adam_step(soup, grads, state: DeviceAdamState, lrs: dict, rasterizer=None, stream=None, check=True):
     """One in-place Adam update of ``soup`` (DeviceSoup, fp32) with ``grads``
