@@ -259,6 +259,23 @@ int ts_child_vertices(ts_context* ctx, int64_t n_child, const int64_t* parent, c
                       const double* uniforms, double max_noise_factor, const void* src_vertices, void* dst_vertices,
                       int dtype, void* stream);
 
+/* ---------------- model I/O: binary PLY body (scene_io.py:365-455) ----------------
+ * ts_ply_pack: the body of export_mesh(..., "ply") for N triangles (vertices
+ * (N,3,3), sh (N,16,3), dtype 0 f32 / 1 f64): vertex_bytes (device, 45 N bytes,
+ * 16-byte aligned) = 3 N records {float x,y,z; uchar r,g,b} with the quantised
+ * degree-0 colour, face_bytes (device, 16 N bytes, 16-byte aligned) = N records
+ * {int 3; int 3i,3i+1,3i+2}.  The header is the caller's (ASCII, scene_io.py:384-396).
+ * ts_ply_unpack: import_ply's body decode for n_face faces over n_vertex vertex
+ * records: vertices from the face indices, SH DC from the first vertex's colour,
+ * opacity 1, sigma given, other SH 0.  bad (device uint64[1]) = all ones if the
+ * body is valid, else (1 << 62 | face) for the first face whose count is not 3,
+ * or (2 << 62 | face) for the first out-of-range index when every count is 3. */
+int ts_ply_pack(ts_context* ctx, const void* vertices, const void* sh, int dtype, int64_t n, uint8_t* vertex_bytes,
+                void* face_bytes, void* stream);
+int ts_ply_unpack(ts_context* ctx, const uint8_t* vertex_bytes, int64_t n_vertex, const void* face_bytes,
+                  int64_t n_face, double sigma, int dtype, void* vertices, void* opacity, void* sigma_out, void* sh,
+                  uint64_t* bad, void* stream);
+
 /* Debug/parity dumps of the last forward pass (device destination):
  *  TS_DUMP_SORTED_IDX  int32[M]       depth-sorted source ids (render.py:275-277)
  *  TS_DUMP_TILE_START  int32[T+1]     CSR tile offsets (render.py:355-357)

@@ -69,7 +69,7 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_photometric_loss",
            "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
-           "ts_pick_info", "ts_gather_rows", "ts_child_vertices"]
+           "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack"]
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -141,7 +141,9 @@ def load(path: str = LIB_PATH):
     lib.ts_pick_info.argtypes = [V, I64, V, V, V, V, I64, V, I, V, V, V, V]
     lib.ts_gather_rows.argtypes = [V, I64, V, V, V, I, I, V]
     lib.ts_child_vertices.argtypes = [V, I64, V, V, V, D, V, V, I, V]
-    for nm in ("ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",
+    lib.ts_ply_pack.argtypes = [V, V, V, I, I64, V, V, V]
+    lib.ts_ply_unpack.argtypes = [V, V, I64, V, I64, D, I, V, V, V, V, V, V]
+    for nm in ("ts_ply_pack", "ts_ply_unpack", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",
                "ts_gather_rows", "ts_child_vertices"):
         getattr(lib, nm).restype = ctypes.c_int
     lib.ts_launch_count.argtypes = [ctypes.c_void_p]

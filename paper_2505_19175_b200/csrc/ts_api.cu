@@ -887,6 +887,31 @@ int ts_child_vertices(ts_context* c, int64_t n_child, const int64_t* parent, con
     return cuda_err(cudaGetLastError());
 }
 
+// ---------------- model I/O: binary PLY body (scene_io.py:382-455) ----------------
+int ts_ply_pack(ts_context* c, const void* vertices, const void* sh, int dtype, int64_t n, uint8_t* vertex_bytes,
+                void* face_bytes, void* stream) {
+    if (!c || n < 0 || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
+    if (n > 0 && (!vertices || !sh || !vertex_bytes || !face_bytes)) return TS_ERR_INVALID_ARG;
+    if (n > (1LL << 31) / 3) return TS_ERR_CAPACITY;  // int32 vertex indices
+    if (((uintptr_t)vertex_bytes & 15) || ((uintptr_t)face_bytes & 15)) return TS_ERR_INVALID_ARG;
+    launch_ply_pack(n, vertices, sh, dtype, vertex_bytes, face_bytes, (cudaStream_t)stream);
+    g_launches += n > 0 ? 1 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_ply_unpack(ts_context* c, const uint8_t* vertex_bytes, int64_t n_vertex, const void* face_bytes,
+                  int64_t n_face, double sigma, int dtype, void* vertices, void* opacity, void* sigma_out, void* sh,
+                  uint64_t* bad, void* stream) {
+    if (!c || n_vertex < 0 || n_face < 0 || !bad || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
+    if (n_face > 0 && (!vertex_bytes || !face_bytes || !vertices || !opacity || !sigma_out || !sh))
+        return TS_ERR_INVALID_ARG;
+    if ((uintptr_t)face_bytes & 15) return TS_ERR_INVALID_ARG;
+    launch_ply_unpack(n_face, n_vertex, vertex_bytes, face_bytes, sigma, dtype, vertices, opacity, sigma_out, sh,
+                      (unsigned long long*)bad, (cudaStream_t)stream);
+    g_launches += n_face > 0 ? 1 : 0;
+    return cuda_err(cudaGetLastError());
+}
+
 int ts_ssim(ts_context* c, const float* x, const float* y, int height, int width, double* out, void* stream) {
     if (!c || !x || !y || !out || height < 1 || width < 1) return TS_ERR_INVALID_ARG;
     int rc;

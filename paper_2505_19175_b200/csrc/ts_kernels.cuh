@@ -205,6 +205,13 @@ void launch_child_vertices(long long n_child, const long long* parent, const int
 void compact_unflagged(long long n, const unsigned char* flags, long long* kept, long long* n_kept,
                        const SortScratch& s, cudaStream_t st);
 
+// ts_io.cu: binary PLY body pack / unpack (scene_io.py:382-455)
+void launch_ply_pack(long long n, const void* vertices, const void* sh, int is_f64, unsigned char* vout,
+                     void* fout, cudaStream_t st);
+void launch_ply_unpack(long long n_face, long long n_vertex, const unsigned char* vin, const void* fin,
+                       double sigma, int is_f64, void* vertices, void* opacity, void* sig, void* sh,
+                       unsigned long long* bad, cudaStream_t st);
+
 // ts_loss.cu: distortion loss over fragment CSR lists, fragment depth map
 size_t distortion_scratch_bytes(long long npix);
 void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,
