@@ -344,7 +344,7 @@ struct PreStage {
     float o[PRE_BLK], sg[PRE_BLK];
 };
 
-template <int NBUF, int MINB>
+template <int NBUF, int MINB, int PF = 0>
 __global__ void __launch_bounds__(PRE_BLK, MINB) k_preprocess_fast32(Cam cam, Opts opt, const float* __restrict__ verts,
                                                                const float* __restrict__ opacity,
                                                                const float* __restrict__ sigma,
@@ -396,6 +396,18 @@ __global__ void __launch_bounds__(PRE_BLK, MINB) k_preprocess_fast32(Cam cam, Op
             cp_async_wait_all();
         }
         __syncthreads();
+        if (PF > 0 && tid < 4 * PF) {  // later stages' rows on their way to L2 while this one computes
+            const int d = (it == 0 ? 1 + (tid >> 2) : PF);  // first pass: distances 1..PF, then PF
+            const long long nx = blk + (long long)d * gridDim.x;
+            if ((it == 0 || tid < 4) && nx < nblk && (nx + 1) * PRE_BLK <= n) {
+                const long long i0 = nx * PRE_BLK;
+                const int f = tid & 3;
+                if (f == 0) prefetch_l2_bulk(sh + i0 * 48, PRE_BLK * 48 * 4);
+                if (f == 1) prefetch_l2_bulk(verts + i0 * 9, PRE_BLK * 9 * 4);
+                if (f == 2) prefetch_l2_bulk(opacity + i0, PRE_BLK * 4);
+                if (f == 3) prefetch_l2_bulk(sigma + i0, PRE_BLK * 4);
+            }
+        }
         const long long i = blk * PRE_BLK + tid;
         if (i < n) {
             const PreStage& S = stage[buf];
@@ -434,7 +446,9 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
             return v ? atoi(v) : 0;
         }();
         // default: single-buffered stage, 4 CTAs per SM (other CTAs overlap each
-        // one's loads; 126 registers); 1: double-buffered, 3 CTAs; 2: single, 5 CTAs
+        // one's loads; 126 registers), the CTA's next stage bulk-prefetched into L2
+        // while it computes; 1: double-buffered, 3 CTAs; 2: single, 5 CTAs;
+        // 3: default without the L2 prefetch
         const int nbuf = variant == 1 ? 2 : 1;
         const int minb = variant == 1 ? 3 : (variant == 2 ? 5 : 4);
         const int smem = nbuf * (int)sizeof(PreStage);
@@ -448,6 +462,9 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
                                  (int)sizeof(PreStage));
             cudaFuncSetAttribute(k_preprocess_fast32<1, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(PreStage));
+            cudaFuncSetAttribute(k_preprocess_fast32<1, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(PreStage));
+
         }
         const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
         const long long grid = std::min<long long>(nblk, (long long)sms * minb);
@@ -459,8 +476,10 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
             k_preprocess_fast32<2, 3><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
         else if (minb == 5)
             k_preprocess_fast32<1, 5><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
-        else
+        else if (variant == 3)
             k_preprocess_fast32<1, 4><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
+        else
+            k_preprocess_fast32<1, 4, 1><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
     }
 }
 
