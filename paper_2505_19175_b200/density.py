@@ -76,17 +76,37 @@ def _dtype_code(soup):
     raise TypeError("DeviceSoup parameters must be float32 or float64")
 
 
+def reduce_across_ranks(max_weight, views, area, n_views: int, group=None):
+    """View-parallel statistics: each rank aggregates the views it
+    rendered; MAX of the peak weights, SUM of the covering-view counts, area
+    sums and view counts over the ranks (in place; returns the global view
+    count).  With replicated soups and identically seeded Generators every rank
+    then takes the same densify_step."""
+    import torch
+    import torch.distributed as dist
+    dist.all_reduce(max_weight, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(views, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(area, op=dist.ReduceOp.SUM, group=group)
+    nv = torch.tensor([int(n_views)], dtype=torch.int64, device=max_weight.device)
+    dist.all_reduce(nv, op=dist.ReduceOp.SUM, group=group)
+    return int(nv.item())
+
+
 class DeviceViewStats:
     """ViewStats (density.py:27-71) with the per-view arrays on the device.
-    Re-recording a view replaces its arrays and keeps its position."""
+    Re-recording a view replaces its arrays and keeps its position.  With
+    ``group`` set (torch.distributed), the aggregates and the view count are
+    reduced over the ranks, each holding the views it rendered."""
 
-    def __init__(self, n_triangles: int):
+    def __init__(self, n_triangles: int, group=None):
         self.n_triangles = int(n_triangles)
         self.per_view: dict = {}  # view id -> (max weight f32, pixel count i32, area f32, min_pixels)
+        self.group = group
+        self._views_total = None
 
     @classmethod
-    def empty(cls, n_triangles: int) -> "DeviceViewStats":
-        return cls(n_triangles)
+    def empty(cls, n_triangles: int, group=None) -> "DeviceViewStats":
+        return cls(n_triangles, group)
 
     def update(self, view_id, output, min_pixels: int = 2):
         """output: a ForwardResult (device tensors) or a RenderOutput (numpy)."""
@@ -103,7 +123,8 @@ class DeviceViewStats:
 
     @property
     def n_views(self) -> int:
-        return len(self.per_view)
+        """Views recorded (over all ranks once aggregated with a group)."""
+        return len(self.per_view) if self.group is None or self._views_total is None else self._views_total
 
     def aggregate(self, rasterizer=None, stream=None):
         """(max weight f64, covering views i32, area sum f64) device tensors."""
@@ -118,6 +139,8 @@ class DeviceViewStats:
         for k, (w, pc, ar, mp) in enumerate(self.per_view.values()):
             _lib.check(lib.ts_view_stats_accumulate(ctx, n, _vp(w), _vp(pc), _vp(ar), mp, int(k == 0), _vp(mw),
                                                     _vp(views), _vp(area), st), "view_stats_accumulate")
+        if self.group is not None:
+            self._views_total = reduce_across_ranks(mw, views, area, len(self.per_view), self.group)
         return mw, views, area
 
     def max_weight(self, **kw):
@@ -127,7 +150,7 @@ class DeviceViewStats:
         return self.aggregate(**kw)[1].to(dtype=__import__("torch").int64)
 
     def mean_area(self, **kw):
-        a = self.aggregate(**kw)[2]
+        a = self.aggregate(**kw)[2]  # (sets the global view count with a group)
         # a tensor divisor: a true division (torch turns a scalar divisor into a reciprocal product)
         return a / a.new_full(a.shape, float(max(self.n_views, 1)))
 

@@ -72,3 +72,44 @@ def test_gloo_world2_allreduce_matches_single_process(tmp_path):
     want = sum(_oracle_flat(soup, intr, poses[v], d_images[v]) for v in range(len(poses)))
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
     assert np.abs(want).max() > 0
+
+
+def _stats_worker(rank, world, port, out_path):
+    # view-parallel density statistics: rank r holds views r, r + world, ...
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import density as OD
+    from paper_2505_19175_b200.density import reduce_across_ranks
+    mw_all, pix_all, area_all = _views()
+    mine = list(range(rank, len(mw_all), world))
+    if mine:
+        mw, views, mean = OD.aggregate([(mw_all[v], pix_all[v] >= 2, area_all[v]) for v in mine])
+        area = mean * len(mine)
+    else:
+        mw, views, area = np.zeros(50), np.zeros(50, np.int64), np.zeros(50)
+    t = [torch.from_numpy(np.ascontiguousarray(a)) for a in (mw, views.astype(np.int32), area)]
+    nv = reduce_across_ranks(t[0], t[1], t[2], len(mine))
+    if rank == 0:
+        np.savez(out_path, mw=t[0].numpy(), views=t[1].numpy(), area=t[2].numpy(), nv=nv)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _views():
+    rng = np.random.default_rng(8)
+    return (np.float32(rng.uniform(0, 0.1, (5, 50))).astype(np.float64), rng.integers(0, 6, (5, 50)),
+            np.float32(rng.uniform(0, 60, (5, 50))).astype(np.float64))
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_density_stats_match_single_process(tmp_path):
+    from oracle import density as OD
+    out = str(tmp_path / "s.npz")
+    mp.spawn(_stats_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    mw_all, pix_all, area_all = _views()
+    mw, views, mean = OD.aggregate([(mw_all[v], pix_all[v] >= 2, area_all[v]) for v in range(5)])
+    assert int(got["nv"]) == 5
+    assert np.array_equal(got["mw"], mw) and np.array_equal(got["views"], views)
+    assert np.allclose(got["area"] / 5, mean, rtol=1e-14)
