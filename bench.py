@@ -280,8 +280,9 @@ def main():
         alpha_host.copy_(f.alpha_map, non_blocking=True)
         torch.cuda.current_stream().synchronize()
 
-    e2e_steps = max(3, min(args.steps, 10))
-    e2e_step()
+    e2e_steps = max(3, min(args.steps, 30))
+    for _ in range(3):
+        e2e_step()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
