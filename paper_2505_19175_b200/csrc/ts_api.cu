@@ -318,7 +318,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
     for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
-                      &c->ctot, &c->binmat, &c->lossbuf})
+                      &c->ctot, &c->binmat, &c->lossbuf, &c->densbuf})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);

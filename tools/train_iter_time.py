@@ -49,4 +49,9 @@ names = ["forward", "collect_fragments", "losses", "backward_fragments"]
 res = {n: round(ev[i].elapsed_time(ev[i + 1]), 3) for i, n in enumerate(names)}
 res["total_ms"] = round(ev[0].elapsed_time(ev[4]), 3)
 res["fragments"] = int(r.fragments().weight.numel())
+r.profile(True)
+it()
+torch.cuda.synchronize()
+res["stages_last"] = {k: round(v, 3) for k, v in r.stage_times().items() if k in ("blend_bwd", "chain_bwd")}
+r.profile(False)
 print(res)
