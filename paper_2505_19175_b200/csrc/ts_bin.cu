@@ -64,6 +64,7 @@ __device__ __forceinline__ unsigned excl_scan_256(unsigned v, unsigned* s_w, uns
 __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __restrict__ tcnt, int* __restrict__ tile_start,
                                                     long long cap, unsigned* overflow, int small_cap,
                                                     int* __restrict__ big_list, int* __restrict__ n_big) {
+    TS_PDL_ENTRY();
     __shared__ unsigned s_w[32];
     __shared__ unsigned long long s_total;
     __shared__ int s_nbig;
@@ -123,6 +124,7 @@ constexpr int BIN_MAX_TILES = 12288;       // shared-memory counters per CTA (48
 
 __global__ void __launch_bounds__(BIN_CT) k_bin_count(long long n, const short4* __restrict__ bbox, int ntx,
                                                       int ntiles, unsigned* __restrict__ mat) {
+    TS_PDL_ENTRY();
     extern __shared__ unsigned s_cnt[];
     const int t0 = blockIdx.y * BIN_MAX_TILES, nt = min(BIN_MAX_TILES, ntiles - t0);  // this CTA's tile range
     for (int t = threadIdx.x; t < nt; t += BIN_CT) s_cnt[t] = 0u;
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_count(long long n, const short4*
 // 32 consecutive tiles (lane) x 8 chunk ranges (warp): coalesced 128-byte rows.
 __global__ void __launch_bounds__(256) k_bin_cols(int nchunk, int ntiles, unsigned* __restrict__ mat,
                                                   unsigned* __restrict__ tcnt) {
+    TS_PDL_ENTRY();
     __shared__ unsigned s_part[8][33];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * 32 + (int)lane;
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(BIN_CT) k_bin_fill(long long n, const short4* 
                                                      const int* __restrict__ tile_start,
                                                      const unsigned long long* __restrict__ key64,
                                                      const Counters* __restrict__ ctr, uint2* __restrict__ bucket) {
+    TS_PDL_ENTRY();
     extern __shared__ unsigned s_cur[];
     if (tile_start[ntiles] == 0) return;  // empty (or over capacity)
     const int t0 = blockIdx.y * BIN_MAX_TILES, nt = min(BIN_MAX_TILES, ntiles - t0);  // this CTA's tile range
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
     __shared__ unsigned long long s_red[2 * BW];
     __shared__ int s_flag;
     // the long-tile kernel (independent tiles) may launch while this grid drains
-    asm volatile("griddepcontrol.launch_dependents;");
+    TS_PDL_ENTRY();
     const int t = blockIdx.x;
     const int base = tile_start[t], cnt = tile_start[t + 1] - base;
     if (cnt <= 0 || cnt > CAP) return;  // (longer tiles: k_tile_sort_big)
@@ -504,6 +508,8 @@ __global__ void __launch_bounds__(BT) k_tile_sort_big(const int* __restrict__ bi
                                                       const unsigned long long* __restrict__ key64,
                                                       unsigned* __restrict__ ent_src, unsigned* gk0, unsigned* gv0,
                                                       unsigned* gk1, unsigned* gv1, int srcbits) {
+    // waits for k_tile_sort (PDL chain: the blend after this grid waits only on it)
+    TS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned long long s_item[];  // [CAP]
     __shared__ unsigned s_hist[NB];
     __shared__ unsigned s_wc[BW][256];
@@ -610,16 +616,16 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
         attr = true;
     }
     if (n > 0) {
-        k_bin_count<<<dim3(nchunk, nrange), BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat);
-        k_bin_cols<<<(ntiles + 31) / 32, 256, 0, st>>>(nchunk, ntiles, mat, tcnt);
+        launch_pdl(k_bin_count, dim3(nchunk, nrange), dim3(BIN_CT), smem, st, n, bbox, ntx, ntiles, mat);
+        launch_pdl(k_bin_cols, dim3((ntiles + 31) / 32), dim3(256), 0, st, nchunk, ntiles, mat, tcnt);
     } else {
         cudaMemsetAsync(tcnt, 0, sizeof(unsigned) * ntiles, st);
     }
     // big_list[ntiles]: tiles longer than SORT_SMALL; its count at big_list[ntiles]
-    k_tile_scan<<<1, 1024, 0, st>>>(ntiles, tcnt, tile_start, cap, overflow, SORT_SMALL, big_list,
+    launch_pdl(k_tile_scan, dim3(1), dim3(1024), 0, st, ntiles, tcnt, tile_start, cap, overflow, SORT_SMALL, big_list,
                                     big_list + ntiles);
     if (n > 0)
-        k_bin_fill<<<dim3(nchunk, nrange), BIN_CT, smem, st>>>(n, bbox, ntx, ntiles, mat, tile_start, key64, ctr,
+        launch_pdl(k_bin_fill, dim3(nchunk, nrange), dim3(BIN_CT), smem, st, n, bbox, ntx, ntiles, mat, tile_start, key64, ctr,
                                                               bucket);
 }
 
@@ -634,7 +640,7 @@ void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2*
                     const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],
                     const int* big_list, cudaStream_t st) {
     const int srcbits = n > 1 ? 64 - __builtin_clzll((unsigned long long)(n - 1)) : 1;
-    k_tile_sort<SORT_SMALL, 4096><<<ntiles, BT, 0, st>>>(ntiles, tile_start, bucket, key64, ent_src, scratch[0],
+    launch_pdl(k_tile_sort<SORT_SMALL, 4096>, dim3(ntiles), dim3(BT), 0, st, ntiles, tile_start, bucket, key64, ent_src, scratch[0],
                                                         scratch[1], scratch[2], scratch[3], srcbits);
     // tiles above SORT_SMALL entries (dense views), listed by k_tile_scan
     static int sms = 0;
@@ -645,8 +651,8 @@ void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2*
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_tile_sort_big<SORT_BIG, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     }
-    // programmatic dependent launch: overlaps the previous kernel's last wave (the
-    // two kernels sort disjoint tiles; everything they read was written before it)
+    // programmatic dependent launch: its CTAs are scheduled during k_tile_sort's last
+    // wave and wait for that grid (TS_PDL_ENTRY), so the blend after it may rely on both
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * sms);
     cfg.blockDim = dim3(BT);

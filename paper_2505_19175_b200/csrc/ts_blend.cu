@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                                                      const unsigned* __restrict__ ent_src,
                                                      const PT* __restrict__ opacity,
                                                      const PT* __restrict__ sigma, FastBlendOut out) {
+    TS_PDL_ENTRY();
     using SM = DenseSmem<DB, PCAP, ACC64, PT>;
     using Real = typename SM::Real;
     constexpr int RR = SM::RR, SR = SM::SR, NW = SM::NW;
@@ -541,8 +542,8 @@ static void launch_dense(const Cam& cam, const Opts& opt, const RecF* rec, const
         attr = true;
     }
     const int ntiles = cam.ntx * cam.nty;
-    k_blend_dense<DB, PCAP, ACC64, PT, MINB><<<ntiles, 256, dyn, st>>>(cam, opt, rec, tile_start, ent_src, opacity, sigma,
-                                                                  out);
+    launch_pdl(k_blend_dense<DB, PCAP, ACC64, PT, MINB>, dim3(ntiles), dim3(256), dyn, st, cam, opt, rec, tile_start,
+               ent_src, opacity, sigma, out);
 }
 
 void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64, const RecF* rec,

@@ -383,3 +383,35 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) 
 
 
 }  // namespace ts
+
+// Programmatic dependent launch of the per-frame kernel chain: each kernel waits
+// for its predecessor grid to complete (griddepcontrol.wait) before touching its
+// outputs, then lets its own successor launch, so successor CTAs are scheduled
+// while this grid's last wave drains.  A no-op for kernels launched without the
+// attribute.  TS_NO_PDL=1 launches normally.
+#define TS_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#ifndef __CUDACC_RTC__
+#include <cstdlib>
+#include <utility>
+namespace ts {
+inline bool pdl_enabled() {
+    static const bool on = getenv("TS_NO_PDL") == nullptr;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+}  // namespace ts
+#endif

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(PRE_BLK, MINB) k_preprocess_fast32(Cam cam, Op
                                                                const float* __restrict__ sigma,
                                                                const float* __restrict__ sh, long long n,
                                                                FastPreOut out) {
+    TS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char s_pre[];
     PreStage* stage = reinterpret_cast<PreStage*>(s_pre);  // [NBUF]
     const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
@@ -479,7 +480,8 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
         else if (variant == 3)
             k_preprocess_fast32<1, 4><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
         else
-            k_preprocess_fast32<1, 4, 1><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
+            launch_pdl(k_preprocess_fast32<1, 4, 1>, dim3((unsigned)grid), dim3(PRE_BLK), smem, st, cam, opt, v, o, sg,
+                       sh, n, out);
     }
 }
 
@@ -1008,6 +1010,7 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                                                    const T* __restrict__ sigma, const RecF* __restrict__ rec,
                                                    const int* __restrict__ tile_start,
                                                    const unsigned* __restrict__ ent_src, FastBlendOut out) {
+    TS_PDL_ENTRY();
     __shared__ double s_a[FXC];
     __shared__ float s_c[3][FXC];
     __shared__ unsigned s_s[FXC];
@@ -1240,11 +1243,11 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
     // the whole chunk are in flight at once
     const int grid = 148 * 2;
     if (dtype == 1)
-        k_fixup_fwd<double><<<grid, FX_T, 0, st>>>(cam, opt, (const double*)soup.opacity,
-                                                  (const double*)soup.sigma, rec, tile_start, ent_src, out);
+        launch_pdl(k_fixup_fwd<double>, dim3(grid), dim3(FX_T), 0, st, cam, opt, (const double*)soup.opacity,
+                   (const double*)soup.sigma, rec, tile_start, ent_src, out);
     else
-        k_fixup_fwd<float><<<grid, FX_T, 0, st>>>(cam, opt, (const float*)soup.opacity,
-                                                 (const float*)soup.sigma, rec, tile_start, ent_src, out);
+        launch_pdl(k_fixup_fwd<float>, dim3(grid), dim3(FX_T), 0, st, cam, opt, (const float*)soup.opacity,
+                   (const float*)soup.sigma, rec, tile_start, ent_src, out);
 }
 
 // ---------------------------------------------------------------------------
