@@ -41,7 +41,7 @@ WORKLOAD = "ns"  # 2M triangles, 1280x720, sigma=1, SH degree 3, forward render
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=WORKLOAD)
@@ -93,6 +93,13 @@ class ClockSampler:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+
+    def rows_so_far(self) -> int:
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except Exception:
+            return 0
 
     def stop(self):
         if self.proc is None:
@@ -218,7 +225,9 @@ def main():
     # clocks drop before the timed frames): ~0.3 s of untimed frames
     rast.set_async(True)
     t_w = time.perf_counter()
-    while time.perf_counter() - t_w < 0.3:
+    # (and until nvidia-smi has reported twice, so the timed frames are sampled)
+    while time.perf_counter() - t_w < 0.3 or (clocks.proc is not None and clocks.rows_so_far() < 2
+                                             and time.perf_counter() - t_w < 3.0):
         for _ in range(20):
             step()
         torch.cuda.synchronize()
