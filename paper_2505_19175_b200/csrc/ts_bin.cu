@@ -18,7 +18,7 @@
 //                   triangles (and their depth keys) in arbitrary order;
 //   k_tile_sort  -- CTA per tile: the depth keys (fp64 bit patterns of the
 //                   positive centroid depth, monotone) are range-reduced to 32
-//                   bits, counting-sorted on their top 12 bits in shared memory,
+//                   bits, counting-sorted on their top 11 bits in shared memory,
 //                   and every run of equal 12-bit keys is ordered by the exact
 //                   (z, idx) pair.  Tiles longer than the shared-memory
 //                   capacity, or with long runs (equal or clustered depths), take
@@ -640,7 +640,7 @@ void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2*
                     const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],
                     const int* big_list, cudaStream_t st) {
     const int srcbits = n > 1 ? 64 - __builtin_clzll((unsigned long long)(n - 1)) : 1;
-    launch_pdl(k_tile_sort<SORT_SMALL, 4096>, dim3(ntiles), dim3(BT), 0, st, ntiles, tile_start, bucket, key64, ent_src, scratch[0],
+    launch_pdl(k_tile_sort<SORT_SMALL, 2048>, dim3(ntiles), dim3(BT), 0, st, ntiles, tile_start, bucket, key64, ent_src, scratch[0],
                                                         scratch[1], scratch[2], scratch[3], srcbits);
     // tiles above SORT_SMALL entries (dense views), listed by k_tile_scan
     static int sms = 0;
