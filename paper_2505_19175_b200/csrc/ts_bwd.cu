@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                                                             const double* __restrict__ fg_dz,
                                                             const unsigned long long* __restrict__ run_if,
                                                             double* __restrict__ sgrad) {
+    TS_PDL_ENTRY();
     if (run_if && *run_if == 0ull) return;  // the streaming backward handled this frame
     using SM = BwdSmem<DB, PCAP, GCAP>;
     constexpr int RR = SM::RR, SR = SM::SR, NW = SM::NW;
@@ -517,9 +518,8 @@ static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, c
         attr = true;
     }
     const int ntiles = cam.ntx * cam.nty;
-    k_blend_bwd_dense<DB, PCAP, GCAP, MINB><<<ntiles, 256, dyn, st>>>(cam, opt, rec, recb, tile_start, ent_src, t_final,
-                                                                 last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz,
-                                                                 run_if, sgrad);
+    launch_pdl(k_blend_bwd_dense<DB, PCAP, GCAP, MINB>, dim3(ntiles), dim3(256), dyn, st, cam, opt, rec, recb,
+               tile_start, ent_src, t_final, last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz, run_if, sgrad);
 }
 
 void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                                                     const FragRec* __restrict__ frec, const Counters* __restrict__ ctr,
                                                     unsigned long long cap, const double* __restrict__ c_total,
                                                     const float* __restrict__ d_image, double* __restrict__ sgrad) {
+    TS_PDL_ENTRY();
     if (ctr->frec_over) return;
     const unsigned long long total = ctr->n_frec;
     const long long n = (long long)(total < cap ? total : cap);
@@ -180,9 +181,8 @@ void launch_bwd_stream(const Cam& cam, const Opts& opt, const ts_soup& soup, int
                                                             (const float*)soup.sigma, frec, ctr, cap, c_total, d_image,
                                                             sgrad);
     else
-        k_bwd_stream<float, 4, float><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
-                                                           (const float*)soup.sigma, frec, ctr, cap, c_total, d_image,
-                                                           sgrad);
+        launch_pdl(k_bwd_stream<float, 4, float>, dim3(grid), dim3(256), 0, st, cam, opt, rec, recb,
+                   (const float*)soup.opacity, (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
 }
 
 }  // namespace ts

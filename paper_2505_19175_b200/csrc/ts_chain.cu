@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(CB, 8) k_chain_bwd32(Cam cam, Opts opt, const 
                                                        const unsigned* __restrict__ flag,
                                                        const double* __restrict__ sgrad, long long n,
                                                        ts_grads grads, int accumulate) {
+    TS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char s_chain[];
     ChainStage& S = *reinterpret_cast<ChainStage*>(s_chain);
     const int tid = threadIdx.x;
@@ -280,8 +281,8 @@ bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup,
         attr = true;
     }
     const unsigned grid = (unsigned)((n + CB - 1) / CB);
-    k_chain_bwd32<<<grid, CB, smem, st>>>(cam, opt, (const float*)soup.vertices, (const float*)soup.sh, flag, sgrad, n,
-                                          g, accumulate);
+    launch_pdl(k_chain_bwd32, dim3(grid), dim3(CB), smem, st, cam, opt, (const float*)soup.vertices,
+               (const float*)soup.sh, flag, sgrad, n, g, accumulate);
     return true;
 }
 
