@@ -129,6 +129,18 @@ int ts_forward(ts_context* ctx, const ts_camera* cam, const ts_options* opt, con
 int ts_set_async(ts_context* ctx, int enable);
 int ts_forward_status(ts_context* ctx, ts_forward_result* result, void* stream);
 
+/* Cross-check paths (tests): the defaults are the product path.
+ *   TS_OPT_LEGACY_BINNING  1: global depth radix sort + tile duplication + stable
+ *                          tile sort (render.py:275-277, 315-361 literally)
+ *                          instead of tile-first binning with per-tile sorts.
+ *   TS_OPT_TILE_BACKWARD   1: the tile backward (per-pixel back-to-front
+ *                          recursion, _kernels.py:245-318) instead of the
+ *                          streaming backward over the training forward's
+ *                          fragment records (it is also the automatic fallback
+ *                          when the record buffer overflows). */
+enum { TS_OPT_LEGACY_BINNING = 1, TS_OPT_TILE_BACKWARD = 2 };
+int ts_set_option(ts_context* ctx, int option, int64_t value);
+
 /* render_backward(): gradients of sum(d_image * image_unclipped) w.r.t. all
  * 59 parameters of every triangle, for the scene of the context's last
  * ts_forward (same soup/camera/options).  The soup parameter buffers passed

@@ -66,10 +66,12 @@ class TsGrads(ctypes.Structure):
 EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_version",
            "ts_forward", "ts_backward", "ts_debug_copy", "ts_launch_count", "ts_profile",
            "ts_stage_times", "ts_flagged_pixels", "ts_fragment_offsets", "ts_collect_fragments",
-           "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_photometric_loss",
+           "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_set_option", "ts_photometric_loss",
            "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
            "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack"]
+TS_OPT_LEGACY_BINNING = 1
+TS_OPT_TILE_BACKWARD = 2
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
 
 _LIB = None
@@ -111,6 +113,8 @@ def load(path: str = LIB_PATH):
     lib.ts_set_async.restype = ctypes.c_int
     lib.ts_forward_status.argtypes = [ctypes.c_void_p, P(TsForwardResult), ctypes.c_void_p]
     lib.ts_forward_status.restype = ctypes.c_int
+    lib.ts_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]
+    lib.ts_set_option.restype = ctypes.c_int
     lib.ts_debug_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                   ctypes.c_size_t, ctypes.c_void_p]
     lib.ts_debug_copy.restype = ctypes.c_int

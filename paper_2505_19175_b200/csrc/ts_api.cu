@@ -48,11 +48,15 @@ struct ts_context {
     int* rank_of = nullptr;
     double* depth = nullptr;
     short4* bbox = nullptr;
-    DevBuf rec64, recf, recb, sg64, sg32;
+    DevBuf rec64, recf, recb, recc, sg64, sg32;
     DevBuf frag_off, cs_scratch;  // expected fragment CSR offsets + scan scratch
     DevBuf frec, ctot;            // training forward: fragment records + final unclipped colour
     unsigned long long frec_cap = 0;
+    long long frec_hint = 0;      // largest fragment-record count seen (record-buffer sizing)
     bool frec_ready = false;      // the last forward wrote fragment records
+    // ts_set_option: cross-check paths for tests (defaults are the product path)
+    bool opt_legacy_binning = false;  // global depth sort + tile duplication instead of tile-first binning
+    bool opt_tile_backward = false;   // tile backward instead of the streaming backward
     // per-entry scratch
     long long cap_e = -1;
     void* ent_buf = nullptr;
@@ -120,6 +124,21 @@ static int cuda_err(cudaError_t e) {
         int _rc = cuda_err((x));      \
         if (_rc != TS_OK) return _rc; \
     } while (0)
+
+// Every entry point runs on the context's device and restores the caller's
+// current device afterwards (torch keeps its own notion of the current device).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const ts_context* c) {
+        if (!c) return;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -281,7 +300,15 @@ const char* ts_error_string(int code) {
 
 int ts_context_create(ts_context** out, int device) {
     if (!out) return TS_ERR_INVALID_ARG;
+    int prev_device = -1;
+    cudaGetDevice(&prev_device);
     TS_CHECK(cudaSetDevice(device));
+    struct Restore {
+        int d;
+        ~Restore() {
+            if (d >= 0) cudaSetDevice(d);
+        }
+    } restore{prev_device};
     ts_context* c = new ts_context();
     c->device = device;
     c->sort.max_blocks = 1184;  // 8 x 148 SMs
@@ -313,11 +340,12 @@ int ts_context_create(ts_context** out, int device) {
 }
 
 int ts_context_destroy(ts_context* c) {
+    DeviceGuard device_guard(c);
     if (!c) return TS_OK;
     cudaFree(c->tri_buf);
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
-    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
+    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
                       &c->ctot, &c->binmat, &c->lossbuf, &c->densbuf})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
@@ -338,6 +366,7 @@ int ts_context_destroy(ts_context* c) {
 int64_t ts_launch_count(ts_context*) { return g_launches.load(); }
 
 int ts_profile(ts_context* c, int enable) {
+    DeviceGuard device_guard(c);
     if (!c) return TS_ERR_INVALID_ARG;
     if (enable && !c->ev[0][0])
         for (int k = 0; k < TS_NUM_STAGES; k++) {
@@ -349,6 +378,7 @@ int ts_profile(ts_context* c, int enable) {
 }
 
 int ts_stage_times(ts_context* c, float* ms, int n) {
+    DeviceGuard device_guard(c);
     if (!c || !ms) return TS_ERR_INVALID_ARG;
     for (int k = 0; k < n && k < TS_NUM_STAGES; k++) {
         ms[k] = 0.f;
@@ -391,8 +421,7 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
     // (the sort grids follow it); more entries raise the sticky overflow flag
     const long long wcap = c->e_hint > 0 ? std::min<long long>(c->cap_e, c->e_hint + c->e_hint / 4 + 4096)
                                          : c->cap_e;
-    static const bool bin_legacy = getenv("TS_BIN_LEGACY") != nullptr;
-    if (n > 0 && !bin_legacy && ntiles <= bin_max_tiles()) {
+    if (n > 0 && !c->opt_legacy_binning && ntiles <= bin_max_tiles()) {
         stage_begin(c, TS_STAGE_BINNING, st);
         bin_tiles_fill(n, c->bbox, c->key, cm.ntx, ntiles, c->tcnt, (unsigned*)c->binmat.p, c->tile_start,
                        c->bucket, c->d_ctr, wcap, c->d_sticky, c->big_list, st);
@@ -434,20 +463,16 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
         FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
                         c->nfrag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
                         c->flags, c->d_ctr};
-        static const bool no_stream = getenv("TS_BWD_TILES") != nullptr;
-        if (opt->keep_backward && !no_stream && c->frec.p) {
-            bo.frec = (FragRec*)c->frec.p;
-            bo.frec_cap = c->frec_cap;
-            bo.c_total64 = (double*)c->ctot.p;
+        if (opt->keep_backward) {
+            bo.recc = (const RecC*)c->recc.p;
+            if (!c->opt_tile_backward && c->frec.p) {
+                bo.frec = (FragRec*)c->frec.p;
+                bo.frec_cap = c->frec_cap;
+                bo.c_total64 = (double*)c->ctot.p;
+            }
         }
         stage_begin(c, TS_STAGE_BLEND, st);
-        static const bool legacy = getenv("TS_BLEND_LEGACY") != nullptr;
-        if (legacy)
-            launch_blend_fast(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
-                              c->bbox, c->tile_start, c->ent_src, bo, st);
-        else
-            launch_blend_dense(cm, op, *soup, opt->param_dtype, opt->keep_backward != 0, (const RecF*)c->recf.p,
-                               c->tile_start, c->ent_src, bo, st);
+        launch_blend_dense(cm, op, opt->keep_backward != 0, (const RecF*)c->recf.p, c->tile_start, c->ent_src, bo, st);
         stage_end(c, TS_STAGE_BLEND, st);
         stage_begin(c, TS_STAGE_FIXUP, st);
         launch_fixup_fwd(cm, op, *soup, opt->param_dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src,
@@ -489,6 +514,7 @@ static int finish_forward(ts_context* c, ts_forward_result* res, bool validate) 
 
 int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const ts_soup* soup,
                const ts_forward_out* out, ts_forward_result* res, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !cam || !opt || !soup || !out) return TS_ERR_INVALID_ARG;
     if (opt->tile_size != TILE) return TS_ERR_TILE_SIZE;
     if (cam->width < 1 || cam->height < 1 || soup->n < 0 || opt->sh_degree < 0 || opt->sh_degree > 3)
@@ -512,6 +538,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     if (fast) {
         if ((rc = ensure(c->recf, sizeof(RecF) * n1))) return rc;
         if (opt->keep_backward && (rc = ensure(c->recb, sizeof(RecB) * n1))) return rc;
+        if (opt->keep_backward && (rc = ensure(c->recc, sizeof(RecC) * n1))) return rc;
     } else {
         if ((rc = ensure(c->rec64, sizeof(Rec64) * n1))) return rc;
     }
@@ -521,8 +548,10 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     if ((rc = ensure(c->binmat, bin_matrix_bytes(n1, cm.ntx * cm.nty)))) return rc;
     c->frec_ready = false;
     if (fast && opt->keep_backward) {
-        // fragment records of the training forward (~6.5 per tile entry here)
-        const long long want = std::max<long long>(8 * std::max<long long>(c->e_hint, n1), 1ll << 20);
+        // fragment records of the training forward (~6.5 per tile entry here; the
+        // largest count seen with headroom once one frame has run)
+        const long long want = c->frec_hint > 0 ? c->frec_hint + c->frec_hint / 4 + 4096
+                                                : std::max<long long>(8 * std::max<long long>(c->e_hint, n1), 1ll << 20);
         if ((rc = ensure(c->frec, sizeof(FragRec) * (size_t)want))) return rc;
         c->frec_cap = c->frec.bytes / sizeof(FragRec);
         if ((rc = ensure(c->ctot, sizeof(double) * 3 * (size_t)P))) return rc;
@@ -534,7 +563,8 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
     }
     stage_begin(c, TS_STAGE_PREPROCESS, st);
     if (fast) {
-        FastPreOut po{(RecF*)c->recf.p, opt->keep_backward ? (RecB*)c->recb.p : nullptr, c->bbox, c->key,
+        FastPreOut po{(RecF*)c->recf.p, opt->keep_backward ? (RecB*)c->recb.p : nullptr,
+                      opt->keep_backward ? (RecC*)c->recc.p : nullptr, c->bbox, c->key,
                       c->tcount, c->flag, out->area, nullptr, c->d_ctr, out->max_weight, out->pixel_count};
         launch_preprocess_fast(cm, op, *soup, opt->param_dtype, po, st);
     } else {
@@ -549,7 +579,7 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     c->have_fwd = true;
     c->have_bwd_state = !fast || opt->keep_backward;
-    c->frec_ready = fast && opt->keep_backward && getenv("TS_BWD_TILES") == nullptr;
+    c->frec_ready = fast && opt->keep_backward && !c->opt_tile_backward;
     c->precision = opt->precision;
     c->cam = cm;
     c->opt = op;
@@ -564,13 +594,22 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         return TS_OK;
     }
     TS_CHECK(cudaStreamSynchronize(st));
-    if (c->h_ctr->e > (unsigned long long)c->wcap) {
+    if (c->frec_ready) c->frec_hint = std::max<long long>(c->frec_hint, (long long)c->h_ctr->n_frec);
+    const bool e_over = c->h_ctr->e > (unsigned long long)c->wcap;
+    const bool f_over = c->frec_ready && c->h_ctr->frec_over;
+    if (e_over || f_over) {
         TS_CHECK(cudaMemsetAsync(c->d_sticky, 0, sizeof(unsigned), st));
-        // more tile entries than the capacity: grow and redo binning + blend
+        // more tile entries than the capacity, or more fragment records than the
+        // record buffer (first training frame of a scene): grow and redo binning + blend
         const long long e = (long long)c->h_ctr->e;
         c->e_hint = std::max(c->e_hint, e);
         if ((rc = ensure_ent(c, e + e / 4 + 4096))) return rc;
         if ((rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1))) return rc;
+        if (f_over) {
+            const long long f = c->frec_hint;
+            if ((rc = ensure(c->frec, sizeof(FragRec) * (size_t)(f + f / 4 + 4096)))) return rc;
+            c->frec_cap = c->frec.bytes / sizeof(FragRec);
+        }
         // n_flagged, n_frec, frec_over
         TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, 3 * sizeof(unsigned long long), st));
         if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
@@ -579,16 +618,24 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         TS_CHECK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
         TS_CHECK(cudaStreamSynchronize(st));
     }
-    return finish_forward(c, res, opt->validate != 0);
+    rc = finish_forward(c, res, opt->validate != 0);
+    if (rc) {  // a failed frame leaves no state a backward could read
+        c->have_fwd = false;
+        c->have_bwd_state = false;
+        c->frec_ready = false;
+    }
+    return rc;
 }
 
 int ts_set_async(ts_context* c, int enable) {
+    DeviceGuard device_guard(c);
     if (!c) return TS_ERR_INVALID_ARG;
     c->async_mode = enable != 0;
     return TS_OK;
 }
 
 int ts_forward_status(ts_context* c, ts_forward_result* res, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     cudaStream_t st = (cudaStream_t)stream;
@@ -597,14 +644,32 @@ int ts_forward_status(ts_context* c, ts_forward_result* res, void* stream) {
     TS_CHECK(cudaMemcpyAsync(&sticky, c->d_sticky, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     TS_CHECK(cudaStreamSynchronize(st));
     c->pending = false;
+    if (c->frec_ready) c->frec_hint = std::max<long long>(c->frec_hint, (long long)c->h_ctr->n_frec);
     if (sticky) {
         TS_CHECK(cudaMemsetAsync(c->d_sticky, 0, sizeof(unsigned), st));
         finish_forward(c, res, false);
         // the next forward sizes its entry buffer from the largest count seen
         c->e_hint = std::max<long long>(c->e_hint, c->e) * 2;
+        c->have_bwd_state = false;
+        c->frec_ready = false;
         return TS_ERR_CAPACITY;
     }
-    return finish_forward(c, res, c->last_validate);
+    const int rc = finish_forward(c, res, c->last_validate);
+    if (rc) {
+        c->have_bwd_state = false;
+        c->frec_ready = false;
+    }
+    return rc;
+}
+
+int ts_set_option(ts_context* c, int option, int64_t value) {
+    DeviceGuard device_guard(c);
+    if (!c) return TS_ERR_INVALID_ARG;
+    switch (option) {
+        case TS_OPT_LEGACY_BINNING: c->opt_legacy_binning = value != 0; return TS_OK;
+        case TS_OPT_TILE_BACKWARD: c->opt_tile_backward = value != 0; return TS_OK;
+        default: return TS_ERR_INVALID_ARG;
+    }
 }
 
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
@@ -612,6 +677,7 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
 
 int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream) {
+    DeviceGuard device_guard(c);
     return backward_impl(c, d_image, grads, accumulate, nullptr, nullptr, nullptr, stream);
 }
 
@@ -631,6 +697,7 @@ static int fragment_offsets(ts_context* c, cudaStream_t st, long long* total) {
 }
 
 int ts_fragment_offsets(ts_context* c, int64_t* offsets, int64_t* n_fragments, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !n_fragments) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     cudaStream_t st = (cudaStream_t)stream;
@@ -646,6 +713,7 @@ int ts_fragment_offsets(ts_context* c, int64_t* offsets, int64_t* n_fragments, v
 
 int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangle, double* weight, double* depth,
                          void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !offsets || !triangle || !weight || !depth) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     if (c->precision != 0) return TS_ERR_INVALID_ARG;  // fragment lists come from the fast path's fp64 replay
@@ -666,8 +734,8 @@ int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangl
     bo.frag_w = weight;
     bo.frag_z = depth;
     bo.zkey = c->key;
-    launch_blend_fast(c->cam, c->opt, c->soup, c->dtype, true, (const RecF*)c->recf.p, c->bbox, c->tile_start,
-                      c->ent_src, bo, st);
+    launch_blend_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, c->bbox, c->tile_start, c->ent_src,
+                      bo, st);
     launch_fixup_fwd(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src, bo, st);
     g_launches += 2;
     return cuda_err(cudaGetLastError());
@@ -675,6 +743,7 @@ int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangl
 
 int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* offsets, const double* d_weight,
                           const double* d_depth, const ts_grads* grads, int accumulate, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !d_image || !grads || !offsets || !d_weight || !d_depth) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
@@ -710,22 +779,19 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
         double* sg = (double*)c->sg64.p;
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
         if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
-        static const bool bwd_legacy = getenv("TS_BWD_LEGACY") != nullptr;
-        if (c->frec_ready && !frag_off && !bwd_legacy) {
+        if (c->frec_ready && !frag_off) {
             // streaming backward over the forward's fragment records; the tile
             // backward runs instead only if the record buffer overflowed
-            launch_bwd_stream(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
+            launch_bwd_stream(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, (const RecC*)c->recc.p,
                               (const FragRec*)c->frec.p, c->d_ctr, c->frec_cap, (const double*)c->ctot.p, d_image,
                               sg, st);
-            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, c->tile_start,
+            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
+                                   (const RecC*)c->recc.p, c->tile_start,
                                    c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, nullptr, nullptr, nullptr,
                                    &c->d_ctr->frec_over, sg, st);
-        } else if (bwd_legacy && !frag_off)
-            launch_blend_bwd_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p,
-                                  (const RecB*)c->recb.p, c->tile_start, c->ent_src, c->t_final, c->last_pos,
-                                  d_image, sg, st);
-        else
-            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, c->tile_start,
+        } else
+            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
+                                   (const RecC*)c->recc.p, c->tile_start,
                                    c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
                                    nullptr, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
@@ -754,6 +820,7 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
 
 int ts_photometric_loss(ts_context* c, const float* rendered, const float* target, int height, int width,
                         double lambda_dssim, double* out, float* d_image, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !rendered || !target || !out || height < 1 || width < 1) return TS_ERR_INVALID_ARG;
     int rc;
     if ((rc = ensure(c->lossbuf, photometric_scratch_bytes(height, width)))) return rc;
@@ -766,6 +833,7 @@ int ts_photometric_loss(ts_context* c, const float* rendered, const float* targe
 int ts_distortion_loss(ts_context* c, const int64_t* offsets, const double* weight, const double* depth,
                        int64_t n_pixels, int64_t image_size, double* out, double* d_weight, double* d_depth,
                        void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !offsets || !out || n_pixels < 0) return TS_ERR_INVALID_ARG;
     int rc;
     if ((rc = ensure(c->lossbuf, distortion_scratch_bytes(n_pixels)))) return rc;
@@ -779,6 +847,7 @@ int ts_distortion_loss(ts_context* c, const int64_t* offsets, const double* weig
 int ts_normal_loss(ts_context* c, const float* vertices, int64_t n, const int64_t* offsets,
                    const int32_t* triangle, const double* weight, int64_t n_fragments, const double* depth,
                    const ts_camera* cam, double* out, double* d_vertices, double* d_weight, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !cam || !out || n < 0 || n_fragments < 0 || !offsets || !depth) return TS_ERR_INVALID_ARG;
     if ((n > 0 && !vertices) || (n_fragments > 0 && (!triangle || !weight))) return TS_ERR_INVALID_ARG;
     const long long npix = (long long)cam->width * cam->height;
@@ -795,6 +864,7 @@ int ts_normal_loss(ts_context* c, const float* vertices, int64_t n, const int64_
 
 int ts_fragment_depth(ts_context* c, const int64_t* offsets, const double* weight, const double* depth,
                       int64_t n_pixels, double* out_depth, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !offsets || !out_depth || n_pixels < 0) return TS_ERR_INVALID_ARG;
     launch_fragment_depth(n_pixels, (const long long*)offsets, weight, depth, out_depth, (cudaStream_t)stream);
     g_launches += n_pixels > 0 ? 1 : 0;
@@ -804,6 +874,7 @@ int ts_fragment_depth(ts_context* c, const int64_t* offsets, const double* weigh
 int ts_adam_step(ts_context* c, float* vertices, float* opacity, float* sigma, float* sh, int64_t n,
                  const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
                  void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !grads || !lrs || !bad || n < 0 || t < 1) return TS_ERR_INVALID_ARG;
     if (n > 0 && (!vertices || !opacity || !sigma || !sh || !m || !v)) return TS_ERR_INVALID_ARG;
     float* const params[4] = {vertices, opacity, sigma, sh};
@@ -817,6 +888,7 @@ int ts_adam_step(ts_context* c, float* vertices, float* opacity, float* sigma, f
 int ts_view_stats_accumulate(ts_context* c, int64_t n, const float* max_weight, const int32_t* pixel_count,
                              const float* area, int min_pixels, int first, double* acc_max_weight,
                              int32_t* acc_views, double* acc_area, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n < 0) return TS_ERR_INVALID_ARG;
     if (n > 0 && (!max_weight || !pixel_count || !area || !acc_max_weight || !acc_views || !acc_area))
         return TS_ERR_INVALID_ARG;
@@ -829,6 +901,7 @@ int ts_view_stats_accumulate(ts_context* c, int64_t n, const float* max_weight, 
 int ts_prune_mark(ts_context* c, int64_t n, const double* acc_max_weight, const int32_t* acc_views,
                   const void* opacity, int dtype, double tau_prune, int min_views, double opacity_dead,
                   uint8_t* flags, int64_t* kept, int64_t* n_kept, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n < 0 || !n_kept || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
     if (n > 0 && (!acc_max_weight || !acc_views || !opacity || !flags || !kept)) return TS_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
@@ -841,6 +914,7 @@ int ts_prune_mark(ts_context* c, int64_t n, const double* acc_max_weight, const 
 int ts_sample_candidates(ts_context* c, int64_t n_pool, const int64_t* pool, const int64_t* kept,
                          const void* param, int dtype, int criterion, const double* exponential, int64_t count,
                          int64_t* picked, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n_pool < 0 || count < 0 || count > n_pool || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
     if (criterion != TS_SAMPLE_INVERSE_SIGMA && criterion != TS_SAMPLE_OPACITY) return TS_ERR_INVALID_ARG;
     if (count == 0) return TS_OK;
@@ -858,6 +932,7 @@ int ts_sample_candidates(ts_context* c, int64_t n_pool, const int64_t* pool, con
 int ts_pick_info(ts_context* c, int64_t count, const int64_t* picked, const int64_t* pool, const int64_t* kept,
                  const double* acc_area, int64_t n_views, const void* vertices, int dtype, int64_t* source,
                  double* mean_area, uint8_t* degenerate, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || count < 0 || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
     if (count > 0 && (!picked || !acc_area || !vertices || !source || !mean_area || !degenerate))
         return TS_ERR_INVALID_ARG;
@@ -869,6 +944,7 @@ int ts_pick_info(ts_context* c, int64_t count, const int64_t* picked, const int6
 
 int ts_gather_rows(ts_context* c, int64_t n_out, const int64_t* origin, const void* src, void* dst, int width,
                    int elem_bytes, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n_out < 0 || width < 0 || (elem_bytes != 4 && elem_bytes != 8)) return TS_ERR_INVALID_ARG;
     if (n_out > 0 && width > 0 && (!origin || !src || !dst)) return TS_ERR_INVALID_ARG;
     launch_gather_rows(n_out, (const long long*)origin, src, dst, width, elem_bytes, (cudaStream_t)stream);
@@ -879,6 +955,7 @@ int ts_gather_rows(ts_context* c, int64_t n_out, const int64_t* origin, const vo
 int ts_child_vertices(ts_context* c, int64_t n_child, const int64_t* parent, const int32_t* code,
                       const double* uniforms, double max_noise_factor, const void* src_vertices, void* dst_vertices,
                       int dtype, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n_child < 0 || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
     if (n_child > 0 && (!parent || !code || !src_vertices || !dst_vertices)) return TS_ERR_INVALID_ARG;
     launch_child_vertices(n_child, (const long long*)parent, code, uniforms, max_noise_factor, src_vertices,
@@ -890,6 +967,7 @@ int ts_child_vertices(ts_context* c, int64_t n_child, const int64_t* parent, con
 // ---------------- model I/O: binary PLY body (scene_io.py:382-455) ----------------
 int ts_ply_pack(ts_context* c, const void* vertices, const void* sh, int dtype, int64_t n, uint8_t* vertex_bytes,
                 void* face_bytes, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n < 0 || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
     if (n > 0 && (!vertices || !sh || !vertex_bytes || !face_bytes)) return TS_ERR_INVALID_ARG;
     if (n > (1LL << 31) / 3) return TS_ERR_CAPACITY;  // int32 vertex indices
@@ -902,6 +980,7 @@ int ts_ply_pack(ts_context* c, const void* vertices, const void* sh, int dtype, 
 int ts_ply_unpack(ts_context* c, const uint8_t* vertex_bytes, int64_t n_vertex, const void* face_bytes,
                   int64_t n_face, double sigma, int dtype, void* vertices, void* opacity, void* sigma_out, void* sh,
                   uint64_t* bad, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || n_vertex < 0 || n_face < 0 || !bad || (dtype != 0 && dtype != 1)) return TS_ERR_INVALID_ARG;
     if (n_face > 0 && (!vertex_bytes || !face_bytes || !vertices || !opacity || !sigma_out || !sh))
         return TS_ERR_INVALID_ARG;
@@ -913,6 +992,7 @@ int ts_ply_unpack(ts_context* c, const uint8_t* vertex_bytes, int64_t n_vertex, 
 }
 
 int ts_ssim(ts_context* c, const float* x, const float* y, int height, int width, double* out, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !x || !y || !out || height < 1 || width < 1) return TS_ERR_INVALID_ARG;
     int rc;
     if ((rc = ensure(c->lossbuf, photometric_scratch_bytes(height, width)))) return rc;
@@ -922,6 +1002,7 @@ int ts_ssim(ts_context* c, const float* x, const float* y, int height, int width
 }
 
 int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream) {
+    DeviceGuard device_guard(c);
     if (!c || !dst) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     cudaStream_t st = (cudaStream_t)stream;
@@ -992,6 +1073,7 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
 }
 
 int ts_flagged_pixels(ts_context* c, int64_t* n_flagged) {
+    DeviceGuard device_guard(c);
     if (!c || !n_flagged) return TS_ERR_INVALID_ARG;
     *n_flagged = (int64_t)c->h_ctr->n_flagged;
     return TS_OK;

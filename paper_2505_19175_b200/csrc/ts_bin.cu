@@ -609,12 +609,8 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
     const int nchunk = (int)((n + BIN_CHUNK - 1) / BIN_CHUNK);
     const int nrange = (ntiles + BIN_MAX_TILES - 1) / BIN_MAX_TILES;  // tile ranges (grid y)
     const int smem = (nrange > 1 ? BIN_MAX_TILES : ntiles) * (int)sizeof(unsigned);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bin_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BIN_MAX_TILES);
-        cudaFuncSetAttribute(k_bin_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * BIN_MAX_TILES);
-        attr = true;
-    }
+    smem_optin((const void*)k_bin_count, 4 * BIN_MAX_TILES);
+    smem_optin((const void*)k_bin_fill, 4 * BIN_MAX_TILES);
     if (n > 0) {
         launch_pdl(k_bin_count, dim3(nchunk, nrange), dim3(BIN_CT), smem, st, n, bbox, ntx, ntiles, mat);
         launch_pdl(k_bin_cols, dim3((ntiles + 31) / 32), dim3(256), 0, st, nchunk, ntiles, mat, tcnt);
@@ -643,14 +639,9 @@ void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2*
     launch_pdl(k_tile_sort<SORT_SMALL, 2048>, dim3(ntiles), dim3(BT), 0, st, ntiles, tile_start, bucket, key64, ent_src, scratch[0],
                                                         scratch[1], scratch[2], scratch[3], srcbits);
     // tiles above SORT_SMALL entries (dense views), listed by k_tile_scan
-    static int sms = 0;
+    const int sms = sm_count();
     const int smem = SORT_BIG * (int)sizeof(unsigned long long);
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_tile_sort_big<SORT_BIG, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    }
+    smem_optin((const void*)k_tile_sort_big<SORT_BIG, 4096>, smem);
     // programmatic dependent launch: its CTAs are scheduled during k_tile_sort's last
     // wave and wait for that grid (TS_PDL_ENTRY), so the blend after it may rely on both
     cudaLaunchConfig_t cfg = {};

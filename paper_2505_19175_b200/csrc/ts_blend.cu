@@ -40,13 +40,13 @@ constexpr float T_MIN_F = 1e-4f;
 constexpr float ALPHA_CLAMP_F = 0.99f;
 }  // namespace
 
-template <int DB, int PCAP, bool ACC64, typename PT>
+template <int DB, int PCAP, bool ACC64>
 struct DenseSmem {
     static constexpr int RR = 2 * DB, SR = 4 * DB, NW = DB / 32;
     using Real = typename std::conditional<ACC64, double, float>::type;
     EvalRec ev[RR];
     TailRec tail[RR];
-    PT os[ACC64 ? RR : 1][2];      // exact (opacity, sigma) of the ring slots (training forwards)
+    RecC rc[ACC64 ? RR : 1];       // training forwards: fp64 colour, opacity, sigma of the ring slots
     Real r[PCAP];                  // per pair: render: alpha (clamped); training: r; NaN = inside the band
     float ea[ACC64 ? 1 : PCAP];    // render: relative error bound of the fp32 alpha
     unsigned mask[NW][256];        // per pixel: bit j = entry j passes (r >= r_lo)
@@ -60,7 +60,6 @@ struct DenseSmem {
     unsigned ein[DB];              // per entry: inclusive (pairs<<16 | segments) within its warp
     unsigned wtot[8];              // per warp: (pairs<<16 | segments) of its 8 entries
     int total;                     // pairs of the batch
-    double2 osj[ACC64 ? DB : 1];   // (opacity, sigma) of batch entry j
     unsigned pbits[ACC64 ? PCAP / 32 : 1];      // training: pair k passes (record slots)
     int wpre[ACC64 ? PCAP / 32 + 1 : 1];        // passing pairs before word w
     unsigned long long rbase;                   // first record of the batch (~0: none)
@@ -69,14 +68,12 @@ struct DenseSmem {
     double xc[TILE], yc[TILE];     // pixel centres of the tile (fp64)
 };
 
-template <int DB, int PCAP, bool ACC64, typename PT, int MINB>
+template <int DB, int PCAP, bool ACC64, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                      const int* __restrict__ tile_start,
-                                                     const unsigned* __restrict__ ent_src,
-                                                     const PT* __restrict__ opacity,
-                                                     const PT* __restrict__ sigma, FastBlendOut out) {
+                                                     const unsigned* __restrict__ ent_src, FastBlendOut out) {
     TS_PDL_ENTRY();
-    using SM = DenseSmem<DB, PCAP, ACC64, PT>;
+    using SM = DenseSmem<DB, PCAP, ACC64>;
     using Real = typename SM::Real;
     constexpr int RR = SM::RR, SR = SM::SR, NW = SM::NW;
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -111,15 +108,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
         if (q < 6) cp_async16(reinterpret_cast<float4*>(&sm.ev[slot]) + q, g);
         else cp_async16(reinterpret_cast<float4*>(&sm.tail[slot]) + (q - 6), g);
         if constexpr (ACC64) {
-            if (q == 0) {
-                if constexpr (sizeof(PT) == 8) {
-                    cp_async8(&sm.os[slot][0], opacity + src);
-                    cp_async8(&sm.os[slot][1], sigma + src);
-                } else {
-                    cp_async4(&sm.os[slot][0], opacity + src);
-                    cp_async4(&sm.os[slot][1], sigma + src);
-                }
-            }
+            if (q < 3) cp_async16(reinterpret_cast<double2*>(&sm.rc[slot]) + q, reinterpret_cast<const double2*>(out.recc + src) + q);
         }
     };
     // prologue: ids of [s, s+3DB), then records of [s, s+DB)
@@ -171,8 +160,6 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 if (q == 0) {
                     sm.col[j] = make_float4(t0.z, t0.w, __int_as_float(t1.x), t0.x);
                     sm.f1[j] = t0.y;
-                    if constexpr (ACC64)
-                        sm.osj[j] = make_double2(opt.solid ? 1.0 : (double)sm.os[slot][0], (double)sm.os[slot][1]);
                 }
                 if (cy0 + q <= cy1 && cx0 <= cx1) {
                     const EvalRec& R = sm.ev[slot];
@@ -426,7 +413,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                     float wout;
                     if constexpr (ACC64) {
                         // the reference's alpha (_kernels.py:43-56) and transmittance in fp64
-                        const double2 os = sm.osj[j];
+                        const RecC& rcj = sm.rc[(b + j) & (RR - 1)];
+                        const double2 os = make_double2(rcj.opa, rcj.sig);
                         double a;
                         if (mode == 0) {
                             const double rc = fmin((double)rv, 1.0);
@@ -454,9 +442,9 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                             reinterpret_cast<uint4*>(fr + 1)[0] =
                                 make_uint4((unsigned)(py * cam.width + px), sm.srcq[(b + j) & (SR - 1)], (unsigned)cnt, 0u);
                         }
-                        C0 += wd64 * col.x;
-                        C1 += wd64 * col.y;
-                        C2 += wd64 * col.z;
+                        C0 += wd64 * rcj.rgb[0];
+                        C1 += wd64 * rcj.rgb[1];
+                        C2 += wd64 * rcj.rgb[2];
                         last = b + j;
                         cnt++;
                         T = tn;
@@ -531,41 +519,22 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
     }
 }
 
-template <int DB, int PCAP, bool ACC64, typename PT, int MINB = 1>
+template <int DB, int PCAP, bool ACC64, int MINB>
 static void launch_dense(const Cam& cam, const Opts& opt, const RecF* rec, const int* tile_start,
-                         const unsigned* ent_src, const PT* opacity, const PT* sigma, const FastBlendOut& out,
-                         cudaStream_t st) {
-    const int dyn = (int)sizeof(DenseSmem<DB, PCAP, ACC64, PT>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_blend_dense<DB, PCAP, ACC64, PT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-        attr = true;
-    }
-    const int ntiles = cam.ntx * cam.nty;
-    launch_pdl(k_blend_dense<DB, PCAP, ACC64, PT, MINB>, dim3(ntiles), dim3(256), dyn, st, cam, opt, rec, tile_start,
-               ent_src, opacity, sigma, out);
+                         const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st) {
+    const int dyn = (int)sizeof(DenseSmem<DB, PCAP, ACC64>);
+    smem_optin((const void*)k_blend_dense<DB, PCAP, ACC64, MINB>, dyn);
+    launch_pdl(k_blend_dense<DB, PCAP, ACC64, MINB>, dim3(cam.ntx * cam.nty), dim3(256), dyn, st, cam, opt, rec,
+               tile_start, ent_src, out);
 }
 
-void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64, const RecF* rec,
-                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st) {
-    if (dtype == 1) {
-        const double* o = (const double*)soup.opacity;
-        const double* sg = (const double*)soup.sigma;
-        if (acc64) launch_dense<64, 2048, true, double, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 2048, false, double, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-    } else {
-        const float* o = (const float*)soup.opacity;
-        const float* sg = (const float*)soup.sigma;
-        static const int variant = [] {
-            const char* v = getenv("TS_DENSE_VARIANT");
-            return v ? atoi(v) : 0;
-        }();
-        // render and training: 4 CTAs per SM (64 registers, no spills; 5 at 48 spills)
-        if (acc64) launch_dense<64, 2048, true, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else if (variant == 1) launch_dense<64, 4096, false, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else if (variant == 2) launch_dense<64, 2048, false, float, 5>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-        else launch_dense<64, 2048, false, float, 4>(cam, opt, rec, tile_start, ent_src, o, sg, out, st);
-    }
+// render forwards (fp32 compositing with the guard band) and training forwards
+// (fp64 alpha / transmittance with the RecC colours, fragment records): 4 CTAs
+// per SM (64 registers, no spills; 5 at 48 registers spill)
+void launch_blend_dense(const Cam& cam, const Opts& opt, bool acc64, const RecF* rec, const int* tile_start,
+                        const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st) {
+    if (acc64) launch_dense<64, 2048, true, 4>(cam, opt, rec, tile_start, ent_src, out, st);
+    else launch_dense<64, 2048, false, 4>(cam, opt, rec, tile_start, ent_src, out, st);
 }
 
 }  // namespace ts

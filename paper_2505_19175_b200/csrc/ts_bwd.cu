@@ -48,13 +48,13 @@ struct BwdSmem {
     EvalRec ev[RR];
     TailRec tail[RR];
     RecB rb[RR];
+    RecC rc[RR];                 // fp64 colour, opacity, sigma
     double al[PCAP];             // per pair: unclamped alpha (fp64)
     float r[PCAP];               // per pair: r (edge in the low 2 bits)
     BwdSlot slot[GCAP];
     unsigned mask[NW][256];      // per pixel: bit jj = entry jj composited
     unsigned srcq[SR];
-    float4 col[DB];              // rgb, f0
-    float4 par[DB];              // opacity, sigma, 1/opacity, 1/phi_s
+    double4 par[DB];             // opacity, sigma, 1/opacity, 1/phi_s (fp64)
     int S[DB + 1];
     unsigned starts[PCAP / 32];  // bit (k & 31) of word k >> 5: an entry starts at pair k
     int jfirst[PCAP / 32];       // entry holding pair 32 w
@@ -71,6 +71,7 @@ struct BwdSmem {
 template <int DB, int PCAP, int GCAP, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                             const RecB* __restrict__ recb,
+                                                            const RecC* __restrict__ recc,
                                                             const int* __restrict__ tile_start,
                                                             const unsigned* __restrict__ ent_src,
                                                             const double* __restrict__ t_final,
@@ -134,7 +135,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
     const int hi = sm.hi;
     if (hi < s) return;
 
-    auto fetch_rec = [&](int p, int q) {  // 16-byte chunk q of (RecF, RecB) at list position p
+    constexpr int NCH = 19;  // 16-byte chunks per entry: RecF 8, RecB 8, RecC 3
+    auto fetch_rec = [&](int p, int q) {  // 16-byte chunk q of (RecF, RecB, RecC) at list position p
         const unsigned src = sm.srcq[p & (SR - 1)];
         const int slot = p & (RR - 1);
         if (q < 6)
@@ -142,9 +144,12 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
         else if (q < 8)
             cp_async16(reinterpret_cast<float4*>(&sm.tail[slot]) + (q - 6),
                        reinterpret_cast<const float4*>(rec + src) + q);
-        else
+        else if (q < 16)
             cp_async16(reinterpret_cast<float4*>(&sm.rb[slot]) + (q - 8),
                        reinterpret_cast<const float4*>(recb + src) + (q - 8));
+        else
+            cp_async16(reinterpret_cast<float4*>(&sm.rc[slot]) + (q - 16),
+                       reinterpret_cast<const float4*>(recc + src) + (q - 16));
     };
     auto rank = [&](int k) {  // composited pairs before pair k
         const int wi = k >> 5;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
-    for (int c = tid; c < (hi + 1 - rlo) * 16; c += 256) fetch_rec(rlo + (c >> 4), c & 15);
+    for (int c = tid; c < (hi + 1 - rlo) * NCH; c += 256) fetch_rec(rlo + c / NCH, c % NCH);
     cp_async_commit();
 
     int nb = 0;
@@ -183,7 +188,6 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                 cx0[hf] = cy0[hf] = w[hf] = h[hf] = 0;
                 if (valid[hf]) {
                     const int slot = (bend - 1 - jj) & (RR - 1);
-                    const float4 t0 = reinterpret_cast<const float4*>(&sm.tail[slot])[0];
                     const int4 t1 = reinterpret_cast<const int4*>(&sm.tail[slot])[1];
                     const int bx0 = (short)(t1.y & 0xffff), bx1 = (short)(t1.y >> 16);
                     const int by0 = (short)(t1.z & 0xffff), by1 = (short)(t1.z >> 16);
@@ -191,10 +195,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                     cy0[hf] = max(by0 - Y0, 0);
                     w[hf] = max(min(bx1 - X0, TILE) - cx0[hf], 0);
                     h[hf] = max(min(by1 - Y0, TILE) - cy0[hf], 0);
-                    sm.col[jj] = make_float4(t0.z, t0.w, __int_as_float(t1.x), t0.x);
-                    const RecB& rb = sm.rb[slot];
-                    const float o = rb.opa;
-                    sm.par[jj] = make_float4(o, rb.sig, 1.f / o, (float)(1.0 / sm.ev[slot].phis));
+                    const RecC& rc = sm.rc[slot];
+                    sm.par[jj] = make_double4(rc.opa, rc.sig, 1.0 / rc.opa, 1.0 / sm.ev[slot].phis);
                 }
                 int a = w[hf] * h[hf];
 #pragma unroll
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
         nb = sm.nb;
         {  // records of the next window [bend-nb-DB, bend-nb)
             const int nrlo = max(s, bend - nb - DB);
-            for (int c = tid; c < (rlo - nrlo) * 16; c += 256) fetch_rec(nrlo + (c >> 4), c & 15);
+            for (int c = tid; c < (rlo - nrlo) * NCH; c += 256) fetch_rec(nrlo + c / NCH, c % NCH);
             rlo = min(rlo, nrlo);
             cp_async_commit();
         }
@@ -281,8 +283,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         if (l1 < rr) { rr = l1; edge = 1; }
                         if (l2 < rr) { rr = l2; edge = 2; }
                         if (rr >= r.r_lo) {
-                            const float4 par = sm.par[jj];
-                            const double o64 = (double)par.x, sg64 = (double)par.y;
+                            const double4 par = sm.par[jj];
+                            const double o64 = par.x, sg64 = par.y;
                             double ae;
                             if (mode == 0) {
                                 const double rc = fmin(rr, 1.0);
@@ -376,10 +378,10 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         sw += u * w;
                         fk--;
                     }
-                    const float4 col = sm.col[jj];
-                    S0 = fma(w, (double)col.x, S0);
-                    S1 = fma(w, (double)col.y, S1);
-                    S2 = fma(w, (double)col.z, S2);
+                    const double* col = sm.rc[(bend - 1 - jj) & (RR - 1)].rgb;
+                    S0 = fma(w, col[0], S0);
+                    S1 = fma(w, col[1], S1);
+                    S2 = fma(w, col[2], S2);
                     T = tb;
                 }
             }
@@ -401,8 +403,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                     const int pix = sl.jp >> 8;
                     const int k = sl.k;
                     const int slot = (bend - 1 - jj) & (RR - 1);
-                    const float4 par = sm.par[jj];  // o, sigma, 1/o, 1/phi_s
-                    const float4 col = sm.col[jj];
+                    const double4 par = sm.par[jj];  // o, sigma, 1/o, 1/phi_s
+                    const double* col = sm.rc[slot].rgb;
                     const double ae = sm.al[k];
                     const bool clamped = ae > ALPHA_CLAMP;
                     const double a = clamped ? ALPHA_CLAMP : ae;
@@ -413,8 +415,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                     g[8] = w * dd0;
                     g[9] = w * dd1;
                     g[10] = w * dd2;
-                    double ga = dd0 * (tb * col.x - sl.s0 * inv1m) + dd1 * (tb * col.y - sl.s1 * inv1m) +
-                                dd2 * (tb * col.z - sl.s2 * inv1m);
+                    double ga = dd0 * (tb * col[0] - sl.s0 * inv1m) + dd1 * (tb * col[1] - sl.s1 * inv1m) +
+                                dd2 * (tb * col[2] - sl.s2 * inv1m);
                     if (has_fg) {
                         ga += sl.u * tb - sl.sw * inv1m;
                         g[12] = sl.dz;
@@ -427,26 +429,25 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         const double pcx = sm.xc[lx], pcy = sm.yc[ly];
                         // fp64 r of the argmax edge for the chain (phi = r * phi_s)
                         const double r64 = fma(er.a[3 * edge], pcx, fma(er.a[3 * edge + 1], pcy, er.a[3 * edge + 2]));
-                        const double window = a * (double)par.z;
+                        const double window = a * par.z;
                         g[6] = ga * window;  // d/d opacity = g_alpha * alpha / o
-                        const double g_win = (double)par.x * ga;
+                        const double g_win = par.x * ga;
                         const double phi = r64 * er.phis;
                         double g_phi;
                         if (mode == 0) {
                             const double rc = fmin(r64, 1.0);
-                            // log(rc) in fp32 to ~1e-7 relative (log1p of the exact rc - 1 near 1)
-                            g[7] = g_win * window * (double)(rc > 0.5 ? log1pf((float)(rc - 1.0)) : logf((float)rc));
-                            const double g_r = g_win * (double)par.y * window / rc;
+                            g[7] = g_win * window * log(rc);
+                            const double g_r = g_win * par.y * window / rc;
                             if (r64 >= 1.0) {
                                 g_phi = 0.0;
                             } else {
-                                g_phi = g_r * (double)par.w;
-                                g[11] = -g_r * r64 * (double)par.w;
+                                g_phi = g_r * par.w;
+                                g[11] = -g_r * r64 * par.w;
                             }
                         } else {
-                            const double E = exp(fmin(phi / (double)par.y, 700.0));
+                            const double E = exp(fmin(phi / par.y, 700.0));
                             const double ww = E / ((1.0 + E) * (1.0 + E));
-                            const double is = 1.0 / (double)par.y;
+                            const double is = 1.0 / par.y;
                             g[7] = g_win * ww * phi * is * is;
                             g_phi = -g_win * ww * is;
                         }
@@ -468,13 +469,11 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         g[5] = edge == 2 ? gay : (ib == 2 ? gby : 0.0);
                     }
                 }
-                // segmented reduction (fp32 partials of fp64 terms): slots of one
-                // entry are consecutive, so a lane adds the lanes below it with the
-                // same entry; the first lane of each run ends with the run's sum.
-                // Only as many levels as the longest run needs.
-                float gf[13];
-#pragma unroll
-                for (int c = 0; c < 13; c++) gf[c] = (float)g[c];
+                // segmented fp64 reduction: slots of one entry are consecutive, so a
+                // lane adds the lanes below it with the same entry; the first lane of
+                // each run ends with the run's sum.  Only as many levels as the
+                // longest run needs.
+                double* gf = g;
                 const int jprev = __shfl_up_sync(0xffffffffu, jj, 1);
                 const bool head = lane == 0 || jprev != jj;
                 const unsigned heads = __ballot_sync(0xffffffffu, head);
@@ -488,7 +487,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                     const bool same = (int)lane + off < 32 && jo == jj;
 #pragma unroll
                     for (int c = 0; c < 13; c++) {
-                        const float v = __shfl_down_sync(0xffffffffu, gf[c], off);
+                        const double v = __shfl_down_sync(0xffffffffu, gf[c], off);
                         if (same) gf[c] += v;
                     }
                 }
@@ -496,7 +495,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                     double* dst = sgrad + (size_t)sm.srcq[(bend - 1 - jj) & (SR - 1)] * SG_STRIDE;
 #pragma unroll
                     for (int c = 0; c < 13; c++)
-                        if (gf[c] != 0.f) atomicAdd(dst + c, (double)gf[c]);
+                        if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);
                 }
             }
         }
@@ -506,36 +505,25 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
 }
 
 template <int DB, int PCAP, int GCAP, int MINB>
-static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
+static void launch_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
                              const int* tile_start, const unsigned* ent_src, const double* t_final,
                              const int* last_pos, const float* d_image, const int* n_frag,
                              const long long* frag_off, const double* fg_dw, const double* fg_dz,
                              const unsigned long long* run_if, double* sgrad, cudaStream_t st) {
     const int dyn = (int)sizeof(BwdSmem<DB, PCAP, GCAP>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_blend_bwd_dense<DB, PCAP, GCAP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-        attr = true;
-    }
+    smem_optin((const void*)k_blend_bwd_dense<DB, PCAP, GCAP, MINB>, dyn);
     const int ntiles = cam.ntx * cam.nty;
-    launch_pdl(k_blend_bwd_dense<DB, PCAP, GCAP, MINB>, dim3(ntiles), dim3(256), dyn, st, cam, opt, rec, recb,
+    launch_pdl(k_blend_bwd_dense<DB, PCAP, GCAP, MINB>, dim3(ntiles), dim3(256), dyn, st, cam, opt, rec, recb, recc,
                tile_start, ent_src, t_final, last_pos, d_image, n_frag, frag_off, fg_dw, fg_dz, run_if, sgrad);
 }
 
-void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
+void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
                             const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
                             const double* fg_dw, const double* fg_dz, const unsigned long long* run_if, double* sgrad,
                             cudaStream_t st) {
-    static const int variant = [] {
-        const char* v = getenv("TS_BWD_VARIANT");
-        return v ? atoi(v) : 0;
-    }();
-    if (variant == 1)
-        launch_bwd_dense<64, 2048, 512, 2>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
-                                           frag_off, fg_dw, fg_dz, run_if, sgrad, st);
-    else  // 3 CTAs per SM
-        launch_bwd_dense<32, 1024, 384, 3>(cam, opt, rec, recb, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
+    // 3 CTAs per SM (measured against 64-entry batches at 2 CTAs per SM)
+    launch_bwd_dense<32, 1024, 384, 3>(cam, opt, rec, recb, recc, tile_start, ent_src, t_final, last_pos, d_image, n_frag,
                                            frag_off, fg_dw, fg_dz, run_if, sgrad, st);
 }
 

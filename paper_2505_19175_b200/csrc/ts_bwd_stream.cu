@@ -10,22 +10,21 @@
 //     w_k = T_k alpha_k,   S_k = C_N - C_k - w_k c_k   (suffix colour),
 //     dL/dalpha_k = sum_c d_c (T_k c_k - S_k / (1 - alpha_k)),
 // so every fragment is independent: one lane per record, r / argmax edge /
-// alpha recomputed in fp64 from the triangle's records, the window and edge
-// chain as in k_blend_bwd_dense, a segmented warp reduction over consecutive
-// records of one triangle and one fp64 atomic per (triangle, component) and
-// warp step.  No tile loop, no CTA barrier.  If the forward's record buffer
-// overflowed, this kernel does nothing and the tile backward runs instead.
+// alpha recomputed in fp64 from the triangle's records (fp64 colour, opacity
+// and sigma from its RecC), the window and edge chain as in k_blend_bwd_dense,
+// an fp64 segmented warp reduction over consecutive records of one triangle and
+// one fp64 atomic per (triangle, component) and warp step.  No tile loop, no
+// CTA barrier.  If the forward's record buffer overflowed, this kernel does
+// nothing and the tile backward runs instead.
 #include "ts_kernels.cuh"
 
 namespace ts {
 
-template <typename PT, int MINB, typename AT>
-__global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, const RecF* __restrict__ rec,
-                                                    const RecB* __restrict__ recb,
-                                                    const PT* __restrict__ opacity, const PT* __restrict__ sigma,
-                                                    const FragRec* __restrict__ frec, const Counters* __restrict__ ctr,
-                                                    unsigned long long cap, const double* __restrict__ c_total,
-                                                    const float* __restrict__ d_image, double* __restrict__ sgrad) {
+__global__ void __launch_bounds__(256, 3) k_bwd_stream(Cam cam, Opts opt, const RecF* __restrict__ rec,
+                                                 const RecB* __restrict__ recb, const RecC* __restrict__ recc,
+                                                 const FragRec* __restrict__ frec, const Counters* __restrict__ ctr,
+                                                 unsigned long long cap, const double* __restrict__ c_total,
+                                                 const float* __restrict__ d_image, double* __restrict__ sgrad) {
     TS_PDL_ENTRY();
     if (ctr->frec_over) return;
     const unsigned long long total = ctr->n_frec;
@@ -36,9 +35,9 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
     const int mode = opt.mode;
     for (long long q0 = gw * 32; q0 < n; q0 += nw * 32) {
         const long long q = q0 + lane;
-        AT gf[12];
+        double gf[12];
 #pragma unroll
-        for (int c = 0; c < 12; c++) gf[c] = (AT)0;
+        for (int c = 0; c < 12; c++) gf[c] = 0.0;
         unsigned key = 0xffffffffu - lane;  // unique keys for idle lanes and holes
         bool act = false;
         if (q < n) {
@@ -52,6 +51,7 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                 key = src;
                 const RecF& R = rec[src];
                 const RecB& B = recb[src];
+                const RecC& Cc = recc[src];
                 const int px = (int)(pix % (unsigned)cam.width), py = (int)(pix / (unsigned)cam.width);
                 const double pcx = px + 0.5, pcy = py + 0.5;
                 const double l0 = fma(__ldg(&R.a[0]), pcx, fma(__ldg(&R.a[1]), pcy, __ldg(&R.a[2])));
@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                 if (l1 < r64) { r64 = l1; edge = 1; }
                 if (l2 < r64) { r64 = l2; edge = 2; }
                 const double phis = __ldg(&R.phis);
-                const double o = opt.solid ? 1.0 : (double)__ldg(opacity + src);
-                const double sg = (double)__ldg(sigma + src);
+                const double2 osg = __ldg(reinterpret_cast<const double2*>(&Cc.opa));
+                const double o = osg.x, sg = osg.y;
                 const double rc = fmin(r64, 1.0);
                 double ae;
                 if (mode == 0) ae = o * (sg == 1.0 ? rc : pow(rc, sg));
@@ -74,38 +74,37 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                 const double inv1m = 1.0 / (1.0 - a);
                 const double tb = tc.x;
                 const double w = tb * a;
-                const float c0 = __ldg(&R.rgb[0]), c1 = __ldg(&R.rgb[1]), c2 = __ldg(&R.rgb[2]);
+                const double2 c01 = __ldg(reinterpret_cast<const double2*>(Cc.rgb));
+                const double c0 = c01.x, c1 = c01.y, c2 = __ldg(&Cc.rgb[2]);
                 const double s0 = __ldg(c_total + pix * 3 + 0) - tc.y - w * c0;
                 const double s1 = __ldg(c_total + pix * 3 + 1) - tc.z - w * c1;
                 const double s2 = __ldg(c_total + pix * 3 + 2) - tc.w - w * c2;
                 const double d0 = __ldg(d_image + pix * 3 + 0), d1 = __ldg(d_image + pix * 3 + 1),
                              d2 = __ldg(d_image + pix * 3 + 2);
-                gf[8] = (AT)(w * d0);
-                gf[9] = (AT)(w * d1);
-                gf[10] = (AT)(w * d2);
+                gf[8] = w * d0;
+                gf[9] = w * d1;
+                gf[10] = w * d2;
                 const double ga = d0 * (tb * c0 - s0 * inv1m) + d1 * (tb * c1 - s1 * inv1m) + d2 * (tb * c2 - s2 * inv1m);
                 if (!clamped) {
                     const double window = a / o;
-                    gf[6] = (AT)(ga * window);  // d/d opacity = g_alpha * alpha / o
+                    gf[6] = ga * window;  // d/d opacity = g_alpha * alpha / o
                     const double g_win = o * ga;
                     const double phi = r64 * phis;
                     double g_phi;
                     if (mode == 0) {
-                        // log(rc) in fp32 to ~1e-7 relative: log1p of the exact rc - 1 near 1, log below
-                        const float lrc = rc > 0.5 ? log1pf((float)(rc - 1.0)) : logf((float)rc);
-                        gf[7] = (AT)(g_win * window * (double)lrc);
+                        gf[7] = g_win * window * log(rc);
                         const double g_r = g_win * sg * window / rc;
                         if (r64 >= 1.0) {
                             g_phi = 0.0;
                         } else {
                             g_phi = g_r / phis;
-                            gf[11] = (AT)(-g_r * r64 / phis);
+                            gf[11] = -g_r * r64 / phis;
                         }
                     } else {
                         const double E = exp(fmin(phi / sg, 700.0));
                         const double ww = E / ((1.0 + E) * (1.0 + E));
                         const double is = 1.0 / sg;
-                        gf[7] = (AT)(g_win * ww * phi * is * is);
+                        gf[7] = g_win * ww * phi * is * is;
                         g_phi = -g_win * ww * is;
                     }
                     const int ib = edge == 2 ? 0 : edge + 1;
@@ -113,16 +112,16 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
                     const double bx = __ldg(&B.qx[ib]), by = __ldg(&B.qy[ib]);
                     const double pxr = (double)(px - __ldg(&R.ox)) + 0.5, pyr = (double)(py - __ldg(&R.oy)) + 0.5;
                     const double sl = __ldg(&B.sl[edge]), ul = __ldg(&B.ul[edge]), vl = __ldg(&B.vl[edge]);
-                    const AT gax = (AT)(g_phi * (sl * (pyr - by) + phi * ul));
-                    const AT gay = (AT)(g_phi * (sl * (bx - pxr) + phi * vl));
-                    const AT gbx = (AT)(g_phi * (sl * (ay - pyr) - phi * ul));
-                    const AT gby = (AT)(g_phi * (sl * (pxr - ax) - phi * vl));
-                    gf[0] = edge == 0 ? gax : (ib == 0 ? gbx : (AT)0);
-                    gf[1] = edge == 0 ? gay : (ib == 0 ? gby : (AT)0);
-                    gf[2] = edge == 1 ? gax : (ib == 1 ? gbx : (AT)0);
-                    gf[3] = edge == 1 ? gay : (ib == 1 ? gby : (AT)0);
-                    gf[4] = edge == 2 ? gax : (ib == 2 ? gbx : (AT)0);
-                    gf[5] = edge == 2 ? gay : (ib == 2 ? gby : (AT)0);
+                    const double gax = g_phi * (sl * (pyr - by) + phi * ul);
+                    const double gay = g_phi * (sl * (bx - pxr) + phi * vl);
+                    const double gbx = g_phi * (sl * (ay - pyr) - phi * ul);
+                    const double gby = g_phi * (sl * (pxr - ax) - phi * vl);
+                    gf[0] = edge == 0 ? gax : (ib == 0 ? gbx : 0.0);
+                    gf[1] = edge == 0 ? gay : (ib == 0 ? gby : 0.0);
+                    gf[2] = edge == 1 ? gax : (ib == 1 ? gbx : 0.0);
+                    gf[3] = edge == 1 ? gay : (ib == 1 ? gby : 0.0);
+                    gf[4] = edge == 2 ? gax : (ib == 2 ? gbx : 0.0);
+                    gf[5] = edge == 2 ? gay : (ib == 2 ? gby : 0.0);
                 }
             }
         }
@@ -142,7 +141,7 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
             const bool same = (int)lane + off < 32 && ro == rid;
 #pragma unroll
             for (int c = 0; c < 12; c++) {
-                const AT v = __shfl_down_sync(0xffffffffu, gf[c], off);
+                const double v = __shfl_down_sync(0xffffffffu, gf[c], off);
                 if (same) gf[c] += v;
             }
         }
@@ -150,39 +149,16 @@ __global__ void __launch_bounds__(256, MINB) k_bwd_stream(Cam cam, Opts opt, con
             double* dst = sgrad + (size_t)key * SG_STRIDE;
 #pragma unroll
             for (int c = 0; c < 12; c++)
-                if (gf[c] != (AT)0) atomicAdd(dst + c, (double)gf[c]);
+                if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);
         }
     }
 }
 
-void launch_bwd_stream(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
-                       const RecB* recb, const FragRec* frec, const Counters* ctr, unsigned long long cap,
-                       const double* c_total, const float* d_image, double* sgrad, cudaStream_t st) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int grid = sms * 8;
-    static const int variant = [] {
-        const char* v = getenv("TS_STREAM_VARIANT");
-        return v ? atoi(v) : 0;
-    }();
-    // per-record gradients summed in fp32 within a warp step, fp64 across
-    // (TS_STREAM_VARIANT=2: fp64 throughout -- measured no more accurate: the
-    // ~5e-5 residual vs the fp64 reference comes from the fp32 SH colour)
-    if (dtype == 1)
-        k_bwd_stream<double, 4, double><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const double*)soup.opacity,
-                                                            (const double*)soup.sigma, frec, ctr, cap, c_total,
-                                                            d_image, sgrad);
-    else if (variant == 2)
-        k_bwd_stream<float, 4, double><<<grid, 256, 0, st>>>(cam, opt, rec, recb, (const float*)soup.opacity,
-                                                            (const float*)soup.sigma, frec, ctr, cap, c_total, d_image,
-                                                            sgrad);
-    else
-        launch_pdl(k_bwd_stream<float, 4, float>, dim3(grid), dim3(256), 0, st, cam, opt, rec, recb,
-                   (const float*)soup.opacity, (const float*)soup.sigma, frec, ctr, cap, c_total, d_image, sgrad);
+void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
+                       const FragRec* frec, const Counters* ctr, unsigned long long cap, const double* c_total,
+                       const float* d_image, double* sgrad, cudaStream_t st) {
+    launch_pdl(k_bwd_stream, dim3(sm_count() * 8), dim3(256), 0, st, cam, opt, rec, recb, recc, frec, ctr, cap, c_total,
+               d_image, sgrad);
 }
 
 }  // namespace ts

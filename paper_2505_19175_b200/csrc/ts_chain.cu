@@ -274,12 +274,8 @@ bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup,
     // 16-byte vector access of the SH / gradient blocks
     if (((uintptr_t)soup.sh | (uintptr_t)g.d_sh | (uintptr_t)soup.vertices) & 15) return false;
     if (n <= 0) return true;
-    static bool attr = false;
     const int smem = (int)sizeof(ChainStage);
-    if (!attr) {
-        cudaFuncSetAttribute(k_chain_bwd32, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    smem_optin((const void*)k_chain_bwd32, smem);
     const unsigned grid = (unsigned)((n + CB - 1) / CB);
     launch_pdl(k_chain_bwd32, dim3(grid), dim3(CB), smem, st, cam, opt, (const float*)soup.vertices,
                (const float*)soup.sh, flag, sgrad, n, g, accumulate);

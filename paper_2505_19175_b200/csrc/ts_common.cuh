@@ -73,9 +73,21 @@ static_assert(sizeof(RecF) == 128, "RecF layout");
 struct __align__(16) RecB {
     double qx[3], qy[3];
     double sl[3], ul[3], vl[3];
-    float opa, sig;  // opacity (1 for solid soups) and sigma, as float
+    double pad;
 };
 static_assert(sizeof(RecB) == 128, "RecB layout");
+
+// Training-only per-source fp64 data (48 B): the SH colour before its fp32
+// rounding (clipped, render.py:302) and the exact opacity (1 for solid soups)
+// and sigma.  The training forward composites and the backward differentiates
+// with these, so the suffix colours S_k and dL/dalpha (_kernels.py:250-277)
+// carry the reference's fp64 colour, not a rounded copy.
+struct __align__(16) RecC {
+    double opa, sig;  // (16-byte aligned pairs: one double2 load each)
+    double rgb[3];
+    double pad;
+};
+static_assert(sizeof(RecC) == 48, "RecC layout");
 
 // Shared-memory images of a RecF for the dense blend kernels: the evaluation
 // part (first 96 B) and the tail (last 32 B), copied with 16-byte cp.async.
@@ -388,16 +400,12 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) 
 // for its predecessor grid to complete (griddepcontrol.wait) before touching its
 // outputs, then lets its own successor launch, so successor CTAs are scheduled
 // while this grid's last wave drains.  A no-op for kernels launched without the
-// attribute.  TS_NO_PDL=1 launches normally.
+// attribute.
 #define TS_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
 #ifndef __CUDACC_RTC__
-#include <cstdlib>
+#include <mutex>
 #include <utility>
 namespace ts {
-inline bool pdl_enabled() {
-    static const bool on = getenv("TS_NO_PDL") == nullptr;
-    return on;
-}
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -410,8 +418,42 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// Per-device launch facts: the SM count and the dynamic shared-memory opt-in of
+// each kernel are properties of the current device, cached per device ordinal
+// (a process may drive several GPUs, one context each).
+constexpr int TS_MAX_DEVICES = 64;
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev < 0 || dev >= TS_MAX_DEVICES ? 0 : dev;
+}
+inline int sm_count() {
+    static int cache[TS_MAX_DEVICES] = {};
+    const int dev = current_device();
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size)
+inline void smem_optin(const void* kernel, int bytes) {
+    struct Entry { const void* k; int dev; int bytes; };
+    static std::mutex mu;
+    static Entry done[256];
+    static int n = 0;
+    if (bytes <= 48 * 1024) return;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < n; i++)
+        if (done[i].k == kernel && done[i].dev == dev && done[i].bytes >= bytes) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (n < 256) done[n++] = Entry{kernel, dev, bytes};
 }
 }  // namespace ts
 #endif

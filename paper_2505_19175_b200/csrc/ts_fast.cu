@@ -4,10 +4,9 @@
 // decision falls inside it.
 //
 //   k_preprocess_fast  render.py:159-190, 193-250, 271-273, 292-302 -> RecF/RecB
-//   k_blend_fast       _kernels.py:59-132 (decisions: skip alpha<1/255 :103,
-//                      T<1e-4 stop :121, pixel count w>1/255 :112)
+//   k_blend_fast       _kernels.py:59-132 with fragment emission (collect_fragments,
+//                      _kernels.py:107-116): fp64 re-composite of a training forward
 //   k_fixup_fwd        exact replay (same arithmetic as k_blend_exact) of flagged pixels
-//   k_blend_bwd_fast   _kernels.py:181-318 back to front from the saved last contributor
 //
 // Decision guard band.  r = phi/phi_s is evaluated in fp64 from fp64 edge
 // coefficients (error ~1e-12 vs the reference's fp64 phi/phi_s), so the skip
@@ -276,9 +275,18 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
                     rb.ul[e] = ex * il * il;
                     rb.vl[e] = ey * il * il;
                 }
-                rb.opa = (float)o;
-                rb.sig = (float)sg;
+                rb.pad = 0.0;
                 out.recb[i] = rb;
+            }
+            if (out.recc) {
+                RecC rc;
+                rc.rgb[0] = fmin(fmax(d0, 0.0), 1.0);
+                rc.rgb[1] = fmin(fmax(d1, 0.0), 1.0);
+                rc.rgb[2] = fmin(fmax(d2, 0.0), 1.0);
+                rc.opa = o;
+                rc.sig = sg;
+                rc.pad = 0.0;
+                out.recc[i] = rc;
             }
             (void)qf;
         }
@@ -441,47 +449,18 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
         k_preprocess_fast64<<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices, (const double*)soup.opacity,
                                                   (const double*)soup.sigma, (const double*)soup.sh, n, out);
     } else {
-        static int sms = 0;
-        static const int variant = [] {
-            const char* v = getenv("TS_PRE_VARIANT");
-            return v ? atoi(v) : 0;
-        }();
-        // default: single-buffered stage, 4 CTAs per SM (other CTAs overlap each
-        // one's loads; 126 registers), the CTA's next stage bulk-prefetched into L2
-        // while it computes; 1: double-buffered, 3 CTAs; 2: single, 5 CTAs;
-        // 3: default without the L2 prefetch
-        const int nbuf = variant == 1 ? 2 : 1;
-        const int minb = variant == 1 ? 3 : (variant == 2 ? 5 : 4);
-        const int smem = nbuf * (int)sizeof(PreStage);
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(k_preprocess_fast32<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 2 * (int)sizeof(PreStage));
-            cudaFuncSetAttribute(k_preprocess_fast32<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(PreStage));
-            cudaFuncSetAttribute(k_preprocess_fast32<1, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(PreStage));
-            cudaFuncSetAttribute(k_preprocess_fast32<1, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(PreStage));
-
-        }
+        // single-buffered stage, 4 CTAs per SM (the other CTAs overlap each one's
+        // loads; 126 registers), the CTA's next stage bulk-prefetched into L2 while
+        // it computes (measured against double buffering at 3 CTAs / 5 CTAs / no
+        // prefetch: DESIGN.md section 6)
+        const int sms = sm_count();
+        const int smem = (int)sizeof(PreStage);
+        smem_optin((const void*)k_preprocess_fast32<1, 4, 1>, smem);
         const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
-        const long long grid = std::min<long long>(nblk, (long long)sms * minb);
-        const float* v = (const float*)soup.vertices;
-        const float* o = (const float*)soup.opacity;
-        const float* sg = (const float*)soup.sigma;
-        const float* sh = (const float*)soup.sh;
-        if (minb == 3)
-            k_preprocess_fast32<2, 3><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
-        else if (minb == 5)
-            k_preprocess_fast32<1, 5><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
-        else if (variant == 3)
-            k_preprocess_fast32<1, 4><<<(unsigned)grid, PRE_BLK, smem, st>>>(cam, opt, v, o, sg, sh, n, out);
-        else
-            launch_pdl(k_preprocess_fast32<1, 4, 1>, dim3((unsigned)grid), dim3(PRE_BLK), smem, st, cam, opt, v, o, sg,
-                       sh, n, out);
+        const long long grid = std::min<long long>(nblk, (long long)sms * 4);
+        launch_pdl(k_preprocess_fast32<1, 4, 1>, dim3((unsigned)grid), dim3(PRE_BLK), smem, st, cam, opt,
+                   (const float*)soup.vertices, (const float*)soup.opacity, (const float*)soup.sigma,
+                   (const float*)soup.sh, n, out);
     }
 }
 
@@ -765,236 +744,6 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
 }
 
 // ---------------------------------------------------------------------------
-// k_blend_render: the render-only forward (fp32 compositing, guard band) with
-// deferred alpha.  Per batch of FB entries, per warp (2x16 strip, 8 groups of
-// 4 lanes = 2x2 quads, as k_blend_fast):
-//   1. evaluation -- each group walks the entries overlapping its quad; a lane
-//      whose pixel is inside the bbox evaluates r in fp64 and, if r >= r_lo,
-//      appends (entry, r) to its slot list (no alpha work here);
-//   2. alpha -- the warp's candidates are processed densely, one per lane;
-//   3. compositing -- lane = pixel walks its slots in entry order.
-// Overflowing a pixel's slots, or any decision inside the guard band, flags
-// the pixel for the exact fix-up (nothing of that batch is committed for it).
-// ---------------------------------------------------------------------------
-constexpr int QCAP = 12;
-
-__global__ void __launch_bounds__(256) k_blend_render(Cam cam, Opts opt, const RecF* __restrict__ rec,
-                                                      const short4* __restrict__ bbox,
-                                                      const int* __restrict__ tile_start,
-                                                      const unsigned* __restrict__ ent_src,
-                                                      FastBlendOut out) {
-    __shared__ SRec s_rec[FB];
-    __shared__ short4 s_bb[FB];
-    __shared__ unsigned s_src[FB];
-    __shared__ unsigned s_maxw[FB];
-    __shared__ int s_pix[FB];
-    __shared__ float s_qa[8][QCAP][32];          // r (fp32) -> alpha; NaN = guard band
-    __shared__ float s_qe[8][QCAP][32];          // relative error bound of alpha
-    __shared__ unsigned char s_qj[8][QCAP][32];  // entry index in the batch
-    const int t = blockIdx.x;
-    const int tx = t % cam.ntx, ty = t / cam.ntx;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned grp = lane >> 2;
-    const int X0 = tx * TILE + 2 * (int)warp;
-    const int Y0 = ty * TILE;
-    const int px = X0 + (int)(lane & 1);
-    const int py = Y0 + 2 * (int)grp + (int)((lane >> 1) & 1);
-    const double pcx = px + 0.5, pcy = py + 0.5;
-    const bool inside = px < cam.width && py < cam.height;
-    const unsigned mybit = 4u * grp + (lane & 3u);
-    const unsigned lt = lanemask_lt();
-    float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, epsT = 0.f;
-    int last = -1, cnt = 0, flag_pos = -1;
-    bool done = !inside;
-    const int s = tile_start[t], e = tile_start[t + 1];
-    const float tau = (float)opt.tau_contrib;
-    if (threadIdx.x < FB) {
-        s_maxw[threadIdx.x] = 0u;
-        s_pix[threadIdx.x] = 0;
-    }
-    for (int b = s; b < e; b += FB) {
-        if (__syncthreads_count(!done) == 0) break;
-        const int nb = min(FB, e - b);
-        for (int c = threadIdx.x; c < nb * 8; c += blockDim.x) {
-            const int j = c >> 3, q = c & 7;
-            const unsigned src = __ldg(ent_src + b + j);
-            if (q == 0) {
-                s_src[j] = src;
-                s_bb[j] = __ldg(bbox + src);
-            }
-            reinterpret_cast<float4*>(&s_rec[j].r)[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
-        }
-        __syncthreads();
-        if (__any_sync(0xffffffffu, !done)) {
-            // ---- 1. evaluation ----
-            int qn = 0;
-            for (int jb = 0; jb < nb; jb += 32) {
-                unsigned W = 0u;
-                const int jl = jb + (int)lane;
-                if (jl < nb) {
-                    const short4 bb = s_bb[jl];
-                    const unsigned cb =
-                        (unsigned)(X0 >= bb.x && X0 < bb.y) | ((unsigned)(X0 + 1 >= bb.x && X0 + 1 < bb.y) << 1);
-                    const int r0 = max((int)bb.z - Y0, 0), r1 = min((int)bb.w - Y0, TILE);
-                    if (cb && r1 > r0) {
-                        unsigned x = ((1u << (r1 - r0)) - 1u) << r0;
-                        x = (x | (x << 8)) & 0x00FF00FFu;
-                        x = (x | (x << 4)) & 0x0F0F0F0Fu;
-                        x = (x | (x << 2)) & 0x33333333u;
-                        x = (x | (x << 1)) & 0x55555555u;
-                        W = x * cb;
-                    }
-                }
-                unsigned gmask = 0u;
-#pragma unroll
-                for (int g = 0; g < 8; g++) {
-                    const unsigned bm = __ballot_sync(0xffffffffu, ((W >> (4 * g)) & 0xFu) != 0u);
-                    if ((int)grp == g) gmask = bm;
-                }
-                if (done) gmask = 0u;
-                while (__any_sync(0xffffffffu, gmask != 0u)) {
-                    const int jo = __ffs(gmask) - 1;
-                    gmask &= gmask - 1;
-                    const unsigned Wj = __shfl_sync(0xffffffffu, W, jo & 31);
-                    if (jo >= 0 && ((Wj >> mybit) & 1u)) {
-                        const int j = jb + jo;
-                        const double* a = s_rec[j].r.a;
-                        const double rlo = s_rec[j].r.r_lo;
-                        const double l0 = fma(a[0], pcx, fma(a[1], pcy, a[2]));
-                        const double l1 = fma(a[3], pcx, fma(a[4], pcy, a[5]));
-                        const double l2 = fma(a[6], pcx, fma(a[7], pcy, a[8]));
-                        if (l0 >= rlo && l1 >= rlo && l2 >= rlo) {
-                            const double m01 = l0 < l1 ? l0 : l1;
-                            const double rr = m01 < l2 ? m01 : l2;
-                            // NaN marks r inside the contribution band (resolved by the fix-up)
-                            const float rv = rr > s_rec[j].r.r_hi ? (float)rr : __int_as_float(0x7fc00000);
-                            if (qn < QCAP) {
-                                s_qa[warp][qn][lane] = rv;
-                                s_qj[warp][qn][lane] = (unsigned char)j;
-                            }
-                            qn++;
-                        }
-                    }
-                }
-            }
-            // ---- 2. alpha for all candidates of the warp, one per lane ----
-            const int qc = min(qn, QCAP);
-            int o = qc;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, o, off);
-                if ((int)lane >= off) o += y;
-            }
-            const int total = __shfl_sync(0xffffffffu, o, 31);
-            o -= qc;  // exclusive
-            __syncwarp();
-            for (int q0 = 0; q0 < total; q0 += 32) {
-                const int q = q0 + (int)lane;
-                int L = 0;
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int cand = L + step;
-                    const int ov = __shfl_sync(0xffffffffu, o, cand & 31);
-                    if (cand < 32 && ov <= q) L = cand;
-                }
-                const int oL = __shfl_sync(0xffffffffu, o, L);
-                if (q < total) {
-                    const int k = q - oL;
-                    const float rv = s_qa[warp][k][L];
-                    if (!isnan(rv)) {
-                        const RecF& r = s_rec[s_qj[warp][k][L]].r;
-                        float a, ea;
-                        if (opt.mode == 0) {
-                            const float lg = fast_lg2(fminf(rv, 1.f));
-                            const float arg = fmaf(r.f0, lg, r.f1);
-                            a = fast_ex2(arg);
-                            ea = 5e-7f + r.f0 * (6e-7f + 2.4e-7f * fabsf(lg)) + 1.2e-7f * fabsf(arg);
-                        } else {
-                            const float x = rv * r.f0;
-                            a = __fdividef(r.f1, 1.0f + fast_ex2(fminf(x, 1009.9f)));
-                            ea = 8e-7f + 1.2e-7f * fabsf(x);
-                        }
-                        s_qa[warp][k][L] = fminf(a, ALPHA_CLAMP_F);
-                        s_qe[warp][k][L] = ea;
-                    }
-                }
-            }
-            __syncwarp();
-            // ---- 3. compositing, lane = pixel, slots in entry order ----
-            if (!done) {
-                if (qn > QCAP) {
-                    flag_pos = b;  // nothing of this batch committed for this pixel
-                    done = true;
-                } else {
-                    for (int k = 0; k < qn; k++) {
-                        const int j = s_qj[warp][k][lane];
-                        const float a = s_qa[warp][k][lane];
-                        if (isnan(a)) {  // r inside the contribution band
-                            flag_pos = b + j;
-                            done = true;
-                            break;
-                        }
-                        const float ea = s_qe[warp][k][lane];
-                        const float w = T * a;
-                        const float tn = fmaf(-T, a, T);
-                        const float en = fmaf(ea * a, __frcp_rn(1.f - a), epsT + 2.4e-7f);
-                        const float ew = epsT + ea + 1.2e-7f;
-                        if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
-                            fabsf(w - tau) <= fmaf(2.f * ew, w, 1e-9f)) {
-                            flag_pos = b + j;
-                            done = true;
-                            break;
-                        }
-                        const RecF& r = s_rec[j].r;
-                        C0 = fmaf(w, r.rgb[0], C0);
-                        C1 = fmaf(w, r.rgb[1], C1);
-                        C2 = fmaf(w, r.rgb[2], C2);
-                        last = b + j;
-                        cnt++;
-                        T = tn;
-                        epsT = en;
-                        red_max_shared(&s_maxw[j], __float_as_uint(w));
-                        if (w > tau) red_add_shared(&s_pix[j], 1);
-                        if (T < T_MIN_F) {
-                            done = true;
-                            break;
-                        }
-                    }
-                }
-            }
-            (void)lt;
-        }
-        __syncthreads();
-        if (threadIdx.x < nb) {
-            const unsigned src = s_src[threadIdx.x];
-            if (s_maxw[threadIdx.x] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
-            if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
-            s_maxw[threadIdx.x] = 0u;
-            s_pix[threadIdx.x] = 0;
-        }
-    }
-    if (inside) {
-        const int p = py * cam.width + px;
-        if (flag_pos >= 0) {
-            unsigned long long k = atomicAdd(&out.ctr->n_flagged, 1ull);
-            out.flags[k] = make_int2(p, flag_pos);
-        } else {
-            if (out.image) {
-                out.image[p * 3 + 0] = fminf(fmaxf(fmaf(T, (float)opt.bg[0], C0), 0.f), 1.f);
-                out.image[p * 3 + 1] = fminf(fmaxf(fmaf(T, (float)opt.bg[1], C1), 0.f), 1.f);
-                out.image[p * 3 + 2] = fminf(fmaxf(fmaf(T, (float)opt.bg[2], C2), 0.f), 1.f);
-            }
-            if (out.alpha_map) out.alpha_map[p] = 1.f - T;
-            out.t_final[p] = T;
-            if (out.t_final64) out.t_final64[p] = (double)T;
-            out.last_pos[p] = last;
-            if (out.n_frag) out.n_frag[p] = cnt;
-            if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // k_fixup_fwd: exact (fp64) replay of flagged pixels, one CTA per pixel.
 // The CTA evaluates alpha for FXC consecutive tile entries in parallel
 // (shared memory), then warp 0 composites the contributing ones in entry
@@ -1012,7 +761,7 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                                                    const unsigned* __restrict__ ent_src, FastBlendOut out) {
     TS_PDL_ENTRY();
     __shared__ double s_a[FXC];
-    __shared__ float s_c[3][FXC];
+    __shared__ double s_c[3][FXC];     // colour (training forwards: the fp64 RecC colour)
     __shared__ unsigned s_s[FXC];
     __shared__ int s_done;
     __shared__ short s_idx[FXC];        // render path: passing entries of the chunk, in order
@@ -1067,9 +816,16 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                     a = alpha_exact_r<T>(r, rr, opt.mode, opt, opacity, sigma, src);
                     if (a > ALPHA_CLAMP) a = ALPHA_CLAMP;
                     if (a < ALPHA_MIN) a = 0.0;
-                    s_c[0][i] = r.rgb[0];
-                    s_c[1][i] = r.rgb[1];
-                    s_c[2][i] = r.rgb[2];
+                    if (out.recc) {
+                        const RecC& rc = out.recc[src];
+                        s_c[0][i] = rc.rgb[0];
+                        s_c[1][i] = rc.rgb[1];
+                        s_c[2][i] = rc.rgb[2];
+                    } else {
+                        s_c[0][i] = r.rgb[0];
+                        s_c[1][i] = r.rgb[1];
+                        s_c[2][i] = r.rgb[2];
+                    }
                 }
                 s_a[i] = a;
                 s_s[i] = src;
@@ -1108,9 +864,9 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                 for (int q = threadIdx.x; q < used; q += FX_T) {
                     const int j = s_idx[q];
                     const double w = s_tb[q] * s_a[j];
-                    c0 += w * (double)s_c[0][j];
-                    c1 += w * (double)s_c[1][j];
-                    c2 += w * (double)s_c[2][j];
+                    c0 += w * s_c[0][j];
+                    c1 += w * s_c[1][j];
+                    c2 += w * s_c[2][j];
                     if (base + j >= fpos) {
                         if (out.max_weight) atomicMax((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
                         if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + s_s[j], 1);
@@ -1169,9 +925,9 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                                 out.ctr->frec_over = 1ull;
                             }
                         }
-                        C0 += w * (double)s_c[0][j];
-                        C1 += w * (double)s_c[1][j];
-                        C2 += w * (double)s_c[2][j];
+                        C0 += w * s_c[0][j];
+                        C1 += w * s_c[1][j];
+                        C2 += w * s_c[2][j];
                         const int posj = base + j;
                         if (lane == 0 && out.frag_tri) {
                             const long long fi = out.frag_off[p] + cnt;
@@ -1219,21 +975,18 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
     }
 }
 
-void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64,
-                       const RecF* rec, const short4* bbox, const int* tile_start, const unsigned* ent_src,
-                       const FastBlendOut& out, cudaStream_t st) {
-    int ntiles = cam.ntx * cam.nty;
-    if (dtype == 1) {
-        const double* o = (const double*)soup.opacity;
-        const double* sg = (const double*)soup.sigma;
-        if (acc64) k_blend_fast<double, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
-        else k_blend_render<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
-    } else {
-        const float* o = (const float*)soup.opacity;
-        const float* sg = (const float*)soup.sigma;
-        if (acc64) k_blend_fast<float, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, o, sg, out);
-        else k_blend_render<<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src, out);
-    }
+// fragment collection (ts_collect_fragments): fp64 re-composite of the last
+// training forward that emits every composited fragment
+void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                       const short4* bbox, const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                       cudaStream_t st) {
+    const int ntiles = cam.ntx * cam.nty;
+    if (dtype == 1)
+        k_blend_fast<double, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src,
+                                                           (const double*)soup.opacity, (const double*)soup.sigma, out);
+    else
+        k_blend_fast<float, true><<<ntiles, 256, 0, st>>>(cam, opt, rec, bbox, tile_start, ent_src,
+                                                          (const float*)soup.opacity, (const float*)soup.sigma, out);
 }
 
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
@@ -1241,7 +994,7 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
                       cudaStream_t st) {
     // 2 entries per thread of a 1024-entry chunk: the dependent record loads of
     // the whole chunk are in flight at once
-    const int grid = 148 * 2;
+    const int grid = sm_count() * 2;
     if (dtype == 1)
         launch_pdl(k_fixup_fwd<double>, dim3(grid), dim3(FX_T), 0, st, cam, opt, (const double*)soup.opacity,
                    (const double*)soup.sigma, rec, tile_start, ent_src, out);
@@ -1250,235 +1003,5 @@ void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int 
                    (const float*)soup.sigma, rec, tile_start, ent_src, out);
 }
 
-// ---------------------------------------------------------------------------
-// k_blend_bwd_fast: back to front from the saved last contributor
-// (_kernels.py:181-318).  CTA per tile, warp = 16x2 pixel strip, all lanes on
-// the same entry so per-entry sums reduce inside the warp.  Per fragment:
-// r from the fp64 edge functions, alpha with the reference formula in fp64
-// (exact opacity/sigma staged per entry), transmittance reconstructed in
-// fp64 from the training forward's fp64 T_final, suffix colour, dL/dalpha and
-// the edge chain in fp64 (near-degenerate triangles cancel heavily).  The 12
-// per-entry values are butterfly reduce-scattered across the warp (16 double
-// shuffles), stored as per-warp partials in shared memory, summed over the
-// CTA's warps and added with one fp64 RED per (tile entry, component).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double bfly_step(double keep, double send, int off) {
-    return keep + __shfl_xor_sync(0xffffffffu, send, off);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256, 3) k_blend_bwd_fast(Cam cam, Opts opt, const T* __restrict__ verts,
-                                                           const T* __restrict__ opacity,
-                                                           const T* __restrict__ sigma,
-                                                           const RecF* __restrict__ rec,
-                                                           const RecB* __restrict__ recb,
-                                                           const int* __restrict__ tile_start,
-                                                           const unsigned* __restrict__ ent_src,
-                                                           const double* __restrict__ t_final,
-                                                           const int* __restrict__ last_pos,
-                                                           const float* __restrict__ d_image,
-                                                           double* __restrict__ sgrad) {
-    (void)verts;
-    constexpr int BB = 32;  // entries per batch
-    __shared__ RecF s_rec[BB];
-    __shared__ RecB s_rb[BB];
-    __shared__ double4 s_os[BB];                 // opacity, sigma, 1/opacity, 1/phis
-    __shared__ unsigned s_src[BB];
-    __shared__ float s_part[8][BB][12];          // per-warp per-entry partial sums
-    __shared__ int s_hi;
-    const int t = blockIdx.x;
-    const int tx = t % cam.ntx, ty = t / cam.ntx;
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int px = tx * TILE + (lane & 15);
-    const int py = ty * TILE + 2 * warp + (lane >> 4);
-    const int wy0 = ty * TILE + 2 * warp;
-    const bool inside = px < cam.width && py < cam.height;
-    const double pcx = px + 0.5, pcy = py + 0.5;
-    const int s = tile_start[t];
-    int my_last = -1;
-    double Tc = 1.0;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-    if (inside) {
-        const int p = py * cam.width + px;
-        my_last = last_pos[p];
-        Tc = t_final[p];
-        d0 = d_image[p * 3 + 0];
-        d1 = d_image[p * 3 + 1];
-        d2 = d_image[p * 3 + 2];
-    }
-    double S0 = Tc * opt.bg[0], S1 = Tc * opt.bg[1], S2 = Tc * opt.bg[2];
-    if (threadIdx.x == 0) s_hi = -1;
-    __syncthreads();
-    if (my_last >= 0) atomicMax(&s_hi, my_last);
-    __syncthreads();
-    const int hi = s_hi;
-    // lane -> reduced component after the butterfly: k = bits(16,8,4,2) of lane
-    const int kred = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    for (int bend = hi + 1; bend > s; bend -= BB) {
-        const int bstart = max(s, bend - BB);
-        const int nb = bend - bstart;
-        __syncthreads();
-        for (int c = threadIdx.x; c < nb * 16; c += blockDim.x) {
-            const int j = c >> 4, q = c & 15;
-            const unsigned src = __ldg(ent_src + bstart + j);
-            if (q < 8)
-                reinterpret_cast<float4*>(&s_rec[j])[q] = __ldg(reinterpret_cast<const float4*>(rec + src) + q);
-            else
-                reinterpret_cast<float4*>(&s_rb[j])[q - 8] = __ldg(reinterpret_cast<const float4*>(recb + src) + (q - 8));
-            if (q == 0) {
-                s_src[j] = src;
-                const double o = opt.solid ? 1.0 : (double)opacity[src];
-                s_os[j] = make_double4(o, (double)sigma[src], 1.0 / o, 0.0);
-            }
-        }
-        for (int c = threadIdx.x; c < 8 * BB * 12; c += blockDim.x) (&s_part[0][0][0])[c] = 0.f;
-        __syncthreads();
-        if (threadIdx.x < nb) s_os[threadIdx.x].w = 1.0 / s_rec[threadIdx.x].phis;
-        __syncthreads();
-        const int jl = (int)lane;
-        const bool ov = jl < nb && s_rec[jl].y0 <= wy0 + 1 && s_rec[jl].y1 > wy0;
-        unsigned mask = __ballot_sync(0xffffffffu, ov);
-        while (mask) {
-            const int j = 31 - __clz(mask);
-            mask &= ~(1u << j);
-            const RecF& r = s_rec[j];
-            const int pos = bstart + j;
-            double g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0, g5 = 0, g6 = 0, g7 = 0, g8 = 0, g9 = 0, g10 = 0, g11 = 0;
-            bool act = false;
-            if (pos <= my_last && px >= r.x0 && px < r.x1 && py >= r.y0 && py < r.y1) {
-                const double l0 = fma(r.a[0], pcx, fma(r.a[1], pcy, r.a[2]));
-                const double l1 = fma(r.a[3], pcx, fma(r.a[4], pcy, r.a[5]));
-                const double l2 = fma(r.a[6], pcx, fma(r.a[7], pcy, r.a[8]));
-                // argmax of phi = argmin of phi/phi_s; ties -> lowest edge (strict >, _kernels.py:36-42)
-                int edge = 0;
-                double rr = l0;
-                if (l1 < rr) { rr = l1; edge = 1; }
-                if (l2 < rr) { rr = l2; edge = 2; }
-                if (rr >= r.r_lo) {
-                    const double4 os = s_os[j];
-                    double a;
-                    const double rc = rr < 1.0 ? rr : 1.0;
-                    if (opt.mode == 0) {
-                        a = rr <= 0.0 ? 0.0 : os.x * (os.y == 1.0 ? rc : pow(rc, os.y));
-                    } else {
-                        double x = rr * r.phis / os.y;
-                        if (x > 700.0) x = 700.0;
-                        a = os.x / (1.0 + exp(x));
-                    }
-                    const bool clamped = a > ALPHA_CLAMP;
-                    if (clamped) a = ALPHA_CLAMP;
-                    if (a >= ALPHA_MIN) {
-                        act = true;
-                        const double inv1m = 1.0 / (1.0 - a);
-                        const double tb = Tc * inv1m;
-                        const double w = tb * a;
-                        const float* c = r.rgb;
-                        g8 = w * d0;
-                        g9 = w * d1;
-                        g10 = w * d2;
-                        const double ga = d0 * (tb * c[0] - S0 * inv1m) + d1 * (tb * c[1] - S1 * inv1m) +
-                                          d2 * (tb * c[2] - S2 * inv1m);
-                        S0 = fma(w, (double)c[0], S0);
-                        S1 = fma(w, (double)c[1], S1);
-                        S2 = fma(w, (double)c[2], S2);
-                        Tc = tb;
-                        if (!clamped) {
-                            const double window = a * os.z;
-                            g6 = ga * window;  // d/d opacity = g_alpha * alpha / o
-                            const double g_win = os.x * ga;
-                            const double phi = rr * r.phis;
-                            double g_phi;
-                            if (opt.mode == 0) {
-                                g7 = g_win * window * log(rc);
-                                const double g_r = g_win * os.y * window / rc;
-                                if (rr >= 1.0) {
-                                    g_phi = 0.0;
-                                } else {
-                                    g_phi = g_r * os.w;
-                                    g11 = -g_r * rr * os.w;
-                                }
-                            } else {
-                                // window*(1-window) = E/(1+E)^2 with E = exp(phi/sigma): no cancellation
-                                const double E = exp(fmin(phi / os.y, 700.0));
-                                const double ww = E / ((1.0 + E) * (1.0 + E));
-                                const double is = 1.0 / os.y;
-                                g7 = g_win * ww * phi * is * is;
-                                g_phi = -g_win * ww * is;
-                            }
-                            const RecB& rb = s_rb[j];
-                            const int ib = edge == 2 ? 0 : edge + 1;
-                            const double ax = rb.qx[edge], ay = rb.qy[edge], bx = rb.qx[ib], by = rb.qy[ib];
-                            const double pxr = (double)(px - r.ox) + 0.5, pyr = (double)(py - r.oy) + 0.5;
-                            const double sl = rb.sl[edge], ul = rb.ul[edge], vl = rb.vl[edge];
-                            const double gax = g_phi * (sl * (pyr - by) + phi * ul);
-                            const double gay = g_phi * (sl * (bx - pxr) + phi * vl);
-                            const double gbx = g_phi * (sl * (ay - pyr) - phi * ul);
-                            const double gby = g_phi * (sl * (pxr - ax) - phi * vl);
-                            g0 = edge == 0 ? gax : (ib == 0 ? gbx : 0.0);
-                            g1 = edge == 0 ? gay : (ib == 0 ? gby : 0.0);
-                            g2 = edge == 1 ? gax : (ib == 1 ? gbx : 0.0);
-                            g3 = edge == 1 ? gay : (ib == 1 ? gby : 0.0);
-                            g4 = edge == 2 ? gax : (ib == 2 ? gbx : 0.0);
-                            g5 = edge == 2 ? gay : (ib == 2 ? gby : 0.0);
-                        }
-                    }
-                }
-            }
-            if (__any_sync(0xffffffffu, act)) {
-                // butterfly reduce-scatter of 16 values (12 used) over the warp
-                const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0, h4 = (lane & 4) != 0, h2 = (lane & 2) != 0;
-                double a0 = h16 ? g8 : g0, b0 = h16 ? g0 : g8;
-                double a1 = h16 ? g9 : g1, b1 = h16 ? g1 : g9;
-                double a2 = h16 ? g10 : g2, b2 = h16 ? g2 : g10;
-                double a3 = h16 ? g11 : g3, b3 = h16 ? g3 : g11;
-                double a4 = h16 ? 0.0 : g4, b4 = h16 ? g4 : 0.0;
-                double a5 = h16 ? 0.0 : g5, b5 = h16 ? g5 : 0.0;
-                double a6 = h16 ? 0.0 : g6, b6 = h16 ? g6 : 0.0;
-                double a7 = h16 ? 0.0 : g7, b7 = h16 ? g7 : 0.0;
-                a0 = bfly_step(a0, b0, 16); a1 = bfly_step(a1, b1, 16); a2 = bfly_step(a2, b2, 16);
-                a3 = bfly_step(a3, b3, 16); a4 = bfly_step(a4, b4, 16); a5 = bfly_step(a5, b5, 16);
-                a6 = bfly_step(a6, b6, 16); a7 = bfly_step(a7, b7, 16);
-                // 8 values: local index i holds component (h16 ? 8 : 0) + i
-                double c0 = h8 ? a4 : a0, e0 = h8 ? a0 : a4;
-                double c1 = h8 ? a5 : a1, e1 = h8 ? a1 : a5;
-                double c2 = h8 ? a6 : a2, e2 = h8 ? a2 : a6;
-                double c3 = h8 ? a7 : a3, e3 = h8 ? a3 : a7;
-                c0 = bfly_step(c0, e0, 8); c1 = bfly_step(c1, e1, 8); c2 = bfly_step(c2, e2, 8); c3 = bfly_step(c3, e3, 8);
-                double f0 = h4 ? c2 : c0, h0 = h4 ? c0 : c2;
-                double f1 = h4 ? c3 : c1, h1 = h4 ? c1 : c3;
-                f0 = bfly_step(f0, h0, 4); f1 = bfly_step(f1, h1, 4);
-                double z = h2 ? f1 : f0, zs = h2 ? f0 : f1;
-                z = bfly_step(z, zs, 2);
-                z += __shfl_xor_sync(0xffffffffu, z, 1);
-                if ((lane & 1) == 0 && kred < 12) s_part[warp][j][kred] = (float)z;
-            }
-        }
-        __syncthreads();
-        for (int c = threadIdx.x; c < nb * 12; c += blockDim.x) {
-            const int j = c / 12, k = c - j * 12;
-            double v = 0.0;
-#pragma unroll
-            for (int w = 0; w < 8; w++) v += (double)s_part[w][j][k];
-            if (v != 0.0) atomicAdd(sgrad + (size_t)s_src[j] * SG_STRIDE + k, v);
-        }
-    }
-}
-
-void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
-                           const RecB* recb, const int* tile_start, const unsigned* ent_src,
-                           const double* t_final, const int* last_pos, const float* d_image, double* sgrad,
-                           cudaStream_t st) {
-    int ntiles = cam.ntx * cam.nty;
-    if (dtype == 1)
-        k_blend_bwd_fast<double><<<ntiles, 256, 0, st>>>(cam, opt, (const double*)soup.vertices,
-                                                         (const double*)soup.opacity,
-                                                         (const double*)soup.sigma, rec, recb, tile_start,
-                                                         ent_src, t_final, last_pos, d_image, sgrad);
-    else
-        k_blend_bwd_fast<float><<<ntiles, 256, 0, st>>>(cam, opt, (const float*)soup.vertices,
-                                                        (const float*)soup.opacity,
-                                                        (const float*)soup.sigma, rec, recb, tile_start,
-                                                        ent_src, t_final, last_pos, d_image, sgrad);
-}
 
 }  // namespace ts

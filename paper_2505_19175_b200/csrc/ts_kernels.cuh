@@ -42,7 +42,8 @@ struct PreOut {
 
 struct FastPreOut {
     RecF* rec;                 // (N) fast records (accepted with tiles only)
-    RecB* recb;                // (N) backward records, nullable
+    RecB* recb;                // (N) backward records, nullable (training forwards)
+    RecC* recc;                // (N) fp64 colour / opacity / sigma, nullable (training forwards)
     short4* bbox;              // (N)
     unsigned long long* key;
     unsigned* tcount;
@@ -77,6 +78,7 @@ struct FastBlendOut {
     FragRec* frec;
     unsigned long long frec_cap;
     double* c_total64;         // (P,3) unclipped colour incl. T_final * background
+    const RecC* recc;          // training forwards: fp64 colours of the sources
 };
 
 struct BlendOut {
@@ -108,31 +110,27 @@ void launch_chain_bwd32(const Cam& cam, const Opts& opt, const ts_soup& soup, in
 // ts_fast.cu
 void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
                             const FastPreOut& out, cudaStream_t st);
-void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64,
-                       const RecF* rec, const short4* bbox, const int* tile_start, const unsigned* ent_src,
-                       const FastBlendOut& out, cudaStream_t st);
+void launch_blend_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
+                       const short4* bbox, const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
+                       cudaStream_t st);
 void launch_fixup_fwd(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
                       const int* tile_start, const unsigned* ent_src, const FastBlendOut& out,
                       cudaStream_t st);
-void launch_blend_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
-                           const RecB* recb, const int* tile_start, const unsigned* ent_src,
-                           const double* t_final, const int* last_pos, const float* d_image, double* sgrad,
-                           cudaStream_t st);
 
 // ts_blend.cu: render-only forward blend (dense pair evaluation)
-void launch_blend_dense(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, bool acc64, const RecF* rec,
-                        const int* tile_start, const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st);
+void launch_blend_dense(const Cam& cam, const Opts& opt, bool acc64, const RecF* rec, const int* tile_start,
+                        const unsigned* ent_src, const FastBlendOut& out, cudaStream_t st);
 
 // ts_bwd.cu: dense backward blend
-void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb,
+void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
                             const int* tile_start, const unsigned* ent_src, const double* t_final,
                             const int* last_pos, const float* d_image, const int* n_frag, const long long* frag_off,
                             const double* fg_dw, const double* fg_dz, const unsigned long long* run_if, double* sgrad,
                             cudaStream_t st);
 // ts_bwd_stream.cu: streaming backward over the training forward's fragment records
-void launch_bwd_stream(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const RecF* rec,
-                       const RecB* recb, const FragRec* frec, const Counters* ctr, unsigned long long cap,
-                       const double* c_total, const float* d_image, double* sgrad, cudaStream_t st);
+void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
+                       const FragRec* frec, const Counters* ctr, unsigned long long cap, const double* c_total,
+                       const float* d_image, double* sgrad, cudaStream_t st);
 
 // ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
 bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,

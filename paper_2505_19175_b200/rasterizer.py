@@ -77,6 +77,14 @@ class DeviceSoup:
         for t in (self.vertices, self.opacity, self.sigma, self.sh):
             if not t.is_cuda or not t.is_contiguous() or t.dtype != self.vertices.dtype:
                 raise ValueError("DeviceSoup tensors must be contiguous CUDA tensors of one dtype")
+        n = len(self)
+        shapes = {"vertices": (tuple(self.vertices.shape), (n, 3, 3)),
+                  "opacity": (tuple(self.opacity.shape), (n,)),
+                  "sigma": (tuple(self.sigma.shape), (n,)),
+                  "sh": (tuple(self.sh.shape), (n, 16, 3))}
+        for name, (got, want) in shapes.items():
+            if got != want:
+                raise ValueError(f"DeviceSoup.{name} must have shape {want}, got {got}")
         return _lib.TsSoup(self.vertices.data_ptr(), self.opacity.data_ptr(),
                            self.sigma.data_ptr(), self.sh.data_ptr(), len(self))
 
@@ -177,6 +185,16 @@ def make_options(mode=0, background=(0.0, 0.0, 0.0), tau_cutoff=DEFAULT_TAU_CUTO
 _NONFINITE_GROUPS = ("vertices", "opacity", "sigma", "sh")
 
 
+def _check_grads(grads: "DeviceGrads", n: int):
+    """The kernels write 59 * n floats of the last forward's soup: the buffer
+    must be sized for exactly that soup (a DeviceGrads kept across a densify
+    step would otherwise be written past its end)."""
+    if grads.n != n or grads.flat.numel() != 59 * n or not grads.flat.is_contiguous() \
+            or grads.flat.dtype != torch.float32 or not grads.flat.is_cuda:
+        raise ValueError(f"gradient buffer is for {grads.n} triangles ({grads.flat.numel()} floats), "
+                         f"the last forward had {n} (needs {59 * n} contiguous float32 on the GPU)")
+
+
 class Rasterizer:
     """One C-ABI context (scratch memory + last forward state) on one device."""
 
@@ -196,6 +214,10 @@ class Rasterizer:
                 self.lib.ts_context_destroy(self._ctx)
         except Exception:
             pass
+
+    def set_option(self, option: int, value: int):
+        """Cross-check paths for tests (_lib.TS_OPT_LEGACY_BINNING, TS_OPT_TILE_BACKWARD)."""
+        _lib.check(self.lib.ts_set_option(self._ctx, int(option), int(value)), "set_option")
 
     def launch_count(self) -> int:
         return int(self.lib.ts_launch_count(self._ctx))
@@ -217,6 +239,9 @@ class Rasterizer:
         dev = torch.device("cuda", self.device)
         st = (stream or torch.cuda.current_stream(dev)).cuda_stream
         rc = self.lib.ts_forward_status(self._ctx, ctypes.byref(res), ctypes.c_void_p(st))
+        if rc != _lib.TS_OK:
+            self._last = None
+            self._last_soup = None
         if rc == _lib.TS_ERR_NONFINITE:
             for g, idx in zip(_NONFINITE_GROUPS, res.err_index):
                 if idx >= 0:
@@ -267,6 +292,9 @@ class Rasterizer:
         rc = self.lib.ts_forward(self._ctx, ctypes.byref(cam), ctypes.byref(opt),
                                  ctypes.byref(ts), ctypes.byref(fo), ctypes.byref(res),
                                  ctypes.c_void_p(st))
+        if rc != _lib.TS_OK:  # the context keeps no state of a failed frame
+            self._last = None
+            self._last_soup = None
         if rc == _lib.TS_ERR_NONFINITE:
             for g, idx in zip(_NONFINITE_GROUPS, res.err_index):
                 if idx >= 0:
@@ -289,6 +317,7 @@ class Rasterizer:
         if grads is None:
             grads = DeviceGrads(torch.empty(n * 59, dtype=torch.float32, device=d_image.device), n)
             accumulate = False
+        _check_grads(grads, n)
         st = (stream or torch.cuda.current_stream(d_image.device)).cuda_stream
         g = grads._ts()
         _lib.check(self.lib.ts_backward(self._ctx, _ptr(d_image), ctypes.byref(g),
@@ -334,6 +363,7 @@ class Rasterizer:
         if grads is None:
             grads = DeviceGrads(torch.empty(n * 59, dtype=torch.float32, device=dev), n)
             accumulate = False
+        _check_grads(grads, n)
         st = (stream or torch.cuda.current_stream(dev)).cuda_stream
         g = grads._ts()
         rc = self.lib.ts_backward_fragments(self._ctx, _ptr(d_image), _ptr(offsets), _ptr(d_weight),

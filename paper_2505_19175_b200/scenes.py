@@ -71,8 +71,12 @@ def make_scene(cfg: SceneConfig | str):
     return soup, intr, pose
 
 
-def make_d_image(seed: int, height: int, width: int) -> np.ndarray:
-    return np.random.default_rng(seed + 100).normal(size=(height, width, 3))
+def make_d_image(seed: int, height: int, width: int, fp32: bool = False) -> np.ndarray:
+    """Upstream image gradient N(0,1); ``fp32=True`` rounds it to fp32 values
+    (held in fp64) so the device's fp32 d_image and the fp64 oracle see the
+    same numbers, as the scene parameters do."""
+    d = np.random.default_rng(seed + 100).normal(size=(height, width, 3))
+    return d.astype(np.float32).astype(np.float64) if fp32 else d
 
 
 def look_at(center, target) -> CameraPose:
