@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrisplat_b200.so")
+LIB_PATH = os.environ.get("TRISPLAT_B200_LIB") or os.path.join(HERE, "libtrisplat_b200.so")
 
 TS_OK = 0
 TS_ERR_NONFINITE = -5
@@ -23,6 +23,8 @@ TS_DUMP_BBOX = 4
 TS_DUMP_DEPTH = 5
 TS_DUMP_SGRAD = 6
 TS_DUMP_FRAGREC = 7
+TS_DUMP_PROJECTION = 8
+PROJ_ROW = 64
 
 
 class TsCamera(ctypes.Structure):
@@ -69,7 +71,8 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_backward_fragments", "ts_set_async", "ts_forward_status", "ts_set_option", "ts_photometric_loss",
            "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
-           "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack"]
+           "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack",
+           "ts_tile_lists"]
 TS_OPT_LEGACY_BINNING = 1
 TS_OPT_TILE_BACKWARD = 2
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
@@ -147,6 +150,8 @@ def load(path: str = LIB_PATH):
     lib.ts_child_vertices.argtypes = [V, I64, V, V, V, D, V, V, I, V]
     lib.ts_ply_pack.argtypes = [V, V, V, I, I64, V, V, V]
     lib.ts_ply_unpack.argtypes = [V, V, I64, V, I64, D, I, V, V, V, V, V, V]
+    lib.ts_tile_lists.argtypes = [V, V, I64, I, I, I, V, V, P(ctypes.c_int64), V]
+    lib.ts_tile_lists.restype = ctypes.c_int
     for nm in ("ts_ply_pack", "ts_ply_unpack", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",
                "ts_gather_rows", "ts_child_vertices"):
         getattr(lib, nm).restype = ctypes.c_int

@@ -38,6 +38,12 @@ namespace ts {
 namespace {
 constexpr float T_MIN_F = 1e-4f;
 constexpr float ALPHA_CLAMP_F = 0.99f;
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 }  // namespace
 
 template <int DB, int PCAP, bool ACC64>
@@ -48,7 +54,7 @@ struct DenseSmem {
     TailRec tail[RR];
     RecC rc[ACC64 ? RR : 1];       // training forwards: fp64 colour, opacity, sigma of the ring slots
     Real r[PCAP];                  // per pair: render: alpha (clamped); training: r; NaN = inside the band
-    float ea[ACC64 ? 1 : PCAP];    // render: relative error bound of the fp32 alpha
+    float2 eq[ACC64 ? 1 : PCAP];   // render: relative error increments of the fp32 weight and transmittance
     unsigned mask[NW][256];        // per pixel: bit j = entry j passes (r >= r_lo)
     unsigned srcq[SR];
     float4 col[DB];                // rgb, f0
@@ -58,7 +64,7 @@ struct DenseSmem {
     unsigned starts[PCAP / 32];    // bit (k & 31) of word k >> 5: a segment starts at pair k
     int jfirst[PCAP / 32];         // segment holding pair 32 w
     unsigned ein[DB];              // per entry: inclusive (pairs<<16 | segments) within its warp
-    unsigned wtot[8];              // per warp: (pairs<<16 | segments) of its 8 entries
+    __align__(16) unsigned wtot[8];  // per warp: (pairs<<16 | segments) of its 8 entries
     int total;                     // pairs of the batch
     unsigned pbits[ACC64 ? PCAP / 32 : 1];      // training: pair k passes (record slots)
     int wpre[ACC64 ? PCAP / 32 + 1 : 1];        // passing pairs before word w
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                     for (int ed = 0; ed < 3; ed++) {
                         const double a0 = R.a[3 * ed], a1 = R.a[3 * ed + 1];
                         const double n0 = rlo - fma(a0, xl, fma(a1, y0, R.a[3 * ed + 2]));
-                        const float inv = __fdividef(1.f, (float)a0);
+                        const float inv = rcp_approx((float)a0);  // (1 ulp; |a0| < 2^-126: inf, not finite)
                         tb0[ed] = (float)n0 * inv;
                         sl[ed] = (float)(-4.0 * a1) * inv;
                         const bool fin = fabsf(inv) < 1e30f && fabsf(tb0[ed]) < 1e6f && fabsf(sl[ed]) < 1e4f;
@@ -225,14 +231,20 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             if (q == 0) sm.ein[j] = ei;
             if (lane == 31) sm.wtot[warp] = ei;
             __syncthreads();
-            unsigned wpre = 0;
-            for (int w2 = 0; w2 < (int)warp; w2++) wpre += sm.wtot[w2];
+            unsigned wpre = 0, all = 0;
+            {
+                const uint4 wa = reinterpret_cast<const uint4*>(sm.wtot)[0];
+                const uint4 wb = reinterpret_cast<const uint4*>(sm.wtot)[1];
+                const unsigned wt[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+                for (int w2 = 0; w2 < 8; w2++) {
+                    wpre += w2 < (int)warp ? wt[w2] : 0u;
+                    all += wt[w2];
+                }
+            }
             // batch = longest prefix of entries whose pairs fit in PCAP (>= 1 entry)
             int n = 0;
             {
-                unsigned all = 0;
-#pragma unroll
-                for (int w2 = 0; w2 < 8; w2++) all += sm.wtot[w2];
                 if ((all >> 16) <= (unsigned)PCAP) {
                     n = navail;
                 } else {
@@ -331,7 +343,9 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                                 a = fminf(a, ALPHA_CLAMP_F);
                             }
                             sm.r[k] = a;
-                            sm.ea[k] = ea;
+                            // error increments of the weight T a (ea + 1.2e-7) and of the
+                            // transmittance T (1 - a) (ea a / (1 - a) + 2.4e-7; 1 - a >= 0.01)
+                            sm.eq[k] = make_float2(ea + 1.2e-7f, fmaf(ea * a, rcp_approx(1.f - a), 2.4e-7f));
                         }
                         atomicOr(&sm.mask[j >> 5][qy * TILE + qx], 1u << (j & 31));
                     }
@@ -452,12 +466,11 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         if (wd64 > opt.tau_contrib) red_add_shared(&sm.pix[j], 1);
                     } else {
                         const float a = (float)rv;  // alpha of the evaluation (clamped)
-                        const float ea = sm.ea[kp];
                         const float wgt = T * a;
                         const float tn = fmaf(-T, a, T);
-                        // (approximate quotient: the tests below keep a 2x margin on en)
-                        const float en = __fdividef(ea * a, 1.f - a) + (epsT + 2.4e-7f);
-                        const float ew = epsT + ea + 1.2e-7f;
+                        // relative error bounds of tn and of wgt (the tests keep a 2x margin)
+                        const float2 eq = sm.eq[kp];
+                        const float en = epsT + eq.y, ew = epsT + eq.x;
                         if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
                             fabsf(wgt - tau) <= fmaf(2.f * ew, wgt, 1e-9f)) {
                             flag_pos = b + j;

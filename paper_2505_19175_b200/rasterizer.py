@@ -425,11 +425,24 @@ def _param_dtype(soup):
     return torch.float32 if v.dtype == np.float32 else torch.float64
 
 
+# bytes the last render() copied device -> host (bench.py's e2e accounting)
+LAST_RENDER_D2H_BYTES = 0
+
+
+def _to_numpy(t: torch.Tensor, dtype) -> np.ndarray:
+    """Device tensor -> new numpy array of ``dtype`` (converted on the device)."""
+    out = np.empty(tuple(t.shape), dtype=dtype)
+    host = torch.from_numpy(out)
+    host.copy_(t.to(dtype=host.dtype))
+    return out
+
+
 def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
            collect_fragments: bool = False, tau_cutoff: float = DEFAULT_TAU_CUTOFF,
            tile_size: int = DEFAULT_TILE_SIZE, active_sh_degree: int = 3,
            precision: str = "fast") -> RenderOutput:
     """Drop-in for trisplat.render.render (render.py:364-432)."""
+    global LAST_RENDER_D2H_BYTES
     _require_cuda()
     soup = as_soup(triangles)
     if collect_fragments and precision != "fast":
@@ -439,12 +452,17 @@ def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
     fwd = rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
                        precision=precision)
     frags = rast.fragments().to_fragment_data() if collect_fragments else None
-    return RenderOutput(image=ImageBuffer(fwd.image.double().cpu().numpy()),
-                        alpha_map=fwd.alpha_map.double().cpu().numpy(),
-                        per_triangle_max_weight=fwd.max_weight.double().cpu().numpy(),
-                        per_triangle_pixel_count=fwd.pixel_count.cpu().numpy().astype(np.int64),
-                        per_triangle_area=fwd.area.double().cpu().numpy(),
-                        fragments=frags)
+    image = _to_numpy(fwd.image, np.float64)
+    alpha = _to_numpy(fwd.alpha_map, np.float64)
+    maxw = _to_numpy(fwd.max_weight, np.float64)
+    pixc = _to_numpy(fwd.pixel_count, np.int64)
+    area = _to_numpy(fwd.area, np.float64)
+    LAST_RENDER_D2H_BYTES = image.nbytes + alpha.nbytes + maxw.nbytes + pixc.nbytes + area.nbytes
+    if frags is not None:
+        LAST_RENDER_D2H_BYTES += sum(np.asarray(a).nbytes for a in (frags.offsets, frags.triangle,
+                                                                      frags.weight, frags.depth))
+    return RenderOutput(image=ImageBuffer(image), alpha_map=alpha, per_triangle_max_weight=maxw,
+                        per_triangle_pixel_count=pixc, per_triangle_area=area, fragments=frags)
 
 
 def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d_image=None,
