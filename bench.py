@@ -432,13 +432,13 @@ def e2e_render(args, soup, intr, pose, world, max_over_ranks):
     import torch
     import torch.distributed as dist
 
-    import paper_2505_19175_b200 as tsb
+    from paper_2505_19175_b200 import rasterizer as tsb
     n = len(soup.vertices)
     h2d = sum(np.asarray(getattr(soup, k)).nbytes for k in ("vertices", "opacity", "sigma", "sh"))
     out = None
     for _ in range(2):
         out = tsb.render(soup, intr, pose)
-    d2h = int(tsb.rasterizer.LAST_RENDER_D2H_BYTES)
+    d2h = int(tsb.LAST_RENDER_D2H_BYTES)
     steps = max(3, min(args.steps, 20))
     if world > 1:
         dist.barrier()

@@ -150,6 +150,16 @@ int ts_set_option(ts_context* ctx, int option, int64_t value);
 int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream);
 
+/* ts_backward with the final chain to the 59 parameter gradients split into
+ * n_chunks triangle ranges [bounds[k], bounds[k+1]) (host int64[n_chunks+1]:
+ * bounds[0] = 0, bounds[n_chunks] = N, every bounds[k < n_chunks] a multiple
+ * of 64), recording the caller's CUDA event events[k] (cudaEvent_t) on the
+ * stream once range k's gradients are final.  A view-parallel trainer makes
+ * its collective stream wait on events[k] and all-reduces that bucket while
+ * the next range computes. */
+int ts_backward_chunked(ts_context* ctx, const float* d_image, const ts_grads* grads, int accumulate, int n_chunks,
+                        const int64_t* bounds, void* const* events, void* stream);
+
 /* Fragment lists of the last ts_forward: render(collect_fragments=True)
  * (render.py:383-399, 420-425; count_fragments _kernels.py:135-178,
  * collect branch _kernels.py:107-116).
@@ -213,12 +223,14 @@ int ts_fragment_depth(ts_context* ctx, const int64_t* offsets, const double* wei
  * (vertices (N,3,3), opacity (N), sigma (N), sh (N,16,3)) with the gradients
  * of ts_backward; m, v: device fp32 moments of 59 N elements in the flat
  * gradient layout [vertices | opacity | sigma | sh], zero-initialised by the
- * caller; t: the step number after this step (1 for the first); lrs: host
+ * caller; t: device int64[1], the steps taken so far (AdamState.t): this
+ * step uses t + 1 for the bias correction and t is incremented only if the
+ * update ran (no non-finite gradient); lrs: host
  * double[4] per-group rates; bad: device int64[4] receiving, per group, the
  * first triangle with a non-finite gradient (-1 if none) -- if any
  * group has one, nothing is updated (the reference raises ValueError). */
 int ts_adam_step(ts_context* ctx, float* vertices, float* opacity, float* sigma, float* sh, int64_t n,
-                 const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
+                 const ts_grads* grads, float* m, float* v, int64_t* t, const double* lrs, int64_t* bad,
                  void* stream);
 
 /* ---------------- adaptive density control (density.py:27-263) ----------------
@@ -305,7 +317,21 @@ int ts_ply_unpack(ts_context* ctx, const uint8_t* vertex_bytes, int64_t n_vertex
 /*  TS_DUMP_FRAGREC uint64 count, then count x 48-byte fragment records of the
  *                  last training forward (T, C[3] fp64; pixel, source, ordinal u32) */
 #define TS_DUMP_FRAGREC 7
+/*  TS_DUMP_PROJECTION float64[M*64 + N]: project_scene (render.py:253-312) of the
+ *                  last forward, one row of 64 per depth-sorted accepted triangle:
+ *                  xc[9] q[6] z area phis nrm[6] doff[3] esign[3] sig opa rgb[3]
+ *                  raw_rgb[3] basis[16] viewdir[3] u_norm bbox[4] (2 pad), in the
+ *                  reference's fp64 operation order; then area_full[N] */
+#define TS_DUMP_PROJECTION 8
 int ts_debug_copy(ts_context* ctx, int what, void* dst, size_t bytes, void* stream);
+
+/* build_tile_lists (render.py:315-361) for any tile size >= 1: bbox is the
+ * device int64 (M x 4) x0,x1,y0,y1 of M triangles in depth-rank order; writes
+ * the device CSR tile_start (int64[ntx*nty+1]) and entry_tri (int64[E], ranks;
+ * each tile's list in rank order) and *n_entries = E.  With tile_start or
+ * entry_tri null it only returns E (size query).  Synchronises the stream. */
+int ts_tile_lists(ts_context* ctx, const int64_t* bbox, int64_t m, int tile_size, int width, int height,
+                  int64_t* tile_start, int64_t* entry_tri, int64_t* n_entries, void* stream);
 
 /* Per-stage device timing with CUDA events recorded on the call's stream.
  * ts_profile(ctx, 1) enables it; ts_stage_times fills ms[TS_NUM_STAGES] with

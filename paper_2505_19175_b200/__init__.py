@@ -7,13 +7,13 @@ include/trisplat_b200.h.  See DESIGN.md.
 __version__ = "0.1.0"
 
 from .types import (CameraIntrinsics, CameraPose, FragmentData, GradientSet,  # noqa: F401
-                    ImageBuffer, RenderOutput, Triangle3D, TriangleSoup, WindowMode)
+                    ImageBuffer, RenderOutput, SceneProjection, Triangle3D, TriangleSoup, WindowMode)
 
 
 def __getattr__(name):
     # torch-dependent API is imported lazily so the types stay importable
     # without a GPU stack.
-    if name in ("render", "render_backward", "install", "Rasterizer", "DeviceSoup",
+    if name in ("render", "render_backward", "project_scene", "build_tile_lists", "install", "Rasterizer", "DeviceSoup",
                 "DeviceGrads", "ForwardResult", "default_rasterizer"):
         from . import rasterizer
         return getattr(rasterizer, name)

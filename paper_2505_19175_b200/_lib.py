@@ -72,7 +72,7 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
            "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack",
-           "ts_tile_lists"]
+           "ts_tile_lists", "ts_backward_chunked"]
 TS_OPT_LEGACY_BINNING = 1
 TS_OPT_TILE_BACKWARD = 2
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
@@ -129,7 +129,7 @@ def load(path: str = LIB_PATH):
                             ctypes.c_void_p, ctypes.c_void_p]
     lib.ts_ssim.restype = ctypes.c_int
     lib.ts_adam_step.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 4 + [ctypes.c_int64, P(TsGrads),
-                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                  P(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p]
     lib.ts_adam_step.restype = ctypes.c_int
     lib.ts_distortion_loss.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + \
@@ -152,6 +152,8 @@ def load(path: str = LIB_PATH):
     lib.ts_ply_unpack.argtypes = [V, V, I64, V, I64, D, I, V, V, V, V, V, V]
     lib.ts_tile_lists.argtypes = [V, V, I64, I, I, I, V, V, P(ctypes.c_int64), V]
     lib.ts_tile_lists.restype = ctypes.c_int
+    lib.ts_backward_chunked.argtypes = [V, V, P(TsGrads), I, I, P(ctypes.c_int64), P(ctypes.c_void_p), V]
+    lib.ts_backward_chunked.restype = ctypes.c_int
     for nm in ("ts_ply_pack", "ts_ply_unpack", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",
                "ts_gather_rows", "ts_child_vertices"):
         getattr(lib, nm).restype = ctypes.c_int

@@ -2,6 +2,11 @@
 
     python -m paper_2505_19175_b200.build          # incremental
     python -m paper_2505_19175_b200.build --force
+    python -m paper_2505_19175_b200.build --checked  # + libtrisplat_b200_checked.so
+
+The checked build compiles the TS_ASSERT bounds / invariant checks into the
+kernels (device asserts); tests run against it with
+TRISPLAT_B200_LIB=paper_2505_19175_b200/libtrisplat_b200_checked.so.
 
 Translation units that restate fp64 reference arithmetic are compiled with
 ``-fmad=false`` (no FMA contraction, as numba without fastmath); the fast
@@ -46,30 +51,33 @@ def headers_mtime() -> float:
     return max(os.path.getmtime(h) for h in hs if os.path.exists(h))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    build_dir = BUILD + ("_checked" if checked else "")
+    lib = LIB.replace(".so", "_checked.so") if checked else LIB
+    extra_all = ["-DTS_CHECKED"] if checked else []
+    os.makedirs(build_dir, exist_ok=True)
     hm = headers_mtime()
     objs = []
-    changed = force or not os.path.exists(LIB)
+    changed = force or not os.path.exists(lib)
     for src in sources():
         sp = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if (not force and os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(sp)
                 and os.path.getmtime(obj) >= hm):
             continue
-        cmd = [nvcc()] + ARCH + COMMON + EXTRA.get(src, []) + ["-c", sp, "-o", obj]
+        cmd = [nvcc()] + ARCH + COMMON + extra_all + EXTRA.get(src, []) + ["-c", sp, "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         changed = True
-    if changed or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    if changed or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv)

@@ -50,6 +50,8 @@ struct ts_context {
     short4* bbox = nullptr;
     DevBuf rec64, recf, recb, recc, sg64, sg32;
     DevBuf frag_off, cs_scratch;  // expected fragment CSR offsets + scan scratch
+    DevBuf tl_cnt, tl_off, tl_cs, tl_kv;  // ts_tile_lists scratch
+    DevBuf adam_ibc;                      // Adam bias corrections of the current step
     DevBuf frec, ctot;            // training forward: fragment records + final unclipped colour
     unsigned long long frec_cap = 0;
     long long frec_hint = 0;      // largest fragment-record count seen (record-buffer sizing)
@@ -345,7 +347,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->tri_buf);
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
-    for (DevBuf* b : {&c->rec64, &c->recf, &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
+    for (DevBuf* b : {&c->adam_ibc, &c->tl_cnt, &c->tl_off, &c->tl_cs, &c->tl_kv, &c->rec64, &c->recf, &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
                       &c->ctot, &c->binmat, &c->lossbuf, &c->densbuf})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
@@ -673,12 +675,24 @@ int ts_set_option(ts_context* c, int option, int64_t value) {
 }
 
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
-                         const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream);
+                         const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream,
+                         int n_chunks = 0, const int64_t* bounds = nullptr, void* const* events = nullptr);
 
 int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream) {
     DeviceGuard device_guard(c);
     return backward_impl(c, d_image, grads, accumulate, nullptr, nullptr, nullptr, stream);
+}
+
+int ts_backward_chunked(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate, int n_chunks,
+                        const int64_t* bounds, void* const* events, void* stream) {
+    DeviceGuard device_guard(c);
+    if (!c || n_chunks < 1 || !bounds || !events) return TS_ERR_INVALID_ARG;
+    if (bounds[0] != 0 || bounds[n_chunks] != c->n) return TS_ERR_INVALID_ARG;
+    for (int k = 0; k < n_chunks; k++) {
+        if (bounds[k + 1] < bounds[k] || (bounds[k] & 63) || !events[k]) return TS_ERR_INVALID_ARG;
+    }
+    return backward_impl(c, d_image, grads, accumulate, nullptr, nullptr, nullptr, stream, n_chunks, bounds, events);
 }
 
 // expected fragment CSR offsets of the last forward into c->frag_off; returns F
@@ -766,7 +780,8 @@ int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* of
 }
 
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
-                         const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream) {
+                         const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream,
+                         int n_chunks, const int64_t* bounds, void* const* events) {
     if (!c || !d_image || !grads) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
@@ -796,8 +811,20 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
                                    nullptr, sg, st);
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
-        if (!launch_chain_bwd_fast(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st))
-            launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+        if (n_chunks > 0 && chain_bwd_fast_ok(c->soup, c->dtype, *grads)) {
+            // the chain in triangle ranges, an event after each: the caller's
+            // collective on a bucket can start while the next range computes
+            for (int k = 0; k < n_chunks; k++) {
+                launch_chain_bwd_fast(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st, bounds[k],
+                                      bounds[k + 1]);
+                TS_CHECK(cudaEventRecord((cudaEvent_t)events[k], st));
+            }
+            g_launches += n_chunks - 1;
+        } else {
+            if (!launch_chain_bwd_fast(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st))
+                launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+            for (int k = 0; k < n_chunks; k++) TS_CHECK(cudaEventRecord((cudaEvent_t)events[k], st));
+        }
         stage_end(c, TS_STAGE_CHAIN_BWD, st);
         c->sgrad_kind = 1;
     } else {
@@ -810,6 +837,7 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
         stage_end(c, TS_STAGE_BLEND_BWD, st);
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
         launch_chain_bwd(c->cam, c->opt, c->soup, c->dtype, c->flag, sg, *grads, accumulate, st);
+        for (int k = 0; k < n_chunks; k++) TS_CHECK(cudaEventRecord((cudaEvent_t)events[k], st));
         stage_end(c, TS_STAGE_CHAIN_BWD, st);
         c->sgrad_kind = 1;
     }
@@ -872,14 +900,17 @@ int ts_fragment_depth(ts_context* c, const int64_t* offsets, const double* weigh
 }
 
 int ts_adam_step(ts_context* c, float* vertices, float* opacity, float* sigma, float* sh, int64_t n,
-                 const ts_grads* grads, float* m, float* v, int64_t t, const double* lrs, int64_t* bad,
+                 const ts_grads* grads, float* m, float* v, int64_t* t, const double* lrs, int64_t* bad,
                  void* stream) {
     DeviceGuard device_guard(c);
-    if (!c || !grads || !lrs || !bad || n < 0 || t < 1) return TS_ERR_INVALID_ARG;
+    if (!c || !grads || !lrs || !bad || !t || n < 0) return TS_ERR_INVALID_ARG;
     if (n > 0 && (!vertices || !opacity || !sigma || !sh || !m || !v)) return TS_ERR_INVALID_ARG;
+    int rc;
+    if ((rc = ensure(c->adam_ibc, 2 * sizeof(double)))) return rc;
     float* const params[4] = {vertices, opacity, sigma, sh};
     const float* const g[4] = {grads->d_vertices, grads->d_opacity, grads->d_sigma, grads->d_sh};
-    launch_adam_step(params, g, n, m, v, t, lrs, (long long*)bad, (cudaStream_t)stream);
+    launch_adam_step(params, g, n, m, v, (long long*)t, lrs, (long long*)bad, (double*)c->adam_ibc.p,
+                     (cudaStream_t)stream);
     g_launches += n > 0 ? 2 : 0;
     return cuda_err(cudaGetLastError());
 }
@@ -1067,9 +1098,51 @@ int ts_debug_copy(ts_context* c, int what, void* dst, size_t bytes, void* stream
             TS_CHECK(cudaStreamSynchronize(st));
             return TS_OK;
         }
+        case TS_DUMP_PROJECTION: {
+            // project_scene of the last forward: PROJ_ROW doubles per depth-sorted
+            // accepted triangle, then area_full (N doubles)
+            if (bytes < 8 * ((size_t)PROJ_ROW * c->m + (size_t)c->n)) return TS_ERR_INVALID_ARG;
+            if (!c->sorted_valid) global_depth_order(c, c->n, st);
+            double* rows = (double*)dst;
+            launch_projection_dump(c->cam, c->opt, c->soup, c->dtype, c->sorted_src, c->m, rows,
+                                   rows + (size_t)PROJ_ROW * c->m, st);
+            g_launches += 1;
+            return cuda_err(cudaGetLastError());
+        }
         default:
             return TS_ERR_INVALID_ARG;
     }
+}
+
+int ts_tile_lists(ts_context* c, const int64_t* bbox, int64_t m, int tile_size, int width, int height,
+                  int64_t* tile_start, int64_t* entry_tri, int64_t* n_entries, void* stream) {
+    DeviceGuard device_guard(c);
+    if (!c || !n_entries || m < 0 || tile_size < 1 || width < 0 || height < 0 || (m > 0 && !bbox))
+        return TS_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long ntx = (width + tile_size - 1) / tile_size, nty = (height + tile_size - 1) / tile_size;
+    if (ntx * nty >= (1ll << 31)) return TS_ERR_INVALID_ARG;
+    const int ntiles = (int)(ntx * nty);
+    const long long m1 = m > 0 ? m : 1;
+    int rc;
+    if ((rc = ensure(c->tl_cnt, sizeof(int) * m1))) return rc;
+    if ((rc = ensure(c->tl_off, sizeof(long long) * (m1 + 1)))) return rc;
+    if ((rc = ensure(c->tl_cs, count_scan_scratch_bytes(m1)))) return rc;
+    tile_lists_count(m, (const long long*)bbox, tile_size, (int*)c->tl_cnt.p, (long long*)c->tl_off.p, c->tl_cs.p, st);
+    long long e = 0;
+    TS_CHECK(cudaMemcpyAsync(&e, (long long*)c->tl_off.p + m, sizeof(e), cudaMemcpyDeviceToHost, st));
+    TS_CHECK(cudaStreamSynchronize(st));
+    *n_entries = e;
+    if (!tile_start || (e > 0 && !entry_tri)) return TS_OK;  // size query
+    if (e >= (1ll << 32)) return TS_ERR_INVALID_ARG;
+    const long long e1 = e > 0 ? e : 1;
+    if ((rc = ensure(c->tl_kv, 4 * sizeof(unsigned) * (size_t)e1))) return rc;
+    unsigned* kv0 = (unsigned*)c->tl_kv.p;
+    unsigned* const kv[4] = {kv0, kv0 + e1, kv0 + 2 * e1, kv0 + 3 * e1};
+    tile_lists_fill(m, e, (const long long*)bbox, tile_size, (int)ntx, ntiles, (const long long*)c->tl_off.p, kv,
+                    c->sort, (long long*)tile_start, (long long*)entry_tri, st);
+    g_launches += 6;
+    return cuda_err(cudaGetLastError());
 }
 
 int ts_flagged_pixels(ts_context* c, int64_t* n_flagged) {

@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
             const unsigned long long y = s_item[j];
             if (y != x) rank += item_less(key64, y, x);
         }
+        TS_ASSERT(bs + rank < be && be <= cnt);
         ent_src[base + bs + rank] = (unsigned)x;
     }
     if (__syncthreads_or(longb))
@@ -592,7 +593,8 @@ __global__ void __launch_bounds__(BT) k_tile_sort_big(const int* __restrict__ bi
                 const unsigned long long y = s_item[j];
                 if (y != x) rank += item_less(key64, y, x);
             }
-            ent_src[base + bs + rank] = (unsigned)x;
+            TS_ASSERT(bs + rank < be && be <= cnt);
+        ent_src[base + bs + rank] = (unsigned)x;
         }
         if (__syncthreads_or(longb))
             sort_tile(cnt, bucket + base, key64, ent_src + base, gk0 + base, gv0 + base, gk1 + base, gv1 + base,

@@ -275,12 +275,16 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         const int ly2 = cy0 + q + 4 * m;
                         const unsigned pm = base + exl[m];
                         const unsigned P0 = pm >> 16, S0 = pm & 0xffffu;
+                        TS_ASSERT(P0 + (unsigned)len[m] <= (unsigned)PCAP && S0 < (unsigned)(DB * TILE) && ly2 < TILE);
                         sm.rowtab[j][ly2] = P0 | ((unsigned)xa[m] << 16);
                         sm.seg[S0] = P0 | ((unsigned)j << 13) | ((unsigned)ly2 << 19) | ((unsigned)xa[m] << 23);
                         atomicOr(&sm.starts[P0 >> 5], 1u << (P0 & 31));
                         // a segment (<= 16 pairs) holds at most one word start
                         const unsigned wq = (P0 + 31) >> 5;
-                        if ((wq << 5) <= P0 + (unsigned)len[m] - 1u) sm.jfirst[wq] = (int)S0;
+                        if ((wq << 5) <= P0 + (unsigned)len[m] - 1u) {
+                            TS_ASSERT(wq < (unsigned)(PCAP / 32));
+                            sm.jfirst[wq] = (int)S0;
+                        }
                     }
                     base += lev[m];
                 }
@@ -404,6 +408,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 const unsigned rth = sm.rowtab[j][ly];
                 const int kh = (int)(rth & 0xffffu) + lx - (int)(rth >> 16);
                 const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
+                TS_ASSERT(kh >= 0 && kh < sm.total && rb + slot < out.frec_cap);
                 out.frec[rb + slot].pix = ~0u;
             }
         };
@@ -416,7 +421,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                     mm &= mm - 1;
                     const unsigned rt = sm.rowtab[j][ly];
                     const int kp = (int)(rt & 0xffffu) + lx - (int)(rt >> 16);
-                    const Real rv = sm.r[kp];
+                    TS_ASSERT(kp >= 0 && kp < sm.total && ((sm.mask[j >> 5][tid] >> (j & 31)) & 1u));
+                const Real rv = sm.r[kp];
                     if (isnan(rv)) {  // r inside the contribution band
                         flag_pos = b + j;
                         done = true;
@@ -451,6 +457,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         if (rb != ~0ull) {
                             const int kr = kp;
                             const int slot = sm.wpre[kr >> 5] + __popc(sm.pbits[kr >> 5] & ((1u << (kr & 31)) - 1u));
+                            TS_ASSERT(rb + slot < out.frec_cap);
                             double4* fr = reinterpret_cast<double4*>(out.frec + rb + slot);
                             fr[0] = make_double4((double)T, (double)C0, (double)C1, (double)C2);
                             reinterpret_cast<uint4*>(fr + 1)[0] =

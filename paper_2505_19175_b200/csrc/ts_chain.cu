@@ -267,18 +267,31 @@ __global__ void __launch_bounds__(CB, 8) k_chain_bwd32(Cam cam, Opts opt, const 
     }
 }
 
+bool chain_bwd_fast_ok(const ts_soup& soup, int dtype, const ts_grads& g) {
+    // fp32 parameters, 16-byte vector access of the SH / gradient blocks
+    return dtype == 0 && !(((uintptr_t)soup.sh | (uintptr_t)g.d_sh | (uintptr_t)soup.vertices) & 15);
+}
+
 bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,
-                           const double* sgrad, const ts_grads& g, int accumulate, cudaStream_t st) {
-    const long long n = soup.n;
-    if (dtype != 0) return false;
-    // 16-byte vector access of the SH / gradient blocks
-    if (((uintptr_t)soup.sh | (uintptr_t)g.d_sh | (uintptr_t)soup.vertices) & 15) return false;
+                           const double* sgrad, const ts_grads& g, int accumulate, cudaStream_t st, long long lo,
+                           long long hi) {
+    if (!chain_bwd_fast_ok(soup, dtype, g)) return false;
+    if (hi < 0) hi = soup.n;
+    const long long n = hi - lo;
     if (n <= 0) return true;
+    // triangles [lo, hi) (lo a multiple of 64: the offset blocks stay 16-byte aligned)
+    const float* verts = (const float*)soup.vertices + 9 * lo;
+    const float* sh = (const float*)soup.sh + 48 * lo;
+    ts_grads gr = g;
+    gr.d_vertices += 9 * lo;
+    gr.d_opacity += lo;
+    gr.d_sigma += lo;
+    gr.d_sh += 48 * lo;
     const int smem = (int)sizeof(ChainStage);
     smem_optin((const void*)k_chain_bwd32, smem);
     const unsigned grid = (unsigned)((n + CB - 1) / CB);
-    launch_pdl(k_chain_bwd32, dim3(grid), dim3(CB), smem, st, cam, opt, (const float*)soup.vertices,
-               (const float*)soup.sh, flag, sgrad, n, g, accumulate);
+    launch_pdl(k_chain_bwd32, dim3(grid), dim3(CB), smem, st, cam, opt, verts, sh, flag + lo,
+               sgrad + (size_t)SG_STRIDE * lo, n, gr, accumulate);
     return true;
 }
 

@@ -6,6 +6,16 @@
 // unit can contract them into FMAs.  Citations are to /root/reference/pkg/src/trisplat.
 #pragma once
 #include <cuda_runtime.h>
+
+// Bounds / invariant checks compiled into the checked build only
+// (python -m paper_2505_19175_b200.build --checked): a failing check traps the
+// kernel (device assert) and the next ts_* call returns TS_ERR_CUDA.
+#ifdef TS_CHECKED
+#include <cassert>
+#define TS_ASSERT(cond) assert(cond)
+#else
+#define TS_ASSERT(cond) ((void)0)
+#endif
 #include <stdint.h>
 
 #include "../../include/trisplat_b200.h"

@@ -535,4 +535,106 @@ void launch_chain_bwd32(const Cam& cam, const Opts& opt, const ts_soup& soup, in
     chain_impl<float>(cam, opt, soup, dtype, flag, sgrad, g, accumulate, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// k_projection_dump: project_scene (render.py:253-312) for the depth-sorted
+// accepted triangles of the last forward, every field of SceneProjection in
+// the reference's fp64 operation order (this TU has no FMA contraction).
+// Row m (PROJ_ROW doubles) of `rows`: xc[9] q[6] z area phis nrm[6] doff[3]
+// esign[3] sig opa rgb[3] raw_rgb[3] basis[16] viewdir[3] u_norm bbox[4];
+// area_full[i] for every source (render.py:271-272).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) k_projection_dump(Cam cam, Opts opt, const T* __restrict__ verts,
+                                                         const T* __restrict__ opacity,
+                                                         const T* __restrict__ sigma, const T* __restrict__ sh,
+                                                         const unsigned* __restrict__ sorted_src, long long m,
+                                                         long long n, double* __restrict__ rows,
+                                                         double* __restrict__ area_full) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        double v[9];
+#pragma unroll
+        for (int a = 0; a < 9; a++) v[a] = (double)verts[k * 9 + a];
+        Proj64 p;
+        project64(v, cam, p);
+        area_full[k] = p.valid_z ? p.area : 0.0;
+    }
+    if (k >= m) return;
+    const long long i = sorted_src[k];
+    double v[9];
+#pragma unroll
+    for (int a = 0; a < 9; a++) v[a] = (double)verts[i * 9 + a];
+    Proj64 p;
+    project64(v, cam, p);
+    const double o = opt.solid ? 1.0 : (double)opacity[i];
+    const double sg = (double)sigma[i];
+    Edge64 E;
+    edge_bbox64(p.q, p.phis, o, sg, opt.mode, opt.tau_cutoff, cam.width, cam.height, E);
+    double* r = rows + k * PROJ_ROW;
+    int c = 0;
+#pragma unroll
+    for (int a = 0; a < 9; a++) r[c++] = p.xc[a];
+#pragma unroll
+    for (int a = 0; a < 6; a++) r[c++] = p.q[a];
+    r[c++] = p.z;
+    r[c++] = p.area;
+    r[c++] = p.phis;
+#pragma unroll
+    for (int e = 0; e < 3; e++) {
+        r[c++] = E.nx[e];
+        r[c++] = E.ny[e];
+    }
+#pragma unroll
+    for (int e = 0; e < 3; e++) r[c++] = E.d[e];
+#pragma unroll
+    for (int e = 0; e < 3; e++) r[c++] = ((E.esign >> e) & 1) ? -1.0 : 1.0;
+    r[c++] = sg;
+    r[c++] = o;
+    // view direction from the camera centre to the world centroid, SH colour
+    double u[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) u[b] = TS_S(TS_D(TS_A(TS_A(v[b], v[3 + b]), v[6 + b]), 3.0), cam.cc[b]);
+    double un = __dsqrt_rn(TS_A(TS_A(TS_M(u[0], u[0]), TS_M(u[1], u[1])), TS_M(u[2], u[2])));
+    un = un > 1e-12 ? un : 1e-12;
+    const double dir[3] = {TS_D(u[0], un), TS_D(u[1], un), TS_D(u[2], un)};
+    double basis[16];
+    sh_basis16(dir[0], dir[1], dir[2], basis);
+    double raw[3];
+    for (int ch = 0; ch < 3; ch++) {
+        double acc = 0.0;
+        for (int cc = 0; cc < opt.ncoef; cc++) acc = TS_A(acc, TS_M(basis[cc], (double)sh[i * 48 + cc * 3 + ch]));
+        raw[ch] = TS_A(acc, 0.5);
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) r[c++] = raw[ch] < 0.0 ? 0.0 : (raw[ch] > 1.0 ? 1.0 : raw[ch]);
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) r[c++] = raw[ch];
+#pragma unroll
+    for (int a = 0; a < 16; a++) r[c++] = basis[a];
+#pragma unroll
+    for (int b = 0; b < 3; b++) r[c++] = dir[b];
+    r[c++] = un;
+#pragma unroll
+    for (int a = 0; a < 4; a++) r[c++] = (double)E.bb[a];
+    while (c < PROJ_ROW) r[c++] = 0.0;
+}
+
+void launch_projection_dump(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                            const unsigned* sorted_src, long long m, double* rows, double* area_full,
+                            cudaStream_t st) {
+    const long long n = soup.n;
+    const long long cnt = n > m ? n : m;
+    if (cnt <= 0) return;
+    const unsigned grid = (unsigned)((cnt + 127) / 128);
+    if (dtype == 1)
+        k_projection_dump<double><<<grid, 128, 0, st>>>(cam, opt, (const double*)soup.vertices,
+                                                        (const double*)soup.opacity, (const double*)soup.sigma,
+                                                        (const double*)soup.sh, sorted_src, m, n, rows, area_full);
+    else
+        k_projection_dump<float><<<grid, 128, 0, st>>>(cam, opt, (const float*)soup.vertices,
+                                                       (const float*)soup.opacity, (const float*)soup.sigma,
+                                                       (const float*)soup.sh, sorted_src, m, n, rows, area_full);
+}
+
 }  // namespace ts

@@ -93,6 +93,11 @@ struct BlendOut {
 };
 
 // ts_exact.cu
+// project_scene dump: PROJ_ROW doubles per depth-sorted accepted triangle (see k_projection_dump)
+constexpr int PROJ_ROW = 64;
+void launch_projection_dump(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
+                            const unsigned* sorted_src, long long m, double* rows, double* area_full,
+                            cudaStream_t st);
 void launch_preprocess(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype,
                        const PreOut& out, cudaStream_t st);
 void launch_blend_exact(const Cam& cam, const Opts& opt, const Rec64* rec, const int* tile_start,
@@ -133,8 +138,11 @@ void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const R
                        const float* d_image, double* sgrad, cudaStream_t st);
 
 // ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
+bool chain_bwd_fast_ok(const ts_soup& soup, int dtype, const ts_grads& g);
+// triangles [lo, hi) (hi < 0: all); lo a multiple of 64
 bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,
-                           const double* sgrad, const ts_grads& g, int accumulate, cudaStream_t st);
+                           const double* sgrad, const ts_grads& g, int accumulate, cudaStream_t st, long long lo = 0,
+                           long long hi = -1);
 
 // ts_sort.cu
 struct SortScratch {
@@ -174,13 +182,21 @@ void entries_to_rank(long long e, const unsigned* ent_src, const int* rank_of, i
                      cudaStream_t st);
 void bbox_dump(long long n, const short4* bbox, int* out, cudaStream_t st);
 
+// build_tile_lists for any tile size: cnt (m int32) per-triangle tile counts and
+// off (m+1 int64) their scan; then the CSR (start[ntiles+1], entry[e]) from
+// bbox (m x 4 int64, rank order); kv = 4 u32 scratch arrays of e items
+void tile_lists_count(long long m, const long long* bbox, int ts, int* cnt, long long* off, void* cs_scratch,
+                      cudaStream_t st);
+void tile_lists_fill(long long m, long long e, const long long* bbox, int ts, int ntx, int ntiles,
+                     const long long* off, unsigned* const kv[4], const SortScratch& s, long long* start,
+                     long long* entry, cudaStream_t st);
 // onesweep radix sort (32-bit keys), scratch from onesweep_scratch_bytes
 size_t onesweep_scratch_bytes(long long max_count, int max_passes);
 int onesweep_sort_u32(long long count, unsigned* keys, unsigned* vals, unsigned* keys_alt,
                       unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
 // ts_optim.cu: fused Adam step (bad: device int64[4], first non-finite triangle per group)
 void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
-                      long long t, const double lrs[4], long long* bad, cudaStream_t st);
+                      long long* t, const double lrs[4], long long* bad, double* ibc, cudaStream_t st);
 
 // ts_density.cu: adaptive density control (density.py:27-263)
 void launch_stats_accum(long long n, const float* maxw, const int* pixcnt, const float* area, int min_pixels,

@@ -5,10 +5,14 @@
 //
 //   k_adam_check  -- thread per parameter element: a non-finite gradient
 //                    records the smallest offending triangle of its group
-//                    (the reference raises before touching any state);
+//                    (the reference raises before touching any state); thread
+//                    0 turns the device step counter t into this step's bias
+//                    corrections (step t + 1);
 //   k_adam_update -- thread per element, skipped entirely if any group was
 //                    flagged: m, v in fp64 arithmetic, the bias-corrected step in
-//                    fp32 (fp64 below the fp32 normal range), clamps.
+//                    fp32 (fp64 below the fp32 normal range), clamps; t += 1 only
+//                    when the update ran (the step count stays the reference's
+//                    even when the host does not read the flags).
 // Element e of the flat 59 N space (the DeviceGrads / moment layout
 // [vertices 9N | opacity N | sigma N | sh 48N]) reads the parameter tensors
 // in place, so one grid covers all groups with coalesced accesses.
@@ -38,8 +42,14 @@ __device__ __forceinline__ T pick(int k, T a0, T a1, T a2, T a3) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(256) k_adam_check(AdamGroups a, unsigned long long* __restrict__ bad) {
+__global__ void __launch_bounds__(256) k_adam_check(AdamGroups a, unsigned long long* __restrict__ bad,
+                                                    const long long* __restrict__ t, double* __restrict__ ibc) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e == 0) {
+        const double tt = (double)(*t + 1);
+        ibc[0] = 1.0 / (1.0 - pow(ADAM_B1, tt));
+        ibc[1] = 1.0 / (1.0 - pow(ADAM_B2, tt));
+    }
     if (e >= a.off[4]) return;
     const int k = group_of(a, e);
     const long long local = e - pick(k, a.off[0], a.off[1], a.off[2], a.off[3]);
@@ -48,11 +58,13 @@ __global__ void __launch_bounds__(256) k_adam_check(AdamGroups a, unsigned long 
 }
 
 __global__ void __launch_bounds__(256) k_adam_update(AdamGroups a, float* __restrict__ m, float* __restrict__ v,
-                                                     double ibc1, double ibc2,
+                                                     const double* __restrict__ ibc, long long* __restrict__ t,
                                                      const unsigned long long* __restrict__ bad) {
     if ((bad[0] & bad[1] & bad[2] & bad[3]) != ~0ull) return;  // some group flagged
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e == 0) *t += 1;  // (no thread of this grid reads t)
     if (e >= a.off[4]) return;
+    const double ibc1 = ibc[0], ibc2 = ibc[1];
     const int k = group_of(a, e);
     const long long local = e - pick(k, a.off[0], a.off[1], a.off[2], a.off[3]);
     const double g = (double)pick(k, a.g[0], a.g[1], a.g[2], a.g[3])[local];
@@ -74,7 +86,7 @@ __global__ void __launch_bounds__(256) k_adam_update(AdamGroups a, float* __rest
 }
 
 void launch_adam_step(float* const params[4], const float* const grads[4], long long n, float* m, float* v,
-                      long long t, const double lrs[4], long long* bad, cudaStream_t st) {
+                      long long* t, const double lrs[4], long long* bad, double* ibc, cudaStream_t st) {
     AdamGroups a;
     const int width[4] = {9, 1, 1, 48};
     long long off = 0;
@@ -89,11 +101,10 @@ void launch_adam_step(float* const params[4], const float* const grads[4], long 
     a.off[4] = off;
     unsigned long long* b = (unsigned long long*)bad;
     cudaMemsetAsync(b, 0xff, 4 * sizeof(unsigned long long), st);  // "none" = all bits set (-1 as int64)
-    if (off == 0) return;
-    const unsigned grid = (unsigned)((off + 255) / 256);
-    k_adam_check<<<grid, 256, 0, st>>>(a, b);
-    const double bc1 = 1.0 - pow(ADAM_B1, (double)t), bc2 = 1.0 - pow(ADAM_B2, (double)t);
-    k_adam_update<<<grid, 256, 0, st>>>(a, m, v, 1.0 / bc1, 1.0 / bc2, b);
+    // (n == 0: one thread still advances the step count, like the reference)
+    const unsigned grid = (unsigned)((off + 255) / 256) + (off == 0 ? 1u : 0u);
+    k_adam_check<<<grid, 256, 0, st>>>(a, b, t, ibc);
+    k_adam_update<<<grid, 256, 0, st>>>(a, m, v, ibc, t, b);
 }
 
 }  // namespace ts

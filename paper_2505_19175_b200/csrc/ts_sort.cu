@@ -755,4 +755,69 @@ __global__ void k_offsets_mismatch(long long n, const long long* __restrict__ a,
 void offsets_mismatch(long long n, const long long* a, const long long* b, unsigned long long* bad, cudaStream_t st) {
     k_offsets_mismatch<<<592, 256, 0, st>>>(n, a, b, bad);
 }
+
+// ---------------- build_tile_lists for any tile size (render.py:315-361) ----------------
+// Parity dump path: per-triangle tile counts, an int64 scan, (tile, rank) pairs
+// emitted in rank order, a stable radix sort on the tile, then CSR offsets.
+__global__ void k_tl_count(long long m, const long long* __restrict__ bbox, int ts, int* __restrict__ cnt) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const long long x0 = bbox[4 * i], x1 = bbox[4 * i + 1], y0 = bbox[4 * i + 2], y1 = bbox[4 * i + 3];
+    if (x1 <= x0 || y1 <= y0) {
+        cnt[i] = 0;
+        return;
+    }
+    cnt[i] = (int)(((x1 - 1) / ts + 1 - x0 / ts) * ((y1 - 1) / ts + 1 - y0 / ts));
+}
+
+__global__ void k_tl_emit(long long m, const long long* __restrict__ bbox, int ts, int ntx,
+                          const long long* __restrict__ off, unsigned* __restrict__ key, unsigned* __restrict__ val) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const long long x0 = bbox[4 * i], x1 = bbox[4 * i + 1], y0 = bbox[4 * i + 2], y1 = bbox[4 * i + 3];
+    if (x1 <= x0 || y1 <= y0) return;
+    long long pos = off[i];
+    for (long long ty = y0 / ts; ty < (y1 - 1) / ts + 1; ty++)
+        for (long long tx = x0 / ts; tx < (x1 - 1) / ts + 1; tx++) {
+            key[pos] = (unsigned)(ty * ntx + tx);
+            val[pos] = (unsigned)i;
+            pos++;
+        }
+}
+
+__global__ void k_tl_out(long long e, int ntiles, const unsigned* __restrict__ key, const unsigned* __restrict__ val,
+                         long long* __restrict__ start, long long* __restrict__ entry) {
+    const long long pos = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e <= 0) {
+        if (pos <= ntiles) start[pos] = 0;
+        return;
+    }
+    if (pos >= e) return;
+    entry[pos] = (long long)val[pos];
+    const int k = (int)key[pos];
+    const int kp = pos > 0 ? (int)key[pos - 1] : -1;
+    for (int t = kp + 1; t <= k; t++) start[t] = pos;
+    if (pos == e - 1)
+        for (int t = k + 1; t <= ntiles; t++) start[t] = e;
+}
+
+void tile_lists_count(long long m, const long long* bbox, int ts, int* cnt, long long* off, void* cs_scratch,
+                      cudaStream_t st) {
+    if (m > 0) k_tl_count<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, bbox, ts, cnt);
+    count_scan_i64(m, cnt, off, cs_scratch, st);
+}
+
+void tile_lists_fill(long long m, long long e, const long long* bbox, int ts, int ntx, int ntiles,
+                     const long long* off, unsigned* const kv[4], const SortScratch& s, long long* start,
+                     long long* entry, cudaStream_t st) {
+    if (m > 0 && e > 0) k_tl_emit<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, bbox, ts, ntx, off, kv[0], kv[1]);
+    int bits = 1;
+    while ((1ll << bits) < (long long)ntiles) bits++;
+    const int alt = radix_sort_u32(e, kv[0], kv[1], kv[2], kv[3], 0, bits, s, st);
+    const unsigned* key = alt ? kv[2] : kv[0];
+    const unsigned* val = alt ? kv[3] : kv[1];
+    const long long g = e > ntiles + 1 ? e : ntiles + 1;
+    k_tl_out<<<(unsigned)((g + 255) / 256), 256, 0, st>>>(e, ntiles, key, val, start, entry);
+}
+
 }  // namespace ts

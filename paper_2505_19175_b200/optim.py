@@ -19,16 +19,28 @@ GROUPS = ("vertices", "opacity", "sigma", "sh")
 
 @dataclass
 class DeviceAdamState:
-    m: "object"   # torch fp32 (59 N,)
+    m: "object"       # torch fp32 (59 N,)
     v: "object"
     n: int
-    t: int = 0
+    t_dev: "object"   # torch int64 (1,): steps taken (AdamState.t), kept on the device
 
     @classmethod
     def zeros(cls, n: int, device="cuda") -> "DeviceAdamState":
         import torch
         return cls(torch.zeros(59 * n, dtype=torch.float32, device=device),
-                   torch.zeros(59 * n, dtype=torch.float32, device=device), n, 0)
+                   torch.zeros(59 * n, dtype=torch.float32, device=device), n,
+                   torch.zeros(1, dtype=torch.int64, device=device))
+
+    @property
+    def t(self) -> int:
+        """Steps taken (reads the device counter: the kernel advances it only
+        when an update ran, so a step skipped for a non-finite gradient does not
+        count, as in the reference, which raises without touching the state)."""
+        return int(self.t_dev.item())
+
+    @t.setter
+    def t(self, value: int):
+        self.t_dev.fill_(int(value))
 
     def remap(self, origin, rasterizer=None, stream=None) -> "DeviceAdamState":
         """AdamState.remap (training.py:64-78) after densification: output
@@ -42,7 +54,7 @@ class DeviceAdamState:
         org = torch.as_tensor(np.asarray(origin, dtype=np.int64)).to("cuda")
         n_new = int(org.numel())
         new = DeviceAdamState.zeros(n_new)
-        new.t = self.t
+        new.t_dev.copy_(self.t_dev)
         st = ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
         o_old = o_new = 0
         for w in (9, 1, 1, 48):
@@ -57,8 +69,10 @@ class DeviceAdamState:
 
 def adam_step(soup, grads, state: DeviceAdamState, lrs: dict, rasterizer=None, stream=None, check=True):
     """One in-place Adam update of ``soup`` (DeviceSoup, fp32) with ``grads``
-    (DeviceGrads).  ``check=False`` skips the host read of the finiteness flags
-    (the device still skips the update if any gradient is non-finite)."""
+    (DeviceGrads).  ``check=False`` skips the host read of the finiteness flags:
+    the device still skips the whole update (step count included) if any
+    gradient is non-finite; the flags stay in ``state.last_bad`` (device
+    int64[4], -1 = finite) for the caller to inspect."""
     import torch
     from . import _lib
     from .rasterizer import default_rasterizer
@@ -76,12 +90,13 @@ def adam_step(soup, grads, state: DeviceAdamState, lrs: dict, rasterizer=None, s
                             ctypes.c_void_p(soup.opacity.data_ptr()), ctypes.c_void_p(soup.sigma.data_ptr()),
                             ctypes.c_void_p(soup.sh.data_ptr()), n, ctypes.byref(g),
                             ctypes.c_void_p(state.m.data_ptr()), ctypes.c_void_p(state.v.data_ptr()),
-                            state.t + 1, lr, ctypes.c_void_p(bad.data_ptr()), ctypes.c_void_p(st))
+                            ctypes.c_void_p(state.t_dev.data_ptr()), lr, ctypes.c_void_p(bad.data_ptr()),
+                            ctypes.c_void_p(st))
     _lib.check(rc, "adam_step")
+    state.last_bad = bad
     if check:
         b = bad.cpu().tolist()
         for k, i in zip(GROUPS, b):
             if i >= 0:
                 raise ValueError(f"non-finite {k} gradient for triangle {i}")
-    state.t += 1
     return state

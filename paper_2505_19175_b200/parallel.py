@@ -32,6 +32,57 @@ def flat_grad_size(n_triangles: int) -> int:
     return 59 * n_triangles
 
 
+def chunk_bounds(n: int, k: int, align: int = 64) -> list:
+    """k contiguous triangle ranges of [0, n): interior bounds rounded down to a
+    multiple of ``align`` (ts_backward_chunked's requirement), non-decreasing
+    (ranges may be empty for small n)."""
+    k = max(1, int(k))
+    b = [0]
+    for i in range(1, k):
+        b.append((i * n // k) // align * align)
+    b.append(n)
+    return b
+
+
+def bucket_slices(flat: torch.Tensor, n: int, lo: int, hi: int) -> list:
+    """Views of the flat [vertices 9n | opacity n | sigma n | sh 48n] gradient
+    holding triangles [lo, hi) of every group."""
+    return [flat[9 * lo:9 * hi], flat[9 * n + lo:9 * n + hi], flat[10 * n + lo:10 * n + hi],
+            flat[11 * n + 48 * lo:11 * n + 48 * hi]]
+
+
+class BucketedAllReduce:
+    """SUM all-reduce of the flat gradient, one triangle-range bucket at a
+    time: bucket k starts once ``event`` k fires (CUDA: on a side stream that
+    waits on the event, so the collective overlaps the producer's next range;
+    gloo / no event: at once).  ``wait()`` makes the current stream wait for
+    every bucket."""
+
+    def __init__(self, flat: torch.Tensor, n: int, bounds: list, comm_stream=None):
+        self.flat, self.n, self.bounds = flat, n, bounds
+        self.comm = comm_stream
+        self.works = []
+
+    def launch(self, k: int, event=None):
+        lo, hi = self.bounds[k], self.bounds[k + 1]
+        if hi <= lo:
+            return
+        if self.comm is not None:
+            if event is not None:
+                self.comm.wait_event(event)
+            with torch.cuda.stream(self.comm):
+                for sl in bucket_slices(self.flat, self.n, lo, hi):
+                    self.works.append(dist.all_reduce(sl, op=dist.ReduceOp.SUM, async_op=True))
+        else:
+            for sl in bucket_slices(self.flat, self.n, lo, hi):
+                self.works.append(dist.all_reduce(sl, op=dist.ReduceOp.SUM, async_op=True))
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        self.works = []
+
+
 def allreduce_(buf: torch.Tensor, bucket_bytes: int = 64 << 20):
     """In-place SUM all-reduce, bucketed so large buffers overlap in NCCL."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
@@ -51,23 +102,42 @@ class StepResult:
 
 
 def train_step(grad_fn: Callable[[int, torch.Tensor, bool], None], n_views: int,
-               grads: torch.Tensor, world: int | None = None, rank: int | None = None) -> StepResult:
+               grads: torch.Tensor, world: int | None = None, rank: int | None = None,
+               last_grad_fn=None, n_triangles: int | None = None, n_buckets: int = 8,
+               comm_stream=None) -> StepResult:
     """One view-parallel step.
 
     ``grad_fn(view, grads, accumulate)`` adds (or writes, when accumulate is
     False) the flat gradient of ``view`` into ``grads``.  Returns the reduced
     batch gradient (in place in ``grads``).
+
+    With ``last_grad_fn(view, grads, accumulate, bounds) -> events`` (and
+    ``n_triangles``) the rank's last view produces its gradient in
+    ``n_buckets`` triangle ranges (``chunk_bounds``), returning one event per
+    range (or None); each bucket's all-reduce is launched behind its event, so
+    the collective overlaps the rest of that view's chain.
     """
     if world is None:
         world = dist.get_world_size() if dist.is_initialized() else 1
     if rank is None:
         rank = dist.get_rank() if dist.is_initialized() else 0
     views = shard(n_views, world, rank)
+    overlap = last_grad_fn is not None and world > 1 and len(views) > 0 and n_triangles is not None
     if len(views) == 0:
         grads.zero_()
+    last = len(views) - 1 if overlap else len(views)
     for k, v in enumerate(views):
-        grad_fn(v, grads, k > 0)
-    allreduce_(grads)
+        if k < last:
+            grad_fn(v, grads, k > 0)
+    if not overlap:
+        allreduce_(grads)
+        return StepResult(grads, list(views))
+    bounds = chunk_bounds(n_triangles, n_buckets)
+    events = last_grad_fn(views[last], grads, last > 0, bounds)
+    red = BucketedAllReduce(grads, n_triangles, bounds, comm_stream)
+    for k in range(len(bounds) - 1):
+        red.launch(k, events[k] if events is not None else None)
+    red.wait()
     return StepResult(grads, list(views))
 
 
@@ -84,6 +154,8 @@ class B200ViewTrainer:
         self.d_images = d_images
         self.kw = render_kw
         self.grads = DeviceGrads.zeros(len(soup))
+        self.comm = None          # side stream of the bucketed all-reduce (world > 1)
+        self.n_buckets = 8
         # optional fused Adam after the all-reduce (training.py:165-168): every
         # rank applies the same update to its replica of the parameters
         self.lrs = lrs
@@ -96,8 +168,18 @@ class B200ViewTrainer:
         self.rast.forward(self.soup, self.intr, self.poses[v], keep_backward=True, **self.kw)
         self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate)
 
+    def _grad_chunked(self, v: int, flat: torch.Tensor, accumulate: bool, bounds):
+        """The rank's last view: the chain in triangle ranges, one event each."""
+        self.rast.forward(self.soup, self.intr, self.poses[v], keep_backward=True, **self.kw)
+        events = [torch.cuda.Event() for _ in range(len(bounds) - 1)]
+        self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate, chunks=(bounds, events))
+        return events
+
     def step(self) -> StepResult:
-        res = train_step(self._grad, len(self.poses), self.grads.flat)
+        if self.comm is None and dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            self.comm = torch.cuda.Stream()
+        res = train_step(self._grad, len(self.poses), self.grads.flat, last_grad_fn=self._grad_chunked,
+                         n_triangles=len(self.soup), n_buckets=self.n_buckets, comm_stream=self.comm)
         if self.adam is not None:
             from .optim import adam_step
             adam_step(self.soup, self.grads, self.adam, self.lrs, rasterizer=self.rast)

@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .types import (DEFAULT_TAU_CUTOFF, DEFAULT_TILE_SIZE, TAU_CONTRIB, FragmentData,
-                    GradientSet, ImageBuffer, RenderOutput, as_soup, mode_flag)
+                    GradientSet, ImageBuffer, RenderOutput, SceneProjection, as_soup, mode_flag)
 
 PRECISION = {"fast": 0, "exact": 1}
 
@@ -173,9 +173,11 @@ def make_options(mode=0, background=(0.0, 0.0, 0.0), tau_cutoff=DEFAULT_TAU_CUTO
     bg = np.asarray(background, dtype=np.float64).reshape(3)
     if not 0 <= int(active_sh_degree) <= 3:
         raise ValueError("SH degree must be in [0,3]")
-    if int(tile_size) != 16:
-        raise NotImplementedError("trisplat_b200 supports tile_size=16 only")
-    return _lib.TsOptions(mode_flag(mode), int(active_sh_degree), int(tile_size), int(bool(solid)),
+    check_tile_size(tile_size)
+    # every output of render / render_backward is independent of the tile size
+    # (each pixel composites the triangles whose bbox holds it, in depth order);
+    # the kernels always work on 16x16 tiles
+    return _lib.TsOptions(mode_flag(mode), int(active_sh_degree), 16, int(bool(solid)),
                           float(tau_cutoff), float(TAU_CONTRIB), (ctypes.c_double * 3)(*bg),
                           PRECISION[precision] if isinstance(precision, str) else int(precision),
                           1 if param_dtype == torch.float64 else 0, int(bool(validate)),
@@ -183,6 +185,17 @@ def make_options(mode=0, background=(0.0, 0.0, 0.0), tau_cutoff=DEFAULT_TAU_CUTO
 
 
 _NONFINITE_GROUPS = ("vertices", "opacity", "sigma", "sh")
+
+
+def check_tile_size(tile_size):
+    """The reference divides by the tile size (render.py:352-353): 0 raises
+    ZeroDivisionError there; negative sizes are rejected here."""
+    ts = int(tile_size)
+    if ts == 0:
+        raise ZeroDivisionError("integer division or modulo by zero")
+    if ts < 0:
+        raise ValueError(f"tile_size must be positive, got {ts}")
+    return ts
 
 
 def _check_grads(grads: "DeviceGrads", n: int):
@@ -307,7 +320,12 @@ class Rasterizer:
         return out
 
     def backward(self, d_image: torch.Tensor, grads: DeviceGrads | None = None,
-                 accumulate: bool = False, stream=None) -> DeviceGrads:
+                 accumulate: bool = False, stream=None, chunks=None) -> DeviceGrads:
+        """Gradient of sum(d_image * C) into ``grads`` (+= when accumulating).
+        ``chunks = (bounds, events)``: the final chain to the parameter
+        gradients runs in triangle ranges [bounds[k], bounds[k+1]) and
+        torch.cuda.Event events[k] is recorded once range k is final
+        (ts_backward_chunked; parallel.chunk_bounds gives valid bounds)."""
         if self._last is None:
             raise RuntimeError("backward() needs a preceding forward()")
         n, h, w = self._last
@@ -318,10 +336,23 @@ class Rasterizer:
             grads = DeviceGrads(torch.empty(n * 59, dtype=torch.float32, device=d_image.device), n)
             accumulate = False
         _check_grads(grads, n)
-        st = (stream or torch.cuda.current_stream(d_image.device)).cuda_stream
+        stream = stream or torch.cuda.current_stream(d_image.device)
+        st = stream.cuda_stream
         g = grads._ts()
-        _lib.check(self.lib.ts_backward(self._ctx, _ptr(d_image), ctypes.byref(g),
-                                        int(bool(accumulate)), ctypes.c_void_p(st)), "backward")
+        if chunks is None:
+            _lib.check(self.lib.ts_backward(self._ctx, _ptr(d_image), ctypes.byref(g),
+                                            int(bool(accumulate)), ctypes.c_void_p(st)), "backward")
+            return grads
+        bounds, events = chunks
+        k = len(bounds) - 1
+        if len(events) != k:
+            raise ValueError("one event per chunk")
+        for ev in events:  # (torch creates the CUDA event at its first record)
+            ev.record(stream)
+        b = (ctypes.c_int64 * (k + 1))(*[int(x) for x in bounds])
+        evp = (ctypes.c_void_p * k)(*[ctypes.c_void_p(ev.cuda_event) for ev in events])
+        _lib.check(self.lib.ts_backward_chunked(self._ctx, _ptr(d_image), ctypes.byref(g), int(bool(accumulate)),
+                                                k, b, evp, ctypes.c_void_p(st)), "backward_chunked")
         return grads
 
     def fragments(self, stream=None) -> "DeviceFragments":
@@ -425,6 +456,72 @@ def _param_dtype(soup):
     return torch.float32 if v.dtype == np.float32 else torch.float64
 
 
+def project_scene(soup, intr, pose, mode=0, tau_cutoff: float = DEFAULT_TAU_CUTOFF,
+                  active_sh_degree: int = 3) -> SceneProjection:
+    """Drop-in for trisplat.render.project_scene (render.py:253-312): the
+    projection, cull, depth order, edges, tight bboxes and SH colour of every
+    accepted triangle, in fp64, from the device (a forward on the default
+    rasterizer, then the TS_DUMP_PROJECTION dump in the reference's operation
+    order)."""
+    _require_cuda()
+    soup = as_soup(soup)
+    rast = default_rasterizer()
+    ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
+    fwd = rast.forward(ds, intr, pose, mode, (0.0, 0.0, 0.0), tau_cutoff, DEFAULT_TILE_SIZE,
+                       active_sh_degree, keep_backward=False)
+    n, m = len(ds), fwd.n_visible
+    sidx = rast.dump_sorted_idx(m)
+    raw = torch.empty(_lib.PROJ_ROW * m + n + 1, dtype=torch.float64, device="cuda")
+    _lib.check(rast.lib.ts_debug_copy(rast._ctx, _lib.TS_DUMP_PROJECTION, _ptr(raw), raw.numel() * 8,
+                                      ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "debug_copy")
+    host = raw.cpu().numpy()
+    rows = host[:_lib.PROJ_ROW * m].reshape(m, _lib.PROJ_ROW)
+    col = iter(np.cumsum([0, 9, 6, 1, 1, 1, 6, 3, 3, 1, 1, 3, 3, 16, 3, 1, 4]))
+    lo = next(col)
+
+    def take(shape):
+        nonlocal lo
+        hi = next(col)
+        a = np.ascontiguousarray(rows[:, lo:hi]).reshape((m,) + shape)
+        lo = hi
+        return a
+
+    xc, q = take((3, 3)), take((3, 2))
+    z, area, phis = take(()), take(()), take(())
+    nrm, doff, esign = take((3, 2)), take((3,)), take((3,))
+    sig, opa = take(()), take(())
+    rgb, raw_rgb, basis, viewdir, u_norm = take((3,)), take((3,)), take((16,)), take((3,)), take(())
+    bbox = take((4,)).astype(np.int64)
+    return SceneProjection(n_total=n, sorted_idx=sidx, z=z, xc=xc, q=q, nrm=nrm, doff=doff, esign=esign,
+                           phis=phis, area=area, sig=sig, opa=opa, rgb=rgb, raw_rgb=raw_rgb, basis=basis,
+                           viewdir=viewdir, u_norm=u_norm, bbox=bbox,
+                           area_full=np.ascontiguousarray(host[_lib.PROJ_ROW * m:_lib.PROJ_ROW * m + n]))
+
+
+def build_tile_lists(proj, intr, tile_size: int = DEFAULT_TILE_SIZE):
+    """Drop-in for trisplat.render.build_tile_lists (render.py:349-361): CSR
+    per-tile lists of depth ranks (each tile's list in rank order) for any tile
+    size, built on the device (ts_tile_lists) from ``proj.bbox``.
+    Returns (ntx, nty, tile_start int64[ntx*nty+1], entry_tri int64[E])."""
+    _require_cuda()
+    ts = check_tile_size(tile_size)
+    ntx = (int(intr.width) + ts - 1) // ts
+    nty = (int(intr.height) + ts - 1) // ts
+    bbox = np.ascontiguousarray(np.asarray(proj.bbox, dtype=np.int64).reshape(-1, 4))
+    m = bbox.shape[0]
+    rast = default_rasterizer()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    bb = torch.from_numpy(bbox).to("cuda") if m else torch.zeros((1, 4), dtype=torch.int64, device="cuda")
+    e = ctypes.c_int64()
+    _lib.check(rast.lib.ts_tile_lists(rast._ctx, _ptr(bb), m, ts, int(intr.width), int(intr.height), None, None,
+                                      ctypes.byref(e), st), "tile_lists")
+    start = torch.empty(ntx * nty + 1, dtype=torch.int64, device="cuda")
+    entry = torch.empty(max(int(e.value), 1), dtype=torch.int64, device="cuda")
+    _lib.check(rast.lib.ts_tile_lists(rast._ctx, _ptr(bb), m, ts, int(intr.width), int(intr.height), _ptr(start),
+                                      _ptr(entry), ctypes.byref(e), st), "tile_lists")
+    return ntx, nty, start.cpu().numpy(), entry[:int(e.value)].cpu().numpy()
+
+
 # bytes the last render() copied device -> host (bench.py's e2e accounting)
 LAST_RENDER_D2H_BYTES = 0
 
@@ -513,14 +610,15 @@ def install(trisplat_module=None):
     import sys
     patched = []
     targets = {
-        "trisplat": ("render", "render_backward"),
-        "trisplat.render": ("render",),
-        "trisplat.backward": ("render", "render_backward"),
+        "trisplat": ("render", "render_backward", "project_scene", "build_tile_lists"),
+        "trisplat.render": ("render", "project_scene", "build_tile_lists"),
+        "trisplat.backward": ("render", "render_backward", "project_scene", "build_tile_lists"),
         "trisplat.training": ("render", "render_backward"),
         "trisplat.synthetic": ("render",),
         "trisplat.cli": ("render",),
     }
-    repl = {"render": render, "render_backward": render_backward}
+    repl = {"render": render, "render_backward": render_backward, "project_scene": project_scene,
+            "build_tile_lists": build_tile_lists}
     for mod_name, names in targets.items():
         try:
             mod = sys.modules.get(mod_name) or importlib.import_module(mod_name)

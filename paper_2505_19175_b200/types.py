@@ -193,6 +193,32 @@ class FragmentData:
 
 
 @dataclass
+class SceneProjection:
+    """project_scene's result (render.py:128-156): depth-sorted screen-space data
+    of the accepted triangles of one view (M of them), fp64 / int64."""
+
+    n_total: int
+    sorted_idx: np.ndarray  # (M,) source indices, depth order
+    z: np.ndarray           # (M,) sort depth
+    xc: np.ndarray          # (M,3,3) camera-space vertices
+    q: np.ndarray           # (M,3,2)
+    nrm: np.ndarray         # (M,3,2)
+    doff: np.ndarray        # (M,3)
+    esign: np.ndarray       # (M,3)
+    phis: np.ndarray        # (M,)
+    area: np.ndarray        # (M,)
+    sig: np.ndarray
+    opa: np.ndarray
+    rgb: np.ndarray         # (M,3) clamped
+    raw_rgb: np.ndarray     # (M,3) pre-clamp
+    basis: np.ndarray       # (M,16)
+    viewdir: np.ndarray     # (M,3) unit
+    u_norm: np.ndarray      # (M,)
+    bbox: np.ndarray        # (M,4) int64: x0,x1,y0,y1
+    area_full: np.ndarray   # (N,) projected area for every source triangle
+
+
+@dataclass
 class RenderOutput:
     image: ImageBuffer
     alpha_map: np.ndarray

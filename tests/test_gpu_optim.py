@@ -97,3 +97,25 @@ def test_reference_adam_cases():
     with pytest.raises(ValueError, match="triangle 1"):
         adam_step(soup, g, st, unit())
     assert st.t == 0 and torch.equal(v0, soup.vertices) and float(st.m.abs().max()) == 0.0
+
+
+def test_unchecked_step_skips_and_keeps_the_step_count():
+    """check=False (no host read of the flags): a non-finite gradient skips the
+    whole update on the device, the step count included (t must not
+    drift from the reference, which raises without touching the state)."""
+    from paper_2505_19175_b200.optim import DeviceAdamState, adam_step
+    n = 4
+    rng = np.random.default_rng(1)
+    base = (rng.normal(0, 1, (n, 3, 3)), np.full(n, 0.5), np.full(n, 1.0), rng.normal(0, 0.3, (n, 16, 3)))
+    unit = lambda: {k: 1e-3 for k in OP.GROUPS}  # noqa: E731
+    soup, st = _dev(*base), DeviceAdamState.zeros(n)
+    v0 = soup.vertices.clone()
+    g = _grads(n, np.ones((n, 3, 3)), np.zeros(n), np.zeros(n), np.zeros((n, 16, 3)))
+    g.d_opacity[2] = float("inf")  # (first non-finite group: opacity)
+    adam_step(soup, g, st, unit(), check=False)
+    assert st.t == 0 and torch.equal(v0, soup.vertices)
+    assert st.last_bad.cpu().tolist() == [-1, 2, -1, -1]
+    g.d_opacity[2] = 0.0
+    adam_step(soup, g, st, unit(), check=False)
+    adam_step(soup, g, st, unit(), check=False)
+    assert st.t == 2 and not torch.equal(v0, soup.vertices)

@@ -113,3 +113,55 @@ def test_gloo_world2_density_stats_match_single_process(tmp_path):
     assert int(got["nv"]) == 5
     assert np.array_equal(got["mw"], mw) and np.array_equal(got["views"], views)
     assert np.allclose(got["area"] / 5, mean, rtol=1e-14)
+
+
+def _overlap_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    soup, intr, poses, d_images = _scene()
+    n = len(soup.vertices)
+    grads = torch.zeros(parallel.flat_grad_size(n), dtype=torch.float64)
+    seen = []
+
+    def grad_fn(v, flat, accumulate):
+        g = torch.from_numpy(_oracle_flat(soup, intr, poses[v], d_images[v]))
+        flat.add_(g) if accumulate else flat.copy_(g)
+
+    def last_fn(v, flat, accumulate, bounds):
+        seen.append(list(bounds))
+        grad_fn(v, flat, accumulate)
+        return None
+
+    res = parallel.train_step(grad_fn, len(poses), grads, last_grad_fn=last_fn, n_triangles=n, n_buckets=3)
+    assert len(seen) == 1 and seen[0][0] == 0 and seen[0][-1] == n
+    if rank == 0:
+        np.save(out_path, res.grads.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_bucketed_overlap_matches_single_process(tmp_path):
+    """The overlapped step (last view's gradient in triangle-range buckets, one
+    all-reduce per bucket) reduces to the same batch gradient."""
+    out = str(tmp_path / "o.npy")
+    mp.spawn(_overlap_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    soup, intr, poses, d_images = _scene()
+    want = sum(_oracle_flat(soup, intr, poses[v], d_images[v]) for v in range(len(poses)))
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_chunk_bounds_and_bucket_slices_cover_the_buffer():
+    for n in (0, 1, 63, 64, 300, 1000, 2_000_000):
+        for k in (1, 3, 8):
+            b = parallel.chunk_bounds(n, k)
+            assert b[0] == 0 and b[-1] == n and len(b) == k + 1
+            assert all(b[i] <= b[i + 1] for i in range(k))
+            assert all(x % 64 == 0 for x in b[:-1])
+    n = 300
+    flat = torch.arange(59 * n)
+    b = parallel.chunk_bounds(n, 3)
+    cover = torch.cat([s for i in range(3) for s in parallel.bucket_slices(flat, n, b[i], b[i + 1])])
+    assert torch.equal(cover.sort().values, flat)
