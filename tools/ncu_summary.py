@@ -73,8 +73,37 @@ def full(path, kernel=None):
     return "\n".join(out)
 
 
+def metrics(path):
+    """--metrics --csv capture (one row per launch and metric) -> per-kernel
+    medians of every metric."""
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, mi, ui, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value", "ID"))
+    per = collections.OrderedDict()
+    units = {}
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("ts::", "")
+        per.setdefault(name, collections.defaultdict(list))[r[mi]].append(float(r[vi].replace(",", "")))
+        units[r[mi]] = r[ui]
+    out = []
+    for name, m in per.items():
+        n = len(next(iter(m.values())))
+        out.append(f"### `{name}` (median of {n} launches)\n")
+        out.append("| metric | value | unit |\n|---|---:|---|")
+        for k, vals in m.items():
+            v = sorted(vals)[len(vals) // 2]
+            out.append(f"| {k} | {v:,.6g} | {units[k]} |")
+        out.append("")
+    return "\n".join(out)
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         print(launches(sys.argv[2]))
+    elif sys.argv[1] == "metrics":
+        print(metrics(sys.argv[2]))
     else:
         print(full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None))
