@@ -39,6 +39,36 @@ namespace {
 constexpr float T_MIN_F = 1e-4f;
 constexpr float ALPHA_CLAMP_F = 0.99f;
 
+// 32-bit shared-memory addressing for the compositing loop (through the
+// generic struct reference the compiler rebuilds the shared window address
+// every iteration)
+__device__ __forceinline__ int lds_s32(unsigned a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f32(unsigned a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f32x2(unsigned a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(unsigned a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void red_s_max(unsigned a, unsigned v) {
+    asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_s_add(unsigned a, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -60,7 +90,7 @@ struct DenseSmem {
     float4 col[DB];                // rgb, f0
     float f1[DB];
     unsigned seg[DB * TILE];       // segment s (one row of one entry): first pair | j<<13 | row<<19 | xa<<23
-    unsigned rowtab[DB][TILE];     // row ly of entry j: first pair | xa<<16 (rows with a non-empty span)
+    int rowtab[DB][TILE];          // row ly of entry j: its first pair minus its first column (pair = rowtab + lx)
     unsigned starts[PCAP / 32];    // bit (k & 31) of word k >> 5: a segment starts at pair k
     int jfirst[PCAP / 32];         // segment holding pair 32 w
     unsigned ein[DB];              // per entry: inclusive (pairs<<16 | segments) within its warp
@@ -276,7 +306,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         const unsigned pm = base + exl[m];
                         const unsigned P0 = pm >> 16, S0 = pm & 0xffffu;
                         TS_ASSERT(P0 + (unsigned)len[m] <= (unsigned)PCAP && S0 < (unsigned)(DB * TILE) && ly2 < TILE);
-                        sm.rowtab[j][ly2] = P0 | ((unsigned)xa[m] << 16);
+                        sm.rowtab[j][ly2] = (int)P0 - xa[m];
                         sm.seg[S0] = P0 | ((unsigned)j << 13) | ((unsigned)ly2 << 19) | ((unsigned)xa[m] << 23);
                         atomicOr(&sm.starts[P0 >> 5], 1u << (P0 & 31));
                         // a segment (<= 16 pairs) holds at most one word start
@@ -405,13 +435,66 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             while (hm) {
                 const int j = __ffsll((long long)hm) - 1;
                 hm &= hm - 1;
-                const unsigned rth = sm.rowtab[j][ly];
-                const int kh = (int)(rth & 0xffffu) + lx - (int)(rth >> 16);
+                const int kh = sm.rowtab[j][ly] + lx;
                 const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
                 TS_ASSERT(kh >= 0 && kh < sm.total && rb + slot < out.frec_cap);
                 out.frec[rb + slot].pix = ~0u;
             }
         };
+        if constexpr (!ACC64) {
+            // render: walk the two mask words; 32-bit shared addressing
+            if (!done) {
+                const unsigned sb = (unsigned)__cvta_generic_to_shared(s_dyn);
+                const unsigned s_rt = sb + (unsigned)offsetof(SM, rowtab) + 4u * (unsigned)ly;
+                const unsigned s_r = sb + (unsigned)offsetof(SM, r), s_eq = sb + (unsigned)offsetof(SM, eq);
+                const unsigned s_col = sb + (unsigned)offsetof(SM, col);
+                const unsigned s_mw = sb + (unsigned)offsetof(SM, maxw), s_px = sb + (unsigned)offsetof(SM, pix);
+                unsigned w = (unsigned)mm, w1 = (unsigned)(mm >> 32);
+                int jb = 0;
+                while (true) {
+                    if (w == 0) {
+                        if (jb != 0 || w1 == 0) break;
+                        w = w1;
+                        jb = 32;
+                    }
+                    const int j = jb + __ffs(w) - 1;
+                    w &= w - 1;
+                    const int kp = lds_s32(s_rt + 64u * (unsigned)j) + lx;
+                    TS_ASSERT(kp >= 0 && kp < sm.total && ((sm.mask[j >> 5][tid] >> (j & 31)) & 1u));
+                    const float a = lds_f32(s_r + 4u * (unsigned)kp);  // alpha (clamped); NaN = in the band
+                    if (isnan(a)) {
+                        flag_pos = b + j;
+                        done = true;
+                        break;
+                    }
+                    const float2 eq = lds_f32x2(s_eq + 8u * (unsigned)kp);
+                    const float wgt = T * a;
+                    const float tn = fmaf(-T, a, T);
+                    // relative error bounds of tn and of wgt (the tests keep a 2x margin)
+                    const float en = epsT + eq.y, ew = epsT + eq.x;
+                    if (fabsf(tn - T_MIN_F) <= fmaf(2.f * en, tn, 1e-11f) ||
+                        fabsf(wgt - tau) <= fmaf(2.f * ew, wgt, 1e-9f)) {
+                        flag_pos = b + j;
+                        done = true;
+                        break;
+                    }
+                    const float4 col = lds_f32x4(s_col + 16u * (unsigned)j);
+                    C0 = fmaf(wgt, col.x, C0);
+                    C1 = fmaf(wgt, col.y, C1);
+                    C2 = fmaf(wgt, col.z, C2);
+                    last = b + j;
+                    cnt++;
+                    T = tn;
+                    epsT = en;
+                    if (wgt > tau) red_s_add(s_px + 4u * (unsigned)j, 1);
+                    red_s_max(s_mw + 4u * (unsigned)j, __float_as_uint(wgt));
+                    if (T < T_MIN_F) {
+                        done = true;
+                        break;
+                    }
+                }
+            }
+        } else
         if (done) {
             if (rb != ~0ull) mark_holes(mm);
         } else {
@@ -419,8 +502,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 while (mm) {
                     const int j = __ffsll((long long)mm) - 1;
                     mm &= mm - 1;
-                    const unsigned rt = sm.rowtab[j][ly];
-                    const int kp = (int)(rt & 0xffffu) + lx - (int)(rt >> 16);
+                    const int kp = sm.rowtab[j][ly] + lx;
                     TS_ASSERT(kp >= 0 && kp < sm.total && ((sm.mask[j >> 5][tid] >> (j & 31)) & 1u));
                 const Real rv = sm.r[kp];
                     if (isnan(rv)) {  // r inside the contribution band
