@@ -571,14 +571,15 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
     dinfo = {"n_before": drep["n_before"], "n_after": drep["n_after"], "n_removed": drep["prune"]["n_removed"],
              "n_split": drep["n_split"], "n_clone": drep["n_clone"], "views": dstats.n_views}
     del dsoup, ast2, ast, dstats
-    # per-stage times of one view (synchronous forward: its entry / visible counts)
+    # per-stage times of one view as in the step (synchronous forward: its entry /
+    # visible counts; the backward accumulating into the batch gradient)
     v0 = mine[0] if len(mine) else 0
     d_img = d_images[v0] if d_images[v0] is not None else torch.zeros((c3.height, c3.width, 3), device="cuda")
     rast.profile(True)
     bw = []
     for _ in range(3):
         fo = rast.forward(ds3, intr3, poses[v0], keep_backward=True, precision=args.precision)
-        rast.backward(d_img, trainer.grads, accumulate=False)
+        rast.backward(d_img, trainer.grads, accumulate=True)
         stt = rast.stage_times()
         bw.append(stt["blend_bwd"] + stt["chain_bwd"])
     rast.profile(False)

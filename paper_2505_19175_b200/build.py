@@ -51,10 +51,13 @@ def headers_mtime() -> float:
     return max(os.path.getmtime(h) for h in hs if os.path.exists(h))
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
-    build_dir = BUILD + ("_checked" if checked else "")
-    lib = LIB.replace(".so", "_checked.so") if checked else LIB
-    extra_all = ["-DTS_CHECKED"] if checked else []
+def build(force: bool = False, verbose: bool = False, checked: bool = False, defines=(), out=None) -> str:
+    """defines: extra -D flags for a measurement variant, built into its own
+    directory and library ``out`` (product builds take none)."""
+    tag = ("_checked" if checked else "") + "".join("_" + d.replace("=", "") for d in defines)
+    build_dir = BUILD + tag
+    lib = out or (LIB.replace(".so", tag + ".so") if tag else LIB)
+    extra_all = (["-DTS_CHECKED"] if checked else []) + ["-D" + d for d in defines]
     os.makedirs(build_dir, exist_ok=True)
     hm = headers_mtime()
     objs = []
@@ -80,4 +83,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv, defines=defs,
+          out=outs[0] if outs else None)
