@@ -450,6 +450,7 @@ def e2e_render(args, soup, intr, pose, world, max_over_ranks):
     assert out.per_triangle_area.shape == (n,)
     return {"value": world * steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": d2h, "steps": steps,
+            "last_call_ms": {k: round(v, 3) for k, v in tsb.LAST_RENDER_TIMES.items()},
             "api": "paper_2505_19175_b200.render(TriangleSoup fp64, intr, pose) -> RenderOutput (numpy), "
                    "wall clock per call"}
 

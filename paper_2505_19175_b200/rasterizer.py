@@ -48,8 +48,10 @@ def _ptr(t):
 # into a small ring of pinned buffers while the previous chunk's DMA runs, about
 # 4x the rate of a pageable copy (the drop-in render() uploads the reference's
 # 944 MB fp64 soup every call)
-_STAGE_CHUNK = 32 << 20
+_STAGE_CHUNK = 16 << 20  # 6 buffers, DMA alternating over 2 streams (measured: 49 GB/s)
+_STAGE_NBUF = 6
 _STAGE: list = []
+_STAGE_STREAMS: list = []
 
 
 def _staged_h2d(a: np.ndarray, device="cuda") -> torch.Tensor:
@@ -61,17 +63,24 @@ def _staged_h2d(a: np.ndarray, device="cuda") -> torch.Tensor:
         return out
     if not _STAGE:
         _STAGE.extend((torch.empty(_STAGE_CHUNK, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
-                      for _ in range(3))
+                      for _ in range(_STAGE_NBUF))
+        _STAGE_STREAMS.extend(torch.cuda.Stream(out.device) for _ in range(2))
     sb = src.reshape(-1).view(torch.uint8)
     ob = out.reshape(-1).view(torch.uint8)
-    stream = torch.cuda.current_stream(out.device)
+    cur = torch.cuda.current_stream(out.device)
+    for st in _STAGE_STREAMS:
+        st.wait_stream(cur)  # (out is allocated on the current stream)
     for i, off in enumerate(range(0, nbytes, _STAGE_CHUNK)):
         buf, ev = _STAGE[i % len(_STAGE)]
+        st = _STAGE_STREAMS[i % len(_STAGE_STREAMS)]
         c = min(_STAGE_CHUNK, nbytes - off)
         ev.synchronize()  # the slot's previous DMA is done
         buf[:c].copy_(sb[off:off + c])
-        ob[off:off + c].copy_(buf[:c], non_blocking=True)
-        ev.record(stream)
+        with torch.cuda.stream(st):
+            ob[off:off + c].copy_(buf[:c], non_blocking=True)
+            ev.record(st)
+    for st in _STAGE_STREAMS:
+        cur.wait_stream(st)
     return out
 
 
@@ -555,16 +564,37 @@ def build_tile_lists(proj, intr, tile_size: int = DEFAULT_TILE_SIZE):
     return ntx, nty, start.cpu().numpy(), entry[:int(e.value)].cpu().numpy()
 
 
-# bytes the last render() copied device -> host (bench.py's e2e accounting)
+# bytes the last render() copied device -> host and the wall-clock split of
+# that call (bench.py's e2e accounting)
 LAST_RENDER_D2H_BYTES = 0
+LAST_RENDER_TIMES: dict = {}
 
 
-def _to_numpy(t: torch.Tensor, dtype) -> np.ndarray:
-    """Device tensor -> new numpy array of ``dtype`` (converted on the device)."""
-    out = np.empty(tuple(t.shape), dtype=dtype)
-    host = torch.from_numpy(out)
-    host.copy_(t.to(dtype=host.dtype))
-    return out
+class _PinnedPool:
+    """Page-locked host buffers for render()'s outputs, reused once every array
+    handed out from a buffer is gone (a fresh cudaHostAlloc of the ~77 MB of
+    outputs costs ~2.5 ms, a pageable array page-faults while it is written).
+    The caller's arrays are numpy views of one ndarray per buffer; a weak
+    reference to that ndarray tells when the last of them has been dropped."""
+
+    def __init__(self):
+        self.entries = []  # [base uint8 pinned tensor, weakref to the ndarray handed out or None]
+
+    def get(self, count: int, dtype: torch.dtype):
+        """(device-copyable host tensor, numpy array on the same memory) of ``count`` items."""
+        import weakref
+        nbytes = count * torch.empty(0, dtype=dtype).element_size()
+        ent = next((e for e in self.entries if e[0].numel() >= nbytes and (e[1] is None or e[1]() is None)), None)
+        if ent is None:
+            ent = [torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True), None]
+            self.entries.append(ent)
+        host = ent[0][:nbytes].view(dtype)
+        arr = host.numpy()
+        ent[1] = weakref.ref(arr)
+        return host, arr
+
+
+_PINNED = _PinnedPool()
 
 
 def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
@@ -572,27 +602,45 @@ def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
            tile_size: int = DEFAULT_TILE_SIZE, active_sh_degree: int = 3,
            precision: str = "fast") -> RenderOutput:
     """Drop-in for trisplat.render.render (render.py:364-432)."""
-    global LAST_RENDER_D2H_BYTES
+    global LAST_RENDER_D2H_BYTES, LAST_RENDER_TIMES
+    import time
+    t0 = time.perf_counter()
     _require_cuda()
     soup = as_soup(triangles)
     if collect_fragments and precision != "fast":
         raise ValueError("collect_fragments needs precision='fast'")
     rast = default_rasterizer()
     ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
+    t1 = time.perf_counter()
     fwd = rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
                        precision=precision)
+    t2 = time.perf_counter()
     frags = rast.fragments().to_fragment_data() if collect_fragments else None
-    image = _to_numpy(fwd.image, np.float64)
-    alpha = _to_numpy(fwd.alpha_map, np.float64)
-    maxw = _to_numpy(fwd.max_weight, np.float64)
-    pixc = _to_numpy(fwd.pixel_count, np.int64)
-    area = _to_numpy(fwd.area, np.float64)
+    # the fp64 outputs converted and packed on the device, one copy each for the
+    # fp64 block and the int64 pixel counts into cached page-locked host memory
+    h, w = fwd.alpha_map.shape
+    n = fwd.max_weight.numel()
+    packed = torch.cat([fwd.image.reshape(-1).double(), fwd.alpha_map.reshape(-1).double(),
+                        fwd.max_weight.double(), fwd.area.double()])
+    pk_h, flat = _PINNED.get(packed.numel(), torch.float64)
+    pk_h.copy_(packed, non_blocking=True)
+    pc_h, pixc = _PINNED.get(n, torch.int64)
+    pc_h.copy_(fwd.pixel_count.long(), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    o1, o2, o3 = h * w * 3, h * w * 4, h * w * 4 + n
+    image, alpha = flat[:o1].reshape(h, w, 3), flat[o1:o2].reshape(h, w)
+    maxw, area = flat[o2:o3], flat[o3:o3 + n]
+    del pk_h, pc_h
+    t3 = time.perf_counter()
     LAST_RENDER_D2H_BYTES = image.nbytes + alpha.nbytes + maxw.nbytes + pixc.nbytes + area.nbytes
     if frags is not None:
         LAST_RENDER_D2H_BYTES += sum(np.asarray(a).nbytes for a in (frags.offsets, frags.triangle,
                                                                       frags.weight, frags.depth))
-    return RenderOutput(image=ImageBuffer(image), alpha_map=alpha, per_triangle_max_weight=maxw,
-                        per_triangle_pixel_count=pixc, per_triangle_area=area, fragments=frags)
+    out = RenderOutput(image=ImageBuffer(image), alpha_map=alpha, per_triangle_max_weight=maxw,
+                       per_triangle_pixel_count=pixc, per_triangle_area=area, fragments=frags)
+    LAST_RENDER_TIMES = {"upload_ms": (t1 - t0) * 1e3, "forward_ms": (t2 - t1) * 1e3,
+                         "download_ms": (t3 - t2) * 1e3, "total_ms": (time.perf_counter() - t0) * 1e3}
+    return out
 
 
 def render_backward(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0), d_image=None,

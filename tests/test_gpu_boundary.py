@@ -102,3 +102,22 @@ def test_tile_size_zero_raises_like_reference():
         tsb.render(soup, intr, pose, mode, tile_size=0)
     with pytest.raises(ValueError):
         tsb.render(soup, intr, pose, mode, tile_size=-16)
+
+
+def test_render_outputs_are_independent_across_calls():
+    """render() returns arrays in pooled page-locked buffers: a buffer is reused
+    only after every array of an earlier call is gone, so holding the outputs of
+    one call while rendering another never changes them."""
+    import gc
+    from paper_2505_19175_b200 import rasterizer as tsb
+    soup, intr, pose, mode = _load(golden_paths()[0])
+    a = tsb.render(soup, intr, pose, mode, background=(0.1, 0.2, 0.3))
+    img_a, maxw_a, pix_a = a.image.rgb.copy(), a.per_triangle_max_weight.copy(), a.per_triangle_pixel_count.copy()
+    b = tsb.render(soup, intr, pose, mode, background=(0.9, 0.8, 0.7))
+    assert np.array_equal(a.image.rgb, img_a) and np.array_equal(a.per_triangle_max_weight, maxw_a)
+    assert np.array_equal(a.per_triangle_pixel_count, pix_a)
+    assert not np.array_equal(a.image.rgb, b.image.rgb)
+    del a, b
+    gc.collect()
+    c = tsb.render(soup, intr, pose, mode, background=(0.1, 0.2, 0.3))
+    assert np.array_equal(c.image.rgb, img_a)

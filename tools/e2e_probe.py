@@ -28,9 +28,18 @@ ms, ds = t(lambda: R.DeviceSoup.from_soup(soup, dtype=torch.float64))
 print(f"upload fp64 soup (staged): {ms:.2f} ms")
 ms, f = t(lambda: rast.forward(ds, intr, pose))
 print(f"forward on the fp64 soup: {ms:.2f} ms")
-ms, _ = t(lambda: R._numpy_after_sync(R._to_numpy(f.image, np.float64), R._to_numpy(f.alpha_map, np.float64),
-                                     R._to_numpy(f.max_weight, np.float64), R._to_numpy(f.pixel_count, np.int64),
-                                     R._to_numpy(f.area, np.float64)))
+def outputs():
+    packed = torch.cat([f.image.reshape(-1).double(), f.alpha_map.reshape(-1).double(), f.max_weight.double(),
+                        f.area.double()])
+    h = torch.empty(packed.numel(), dtype=torch.float64, pin_memory=True)
+    h.copy_(packed, non_blocking=True)
+    hp = torch.empty(f.pixel_count.numel(), dtype=torch.int64, pin_memory=True)
+    hp.copy_(f.pixel_count.long(), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy(), hp.numpy()
+
+
+ms, _ = t(outputs)
 print(f"outputs to host (pinned): {ms:.2f} ms")
 ms, _ = t(lambda: R.render(soup, intr, pose))
 print(f"render() total: {ms:.2f} ms ({1e3 / ms:.1f} FPS)")
