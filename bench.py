@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--train-views", type=int, default=64)
     ap.add_argument("--train-steps", type=int, default=2)
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo launcher + collective check, no kernels")
+    ap.add_argument("--tile-backward", action="store_true", help="training: tile backward instead of the streaming one")
     return ap.parse_args()
 
 
@@ -519,6 +520,9 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
     mine = shard(len(poses), world, rank)
     d_images = [torch.randn((c3.height, c3.width, 3), device="cuda", generator=gen)
                 if v in mine else None for v in range(len(poses))]
+    if args.tile_backward:
+        from paper_2505_19175_b200 import _lib
+        rast.set_option(_lib.TS_OPT_TILE_BACKWARD, 1)
     trainer = B200ViewTrainer(ds3, intr3, poses, d_images, rasterizer=rast, precision=args.precision)
     trainer.step()  # warm-up (synchronous forwards size the buffers)
     torch.cuda.synchronize()
