@@ -636,7 +636,7 @@ def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
     if frags is not None:
         LAST_RENDER_D2H_BYTES += sum(np.asarray(a).nbytes for a in (frags.offsets, frags.triangle,
                                                                       frags.weight, frags.depth))
-    out = RenderOutput(image=ImageBuffer(image), alpha_map=alpha, per_triangle_max_weight=maxw,
+    out = RenderOutput(image=ImageBuffer.trusted(image), alpha_map=alpha, per_triangle_max_weight=maxw,
                        per_triangle_pixel_count=pixc, per_triangle_area=area, fragments=frags)
     LAST_RENDER_TIMES = {"upload_ms": (t1 - t0) * 1e3, "forward_ms": (t2 - t1) * 1e3,
                          "download_ms": (t3 - t2) * 1e3, "total_ms": (time.perf_counter() - t0) * 1e3}

@@ -113,6 +113,7 @@ def test_render_outputs_are_independent_across_calls():
     soup, intr, pose, mode = _load(golden_paths()[0])
     a = tsb.render(soup, intr, pose, mode, background=(0.1, 0.2, 0.3))
     img_a, maxw_a, pix_a = a.image.rgb.copy(), a.per_triangle_max_weight.copy(), a.per_triangle_pixel_count.copy()
+    assert np.isfinite(img_a).all() and img_a.min() >= 0.0 and img_a.max() <= 1.0  # (ImageBuffer.trusted)
     b = tsb.render(soup, intr, pose, mode, background=(0.9, 0.8, 0.7))
     assert np.array_equal(a.image.rgb, img_a) and np.array_equal(a.per_triangle_max_weight, maxw_a)
     assert np.array_equal(a.per_triangle_pixel_count, pix_a)
