@@ -94,19 +94,23 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 gf[10] = w * d2;
                 const double ga = d0 * (tb * c0 - s0 * inv1m) + d1 * (tb * c1 - s1 * inv1m) + d2 * (tb * c2 - s2 * inv1m);
                 if (!clamped) {
-                    const double window = a / o;
+                    // (reciprocals of the opacity and of phi_s precomputed per triangle: the
+                    // products differ from the quotients by <= 1 ulp)
+                    const double inv_o = __ldg(&Cc.inv_opa), inv_phis = __ldg(&B.inv_phis);
+                    const double window = a * inv_o;
                     gf[6] = ga * window;  // d/d opacity = g_alpha * alpha / o
                     const double g_win = o * ga;
                     const double phi = r64 * phis;
                     double g_phi;
                     if (mode == 0) {
                         gf[7] = g_win * window * log(rc);
-                        const double g_r = g_win * sg * window / rc;
+                        // window / rc = rc^(sigma - 1): 1 for sigma = 1
+                        const double g_r = g_win * sg * (sg == 1.0 ? 1.0 : window / rc);
                         if (r64 >= 1.0) {
                             g_phi = 0.0;
                         } else {
-                            g_phi = g_r / phis;
-                            gf[11] = -g_r * r64 / phis;
+                            g_phi = g_r * inv_phis;
+                            gf[11] = -g_r * r64 * inv_phis;
                         }
                     } else {
                         const double E = exp(fmin(phi / sg, 700.0));

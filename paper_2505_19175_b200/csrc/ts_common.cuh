@@ -83,7 +83,7 @@ static_assert(sizeof(RecF) == 128, "RecF layout");
 struct __align__(16) RecB {
     double qx[3], qy[3];
     double sl[3], ul[3], vl[3];
-    double pad;
+    double inv_phis;  // 1 / phi_s (the backward multiplies instead of dividing)
 };
 static_assert(sizeof(RecB) == 128, "RecB layout");
 
@@ -95,7 +95,7 @@ static_assert(sizeof(RecB) == 128, "RecB layout");
 struct __align__(16) RecC {
     double opa, sig;  // (16-byte aligned pairs: one double2 load each)
     double rgb[3];
-    double pad;
+    double inv_opa;   // 1 / opacity (the backward multiplies instead of dividing)
 };
 static_assert(sizeof(RecC) == 48, "RecC layout");
 

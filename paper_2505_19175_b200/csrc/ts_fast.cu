@@ -275,7 +275,7 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
                     rb.ul[e] = ex * il * il;
                     rb.vl[e] = ey * il * il;
                 }
-                rb.pad = 0.0;
+                rb.inv_phis = 1.0 / phis;
                 out.recb[i] = rb;
             }
             if (out.recc) {
@@ -285,7 +285,7 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
                 rc.rgb[2] = fmin(fmax(d2, 0.0), 1.0);
                 rc.opa = o;
                 rc.sig = sg;
-                rc.pad = 0.0;
+                rc.inv_opa = 1.0 / o;
                 out.recc[i] = rc;
             }
             (void)qf;
