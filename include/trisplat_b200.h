@@ -181,8 +181,11 @@ int ts_collect_fragments(ts_context* ctx, const int64_t* offsets, int32_t* trian
  * weight and depth of every fragment of the last forward, in the CSR layout
  * of ts_fragment_offsets (device arrays).  A layout that differs from this
  * scene/camera returns TS_ERR_FRAGMENTS.  Needs a keep_backward forward on
- * the fast path. */
-int ts_backward_fragments(ts_context* ctx, const float* d_image, const int64_t* offsets,
+ * the fast path.  weight (nullable): the fragments' blend weights of this
+ * forward (ts_collect_fragments' weight array); with it the gradient streams
+ * over the forward's fragment records (per-pixel suffix sums of d_weight *
+ * weight from the CSR), without it the tile backward replays every pixel. */
+int ts_backward_fragments(ts_context* ctx, const float* d_image, const int64_t* offsets, const double* weight,
                           const double* d_weight, const double* d_depth, const ts_grads* grads,
                           int accumulate, void* stream);
 

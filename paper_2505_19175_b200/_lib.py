@@ -110,7 +110,8 @@ def load(path: str = LIB_PATH):
                                          ctypes.c_void_p, ctypes.c_void_p]
     lib.ts_collect_fragments.restype = ctypes.c_int
     lib.ts_backward_fragments.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                          ctypes.c_void_p, P(TsGrads), ctypes.c_int, ctypes.c_void_p]
+                                          ctypes.c_void_p, ctypes.c_void_p, P(TsGrads), ctypes.c_int,
+                                          ctypes.c_void_p]
     lib.ts_backward_fragments.restype = ctypes.c_int
     lib.ts_set_async.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.ts_set_async.restype = ctypes.c_int

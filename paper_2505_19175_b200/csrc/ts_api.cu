@@ -52,6 +52,7 @@ struct ts_context {
     DevBuf frag_off, cs_scratch;  // expected fragment CSR offsets + scan scratch
     DevBuf tl_cnt, tl_off, tl_cs, tl_kv;  // ts_tile_lists scratch
     DevBuf adam_ibc;                      // Adam bias corrections of the current step
+    DevBuf fsw;                           // per fragment: suffix of dw * w (fragment-gradient backward)
     DevBuf frec, ctot;            // training forward: fragment records + final unclipped colour
     unsigned long long frec_cap = 0;
     long long frec_hint = 0;      // largest fragment-record count seen (record-buffer sizing)
@@ -347,7 +348,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->tri_buf);
     cudaFree(c->ent_buf);
     cudaFree(c->pix_buf);
-    for (DevBuf* b : {&c->adam_ibc, &c->tl_cnt, &c->tl_off, &c->tl_cs, &c->tl_kv, &c->rec64, &c->recf, &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
+    for (DevBuf* b : {&c->fsw, &c->adam_ibc, &c->tl_cnt, &c->tl_off, &c->tl_cs, &c->tl_kv, &c->rec64, &c->recf, &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
                       &c->ctot, &c->binmat, &c->lossbuf, &c->densbuf})
         cudaFree(b->p);
     cudaFree(c->sort_buf);
@@ -676,7 +677,8 @@ int ts_set_option(ts_context* c, int option, int64_t value) {
 
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                          const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream,
-                         int n_chunks = 0, const int64_t* bounds = nullptr, void* const* events = nullptr);
+                         int n_chunks = 0, const int64_t* bounds = nullptr, void* const* events = nullptr,
+                         const double* frag_w = nullptr, long long n_frag_total = 0);
 
 int ts_backward(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                 void* stream) {
@@ -755,8 +757,9 @@ int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangl
     return cuda_err(cudaGetLastError());
 }
 
-int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* offsets, const double* d_weight,
-                          const double* d_depth, const ts_grads* grads, int accumulate, void* stream) {
+int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* offsets, const double* weight,
+                          const double* d_weight, const double* d_depth, const ts_grads* grads, int accumulate,
+                          void* stream) {
     DeviceGuard device_guard(c);
     if (!c || !d_image || !grads || !offsets || !d_weight || !d_depth) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
@@ -775,13 +778,14 @@ int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* of
     TS_CHECK(cudaMemcpyAsync(&bad, &c->d_ctr->pad[0], sizeof(bad), cudaMemcpyDeviceToHost, st));
     TS_CHECK(cudaStreamSynchronize(st));
     if (bad) return TS_ERR_FRAGMENTS;
-    (void)f;
-    return backward_impl(c, d_image, grads, accumulate, (const long long*)offsets, d_weight, d_depth, stream);
+    return backward_impl(c, d_image, grads, accumulate, (const long long*)offsets, d_weight, d_depth, stream, 0,
+                         nullptr, nullptr, weight, f);
 }
 
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                          const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream,
-                         int n_chunks, const int64_t* bounds, void* const* events) {
+                         int n_chunks, const int64_t* bounds, void* const* events, const double* frag_w,
+                         long long n_frag_total) {
     if (!c || !d_image || !grads) return TS_ERR_INVALID_ARG;
     if (!c->have_fwd) return TS_ERR_NO_FORWARD;
     if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
@@ -794,16 +798,20 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
         double* sg = (double*)c->sg64.p;
         stage_begin(c, TS_STAGE_BLEND_BWD, st);
         if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
-        if (c->frec_ready && !frag_off) {
-            // streaming backward over the forward's fragment records; the tile
-            // backward runs instead only if the record buffer overflowed
+        if (c->frec_ready && (!frag_off || frag_w)) {
+            // streaming backward over the forward's fragment records (with the
+            // fragment-gradient terms when the caller passes the fragments' weights);
+            // the tile backward runs instead only if the record buffer overflowed
+            if (frag_off && (rc = ensure(c->fsw, sizeof(double) * (size_t)(n_frag_total > 0 ? n_frag_total : 1))))
+                return rc;
             launch_bwd_stream(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, (const RecC*)c->recc.p,
                               (const FragRec*)c->frec.p, c->d_ctr, c->frec_cap, (const double*)c->ctot.p, d_image,
-                              sg, st);
+                              sg, st, frag_off, frag_w, fg_dw, fg_dz, frag_off ? (double*)c->fsw.p : nullptr);
             launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
                                    (const RecC*)c->recc.p, c->tile_start,
-                                   c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, nullptr, nullptr, nullptr,
+                                   c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
                                    &c->d_ctr->frec_over, sg, st);
+            g_launches += frag_off ? 1 : 0;
         } else
             launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
                                    (const RecC*)c->recc.p, c->tile_start,

@@ -27,11 +27,40 @@ namespace ts {
 #define TS_BWD_GRID 3  // CTAs per SM in the launch (one resident wave: 1.29 -> 1.19 ms at C3 against 8)
 #endif
 
+// Upstream gradients on the fragments' blend weights and depths (render_backward
+// with frag_grads, _kernels.py:262-272), addressed through the fragment CSR:
+// record (pixel p, ordinal k) is fragment off[p] + k.  sw[i] = sum over the
+// pixel's later fragments of dw * w (k_frag_suffix).
+struct FragGrads {
+    const long long* off;
+    const double* dw;
+    const double* dz;
+    const double* sw;
+};
+
+// sw[i] = sum_{i < k < end(p)} dw[k] w[k] per pixel p, back to front (the
+// reference's running `sw`, _kernels.py:265-268)
+__global__ void __launch_bounds__(256) k_frag_suffix(long long npix, const long long* __restrict__ off,
+                                                     const double* __restrict__ w, const double* __restrict__ dw,
+                                                     double* __restrict__ sw) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npix) return;
+    const long long lo = off[p], hi = off[p + 1];
+    double acc = 0.0;
+    for (long long i = hi - 1; i >= lo; i--) {
+        sw[i] = acc;
+        acc += dw[i] * w[i];
+    }
+}
+
+template <bool FRAG>
 __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts opt, const RecF* __restrict__ rec,
                                                  const RecB* __restrict__ recb, const RecC* __restrict__ recc,
                                                  const FragRec* __restrict__ frec, const Counters* __restrict__ ctr,
                                                  unsigned long long cap, const double* __restrict__ c_total,
-                                                 const float* __restrict__ d_image, double* __restrict__ sgrad) {
+                                                 const float* __restrict__ d_image, double* __restrict__ sgrad,
+                                                 FragGrads fg) {
+    constexpr int NG = FRAG ? 13 : 12;  // reduced components: gq[6] go gsig grgb[3] gphis (+ gz)
     TS_PDL_ENTRY();
     if (ctr->frec_over) return;
     const unsigned long long total = ctr->n_frec;
@@ -43,16 +72,16 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
     // (interleaved 32-record steps: measured faster than one contiguous range per warp)
     for (long long q0 = gw * 32; q0 < n; q0 += nw * 32) {
         const long long q = q0 + lane;
-        double gf[12];
+        double gf[NG];
 #pragma unroll
-        for (int c = 0; c < 12; c++) gf[c] = 0.0;
+        for (int c = 0; c < NG; c++) gf[c] = 0.0;
         unsigned key = 0xffffffffu - lane;  // unique keys for idle lanes and holes
         bool act = false;
         if (q < n) {
             const double2 ta = __ldg(reinterpret_cast<const double2*>(frec + q));
             const double2 tb2 = __ldg(reinterpret_cast<const double2*>(frec + q) + 1);
             const double4 tc = make_double4(ta.x, ta.y, tb2.x, tb2.y);
-            const uint4 ids = __ldg(reinterpret_cast<const uint4*>(frec + q) + 2);
+            const uint4 ids = __ldg(reinterpret_cast<const uint4*>(frec + q) + 2);  // pix, src, ordinal
             if (ids.x != 0xffffffffu) {
                 act = true;
                 const unsigned pix = ids.x, src = ids.y;
@@ -92,7 +121,12 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 gf[8] = w * d0;
                 gf[9] = w * d1;
                 gf[10] = w * d2;
-                const double ga = d0 * (tb * c0 - s0 * inv1m) + d1 * (tb * c1 - s1 * inv1m) + d2 * (tb * c2 - s2 * inv1m);
+                double ga = d0 * (tb * c0 - s0 * inv1m) + d1 * (tb * c1 - s1 * inv1m) + d2 * (tb * c2 - s2 * inv1m);
+                if constexpr (FRAG) {
+                    const long long fi = __ldg(fg.off + pix) + ids.z;
+                    ga += __ldg(fg.dw + fi) * tb - __ldg(fg.sw + fi) * inv1m;
+                    gf[12] = __ldg(fg.dz + fi);
+                }
                 if (!clamped) {
                     // (reciprocals of the opacity and of phi_s precomputed per triangle: the
                     // products differ from the quotients by <= 1 ulp)
@@ -152,7 +186,7 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
             const unsigned ro = __shfl_down_sync(0xffffffffu, rid, off);
             const bool same = (int)lane + off < 32 && ro == rid;
 #pragma unroll
-            for (int c = 0; c < 12; c++) {
+            for (int c = 0; c < NG; c++) {
                 const double v = __shfl_down_sync(0xffffffffu, gf[c], off);
                 if (same) gf[c] += v;
             }
@@ -160,17 +194,26 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
         if (act && head) {
             double* dst = sgrad + (size_t)key * SG_STRIDE;
 #pragma unroll
-            for (int c = 0; c < 12; c++)
-                if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);
+            for (int c = 0; c < NG; c++)
+                if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);  // (component 12 = SG_GZ)
         }
     }
 }
 
 void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
                        const FragRec* frec, const Counters* ctr, unsigned long long cap, const double* c_total,
-                       const float* d_image, double* sgrad, cudaStream_t st) {
-    launch_pdl(k_bwd_stream, dim3(sm_count() * TS_BWD_GRID), dim3(256), 0, st, cam, opt, rec, recb, recc, frec, ctr, cap, c_total,
-               d_image, sgrad);
+                       const float* d_image, double* sgrad, cudaStream_t st, const long long* frag_off,
+                       const double* frag_w, const double* fg_dw, const double* fg_dz, double* sw) {
+    const dim3 grid(sm_count() * TS_BWD_GRID);
+    if (!frag_off) {
+        launch_pdl(k_bwd_stream<false>, grid, dim3(256), 0, st, cam, opt, rec, recb, recc, frec, ctr, cap, c_total,
+                   d_image, sgrad, FragGrads{});
+        return;
+    }
+    const long long npix = (long long)cam.width * cam.height;
+    if (npix > 0) k_frag_suffix<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(npix, frag_off, frag_w, fg_dw, sw);
+    launch_pdl(k_bwd_stream<true>, grid, dim3(256), 0, st, cam, opt, rec, recb, recc, frec, ctr, cap, c_total, d_image,
+               sgrad, FragGrads{frag_off, fg_dw, fg_dz, sw});
 }
 
 }  // namespace ts

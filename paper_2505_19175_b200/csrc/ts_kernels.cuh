@@ -133,9 +133,13 @@ void launch_blend_bwd_dense(const Cam& cam, const Opts& opt, const RecF* rec, co
                             const double* fg_dw, const double* fg_dz, const unsigned long long* run_if, double* sgrad,
                             cudaStream_t st);
 // ts_bwd_stream.cu: streaming backward over the training forward's fragment records
+// with frag_off: the fragment-gradient terms too (frag_w: the fragments' blend weights from
+// ts_collect_fragments of the same forward; sw: scratch of F doubles)
 void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const RecB* recb, const RecC* recc,
                        const FragRec* frec, const Counters* ctr, unsigned long long cap, const double* c_total,
-                       const float* d_image, double* sgrad, cudaStream_t st);
+                       const float* d_image, double* sgrad, cudaStream_t st, const long long* frag_off = nullptr,
+                       const double* frag_w = nullptr, const double* fg_dw = nullptr, const double* fg_dz = nullptr,
+                       double* sw = nullptr);
 
 // ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
 bool chain_bwd_fast_ok(const ts_soup& soup, int dtype, const ts_grads& g);

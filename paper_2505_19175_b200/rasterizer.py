@@ -420,9 +420,12 @@ class Rasterizer:
 
     def backward_fragments(self, d_image: torch.Tensor, offsets: torch.Tensor, d_weight: torch.Tensor,
                            d_depth: torch.Tensor, grads: DeviceGrads | None = None, accumulate: bool = False,
-                           stream=None) -> DeviceGrads:
+                           stream=None, weight: torch.Tensor | None = None) -> DeviceGrads:
         """backward() plus upstream gradients on the blend weight and depth of
-        every fragment (render_backward(frag_grads=...), backward.py:122-142)."""
+        every fragment (render_backward(frag_grads=...), backward.py:122-142).
+        ``weight``: the fragments' blend weights of this forward
+        (``fragments().weight``); with it the gradient streams over the
+        forward's fragment records instead of replaying every pixel."""
         if self._last is None:
             raise RuntimeError("backward_fragments() needs a preceding forward()")
         n, h, w = self._last
@@ -439,7 +442,11 @@ class Rasterizer:
         _check_grads(grads, n)
         st = (stream or torch.cuda.current_stream(dev)).cuda_stream
         g = grads._ts()
-        rc = self.lib.ts_backward_fragments(self._ctx, _ptr(d_image), _ptr(offsets), _ptr(d_weight),
+        if weight is not None:
+            weight = weight.to(device=dev, dtype=torch.float64).contiguous()
+            if weight.numel() != d_weight.numel():
+                raise ValueError("fragment gradients do not match this scene/camera")
+        rc = self.lib.ts_backward_fragments(self._ctx, _ptr(d_image), _ptr(offsets), _ptr(weight), _ptr(d_weight),
                                             _ptr(d_depth), ctypes.byref(g), int(bool(accumulate)),
                                             ctypes.c_void_p(st))
         if rc == _lib.TS_ERR_FRAGMENTS:

@@ -44,14 +44,21 @@ def test_golden_fragment_lists(rast, path):
     assert np.abs(fr.weight - g["frag_weight"]).max(initial=0.0) <= 1e-9
 
 
+def _weights(rast, backward):
+    """The stream backward takes the fragments' weights of the same forward."""
+    return rast.fragments().weight if backward == "stream" else None
+
+
+@pytest.mark.parametrize("backward", ["tile", "stream"])
 @pytest.mark.parametrize("path", golden_paths()[:6], ids=lambda p: p.split("/")[-1])
-def test_golden_fragment_gradients(rast, path):
+def test_golden_fragment_gradients(rast, path, backward):
     from oracle import oracle as O
     g = GoldenScene(path)
     rast.forward(_dev(g.soup), g.intr, g.pose, mode=g.mode, background=g.background)
     off, dw, dz = _fg(g["frag_offsets"], 7)
     gr = rast.backward_fragments(torch.as_tensor(g.d_image, dtype=torch.float32, device="cuda"),
-                                 torch.from_numpy(off), torch.from_numpy(dw), torch.from_numpy(dz))
+                                 torch.from_numpy(off), torch.from_numpy(dw), torch.from_numpy(dz),
+                                 weight=_weights(rast, backward))
     ref = O.render_backward(g.soup, g.intr, g.pose, mode=g.mode, background=g.background,
                             d_image=g.d_image, frag_grads=(off, dw, dz))
     for k in ("d_vertices", "d_opacity", "d_sigma", "d_sh"):
@@ -59,8 +66,9 @@ def test_golden_fragment_gradients(rast, path):
         assert err < GRAD_RTOL, f"{g.name} {k} rel err {err}"
 
 
+@pytest.mark.parametrize("backward", ["tile", "stream"])
 @pytest.mark.parametrize("mode", ["normalized", "sigmoid"])
-def test_mid_scene_fragments_and_gradients(rast, mode):
+def test_mid_scene_fragments_and_gradients(rast, mode, backward):
     from oracle import oracle as O
     from paper_2505_19175_b200 import scenes
     soup = scenes.make_soup(20000, seed=5, size=0.08, sigma=(0.5, 3.0))
@@ -75,7 +83,8 @@ def test_mid_scene_fragments_and_gradients(rast, mode):
     d_image = scenes.make_d_image(5, intr.height, intr.width)
     off, dw, dz = _fg(fr.offsets, 9)
     gr = rast.backward_fragments(torch.as_tensor(d_image, dtype=torch.float32, device="cuda"),
-                                 torch.from_numpy(off), torch.from_numpy(dw), torch.from_numpy(dz))
+                                 torch.from_numpy(off), torch.from_numpy(dw), torch.from_numpy(dz),
+                                 weight=_weights(rast, backward))
     gref = O.render_backward(soup, intr, pose, mode=mode, d_image=d_image, frag_grads=(off, dw, dz))
     for k in ("d_vertices", "d_opacity", "d_sigma", "d_sh"):
         err = rel_err(getattr(gr, k).double().cpu().numpy(), getattr(gref, k))

@@ -143,3 +143,32 @@ def test_legacy_binning_cross_check(rast):
         rast.set_option(_lib.TS_OPT_LEGACY_BINNING, 0)
     assert np.array_equal(er, ref.entry_tri) and np.array_equal(ts, ref.tile_start)
     assert np.array_equal(last, ref.last_src)
+
+
+def test_c3_fragment_gradient_stream_parity(rast):
+    """configs[2] with the reference's default training regularisers in play:
+    render_backward(frag_grads=(offsets, d_weight, d_depth)) through the
+    streaming backward (the forward's fragment records, per-pixel suffix sums
+    of d_weight * weight over the CSR of fragments()) against the oracle, every
+    element within the reference's rtol 1e-4 + atol 1e-7."""
+    from oracle import oracle as O
+    from paper_2505_19175_b200 import scenes
+    soup, intr, pose, ds, ref, z = scene("c3")
+    d_image = scenes.make_d_image(3, intr.height, intr.width, fp32=True)
+    rast.forward(ds, intr, pose, precision="fast")
+    fr = rast.fragments()
+    off = _np(fr.offsets)
+    nf = int(off[-1])
+    rng = np.random.default_rng(31)
+    dw = rng.normal(size=nf) * 1e-2
+    dz = rng.normal(size=nf) * 1e-3
+    g = rast.backward_fragments(torch.as_tensor(d_image, dtype=torch.float32, device="cuda"), fr.offsets,
+                                torch.from_numpy(dw).cuda(), torch.from_numpy(dz).cuda(), weight=fr.weight)
+    torch.cuda.synchronize()
+    gref = O.render_backward(soup, intr, pose, d_image=d_image, frag_grads=(off, dw, dz))
+    msgs = []
+    for k in SG.GROUPS:
+        nb, worst = SG.grad_violations(_np(getattr(g, k)), getattr(gref, k))
+        if nb:
+            msgs.append(f"{k}: {nb} values outside rtol 1e-4 + atol 1e-7 (worst {worst:.2f}x tolerance)")
+    assert not msgs, "; ".join(msgs)

@@ -34,7 +34,7 @@ def it(ev=None):
     depth = losses.depth_from_fragments(frags, c3.height, c3.width, rasterizer=r)
     _, dv, d_w2 = losses.normal_loss(ds, frags, depth, intr, pose, rasterizer=r)
     mark(3)
-    g = r.backward_fragments(d_img, frags.offsets, d_w * 100.0 + d_w2 * 1e-4, d_z * 100.0)
+    g = r.backward_fragments(d_img, frags.offsets, d_w * 100.0 + d_w2 * 1e-4, d_z * 100.0, weight=frags.weight)
     mark(4)
     return g
 
