@@ -750,8 +750,15 @@ int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangl
     bo.frag_w = weight;
     bo.frag_z = depth;
     bo.zkey = c->key;
-    launch_blend_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, c->bbox, c->tile_start, c->ent_src,
-                      bo, st);
+    if (c->have_bwd_state) {
+        // a training forward: its fp64-compositing dense blend again, emitting each
+        // pixel's fragments into its CSR list (no records, images or statistics)
+        bo.recc = (const RecC*)c->recc.p;
+        launch_blend_dense(c->cam, c->opt, true, (const RecF*)c->recf.p, c->tile_start, c->ent_src, bo, st);
+    } else {
+        launch_blend_fast(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, c->bbox, c->tile_start,
+                          c->ent_src, bo, st);
+    }
     launch_fixup_fwd(c->cam, c->opt, c->soup, c->dtype, (const RecF*)c->recf.p, c->tile_start, c->ent_src, bo, st);
     g_launches += 2;
     return cuda_err(cudaGetLastError());

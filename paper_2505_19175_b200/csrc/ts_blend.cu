@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
     float epsT = 0.f;  // relative error bound of the fp32 transmittance
     int last = -1, cnt = 0, flag_pos = -1;
     bool done = !inside;
+    long long fbase = 0;  // collect_fragments: the pixel's first CSR slot
+    if constexpr (ACC64)
+        if (out.frag_tri && inside) fbase = out.frag_off[py * cam.width + px];
     if (tid < DB) {
         sm.maxw[tid] = 0u;
         sm.pix[tid] = 0;
@@ -544,6 +547,13 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                             fr[0] = make_double4((double)T, (double)C0, (double)C1, (double)C2);
                             reinterpret_cast<uint4*>(fr + 1)[0] =
                                 make_uint4((unsigned)(py * cam.width + px), sm.srcq[(b + j) & (SR - 1)], (unsigned)cnt, 0u);
+                        }
+                        if (out.frag_tri) {  // collect_fragments: fragment cnt of this pixel's CSR list
+                            const long long fi = fbase + cnt;
+                            const unsigned src = sm.srcq[(b + j) & (SR - 1)];
+                            out.frag_tri[fi] = (int)src;
+                            out.frag_w[fi] = wd64;
+                            out.frag_z[fi] = __longlong_as_double((long long)__ldg(out.zkey + src));
                         }
                         C0 += wd64 * rcj.rgb[0];
                         C1 += wd64 * rcj.rgb[1];
