@@ -281,51 +281,88 @@ void launch_photometric_loss(const float* x, const float* y, int H, int W, doubl
 // its CSR fragment run: the reference's O(F) prefix-sum form when the run is
 // sorted by depth (the compositing order), the pairwise form otherwise.
 // ---------------------------------------------------------------------------
+// warp-inclusive scan of v over the lanes
+__device__ __forceinline__ double warp_incl_scan(double v, unsigned lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, v, off);
+        if ((int)lane >= off) v += y;
+    }
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Warp per pixel: the pixel's fragment list is read with coalesced loads, 32 fragments
+// per step.  Depth-sorted lists (every list the rasterizer emits: fragments are
+// composited in depth order) take the prefix-sum form -- fragment k's weight /
+// weighted depth in front (wb, sb) are warp scans, the totals (tw, ts) a first
+// pass; other lists the pairwise form (_distortion_pairwise :153-166).
 __global__ void __launch_bounds__(256) k_distortion(long long npix, const long long* __restrict__ off,
                                                     const double* __restrict__ w, const double* __restrict__ z,
                                                     double scale, double* __restrict__ d_w,
                                                     double* __restrict__ d_z, double* __restrict__ part) {
     __shared__ double s_red[8];
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned lane = threadIdx.x & 31;
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     double tot = 0.0;
     if (p < npix) {
         const long long lo = off[p], hi = off[p + 1];
-        bool sorted = true;
-        double tw = 0.0, ts = 0.0;
-        for (long long k = lo; k < hi; k++) {
-            tw += w[k];
-            ts += w[k] * z[k];
-            if (k > lo && z[k] < z[k - 1]) sorted = false;
-        }
         if (hi - lo < 2) {
-            for (long long k = lo; k < hi; k++) {
-                if (d_w) d_w[k] = 0.0;
-                if (d_z) d_z[k] = 0.0;
+            if (lane == 0 && hi > lo) {
+                if (d_w) d_w[lo] = 0.0;
+                if (d_z) d_z[lo] = 0.0;
             }
-        } else if (sorted) {
-            double wb = 0.0, sb = 0.0;  // weight / weighted depth in front
-            for (long long k = lo; k < hi; k++) {
-                const double wk = w[k], zk = z[k];
-                const double wa = tw - wb - wk, sa = ts - sb - wk * zk;
-                const double fwd = zk * wb - sb;
-                tot += wk * fwd;
-                if (d_w) d_w[k] = 2.0 * (fwd + (sa - zk * wa)) * scale;
-                if (d_z) d_z[k] = 2.0 * wk * (wb - wa) * scale;
-                wb += wk;
-                sb += wk * zk;
-            }
-            tot *= 2.0;
-        } else {  // pairwise (_distortion_pairwise :153-166)
-            for (long long i = lo; i < hi; i++) {
-                double gw_ = 0.0, gz = 0.0;
-                for (long long j = lo; j < hi; j++) {
-                    const double dz = z[i] - z[j];
-                    tot += w[i] * fabs(dz) * w[j];
-                    gw_ += fabs(dz) * w[j];
-                    gz += (double)((dz > 0.0) - (dz < 0.0)) * w[j];
+        } else {
+            double tw = 0.0, ts = 0.0;
+            bool sorted = true;
+            for (long long k0 = lo; k0 < hi; k0 += 32) {
+                const long long k = k0 + lane;
+                double wk = 0.0, zk = 0.0;
+                if (k < hi) {
+                    wk = w[k];
+                    zk = z[k];
+                    if (k > lo && zk < z[k - 1]) sorted = false;
                 }
-                if (d_w) d_w[i] = 2.0 * gw_ * scale;
-                if (d_z) d_z[i] = 2.0 * gz * w[i] * scale;
+                tw += wk;
+                ts += wk * zk;
+            }
+            tw = warp_sum(tw);
+            ts = warp_sum(ts);
+            if (__all_sync(0xffffffffu, sorted)) {
+                double cw = 0.0, cs = 0.0;  // carried from earlier steps
+                for (long long k0 = lo; k0 < hi; k0 += 32) {
+                    const long long k = k0 + lane;
+                    const bool in = k < hi;
+                    const double wk = in ? w[k] : 0.0, zk = in ? z[k] : 0.0;
+                    const double iw = warp_incl_scan(wk, lane), is = warp_incl_scan(wk * zk, lane);
+                    const double wb = cw + iw - wk, sb = cs + is - wk * zk;
+                    if (in) {
+                        const double wa = tw - wb - wk, sa = ts - sb - wk * zk;
+                        const double fwd = zk * wb - sb;
+                        tot += wk * fwd;
+                        if (d_w) d_w[k] = 2.0 * (fwd + (sa - zk * wa)) * scale;
+                        if (d_z) d_z[k] = 2.0 * wk * (wb - wa) * scale;
+                    }
+                    cw += __shfl_sync(0xffffffffu, iw, 31);
+                    cs += __shfl_sync(0xffffffffu, is, 31);
+                }
+                tot *= 2.0;
+            } else {  // pairwise (_distortion_pairwise :153-166)
+                for (long long i = lo + lane; i < hi; i += 32) {
+                    double gw_ = 0.0, gz = 0.0;
+                    for (long long j = lo; j < hi; j++) {
+                        const double dz = z[i] - z[j];
+                        tot += w[i] * fabs(dz) * w[j];
+                        gw_ += fabs(dz) * w[j];
+                        gz += (double)((dz > 0.0) - (dz < 0.0)) * w[j];
+                    }
+                    if (d_w) d_w[i] = 2.0 * gw_ * scale;
+                    if (d_z) d_z[i] = 2.0 * gz * w[i] * scale;
+                }
             }
         }
     }
@@ -504,13 +541,13 @@ void launch_normal_loss(const float* v, long long n, const long long* off, const
     if (n > 0 && d_vertices) k_normal_chain<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, gc, d_vertices);
 }
 
-size_t distortion_scratch_bytes(long long npix) { return sizeof(double) * (size_t)((npix + 255) / 256 + 1); }
+size_t distortion_scratch_bytes(long long npix) { return sizeof(double) * (size_t)((npix + 7) / 8 + 1); }
 
 void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,
                             long long image_size, double* out, double* d_w, double* d_z, void* scratch,
                             cudaStream_t st) {
     const double scale = 1.0 / (double)(image_size > 1 ? image_size : 1);
-    const int nb = (int)((npix + 255) / 256);
+    const int nb = (int)((npix + 7) / 8);  // warp per pixel
     double* part = (double*)scratch;
     if (nb > 0) k_distortion<<<nb, 256, 0, st>>>(npix, off, w, z, scale, d_w, d_z, part);
     k_sum_scaled<<<1, 256, 0, st>>>(part, nb, scale, out);
