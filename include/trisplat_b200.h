@@ -125,7 +125,11 @@ int ts_forward(ts_context* ctx, const ts_camera* cam, const ts_options* opt, con
  * ts_forward_status synchronizes the stream, fills *result for the last
  * forward and returns its status: TS_ERR_NONFINITE (validate=1),
  * TS_ERR_CAPACITY if its tile entries outgrew the context's buffer (the frame
- * must be repeated; the next forward allocates enough), else TS_OK. */
+ * must be repeated; the next forward allocates enough), else TS_OK.  An
+ * overflow is also reported without polling: the overflow flag lives in
+ * mapped page-locked memory and the next asynchronous ts_forward returns
+ * TS_ERR_CAPACITY (enqueuing nothing) once the device has raised it; the
+ * caller then calls ts_forward_status and repeats the affected frames. */
 int ts_set_async(ts_context* ctx, int enable);
 int ts_forward_status(ts_context* ctx, ts_forward_result* result, void* stream);
 

@@ -90,7 +90,9 @@ struct ts_context {
     Counters* d_ctr = nullptr;
     Counters* h_ctr = nullptr;   // readback of the last frame's counters
     Counters* h_init = nullptr;  // initial counters (never a copy destination: async frames overlap)
-    unsigned* d_sticky = nullptr;  // entry-capacity overflow since the last ts_forward_status
+    unsigned* d_sticky = nullptr;  // entry-capacity overflow since the last ts_forward_status (device view)
+    unsigned* h_sticky = nullptr;  // the same word, page-locked and mapped: an asynchronous forward sees
+                                   // an earlier frame's overflow without a host synchronisation
     // last forward
     bool have_fwd = false;
     bool have_bwd_state = false;
@@ -332,8 +334,11 @@ int ts_context_create(ts_context** out, int device) {
         c->h_init->key_min = ~0ull;
         for (int k = 0; k < 4; k++) c->h_init->err[k] = 0x7fffffffffffffffLL;
     }
-    if (!rc) rc = cuda_err(cudaMalloc(&c->d_sticky, sizeof(unsigned)));
-    if (!rc) rc = cuda_err(cudaMemset(c->d_sticky, 0, sizeof(unsigned)));
+    if (!rc) rc = cuda_err(cudaHostAlloc((void**)&c->h_sticky, sizeof(unsigned), cudaHostAllocMapped));
+    if (!rc) {
+        *(volatile unsigned*)c->h_sticky = 0u;
+        rc = cuda_err(cudaHostGetDevicePointer((void**)&c->d_sticky, c->h_sticky, 0));
+    }
     if (rc) {
         delete c;
         return rc;
@@ -354,7 +359,7 @@ int ts_context_destroy(ts_context* c) {
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
     cudaFree(c->d_ctr);
-    cudaFree(c->d_sticky);
+    cudaFreeHost(c->h_sticky);
     cudaFreeHost(c->h_ctr);
     cudaFreeHost(c->h_init);
     for (int k = 0; k < TS_NUM_STAGES; k++)
@@ -524,6 +529,12 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
         return TS_ERR_INVALID_ARG;
     if (soup->n >= (1ll << 31) || cam->width > 32000 || cam->height > 32000) return TS_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->async_mode && *(volatile unsigned*)c->h_sticky) {
+        // an earlier asynchronous frame outgrew the tile-entry capacity (its tile lists
+        // were emptied): report it here, before more frames are enqueued, whether or
+        // not the caller polls ts_forward_status (which grows the capacity and clears it)
+        return TS_ERR_CAPACITY;
+    }
     c->have_fwd = false;
     c->have_bwd_state = false;
     for (int k = 0; k < TS_NUM_STAGES; k++) c->ev_used[k] = false;

@@ -1,0 +1,33 @@
+"""Asynchronous forwards (ts_set_async): an entry-capacity overflow of a frame
+that nobody polls is reported by the next forward (it used to render
+background silently until ts_forward_status), the status call grows the
+capacity, and the repeated frame matches a synchronous one."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_async_overflow_is_reported_by_the_next_forward():
+    from paper_2505_19175_b200 import scenes
+    from paper_2505_19175_b200.rasterizer import DeviceSoup, Rasterizer
+    r = Rasterizer()
+    intr, pose = scenes.frontal_camera(256, 192, 300.0)
+    sparse = DeviceSoup.from_soup(scenes.make_soup(2000, seed=1, size=0.05, sigma=1.0), dtype=torch.float32)
+    dense = DeviceSoup.from_soup(scenes.make_soup(60000, seed=2, size=0.3, sigma=1.0), dtype=torch.float32)
+    ref = r.forward(dense, intr, pose, keep_backward=False)  # synchronous: grows as needed
+    img_ref = ref.image.clone()
+    r2 = Rasterizer()
+    r2.forward(sparse, intr, pose, keep_backward=False)       # small working capacity
+    r2.set_async(True)
+    r2.forward(dense, intr, pose, keep_backward=False)        # outgrows it
+    torch.cuda.synchronize()
+    with pytest.raises(RuntimeError, match="capacity"):
+        r2.forward(dense, intr, pose, keep_backward=False)
+    with pytest.raises(RuntimeError, match="capacity"):
+        r2.status()                                           # clears the flag, grows the capacity
+    f = r2.forward(dense, intr, pose, keep_backward=False)
+    r2.status()
+    r2.set_async(False)
+    assert np.array_equal(f.image.cpu().numpy(), img_ref.cpu().numpy())
