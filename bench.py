@@ -576,6 +576,38 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
     dinfo = {"n_before": drep["n_before"], "n_after": drep["n_after"], "n_removed": drep["prune"]["n_removed"],
              "n_split": drep["n_split"], "n_clone": drep["n_clone"], "views": dstats.n_views}
     del dsoup, ast2, ast, dstats
+    # the reference's default training iteration (training.py:121-160: beta_distortion,
+    # beta_normal > 0, so fragments every iteration) on one C3 view: training forward,
+    # fragments(), photometric + distortion + depth + normal losses, the backward with
+    # fragment gradients (streaming, weights from fragments())
+    from paper_2505_19175_b200 import losses as L
+    tgt = torch.rand((c3.height, c3.width, 3), device="cuda", generator=gen)
+    v1 = mine[0] if len(mine) else 0
+
+    def default_iteration(ev=None):
+        mark = (lambda k: ev[k].record(stream)) if ev else (lambda k: None)
+        mark(0)
+        fo = rast.forward(ds3, intr3, poses[v1], keep_backward=True, precision=args.precision)
+        mark(1)
+        fr = rast.fragments()
+        mark(2)
+        _, d_img = L.photometric_loss(fo.image, tgt, 0.2, rasterizer=rast)
+        _, d_w, d_z = L.distortion_loss(fr, rasterizer=rast)
+        dep = L.depth_from_fragments(fr, c3.height, c3.width, rasterizer=rast)
+        _, _, d_w2 = L.normal_loss(ds3, fr, dep, intr3, poses[v1], rasterizer=rast)
+        mark(3)
+        rast.backward_fragments(d_img, fr.offsets, d_w * 100.0 + d_w2 * 1e-4, d_z * 100.0, trainer.grads,
+                                accumulate=True, weight=fr.weight)
+        mark(4)
+
+    default_iteration()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    default_iteration(evs)
+    torch.cuda.synchronize()
+    parts = ["forward", "fragments", "losses", "backward_fragments"]
+    default_it = {p: round(evs[i].elapsed_time(evs[i + 1]), 3) for i, p in enumerate(parts)}
+    default_it["total_ms"] = round(evs[0].elapsed_time(evs[4]), 3)
     # per-stage times of one view as in the step (synchronous forward: its entry /
     # visible counts; the backward accumulating into the batch gradient)
     v0 = mine[0] if len(mine) else 0
@@ -603,6 +635,7 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
              "optimizer": "none in the timed step (the metric is fwd+bwd); fused Adam timed separately as adam_ms",
              "gpu_launches_per_step": launches / args.train_steps,
              "adam_ms": adam_ms,
+             "default_iteration_ms": default_it,
              "densify_ms": densify_ms, "densify": dinfo,
              "workload": f"{c3.n} triangles, {c3.width}x{c3.height}, orbit cameras r=6",
              "last_view_stages_ms": {k: round(v, 4) for k, v in stt.items()}}
