@@ -591,8 +591,11 @@ class _PinnedPool:
         """(device-copyable host tensor, numpy array on the same memory) of ``count`` items."""
         import weakref
         nbytes = count * torch.empty(0, dtype=dtype).element_size()
-        ent = next((e for e in self.entries if e[0].numel() >= nbytes and (e[1] is None or e[1]() is None)), None)
+        free = [e for e in self.entries if e[1] is None or e[1]() is None]
+        ent = next((e for e in free if e[0].numel() >= nbytes), None)
         if ent is None:
+            # free buffers too small for this request are released (scene sizes change)
+            self.entries = [e for e in self.entries if e not in free]
             ent = [torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True), None]
             self.entries.append(ent)
         host = ent[0][:nbytes].view(dtype)
