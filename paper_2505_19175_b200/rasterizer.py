@@ -595,7 +595,8 @@ class _PinnedPool:
         ent = next((e for e in free if e[0].numel() >= nbytes), None)
         if ent is None:
             # free buffers too small for this request are released (scene sizes change)
-            self.entries = [e for e in self.entries if e not in free]
+            free_ids = {id(e) for e in free}
+            self.entries = [e for e in self.entries if id(e) not in free_ids]
             ent = [torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True), None]
             self.entries.append(ent)
         host = ent[0][:nbytes].view(dtype)
