@@ -50,8 +50,7 @@ def _ptr(t):
 # 944 MB fp64 soup every call)
 _STAGE_CHUNK = 16 << 20  # 6 buffers, DMA alternating over 2 streams (measured: 49 GB/s)
 _STAGE_NBUF = 6
-_STAGE: list = []
-_STAGE_STREAMS: list = []
+_STAGE: dict = {}  # device index -> ([(pinned buffer, event)], [copy streams])
 
 
 def _staged_h2d(a: np.ndarray, device="cuda") -> torch.Tensor:
@@ -61,25 +60,27 @@ def _staged_h2d(a: np.ndarray, device="cuda") -> torch.Tensor:
     if nbytes < (4 << 20):
         out.copy_(src)
         return out
-    if not _STAGE:
-        _STAGE.extend((torch.empty(_STAGE_CHUNK, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
-                      for _ in range(_STAGE_NBUF))
-        _STAGE_STREAMS.extend(torch.cuda.Stream(out.device) for _ in range(2))
+    dev = out.device.index if out.device.index is not None else torch.cuda.current_device()
+    if dev not in _STAGE:
+        with torch.cuda.device(dev):
+            _STAGE[dev] = ([(torch.empty(_STAGE_CHUNK, dtype=torch.uint8).pin_memory(), torch.cuda.Event())
+                            for _ in range(_STAGE_NBUF)], [torch.cuda.Stream(dev) for _ in range(2)])
+    ring, streams = _STAGE[dev]
     sb = src.reshape(-1).view(torch.uint8)
     ob = out.reshape(-1).view(torch.uint8)
     cur = torch.cuda.current_stream(out.device)
-    for st in _STAGE_STREAMS:
+    for st in streams:
         st.wait_stream(cur)  # (out is allocated on the current stream)
     for i, off in enumerate(range(0, nbytes, _STAGE_CHUNK)):
-        buf, ev = _STAGE[i % len(_STAGE)]
-        st = _STAGE_STREAMS[i % len(_STAGE_STREAMS)]
+        buf, ev = ring[i % len(ring)]
+        st = streams[i % len(streams)]
         c = min(_STAGE_CHUNK, nbytes - off)
         ev.synchronize()  # the slot's previous DMA is done
         buf[:c].copy_(sb[off:off + c])
         with torch.cuda.stream(st):
             ob[off:off + c].copy_(buf[:c], non_blocking=True)
             ev.record(st)
-    for st in _STAGE_STREAMS:
+    for st in streams:
         cur.wait_stream(st)
     return out
 
