@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--train-steps", type=int, default=2)
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo launcher + collective check, no kernels")
     ap.add_argument("--tile-backward", action="store_true", help="training: tile backward instead of the streaming one")
+    ap.add_argument("--chain-views", type=int, default=8,
+                    help="training: views chained to parameter gradients per pass (1 = per view)")
     return ap.parse_args()
 
 
@@ -523,7 +525,8 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
     if args.tile_backward:
         from paper_2505_19175_b200 import _lib
         rast.set_option(_lib.TS_OPT_TILE_BACKWARD, 1)
-    trainer = B200ViewTrainer(ds3, intr3, poses, d_images, rasterizer=rast, precision=args.precision)
+    trainer = B200ViewTrainer(ds3, intr3, poses, d_images, rasterizer=rast, precision=args.precision,
+                              chain_views=args.chain_views)
     trainer.step()  # warm-up (synchronous forwards size the buffers)
     torch.cuda.synchronize()
     if world > 1:
@@ -619,6 +622,15 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
         rast.backward(d_img, trainer.grads, accumulate=True)
         stt = rast.stage_times()
         bw.append(stt["blend_bwd"] + stt["chain_bwd"])
+    # the deferred chain of the step (chain_views views per pass): ms per view
+    kdef = trainer.chain_views
+    chain_def = None
+    if kdef > 1:
+        for v in range(kdef):
+            rast.forward(ds3, intr3, poses[v0], keep_backward=True, precision=args.precision)
+            rast.backward_screen(d_img)
+        rast.chain_views(trainer.grads, accumulate=True)
+        chain_def = round(rast.stage_times()["chain_bwd"] / kdef, 4)
     rast.profile(False)
     bwd_ms = sorted(bw)[len(bw) // 2]
     bbytes = backward_bytes(c3.n, fo.n_entries, c3.width * c3.height, fo.n_visible)
@@ -634,6 +646,8 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
              "allreduce": "NCCL SUM of the flat fp32 gradient inside the timed step" if world > 1 else "none (N=1)",
              "optimizer": "none in the timed step (the metric is fwd+bwd); fused Adam timed separately as adam_ms",
              "gpu_launches_per_step": launches / args.train_steps,
+             "chain_views": kdef,
+             "deferred_chain_ms_per_view": chain_def,
              "adam_ms": adam_ms,
              "default_iteration_ms": default_it,
              "densify_ms": densify_ms, "densify": dinfo,

@@ -164,6 +164,27 @@ int ts_backward(ts_context* ctx, const float* d_image, const ts_grads* grads, in
 int ts_backward_chunked(ts_context* ctx, const float* d_image, const ts_grads* grads, int accumulate, int n_chunks,
                         const int64_t* bounds, void* const* events, void* stream);
 
+/* Deferred chain for training steps over several views of one soup (SURVEY
+ * 8e: the batch gradient is the sum of the views' render_backward results).
+ * ts_backward_screen runs the blend backward of the last ts_forward (a
+ * training forward, fast path, fp32 parameters) into the next of up to
+ * TS_MAX_CHAIN_VIEWS (8) pending-view slots, keeping the view's camera and
+ * cull flags; ts_chain_views then chains every pending view to the 59
+ * parameter gradients in one pass (one read of the parameters and one
+ * read-add-write of grads for all of them, instead of one per view) and empties
+ * the slots.  Equivalent to ts_backward on each view in turn with accumulate=1
+ * after the first (the per-view fp64 vertex / opacity / sigma terms are summed
+ * before their single fp32 rounding).  The soup buffers must stay unmodified
+ * until ts_chain_views returns; n_chunks / bounds / events as in
+ * ts_backward_chunked (0 / NULL / NULL for one pass).  ts_pending_views returns
+ * the number of filled slots.  TS_ERR_INVALID_ARG: slots full, a different soup
+ * or mode than the pending views, exact precision or fp64 parameters;
+ * TS_ERR_NO_BWD_STATE from ts_chain_views: no pending view. */
+int ts_backward_screen(ts_context* ctx, const float* d_image, void* stream);
+int ts_chain_views(ts_context* ctx, const ts_grads* grads, int accumulate, int n_chunks, const int64_t* bounds,
+                   void* const* events, void* stream);
+int ts_pending_views(ts_context* ctx);
+
 /* Fragment lists of the last ts_forward: render(collect_fragments=True)
  * (render.py:383-399, 420-425; count_fragments _kernels.py:135-178,
  * collect branch _kernels.py:107-116).

@@ -72,7 +72,8 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_ssim", "ts_adam_step", "ts_distortion_loss", "ts_fragment_depth",
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
            "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack",
-           "ts_tile_lists", "ts_backward_chunked"]
+           "ts_tile_lists", "ts_backward_chunked", "ts_backward_screen", "ts_chain_views",
+           "ts_pending_views"]
 TS_OPT_LEGACY_BINNING = 1
 TS_OPT_TILE_BACKWARD = 2
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
@@ -155,6 +156,12 @@ def load(path: str = LIB_PATH):
     lib.ts_tile_lists.restype = ctypes.c_int
     lib.ts_backward_chunked.argtypes = [V, V, P(TsGrads), I, I, P(ctypes.c_int64), P(ctypes.c_void_p), V]
     lib.ts_backward_chunked.restype = ctypes.c_int
+    lib.ts_backward_screen.argtypes = [V, V, V]
+    lib.ts_backward_screen.restype = ctypes.c_int
+    lib.ts_chain_views.argtypes = [V, P(TsGrads), I, I, P(ctypes.c_int64), P(ctypes.c_void_p), V]
+    lib.ts_chain_views.restype = ctypes.c_int
+    lib.ts_pending_views.argtypes = [V]
+    lib.ts_pending_views.restype = ctypes.c_int
     for nm in ("ts_ply_pack", "ts_ply_unpack", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",
                "ts_gather_rows", "ts_child_vertices"):
         getattr(lib, nm).restype = ctypes.c_int

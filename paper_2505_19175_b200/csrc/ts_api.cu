@@ -53,6 +53,13 @@ struct ts_context {
     DevBuf tl_cnt, tl_off, tl_cs, tl_kv;  // ts_tile_lists scratch
     DevBuf adam_ibc;                      // Adam bias corrections of the current step
     DevBuf fsw;                           // per fragment: suffix of dw * w (fragment-gradient backward)
+    // deferred chain (ts_backward_screen / ts_chain_views): per pending view its
+    // screen-space gradients, cull flags and camera
+    DevBuf slot_sg[TS_MAX_CHAIN_VIEWS], slot_flag[TS_MAX_CHAIN_VIEWS];
+    Cam slot_cam[TS_MAX_CHAIN_VIEWS];
+    int n_slots = 0;
+    ts_soup slot_soup{};
+    Opts slot_opt{};
     DevBuf frec, ctot;            // training forward: fragment records + final unclipped colour
     unsigned long long frec_cap = 0;
     long long frec_hint = 0;      // largest fragment-record count seen (record-buffer sizing)
@@ -356,6 +363,10 @@ int ts_context_destroy(ts_context* c) {
     for (DevBuf* b : {&c->fsw, &c->adam_ibc, &c->tl_cnt, &c->tl_off, &c->tl_cs, &c->tl_kv, &c->rec64, &c->recf, &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec,
                       &c->ctot, &c->binmat, &c->lossbuf, &c->densbuf})
         cudaFree(b->p);
+    for (int k = 0; k < TS_MAX_CHAIN_VIEWS; k++) {
+        cudaFree(c->slot_sg[k].p);
+        cudaFree(c->slot_flag[k].p);
+    }
     cudaFree(c->sort_buf);
     cudaFree(c->os_buf);
     cudaFree(c->d_ctr);
@@ -800,6 +811,38 @@ int ts_backward_fragments(ts_context* c, const float* d_image, const int64_t* of
                          nullptr, nullptr, weight, f);
 }
 
+// Screen-space part of a fast-path backward (the blend backward into the
+// per-triangle fp64 rows sg, zeroed first): the streaming backward over the
+// training forward's fragment records, or the tile backward.
+static int screen_backward_fast(ts_context* c, const float* d_image, double* sg, const long long* frag_off,
+                                const double* fg_dw, const double* fg_dz, const double* frag_w,
+                                long long n_frag_total, cudaStream_t st) {
+    int rc;
+    stage_begin(c, TS_STAGE_BLEND_BWD, st);
+    if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
+    if (c->frec_ready && (!frag_off || frag_w)) {
+        // streaming backward over the forward's fragment records (with the
+        // fragment-gradient terms when the caller passes the fragments' weights);
+        // the tile backward runs instead only if the record buffer overflowed
+        if (frag_off && (rc = ensure(c->fsw, sizeof(double) * (size_t)(n_frag_total > 0 ? n_frag_total : 1))))
+            return rc;
+        launch_bwd_stream(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, (const RecC*)c->recc.p,
+                          (const FragRec*)c->frec.p, c->d_ctr, c->frec_cap, (const double*)c->ctot.p, d_image,
+                          sg, st, frag_off, frag_w, fg_dw, fg_dz, frag_off ? (double*)c->fsw.p : nullptr);
+        launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
+                               (const RecC*)c->recc.p, c->tile_start,
+                               c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
+                               &c->d_ctr->frec_over, sg, st);
+        g_launches += frag_off ? 1 : 0;
+    } else
+        launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
+                               (const RecC*)c->recc.p, c->tile_start,
+                               c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
+                               nullptr, sg, st);
+    stage_end(c, TS_STAGE_BLEND_BWD, st);
+    return TS_OK;
+}
+
 static int backward_impl(ts_context* c, const float* d_image, const ts_grads* grads, int accumulate,
                          const long long* frag_off, const double* fg_dw, const double* fg_dz, void* stream,
                          int n_chunks, const int64_t* bounds, void* const* events, const double* frag_w,
@@ -814,28 +857,7 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
     if (c->precision == 0) {
         if ((rc = ensure(c->sg64, sizeof(double) * SG_STRIDE * n1))) return rc;
         double* sg = (double*)c->sg64.p;
-        stage_begin(c, TS_STAGE_BLEND_BWD, st);
-        if (c->n > 0) TS_CHECK(cudaMemsetAsync(sg, 0, sizeof(double) * SG_STRIDE * c->n, st));
-        if (c->frec_ready && (!frag_off || frag_w)) {
-            // streaming backward over the forward's fragment records (with the
-            // fragment-gradient terms when the caller passes the fragments' weights);
-            // the tile backward runs instead only if the record buffer overflowed
-            if (frag_off && (rc = ensure(c->fsw, sizeof(double) * (size_t)(n_frag_total > 0 ? n_frag_total : 1))))
-                return rc;
-            launch_bwd_stream(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p, (const RecC*)c->recc.p,
-                              (const FragRec*)c->frec.p, c->d_ctr, c->frec_cap, (const double*)c->ctot.p, d_image,
-                              sg, st, frag_off, frag_w, fg_dw, fg_dz, frag_off ? (double*)c->fsw.p : nullptr);
-            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
-                                   (const RecC*)c->recc.p, c->tile_start,
-                                   c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
-                                   &c->d_ctr->frec_over, sg, st);
-            g_launches += frag_off ? 1 : 0;
-        } else
-            launch_blend_bwd_dense(c->cam, c->opt, (const RecF*)c->recf.p, (const RecB*)c->recb.p,
-                                   (const RecC*)c->recc.p, c->tile_start,
-                                   c->ent_src, c->t_final, c->last_pos, d_image, c->nfrag, frag_off, fg_dw, fg_dz,
-                                   nullptr, sg, st);
-        stage_end(c, TS_STAGE_BLEND_BWD, st);
+        if ((rc = screen_backward_fast(c, d_image, sg, frag_off, fg_dw, fg_dz, frag_w, n_frag_total, st))) return rc;
         stage_begin(c, TS_STAGE_CHAIN_BWD, st);
         if (n_chunks > 0 && chain_bwd_fast_ok(c->soup, c->dtype, *grads)) {
             // the chain in triangle ranges, an event after each: the caller's
@@ -870,6 +892,79 @@ static int backward_impl(ts_context* c, const float* d_image, const ts_grads* gr
     g_launches += 2;
     TS_CHECK(cudaGetLastError());
     return TS_OK;
+}
+
+int ts_backward_screen(ts_context* c, const float* d_image, void* stream) {
+    DeviceGuard device_guard(c);
+    if (!c || !d_image) return TS_ERR_INVALID_ARG;
+    if (!c->have_fwd) return TS_ERR_NO_FORWARD;
+    if (!c->have_bwd_state) return TS_ERR_NO_BWD_STATE;
+    // fast path, fp32 parameters with 16-byte aligned blocks (the chain's staged loads)
+    if (c->precision != 0 || c->dtype != 0 || (((uintptr_t)c->soup.sh | (uintptr_t)c->soup.vertices) & 15))
+        return TS_ERR_INVALID_ARG;
+    if (c->n_slots >= TS_MAX_CHAIN_VIEWS) return TS_ERR_INVALID_ARG;  // ts_chain_views first
+    if (c->n_slots > 0 && (c->soup.n != c->slot_soup.n || c->soup.vertices != c->slot_soup.vertices ||
+                           c->soup.sh != c->slot_soup.sh || c->opt.mode != c->slot_opt.mode ||
+                           c->opt.ncoef != c->slot_opt.ncoef))
+        return TS_ERR_INVALID_ARG;  // every pending view renders the same soup with the same options
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n1 = c->n > 0 ? c->n : 1;
+    const int k = c->n_slots;
+    int rc;
+    if ((rc = ensure(c->slot_sg[k], sizeof(double) * SG_STRIDE * n1))) return rc;
+    if ((rc = ensure(c->slot_flag[k], sizeof(unsigned) * n1))) return rc;
+    c->ev_used[TS_STAGE_BLEND_BWD] = c->ev_used[TS_STAGE_CHAIN_BWD] = false;
+    if ((rc = screen_backward_fast(c, d_image, (double*)c->slot_sg[k].p, nullptr, nullptr, nullptr, nullptr, 0, st)))
+        return rc;
+    if (c->n > 0)
+        TS_CHECK(cudaMemcpyAsync(c->slot_flag[k].p, c->flag, sizeof(unsigned) * c->n, cudaMemcpyDeviceToDevice, st));
+    c->slot_cam[k] = c->cam;
+    if (k == 0) {
+        c->slot_soup = c->soup;
+        c->slot_opt = c->opt;
+    }
+    c->n_slots = k + 1;
+    g_launches += 1;
+    return cuda_err(cudaGetLastError());
+}
+
+int ts_pending_views(ts_context* c) { return c ? c->n_slots : 0; }
+
+int ts_chain_views(ts_context* c, const ts_grads* grads, int accumulate, int n_chunks, const int64_t* bounds,
+                   void* const* events, void* stream) {
+    DeviceGuard device_guard(c);
+    if (!c || !grads) return TS_ERR_INVALID_ARG;
+    if (c->n_slots == 0) return TS_ERR_NO_BWD_STATE;
+    if (!chain_bwd_fast_ok(c->slot_soup, 0, *grads)) return TS_ERR_INVALID_ARG;
+    const long long n = c->slot_soup.n;
+    if (n_chunks > 0) {
+        if (!bounds || !events || bounds[0] != 0 || bounds[n_chunks] != n) return TS_ERR_INVALID_ARG;
+        for (int k = 0; k < n_chunks; k++)
+            if (bounds[k + 1] < bounds[k] || (bounds[k] & 63) || !events[k]) return TS_ERR_INVALID_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    ChainViews cv{};
+    cv.n = c->n_slots;
+    for (int k = 0; k < cv.n; k++) {
+        cv.cam[k] = c->slot_cam[k];
+        cv.flag[k] = (const unsigned*)c->slot_flag[k].p;
+        cv.sgrad[k] = (const double*)c->slot_sg[k].p;
+    }
+    c->ev_used[TS_STAGE_CHAIN_BWD] = false;
+    stage_begin(c, TS_STAGE_CHAIN_BWD, st);
+    if (n_chunks > 0) {
+        for (int k = 0; k < n_chunks; k++) {
+            launch_chain_multi(cv, c->slot_opt, c->slot_soup, *grads, accumulate, st, bounds[k], bounds[k + 1]);
+            TS_CHECK(cudaEventRecord((cudaEvent_t)events[k], st));
+        }
+        g_launches += n_chunks;
+    } else {
+        launch_chain_multi(cv, c->slot_opt, c->slot_soup, *grads, accumulate, st);
+        g_launches += 1;
+    }
+    stage_end(c, TS_STAGE_CHAIN_BWD, st);
+    c->n_slots = 0;
+    return cuda_err(cudaGetLastError());
 }
 
 int ts_photometric_loss(ts_context* c, const float* rendered, const float* target, int height, int width,

@@ -75,6 +75,121 @@ __device__ __forceinline__ void sh_weighted_grad(double x, double y, double z, c
 }
 }  // namespace
 
+// One view's chain for one triangle the view's forward kept (flag set): its
+// screen-space gradient row sg -> dv += d_vertices, dop += d_opacity, dsig +=
+// d_sigma, and d_sh = basis * dL/draw, written over the SH row (IN_PLACE: one
+// view) or added to dsh (several views against the same SH row).
+template <bool IN_PLACE>
+__device__ __forceinline__ void chain_tri(const Cam& cam, const Opts& opt, const double* v, float4* shrow,
+                                          float4* dsh, const double* sg, double* dv, double& dop, double& dsig) {
+    double gq[6];
+#pragma unroll
+    for (int k = 0; k < 6; k++) gq[k] = sg[SG_GQ + k];
+    dop += sg[SG_GO];
+    dsig += sg[SG_GSIG];
+    const double grgb[3] = {sg[SG_GRGB], sg[SG_GRGB + 1], sg[SG_GRGB + 2]};
+    const double gphis = sg[SG_GPHIS], gzz = sg[SG_GZ];
+    Proj64 p;
+    project64(v, cam, p);
+    const double* q = p.q;
+    if (opt.mode == 0) {
+        // _phis_q_grad, backward.py:59-90: phi_s = -2 area / perimeter
+        const double e1x = q[2] - q[0], e1y = q[3] - q[1];
+        const double e2x = q[4] - q[0], e2y = q[5] - q[1];
+        const double cross = e1x * e2y - e1y * e2x;
+        const double sgn = (cross > 0) - (cross < 0);
+        double dperim[6] = {0, 0, 0, 0, 0, 0};
+        double perim = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const int b = a == 2 ? 0 : a + 1;
+            const double dx = q[a * 2] - q[b * 2], dy = q[a * 2 + 1] - q[b * 2 + 1];
+            const double nd = sqrt(dx * dx + dy * dy);
+            perim += nd;
+            const double ux = dx / nd, uy = dy / nd;
+            dperim[a * 2] += ux;
+            dperim[a * 2 + 1] += uy;
+            dperim[b * 2] -= ux;
+            dperim[b * 2 + 1] -= uy;
+        }
+        const double area = fabs(cross) * 0.5;
+        const double dcross[6] = {q[3] - q[5], q[4] - q[2], q[5] - q[1], q[0] - q[4], q[1] - q[3], q[2] - q[0]};
+        const double coef_a = -2.0 / perim;
+        const double coef_p = 2.0 * area / (perim * perim);
+#pragma unroll
+        for (int k = 0; k < 6; k++) gq[k] += gphis * (coef_a * (0.5 * sgn * dcross[k]) + coef_p * dperim[k]);
+    }
+    // projection Jacobian, backward.py:181-190
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const double zc = p.xc[k * 3 + 2];
+        const double iz = 1.0 / zc;
+        const double dx = cam.fx * gq[k * 2] * iz;
+        const double dy = cam.fy * gq[k * 2 + 1] * iz;
+        const double dz = (-cam.fx * p.xc[k * 3] * gq[k * 2] - cam.fy * p.xc[k * 3 + 1] * gq[k * 2 + 1]) * (iz * iz) +
+                          gzz / 3.0;
+#pragma unroll
+        for (int b = 0; b < 3; b++) dv[k * 3 + b] += dx * cam.R[b] + dy * cam.R[3 + b] + dz * cam.R[6 + b];
+    }
+    // colour path, backward.py:192-205 (sh.py:30-52 basis, 55-100 gradient)
+    double u[3];
+#pragma unroll
+    for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) / 3.0 - cam.cc[b];
+    double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    un = un > 1e-12 ? un : 1e-12;
+    const double vx = u[0] / un, vy = u[1] / un, vz = u[2] / un;
+    double basis[16];
+    sh_basis16(vx, vy, vz, basis);
+    const int ncoef = opt.ncoef;
+    double raw[3] = {0.5, 0.5, 0.5};
+#pragma unroll
+    for (int qd = 0; qd < 12; qd++) {
+        const float4 c4 = shrow[qd];
+        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int uu = 0; uu < 4; uu++) {
+            const int idx = qd * 4 + uu;
+            if (idx / 3 < ncoef) raw[idx % 3] += basis[idx / 3] * (double)cv[uu];
+        }
+    }
+    double d_raw[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) d_raw[ch] = (raw[ch] > 0.0 && raw[ch] < 1.0) ? grgb[ch] : 0.0;
+    // s_c = sum_ch d_raw[ch] * coef[c][ch]; d_sh[c][ch] = basis[c] * d_raw[ch] (IN_PLACE)
+    double s[16];
+#pragma unroll
+    for (int c = 0; c < 16; c++) s[c] = 0.0;
+#pragma unroll
+    for (int qd = 0; qd < 12; qd++) {
+        const float4 c4 = shrow[qd];
+        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+        float o4[4];
+#pragma unroll
+        for (int uu = 0; uu < 4; uu++) {
+            const int idx = qd * 4 + uu, c = idx / 3, ch = idx % 3;
+            const bool on = c < ncoef;
+            if (on) s[c] += d_raw[ch] * (double)cv[uu];
+            o4[uu] = on ? (float)(basis[c] * d_raw[ch]) : 0.f;
+        }
+        if constexpr (IN_PLACE) {
+            shrow[qd] = make_float4(o4[0], o4[1], o4[2], o4[3]);
+        } else {
+            float4 a4 = dsh[qd];
+            a4.x += o4[0]; a4.y += o4[1]; a4.z += o4[2]; a4.w += o4[3];
+            dsh[qd] = a4;
+        }
+    }
+    double ddir[3];
+    sh_weighted_grad(vx, vy, vz, s, ddir);
+    const double dot = vx * ddir[0] + vy * ddir[1] + vz * ddir[2];
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+        const double du = (ddir[b] - (b == 0 ? vx : b == 1 ? vy : vz) * dot) / un / 3.0;
+#pragma unroll
+        for (int k = 0; k < 3; k++) dv[k * 3 + b] += du;
+    }
+}
+
 __global__ void __launch_bounds__(CB, 8) k_chain_bwd32(Cam cam, Opts opt, const float* __restrict__ verts,
                                                        const float* __restrict__ sh,
                                                        const unsigned* __restrict__ flag,
@@ -135,109 +250,10 @@ __global__ void __launch_bounds__(CB, 8) k_chain_bwd32(Cam cam, Opts opt, const 
             for (int q = 0; q < 12; q++) shrow[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
             const double* sg = &S.sg[tid * SGW];
-            double gq[6];
-#pragma unroll
-            for (int k = 0; k < 6; k++) gq[k] = sg[SG_GQ + k];
-            dop = sg[SG_GO];
-            dsig = sg[SG_GSIG];
-            const double grgb[3] = {sg[SG_GRGB], sg[SG_GRGB + 1], sg[SG_GRGB + 2]};
-            const double gphis = sg[SG_GPHIS], gzz = sg[SG_GZ];
             double v[9];
 #pragma unroll
             for (int k = 0; k < 9; k++) v[k] = (double)vrow[k];
-            Proj64 p;
-            project64(v, cam, p);
-            const double* q = p.q;
-            if (opt.mode == 0) {
-                // _phis_q_grad, backward.py:59-90: phi_s = -2 area / perimeter
-                const double e1x = q[2] - q[0], e1y = q[3] - q[1];
-                const double e2x = q[4] - q[0], e2y = q[5] - q[1];
-                const double cross = e1x * e2y - e1y * e2x;
-                const double sgn = (cross > 0) - (cross < 0);
-                double dperim[6] = {0, 0, 0, 0, 0, 0};
-                double perim = 0.0;
-#pragma unroll
-                for (int a = 0; a < 3; a++) {
-                    const int b = a == 2 ? 0 : a + 1;
-                    const double dx = q[a * 2] - q[b * 2], dy = q[a * 2 + 1] - q[b * 2 + 1];
-                    const double nd = sqrt(dx * dx + dy * dy);
-                    perim += nd;
-                    const double ux = dx / nd, uy = dy / nd;
-                    dperim[a * 2] += ux;
-                    dperim[a * 2 + 1] += uy;
-                    dperim[b * 2] -= ux;
-                    dperim[b * 2 + 1] -= uy;
-                }
-                const double area = fabs(cross) * 0.5;
-                const double dcross[6] = {q[3] - q[5], q[4] - q[2], q[5] - q[1], q[0] - q[4], q[1] - q[3], q[2] - q[0]};
-                const double coef_a = -2.0 / perim;
-                const double coef_p = 2.0 * area / (perim * perim);
-#pragma unroll
-                for (int k = 0; k < 6; k++) gq[k] += gphis * (coef_a * (0.5 * sgn * dcross[k]) + coef_p * dperim[k]);
-            }
-            // projection Jacobian, backward.py:181-190
-#pragma unroll
-            for (int k = 0; k < 3; k++) {
-                const double zc = p.xc[k * 3 + 2];
-                const double iz = 1.0 / zc;
-                const double dx = cam.fx * gq[k * 2] * iz;
-                const double dy = cam.fy * gq[k * 2 + 1] * iz;
-                const double dz = (-cam.fx * p.xc[k * 3] * gq[k * 2] - cam.fy * p.xc[k * 3 + 1] * gq[k * 2 + 1]) * (iz * iz) +
-                                  gzz / 3.0;
-#pragma unroll
-                for (int b = 0; b < 3; b++) dv[k * 3 + b] = dx * cam.R[b] + dy * cam.R[3 + b] + dz * cam.R[6 + b];
-            }
-            // colour path, backward.py:192-205 (sh.py:30-52 basis, 55-100 gradient)
-            double u[3];
-#pragma unroll
-            for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) / 3.0 - cam.cc[b];
-            double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-            un = un > 1e-12 ? un : 1e-12;
-            const double vx = u[0] / un, vy = u[1] / un, vz = u[2] / un;
-            double basis[16];
-            sh_basis16(vx, vy, vz, basis);
-            const int ncoef = opt.ncoef;
-            double raw[3] = {0.5, 0.5, 0.5};
-#pragma unroll
-            for (int qd = 0; qd < 12; qd++) {
-                const float4 c4 = shrow[qd];
-                const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-                for (int uu = 0; uu < 4; uu++) {
-                    const int idx = qd * 4 + uu;
-                    if (idx / 3 < ncoef) raw[idx % 3] += basis[idx / 3] * (double)cv[uu];
-                }
-            }
-            double d_raw[3];
-#pragma unroll
-            for (int ch = 0; ch < 3; ch++) d_raw[ch] = (raw[ch] > 0.0 && raw[ch] < 1.0) ? grgb[ch] : 0.0;
-            // s_c = sum_ch d_raw[ch] * coef[c][ch]; d_sh[c][ch] = basis[c] * d_raw[ch] (in place)
-            double s[16];
-#pragma unroll
-            for (int c = 0; c < 16; c++) s[c] = 0.0;
-#pragma unroll
-            for (int qd = 0; qd < 12; qd++) {
-                const float4 c4 = shrow[qd];
-                const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-                float o4[4];
-#pragma unroll
-                for (int uu = 0; uu < 4; uu++) {
-                    const int idx = qd * 4 + uu, c = idx / 3, ch = idx % 3;
-                    const bool on = c < ncoef;
-                    if (on) s[c] += d_raw[ch] * (double)cv[uu];
-                    o4[uu] = on ? (float)(basis[c] * d_raw[ch]) : 0.f;
-                }
-                shrow[qd] = make_float4(o4[0], o4[1], o4[2], o4[3]);
-            }
-            double ddir[3];
-            sh_weighted_grad(vx, vy, vz, s, ddir);
-            const double dot = vx * ddir[0] + vy * ddir[1] + vz * ddir[2];
-#pragma unroll
-            for (int b = 0; b < 3; b++) {
-                const double du = (ddir[b] - (b == 0 ? vx : b == 1 ? vy : vz) * dot) / un / 3.0;
-#pragma unroll
-                for (int k = 0; k < 3; k++) dv[k * 3 + b] += du;
-            }
+            chain_tri<true>(cam, opt, v, shrow, nullptr, sg, dv, dop, dsig);
         }
 #pragma unroll
         for (int k = 0; k < 9; k++) vrow[k] = (float)dv[k];
@@ -263,6 +279,110 @@ __global__ void __launch_bounds__(CB, 8) k_chain_bwd32(Cam cam, Opts opt, const 
         if (tid < nt) {
             grads.d_opacity[i0 + tid] = accumulate ? S.aos[0][tid] + S.os[0][tid] : S.os[0][tid];
             grads.d_sigma[i0 + tid] = accumulate ? S.aos[1][tid] + S.os[1][tid] : S.os[1][tid];
+        }
+    }
+}
+
+// Deferred chain of several views of one scene (training steps over many
+// views): each view's blend backward left its screen-space gradients in its
+// own slot, and this kernel chains all of them per triangle against ONE read
+// of the parameters and ONE read-add-write of the accumulated gradients
+// (instead of one of each per view: 1.6 GB -> ~0.4 + 0.26 GB per view at
+// 2M triangles).  Same stage / write-out scheme as k_chain_bwd32, with a
+// padded d_sh accumulator instead of the in-place SH row.
+struct ChainMultiStage {
+    float4 sh[CB * 13];
+    float4 dsh[CB * 13];    // d_sh accumulator (the output's values when accumulating)
+    float v[CB * 9];
+    float av[CB * 9];
+    float aos[2][CB];
+};
+
+#ifndef TS_CHAIN_MULTI_MINB
+#define TS_CHAIN_MULTI_MINB 6  // (8: 0.272 ms per view at 8 views, spilling; 6: 0.258; 4: 0.315)
+#endif
+__global__ void __launch_bounds__(CB, TS_CHAIN_MULTI_MINB) k_chain_multi32(ChainViews cv, Opts opt, const float* __restrict__ verts,
+                                                         const float* __restrict__ sh, long long lo, long long n,
+                                                         ts_grads grads, int accumulate) {
+    TS_PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char s_chain[];
+    ChainMultiStage& S = *reinterpret_cast<ChainMultiStage*>(s_chain);
+    const int tid = threadIdx.x;
+    const long long i0 = (long long)blockIdx.x * CB;  // (relative to lo: every pointer below is offset)
+    const int nt = (int)min((long long)CB, n - i0);
+    {
+        const float4* g = reinterpret_cast<const float4*>(sh + i0 * 48);
+        for (int c = tid; c < nt * 12; c += CB) {
+            const int tri = c / 12;
+            cp_async16(&S.sh[tri * 13 + (c - tri * 12)], g + c);
+        }
+        const float* gv = verts + i0 * 9;
+        if (nt == CB) {
+            for (int c = tid; c < CB * 9 / 4; c += CB)
+                cp_async16(reinterpret_cast<float4*>(S.v) + c, reinterpret_cast<const float4*>(gv) + c);
+        } else {
+            for (int c = tid; c < nt * 9; c += CB) cp_async4(S.v + c, gv + c);
+        }
+        if (accumulate) {
+            const float4* ga = reinterpret_cast<const float4*>(grads.d_sh + i0 * 48);
+            for (int c = tid; c < nt * 12; c += CB) {
+                const int tri = c / 12;
+                cp_async16(&S.dsh[tri * 13 + (c - tri * 12)], ga + c);
+            }
+            const float* gva = grads.d_vertices + i0 * 9;
+            for (int c = tid; c < nt * 9; c += CB) cp_async4(&S.av[c], gva + c);
+            if (tid < nt) {
+                cp_async4(&S.aos[0][tid], grads.d_opacity + i0 + tid);
+                cp_async4(&S.aos[1][tid], grads.d_sigma + i0 + tid);
+            }
+        } else {
+            for (int c = tid; c < nt * 13; c += CB) S.dsh[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int c = tid; c < nt * 9; c += CB) S.av[c] = 0.f;
+            if (tid < nt) S.aos[0][tid] = S.aos[1][tid] = 0.f;
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    const long long i = lo + i0 + tid;  // absolute triangle index (flags, screen-space rows)
+    if (tid < nt) {
+        float* vrow = &S.v[tid * 9];
+        double v[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) v[k] = (double)vrow[k];
+        double dv[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) dv[k] = 0.0;
+        double dop = 0.0, dsig = 0.0;
+        for (int w = 0; w < cv.n; w++) {
+            if (!__ldg(cv.flag[w] + i)) continue;
+            const double2* row = reinterpret_cast<const double2*>(cv.sgrad[w] + (size_t)i * SG_STRIDE);
+            double sg[14];
+#pragma unroll
+            for (int k = 0; k < 7; k++) {
+                const double2 t = __ldg(row + k);
+                sg[2 * k] = t.x;
+                sg[2 * k + 1] = t.y;
+            }
+            chain_tri<false>(cv.cam[w], opt, v, &S.sh[tid * 13], &S.dsh[tid * 13], sg, dv, dop, dsig);
+        }
+#pragma unroll
+        for (int k = 0; k < 9; k++) vrow[k] = (float)dv[k];
+        S.aos[0][tid] += (float)dop;
+        S.aos[1][tid] += (float)dsig;
+    }
+    __syncthreads();
+    {
+        float4* g = reinterpret_cast<float4*>(grads.d_sh + i0 * 48);
+        for (int c = tid; c < nt * 12; c += CB) {
+            const int tri = c / 12;
+            g[c] = S.dsh[tri * 13 + (c - tri * 12)];
+        }
+        float* gv = grads.d_vertices + i0 * 9;
+        for (int c = tid; c < nt * 9; c += CB) gv[c] = S.av[c] + S.v[c];
+        if (tid < nt) {
+            grads.d_opacity[i0 + tid] = S.aos[0][tid];
+            grads.d_sigma[i0 + tid] = S.aos[1][tid];
         }
     }
 }
@@ -293,6 +413,24 @@ bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup,
     launch_pdl(k_chain_bwd32, dim3(grid), dim3(CB), smem, st, cam, opt, verts, sh, flag + lo,
                sgrad + (size_t)SG_STRIDE * lo, n, gr, accumulate);
     return true;
+}
+
+void launch_chain_multi(const ChainViews& cv, const Opts& opt, const ts_soup& soup, const ts_grads& g,
+                        int accumulate, cudaStream_t st, long long lo, long long hi) {
+    if (hi < 0) hi = soup.n;
+    const long long n = hi - lo;
+    if (n <= 0) return;
+    const float* verts = (const float*)soup.vertices + 9 * lo;
+    const float* sh = (const float*)soup.sh + 48 * lo;
+    ts_grads gr = g;
+    gr.d_vertices += 9 * lo;
+    gr.d_opacity += lo;
+    gr.d_sigma += lo;
+    gr.d_sh += 48 * lo;
+    const int smem = (int)sizeof(ChainMultiStage);
+    smem_optin((const void*)k_chain_multi32, smem);
+    launch_pdl(k_chain_multi32, dim3((unsigned)((n + CB - 1) / CB)), dim3(CB), smem, st, cv, opt, verts, sh, lo, n,
+               gr, accumulate);
 }
 
 }  // namespace ts

@@ -142,6 +142,16 @@ void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const R
                        double* sw = nullptr);
 
 // ts_chain.cu: fp32-parameter chain to the 59 parameter gradients (false: not applicable)
+// deferred multi-view chain (ts_backward_screen / ts_chain_views)
+constexpr int TS_MAX_CHAIN_VIEWS = 8;
+struct ChainViews {
+    Cam cam[TS_MAX_CHAIN_VIEWS];
+    const unsigned* flag[TS_MAX_CHAIN_VIEWS];
+    const double* sgrad[TS_MAX_CHAIN_VIEWS];
+    int n;
+};
+void launch_chain_multi(const ChainViews& cv, const Opts& opt, const ts_soup& soup, const ts_grads& g,
+                        int accumulate, cudaStream_t st, long long lo = 0, long long hi = -1);
 bool chain_bwd_fast_ok(const ts_soup& soup, int dtype, const ts_grads& g);
 // triangles [lo, hi) (hi < 0: all); lo a multiple of 64
 bool launch_chain_bwd_fast(const Cam& cam, const Opts& opt, const ts_soup& soup, int dtype, const unsigned* flag,

@@ -143,9 +143,16 @@ def train_step(grad_fn: Callable[[int, torch.Tensor, bool], None], n_views: int,
 
 class B200ViewTrainer:
     """Forward + backward of each local view on the B200 rasterizer, then one
-    NCCL all-reduce.  ``poses`` / ``d_images`` index the batch."""
+    NCCL all-reduce.  ``poses`` / ``d_images`` index the batch.
 
-    def __init__(self, soup, intr, poses, d_images, rasterizer=None, lrs=None, **render_kw):
+    ``chain_views`` > 1 defers the chain to the parameter gradients: each
+    view's blend backward fills a pending-view slot (ts_backward_screen) and
+    every ``chain_views`` views -- and at the rank's last view -- one pass chains
+    them all (ts_chain_views: one read of the parameters and one
+    read-add-write of the gradient for the group instead of one per view)."""
+
+    def __init__(self, soup, intr, poses, d_images, rasterizer=None, lrs=None, chain_views: int = 8,
+                 **render_kw):
         from .rasterizer import DeviceGrads, Rasterizer
         self.rast = rasterizer or Rasterizer()
         self.soup = soup
@@ -156,6 +163,12 @@ class B200ViewTrainer:
         self.grads = DeviceGrads.zeros(len(soup))
         self.comm = None          # side stream of the bucketed all-reduce (world > 1)
         self.n_buckets = 8
+        self.chain_views = max(1, min(int(chain_views), Rasterizer.MAX_PENDING_VIEWS))
+        # deferral needs the fast path with fp32 parameters
+        if render_kw.get("precision", "fast") != "fast" or soup.vertices.dtype != torch.float32:
+            self.chain_views = 1
+        self._acc = False         # the gradient buffer already holds views of this step
+        self._last_view = None
         # optional fused Adam after the all-reduce (training.py:165-168): every
         # rank applies the same update to its replica of the parameters
         self.lrs = lrs
@@ -164,22 +177,43 @@ class B200ViewTrainer:
             from .optim import DeviceAdamState
             self.adam = DeviceAdamState.zeros(len(soup))
 
+    def _flush(self, chunks=None):
+        self.rast.chain_views(self.grads, accumulate=self._acc, chunks=chunks)
+        self._acc = True
+
     def _grad(self, v: int, flat: torch.Tensor, accumulate: bool):
         self.rast.forward(self.soup, self.intr, self.poses[v], keep_backward=True, **self.kw)
-        self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate)
+        if self.chain_views == 1:
+            self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate)
+            return
+        pending = self.rast.backward_screen(self.d_images[v])
+        if pending >= self.chain_views or v == self._last_view:
+            self._flush()
 
     def _grad_chunked(self, v: int, flat: torch.Tensor, accumulate: bool, bounds):
         """The rank's last view: the chain in triangle ranges, one event each."""
         self.rast.forward(self.soup, self.intr, self.poses[v], keep_backward=True, **self.kw)
         events = [torch.cuda.Event() for _ in range(len(bounds) - 1)]
-        self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate, chunks=(bounds, events))
+        if self.chain_views == 1:
+            self.rast.backward(self.d_images[v], self.grads, accumulate=accumulate, chunks=(bounds, events))
+        else:
+            self.rast.backward_screen(self.d_images[v])
+            self._flush(chunks=(bounds, events))
         return events
 
     def step(self) -> StepResult:
-        if self.comm is None and dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+        rank = dist.get_rank() if world > 1 else 0
+        if self.comm is None and world > 1:
             self.comm = torch.cuda.Stream()
-        res = train_step(self._grad, len(self.poses), self.grads.flat, last_grad_fn=self._grad_chunked,
-                         n_triangles=len(self.soup), n_buckets=self.n_buckets, comm_stream=self.comm)
+        mine = shard(len(self.poses), world, rank)
+        self._last_view = mine[-1] if len(mine) else None
+        self._acc = False
+        if self.chain_views > 1 and self.rast.pending_views():
+            raise RuntimeError("pending views from an interrupted step: call rast.chain_views() first")
+        res = train_step(self._grad, len(self.poses), self.grads.flat, world=world, rank=rank,
+                         last_grad_fn=self._grad_chunked, n_triangles=len(self.soup), n_buckets=self.n_buckets,
+                         comm_stream=self.comm)
         if self.adam is not None:
             from .optim import adam_step
             adam_step(self.soup, self.grads, self.adam, self.lrs, rasterizer=self.rast)

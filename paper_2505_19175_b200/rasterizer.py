@@ -398,6 +398,50 @@ class Rasterizer:
                                                 k, b, evp, ctypes.c_void_p(st)), "backward_chunked")
         return grads
 
+    MAX_PENDING_VIEWS = 8
+
+    def backward_screen(self, d_image: torch.Tensor, stream=None) -> int:
+        """Blend backward of the last (training) forward into the next pending-view
+        slot (ts_backward_screen); ``chain_views`` later turns every pending view
+        into parameter gradients in one pass.  Returns the number of pending views."""
+        if self._last is None:
+            raise RuntimeError("backward_screen() needs a preceding forward()")
+        _, h, w = self._last
+        if tuple(d_image.shape) != (h, w, 3):
+            raise ValueError(f"d_image must be {(h, w, 3)}, got {tuple(d_image.shape)}")
+        d_image = d_image.to(dtype=torch.float32).contiguous()
+        st = (stream or torch.cuda.current_stream(d_image.device)).cuda_stream
+        _lib.check(self.lib.ts_backward_screen(self._ctx, _ptr(d_image), ctypes.c_void_p(st)), "backward_screen")
+        return int(self.lib.ts_pending_views(self._ctx))
+
+    def chain_views(self, grads: DeviceGrads, accumulate: bool = False, stream=None, chunks=None) -> DeviceGrads:
+        """Parameter gradients of every pending view (ts_chain_views): ``grads``
+        gets their sum (+= when accumulating), as ``backward`` on each view in
+        turn would; ``chunks = (bounds, events)`` as in ``backward``."""
+        _check_grads(grads, self._last[0] if self._last is not None else grads.n)
+        dev = torch.device("cuda", self.device)
+        stream = stream or torch.cuda.current_stream(dev)
+        st = stream.cuda_stream
+        g = grads._ts()
+        if chunks is None:
+            _lib.check(self.lib.ts_chain_views(self._ctx, ctypes.byref(g), int(bool(accumulate)), 0, None, None,
+                                               ctypes.c_void_p(st)), "chain_views")
+            return grads
+        bounds, events = chunks
+        k = len(bounds) - 1
+        if len(events) != k:
+            raise ValueError("one event per chunk")
+        for ev in events:
+            ev.record(stream)
+        b = (ctypes.c_int64 * (k + 1))(*[int(x) for x in bounds])
+        evp = (ctypes.c_void_p * k)(*[ctypes.c_void_p(ev.cuda_event) for ev in events])
+        _lib.check(self.lib.ts_chain_views(self._ctx, ctypes.byref(g), int(bool(accumulate)), k, b, evp,
+                                           ctypes.c_void_p(st)), "chain_views")
+        return grads
+
+    def pending_views(self) -> int:
+        return int(self.lib.ts_pending_views(self._ctx))
+
     def fragments(self, stream=None) -> "DeviceFragments":
         """Fragment lists of the last forward (render(collect_fragments=True),
         render.py:383-399, 420-425): CSR offsets (int64, H*W+1), source ids,

@@ -260,8 +260,11 @@ def test_north_star_forward_parity(rast, precision):
     check_forward(rast, f, ref, intr, f"ns-{precision}")
 
 
-def test_view_parallel_step_matches_sum_of_oracle_views(rast):
-    """B200ViewTrainer (world 1): batch gradient == sum of per-view oracle gradients."""
+@pytest.mark.parametrize("chain_views", [1, 3, 4])
+def test_view_parallel_step_matches_sum_of_oracle_views(rast, chain_views):
+    """B200ViewTrainer (world 1): batch gradient == sum of per-view oracle
+    gradients, with the chain per view or deferred over groups of views (3: a
+    full group then the rank's last view flushes the rest)."""
     from oracle import oracle as O
     from paper_2505_19175_b200 import scenes
     from paper_2505_19175_b200.parallel import B200ViewTrainer
@@ -270,8 +273,10 @@ def test_view_parallel_step_matches_sum_of_oracle_views(rast):
     poses = scenes.orbit_cameras(4, seed=4)
     d_np = [np.random.default_rng(100 + v).normal(size=(80, 96, 3)) for v in range(4)]
     d_dev = [torch.as_tensor(d, dtype=torch.float32, device="cuda") for d in d_np]
-    tr = B200ViewTrainer(_dev(soup), intr, poses, d_dev, rasterizer=rast)
+    tr = B200ViewTrainer(_dev(soup), intr, poses, d_dev, rasterizer=rast, chain_views=chain_views)
+    tr.step()  # twice: the second step must start from a fresh buffer
     g = tr.step().grads.double().cpu().numpy()
+    assert rast.pending_views() == 0
     want = 0
     for v in range(4):
         gr = O.render_backward(soup, intr, poses[v], d_image=d_np[v])
