@@ -89,9 +89,19 @@ __device__ __forceinline__ void chain_tri(const Cam& cam, const Opts& opt, const
     dsig += sg[SG_GSIG];
     const double grgb[3] = {sg[SG_GRGB], sg[SG_GRGB + 1], sg[SG_GRGB + 2]};
     const double gphis = sg[SG_GPHIS], gzz = sg[SG_GZ];
-    Proj64 p;
-    project64(v, cam, p);
-    const double* q = p.q;
+    // camera-space vertices and their projections; the gradient only needs them
+    // accurate (not bit-exact): one reciprocal per vertex instead of two quotients
+    double xc[9], iz[3], q[6];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+            xc[k * 3 + a] = fma(v[k * 3 + 0], cam.R[a * 3 + 0],
+                                fma(v[k * 3 + 1], cam.R[a * 3 + 1], fma(v[k * 3 + 2], cam.R[a * 3 + 2], cam.t[a])));
+        iz[k] = 1.0 / xc[k * 3 + 2];
+        q[k * 2 + 0] = fma(cam.fx * xc[k * 3 + 0], iz[k], cam.cx);
+        q[k * 2 + 1] = fma(cam.fy * xc[k * 3 + 1], iz[k], cam.cy);
+    }
     if (opt.mode == 0) {
         // _phis_q_grad, backward.py:59-90: phi_s = -2 area / perimeter
         const double e1x = q[2] - q[0], e1y = q[3] - q[1];
@@ -104,9 +114,10 @@ __device__ __forceinline__ void chain_tri(const Cam& cam, const Opts& opt, const
         for (int a = 0; a < 3; a++) {
             const int b = a == 2 ? 0 : a + 1;
             const double dx = q[a * 2] - q[b * 2], dy = q[a * 2 + 1] - q[b * 2 + 1];
-            const double nd = sqrt(dx * dx + dy * dy);
-            perim += nd;
-            const double ux = dx / nd, uy = dy / nd;
+            const double nn = dx * dx + dy * dy;
+            const double ind = rsqrt(nn);
+            perim += nn * ind;
+            const double ux = dx * ind, uy = dy * ind;
             dperim[a * 2] += ux;
             dperim[a * 2 + 1] += uy;
             dperim[b * 2] -= ux;
@@ -114,30 +125,31 @@ __device__ __forceinline__ void chain_tri(const Cam& cam, const Opts& opt, const
         }
         const double area = fabs(cross) * 0.5;
         const double dcross[6] = {q[3] - q[5], q[4] - q[2], q[5] - q[1], q[0] - q[4], q[1] - q[3], q[2] - q[0]};
-        const double coef_a = -2.0 / perim;
-        const double coef_p = 2.0 * area / (perim * perim);
+        const double ip = 1.0 / perim;
+        const double coef_a = -2.0 * ip;
+        const double coef_p = 2.0 * area * ip * ip;
 #pragma unroll
         for (int k = 0; k < 6; k++) gq[k] += gphis * (coef_a * (0.5 * sgn * dcross[k]) + coef_p * dperim[k]);
     }
     // projection Jacobian, backward.py:181-190
 #pragma unroll
     for (int k = 0; k < 3; k++) {
-        const double zc = p.xc[k * 3 + 2];
-        const double iz = 1.0 / zc;
-        const double dx = cam.fx * gq[k * 2] * iz;
-        const double dy = cam.fy * gq[k * 2 + 1] * iz;
-        const double dz = (-cam.fx * p.xc[k * 3] * gq[k * 2] - cam.fy * p.xc[k * 3 + 1] * gq[k * 2 + 1]) * (iz * iz) +
-                          gzz / 3.0;
+        const double izk = iz[k];
+        const double dx = cam.fx * gq[k * 2] * izk;
+        const double dy = cam.fy * gq[k * 2 + 1] * izk;
+        const double dz = (-cam.fx * xc[k * 3] * gq[k * 2] - cam.fy * xc[k * 3 + 1] * gq[k * 2 + 1]) * (izk * izk) +
+                          gzz * (1.0 / 3.0);
 #pragma unroll
         for (int b = 0; b < 3; b++) dv[k * 3 + b] += dx * cam.R[b] + dy * cam.R[3 + b] + dz * cam.R[6 + b];
     }
     // colour path, backward.py:192-205 (sh.py:30-52 basis, 55-100 gradient)
     double u[3];
 #pragma unroll
-    for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) / 3.0 - cam.cc[b];
-    double un = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-    un = un > 1e-12 ? un : 1e-12;
-    const double vx = u[0] / un, vy = u[1] / un, vz = u[2] / un;
+    for (int b = 0; b < 3; b++) u[b] = (v[b] + v[3 + b] + v[6 + b]) * (1.0 / 3.0) - cam.cc[b];
+    // 1 / max(|u|, 1e-12)
+    const double uu2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    const double iun = uu2 > 1e-24 ? rsqrt(uu2) : 1e12;
+    const double vx = u[0] * iun, vy = u[1] * iun, vz = u[2] * iun;
     double basis[16];
     sh_basis16(vx, vy, vz, basis);
     const int ncoef = opt.ncoef;
@@ -184,7 +196,7 @@ __device__ __forceinline__ void chain_tri(const Cam& cam, const Opts& opt, const
     const double dot = vx * ddir[0] + vy * ddir[1] + vz * ddir[2];
 #pragma unroll
     for (int b = 0; b < 3; b++) {
-        const double du = (ddir[b] - (b == 0 ? vx : b == 1 ? vy : vz) * dot) / un / 3.0;
+        const double du = (ddir[b] - (b == 0 ? vx : b == 1 ? vy : vz) * dot) * (iun * (1.0 / 3.0));
 #pragma unroll
         for (int k = 0; k < 3; k++) dv[k * 3 + b] += du;
     }
