@@ -23,6 +23,9 @@ namespace ts {
 #ifndef TS_BWD_MINB
 #define TS_BWD_MINB 3  // CTAs per SM (registers: 80 at 3)
 #endif
+#ifndef TS_BWD_SMEMRED
+#define TS_BWD_SMEMRED 1  // run sums through shared memory, one lane per (run, component)
+#endif
 #ifndef TS_BWD_GRID
 #define TS_BWD_GRID 3  // CTAs per SM in the launch (one resident wave: 1.29 -> 1.19 ms at C3 against 8)
 #endif
@@ -69,6 +72,14 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const int mode = opt.mode;
+#if TS_BWD_SMEMRED
+    // per warp: the step's per-record components (component-major, padded) and
+    // its runs (first lane, triangle)
+    __shared__ double s_red[8][NG][33];
+    __shared__ unsigned s_run[8][33];
+    __shared__ unsigned s_rkey[8][32];
+    const int wl = threadIdx.x >> 5;
+#endif
     // (interleaved 32-record steps: measured faster than one contiguous range per warp)
     for (long long q0 = gw * 32; q0 < n; q0 += nw * 32) {
         const long long q = q0 + lane;
@@ -175,6 +186,32 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
         const unsigned kprev = __shfl_up_sync(0xffffffffu, key, 1);
         const bool head = lane == 0 || kprev != key;
         const unsigned heads = __ballot_sync(0xffffffffu, head);
+#if TS_BWD_SMEMRED
+        {
+            // run r = lanes [s_run[r], s_run[r+1]); lane L sums components of the
+            // (run, component) items L, L+32, ... and adds each sum with one atomic
+            const int nr = __popc(heads);
+            const int r = __popc(heads & ((2u << lane) - 1u)) - 1;
+#pragma unroll
+            for (int c = 0; c < NG; c++) s_red[wl][c][lane] = gf[c];
+            if (head) {
+                s_run[wl][r] = lane;
+                s_rkey[wl][r] = act ? key : 0xffffffffu;
+            }
+            if (lane == 0) s_run[wl][nr] = 32;
+            __syncwarp();
+            for (int item = lane; item < nr * NG; item += 32) {
+                const int rr = item / NG, c = item - rr * NG;
+                const unsigned k = s_rkey[wl][rr];
+                if (k == 0xffffffffu) continue;
+                const int lo = s_run[wl][rr], hi = s_run[wl][rr + 1];
+                double acc = 0.0;
+                for (int j = lo; j < hi; j++) acc += s_red[wl][c][j];
+                if (acc != 0.0) atomicAdd(sgrad + (size_t)k * SG_STRIDE + c, acc);  // (component 12 = SG_GZ)
+            }
+            __syncwarp();
+        }
+#else
         const unsigned later = heads & ~((2u << lane) - 1u);
         const int runlen = head ? (later ? __ffs(later) - 1 : 32) - (int)lane : 0;
         const int maxrun = __reduce_max_sync(0xffffffffu, runlen);
@@ -197,6 +234,7 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
             for (int c = 0; c < NG; c++)
                 if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);  // (component 12 = SG_GZ)
         }
+#endif
     }
 }
 
