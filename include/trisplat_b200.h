@@ -185,6 +185,15 @@ int ts_chain_views(ts_context* ctx, const ts_grads* grads, int accumulate, int n
                    void* const* events, void* stream);
 int ts_pending_views(ts_context* ctx);
 
+/* Host helper of the drop-in upload: dst[i] = (float)src[i] for i < n on a
+ * persistent pool of up to `threads` host threads (<= 0: all, at most 16).
+ * Returns 1 if every value converted exactly (the fp64 array holds fp32 values,
+ * e.g. the reference's synthetic soups, which round every parameter to fp32),
+ * 0 if not (dst then holds the rounded values), TS_ERR_INVALID_ARG for bad
+ * arguments.  render() uploads such soups as fp32 -- half the PCIe bytes, the
+ * same values -- and fp64 otherwise. */
+int ts_pack_f32(const double* src, float* dst, int64_t n, int threads);
+
 /* Fragment lists of the last ts_forward: render(collect_fragments=True)
  * (render.py:383-399, 420-425; count_fragments _kernels.py:135-178,
  * collect branch _kernels.py:107-116).

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TRISPLAT_B200_LIB") or os.path.join(HERE, "libtrisplat_b200.so")
 
 TS_OK = 0
+TS_ERR_INVALID_ARG = -1
 TS_ERR_NONFINITE = -5
 TS_ERR_FRAGMENTS = -7
 TS_ERR_CAPACITY = -9
@@ -73,7 +74,7 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
            "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack",
            "ts_tile_lists", "ts_backward_chunked", "ts_backward_screen", "ts_chain_views",
-           "ts_pending_views"]
+           "ts_pending_views", "ts_pack_f32"]
 TS_OPT_LEGACY_BINNING = 1
 TS_OPT_TILE_BACKWARD = 2
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
@@ -160,6 +161,8 @@ def load(path: str = LIB_PATH):
     lib.ts_backward_screen.restype = ctypes.c_int
     lib.ts_chain_views.argtypes = [V, P(TsGrads), I, I, P(ctypes.c_int64), P(ctypes.c_void_p), V]
     lib.ts_chain_views.restype = ctypes.c_int
+    lib.ts_pack_f32.argtypes = [V, V, ctypes.c_int64, I]
+    lib.ts_pack_f32.restype = ctypes.c_int
     lib.ts_pending_views.argtypes = [V]
     lib.ts_pending_views.restype = ctypes.c_int
     for nm in ("ts_ply_pack", "ts_ply_unpack", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",

@@ -42,7 +42,10 @@ def nvcc() -> str:
 
 
 def sources():
-    return sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+    return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+
+
+HOST_CXX = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I", INCLUDE, "-I", CSRC]
 
 
 def headers_mtime() -> float:
@@ -64,18 +67,21 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False, def
     changed = force or not os.path.exists(lib)
     for src in sources():
         sp = os.path.join(CSRC, src)
-        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         if (not force and os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(sp)
                 and os.path.getmtime(obj) >= hm):
             continue
-        cmd = [nvcc()] + ARCH + COMMON + extra_all + EXTRA.get(src, []) + ["-c", sp, "-o", obj]
+        if src.endswith(".cpp"):  # host-only code: the host compiler directly
+            cmd = [os.environ.get("CXX", "g++")] + HOST_CXX + extra_all + ["-c", sp, "-o", obj]
+        else:
+            cmd = [nvcc()] + ARCH + COMMON + extra_all + EXTRA.get(src, []) + ["-c", sp, "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         changed = True
     if changed or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart", "-Xcompiler", "-pthread"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

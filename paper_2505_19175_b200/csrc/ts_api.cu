@@ -930,6 +930,7 @@ int ts_backward_screen(ts_context* c, const float* d_image, void* stream) {
 
 int ts_pending_views(ts_context* c) { return c ? c->n_slots : 0; }
 
+
 int ts_chain_views(ts_context* c, const ts_grads* grads, int accumulate, int n_chunks, const int64_t* bounds,
                    void* const* events, void* stream) {
     DeviceGuard device_guard(c);

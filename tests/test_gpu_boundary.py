@@ -122,3 +122,29 @@ def test_render_outputs_are_independent_across_calls():
     gc.collect()
     c = tsb.render(soup, intr, pose, mode, background=(0.1, 0.2, 0.3))
     assert np.array_equal(c.image.rgb, img_a)
+
+
+@pytest.mark.parametrize("perturb", [False, True])
+def test_render_upload_f32_exact_or_f64(perturb):
+    """render() with the reference's fp64 soup: a soup of fp32 values crosses PCIe
+    as fp32 (ts_pack_f32), one value that is not an fp32 value sends the whole soup
+    as fp64; both render the oracle's frame (discrete outputs exact, RGB 1e-5)."""
+    from oracle import oracle as O
+    from paper_2505_19175_b200 import rasterizer as R
+    from paper_2505_19175_b200 import scenes
+    from paper_2505_19175_b200.types import TriangleSoup
+    soup, intr, pose = scenes.make_scene("c1")
+    if perturb:
+        sh = np.array(soup.sh, dtype=np.float64)
+        sh[len(sh) // 2, 0, 0] += 1e-13
+        soup = TriangleSoup(np.asarray(soup.vertices), np.asarray(soup.opacity), np.asarray(soup.sigma), sh)
+    out = R.render(soup, intr, pose)
+    assert R.LAST_RENDER_TIMES["upload"] == ("f64" if perturb else "f32")
+    n = len(soup.vertices)
+    assert R.LAST_RENDER_TIMES["upload_bytes"] == (8 if perturb else 4) * 59 * n
+    ref = O.render(soup, intr, pose)
+    np.testing.assert_array_equal(out.per_triangle_pixel_count, ref.per_triangle_pixel_count)
+    np.testing.assert_allclose(out.image.rgb, getattr(ref.image, "rgb", ref.image), atol=1e-5, rtol=0)
+    np.testing.assert_allclose(out.alpha_map, ref.alpha_map, atol=1e-5, rtol=0)
+    np.testing.assert_allclose(out.per_triangle_max_weight, ref.per_triangle_max_weight, atol=1e-6, rtol=0)
+    np.testing.assert_allclose(out.per_triangle_area, ref.per_triangle_area, rtol=1e-6, atol=0)

@@ -28,6 +28,10 @@ ms, ds = t(lambda: R.DeviceSoup.from_soup(soup, dtype=torch.float64))
 print(f"upload fp64 soup (staged): {ms:.2f} ms")
 ms, f = t(lambda: rast.forward(ds, intr, pose))
 print(f"forward on the fp64 soup: {ms:.2f} ms")
+ms, ds32 = t(lambda: R.DeviceSoup.from_soup_f32_exact(soup))
+print(f"upload fp64 soup as exact fp32 (ts_pack_f32 + staged DMA): {ms:.2f} ms")
+ms, _ = t(lambda: rast.forward(ds32, intr, pose))
+print(f"forward on the fp32 soup: {ms:.2f} ms")
 def outputs():
     packed = torch.cat([f.image.reshape(-1).double(), f.alpha_map.reshape(-1).double(), f.max_weight.double(),
                         f.area.double()])
@@ -42,7 +46,8 @@ def outputs():
 ms, _ = t(outputs)
 print(f"outputs to host (pinned): {ms:.2f} ms")
 ms, _ = t(lambda: R.render(soup, intr, pose))
-print(f"render() total: {ms:.2f} ms ({1e3 / ms:.1f} FPS)")
+print(f"render() total: {ms:.2f} ms ({1e3 / ms:.1f} FPS)", {k: (round(v, 2) if isinstance(v, float) else v)
+                                                           for k, v in R.LAST_RENDER_TIMES.items()})
 
 from paper_2505_19175_b200.types import ImageBuffer  # noqa: E402
 img = np.random.default_rng(0).random((720, 1280, 3))
