@@ -102,15 +102,19 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 const RecC& Cc = recc[src];
                 const int px = (int)(pix % (unsigned)cam.width), py = (int)(pix / (unsigned)cam.width);
                 const double pcx = px + 0.5, pcy = py + 0.5;
-                const double l0 = fma(__ldg(&R.a[0]), pcx, fma(__ldg(&R.a[1]), pcy, __ldg(&R.a[2])));
-                const double l1 = fma(__ldg(&R.a[3]), pcx, fma(__ldg(&R.a[4]), pcy, __ldg(&R.a[5])));
-                const double l2 = fma(__ldg(&R.a[6]), pcx, fma(__ldg(&R.a[7]), pcy, __ldg(&R.a[8])));
+                // the record's edge functions and phi_s as five 16-byte loads
+                const double2* ra = reinterpret_cast<const double2*>(R.a);
+                const double2 a01 = __ldg(ra), a23 = __ldg(ra + 1), a45 = __ldg(ra + 2), a67 = __ldg(ra + 3);
+                const double2 a8p = __ldg(ra + 4);  // (a[8], phis)
+                const double l0 = fma(a01.x, pcx, fma(a01.y, pcy, a23.x));
+                const double l1 = fma(a23.y, pcx, fma(a45.x, pcy, a45.y));
+                const double l2 = fma(a67.x, pcx, fma(a67.y, pcy, a8p.x));
                 // argmax of phi = argmin of phi/phi_s, ties -> lowest edge (_kernels.py:36-42)
                 double r64 = l0;
                 int edge = 0;
                 if (l1 < r64) { r64 = l1; edge = 1; }
                 if (l2 < r64) { r64 = l2; edge = 2; }
-                const double phis = __ldg(&R.phis);
+                const double phis = a8p.y;
                 const double2 osg = __ldg(reinterpret_cast<const double2*>(&Cc.opa));
                 const double o = osg.x, sg = osg.y;
                 const double rc = fmin(r64, 1.0);
@@ -123,7 +127,8 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 const double tb = tc.x;
                 const double w = tb * a;
                 const double2 c01 = __ldg(reinterpret_cast<const double2*>(Cc.rgb));
-                const double c0 = c01.x, c1 = c01.y, c2 = __ldg(&Cc.rgb[2]);
+                const double2 c2io = __ldg(reinterpret_cast<const double2*>(Cc.rgb + 2));  // (rgb[2], inv_opa)
+                const double c0 = c01.x, c1 = c01.y, c2 = c2io.x;
                 const double s0 = __ldg(c_total + pix * 3 + 0) - tc.y - w * c0;
                 const double s1 = __ldg(c_total + pix * 3 + 1) - tc.z - w * c1;
                 const double s2 = __ldg(c_total + pix * 3 + 2) - tc.w - w * c2;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 if (!clamped) {
                     // (reciprocals of the opacity and of phi_s precomputed per triangle: the
                     // products differ from the quotients by <= 1 ulp)
-                    const double inv_o = __ldg(&Cc.inv_opa), inv_phis = __ldg(&B.inv_phis);
+                    const double inv_o = c2io.y, inv_phis = __ldg(&B.inv_phis);
                     const double window = a * inv_o;
                     gf[6] = ga * window;  // d/d opacity = g_alpha * alpha / o
                     const double g_win = o * ga;
@@ -167,7 +172,9 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                     const int ib = edge == 2 ? 0 : edge + 1;
                     const double ax = __ldg(&B.qx[edge]), ay = __ldg(&B.qy[edge]);
                     const double bx = __ldg(&B.qx[ib]), by = __ldg(&B.qy[ib]);
-                    const double pxr = (double)(px - __ldg(&R.ox)) + 0.5, pyr = (double)(py - __ldg(&R.oy)) + 0.5;
+                    const unsigned oxy = __ldg(reinterpret_cast<const unsigned*>(&R.ox));  // (ox, oy) shorts
+                    const double pxr = (double)(px - (int)(short)(oxy & 0xffffu)) + 0.5;
+                    const double pyr = (double)(py - (int)(short)(oxy >> 16)) + 0.5;
                     const double sl = __ldg(&B.sl[edge]), ul = __ldg(&B.ul[edge]), vl = __ldg(&B.vl[edge]);
                     const double gax = g_phi * (sl * (pyr - by) + phi * ul);
                     const double gay = g_phi * (sl * (bx - pxr) + phi * vl);

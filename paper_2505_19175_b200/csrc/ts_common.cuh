@@ -98,6 +98,11 @@ struct __align__(16) RecC {
     double inv_opa;   // 1 / opacity (the backward multiplies instead of dividing)
 };
 static_assert(sizeof(RecC) == 48, "RecC layout");
+// (the streaming backward reads (a[8], phis), (rgb[2], inv_opa) and (ox, oy) as pairs)
+static_assert(offsetof(RecF, phis) == offsetof(RecF, a) + 64 + 8 && offsetof(RecF, oy) == offsetof(RecF, ox) + 2 &&
+                  offsetof(RecF, ox) % 4 == 0 && offsetof(RecC, inv_opa) == offsetof(RecC, rgb) + 24 &&
+                  offsetof(RecC, rgb) % 16 == 0,
+              "record layouts of the paired loads");
 
 // Shared-memory images of a RecF for the dense blend kernels: the evaluation
 // part (first 96 B) and the tail (last 32 B), copied with 16-byte cp.async.
