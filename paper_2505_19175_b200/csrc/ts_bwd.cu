@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         const RecB& rb = sm.rb[slot];
                         const TailRec& tr = sm.tail[slot];
                         const int ib = edge == 2 ? 0 : edge + 1;
-                        const double ax = rb.qx[edge], ay = rb.qy[edge], bx = rb.qx[ib], by = rb.qy[ib];
+                        const double ax = rb.q[edge].x, ay = rb.q[edge].y, bx = rb.q[ib].x, by = rb.q[ib].y;
                         const double pxr = (double)(X0 + lx - tr.ox) + 0.5, pyr = (double)(Y0 + ly - tr.oy) + 0.5;
                         const double sl_ = rb.sl[edge], ul = rb.ul[edge], vl = rb.vl[edge];
                         const double gax = g_phi * (sl_ * (pyr - by) + phi * ul);

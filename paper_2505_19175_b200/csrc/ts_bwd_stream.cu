@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                         g_phi = -g_win * ww * is;
                     }
                     const int ib = edge == 2 ? 0 : edge + 1;
-                    const double ax = __ldg(&B.qx[edge]), ay = __ldg(&B.qy[edge]);
-                    const double bx = __ldg(&B.qx[ib]), by = __ldg(&B.qy[ib]);
+                    const double2 qa = __ldg(&B.q[edge]), qb = __ldg(&B.q[ib]);
+                    const double ax = qa.x, ay = qa.y, bx = qb.x, by = qb.y;
                     const unsigned oxy = __ldg(reinterpret_cast<const unsigned*>(&R.ox));  // (ox, oy) shorts
                     const double pxr = (double)(px - (int)(short)(oxy & 0xffffu)) + 0.5;
                     const double pyr = (double)(py - (int)(short)(oxy >> 16)) + 0.5;

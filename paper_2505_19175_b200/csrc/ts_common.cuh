@@ -81,7 +81,7 @@ static_assert(sizeof(RecF) == 128, "RecF layout");
 // derivative (_kernels.py:296-318) in fp64 -- edge lengths of near-degenerate
 // triangles are ill-conditioned:  sl = s/l,  ul = (b-a)_x/l^2,  vl = (b-a)_y/l^2.
 struct __align__(16) RecB {
-    double qx[3], qy[3];
+    double2 q[3];  // (x, y) per vertex (one 16-byte load each)
     double sl[3], ul[3], vl[3];
     double inv_phis;  // 1 / phi_s (the backward multiplies instead of dividing)
 };

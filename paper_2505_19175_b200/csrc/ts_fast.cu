@@ -266,8 +266,7 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
                 RecB rb;
 #pragma unroll
                 for (int e = 0; e < 3; e++) {
-                    rb.qx[e] = q[e * 2] - ox;
-                    rb.qy[e] = q[e * 2 + 1] - oy;
+                    rb.q[e] = make_double2(q[e * 2] - ox, q[e * 2 + 1] - oy);
                     const int bi = e == 2 ? 0 : e + 1;
                     const double ex = q[bi * 2] - q[e * 2], ey = q[bi * 2 + 1] - q[e * 2 + 1];
                     const double il = 1.0 / sqrt(ex * ex + ey * ey);
