@@ -194,6 +194,17 @@ int ts_pending_views(ts_context* ctx);
  * same values -- and fp64 otherwise. */
 int ts_pack_f32(const double* src, float* dst, int64_t n, int threads);
 
+/* The whole lossless upload in one call: src (host fp64, n values) -> dst
+ * (device fp32) on `stream`, chunk by chunk through a small ring of page-locked
+ * slots (nslot slots of chunk_bytes; <= 0: 4 x 4 MB) on the current device; the
+ * conversion of a chunk (ts_pack_f32's thread pool) overlaps the DMA of the
+ * previous one.  flags bit 0: streaming (non-temporal) stores into the slots.
+ * Returns 1 when every value was an fp32 value (dst is complete once `stream`
+ * reaches the copies), 0 when one was not (the copies issued so far have
+ * finished, dst is incomplete: upload fp64 instead), < 0 on error. */
+int ts_upload_f32(const double* src, int64_t n, float* dst, void* stream, int64_t chunk_bytes, int nslot,
+                  int flags);
+
 /* Fragment lists of the last ts_forward: render(collect_fragments=True)
  * (render.py:383-399, 420-425; count_fragments _kernels.py:135-178,
  * collect branch _kernels.py:107-116).

@@ -45,7 +45,9 @@ def sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
-HOST_CXX = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I", INCLUDE, "-I", CSRC]
+def host_cxx_flags():
+    cuda_inc = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(nvcc()))), "include")
+    return ["-O3", "-std=c++17", "-fPIC", "-pthread", "-I", INCLUDE, "-I", CSRC, "-I", cuda_inc]
 
 
 def headers_mtime() -> float:
@@ -73,7 +75,7 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False, def
                 and os.path.getmtime(obj) >= hm):
             continue
         if src.endswith(".cpp"):  # host-only code: the host compiler directly
-            cmd = [os.environ.get("CXX", "g++")] + HOST_CXX + extra_all + ["-c", sp, "-o", obj]
+            cmd = [os.environ.get("CXX", "g++")] + host_cxx_flags() + extra_all + ["-c", sp, "-o", obj]
         else:
             cmd = [nvcc()] + ARCH + COMMON + extra_all + EXTRA.get(src, []) + ["-c", sp, "-o", obj]
         if verbose:

@@ -17,11 +17,11 @@
 #include <thread>
 #include <vector>
 
-#include "trisplat_b200.h"
+#include <cuda_runtime.h>
 
-#ifndef TS_PACK_STREAM
-#define TS_PACK_STREAM 1
-#endif
+#include <map>
+
+#include "trisplat_b200.h"
 
 namespace {
 
@@ -103,6 +103,7 @@ int pack_scalar(const double* __restrict__ s, float* __restrict__ d, int64_t n) 
 
 // 8 values per step; streaming (non-temporal) stores: the staging chunk is read
 // next by the DMA engine, not by this core
+template <bool STREAM>
 __attribute__((target("avx2"))) int pack_avx2(const double* __restrict__ s, float* __restrict__ d, int64_t n) {
     int64_t i = 0;
     int ok = 1;
@@ -115,16 +116,15 @@ __attribute__((target("avx2"))) int pack_avx2(const double* __restrict__ s, floa
     for (; i + 8 <= n; i += 8) {
         const __m256d a = _mm256_loadu_pd(s + i), b = _mm256_loadu_pd(s + i + 4);
         const __m128 fa = _mm256_cvtpd_ps(a), fb = _mm256_cvtpd_ps(b);
-#if TS_PACK_STREAM
-        _mm256_stream_ps(d + i, _mm256_set_m128(fb, fa));
-#else
-        _mm256_store_ps(d + i, _mm256_set_m128(fb, fa));
-#endif
+        if constexpr (STREAM)
+            _mm256_stream_ps(d + i, _mm256_set_m128(fb, fa));
+        else
+            _mm256_store_ps(d + i, _mm256_set_m128(fb, fa));
         const __m256d ea = _mm256_cmp_pd(_mm256_cvtps_pd(fa), a, _CMP_EQ_OQ);
         const __m256d eb = _mm256_cmp_pd(_mm256_cvtps_pd(fb), b, _CMP_EQ_OQ);
         all = _mm256_and_pd(all, _mm256_and_pd(ea, eb));
     }
-    _mm_sfence();
+    if constexpr (STREAM) _mm_sfence();
     ok &= _mm256_movemask_pd(all) == 0xF;
     for (; i < n; i++) {
         const float f = (float)s[i];
@@ -147,8 +147,100 @@ extern "C" int ts_pack_f32(const double* src, float* dst, int64_t n, int threads
     const int64_t per = ((n + parts - 1) / parts + 15) / 16 * 16;
     pool.run(parts, [&](int k) {
         const int64_t lo = std::min<int64_t>(n, k * per), hi = std::min<int64_t>(n, lo + per);
-        const int ok = avx2 ? pack_avx2(src + lo, dst + lo, hi - lo) : pack_scalar(src + lo, dst + lo, hi - lo);
+        const int ok = avx2 ? pack_avx2<true>(src + lo, dst + lo, hi - lo) : pack_scalar(src + lo, dst + lo, hi - lo);
         if (!ok) exact.store(0, std::memory_order_relaxed);
     });
     return exact.load();
+}
+
+// ---------------------------------------------------------------------------
+// Whole upload in one call: chunks of the fp64 array are converted into a small
+// ring of page-locked slots (small enough to stay in the host's last-level cache
+// between the conversion and the DMA that reads it) and copied to dst on
+// `stream`; the conversion of chunk i+1 overlaps the DMA of chunk i.  Returns 1
+// when every value was an fp32 value (dst complete once the stream reaches the
+// copies), 0 when one was not (the copies issued so far have finished; dst is
+// incomplete), < 0 on a CUDA error.
+// ---------------------------------------------------------------------------
+namespace {
+struct UploadRing {
+    std::vector<float*> slot;
+    std::vector<cudaEvent_t> ev;
+    int64_t slot_floats = 0;
+};
+std::mutex g_ring_m;
+std::map<int, UploadRing> g_rings;  // per device
+
+int ring_for(int dev, int64_t slot_floats, int nslot, UploadRing** out) {
+    UploadRing& r = g_rings[dev];
+    if (r.slot_floats != slot_floats || (int)r.slot.size() != nslot) {
+        for (size_t k = 0; k < r.slot.size(); k++) {
+            cudaEventSynchronize(r.ev[k]);
+            cudaEventDestroy(r.ev[k]);
+            cudaFreeHost(r.slot[k]);
+        }
+        r.slot.assign(nslot, nullptr);
+        r.ev.assign(nslot, nullptr);
+        r.slot_floats = slot_floats;
+        for (int k = 0; k < nslot; k++) {
+            if (cudaHostAlloc((void**)&r.slot[k], sizeof(float) * slot_floats, cudaHostAllocPortable) != cudaSuccess ||
+                cudaEventCreateWithFlags(&r.ev[k], cudaEventDisableTiming) != cudaSuccess) {
+                r.slot_floats = 0;
+                return TS_ERR_OOM;
+            }
+        }
+    }
+    *out = &r;
+    return TS_OK;
+}
+}  // namespace
+
+extern "C" int ts_upload_f32(const double* src, int64_t n, float* dst, void* stream, int64_t chunk_bytes,
+                             int nslot, int flags) {
+    if (n < 0 || (n > 0 && (!src || !dst))) return TS_ERR_INVALID_ARG;
+    if (n == 0) return 1;
+    const int64_t cb = chunk_bytes > 0 ? chunk_bytes : (4ll << 20);
+    const int64_t step = std::max<int64_t>(1024, cb / 4 / 64 * 64);
+    nslot = nslot > 1 ? nslot : 4;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return TS_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(g_ring_m);
+    UploadRing* r = nullptr;
+    int rc = ring_for(dev, step, nslot, &r);
+    if (rc) return rc;
+    HostPool& pool = host_pool();
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    const bool stream_stores = (flags & 1) != 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int exact = 1;
+    int64_t i = 0;
+    for (int64_t off = 0; off < n; off += step, i++) {
+        const int k = (int)(i % nslot);
+        const int64_t c = std::min(step, n - off);
+        if (cudaEventSynchronize(r->ev[k]) != cudaSuccess) return TS_ERR_CUDA;  // the slot's last DMA is done
+        float* slot = r->slot[k];
+        const int parts = c < (1 << 16) ? 1 : pool.size();
+        const int64_t per = ((c + parts - 1) / parts + 15) / 16 * 16;
+        std::atomic<int> ok{1};
+        pool.run(parts, [&](int p) {
+            const int64_t lo = std::min<int64_t>(c, p * per), hi = std::min<int64_t>(c, lo + per);
+            int good;
+            if (!avx2)
+                good = pack_scalar(src + off + lo, slot + lo, hi - lo);
+            else if (stream_stores)
+                good = pack_avx2<true>(src + off + lo, slot + lo, hi - lo);
+            else
+                good = pack_avx2<false>(src + off + lo, slot + lo, hi - lo);
+            if (!good) ok.store(0, std::memory_order_relaxed);
+        });
+        if (!ok.load()) {
+            exact = 0;
+            break;
+        }
+        if (cudaMemcpyAsync(dst + off, slot, sizeof(float) * c, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaEventRecord(r->ev[k], st) != cudaSuccess)
+            return TS_ERR_CUDA;
+    }
+    if (!exact && cudaStreamSynchronize(st) != cudaSuccess) return TS_ERR_CUDA;
+    return exact;
 }

@@ -85,47 +85,25 @@ def _staged_h2d(a: np.ndarray, device="cuda") -> torch.Tensor:
     return out
 
 
-_STAGE32_CHUNK = 32 << 20  # fp32 bytes per chunk of the packed upload
-_STAGE32_NBUF = 6  # (north-star soup: 16 MB x 6 15.7 ms, 32 MB x 4 16.7, 32 MB x 6 13.4, 64 MB x 4 13.8)
-_STAGE32: dict = {}  # device index -> ([(pinned buffer, event)], [copy streams])
+# lossless fp32 upload (ts_upload_f32): chunk bytes, ring slots, flags (bit 0: streaming stores)
+_UPLOAD_F32 = (16 << 20, 4, 1)  # (tools/upload_probe.py: 12.7 ms for the north-star soup; 4 MB x 4 regular stores 15.8)
 
 
 def _staged_h2d_f32(a: np.ndarray, device="cuda") -> "torch.Tensor | None":
     """fp64 array -> fp32 device tensor when every value is an fp32 value
-    (ts_pack_f32 converts each chunk into a page-locked ring slot on the host's
-    threads while the previous chunks' DMAs run), else None."""
+    (ts_upload_f32: each chunk converted on the host's threads into a
+    page-locked ring slot while the previous chunk's DMA runs), else None."""
     lib = _lib.load()
     src = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
     out = torch.empty(a.shape, dtype=torch.float32, device=device)
-    n = src.size
-    dev = out.device.index if out.device.index is not None else torch.cuda.current_device()
-    if dev not in _STAGE32:
-        with torch.cuda.device(dev):
-            _STAGE32[dev] = ([(torch.empty(_STAGE32_CHUNK // 4, dtype=torch.float32).pin_memory(), torch.cuda.Event())
-                              for _ in range(_STAGE32_NBUF)], [torch.cuda.Stream(dev) for _ in range(2)])
-    ring, streams = _STAGE32[dev]
-    ob = out.reshape(-1)
-    cur = torch.cuda.current_stream(out.device)
-    for st in streams:
-        st.wait_stream(cur)
-    step = ring[0][0].numel()
-    base = src.ctypes.data
-    exact = True
-    for i, off in enumerate(range(0, n, step)):
-        buf, ev = ring[i % len(ring)]
-        st = streams[i % len(streams)]
-        c = min(step, n - off)
-        ev.synchronize()
-        rc = lib.ts_pack_f32(ctypes.c_void_p(base + 8 * off), ctypes.c_void_p(buf.data_ptr()), c, 0)
-        if rc != 1:
-            exact = False
-            break
-        with torch.cuda.stream(st):
-            ob[off:off + c].copy_(buf[:c], non_blocking=True)
-            ev.record(st)
-    for st in streams:
-        cur.wait_stream(st)  # (also before `out` is released on a failed pack)
-    return out if exact else None
+    with torch.cuda.device(out.device):
+        st = torch.cuda.current_stream(out.device)
+        chunk, nslot, flags = _UPLOAD_F32
+        rc = lib.ts_upload_f32(ctypes.c_void_p(src.ctypes.data), src.size, ctypes.c_void_p(out.data_ptr()),
+                               ctypes.c_void_p(st.cuda_stream), chunk, nslot, flags)
+    if rc < 0:
+        _lib.check(rc, "upload_f32")
+    return out if rc == 1 else None
 
 
 @dataclass

@@ -148,3 +148,19 @@ def test_render_upload_f32_exact_or_f64(perturb):
     np.testing.assert_allclose(out.alpha_map, ref.alpha_map, atol=1e-5, rtol=0)
     np.testing.assert_allclose(out.per_triangle_max_weight, ref.per_triangle_max_weight, atol=1e-6, rtol=0)
     np.testing.assert_allclose(out.per_triangle_area, ref.per_triangle_area, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 5_000_003])
+def test_upload_f32(n):
+    """ts_upload_f32 (the lossless upload of render()): fp32 values arrive bit for
+    bit; one value that is not an fp32 value -> 0 and no tensor."""
+    from paper_2505_19175_b200 import rasterizer as R
+    a = np.random.default_rng(n).normal(size=n).astype(np.float32).astype(np.float64)
+    t = R._staged_h2d_f32(a)
+    assert t is not None and t.dtype == torch.float32
+    np.testing.assert_array_equal(t.cpu().numpy(), a.astype(np.float32))
+    b = a.copy()
+    b[-1] += 1e-9
+    assert R._staged_h2d_f32(b) is None
+    t2 = R._staged_h2d_f32(a)  # the ring is reusable after a failed upload
+    np.testing.assert_array_equal(t2.cpu().numpy(), a.astype(np.float32))
