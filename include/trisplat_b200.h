@@ -185,6 +185,15 @@ int ts_chain_views(ts_context* ctx, const ts_grads* grads, int accumulate, int n
                    void* const* events, void* stream);
 int ts_pending_views(ts_context* ctx);
 
+/* Two-phase allocation: size every per-frame buffer of the context for scenes of
+ * up to n triangles at width x height (entries: expected tile entries, <= 0:
+ * 4 per triangle; keep_backward: also the training forward's records, the
+ * fragment-record buffer for 8 fragments per entry and the backward's
+ * screen-space rows), so later ts_forward / ts_backward calls of that size
+ * allocate nothing.  ts_workspace_bytes: device bytes the context holds. */
+int ts_reserve(ts_context* ctx, int64_t n, int width, int height, int64_t entries, int keep_backward);
+int64_t ts_workspace_bytes(ts_context* ctx);
+
 /* Host helper of the drop-in upload: dst[i] = (float)src[i] for i < n on a
  * persistent pool of up to `threads` host threads (<= 0: all, at most 16).
  * Returns 1 if every value converted exactly (the fp64 array holds fp32 values,

@@ -74,7 +74,7 @@ EXPORTS = ["ts_context_create", "ts_context_destroy", "ts_error_string", "ts_ver
            "ts_normal_loss", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates",
            "ts_pick_info", "ts_gather_rows", "ts_child_vertices", "ts_ply_pack", "ts_ply_unpack",
            "ts_tile_lists", "ts_backward_chunked", "ts_backward_screen", "ts_chain_views",
-           "ts_pending_views", "ts_pack_f32", "ts_upload_f32"]
+           "ts_pending_views", "ts_pack_f32", "ts_upload_f32", "ts_reserve", "ts_workspace_bytes"]
 TS_OPT_LEGACY_BINNING = 1
 TS_OPT_TILE_BACKWARD = 2
 STAGES = ["preprocess", "depth_sort", "binning", "blend", "fixup", "blend_bwd", "chain_bwd"]
@@ -165,6 +165,10 @@ def load(path: str = LIB_PATH):
     lib.ts_pack_f32.restype = ctypes.c_int
     lib.ts_upload_f32.argtypes = [V, ctypes.c_int64, V, V, ctypes.c_int64, I, I]
     lib.ts_upload_f32.restype = ctypes.c_int
+    lib.ts_reserve.argtypes = [V, ctypes.c_int64, I, I, ctypes.c_int64, I]
+    lib.ts_reserve.restype = ctypes.c_int
+    lib.ts_workspace_bytes.argtypes = [V]
+    lib.ts_workspace_bytes.restype = ctypes.c_int64
     lib.ts_pending_views.argtypes = [V]
     lib.ts_pending_views.restype = ctypes.c_int
     for nm in ("ts_ply_pack", "ts_ply_unpack", "ts_view_stats_accumulate", "ts_prune_mark", "ts_sample_candidates", "ts_pick_info",

@@ -37,6 +37,7 @@ struct ts_context {
     // per-triangle scratch (capacity in triangles)
     long long cap_n = -1;
     void* tri_buf = nullptr;
+    size_t tri_bytes = 0, ent_bytes = 0, pix_bytes = 0, os_bytes = 0;  // (ts_workspace_bytes)
     unsigned long long* key = nullptr;
     unsigned* tcount = nullptr;
     unsigned* flag = nullptr;
@@ -190,6 +191,7 @@ static int ensure_tri(ts_context* c, long long n) {
            o_vc = take(4 * cap), o_ka = take(8 * cap), o_va = take(4 * cap), o_of = take(4 * (cap + 1)),
            o_rk = take(4 * cap), o_dp = take(8 * cap), o_bb = take(8 * cap);
     TS_CHECK(cudaMalloc(&c->tri_buf, off));
+    c->tri_bytes = off;
     char* b = (char*)c->tri_buf;
     c->key = (unsigned long long*)(b + o_key);
     c->tcount = (unsigned*)(b + o_tc);
@@ -213,6 +215,7 @@ static int ensure_ent(ts_context* c, long long e) {
     c->ent_buf = nullptr;
     size_t one = align_up(4 * cap, 256);
     TS_CHECK(cudaMalloc(&c->ent_buf, 8 * one));
+    c->ent_bytes = 8 * one;
     char* b = (char*)c->ent_buf;
     c->tkey = (unsigned*)b;
     c->tval = (unsigned*)(b + one);
@@ -240,6 +243,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     size_t o_tf = take(8 * cp), o_t32 = take(4 * cp), o_lp = take(4 * cp), o_fg = take(8 * cp),
            o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp), o_tc = take(4 * (ct + 1)), o_bl = take(4 * (ct + 1));
     TS_CHECK(cudaMalloc(&c->pix_buf, off));
+    c->pix_bytes = off;
     char* b = (char*)c->pix_buf;
     c->t_final = (double*)(b + o_tf);
     c->t_final32 = (float*)(b + o_t32);
@@ -260,6 +264,7 @@ static int ensure_os(ts_context* c, long long count) {
     if (c->os_buf) cudaFree(c->os_buf);
     c->os_buf = nullptr;
     TS_CHECK(cudaMalloc(&c->os_buf, onesweep_scratch_bytes(cap, 4)));
+    c->os_bytes = onesweep_scratch_bytes(cap, 4);
     c->os_cap = cap;
     return TS_OK;
 }
@@ -929,6 +934,45 @@ int ts_backward_screen(ts_context* c, const float* d_image, void* stream) {
 }
 
 int ts_pending_views(ts_context* c) { return c ? c->n_slots : 0; }
+
+int ts_reserve(ts_context* c, int64_t n, int width, int height, int64_t entries, int keep_backward) {
+    DeviceGuard device_guard(c);
+    if (!c || n < 0 || width < 1 || height < 1 || width > 32000 || height > 32000 || n >= (1ll << 31))
+        return TS_ERR_INVALID_ARG;
+    const long long n1 = n > 0 ? n : 1;
+    const long long P = (long long)width * height;
+    const int ntiles = ((width + TILE - 1) / TILE) * ((height + TILE - 1) / TILE);
+    const long long e = entries > 0 ? entries : 4 * n1 + 4096;
+    c->e_hint = std::max<long long>(c->e_hint, e);  // the forwards' working capacity follows it
+    int rc;
+    if ((rc = ensure_tri(c, n1)) || (rc = ensure_pix(c, P, ntiles)) ||
+        (rc = ensure(c->recf, sizeof(RecF) * n1)) ||
+        (rc = ensure_ent(c, std::max<long long>(4 * n1 + 4096, c->e_hint + c->e_hint / 2))) ||
+        (rc = ensure_os(c, std::max<long long>(n1, c->cap_e) + 1)) || (rc = ensure(c->binmat, bin_matrix_bytes(n1, ntiles))))
+        return rc;
+    if (keep_backward) {
+        const long long f = std::max<long long>(c->frec_hint, 8 * std::max<long long>(c->e_hint, n1));
+        c->frec_hint = std::max<long long>(c->frec_hint, f);
+        if ((rc = ensure(c->recb, sizeof(RecB) * n1)) || (rc = ensure(c->recc, sizeof(RecC) * n1)) ||
+            (rc = ensure(c->sg64, sizeof(double) * SG_STRIDE * n1)) ||
+            (rc = ensure(c->frec, sizeof(FragRec) * (size_t)(f + f / 4 + 4096))) ||
+            (rc = ensure(c->ctot, sizeof(double) * 3 * (size_t)P)))
+            return rc;
+        c->frec_cap = c->frec.bytes / sizeof(FragRec);
+    }
+    return TS_OK;
+}
+
+int64_t ts_workspace_bytes(ts_context* c) {
+    if (!c) return 0;
+    int64_t t = (int64_t)(c->tri_bytes + c->ent_bytes + c->pix_bytes + c->os_bytes);
+    for (const DevBuf* b : {&c->fsw, &c->adam_ibc, &c->tl_cnt, &c->tl_off, &c->tl_cs, &c->tl_kv, &c->rec64, &c->recf,
+                            &c->recb, &c->recc, &c->sg64, &c->sg32, &c->frag_off, &c->cs_scratch, &c->frec, &c->ctot,
+                            &c->binmat, &c->lossbuf, &c->densbuf})
+        t += (int64_t)b->bytes;
+    for (int k = 0; k < TS_MAX_CHAIN_VIEWS; k++) t += (int64_t)(c->slot_sg[k].bytes + c->slot_flag[k].bytes);
+    return t;
+}
 
 
 int ts_chain_views(ts_context* c, const ts_grads* grads, int accumulate, int n_chunks, const int64_t* bounds,

@@ -440,6 +440,17 @@ class Rasterizer:
                                                 k, b, evp, ctypes.c_void_p(st)), "backward_chunked")
         return grads
 
+    def reserve(self, n: int, width: int, height: int, entries: int = 0, keep_backward: bool = False) -> int:
+        """Size every per-frame buffer for scenes of up to n triangles at
+        width x height (ts_reserve), so later forwards / backwards of that size
+        allocate nothing; returns the device bytes the context holds."""
+        _lib.check(self.lib.ts_reserve(self._ctx, int(n), int(width), int(height), int(entries),
+                                       int(bool(keep_backward))), "reserve")
+        return self.workspace_bytes()
+
+    def workspace_bytes(self) -> int:
+        return int(self.lib.ts_workspace_bytes(self._ctx))
+
     MAX_PENDING_VIEWS = 8
 
     def backward_screen(self, d_image: torch.Tensor, stream=None) -> int:

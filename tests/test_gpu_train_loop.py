@@ -75,3 +75,26 @@ def test_chunked_backward_matches_backward():
         rast.forward(ds, intr, pose)
         rast.backward(d, g, accumulate=True, chunks=(b, ev))
         assert torch.allclose(g.flat, 2 * ref.flat, rtol=1e-6, atol=1e-12)
+
+
+def test_reserve_then_no_allocation():
+    """ts_reserve sizes the per-frame buffers up front (two-phase allocation):
+    a training forward + backward of that size allocates nothing more, and the
+    results equal those of a context that grew on demand."""
+    from paper_2505_19175_b200 import DeviceSoup, Rasterizer, scenes
+    soup = DeviceSoup.from_soup(scenes.make_soup(200_000, seed=3, size=0.02, sigma=(1.0, 1.0)), dtype=torch.float32)
+    intr, pose = scenes.frontal_camera(640, 360, 550.0)
+    d_img = torch.randn((360, 640, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    grow = Rasterizer()
+    f0 = grow.forward(soup, intr, pose, keep_backward=True)
+    g0 = grow.backward(d_img)
+    r = Rasterizer()
+    b = r.reserve(len(soup), 640, 360, entries=f0.n_entries, keep_backward=True)
+    assert b > 0 and b == r.workspace_bytes()
+    f1 = r.forward(soup, intr, pose, keep_backward=True)
+    g1 = r.backward(d_img)
+    torch.cuda.synchronize()
+    assert r.workspace_bytes() == b
+    assert torch.equal(f0.image, f1.image) and torch.equal(f0.pixel_count, f1.pixel_count)
+    # (fp64 atomics: the summation order, and so the last bits, may differ between runs)
+    torch.testing.assert_close(g1.flat, g0.flat, rtol=1e-6, atol=1e-6 * float(g0.flat.abs().max()))
