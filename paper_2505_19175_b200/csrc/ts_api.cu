@@ -433,7 +433,7 @@ static void global_depth_order(ts_context* c, long long n, cudaStream_t st) {
 // Binning + blend of the current forward, sized from host capacities and the
 // device counters of the preprocess (no host round trip).  Default: tile-first
 // binning (ts_bin.cu) -- per-tile counts, scan, bucket fill, then every tile's
-// list sorted by exact (z, idx) in shared memory.  TS_BIN_LEGACY: global depth
+// list sorted by exact (z, idx) in shared memory.  TS_OPT_LEGACY_BINNING: global depth
 // sort, rank offsets, tile duplication, stable radix sort by tile, ranges.
 static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_options* opt, const ts_soup* soup,
                         const ts_forward_out* out, cudaStream_t st) {
