@@ -253,6 +253,10 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     c->nfrag = (int*)(b + o_nf);
     c->tcnt = (unsigned*)(b + o_tc);
     c->big_list = (int*)(b + o_bl);
+    // flagged-pixel list entries start empty (pixel -1); the fix-up empties each
+    // entry it consumes, so the list is clean for the next frame
+    TS_CHECK(cudaMemset(c->flags, 0xff, 8 * (size_t)cp));
+    TS_CHECK(cudaDeviceSynchronize());
     c->cap_p = cp;
     c->cap_tiles = ct;
     return TS_OK;
@@ -640,8 +644,9 @@ int ts_forward(ts_context* c, const ts_camera* cam, const ts_options* opt, const
             if ((rc = ensure(c->frec, sizeof(FragRec) * (size_t)(f + f / 4 + 4096)))) return rc;
             c->frec_cap = c->frec.bytes / sizeof(FragRec);
         }
-        // n_flagged, n_frec, frec_over
-        TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, 3 * sizeof(unsigned long long), st));
+        // n_flagged, n_frec, frec_over, blend_done
+        static_assert(offsetof(Counters, blend_done) == offsetof(Counters, n_flagged) + 24, "counter order");
+        TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, 4 * sizeof(unsigned long long), st));
         if (out->max_weight && n) TS_CHECK(cudaMemsetAsync(out->max_weight, 0, sizeof(float) * n, st));
         if (out->pixel_count && n) TS_CHECK(cudaMemsetAsync(out->pixel_count, 0, sizeof(int) * n, st));
         if ((rc = enqueue_tail(c, cm, op, opt, soup, out, st))) return rc;
@@ -765,6 +770,7 @@ int ts_collect_fragments(ts_context* c, const int64_t* offsets, int32_t* triangl
     // (rasterize_forward collect branch, _kernels.py:107-116); statistics and
     // images are not touched, flagged pixels are re-emitted by the fix-up
     TS_CHECK(cudaMemsetAsync(&c->d_ctr->n_flagged, 0, sizeof(unsigned long long), st));
+    TS_CHECK(cudaMemsetAsync(&c->d_ctr->blend_done, 0, sizeof(unsigned long long), st));
     FastBlendOut bo{};
     bo.t_final = c->t_final32;
     bo.t_final64 = nullptr;

@@ -609,7 +609,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
         const int p = py * cam.width + px;
         if (flag_pos >= 0) {
             unsigned long long k = atomicAdd(&out.ctr->n_flagged, 1ull);
-            out.flags[k] = make_int2(p, flag_pos);
+            out.flags[k] = make_int2(p, flag_pos);  // (pixel >= 0: the entry is published)
+            __threadfence();
         } else {
             if (out.image) {
                 out.image[p * 3 + 0] = (float)fmin(fmax(C0 + T * (Real)opt.bg[0], (Real)0), (Real)1);
@@ -629,6 +630,9 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
         }
     }
+    // this tile's flags are published: count the CTA (k_fixup_fwd ends when all have)
+    __syncthreads();
+    if (tid == 0) atomicAdd(&out.ctr->blend_done, 1ull);
 }
 
 template <int DB, int PCAP, bool ACC64, int MINB>

@@ -417,6 +417,9 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) 
 // while this grid's last wave drains.  A no-op for kernels launched without the
 // attribute.
 #define TS_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+// (the fix-up: its CTAs start while the blend's last wave runs and take each
+// flagged pixel as soon as the blend publishes it; no grid-wide wait)
+#define TS_PDL_LAUNCH_ONLY() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 #ifndef __CUDACC_RTC__
 #include <mutex>
 #include <utility>

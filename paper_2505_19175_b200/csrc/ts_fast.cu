@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
         const int p = py * cam.width + px;
         if (flag_pos >= 0) {
             unsigned long long k = atomicAdd(&out.ctr->n_flagged, 1ull);
-            out.flags[k] = make_int2(p, flag_pos);
+            out.flags[k] = make_int2(p, flag_pos);  // (pixel >= 0: the entry is published)
+            __threadfence();
         } else {
             if (out.image) {
                 out.image[p * 3 + 0] = (float)fmin(fmax(C0 + T * (Real)opt.bg[0], (Real)0), (Real)1);
@@ -740,6 +741,9 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
         }
     }
+    // this tile's flags are published: count the CTA (k_fixup_fwd ends when all have)
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&out.ctr->blend_done, 1ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -758,7 +762,7 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                                                    const T* __restrict__ sigma, const RecF* __restrict__ rec,
                                                    const int* __restrict__ tile_start,
                                                    const unsigned* __restrict__ ent_src, FastBlendOut out) {
-    TS_PDL_ENTRY();
+    TS_PDL_LAUNCH_ONLY();
     __shared__ double s_a[FXC];
     __shared__ double s_c[3][FXC];     // colour (training forwards: the fp64 RecC colour)
     __shared__ unsigned s_s[FXC];
@@ -766,15 +770,41 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
     __shared__ short s_idx[FXC];        // render path: passing entries of the chunk, in order
     __shared__ double s_tb[FXC];        // ... and the transmittance in front of each
     __shared__ int s_np, s_used;
+    __shared__ int2 s_flag;
     __shared__ double s_red[3][FX_T / 32];
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // render forwards (no records / fragments / fp64 colour totals): only the
     // transmittance chain is sequential (one lane); weights, colour sums and
     // statistics of the chunk's fragments are computed in parallel
     const bool fastc = out.frec == nullptr && out.frag_tri == nullptr && out.c_total64 == nullptr;
-    const long long nflag = (long long)out.ctr->n_flagged;
-    for (long long k = blockIdx.x; k < nflag; k += gridDim.x) {
-        const int2 f = out.flags[k];
+    // flagged pixel k is published by the blend CTA that stopped on it (pixel >= 0
+    // in flags[k]); the list ends when every blend CTA has finished and entry k is
+    // still empty.  Entries are consumed (reset to -1) for the next frame.
+    const unsigned long long nblend = (unsigned long long)cam.ntx * cam.nty;
+    const long long kcap = (long long)cam.width * cam.height;
+    for (long long k = blockIdx.x; k < kcap; k += gridDim.x) {
+        if (threadIdx.x == 0) {
+            volatile int2* fv = reinterpret_cast<volatile int2*>(out.flags + k);
+            volatile unsigned long long* dv = &out.ctr->blend_done;
+            int2 g;
+            for (long long spin = 0;; spin++) {
+                g.x = fv->x;
+                if (g.x >= 0) break;
+                if (*dv >= nblend) {
+                    __threadfence();
+                    g.x = fv->x;
+                    break;
+                }
+                if (spin > (1ll << 25)) __trap();  // (seconds: the blend never finished -- fail, do not hang)
+                __nanosleep(200);
+            }
+            __threadfence();
+            g.y = fv->y;
+            s_flag = g;
+        }
+        __syncthreads();
+        const int2 f = s_flag;
+        if (f.x < 0) break;
         const int p = f.x, fpos = f.y;
         const int px = p % cam.width, py = p / cam.width;
         const int t = (py / TILE) * cam.ntx + px / TILE;
@@ -969,6 +999,7 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
             out.last_pos[p] = last;
             if (out.n_frag) out.n_frag[p] = cnt;
             if (out.last_src) out.last_src[p] = last >= 0 ? (int)ent_src[last] : -1;
+            out.flags[k] = make_int2(-1, -1);  // consumed
         }
         __syncthreads();
     }

@@ -15,7 +15,8 @@ struct Counters {
     unsigned long long n_flagged;
     unsigned long long n_frec;       // fragment records emitted by the training forward
     unsigned long long frec_over;    // 1: the record buffer overflowed (backward falls back)
-    unsigned long long pad[3];
+    unsigned long long blend_done;   // blend CTAs finished (the fix-up's end-of-flags signal)
+    unsigned long long pad[2];
 };
 
 // One composited fragment of a training forward, in (tile, batch, entry-major)
