@@ -21,13 +21,13 @@
 namespace ts {
 
 #ifndef TS_BWD_MINB
-#define TS_BWD_MINB 3  // CTAs per SM (registers: 80 at 3)
+#define TS_BWD_MINB 4  // CTAs per SM (64 registers, no spills with the shared-memory components; 80 at 3)
 #endif
 #ifndef TS_BWD_SMEMRED
 #define TS_BWD_SMEMRED 1  // run sums through shared memory, one lane per (run, component)
 #endif
 #ifndef TS_BWD_GRID
-#define TS_BWD_GRID 3  // CTAs per SM in the launch (one resident wave: 1.29 -> 1.19 ms at C3 against 8)
+#define TS_BWD_GRID 4  // CTAs per SM in the launch (one resident wave; 4 x 64 registers: 1.13 -> 0.97 ms at C3 against 3 x 80)
 #endif
 
 // Upstream gradients on the fragments' blend weights and depths (render_backward
@@ -83,9 +83,19 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
     // (interleaved 32-record steps: measured faster than one contiguous range per warp)
     for (long long q0 = gw * 32; q0 < n; q0 += nw * 32) {
         const long long q = q0 + lane;
+#if TS_BWD_SMEMRED
+        // the lane's components go straight to its shared-memory column (short
+        // register live ranges)
+        double* gsl = &s_red[wl][0][lane];
+#pragma unroll
+        for (int c = 0; c < NG; c++) gsl[c * 33] = 0.0;
+#define GF(c, v) (gsl[(c) * 33] = (v))
+#else
         double gf[NG];
 #pragma unroll
         for (int c = 0; c < NG; c++) gf[c] = 0.0;
+#define GF(c, v) (gf[c] = (v))
+#endif
         unsigned key = 0xffffffffu - lane;  // unique keys for idle lanes and holes
         bool act = false;
         if (q < n) {
@@ -134,39 +144,39 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 const double s2 = __ldg(c_total + pix * 3 + 2) - tc.w - w * c2;
                 const double d0 = __ldg(d_image + pix * 3 + 0), d1 = __ldg(d_image + pix * 3 + 1),
                              d2 = __ldg(d_image + pix * 3 + 2);
-                gf[8] = w * d0;
-                gf[9] = w * d1;
-                gf[10] = w * d2;
+                GF(8, w * d0);
+                GF(9, w * d1);
+                GF(10, w * d2);
                 double ga = d0 * (tb * c0 - s0 * inv1m) + d1 * (tb * c1 - s1 * inv1m) + d2 * (tb * c2 - s2 * inv1m);
                 if constexpr (FRAG) {
                     const long long fi = __ldg(fg.off + pix) + ids.z;
                     ga += __ldg(fg.dw + fi) * tb - __ldg(fg.sw + fi) * inv1m;
-                    gf[12] = __ldg(fg.dz + fi);
+                    GF(12, __ldg(fg.dz + fi));
                 }
                 if (!clamped) {
                     // (reciprocals of the opacity and of phi_s precomputed per triangle: the
                     // products differ from the quotients by <= 1 ulp)
                     const double inv_o = c2io.y, inv_phis = __ldg(&B.inv_phis);
                     const double window = a * inv_o;
-                    gf[6] = ga * window;  // d/d opacity = g_alpha * alpha / o
+                    GF(6, ga * window);  // d/d opacity = g_alpha * alpha / o
                     const double g_win = o * ga;
                     const double phi = r64 * phis;
                     double g_phi;
                     if (mode == 0) {
-                        gf[7] = g_win * window * log(rc);
+                        GF(7, g_win * window * log(rc));
                         // window / rc = rc^(sigma - 1): 1 for sigma = 1
                         const double g_r = g_win * sg * (sg == 1.0 ? 1.0 : window / rc);
                         if (r64 >= 1.0) {
                             g_phi = 0.0;
                         } else {
                             g_phi = g_r * inv_phis;
-                            gf[11] = -g_r * r64 * inv_phis;
+                            GF(11, -g_r * r64 * inv_phis);
                         }
                     } else {
                         const double E = exp(fmin(phi / sg, 700.0));
                         const double ww = E / ((1.0 + E) * (1.0 + E));
                         const double is = 1.0 / sg;
-                        gf[7] = g_win * ww * phi * is * is;
+                        GF(7, g_win * ww * phi * is * is);
                         g_phi = -g_win * ww * is;
                     }
                     const int ib = edge == 2 ? 0 : edge + 1;
@@ -180,12 +190,12 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                     const double gay = g_phi * (sl * (bx - pxr) + phi * vl);
                     const double gbx = g_phi * (sl * (ay - pyr) - phi * ul);
                     const double gby = g_phi * (sl * (pxr - ax) - phi * vl);
-                    gf[0] = edge == 0 ? gax : (ib == 0 ? gbx : 0.0);
-                    gf[1] = edge == 0 ? gay : (ib == 0 ? gby : 0.0);
-                    gf[2] = edge == 1 ? gax : (ib == 1 ? gbx : 0.0);
-                    gf[3] = edge == 1 ? gay : (ib == 1 ? gby : 0.0);
-                    gf[4] = edge == 2 ? gax : (ib == 2 ? gbx : 0.0);
-                    gf[5] = edge == 2 ? gay : (ib == 2 ? gby : 0.0);
+                    GF(0, edge == 0 ? gax : (ib == 0 ? gbx : 0.0));
+                    GF(1, edge == 0 ? gay : (ib == 0 ? gby : 0.0));
+                    GF(2, edge == 1 ? gax : (ib == 1 ? gbx : 0.0));
+                    GF(3, edge == 1 ? gay : (ib == 1 ? gby : 0.0));
+                    GF(4, edge == 2 ? gax : (ib == 2 ? gbx : 0.0));
+                    GF(5, edge == 2 ? gay : (ib == 2 ? gby : 0.0));
                 }
             }
         }
@@ -199,8 +209,6 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
             // (run, component) items L, L+32, ... and adds each sum with one atomic
             const int nr = __popc(heads);
             const int r = __popc(heads & ((2u << lane) - 1u)) - 1;
-#pragma unroll
-            for (int c = 0; c < NG; c++) s_red[wl][c][lane] = gf[c];
             if (head) {
                 s_run[wl][r] = lane;
                 s_rkey[wl][r] = act ? key : 0xffffffffu;
@@ -242,6 +250,7 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                 if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);  // (component 12 = SG_GZ)
         }
 #endif
+#undef GF
     }
 }
 
