@@ -345,6 +345,9 @@ __global__ void __launch_bounds__(128) k_preprocess_fast64(Cam cam, Opts opt, co
 // (cp.async, double-buffered, SH rows padded to 13 float4 so per-thread row
 // reads are bank-conflict free) while the current block is computed.
 constexpr int PRE_BLK = 128;
+#ifndef TS_PRE_MINB
+#define TS_PRE_MINB 4  // CTAs per SM of the staged preprocess
+#endif
 struct PreStage {
     float4 sh[PRE_BLK * 13];
     float v[PRE_BLK * 9];
@@ -454,10 +457,10 @@ void launch_preprocess_fast(const Cam& cam, const Opts& opt, const ts_soup& soup
         // prefetch: DESIGN.md section 6)
         const int sms = sm_count();
         const int smem = (int)sizeof(PreStage);
-        smem_optin((const void*)k_preprocess_fast32<1, 4, 1>, smem);
+        smem_optin((const void*)k_preprocess_fast32<1, TS_PRE_MINB, 1>, smem);
         const long long nblk = (n + PRE_BLK - 1) / PRE_BLK;
-        const long long grid = std::min<long long>(nblk, (long long)sms * 4);
-        launch_pdl(k_preprocess_fast32<1, 4, 1>, dim3((unsigned)grid), dim3(PRE_BLK), smem, st, cam, opt,
+        const long long grid = std::min<long long>(nblk, (long long)sms * TS_PRE_MINB);
+        launch_pdl(k_preprocess_fast32<1, TS_PRE_MINB, 1>, dim3((unsigned)grid), dim3(PRE_BLK), smem, st, cam, opt,
                    (const float*)soup.vertices, (const float*)soup.opacity, (const float*)soup.sigma,
                    (const float*)soup.sh, n, out);
     }
