@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
     const int hi = sm.hi;
     if (hi < s) return;
 
-    constexpr int NCH = 19;  // 16-byte chunks per entry: RecF 8, RecB 8, RecC 3
+    constexpr int NCH = 15;  // 16-byte chunks per entry: RecF 8, RecB 4, RecC 3
     auto fetch_rec = [&](int p, int q) {  // 16-byte chunk q of (RecF, RecB, RecC) at list position p
         const unsigned src = sm.srcq[p & (SR - 1)];
         const int slot = p & (RR - 1);
@@ -144,12 +144,12 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
         else if (q < 8)
             cp_async16(reinterpret_cast<float4*>(&sm.tail[slot]) + (q - 6),
                        reinterpret_cast<const float4*>(rec + src) + q);
-        else if (q < 16)
+        else if (q < 12)
             cp_async16(reinterpret_cast<float4*>(&sm.rb[slot]) + (q - 8),
                        reinterpret_cast<const float4*>(recb + src) + (q - 8));
         else
-            cp_async16(reinterpret_cast<float4*>(&sm.rc[slot]) + (q - 16),
-                       reinterpret_cast<const float4*>(recc + src) + (q - 16));
+            cp_async16(reinterpret_cast<float4*>(&sm.rc[slot]) + (q - 12),
+                       reinterpret_cast<const float4*>(recc + src) + (q - 12));
     };
     auto rank = [&](int k) {  // composited pairs before pair k
         const int wi = k >> 5;
@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_bwd_dense(Cam cam, Opts opt
                         const int ib = edge == 2 ? 0 : edge + 1;
                         const double ax = rb.q[edge].x, ay = rb.q[edge].y, bx = rb.q[ib].x, by = rb.q[ib].y;
                         const double pxr = (double)(X0 + lx - tr.ox) + 0.5, pyr = (double)(Y0 + ly - tr.oy) + 0.5;
-                        const double sl_ = rb.sl[edge], ul = rb.ul[edge], vl = rb.vl[edge];
+                        double sl_, ul, vl;
+                        rb_edge(rb.q[edge], rb.q[ib], rb.esign, edge, sl_, ul, vl);
                         const double gax = g_phi * (sl_ * (pyr - by) + phi * ul);
                         const double gay = g_phi * (sl_ * (bx - pxr) + phi * vl);
                         const double gbx = g_phi * (sl_ * (ay - pyr) - phi * ul);

@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
                     const unsigned oxy = __ldg(reinterpret_cast<const unsigned*>(&R.ox));  // (ox, oy) shorts
                     const double pxr = (double)(px - (int)(short)(oxy & 0xffffu)) + 0.5;
                     const double pyr = (double)(py - (int)(short)(oxy >> 16)) + 0.5;
-                    const double sl = __ldg(&B.sl[edge]), ul = __ldg(&B.ul[edge]), vl = __ldg(&B.vl[edge]);
+                    double sl, ul, vl;
+                    rb_edge(qa, qb, __ldg(&B.esign), edge, sl, ul, vl);
                     const double gax = g_phi * (sl * (pyr - by) + phi * ul);
                     const double gay = g_phi * (sl * (bx - pxr) + phi * vl);
                     const double gbx = g_phi * (sl * (ay - pyr) - phi * ul);

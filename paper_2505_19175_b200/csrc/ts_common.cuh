@@ -76,16 +76,29 @@ struct __align__(16) RecF {
 };
 static_assert(sizeof(RecF) == 128, "RecF layout");
 
-// Backward-only per-source data (128 B).  Vertices relative to the record
-// origin and, per edge e (q_e -> q_{e+1}), the constants of its endpoint
-// derivative (_kernels.py:296-318) in fp64 -- edge lengths of near-degenerate
-// triangles are ill-conditioned:  sl = s/l,  ul = (b-a)_x/l^2,  vl = (b-a)_y/l^2.
+// Backward-only per-source data (64 B): vertices relative to the record origin,
+// 1 / phi_s and the orientation bits of the edges.  The constants of an edge's
+// endpoint derivative (_kernels.py:296-318) -- sl = s/l, ul = (b-a)_x/l^2,
+// vl = (b-a)_y/l^2 with s the edge's outward sign -- are derived from the
+// vertices where they are used (rb_edge), in fp64: edge lengths of
+// near-degenerate triangles are ill-conditioned.
 struct __align__(16) RecB {
-    double2 q[3];  // (x, y) per vertex (one 16-byte load each)
-    double sl[3], ul[3], vl[3];
+    double2 q[3];     // (x, y) per vertex (one 16-byte load each)
     double inv_phis;  // 1 / phi_s (the backward multiplies instead of dividing)
+    unsigned esign;   // bit e: edge e's normal was flipped (s = -1)
+    unsigned pad;
 };
-static_assert(sizeof(RecB) == 128, "RecB layout");
+static_assert(sizeof(RecB) == 64, "RecB layout");
+
+// the derivative constants of edge e = (a -> b) of a RecB
+__device__ __forceinline__ void rb_edge(double2 a, double2 b, unsigned esign, int e, double& sl, double& ul,
+                                        double& vl) {
+    const double ex = b.x - a.x, ey = b.y - a.y;
+    const double il = rsqrt(ex * ex + ey * ey);
+    sl = ((esign >> e) & 1) ? -il : il;
+    ul = ex * il * il;
+    vl = ey * il * il;
+}
 
 // Training-only per-source fp64 data (48 B): the SH colour before its fp32
 // rounding (clipped, render.py:302) and the exact opacity (1 for solid soups)

@@ -265,16 +265,10 @@ __device__ __forceinline__ bool pre_tri(const Cam& cam, const Opts& opt, long lo
             if (out.recb) {
                 RecB rb;
 #pragma unroll
-                for (int e = 0; e < 3; e++) {
-                    rb.q[e] = make_double2(q[e * 2] - ox, q[e * 2 + 1] - oy);
-                    const int bi = e == 2 ? 0 : e + 1;
-                    const double ex = q[bi * 2] - q[e * 2], ey = q[bi * 2 + 1] - q[e * 2 + 1];
-                    const double il = 1.0 / sqrt(ex * ex + ey * ey);
-                    rb.sl[e] = ((esign >> e) & 1) ? -il : il;
-                    rb.ul[e] = ex * il * il;
-                    rb.vl[e] = ey * il * il;
-                }
+                for (int e = 0; e < 3; e++) rb.q[e] = make_double2(q[e * 2] - ox, q[e * 2 + 1] - oy);
                 rb.inv_phis = 1.0 / phis;
+                rb.esign = (unsigned)esign;
+                rb.pad = 0u;
                 out.recb[i] = rb;
             }
             if (out.recc) {
