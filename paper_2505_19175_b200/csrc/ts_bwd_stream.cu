@@ -41,18 +41,32 @@ struct FragGrads {
     const double* sw;
 };
 
-// sw[i] = sum_{i < k < end(p)} dw[k] w[k] per pixel p, back to front (the
-// reference's running `sw`, _kernels.py:265-268)
+// sw[i] = sum_{i < k < end(p)} dw[k] w[k] per pixel p (the reference's running
+// `sw`, _kernels.py:265-268, back to front).  Warp per pixel: the list is read
+// with coalesced loads from its back end, 32 fragments per step; a suffix sum is
+// the step total minus an inclusive warp scan, plus the sum of the later steps.
 __global__ void __launch_bounds__(256) k_frag_suffix(long long npix, const long long* __restrict__ off,
                                                      const double* __restrict__ w, const double* __restrict__ dw,
                                                      double* __restrict__ sw) {
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = threadIdx.x & 31;
     if (p >= npix) return;
     const long long lo = off[p], hi = off[p + 1];
-    double acc = 0.0;
-    for (long long i = hi - 1; i >= lo; i--) {
-        sw[i] = acc;
-        acc += dw[i] * w[i];
+    double carry = 0.0;  // sum over the fragments after the current step
+    for (long long top = hi; top > lo; top -= 32) {
+        const long long base = top - 32 > lo ? top - 32 : lo;
+        const long long i = base + lane;
+        const bool in = i < top;
+        const double x = in ? dw[i] * w[i] : 0.0;
+        // inclusive scan from the back: lane L gets sum_{L <= j < 32} x_j
+        double v = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_down_sync(0xffffffffu, v, o);
+            if ((int)lane + o < 32) v += y;
+        }
+        if (in) sw[i] = carry + (v - x);
+        carry += __shfl_sync(0xffffffffu, v, 0);
     }
 }
 
@@ -266,7 +280,7 @@ void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const R
         return;
     }
     const long long npix = (long long)cam.width * cam.height;
-    if (npix > 0) k_frag_suffix<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(npix, frag_off, frag_w, fg_dw, sw);
+    if (npix > 0) k_frag_suffix<<<(unsigned)((npix + 7) / 8), 256, 0, st>>>(npix, frag_off, frag_w, fg_dw, sw);
     launch_pdl(k_bwd_stream<true>, grid, dim3(256), 0, st, cam, opt, rec, recb, recc, frec, ctr, cap, c_total, d_image,
                sgrad, FragGrads{frag_off, fg_dw, fg_dz, sw});
 }
