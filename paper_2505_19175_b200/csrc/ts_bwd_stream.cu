@@ -12,8 +12,9 @@
 // so every fragment is independent: one lane per record, r / argmax edge /
 // alpha recomputed in fp64 from the triangle's records (fp64 colour, opacity
 // and sigma from its RecC), the window and edge chain as in k_blend_bwd_dense,
-// an fp64 segmented warp reduction over consecutive records of one triangle and
-// one fp64 atomic per (triangle, component) and warp step.  No tile loop, no
+// per warp step the components in shared memory, one lane per (run of records
+// of one triangle, component) summing its run in fp64 and adding it with one
+// atomic.  No tile loop, no
 // CTA barrier.  If the forward's record buffer overflowed, this kernel does
 // nothing and the tile backward runs instead.
 #include "ts_kernels.cuh"
@@ -22,9 +23,6 @@ namespace ts {
 
 #ifndef TS_BWD_MINB
 #define TS_BWD_MINB 4  // CTAs per SM (64 registers, no spills with the shared-memory components; 80 at 3)
-#endif
-#ifndef TS_BWD_SMEMRED
-#define TS_BWD_SMEMRED 1  // run sums through shared memory, one lane per (run, component)
 #endif
 #ifndef TS_BWD_GRID
 #define TS_BWD_GRID 4  // CTAs per SM in the launch (one resident wave; 4 x 64 registers: 1.13 -> 0.97 ms at C3 against 3 x 80)
@@ -86,30 +84,21 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const int mode = opt.mode;
-#if TS_BWD_SMEMRED
     // per warp: the step's per-record components (component-major, padded) and
     // its runs (first lane, triangle)
     __shared__ double s_red[8][NG][33];
     __shared__ unsigned s_run[8][33];
     __shared__ unsigned s_rkey[8][32];
     const int wl = threadIdx.x >> 5;
-#endif
     // (interleaved 32-record steps: measured faster than one contiguous range per warp)
     for (long long q0 = gw * 32; q0 < n; q0 += nw * 32) {
         const long long q = q0 + lane;
-#if TS_BWD_SMEMRED
         // the lane's components go straight to its shared-memory column (short
-        // register live ranges)
+        // register live ranges: 64 registers, 4 CTAs per SM)
         double* gsl = &s_red[wl][0][lane];
 #pragma unroll
         for (int c = 0; c < NG; c++) gsl[c * 33] = 0.0;
 #define GF(c, v) (gsl[(c) * 33] = (v))
-#else
-        double gf[NG];
-#pragma unroll
-        for (int c = 0; c < NG; c++) gf[c] = 0.0;
-#define GF(c, v) (gf[c] = (v))
-#endif
         unsigned key = 0xffffffffu - lane;  // unique keys for idle lanes and holes
         bool act = false;
         if (q < n) {
@@ -218,7 +207,6 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
         const unsigned kprev = __shfl_up_sync(0xffffffffu, key, 1);
         const bool head = lane == 0 || kprev != key;
         const unsigned heads = __ballot_sync(0xffffffffu, head);
-#if TS_BWD_SMEMRED
         {
             // run r = lanes [s_run[r], s_run[r+1]); lane L sums components of the
             // (run, component) items L, L+32, ... and adds each sum with one atomic
@@ -241,30 +229,6 @@ __global__ void __launch_bounds__(256, TS_BWD_MINB) k_bwd_stream(Cam cam, Opts o
             }
             __syncwarp();
         }
-#else
-        const unsigned later = heads & ~((2u << lane) - 1u);
-        const int runlen = head ? (later ? __ffs(later) - 1 : 32) - (int)lane : 0;
-        const int maxrun = __reduce_max_sync(0xffffffffu, runlen);
-        // run id (a triangle can reappear after another one within a step)
-        const unsigned rid = __popc(heads & ((2u << lane) - 1u));
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            if (off >= maxrun) break;
-            const unsigned ro = __shfl_down_sync(0xffffffffu, rid, off);
-            const bool same = (int)lane + off < 32 && ro == rid;
-#pragma unroll
-            for (int c = 0; c < NG; c++) {
-                const double v = __shfl_down_sync(0xffffffffu, gf[c], off);
-                if (same) gf[c] += v;
-            }
-        }
-        if (act && head) {
-            double* dst = sgrad + (size_t)key * SG_STRIDE;
-#pragma unroll
-            for (int c = 0; c < NG; c++)
-                if (gf[c] != 0.0) atomicAdd(dst + c, gf[c]);  // (component 12 = SG_GZ)
-        }
-#endif
 #undef GF
     }
 }
