@@ -126,6 +126,19 @@ def traffic_for(workload: str, kernel: str):
         return None
 
 
+def issue_roofline(workload: str, blend_ms, clk):
+    """The blend's binding resource is instruction issue, not HBM: its warp-
+    instructions per launch (ncu, profiles/traffic.json) over the event-timed blend
+    against 4 issue slots per SM per clock (148 SMs at the sampled SM clock)."""
+    inst = traffic_for(workload, "k_blend_dense_warp_instructions")
+    if not inst or not blend_ms:
+        return None
+    mhz = (clk or {}).get("sm_mhz") or 1965
+    slots = 148 * 4 * mhz * 1e6 * (blend_ms / 1e3)
+    return {"bound": "issue", "warp_instructions": inst, "issue_slots": slots, "frac": inst / slots,
+            "source": "smsp__inst_executed.sum of the committed ncu capture; blend stage time of this run"}
+
+
 def bench_config(cfg, world: int) -> dict:
     """The ``config`` of both arms (identical dicts: same workload, same sharding)."""
     return {"workload": f"{cfg.name}: {cfg.n} triangles, {cfg.width}x{cfg.height}, sigma={cfg.sigma}, "
@@ -416,7 +429,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "k_blend_dense (+ k_fixup_fwd)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_for(cfg.name, "k_blend_dense"),
-                     "bytes_per_launch": bbytes, "avg_ms": blend_avg, "peak_source": peak_src},
+                     "bytes_per_launch": bbytes, "avg_ms": blend_avg, "peak_source": peak_src,
+                     "issue": issue_roofline(cfg.name, stages.get("blend"), clk)},
         "roofline_bwd": roof_bwd,
         "cpu_baseline": cpu,
         "stages_ms": stages,
