@@ -31,3 +31,31 @@ def test_async_overflow_is_reported_by_the_next_forward():
     r2.status()
     r2.set_async(False)
     assert np.array_equal(f.image.cpu().numpy(), img_ref.cpu().numpy())
+
+
+def test_concurrent_contexts_on_streams():
+    """Frames in flight on three contexts, one stream each (bench.py
+    concurrent_frames): every frame equals the single-context frame."""
+    from paper_2505_19175_b200 import DeviceSoup, Rasterizer, scenes
+    soup = DeviceSoup.from_soup(scenes.make_soup(50_000, seed=3, size=0.05, sigma=(1.0, 1.0)), dtype=torch.float32)
+    intr, pose = scenes.frontal_camera(320, 240, 300.0)
+    poses = scenes.orbit_cameras(6, seed=4)
+    ref = Rasterizer()
+    want = [ref.forward(soup, intr, p, keep_backward=False).image.clone() for p in poses]
+    rs = [Rasterizer() for _ in range(3)]
+    sts = [torch.cuda.Stream() for _ in range(3)]
+    for r, st in zip(rs, sts):  # (sizes the buffers), then asynchronous frames in flight
+        with torch.cuda.stream(st):
+            r.forward(soup, intr, poses[0], keep_backward=False)
+        r.set_async(True)
+    torch.cuda.synchronize()
+    outs = []
+    for i, p in enumerate(poses):
+        with torch.cuda.stream(sts[i % 3]):
+            outs.append(rs[i % 3].forward(soup, intr, p, keep_backward=False).image)
+    torch.cuda.synchronize()
+    for r, st in zip(rs, sts):
+        r.status(stream=st)
+        r.set_async(False)
+    for got, w in zip(outs, want):
+        assert torch.equal(got, w)
