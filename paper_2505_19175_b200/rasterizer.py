@@ -329,6 +329,11 @@ class Rasterizer:
         waiting for the GPU (ForwardResult counts are then -1); status() waits and
         reports the last frame."""
         _lib.check(self.lib.ts_set_async(self._ctx, int(bool(enable))), "set_async")
+        self._async = bool(enable)
+
+    @property
+    def is_async(self) -> bool:
+        return bool(getattr(self, "_async", False))
 
     def status(self, stream=None) -> dict:
         """Wait for the last forward and return its counts; raises on non-finite
@@ -726,25 +731,46 @@ def render(triangles, intr, pose, mode=0, background=(0.0, 0.0, 0.0),
     if ds is None:
         ds = DeviceSoup.from_soup(soup, dtype=_param_dtype(soup))
     t1 = time.perf_counter()
-    fwd = rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
-                       precision=precision)
+
+    def frame_and_outputs(asynchronous: bool):
+        # asynchronous: the frame, the output packing and the copies are enqueued
+        # back to back and the host waits once (ts_forward_status checks the frame)
+        was = rast.is_async
+        rast.set_async(asynchronous)
+        try:
+            f = rast.forward(ds, intr, pose, mode, background, tau_cutoff, tile_size, active_sh_degree,
+                             precision=precision)
+            # the fp64 outputs converted and packed on the device, one copy each for the
+            # fp64 block and the int64 pixel counts into cached page-locked host memory
+            pk = torch.cat([f.image.reshape(-1).double(), f.alpha_map.reshape(-1).double(),
+                            f.max_weight.double(), f.area.double()])
+            pk_h, flat = _PINNED.get(pk.numel(), torch.float64)
+            pk_h.copy_(pk, non_blocking=True)
+            pc_h, pixc = _PINNED.get(f.max_weight.numel(), torch.int64)
+            pc_h.copy_(f.pixel_count.long(), non_blocking=True)
+            if asynchronous:
+                rast.status()  # waits for the frame and the copies; raises like a synchronous forward
+            torch.cuda.current_stream().synchronize()
+            return f, flat, pixc
+        finally:
+            rast.set_async(was)
+
+    if collect_fragments:
+        fwd, flat, pixc = frame_and_outputs(False)
+    else:
+        try:
+            fwd, flat, pixc = frame_and_outputs(True)
+        except RuntimeError:
+            # an asynchronous frame that outgrew the tile-entry buffer (the status
+            # grew it): the synchronous forward redoes it
+            fwd, flat, pixc = frame_and_outputs(False)
     t2 = time.perf_counter()
     frags = rast.fragments().to_fragment_data() if collect_fragments else None
-    # the fp64 outputs converted and packed on the device, one copy each for the
-    # fp64 block and the int64 pixel counts into cached page-locked host memory
     h, w = fwd.alpha_map.shape
     n = fwd.max_weight.numel()
-    packed = torch.cat([fwd.image.reshape(-1).double(), fwd.alpha_map.reshape(-1).double(),
-                        fwd.max_weight.double(), fwd.area.double()])
-    pk_h, flat = _PINNED.get(packed.numel(), torch.float64)
-    pk_h.copy_(packed, non_blocking=True)
-    pc_h, pixc = _PINNED.get(n, torch.int64)
-    pc_h.copy_(fwd.pixel_count.long(), non_blocking=True)
-    torch.cuda.current_stream().synchronize()
     o1, o2, o3 = h * w * 3, h * w * 4, h * w * 4 + n
     image, alpha = flat[:o1].reshape(h, w, 3), flat[o1:o2].reshape(h, w)
     maxw, area = flat[o2:o3], flat[o3:o3 + n]
-    del pk_h, pc_h
     t3 = time.perf_counter()
     LAST_RENDER_D2H_BYTES = image.nbytes + alpha.nbytes + maxw.nbytes + pixc.nbytes + area.nbytes
     if frags is not None:
