@@ -96,8 +96,7 @@ struct DenseSmem {
     unsigned ein[DB];              // per entry: inclusive (pairs<<16 | segments) within its warp
     __align__(16) unsigned wtot[8];  // per warp: (pairs<<16 | segments) of its 8 entries
     int total;                     // pairs of the batch
-    unsigned pbits[ACC64 ? PCAP / 32 : 1];      // training: pair k passes (record slots)
-    int wpre[ACC64 ? PCAP / 32 + 1 : 1];        // passing pairs before word w
+    unsigned pbits[ACC64 ? PCAP / 32 : 1];      // training: pair k passes (the others' record slots are holes)
     unsigned long long rbase;                   // first record of the batch (~0: none)
     unsigned maxw[DB];
     int pix[DB];
@@ -333,6 +332,12 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
         }
         // ---- 2. evaluate: warp w takes a contiguous range of pairs, 32 consecutive
         //         pairs per step (lane-uniform control flow, broadcast record loads) ----
+        // training records: one slot per pair of the batch (record of pair k at
+        // rbase + k; pairs that fail the test -- ~0.1 % -- become holes), reserved
+        // here so the atomic's round trip overlaps the evaluation
+        unsigned long long rb_res = 0;
+        if constexpr (ACC64)
+            if (out.frec && tid == 0) rb_res = atomicAdd(&out.ctr->n_frec, (unsigned long long)sm.total);
         {
             const int total = sm.total;
             const int chunk = ((total + 255) >> 8) << 5;
@@ -393,37 +398,31 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 }
             }
         }
+        if constexpr (ACC64) {
+            if (out.frec && tid == 0) {
+                unsigned long long base = rb_res;
+                if (base + (unsigned long long)sm.total > out.frec_cap) {
+                    out.ctr->frec_over = 1ull;
+                    base = ~0ull;
+                }
+                sm.rbase = base;
+            }
+        }
         __syncthreads();
         if (tid < PCAP / 32) sm.starts[tid] = 0u;  // for the next batch (read by the evaluation only)
         if constexpr (ACC64) {
-            // record slots of the batch: passing pairs in entry-major order
-            if (out.frec) {
-                if (warp == 0) {
-                    const int total = sm.total;
-                    const int nwd = (total + 31) >> 5;
-                    int carry = 0;
-                    for (int w0 = 0; w0 < nwd; w0 += 32) {
-                        const int wi = w0 + (int)lane;
-                        const int c = wi < nwd ? __popc(sm.pbits[wi]) : 0;
-                        int incl = c;
-#pragma unroll
-                        for (int off = 1; off < 32; off <<= 1) {
-                            const int y = __shfl_up_sync(0xffffffffu, incl, off);
-                            if ((int)lane >= off) incl += y;
-                        }
-                        if (wi < nwd) sm.wpre[wi] = incl - c + carry;
-                        carry += __shfl_sync(0xffffffffu, incl, 31);
-                    }
-                    if (lane == 0) {
-                        unsigned long long base = atomicAdd(&out.ctr->n_frec, (unsigned long long)carry);
-                        if (base + carry > out.frec_cap) {
-                            out.ctr->frec_over = 1ull;
-                            base = ~0ull;
-                        }
-                        sm.rbase = base;
+            // the slots of pairs that failed the contribution test are holes
+            if (out.frec && sm.rbase != ~0ull) {
+                const int total = sm.total;
+                for (int wi = tid; wi < ((total + 31) >> 5); wi += 256) {
+                    const int nv = min(32, total - 32 * wi);
+                    unsigned miss = ~sm.pbits[wi] & (nv == 32 ? 0xffffffffu : ((1u << nv) - 1u));
+                    while (miss) {
+                        const int k = 32 * wi + __ffs(miss) - 1;
+                        miss &= miss - 1;
+                        out.frec[sm.rbase + k].pix = ~0u;
                     }
                 }
-                __syncthreads();
             }
         }
         // ---- 3. composite: thread = pixel, passing entries in depth order ----
@@ -439,7 +438,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                 const int j = __ffsll((long long)hm) - 1;
                 hm &= hm - 1;
                 const int kh = sm.rowtab[j][ly] + lx;
-                const int slot = sm.wpre[kh >> 5] + __popc(sm.pbits[kh >> 5] & ((1u << (kh & 31)) - 1u));
+                const int slot = kh;
                 TS_ASSERT(kh >= 0 && kh < sm.total && rb + slot < out.frec_cap);
                 out.frec[rb + slot].pix = ~0u;
             }
@@ -541,7 +540,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
                         }
                         if (rb != ~0ull) {
                             const int kr = kp;
-                            const int slot = sm.wpre[kr >> 5] + __popc(sm.pbits[kr >> 5] & ((1u << (kr & 31)) - 1u));
+                            const int slot = kr;
                             TS_ASSERT(rb + slot < out.frec_cap);
                             double4* fr = reinterpret_cast<double4*>(out.frec + rb + slot);
                             fr[0] = make_double4((double)T, (double)C0, (double)C1, (double)C2);
