@@ -75,6 +75,7 @@ struct ts_context {
     unsigned *tscr0 = nullptr, *tscr1 = nullptr;  // tile-sort scratch (tiles longer than shared memory)
     unsigned* tcnt = nullptr;                      // per-tile entry counts
     int* big_list = nullptr;                       // tiles for the long-tile sort, count at [ntiles]
+    int* tile_order = nullptr;                     // blend order of the tiles (longest first)
     uint2* bucket = nullptr;                       // (reduced depth key, source) of every tile entry, unsorted
     DevBuf binmat;                                 // chunk x tile count matrix of the binning
     DevBuf lossbuf;                                // photometric loss scratch
@@ -241,7 +242,8 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
         return o;
     };
     size_t o_tf = take(8 * cp), o_t32 = take(4 * cp), o_lp = take(4 * cp), o_fg = take(8 * cp),
-           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp), o_tc = take(4 * (ct + 1)), o_bl = take(4 * (ct + 1));
+           o_ts = take(4 * (ct + 1)), o_nf = take(4 * cp), o_tc = take(4 * (ct + 1)), o_bl = take(4 * (ct + 1)),
+           o_or = take(4 * (ct + 1));
     TS_CHECK(cudaMalloc(&c->pix_buf, off));
     c->pix_bytes = off;
     char* b = (char*)c->pix_buf;
@@ -253,6 +255,7 @@ static int ensure_pix(ts_context* c, long long p, long long ntiles) {
     c->nfrag = (int*)(b + o_nf);
     c->tcnt = (unsigned*)(b + o_tc);
     c->big_list = (int*)(b + o_bl);
+    c->tile_order = (int*)(b + o_or);
     // flagged-pixel list entries start empty (pixel -1); the fix-up empties each
     // entry it consumes, so the list is clean for the next frame
     TS_CHECK(cudaMemset(c->flags, 0xff, 8 * (size_t)cp));
@@ -449,10 +452,12 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
     // (the sort grids follow it); more entries raise the sticky overflow flag
     const long long wcap = c->e_hint > 0 ? std::min<long long>(c->cap_e, c->e_hint + c->e_hint / 4 + 4096)
                                          : c->cap_e;
+    const int* order = nullptr;  // blend order of the tiles (tile-first binning only)
     if (n > 0 && !c->opt_legacy_binning && ntiles <= bin_max_tiles()) {
         stage_begin(c, TS_STAGE_BINNING, st);
         bin_tiles_fill(n, c->bbox, c->key, cm.ntx, ntiles, c->tcnt, (unsigned*)c->binmat.p, c->tile_start,
-                       c->bucket, c->d_ctr, wcap, c->d_sticky, c->big_list, st);
+                       c->bucket, c->d_ctr, wcap, c->d_sticky, c->big_list, st, c->tile_order);
+        order = c->tile_order;
         stage_end(c, TS_STAGE_BINNING, st);
         stage_begin(c, TS_STAGE_DEPTH_SORT, st);
         unsigned* const scr[4] = {c->tkey_alt, c->tval_alt, c->tscr0, c->tscr1};
@@ -491,6 +496,7 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
         FastBlendOut bo{out->image, out->alpha_map, out->max_weight, out->pixel_count, out->last_src,
                         c->nfrag, c->t_final32, opt->keep_backward ? c->t_final : nullptr, c->last_pos,
                         c->flags, c->d_ctr};
+        bo.tile_order = order;
         if (opt->keep_backward) {
             bo.recc = (const RecC*)c->recc.p;
             if (!c->opt_tile_backward && c->frec.p) {

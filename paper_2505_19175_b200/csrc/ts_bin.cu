@@ -115,6 +115,32 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __rest
     }
 }
 
+// Blend order of the tiles: longest lists first (16 classes by log2 of the entry
+// count, any order within a class), so the frame's tail is not a long tile that
+// happened to come last.  One CTA; the blend reads order[blockIdx.x].
+__global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_start,
+                                                     int* __restrict__ order) {
+    TS_PDL_ENTRY();
+    __shared__ int s_cnt[16], s_cur[16];
+    if (threadIdx.x < 16) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    auto cls = [&](int t) {
+        const int c = tile_start[t + 1] - tile_start[t];
+        return 15 - min(15, 31 - __clz(c + 1));  // heavier -> lower class
+    };
+    for (int t = threadIdx.x; t < ntiles; t += 1024) atomicAdd(&s_cnt[cls(t)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int k = 0; k < 16; k++) {
+            s_cur[k] = run;
+            run += s_cnt[k];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += 1024) order[atomicAdd(&s_cur[cls(t)], 1)] = t;
+}
+
 // ---------------------------------------------------------------------------
 // Two-level counting (chunk x tile matrix): no contended global atomics.
 constexpr int BIN_CT = 1024;               // threads per chunk CTA
@@ -607,7 +633,7 @@ constexpr int SORT_SMALL = 2048, SORT_BIG = 8192;
 
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
                     unsigned* tcnt, unsigned* mat, int* tile_start, uint2* bucket, const Counters* ctr,
-                    long long cap, unsigned* overflow, int* big_list, cudaStream_t st) {
+                    long long cap, unsigned* overflow, int* big_list, cudaStream_t st, int* tile_order) {
     const int nchunk = (int)((n + BIN_CHUNK - 1) / BIN_CHUNK);
     const int nrange = (ntiles + BIN_MAX_TILES - 1) / BIN_MAX_TILES;  // tile ranges (grid y)
     const int smem = (nrange > 1 ? BIN_MAX_TILES : ntiles) * (int)sizeof(unsigned);
@@ -622,6 +648,7 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
     // big_list[ntiles]: tiles longer than SORT_SMALL; its count at big_list[ntiles]
     launch_pdl(k_tile_scan, dim3(1), dim3(1024), 0, st, ntiles, tcnt, tile_start, cap, overflow, SORT_SMALL, big_list,
                                     big_list + ntiles);
+    if (tile_order) launch_pdl(k_tile_order, dim3(1), dim3(1024), 0, st, ntiles, (const int*)tile_start, tile_order);
     if (n > 0)
         launch_pdl(k_bin_fill, dim3(nchunk, nrange), dim3(BIN_CT), smem, st, n, bbox, ntx, ntiles, mat, tile_start, key64, ctr,
                                                               bucket);

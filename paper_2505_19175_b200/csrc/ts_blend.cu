@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
 
     const int tid = threadIdx.x;
     const unsigned lane = tid & 31, warp = tid >> 5;
-    const int t = blockIdx.x;
+    const int t = out.tile_order ? __ldg(out.tile_order + blockIdx.x) : (int)blockIdx.x;
     const int tx = t % cam.ntx, ty = t / cam.ntx;
     const int X0 = tx * TILE, Y0 = ty * TILE;
     const int lx = tid & 15, ly = tid >> 4;

@@ -80,6 +80,7 @@ struct FastBlendOut {
     unsigned long long frec_cap;
     double* c_total64;         // (P,3) unclipped colour incl. T_final * background
     const RecC* recc;          // training forwards: fp64 colours of the sources
+    const int* tile_order;     // blend order of the tiles (longest first), null = tile id order
 };
 
 struct BlendOut {
@@ -262,7 +263,7 @@ void launch_photometric_loss(const float* x, const float* y, int H, int W, doubl
 // bucket: one (32-bit range-reduced depth key, source) record per tile entry.
 void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* key64, int ntx, int ntiles,
                     unsigned* tcnt, unsigned* mat, int* tile_start, uint2* bucket, const Counters* ctr,
-                    long long cap, unsigned* overflow, int* big_list, cudaStream_t st);
+                    long long cap, unsigned* overflow, int* big_list, cudaStream_t st, int* tile_order = nullptr);
 size_t bin_matrix_bytes(long long n, int ntiles);
 int bin_max_tiles();
 void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
