@@ -61,14 +61,24 @@ __device__ __forceinline__ unsigned excl_scan_256(unsigned v, unsigned* s_w, uns
 }
 }  // namespace
 
+// tile blend-order class: longest lists first, two classes per octave of the length
+__device__ __forceinline__ int tile_class(unsigned c) {
+    const int l = 31 - __clz(c + 1);                               // floor(log2(c + 1))
+    const int h = l > 0 ? (int)(((c + 1) >> (l - 1)) & 1u) : 0;    // upper half of the octave
+    return 63 - min(63, 2 * l + h);
+}
+
 __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __restrict__ tcnt, int* __restrict__ tile_start,
                                                     long long cap, unsigned* overflow, int small_cap,
-                                                    int* __restrict__ big_list, int* __restrict__ n_big) {
+                                                    int* __restrict__ big_list, int* __restrict__ n_big,
+                                                    int* __restrict__ order) {
     TS_PDL_ENTRY();
     __shared__ unsigned s_w[32];
     __shared__ unsigned long long s_total;
     __shared__ int s_nbig;
+    __shared__ int s_ccnt[64];
     if (threadIdx.x == 0) s_nbig = 0;
+    if (threadIdx.x < 64) s_ccnt[threadIdx.x] = 0;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long carry = 0;
     for (int b0 = 0; b0 < ntiles; b0 += 1024) {
@@ -96,6 +106,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __rest
         if (i < ntiles) {
             tile_start[i] = (int)ex;
             if ((int)v > small_cap) big_list[atomicAdd(&s_nbig, 1)] = i;  // long tiles, any order
+            if (order) atomicAdd(&s_ccnt[tile_class(v)], 1);
         }
         carry += s_w[31];
         __syncthreads();
@@ -113,32 +124,21 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int ntiles, unsigned* __rest
         tile_start[ntiles] = (int)s_total;
         *n_big = s_nbig;
     }
-}
-
-// Blend order of the tiles: longest lists first (16 classes by log2 of the entry
-// count, any order within a class), so the frame's tail is not a long tile that
-// happened to come last.  One CTA; the blend reads order[blockIdx.x].
-__global__ void __launch_bounds__(1024) k_tile_order(int ntiles, const int* __restrict__ tile_start,
-                                                     int* __restrict__ order) {
-    TS_PDL_ENTRY();
-    __shared__ int s_cnt[16], s_cur[16];
-    if (threadIdx.x < 16) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
-    auto cls = [&](int t) {
-        const int c = tile_start[t + 1] - tile_start[t];
-        return 15 - min(15, 31 - __clz(c + 1));  // heavier -> lower class
-    };
-    for (int t = threadIdx.x; t < ntiles; t += 1024) atomicAdd(&s_cnt[cls(t)], 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int k = 0; k < 16; k++) {
-            s_cur[k] = run;
-            run += s_cnt[k];
+    if (order) {
+        // blend order of the tiles: longest lists first (any order within a class),
+        // so the frame's tail is not a long tile that happened to come last
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int k = 0; k < 64; k++) {
+                const int c = s_ccnt[k];
+                s_ccnt[k] = run;
+                run += c;
+            }
         }
+        __syncthreads();
+        for (int t = threadIdx.x; t < ntiles; t += 1024) order[atomicAdd(&s_ccnt[tile_class(tcnt[t])], 1)] = t;
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < ntiles; t += 1024) order[atomicAdd(&s_cur[cls(t)], 1)] = t;
 }
 
 // ---------------------------------------------------------------------------
@@ -647,8 +647,7 @@ void bin_tiles_fill(long long n, const short4* bbox, const unsigned long long* k
     }
     // big_list[ntiles]: tiles longer than SORT_SMALL; its count at big_list[ntiles]
     launch_pdl(k_tile_scan, dim3(1), dim3(1024), 0, st, ntiles, tcnt, tile_start, cap, overflow, SORT_SMALL, big_list,
-                                    big_list + ntiles);
-    if (tile_order) launch_pdl(k_tile_order, dim3(1), dim3(1024), 0, st, ntiles, (const int*)tile_start, tile_order);
+                                    big_list + ntiles, tile_order);
     if (n > 0)
         launch_pdl(k_bin_fill, dim3(nchunk, nrange), dim3(BIN_CT), smem, st, n, bbox, ntx, ntiles, mat, tile_start, key64, ctr,
                                                               bucket);
