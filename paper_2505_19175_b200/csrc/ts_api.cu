@@ -461,7 +461,7 @@ static int enqueue_tail(ts_context* c, const Cam& cm, const Opts& op, const ts_o
         stage_end(c, TS_STAGE_BINNING, st);
         stage_begin(c, TS_STAGE_DEPTH_SORT, st);
         unsigned* const scr[4] = {c->tkey_alt, c->tval_alt, c->tscr0, c->tscr1};
-        bin_tiles_sort(n, ntiles, c->tile_start, c->bucket, c->key, c->tval, scr, c->big_list, st);
+        bin_tiles_sort(n, ntiles, c->tile_start, c->bucket, c->key, c->tval, scr, c->big_list, st, c->tile_order);
         stage_end(c, TS_STAGE_DEPTH_SORT, st);
         c->ent_src = c->tval;
         c->sorted_src = c->vals_c;

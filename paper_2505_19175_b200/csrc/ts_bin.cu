@@ -410,7 +410,8 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
                                                   const uint2* __restrict__ bucket,
                                                   const unsigned long long* __restrict__ key64,
                                                   unsigned* __restrict__ ent_src, unsigned* gk0, unsigned* gv0,
-                                                  unsigned* gk1, unsigned* gv1, int srcbits) {
+                                                  unsigned* gk1, unsigned* gv1, int srcbits,
+                                                  const int* __restrict__ order) {
     constexpr int IPT = CAP / BT;
     __shared__ unsigned long long s_item[CAP];   // reduced key << 32 | src
     __shared__ unsigned s_hist[NB];
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(BT) k_tile_sort(int ntiles, const int* __restr
     __shared__ int s_flag;
     // the long-tile kernel (independent tiles) may launch while this grid drains
     TS_PDL_ENTRY();
-    const int t = blockIdx.x;
+    const int t = order ? order[blockIdx.x] : (int)blockIdx.x;  // (longest lists first)
     const int base = tile_start[t], cnt = tile_start[t + 1] - base;
     if (cnt <= 0 || cnt > CAP) return;  // (longer tiles: k_tile_sort_big)
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -662,10 +663,10 @@ int bin_max_tiles() { return 1 << 22; }  // (any view: larger tile counts use se
 
 void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
                     const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],
-                    const int* big_list, cudaStream_t st) {
+                    const int* big_list, cudaStream_t st, const int* tile_order) {
     const int srcbits = n > 1 ? 64 - __builtin_clzll((unsigned long long)(n - 1)) : 1;
     launch_pdl(k_tile_sort<SORT_SMALL, 2048>, dim3(ntiles), dim3(BT), 0, st, ntiles, tile_start, bucket, key64, ent_src, scratch[0],
-                                                        scratch[1], scratch[2], scratch[3], srcbits);
+                                                        scratch[1], scratch[2], scratch[3], srcbits, tile_order);
     // tiles above SORT_SMALL entries (dense views), listed by k_tile_scan
     const int sms = sm_count();
     const int smem = SORT_BIG * (int)sizeof(unsigned long long);

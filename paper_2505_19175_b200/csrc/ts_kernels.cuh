@@ -268,7 +268,7 @@ size_t bin_matrix_bytes(long long n, int ntiles);
 int bin_max_tiles();
 void bin_tiles_sort(long long n, int ntiles, const int* tile_start, const uint2* bucket,
                     const unsigned long long* key64, unsigned* ent_src, unsigned* const scratch[4],
-                    const int* big_list, cudaStream_t st);
+                    const int* big_list, cudaStream_t st, const int* tile_order = nullptr);
 // count = min(cap, *dcount), read on the device
 int onesweep_sort_u32_dev(long long cap, const unsigned long long* dcount, unsigned* keys, unsigned* vals,
                           unsigned* keys_alt, unsigned* vals_alt, int nbits, void* scratch, cudaStream_t st);
