@@ -59,3 +59,37 @@ def test_concurrent_contexts_on_streams():
         r.set_async(False)
     for got, w in zip(outs, want):
         assert torch.equal(got, w)
+
+
+def test_forward_captured_in_cuda_graph():
+    """An asynchronous forward captured in a CUDA graph (stream capture of the
+    whole frame: counter reset, preprocess, binning, sort, blend, fix-up) replays
+    to the eager frame; the same soup buffers updated in place render anew."""
+    from paper_2505_19175_b200 import DeviceSoup, Rasterizer, scenes
+    soup = DeviceSoup.from_soup(scenes.make_soup(50_000, seed=3, size=0.05, sigma=(1.0, 1.0)), dtype=torch.float32)
+    intr, pose = scenes.frontal_camera(320, 240, 300.0)
+    r = Rasterizer()
+    want = r.forward(soup, intr, pose, keep_backward=False).image.clone()
+    r.set_async(True)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            r.forward(soup, intr, pose, keep_backward=False)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = r.forward(soup, intr, pose, keep_backward=False)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.image, want)
+    # parameters changed in place: the replay renders the new values
+    soup.sh.mul_(0.5)
+    g.replay()
+    torch.cuda.synchronize()
+    r.status()
+    r.set_async(False)
+    want2 = Rasterizer().forward(soup, intr, pose, keep_backward=False).image
+    assert torch.equal(out.image, want2) and not torch.equal(want2, want)
