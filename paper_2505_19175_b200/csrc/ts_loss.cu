@@ -316,6 +316,41 @@ __global__ void __launch_bounds__(256) k_distortion(long long npix, const long l
                 if (d_w) d_w[lo] = 0.0;
                 if (d_z) d_z[lo] = 0.0;
             }
+        } else if (hi - lo <= 32) {
+            // one step (most pixels): the fragment stays in registers for both passes
+            const long long k = lo + lane;
+            const bool in = k < hi;
+            const double wk = in ? w[k] : 0.0, zk = in ? z[k] : 0.0;
+            const double zp = __shfl_up_sync(0xffffffffu, zk, 1);
+            const bool sorted = __all_sync(0xffffffffu, !(in && k > lo && zk < zp));
+            const double tw = warp_sum(wk), ts = warp_sum(wk * zk);
+            if (sorted) {
+                const double iw = warp_incl_scan(wk, lane), is = warp_incl_scan(wk * zk, lane);
+                const double wb = iw - wk, sb = is - wk * zk;
+                if (in) {
+                    const double wa = tw - wb - wk, sa = ts - sb - wk * zk;
+                    const double fwd = zk * wb - sb;
+                    tot += wk * fwd;
+                    if (d_w) d_w[k] = 2.0 * (fwd + (sa - zk * wa)) * scale;
+                    if (d_z) d_z[k] = 2.0 * wk * (wb - wa) * scale;
+                }
+                tot *= 2.0;
+            } else {  // pairwise (_distortion_pairwise :153-166)
+                double gw_ = 0.0, gz = 0.0;
+                for (int j = 0; j < (int)(hi - lo); j++) {
+                    const double zj = __shfl_sync(0xffffffffu, zk, j), wj = __shfl_sync(0xffffffffu, wk, j);
+                    const double dz = zk - zj;
+                    tot += wk * fabs(dz) * wj;
+                    gw_ += fabs(dz) * wj;
+                    gz += (double)((dz > 0.0) - (dz < 0.0)) * wj;
+                }
+                if (in) {
+                    if (d_w) d_w[k] = 2.0 * gw_ * scale;
+                    if (d_z) d_z[k] = 2.0 * gz * wk * scale;
+                } else {
+                    tot = 0.0;
+                }
+            }
         } else {
             double tw = 0.0, ts = 0.0;
             bool sorted = true;
