@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
         const int navail = min(DB, e - b);
         if (tid < pnb) {  // per-entry statistics of the previous batch (complete since the barrier)
             const unsigned src = sm.srcq[(pb + tid) & (SR - 1)];
-            if (sm.maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, sm.maxw[tid]);
-            if (sm.pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, sm.pix[tid]);
+            if (sm.maxw[tid] && out.max_weight) red_gmax_u32((unsigned*)out.max_weight + src, sm.maxw[tid]);
+            if (sm.pix[tid] && out.pixel_count) red_gadd_s32(out.pixel_count + src, sm.pix[tid]);
             sm.maxw[tid] = 0u;
             sm.pix[tid] = 0;
         }
@@ -600,8 +600,8 @@ __global__ void __launch_bounds__(256, MINB) k_blend_dense(Cam cam, Opts opt, co
     __syncthreads();
     if (tid < pnb) {
         const unsigned src = sm.srcq[(pb + tid) & (SR - 1)];
-        if (sm.maxw[tid] && out.max_weight) atomicMax((unsigned*)out.max_weight + src, sm.maxw[tid]);
-        if (sm.pix[tid] && out.pixel_count) atomicAdd(out.pixel_count + src, sm.pix[tid]);
+        if (sm.maxw[tid] && out.max_weight) red_gmax_u32((unsigned*)out.max_weight + src, sm.maxw[tid]);
+        if (sm.pix[tid] && out.pixel_count) red_gadd_s32(out.pixel_count + src, sm.pix[tid]);
     }
     cp_async_wait_all();
     if (inside) {

@@ -397,6 +397,14 @@ __device__ __forceinline__ float fast_ex2(float x) {
     return y;
 }
 
+// fire-and-forget global reductions (RED: no value returns to a register)
+__device__ __forceinline__ void red_gmax_u32(unsigned* a, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.max.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_gadd_s32(int* a, int v) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
 // asynchronous global -> shared copies (LDGSTS)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
