@@ -712,8 +712,8 @@ __global__ void __launch_bounds__(256) k_blend_fast(Cam cam, Opts opt, const Rec
         if (threadIdx.x < nb) {
             const unsigned src = s_src[threadIdx.x];
             if (s_maxw[threadIdx.x] && out.max_weight)
-                atomicMax((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
-            if (s_pix[threadIdx.x] && out.pixel_count) atomicAdd(out.pixel_count + src, s_pix[threadIdx.x]);
+                red_gmax_u32((unsigned*)out.max_weight + src, s_maxw[threadIdx.x]);
+            if (s_pix[threadIdx.x] && out.pixel_count) red_gadd_s32(out.pixel_count + src, s_pix[threadIdx.x]);
             s_maxw[threadIdx.x] = 0u;
             s_pix[threadIdx.x] = 0;
         }
@@ -894,8 +894,8 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                     c1 += w * s_c[1][j];
                     c2 += w * s_c[2][j];
                     if (base + j >= fpos) {
-                        if (out.max_weight) atomicMax((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
-                        if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + s_s[j], 1);
+                        if (out.max_weight) red_gmax_u32((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
+                        if (w > opt.tau_contrib && out.pixel_count) red_gadd_s32(out.pixel_count + s_s[j], 1);
                     }
                 }
 #pragma unroll
@@ -962,8 +962,8 @@ __global__ void __launch_bounds__(FX_T, 2) k_fixup_fwd(Cam cam, Opts opt, const 
                             out.frag_z[fi] = __longlong_as_double((long long)out.zkey[s_s[j]]);
                         }
                         if (lane == 0 && posj >= fpos) {
-                            if (out.max_weight) atomicMax((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
-                            if (w > opt.tau_contrib && out.pixel_count) atomicAdd(out.pixel_count + s_s[j], 1);
+                            if (out.max_weight) red_gmax_u32((unsigned*)out.max_weight + s_s[j], __float_as_uint((float)w));
+                            if (w > opt.tau_contrib && out.pixel_count) red_gadd_s32(out.pixel_count + s_s[j], 1);
                         }
                         last = posj;
                         cnt++;
