@@ -366,8 +366,10 @@ __global__ void __launch_bounds__(CB, TS_CHAIN_MULTI_MINB) k_chain_multi32(Chain
 #pragma unroll
         for (int k = 0; k < 9; k++) dv[k] = 0.0;
         double dop = 0.0, dsig = 0.0;
+        unsigned vis = 0u;  // the views that kept the triangle: all flags in flight at once
+        for (int w = 0; w < cv.n; w++) vis |= (__ldg(cv.flag[w] + i) != 0u ? 1u : 0u) << w;
         for (int w = 0; w < cv.n; w++) {
-            if (!__ldg(cv.flag[w] + i)) continue;
+            if (!((vis >> w) & 1u)) continue;
             const double2* row = reinterpret_cast<const double2*>(cv.sgrad[w] + (size_t)i * SG_STRIDE);
             double sg[14];
 #pragma unroll
