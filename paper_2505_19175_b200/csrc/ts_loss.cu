@@ -512,18 +512,40 @@ __global__ void __launch_bounds__(256) k_normal_frag(long long npix, const long 
     double sum = 0.0;
     if (p < npix) {
         const double m0 = nmap[p * 3 + 0], m1 = nmap[p * 3 + 1], m2 = nmap[p * 3 + 2];
-        for (long long k = off[p]; k < off[p + 1]; k++) {
-            const long long t = ftri[k];
-            const double* o = tri + t * 8;
-            const double c0 = o[0], c1 = o[1], c2 = o[2], cn = o[3], fl = o[4];
-            const double cm = c0 * m0 + c1 * m1 + c2 * m2;
-            const double dot = cm * fl;
-            sum += w[k] * (1.0 - dot);
-            if (d_w) d_w[k] = (1.0 - dot) * inv_nf;
-            const double coef = -w[k] * fl * inv_nf / cn;
-            atomicAdd(gc + t * 3 + 0, coef * (m0 - c0 * cm));
-            atomicAdd(gc + t * 3 + 1, coef * (m1 - c1 * cm));
-            atomicAdd(gc + t * 3 + 2, coef * (m2 - c2 * cm));
+        const long long k0 = off[p], k1 = off[p + 1];
+        // four fragments per step: their source ids and triangle rows are all in
+        // flight at once (the gathers, not the arithmetic, bound this loop)
+        constexpr int U = 4;
+        for (long long kb = k0; kb < k1; kb += U) {
+            long long t[U];
+            double wk[U], c[U][5];
+#pragma unroll
+            for (int u = 0; u < U; u++) t[u] = kb + u < k1 ? (long long)ftri[kb + u] : -1;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                wk[u] = 0.0;
+                if (t[u] >= 0) {
+                    const double* o = tri + t[u] * 8;
+                    const double2 a = *reinterpret_cast<const double2*>(o);
+                    const double2 b = *reinterpret_cast<const double2*>(o + 2);
+                    c[u][0] = a.x; c[u][1] = a.y; c[u][2] = b.x; c[u][3] = b.y; c[u][4] = o[4];
+                    wk[u] = w[kb + u];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (t[u] < 0) continue;
+                const long long k = kb + u;
+                const double c0 = c[u][0], c1 = c[u][1], c2 = c[u][2], cn = c[u][3], fl = c[u][4];
+                const double cm = c0 * m0 + c1 * m1 + c2 * m2;
+                const double dot = cm * fl;
+                sum += wk[u] * (1.0 - dot);
+                if (d_w) d_w[k] = (1.0 - dot) * inv_nf;
+                const double coef = -wk[u] * fl * inv_nf / cn;
+                atomicAdd(gc + t[u] * 3 + 0, coef * (m0 - c0 * cm));
+                atomicAdd(gc + t[u] * 3 + 1, coef * (m1 - c1 * cm));
+                atomicAdd(gc + t[u] * 3 + 2, coef * (m2 - c2 * cm));
+            }
         }
     }
     const double s = block_sum_256(sum, s_red);
