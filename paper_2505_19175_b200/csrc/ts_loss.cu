@@ -440,6 +440,9 @@ __global__ void __launch_bounds__(256) k_fragment_depth(long long npix, const lo
 //                      weight gradient, and dL/dc per triangle (fp64 atomics);
 //   k_normal_chain  -- per triangle: the cross-product chain into d_vertices.
 // ---------------------------------------------------------------------------
+#ifndef TS_NORMAL_U
+#define TS_NORMAL_U 4  // fragments per step of k_normal_frag
+#endif
 struct NCam {
     double fx, fy, cx, cy, R[9], t[3];
 };
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(256) k_normal_frag(long long npix, const long 
         const long long k0 = off[p], k1 = off[p + 1];
         // four fragments per step: their source ids and triangle rows are all in
         // flight at once (the gathers, not the arithmetic, bound this loop)
-        constexpr int U = 4;
+        constexpr int U = TS_NORMAL_U;
         for (long long kb = k0; kb < k1; kb += U) {
             long long t[U];
             double wk[U], c[U][5];
