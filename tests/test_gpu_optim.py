@@ -119,3 +119,30 @@ def test_unchecked_step_skips_and_keeps_the_step_count():
     adam_step(soup, g, st, unit(), check=False)
     adam_step(soup, g, st, unit(), check=False)
     assert st.t == 2 and not torch.equal(v0, soup.vertices)
+
+
+def test_quad_path_equals_element_path():
+    """n % 4 == 0 takes the 16-byte (four elements per thread) kernels: every
+    element's update is bit-identical to the element-per-thread kernels' (n + 1
+    triangles), and the first non-finite triangle of each group is the same."""
+    from paper_2505_19175_b200.optim import DeviceAdamState, adam_step
+    rng = np.random.default_rng(7)
+    n = 1000
+    base = (rng.normal(0, 1, (n + 1, 3, 3)), rng.uniform(0.1, 0.9, n + 1), rng.uniform(0.5, 3, n + 1),
+            rng.normal(0, 0.3, (n + 1, 16, 3)))
+    gr = (rng.normal(0, 1, (n + 1, 3, 3)), rng.normal(0, 1, n + 1), rng.normal(0, 1, n + 1),
+          rng.normal(0, 1, (n + 1, 16, 3)))
+    lrs = {k: 1e-3 * (i + 1) for i, k in enumerate(OP.GROUPS)}
+    a, sa = _dev(*(x[:n] for x in base)), DeviceAdamState.zeros(n)
+    b, sb = _dev(*base), DeviceAdamState.zeros(n + 1)
+    for _ in range(3):
+        adam_step(a, _grads(n, *(x[:n] for x in gr)), sa, lrs)
+        adam_step(b, _grads(n + 1, *gr), sb, lrs)
+    for ta, tb in ((a.vertices, b.vertices), (a.opacity, b.opacity), (a.sigma, b.sigma), (a.sh, b.sh)):
+        assert torch.equal(ta, tb[:n])
+    g = _grads(n, *(x[:n] for x in gr))
+    g.d_sh[517, 3, 1] = float("nan")
+    g.d_sh[516, 15, 2] = float("inf")   # (same quad region, smaller triangle)
+    g.d_vertices[999, 2, 2] = float("-inf")
+    adam_step(a, g, sa, lrs, check=False)
+    assert sa.last_bad.cpu().tolist() == [999, -1, -1, 516]
