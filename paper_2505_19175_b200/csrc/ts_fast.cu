@@ -338,9 +338,12 @@ __global__ void __launch_bounds__(128) k_preprocess_fast64(Cam cam, Opts opt, co
 // block's vertices, opacity, sigma and SH rows are copied to shared memory
 // (cp.async, double-buffered, SH rows padded to 13 float4 so per-thread row
 // reads are bank-conflict free) while the current block is computed.
-constexpr int PRE_BLK = 128;
+#ifndef TS_PRE_BLK
+#define TS_PRE_BLK 64  // (64 x 8 CTAs per SM: more independent stages in flight than 128 x 4)
+#endif
+constexpr int PRE_BLK = TS_PRE_BLK;  // triangles (threads) per CTA stage
 #ifndef TS_PRE_MINB
-#define TS_PRE_MINB 4  // CTAs per SM of the staged preprocess
+#define TS_PRE_MINB 8  // CTAs per SM of the staged preprocess
 #endif
 struct PreStage {
     float4 sh[PRE_BLK * 13];
