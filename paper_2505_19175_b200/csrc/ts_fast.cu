@@ -339,11 +339,11 @@ __global__ void __launch_bounds__(128) k_preprocess_fast64(Cam cam, Opts opt, co
 // (cp.async, double-buffered, SH rows padded to 13 float4 so per-thread row
 // reads are bank-conflict free) while the current block is computed.
 #ifndef TS_PRE_BLK
-#define TS_PRE_BLK 64  // (64 x 8 CTAs per SM: more independent stages in flight than 128 x 4)
+#define TS_PRE_BLK 32  // (one warp x 16 CTAs per SM: more independent stages in flight; 64 x 8 and 128 x 4 slower)
 #endif
 constexpr int PRE_BLK = TS_PRE_BLK;  // triangles (threads) per CTA stage
 #ifndef TS_PRE_MINB
-#define TS_PRE_MINB 8  // CTAs per SM of the staged preprocess
+#define TS_PRE_MINB 16  // CTAs per SM of the staged preprocess
 #endif
 struct PreStage {
     float4 sh[PRE_BLK * 13];
