@@ -160,7 +160,7 @@ class B200ViewTrainer:
         self.poses = poses
         self.d_images = d_images
         self.kw = render_kw
-        self.grads = DeviceGrads.zeros(len(soup))
+        self.grads = DeviceGrads.zeros(len(soup), device=soup.vertices.device)
         self.comm = None          # side stream of the bucketed all-reduce (world > 1)
         self.n_buckets = 8
         self.chain_views = max(1, min(int(chain_views), Rasterizer.MAX_PENDING_VIEWS))
@@ -204,7 +204,7 @@ class B200ViewTrainer:
     def step(self) -> StepResult:
         world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
         rank = dist.get_rank() if world > 1 else 0
-        if self.comm is None and world > 1:
+        if self.comm is None and world > 1 and self.grads.flat.is_cuda:
             self.comm = torch.cuda.Stream()
         mine = shard(len(self.poses), world, rank)
         self._last_view = mine[-1] if len(mine) else None
