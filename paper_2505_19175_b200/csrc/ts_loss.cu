@@ -277,132 +277,162 @@ void launch_photometric_loss(const float* x, const float* y, int H, int W, doubl
 // ---------------------------------------------------------------------------
 // Distortion loss (losses.py:153-203): per pixel, sum over ordered fragment
 // pairs of w_i w_j |z_i - z_j|, averaged over image_size pixels, with its
-// gradients w.r.t. every fragment's weight and depth.  Thread per pixel over
-// its CSR fragment run: the reference's O(F) prefix-sum form when the run is
-// sorted by depth (the compositing order), the pairwise form otherwise.
+// gradients w.r.t. every fragment's weight and depth, over the CSR fragment runs.
 // ---------------------------------------------------------------------------
-// warp-inclusive scan of v over the lanes
-__device__ __forceinline__ double warp_incl_scan(double v, unsigned lane) {
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, v, off);
-        if ((int)lane >= off) v += y;
-    }
-    return v;
-}
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-}
+// Eight lanes per pixel (four pixels per warp), each lane holding four consecutive
+// fragments of a 32-fragment chunk: the prefix sums are a serial sum inside the lane
+// and a 3-step exclusive scan across the group, so a warp spends its instructions on
+// four pixels instead of one (most lists are far shorter than 32).  Lists longer than
+// one chunk are read twice (totals, then prefixes with a carry).  As in the reference
+// (losses.py:178-203) the form is chosen for the whole fragment set: the prefix-sum
+// form when every run is depth sorted, else the pairwise form for every run
+// (_distortion_pairwise :153-166) -- the two differ on depth ties (d_depth).  The
+// prefix pass checks the order as it reads the runs; the pairwise kernel after it
+// exits at once unless a run was out of order, and then rewrites every output.
+constexpr int DIST_PW_BLOCKS = 148 * 8;  // grid of the pairwise redo (grid-stride)
+constexpr int DIST_SUM_BLOCKS = 256;     // first level of the deterministic loss sum
 
-// Warp per pixel: the pixel's fragment list is read with coalesced loads, 32 fragments
-// per step.  Depth-sorted lists (every list the rasterizer emits: fragments are
-// composited in depth order) take the prefix-sum form -- fragment k's weight /
-// weighted depth in front (wb, sb) are warp scans, the totals (tw, ts) a first
-// pass; other lists the pairwise form (_distortion_pairwise :153-166).
-__global__ void __launch_bounds__(256) k_distortion(long long npix, const long long* __restrict__ off,
-                                                    const double* __restrict__ w, const double* __restrict__ z,
-                                                    double scale, double* __restrict__ d_w,
-                                                    double* __restrict__ d_z, double* __restrict__ part) {
-    __shared__ double s_red[8];
-    const unsigned lane = threadIdx.x & 31;
-    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__global__ void __launch_bounds__(256, 4) k_distortion_g8(long long npix, const long long* __restrict__ off,
+                                                          const double* __restrict__ w, const double* __restrict__ z,
+                                                          double scale, unsigned* __restrict__ unsorted,
+                                                          double* __restrict__ d_w, double* __restrict__ d_z,
+                                                          double* __restrict__ wpart) {
+    const unsigned lane = threadIdx.x & 31, gl = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
     double tot = 0.0;
+    bool bad = false;
     if (p < npix) {
         const long long lo = off[p], hi = off[p + 1];
         if (hi - lo < 2) {
-            if (lane == 0 && hi > lo) {
+            if (gl == 0 && hi > lo) {
                 if (d_w) d_w[lo] = 0.0;
                 if (d_z) d_z[lo] = 0.0;
             }
-        } else if (hi - lo <= 32) {
-            // one step (most pixels): the fragment stays in registers for both passes
-            const long long k = lo + lane;
-            const bool in = k < hi;
-            const double wk = in ? w[k] : 0.0, zk = in ? z[k] : 0.0;
-            const double zp = __shfl_up_sync(0xffffffffu, zk, 1);
-            const bool sorted = __all_sync(0xffffffffu, !(in && k > lo && zk < zp));
-            const double tw = warp_sum(wk), ts = warp_sum(wk * zk);
-            if (sorted) {
-                const double iw = warp_incl_scan(wk, lane), is = warp_incl_scan(wk * zk, lane);
-                const double wb = iw - wk, sb = is - wk * zk;
-                if (in) {
+        } else {
+            const bool multi = hi - lo > 32;
+            double wv[4], zv[4];
+            auto load = [&](long long c0) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    const long long k = c0 + 4 * gl + r;
+                    wv[r] = k < hi ? w[k] : 0.0;
+                    zv[r] = k < hi ? z[k] : 0.0;
+                }
+            };
+            // pass 1: the run's totals and its depth order
+            double tw = 0.0, ts = 0.0, zc = 0.0;
+            for (long long c0 = lo; c0 < hi; c0 += 32) {
+                load(c0);
+                const long long kf = c0 + 4 * gl;
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    tw += wv[r];
+                    ts += wv[r] * zv[r];
+                    if (r > 0) bad |= kf + r < hi && zv[r] < zv[r - 1];
+                }
+                const double zl = __shfl_up_sync(gmask, zv[3], 1, 8);  // the previous lane's last
+                bad |= kf < hi && kf > lo && zv[0] < (gl > 0 ? zl : zc);
+                zc = __shfl_sync(gmask, zv[3], 7, 8);  // the next chunk's predecessor
+            }
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                tw += __shfl_xor_sync(gmask, tw, o, 8);
+                ts += __shfl_xor_sync(gmask, ts, o, 8);
+            }
+            // pass 2: weight / weighted depth in front of each fragment
+            double cw = 0.0, cs = 0.0;  // carried from earlier chunks
+            for (long long c0 = lo; c0 < hi; c0 += 32) {
+                if (multi) load(c0);
+                double aw = 0.0, as = 0.0;  // the lane's totals
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    aw += wv[r];
+                    as += wv[r] * zv[r];
+                }
+                double iw = aw, is = as;  // inclusive scan of the lane totals
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    const double yw = __shfl_up_sync(gmask, iw, o, 8), ys = __shfl_up_sync(gmask, is, o, 8);
+                    if ((int)gl >= o) {
+                        iw += yw;
+                        is += ys;
+                    }
+                }
+                double wb = cw + (iw - aw), sb = cs + (is - as);  // in front of the lane's first
+                const long long kf = c0 + 4 * gl;
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    if (kf + r >= hi) break;
+                    const double wk = wv[r], zk = zv[r];
                     const double wa = tw - wb - wk, sa = ts - sb - wk * zk;
                     const double fwd = zk * wb - sb;
                     tot += wk * fwd;
-                    if (d_w) d_w[k] = 2.0 * (fwd + (sa - zk * wa)) * scale;
-                    if (d_z) d_z[k] = 2.0 * wk * (wb - wa) * scale;
+                    if (d_w) d_w[kf + r] = 2.0 * (fwd + (sa - zk * wa)) * scale;
+                    if (d_z) d_z[kf + r] = 2.0 * wk * (wb - wa) * scale;
+                    wb += wk;
+                    sb += wk * zk;
                 }
-                tot *= 2.0;
-            } else {  // pairwise (_distortion_pairwise :153-166)
-                double gw_ = 0.0, gz = 0.0;
-                for (int j = 0; j < (int)(hi - lo); j++) {
-                    const double zj = __shfl_sync(0xffffffffu, zk, j), wj = __shfl_sync(0xffffffffu, wk, j);
-                    const double dz = zk - zj;
-                    tot += wk * fabs(dz) * wj;
-                    gw_ += fabs(dz) * wj;
-                    gz += (double)((dz > 0.0) - (dz < 0.0)) * wj;
-                }
-                if (in) {
-                    if (d_w) d_w[k] = 2.0 * gw_ * scale;
-                    if (d_z) d_z[k] = 2.0 * gz * wk * scale;
-                } else {
-                    tot = 0.0;
-                }
+                cw += __shfl_sync(gmask, iw, 7, 8);
+                cs += __shfl_sync(gmask, is, 7, 8);
             }
-        } else {
-            double tw = 0.0, ts = 0.0;
-            bool sorted = true;
-            for (long long k0 = lo; k0 < hi; k0 += 32) {
-                const long long k = k0 + lane;
-                double wk = 0.0, zk = 0.0;
-                if (k < hi) {
-                    wk = w[k];
-                    zk = z[k];
-                    if (k > lo && zk < z[k - 1]) sorted = false;
-                }
-                tw += wk;
-                ts += wk * zk;
+            tot *= 2.0;
+        }
+    }
+    // per-warp partial (no block barrier: a warp with short runs retires early)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(unsorted, 1u);
+    if (lane == 0) wpart[((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5] = tot;
+}
+
+// the pairwise form for every run when any run is out of depth order
+__global__ void __launch_bounds__(256) k_distortion_pairwise(long long npix, const long long* __restrict__ off,
+                                                             const double* __restrict__ w,
+                                                             const double* __restrict__ z, double scale,
+                                                             const unsigned* __restrict__ unsorted,
+                                                             double* __restrict__ d_w, double* __restrict__ d_z,
+                                                             double* __restrict__ fpart) {
+    __shared__ double s_red[8];
+    if (*unsorted == 0u) return;
+    const unsigned gl = threadIdx.x & 7;
+    double tot = 0.0;
+    for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3; p < npix;
+         p += (long long)gridDim.x * (blockDim.x >> 3)) {
+        const long long lo = off[p], hi = off[p + 1];
+        if (hi - lo < 2) continue;
+        for (long long i = lo + gl; i < hi; i += 8) {
+            double gw_ = 0.0, gz = 0.0;
+            const double zi = z[i], wi = w[i];
+            for (long long j = lo; j < hi; j++) {
+                const double dz = zi - z[j];
+                tot += wi * fabs(dz) * w[j];
+                gw_ += fabs(dz) * w[j];
+                gz += (double)((dz > 0.0) - (dz < 0.0)) * w[j];
             }
-            tw = warp_sum(tw);
-            ts = warp_sum(ts);
-            if (__all_sync(0xffffffffu, sorted)) {
-                double cw = 0.0, cs = 0.0;  // carried from earlier steps
-                for (long long k0 = lo; k0 < hi; k0 += 32) {
-                    const long long k = k0 + lane;
-                    const bool in = k < hi;
-                    const double wk = in ? w[k] : 0.0, zk = in ? z[k] : 0.0;
-                    const double iw = warp_incl_scan(wk, lane), is = warp_incl_scan(wk * zk, lane);
-                    const double wb = cw + iw - wk, sb = cs + is - wk * zk;
-                    if (in) {
-                        const double wa = tw - wb - wk, sa = ts - sb - wk * zk;
-                        const double fwd = zk * wb - sb;
-                        tot += wk * fwd;
-                        if (d_w) d_w[k] = 2.0 * (fwd + (sa - zk * wa)) * scale;
-                        if (d_z) d_z[k] = 2.0 * wk * (wb - wa) * scale;
-                    }
-                    cw += __shfl_sync(0xffffffffu, iw, 31);
-                    cs += __shfl_sync(0xffffffffu, is, 31);
-                }
-                tot *= 2.0;
-            } else {  // pairwise (_distortion_pairwise :153-166)
-                for (long long i = lo + lane; i < hi; i += 32) {
-                    double gw_ = 0.0, gz = 0.0;
-                    for (long long j = lo; j < hi; j++) {
-                        const double dz = z[i] - z[j];
-                        tot += w[i] * fabs(dz) * w[j];
-                        gw_ += fabs(dz) * w[j];
-                        gz += (double)((dz > 0.0) - (dz < 0.0)) * w[j];
-                    }
-                    if (d_w) d_w[i] = 2.0 * gw_ * scale;
-                    if (d_z) d_z[i] = 2.0 * gz * w[i] * scale;
-                }
-            }
+            if (d_w) d_w[i] = 2.0 * gw_ * scale;
+            if (d_z) d_z[i] = 2.0 * gz * wi * scale;
         }
     }
     const double t = block_sum_256(tot, s_red);
-    if (threadIdx.x == 0) part[blockIdx.x] = t;
+    if (threadIdx.x == 0) fpart[blockIdx.x] = t;
+}
+
+// first level of the loss sum over the partials of whichever form ran (fixed
+// slices: the sum is deterministic)
+__global__ void __launch_bounds__(256) k_distortion_sum(const double* __restrict__ wpart, long long nw,
+                                                        const double* __restrict__ fpart,
+                                                        const unsigned* __restrict__ unsorted,
+                                                        double* __restrict__ p2) {
+    __shared__ double s_red[8];
+    const bool pw = *unsorted != 0u;
+    const double* src = pw ? fpart : wpart;
+    const long long n = pw ? DIST_PW_BLOCKS : nw;
+    double a = 0.0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        a += src[k];
+    const double t = block_sum_256(a, s_red);
+    if (threadIdx.x == 0) p2[blockIdx.x] = t;
 }
 
 __global__ void __launch_bounds__(256) k_sum_scaled(const double* __restrict__ part, int n, double scale,
@@ -601,16 +631,28 @@ void launch_normal_loss(const float* v, long long n, const long long* off, const
     if (n > 0 && d_vertices) k_normal_chain<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, gc, d_vertices);
 }
 
-size_t distortion_scratch_bytes(long long npix) { return sizeof(double) * (size_t)((npix + 7) / 8 + 1); }
+// per-warp partials (or the pairwise kernel's per-CTA partials), the first-level sums
+// and the order flag
+size_t distortion_scratch_bytes(long long npix) {
+    return sizeof(double) * (size_t)((npix + 7) / 8 + (npix + 3) / 4 + DIST_PW_BLOCKS + DIST_SUM_BLOCKS + 1);
+}
 
 void launch_distortion_loss(long long npix, const long long* off, const double* w, const double* z,
                             long long image_size, double* out, double* d_w, double* d_z, void* scratch,
                             cudaStream_t st) {
     const double scale = 1.0 / (double)(image_size > 1 ? image_size : 1);
-    const int nb = (int)((npix + 7) / 8);  // warp per pixel
     double* part = (double*)scratch;
-    if (nb > 0) k_distortion<<<nb, 256, 0, st>>>(npix, off, w, z, scale, d_w, d_z, part);
-    k_sum_scaled<<<1, 256, 0, st>>>(part, nb, scale, out);
+    const int nb = (int)((npix + 31) / 32);  // eight lanes per pixel, 32 pixels per CTA
+    double* fpart = part + (npix + 3) / 4;
+    double* p2 = fpart + DIST_PW_BLOCKS;
+    unsigned* unsorted = (unsigned*)(p2 + DIST_SUM_BLOCKS);
+    cudaMemsetAsync(unsorted, 0, sizeof(unsigned), st);
+    if (nb > 0) {
+        k_distortion_g8<<<nb, 256, 0, st>>>(npix, off, w, z, scale, unsorted, d_w, d_z, part);
+        k_distortion_pairwise<<<DIST_PW_BLOCKS, 256, 0, st>>>(npix, off, w, z, scale, unsorted, d_w, d_z, fpart);
+    }
+    k_distortion_sum<<<DIST_SUM_BLOCKS, 256, 0, st>>>(part, nb > 0 ? (long long)nb * 8 : 0, fpart, unsorted, p2);
+    k_sum_scaled<<<1, 256, 0, st>>>(p2, DIST_SUM_BLOCKS, scale, out);
 }
 
 void launch_fragment_depth(long long npix, const long long* off, const double* w, const double* z, double* depth,

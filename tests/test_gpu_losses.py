@@ -87,6 +87,33 @@ def test_distortion_and_depth_against_fixtures():
         assert np.abs(d - z[f"depth_{tag}"]).max() <= 1e-12
 
 
+def test_distortion_long_and_mixed_runs():
+    # run lengths 0..140 (one, two and five 32-fragment chunks), sorted runs with ties,
+    # and shuffled runs whose first out-of-order pair sits at a chunk or lane boundary
+    from paper_2505_19175_b200 import losses as DL
+    from paper_2505_19175_b200.types import FragmentData
+    rng = np.random.default_rng(17)
+    lens = np.concatenate([np.arange(0, 141), rng.integers(0, 70, 300)])
+    rng.shuffle(lens)
+    off = np.zeros(len(lens) + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    w = rng.random(off[-1]) * 0.5
+    z = np.empty(off[-1])
+    for i, n in enumerate(lens):
+        zz = np.sort(np.round(rng.random(n) * 20.0, 1) + 1.0)  # sorted, with ties
+        if n >= 2 and i % 3 == 0:  # out of order at a lane / chunk boundary or anywhere
+            k = [4, 8, 32, 33, int(rng.integers(1, n))][i % 5]
+            k = k if k < n else int(rng.integers(1, n))
+            zz[k - 1], zz[k] = zz[k] + 0.5, zz[k - 1]
+        z[off[i]:off[i + 1]] = zz
+    fr = FragmentData(off, np.zeros(len(w), np.int64), w, z)
+    v, dw, dz = DL.distortion_loss(fr, image_size=len(lens))
+    wv, wdw, wdz = OL.distortion_loss(off, w, z, image_size=len(lens))
+    assert abs(v - wv) <= 1e-12 * max(1.0, abs(wv))
+    assert np.abs(dw - wdw).max() <= 1e-12 * max(1.0, np.abs(wdw).max())
+    assert np.abs(dz - wdz).max() <= 1e-12 * max(1.0, np.abs(wdz).max())
+
+
 def test_distortion_on_rendered_fragments():
     # fragments of a real frame stay on the device: loss and gradients vs the oracle
     from paper_2505_19175_b200 import losses as DL
