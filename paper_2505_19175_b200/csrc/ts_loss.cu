@@ -444,18 +444,27 @@ __global__ void __launch_bounds__(256) k_sum_scaled(const double* __restrict__ p
     if (threadIdx.x == 0) out[0] = t * scale;
 }
 
-// depth_from_fragments (losses.py:206-216): blend-weight-normalised depth per pixel
+// depth_from_fragments (losses.py:206-216): blend-weight-normalised depth per pixel;
+// eight lanes per pixel over fragments l, l+8, ... (coalesced run reads)
 __global__ void __launch_bounds__(256) k_fragment_depth(long long npix, const long long* __restrict__ off,
                                                         const double* __restrict__ w, const double* __restrict__ z,
                                                         double* __restrict__ depth) {
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= npix) return;
+    const unsigned gl = threadIdx.x & 7, lane = threadIdx.x & 31;
+    const unsigned gmask = 0xffu << (lane & 24);
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    if (p >= npix) return;  // whole groups leave together
     double a = 0.0, b = 0.0;
-    for (long long k = off[p]; k < off[p + 1]; k++) {
-        a += w[k] * z[k];
-        b += w[k];
+    for (long long k = off[p] + gl, k1 = off[p + 1]; k < k1; k += 8) {
+        const double wk = w[k];
+        a += wk * z[k];
+        b += wk;
     }
-    depth[p] = a / fmax(b, 1e-8);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(gmask, a, o, 8);
+        b += __shfl_xor_sync(gmask, b, o, 8);
+    }
+    if (gl == 0) depth[p] = a / fmax(b, 1e-8);
 }
 
 // ---------------------------------------------------------------------------
@@ -466,13 +475,14 @@ __global__ void __launch_bounds__(256) k_fragment_depth(long long npix, const lo
 //                      rotated into the world frame (n @ R);
 //   k_tri_normals   -- per triangle: c = (v1-v0) x (v2-v0), |c| (floored), the
 //                      unit normal and its camera-facing sign;
-//   k_normal_frag   -- thread per pixel over its fragments: w (1 - n.N), the
+//   k_normal_frag   -- eight lanes per pixel over its fragments: w (1 - n.N), the
 //                      weight gradient, and dL/dc per triangle (fp64 atomics);
 //   k_normal_chain  -- per triangle: the cross-product chain into d_vertices.
 // ---------------------------------------------------------------------------
 #ifndef TS_NORMAL_U
-#define TS_NORMAL_U 4  // fragments per step of k_normal_frag
+#define TS_NORMAL_U 1  // fragments per lane per step of k_normal_frag
 #endif
+constexpr int NORMAL_SUM_BLOCKS = 256;
 struct NCam {
     double fx, fy, cx, cy, R[9], t[3];
 };
@@ -510,7 +520,8 @@ __global__ void __launch_bounds__(256) k_depth_normals(const double* __restrict_
         nmap[(size_t)p * 3 + j] = n[0] * cm.R[0 * 3 + j] + n[1] * cm.R[1 * 3 + j] + n[2] * cm.R[2 * 3 + j];
 }
 
-// tri[8 per triangle]: chat xyz, |c|, flip, pad
+// tri[4 per triangle]: chat xyz, flip / |c| (one 32-byte sector per gather; the sign
+// is the flip: |c| is floored above zero)
 __global__ void __launch_bounds__(256) k_tri_normals(const float* __restrict__ v, long long n, NCam cm,
                                                      double* __restrict__ tri, double* __restrict__ gc) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -530,59 +541,74 @@ __global__ void __launch_bounds__(256) k_tri_normals(const float* __restrict__ v
         const double nc = ch[0] * cm.R[r * 3 + 0] + ch[1] * cm.R[r * 3 + 1] + ch[2] * cm.R[r * 3 + 2];
         facing += nc * cc;
     }
-    double* o = tri + i * 8;
-    o[0] = ch[0]; o[1] = ch[1]; o[2] = ch[2]; o[3] = cn; o[4] = facing > 0.0 ? -1.0 : 1.0;
+    double* o = tri + i * 4;
+    o[0] = ch[0]; o[1] = ch[1]; o[2] = ch[2]; o[3] = (facing > 0.0 ? -1.0 : 1.0) / cn;
     gc[i * 3 + 0] = gc[i * 3 + 1] = gc[i * 3 + 2] = 0.0;
 }
 
+// Eight lanes per pixel (four pixels per warp): lane l of a pixel's group takes
+// fragments l, l+8, ... -- the source ids, weights and d_weight stores are
+// coalesced, and a warp has up to eight triangle-row gathers in flight per pixel.
 __global__ void __launch_bounds__(256) k_normal_frag(long long npix, const long long* __restrict__ off,
                                                      const int* __restrict__ ftri, const double* __restrict__ w,
                                                      const double* __restrict__ nmap, const double* __restrict__ tri,
                                                      double inv_nf, double* __restrict__ d_w, double* __restrict__ gc,
                                                      double* __restrict__ part) {
-    __shared__ double s_red[8];
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned gl = threadIdx.x & 7;
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
     double sum = 0.0;
     if (p < npix) {
         const double m0 = nmap[p * 3 + 0], m1 = nmap[p * 3 + 1], m2 = nmap[p * 3 + 2];
         const long long k0 = off[p], k1 = off[p + 1];
-        // four fragments per step: their source ids and triangle rows are all in
-        // flight at once (the gathers, not the arithmetic, bound this loop)
-        constexpr int U = TS_NORMAL_U;
-        for (long long kb = k0; kb < k1; kb += U) {
+        constexpr int U = TS_NORMAL_U;  // fragments per lane in flight at once
+        for (long long kb = k0 + gl; kb < k1; kb += 8 * U) {
             long long t[U];
-            double wk[U], c[U][5];
+            double wk[U], c[U][4];
 #pragma unroll
-            for (int u = 0; u < U; u++) t[u] = kb + u < k1 ? (long long)ftri[kb + u] : -1;
+            for (int u = 0; u < U; u++) t[u] = kb + 8 * u < k1 ? (long long)ftri[kb + 8 * u] : -1;
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 wk[u] = 0.0;
                 if (t[u] >= 0) {
-                    const double* o = tri + t[u] * 8;
+                    const double* o = tri + t[u] * 4;
                     const double2 a = *reinterpret_cast<const double2*>(o);
                     const double2 b = *reinterpret_cast<const double2*>(o + 2);
-                    c[u][0] = a.x; c[u][1] = a.y; c[u][2] = b.x; c[u][3] = b.y; c[u][4] = o[4];
-                    wk[u] = w[kb + u];
+                    c[u][0] = a.x; c[u][1] = a.y; c[u][2] = b.x; c[u][3] = b.y;
+                    wk[u] = w[kb + 8 * u];
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 if (t[u] < 0) continue;
-                const long long k = kb + u;
-                const double c0 = c[u][0], c1 = c[u][1], c2 = c[u][2], cn = c[u][3], fl = c[u][4];
+                const long long k = kb + 8 * u;
+                const double c0 = c[u][0], c1 = c[u][1], c2 = c[u][2], fc = c[u][3];
+                const double fl = fc < 0.0 ? -1.0 : 1.0;
                 const double cm = c0 * m0 + c1 * m1 + c2 * m2;
                 const double dot = cm * fl;
                 sum += wk[u] * (1.0 - dot);
                 if (d_w) d_w[k] = (1.0 - dot) * inv_nf;
-                const double coef = -wk[u] * fl * inv_nf / cn;
+                const double coef = -wk[u] * inv_nf * fc;
                 atomicAdd(gc + t[u] * 3 + 0, coef * (m0 - c0 * cm));
                 atomicAdd(gc + t[u] * 3 + 1, coef * (m1 - c1 * cm));
                 atomicAdd(gc + t[u] * 3 + 2, coef * (m2 - c2 * cm));
             }
         }
     }
-    const double s = block_sum_256(sum, s_red);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    // per-warp partial (no block barrier: a warp with short runs retires early)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) part[((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5] = sum;
+}
+
+// first level of a deterministic sum of n partials (fixed slices per CTA)
+__global__ void __launch_bounds__(256) k_sum_level1(const double* __restrict__ src, long long n,
+                                                    double* __restrict__ p2) {
+    __shared__ double s_red[8];
+    double a = 0.0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        a += src[k];
+    const double t = block_sum_256(a, s_red);
+    if (threadIdx.x == 0) p2[blockIdx.x] = t;
 }
 
 __global__ void __launch_bounds__(256) k_normal_chain(const float* __restrict__ v, long long n,
@@ -605,7 +631,7 @@ __global__ void __launch_bounds__(256) k_normal_chain(const float* __restrict__ 
 }
 
 size_t normal_scratch_bytes(long long n, long long npix) {
-    return sizeof(double) * (size_t)(8 * n + 3 * n + 3 * npix + (npix + 255) / 256 + 8);
+    return sizeof(double) * (size_t)(4 * n + 3 * n + 3 * npix + (npix + 3) / 4 + NORMAL_SUM_BLOCKS + 8);
 }
 
 void launch_normal_loss(const float* v, long long n, const long long* off, const int* ftri, const double* w,
@@ -617,17 +643,19 @@ void launch_normal_loss(const float* v, long long n, const long long* off, const
     for (int k = 0; k < 3; k++) cm.t[k] = cam[13 + k];
     const long long npix = (long long)H * W;
     double* tri = (double*)scratch;
-    double* gc = tri + 8 * n;
+    double* gc = tri + 4 * n;
     double* nmap = gc + 3 * n;
     double* part = nmap + 3 * npix;
-    const int nb = (int)((npix + 255) / 256);
+    double* p2 = part + (npix + 3) / 4;  // after the per-warp partials
+    const int nb = (int)((npix + 31) / 32);  // eight lanes per pixel
     if (n > 0) k_tri_normals<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, cm, tri, gc);
     if (npix > 0) {
-        k_depth_normals<<<nb, 256, 0, st>>>(depth, H, W, cm, nmap);
+        k_depth_normals<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(depth, H, W, cm, nmap);
         k_normal_frag<<<nb, 256, 0, st>>>(npix, off, ftri, w, nmap, tri, nfrag > 0 ? 1.0 / (double)nfrag : 0.0, d_w,
                                           gc, part);
     }
-    k_sum_scaled<<<1, 256, 0, st>>>(part, npix > 0 ? nb : 0, nfrag > 0 ? 1.0 / (double)nfrag : 0.0, out);
+    k_sum_level1<<<NORMAL_SUM_BLOCKS, 256, 0, st>>>(part, npix > 0 ? (long long)nb * 8 : 0, p2);
+    k_sum_scaled<<<1, 256, 0, st>>>(p2, NORMAL_SUM_BLOCKS, nfrag > 0 ? 1.0 / (double)nfrag : 0.0, out);
     if (n > 0 && d_vertices) k_normal_chain<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(v, n, gc, d_vertices);
 }
 
@@ -657,7 +685,7 @@ void launch_distortion_loss(long long npix, const long long* off, const double* 
 
 void launch_fragment_depth(long long npix, const long long* off, const double* w, const double* z, double* depth,
                            cudaStream_t st) {
-    if (npix > 0) k_fragment_depth<<<(unsigned)((npix + 255) / 256), 256, 0, st>>>(npix, off, w, z, depth);
+    if (npix > 0) k_fragment_depth<<<(unsigned)((npix + 31) / 32), 256, 0, st>>>(npix, off, w, z, depth);
 }
 
 }  // namespace ts
