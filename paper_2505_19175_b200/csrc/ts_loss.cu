@@ -522,12 +522,23 @@ __global__ void __launch_bounds__(256) k_depth_normals(const double* __restrict_
 
 // tri[4 per triangle]: chat xyz, flip / |c| (one 32-byte sector per gather; the sign
 // is the flip: |c| is floored above zero)
+// the CTA's 256 vertex rows (9 floats each) staged through shared memory with
+// coalesced loads; the odd row stride reads them back without bank conflicts
+__device__ __forceinline__ void stage_vertex_rows(const float* __restrict__ v, long long n, float* s_v) {
+    const long long base = (long long)blockIdx.x * 256;
+    const int cnt = (int)min(256LL, n - base) * 9;
+    for (int k = threadIdx.x; k < cnt; k += 256) s_v[k] = v[base * 9 + k];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) k_tri_normals(const float* __restrict__ v, long long n, NCam cm,
                                                      double* __restrict__ tri, double* __restrict__ gc) {
+    __shared__ float s_v[256 * 9];
+    stage_vertex_rows(v, n, s_v);
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double p[9];
-    for (int k = 0; k < 9; k++) p[k] = (double)v[i * 9 + k];
+    for (int k = 0; k < 9; k++) p[k] = (double)s_v[threadIdx.x * 9 + k];
     const double a[3] = {p[3] - p[0], p[4] - p[1], p[5] - p[2]};
     const double b[3] = {p[6] - p[0], p[7] - p[1], p[8] - p[2]};
     const double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
@@ -613,21 +624,27 @@ __global__ void __launch_bounds__(256) k_sum_level1(const double* __restrict__ s
 
 __global__ void __launch_bounds__(256) k_normal_chain(const float* __restrict__ v, long long n,
                                                       const double* __restrict__ gc, double* __restrict__ dv) {
+    __shared__ float s_v[256 * 9];
+    __shared__ double s_o[256 * 9];
+    stage_vertex_rows(v, n, s_v);
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const long long base = (long long)blockIdx.x * 256;
+    const int cnt = (int)min(256LL, n - base) * 9;
     double p[9];
-    for (int k = 0; k < 9; k++) p[k] = (double)v[i * 9 + k];
+    for (int k = 0; k < 9; k++) p[k] = (double)s_v[threadIdx.x * 9 + k];
     const double a[3] = {p[3] - p[0], p[4] - p[1], p[5] - p[2]};
     const double b[3] = {p[6] - p[0], p[7] - p[1], p[8] - p[2]};
-    const double g[3] = {gc[i * 3], gc[i * 3 + 1], gc[i * 3 + 2]};
+    const double g[3] = {i < n ? gc[i * 3] : 0.0, i < n ? gc[i * 3 + 1] : 0.0, i < n ? gc[i * 3 + 2] : 0.0};
     const double da[3] = {b[1] * g[2] - b[2] * g[1], b[2] * g[0] - b[0] * g[2], b[0] * g[1] - b[1] * g[0]};
     const double db[3] = {g[1] * a[2] - g[2] * a[1], g[2] * a[0] - g[0] * a[2], g[0] * a[1] - g[1] * a[0]};
-    double* o = dv + i * 9;
+    double* o = s_o + threadIdx.x * 9;  // staged for coalesced row stores
     for (int k = 0; k < 3; k++) {
         o[3 + k] = da[k];
         o[6 + k] = db[k];
         o[k] = -(da[k] + db[k]);
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < cnt; k += 256) dv[base * 9 + k] = s_o[k];
 }
 
 size_t normal_scratch_bytes(long long n, long long npix) {
