@@ -40,31 +40,42 @@ struct FragGrads {
 };
 
 // sw[i] = sum_{i < k < end(p)} dw[k] w[k] per pixel p (the reference's running
-// `sw`, _kernels.py:265-268, back to front).  Warp per pixel: the list is read
-// with coalesced loads from its back end, 32 fragments per step; a suffix sum is
-// the step total minus an inclusive warp scan, plus the sum of the later steps.
+// `sw`, _kernels.py:265-268, back to front).  Eight lanes per pixel (four pixels per
+// warp), 32-fragment chunks from the list's back end, each lane holding four
+// consecutive fragments: the suffix inside the lane is serial, across the group a
+// 3-step suffix scan of the lane totals, plus the sum of the later chunks.
 __global__ void __launch_bounds__(256) k_frag_suffix(long long npix, const long long* __restrict__ off,
                                                      const double* __restrict__ w, const double* __restrict__ dw,
                                                      double* __restrict__ sw) {
-    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned lane = threadIdx.x & 31;
-    if (p >= npix) return;
+    const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    const unsigned lane = threadIdx.x & 31, gl = lane & 7;
+    const unsigned gmask = 0xffu << (lane & 24);
+    if (p >= npix) return;  // whole groups leave together
     const long long lo = off[p], hi = off[p + 1];
-    double carry = 0.0;  // sum over the fragments after the current step
+    double carry = 0.0;  // sum over the chunks after the current one
     for (long long top = hi; top > lo; top -= 32) {
         const long long base = top - 32 > lo ? top - 32 : lo;
-        const long long i = base + lane;
-        const bool in = i < top;
-        const double x = in ? dw[i] * w[i] : 0.0;
-        // inclusive scan from the back: lane L gets sum_{L <= j < 32} x_j
-        double v = x;
+        const long long kf = base + 4 * gl;
+        double x[4], t = 0.0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_down_sync(0xffffffffu, v, o);
-            if ((int)lane + o < 32) v += y;
+        for (int r = 0; r < 4; r++) {
+            x[r] = kf + r < top ? dw[kf + r] * w[kf + r] : 0.0;
+            t += x[r];
         }
-        if (in) sw[i] = carry + (v - x);
-        carry += __shfl_sync(0xffffffffu, v, 0);
+        // inclusive suffix scan of the lane totals: lane L gets sum_{L <= j < 8} t_j
+        double v = t;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const double y = __shfl_down_sync(gmask, v, o, 8);
+            if ((int)gl + o < 8) v += y;
+        }
+        double after = carry + (v - t);  // everything after this lane's last fragment
+#pragma unroll
+        for (int r = 3; r >= 0; r--) {
+            if (kf + r < top) sw[kf + r] = after;
+            after += x[r];
+        }
+        carry += __shfl_sync(gmask, v, 0, 8);
     }
 }
 
@@ -244,7 +255,7 @@ void launch_bwd_stream(const Cam& cam, const Opts& opt, const RecF* rec, const R
         return;
     }
     const long long npix = (long long)cam.width * cam.height;
-    if (npix > 0) k_frag_suffix<<<(unsigned)((npix + 7) / 8), 256, 0, st>>>(npix, frag_off, frag_w, fg_dw, sw);
+    if (npix > 0) k_frag_suffix<<<(unsigned)((npix + 31) / 32), 256, 0, st>>>(npix, frag_off, frag_w, fg_dw, sw);
     launch_pdl(k_bwd_stream<true>, grid, dim3(256), 0, st, cam, opt, rec, recb, recc, frec, ctr, cap, c_total, d_image,
                sgrad, FragGrads{frag_off, fg_dw, fg_dz, sw});
 }
