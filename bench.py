@@ -659,8 +659,9 @@ def train_step_bench(args, rast, ds, cfg, world, rank, stream, max_over_ranks):
         dep = L.depth_from_fragments(fr, c3.height, c3.width, rasterizer=rast)
         _, _, d_w2 = L.normal_loss(ds3, fr, dep, intr3, poses[v1], rasterizer=rast)
         mark(3)
-        rast.backward_fragments(d_img, fr.offsets, d_w * 100.0 + d_w2 * 1e-4, d_z * 100.0, trainer.grads,
-                                accumulate=True, weight=fr.weight)
+        # the caller's loss weights, combined in place on the fresh loss gradients
+        rast.backward_fragments(d_img, fr.offsets, d_w.mul_(100.0).add_(d_w2, alpha=1e-4), d_z.mul_(100.0),
+                                trainer.grads, accumulate=True, weight=fr.weight)
         mark(4)
 
     default_iteration()
